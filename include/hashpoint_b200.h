@@ -1,0 +1,164 @@
+/*
+ * hashpoint_b200.h — C ABI of the B200-native HashPoint hot path.
+ *
+ * Drop-in boundary for the reference's operator layer.  All
+ * array arguments are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ * C-contiguous, in the reference's dtypes (int64 ids/offsets/tables, float64
+ * coordinates and values).  Sizes are element counts.  Every function returns
+ * 0 on success or a negative HP_E* code; hp_last_error() returns a
+ * thread-local message for the last failure.  Functions are stateless and
+ * enqueue work on `stream` (a cudaStream_t); they never synchronise the device
+ * except where stated.  Scratch comes from a caller-provided workspace whose
+ * size the matching *_workspace_bytes function reports.
+ *
+ * Reference interfaces replaced (reference = /root/reference/pkg/src/hashpoint):
+ *   hp_build            hash_index.build            hash_index.py:151-190
+ *                       + _kernels.scatter_by_bucket  _kernels.py:76-83
+ *                       + rasterize_points / morton_codes hash_index.py:81-112
+ *   hp_layout_from_table (internal re-layout of a HashIndex built elsewhere;
+ *                       consumes the arrays of HashIndex hash_index.py:115-148)
+ *   hp_query_count /    _kernels.hash_query_batch   _kernels.py:86-157
+ *   hp_query_fill         (+ _cone_test :22-36, _canonical_sort :39-73);
+ *                       two-phase because Q is unknown before the call
+ *                       (the reference grows its buffers, :141-151)
+ *   hp_sample_run /     _kernels.sample_batch        _kernels.py:552-700
+ *   hp_sample_emit        (two-phase for the same reason; R unknown)
+ *   hp_primary_surface  derived: first retained candidate per ray
+ */
+#ifndef HASHPOINT_B200_H
+#define HASHPOINT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_OK 0
+#define HP_EINVAL (-1)  /* invalid argument (the reference raises ValueError) */
+#define HP_ECUDA (-2)   /* CUDA runtime error (RuntimeError) */
+#define HP_ESPACE (-3)  /* workspace too small */
+
+typedef void* hp_stream_t; /* cudaStream_t */
+
+/* Pinhole camera (reference geometry.py:50-134). Host struct, passed by pointer. */
+typedef struct {
+    double origin[3];
+    double right[3];
+    double up[3];
+    double forward[3];
+    double focal_length;
+    double pixel_width;
+    double pixel_height;
+    int64_t width;
+    int64_t height;
+} hp_camera;
+
+/* Query layout: the index's points re-laid out row-major by padded pixel
+ * (within a pixel: ascending original id, as in the reference's slots), with
+ * coordinates pre-shifted by the camera origin.  A kernel row of s pixels is
+ * then ONE contiguous slot range.  Device arrays; caller-allocated:
+ * row_ptr[P+1], rel_x/rel_y/rel_z/point_id[N_in] (capacity n for hp_build). */
+typedef struct {
+    int32_t* row_ptr;
+    double* rel_x;
+    double* rel_y;
+    double* rel_z;
+    int32_t* point_id;
+} hp_query_layout;
+
+typedef struct {
+    int32_t k_neighbors; /* K >= 1 (device limit HP_MAX_K) */
+    int32_t eps_mode;    /* 1: keep w >= eps; 0: tau mode */
+    int32_t want_color;  /* 1: colors != NULL, emit r_color */
+    int32_t exact_t_end; /* 1: t_end over all candidates (reference semantics);
+                            0: transmittance at the exit of retention */
+    double beta2;        /* beta*beta, computed by the caller as in sampler.py:215 */
+    double gamma;
+    double eps;
+    double tau_min;
+} hp_sampler_params;
+
+#define HP_MAX_K 256
+
+const char* hp_last_error(void);
+int hp_version(void);
+
+/* ---------------- build ---------------- */
+int hp_build_workspace_bytes(int64_t n, int64_t padded_w, int64_t padded_h, size_t* bytes);
+/* positions: float64 [n,3].  Outputs: table_start/table_count int64 [P];
+ * reordered_ids int64, slot_x/y/z float64 with capacity n; layout (capacity n);
+ * n_in: device int64 scalar receiving N_in.  Errors: padded size > 0xFFFF
+ * ("padded image exceeds 16-bit pixel coordinates"), n >= 2^31. */
+int hp_build(const double* positions, int64_t n, const hp_camera* cam, int64_t pad,
+             int64_t* table_start, int64_t* table_count, int64_t* reordered_ids,
+             double* slot_x, double* slot_y, double* slot_z, hp_query_layout layout,
+             int64_t* n_in, void* workspace, size_t workspace_bytes, hp_stream_t stream);
+
+int hp_layout_workspace_bytes(int64_t n_in, int64_t padded_w, int64_t padded_h, size_t* bytes);
+int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
+                         const double* slot_x, const double* slot_y, const double* slot_z,
+                         const int64_t* slot_ids, int64_t n_in, int64_t padded_w,
+                         int64_t padded_h, const double* origin_host, hp_query_layout layout,
+                         void* workspace, size_t workspace_bytes, hp_stream_t stream);
+
+/* ---------------- query ---------------- */
+int hp_query_workspace_bytes(int64_t m, int64_t pad, size_t* bytes);
+/* Pass 1.  pixels: int64 [m,2] (u, v) with element stride pixel_stride between
+ * rays (2 for an (m,2) array); dirs float64 [m,3]; t_near/t_far/slopes [m];
+ * origin_host: the index camera origin (host).  Writes probes/scanned [m]
+ * (int64) and offsets [m+1] (int64 CSR offsets; offsets[m] = Q). */
+int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t padded_h, int64_t pad,
+                   const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                   const double* t_near, const double* t_far, const double* slopes, int64_t m,
+                   int64_t* offsets, int64_t* probes, int64_t* scanned, void* workspace,
+                   size_t workspace_bytes, hp_stream_t stream);
+/* Pass 2.  Same inputs + offsets from pass 1 and total = Q (host value).
+ * Fills ids int64 [Q], t_proj / dist_perp float64 [Q], sorted by (t, id) per ray. */
+int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t padded_h, int64_t pad,
+                  const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                  const double* t_near, const double* t_far, const double* slopes, int64_t m,
+                  const int64_t* offsets, int64_t total, int64_t* ids, double* t_proj,
+                  double* dist_perp, void* workspace, size_t workspace_bytes,
+                  hp_stream_t stream);
+
+/* ---------------- sample ---------------- */
+/* max_q: longest per-ray segment of the CSR (hp_csr_stats); rays longer than
+ * the shared-memory capacity use global scratch sized from `total`. */
+int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t max_q, int64_t stage_capacity,
+                              const hp_sampler_params* p, size_t* bytes);
+/* Pass 1 over the query CSR (offsets [m+1], ids/t/dist [total], slopes [m],
+ * colors float64 [n_colors,3] or NULL).  Writes t_end [m] and r_off [m+1]
+ * (r_off[m] = R).  Retained candidates are staged in the workspace. */
+int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
+                  const double* dist, int64_t total, int64_t max_q, const double* slopes,
+                  const hp_sampler_params* p, const double* colors, int64_t n_colors,
+                  int64_t stage_capacity, int64_t* r_off, double* t_end, void* workspace,
+                  size_t workspace_bytes, hp_stream_t stream);
+/* Pass 2: write the R retained candidates (R = r_off[m], host value) in ray
+ * order: r_id int64, r_t/r_dist/r_udf/r_alpha/r_w float64 [R], r_color
+ * float64 [R,3] (may be NULL without colors). */
+int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
+                   const double* dist, int64_t total, int64_t max_q, const double* slopes,
+                   const hp_sampler_params* p, const double* colors, int64_t n_colors,
+                   int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id,
+                   double* r_t, double* r_dist, double* r_udf, double* r_alpha, double* r_w,
+                   double* r_color, void* workspace, size_t workspace_bytes,
+                   hp_stream_t stream);
+
+/* out2[0] = offsets[m] (total), out2[1] = max_r (offsets[r+1] - offsets[r]).
+ * Device int64[2]. */
+int hp_csr_stats(const int64_t* offsets, int64_t m, int64_t* out2, hp_stream_t stream);
+
+/* primary_id[r] = r_id[r_off[r]] or -1; primary_t[r] = r_t[r_off[r]] or NaN. */
+int hp_primary_surface(const int64_t* r_off, int64_t m, const int64_t* r_id, const double* r_t,
+                       int64_t* primary_id, double* primary_t, hp_stream_t stream);
+
+/* Kernel launches issued by this library since load (for bench gpu_launches). */
+int64_t hp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

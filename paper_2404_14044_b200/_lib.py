@@ -1,0 +1,106 @@
+"""ctypes binding of the C ABI in include/hashpoint_b200.h (libhp_b200.so).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, every compute entry point raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhp_b200.so")
+
+HP_EINVAL = -1
+
+c_p = ctypes.c_void_p
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int32
+c_f64 = ctypes.c_double
+c_size = ctypes.c_size_t
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("origin", c_f64 * 3), ("right", c_f64 * 3), ("up", c_f64 * 3),
+                ("forward", c_f64 * 3), ("focal_length", c_f64), ("pixel_width", c_f64),
+                ("pixel_height", c_f64), ("width", c_i64), ("height", c_i64)]
+
+
+class Layout(ctypes.Structure):
+    _fields_ = [("row_ptr", c_p), ("rel_x", c_p), ("rel_y", c_p), ("rel_z", c_p),
+                ("point_id", c_p)]
+
+
+class SamplerParams(ctypes.Structure):
+    _fields_ = [("k_neighbors", c_i32), ("eps_mode", c_i32), ("want_color", c_i32),
+                ("exact_t_end", c_i32), ("beta2", c_f64), ("gamma", c_f64), ("eps", c_f64),
+                ("tau_min", c_f64)]
+
+
+_SIGNATURES = {
+    "hp_last_error": (ctypes.c_char_p, []),
+    "hp_version": (ctypes.c_int, []),
+    "hp_launch_count": (c_i64, []),
+    "hp_build_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_build": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(Camera), c_i64, c_p, c_p, c_p, c_p, c_p,
+                                c_p, Layout, c_p, c_p, c_size, c_p]),
+    "hp_layout_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_layout_from_table": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, c_i64,
+                                            ctypes.POINTER(c_f64), Layout, c_p, c_size, c_p]),
+    "hp_query_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_query_count": (ctypes.c_int, [Layout, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_p, c_p,
+                                      c_i64, c_p, c_p, c_p, c_p, c_size, c_p]),
+    "hp_query_fill": (ctypes.c_int, [Layout, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_p, c_p,
+                                     c_i64, c_p, c_i64, c_p, c_p, c_p, c_p, c_size, c_p]),
+    "hp_sample_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i64,
+                                                 ctypes.POINTER(SamplerParams),
+                                                 ctypes.POINTER(c_size)]),
+    "hp_sample_run": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
+                                     ctypes.POINTER(SamplerParams), c_p, c_i64, c_i64, c_p, c_p,
+                                     c_p, c_size, c_p]),
+    "hp_sample_emit": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
+                                      ctypes.POINTER(SamplerParams), c_p, c_i64, c_i64, c_p, c_i64,
+                                      c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
+    "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
+    "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
+}
+
+EXPORTS = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def load(require_device: bool = False):
+    """Load the shared library (no GPU needed just to load it)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    if require_device:
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2404_14044_b200 needs a CUDA device (B200, sm_100a); "
+                               "there is no CPU fallback")
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (_lib.hp_last_error() or b"").decode()
+    if rc == HP_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def launch_count() -> int:
+    return int(load().hp_launch_count())

@@ -1,0 +1,122 @@
+// hp_common.cu — error state, launch accounting and the device-wide exclusive
+// scan used for CSR offsets, Morton-order table starts and row pointers.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "hp_common.cuh"
+
+namespace hp {
+
+static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    set_error("CUDA error in %s: %s", where, cudaGetErrorString(e));
+    return HP_ECUDA;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------ scan
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int64_t kScanTile = int64_t(kScanThreads) * kScanItems;
+
+template <class In>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums(const In* __restrict__ in, int64_t n,
+                                                               int64_t* __restrict__ sums) {
+    __shared__ int64_t sh[kScanThreads / 32 + 1];
+    const int64_t base = int64_t(blockIdx.x) * kScanTile + int64_t(threadIdx.x) * kScanItems;
+    int64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++)
+        if (base + k < n) acc += static_cast<int64_t>(in[base + k]);
+    int64_t total;
+    block_excl_scan<int64_t>(acc, sh, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// one block: exclusive scan of the tile sums (sequential chunks per thread)
+__global__ void __launch_bounds__(1024) scan_sums(int64_t* __restrict__ sums, int64_t tiles) {
+    __shared__ int64_t sh[1024 / 32 + 1];
+    const int64_t per = (tiles + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = int64_t(threadIdx.x) * per;
+    const int64_t hi = lo + per < tiles ? lo + per : tiles;
+    int64_t acc = 0;
+    for (int64_t i = lo; i < hi; i++) acc += sums[i];
+    int64_t total;
+    int64_t run = block_excl_scan<int64_t>(acc, sh, &total);
+    for (int64_t i = lo; i < hi; i++) {
+        int64_t v = sums[i];
+        sums[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) sums[tiles] = total;
+}
+
+template <class In, class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_tiles(const In* in, Out* out, int64_t n,
+                                                           const int64_t* __restrict__ sums) {
+    __shared__ int64_t sh[kScanThreads / 32 + 1];
+    const int64_t base = int64_t(blockIdx.x) * kScanTile + int64_t(threadIdx.x) * kScanItems;
+    int64_t v[kScanItems];
+    int64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        v[k] = base + k < n ? static_cast<int64_t>(in[base + k]) : 0;
+        acc += v[k];
+    }
+    int64_t total;
+    int64_t run = block_excl_scan<int64_t>(acc, sh, &total) + sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        if (base + k < n) out[base + k] = static_cast<Out>(run);
+        run += v[k];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = static_cast<Out>(sums[gridDim.x]);
+}
+
+size_t scan_workspace_bytes(int64_t n) {
+    int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles < 1) tiles = 1;
+    return size_t(tiles + 1) * sizeof(int64_t) + 256;
+}
+
+template <class In, class Out>
+static int scan_impl(const In* in, Out* out, int64_t n, void* ws, cudaStream_t s) {
+    int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles < 1) tiles = 1;
+    int64_t* sums = static_cast<int64_t*>(ws);
+    scan_tile_sums<In><<<unsigned(tiles), kScanThreads, 0, s>>>(in, n, sums);
+    HP_CHECK_LAUNCH("scan_tile_sums");
+    scan_sums<<<1, 1024, 0, s>>>(sums, tiles);
+    HP_CHECK_LAUNCH("scan_sums");
+    scan_tiles<In, Out><<<unsigned(tiles), kScanThreads, 0, s>>>(in, out, n, sums);
+    HP_CHECK_LAUNCH("scan_tiles");
+    return HP_OK;
+}
+
+int exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t s) {
+    return scan_impl<int64_t, int64_t>(in, out, n, ws, s);
+}
+int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t s) {
+    return scan_impl<int32_t, int32_t>(in, out, n, ws, s);
+}
+int exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, void* ws,
+                              cudaStream_t s) {
+    return scan_impl<int32_t, int64_t>(in, out, n, ws, s);
+}
+
+}  // namespace hp
+
+extern "C" const char* hp_last_error(void) { return hp::g_err; }
+extern "C" int hp_version(void) { return 1; }
+extern "C" int64_t hp_launch_count(void) { return hp::g_launches.load(); }

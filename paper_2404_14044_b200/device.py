@@ -1,0 +1,244 @@
+"""Device-resident pipeline: torch CUDA tensors in, torch CUDA tensors out.
+
+These are the functions the drop-in wrappers (hash_index.py, sampler.py) and
+the benchmark call.  Each one enqueues the sm_100a kernels of libhp_b200.so on
+torch's current CUDA stream through the C ABI; torch only provides device
+memory, streams and the host<->device copies.  Host synchronisation happens
+only where a size must be known to allocate an output (N_in after the build,
+Q after the query count pass, R after the sampler), as in the two-phase C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import c_i64, c_size
+
+__all__ = ["DeviceIndex", "build", "build_from_table", "query", "sample", "primary_surface",
+           "SAMPLE_STAGE_PER_RAY"]
+
+SAMPLE_STAGE_PER_RAY = 8  # staging slots reserved per ray for retained candidates
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def camera_struct(camera) -> _lib.Camera:
+    c = _lib.Camera()
+    o = np.asarray(camera.origin, np.float64)
+    rot = np.asarray(camera.orientation, np.float64)
+    for k in range(3):
+        c.origin[k] = float(o[k])
+        c.right[k] = float(rot[0, k])
+        c.up[k] = float(rot[1, k])
+        c.forward[k] = float(rot[2, k])
+    c.focal_length = float(camera.focal_length)
+    c.pixel_width = float(camera.pixel_width)
+    c.pixel_height = float(camera.pixel_height)
+    c.width = int(camera.width)
+    c.height = int(camera.height)
+    return c
+
+
+@dataclass
+class DeviceIndex:
+    """Hash index in HBM: the reference's HashIndex arrays plus the row-major
+    query layout (origin-relative fp64 coordinates, int32 ids, row pointers)."""
+
+    camera: object
+    pad: int
+    padded_width: int
+    padded_height: int
+    n_in: int
+    table_start: torch.Tensor   # int64 [P]
+    table_count: torch.Tensor   # int64 [P]
+    reordered_ids: torch.Tensor  # int64 [N_in]
+    slot_x: torch.Tensor
+    slot_y: torch.Tensor
+    slot_z: torch.Tensor
+    row_ptr: torch.Tensor       # int32 [P+1]
+    rel_x: torch.Tensor
+    rel_y: torch.Tensor
+    rel_z: torch.Tensor
+    point_id: torch.Tensor      # int32
+
+    def layout(self) -> _lib.Layout:
+        L = _lib.Layout()
+        L.row_ptr = _ptr(self.row_ptr)
+        L.rel_x = _ptr(self.rel_x)
+        L.rel_y = _ptr(self.rel_y)
+        L.rel_z = _ptr(self.rel_z)
+        L.point_id = _ptr(self.point_id)
+        return L
+
+
+def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
+    """hash_index.build on the device (reference hash_index.py:151-190)."""
+    lib = _lib.load(require_device=True)
+    pad = int(pad)
+    wp, hp = int(camera.width) + 2 * pad, int(camera.height) + 2 * pad
+    if max(wp, hp) > 0xFFFF:
+        raise ValueError("padded image exceeds 16-bit pixel coordinates")
+    dev = positions.device
+    xyz = positions.contiguous().view(-1, 3)
+    n = xyz.shape[0]
+    P = wp * hp
+    nb = c_size(0)
+    _lib.check(lib.hp_build_workspace_bytes(n, wp, hp, ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
+    i64 = dict(dtype=torch.int64, device=dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    ts, tc = torch.empty(P, **i64), torch.empty(P, **i64)
+    cap = max(n, 1)
+    rid = torch.empty(cap, **i64)
+    sx, sy, sz = (torch.empty(cap, **f64) for _ in range(3))
+    row_ptr = torch.empty(P + 1, dtype=torch.int32, device=dev)
+    rx, ry, rz = (torch.empty(cap, **f64) for _ in range(3))
+    pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    n_in_d = torch.zeros(1, **i64)
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid))
+    cam = camera_struct(camera)
+    _lib.check(lib.hp_build(_ptr(xyz), n, ctypes.byref(cam), pad, _ptr(ts), _ptr(tc), _ptr(rid),
+                            _ptr(sx), _ptr(sy), _ptr(sz), L, _ptr(n_in_d), _ptr(ws), nb.value,
+                            _stream()))
+    n_in = int(n_in_d.item()) if n > 0 else 0
+    return DeviceIndex(camera, pad, wp, hp, n_in, ts, tc, rid[:n_in], sx[:n_in], sy[:n_in],
+                       sz[:n_in], row_ptr, rx[:max(n_in, 1)], ry[:max(n_in, 1)],
+                       rz[:max(n_in, 1)], pid[:max(n_in, 1)])
+
+
+def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered_ids, camera,
+                     pad: int) -> DeviceIndex:
+    """Device index from HashIndex arrays built elsewhere (e.g. by the reference)."""
+    lib = _lib.load(require_device=True)
+    dev = table_start.device
+    pad = int(pad)
+    wp, hp = int(camera.width) + 2 * pad, int(camera.height) + 2 * pad
+    P = wp * hp
+    n_in = int(reordered_ids.numel())
+    cap = max(n_in, 1)
+    row_ptr = torch.empty(P + 1, dtype=torch.int32, device=dev)
+    rx, ry, rz = (torch.empty(cap, dtype=torch.float64, device=dev) for _ in range(3))
+    pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    nb = c_size(0)
+    _lib.check(lib.hp_layout_workspace_bytes(n_in, wp, hp, ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
+    origin = (ctypes.c_double * 3)(*[float(v) for v in np.asarray(camera.origin)])
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid))
+    _lib.check(lib.hp_layout_from_table(_ptr(table_start), _ptr(table_count), _ptr(slot_x),
+                                        _ptr(slot_y), _ptr(slot_z), _ptr(reordered_ids), n_in, wp,
+                                        hp, origin, L, _ptr(ws), nb.value, _stream()))
+    return DeviceIndex(camera, pad, wp, hp, n_in, table_start, table_count, reordered_ids, slot_x,
+                       slot_y, slot_z, row_ptr, rx, ry, rz, pid)
+
+
+def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
+          t_far: torch.Tensor, slopes: torch.Tensor):
+    """_kernels.hash_query_batch on the device (reference _kernels.py:86-157).
+
+    Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors.
+    """
+    lib = _lib.load(require_device=True)
+    dev = index.table_start.device
+    m = int(pixels.shape[0])
+    pixels = pixels.contiguous()
+    dirs = dirs.contiguous()
+    nb = c_size(0)
+    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
+    offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    probes = torch.empty(m, dtype=torch.int64, device=dev)
+    scanned = torch.empty(m, dtype=torch.int64, device=dev)
+    L = index.layout()
+    args = (L, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
+            _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
+    _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), _ptr(ws),
+                                  nb.value, _stream()))
+    total = int(offsets[m].item())
+    ids = torch.empty(total, dtype=torch.int64, device=dev)
+    t = torch.empty(total, dtype=torch.float64, device=dev)
+    d = torch.empty(total, dtype=torch.float64, device=dev)
+    _lib.check(lib.hp_query_fill(*args, _ptr(offsets), total, _ptr(ids), _ptr(t), _ptr(d),
+                                 _ptr(ws), nb.value, _stream()))
+    return offsets, ids, t, d, probes, scanned
+
+
+def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerParams:
+    p = _lib.SamplerParams()
+    p.k_neighbors = int(cfg.k_neighbors)
+    p.eps_mode = 1 if cfg.retention_mode == "epsilon" else 0
+    p.want_color = 1 if want_color else 0
+    p.exact_t_end = 1 if exact_t_end else 0
+    p.beta2 = float(cfg.beta * cfg.beta)      # as sampler.py:215
+    p.gamma = float(cfg.gamma)
+    p.eps = float(cfg.epsilon)
+    p.tau_min = float(cfg.tau_min)
+    return p
+
+
+def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torch.Tensor,
+           slopes: torch.Tensor, cfg, colors: torch.Tensor | None = None,
+           exact_t_end: bool = True):
+    """_kernels.sample_batch on the device (reference _kernels.py:552-700).
+
+    Returns (r_off, r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color, t_end).
+    ``exact_t_end=False`` stops each ray once retention is decided and reports
+    the transmittance at that point instead of over all candidates.
+    """
+    lib = _lib.load(require_device=True)
+    dev = offsets.device
+    m = int(offsets.shape[0]) - 1
+    total = int(ids.numel())
+    want = colors is not None
+    p = sampler_params(cfg, want, exact_t_end)
+    stats = torch.empty(2, dtype=torch.int64, device=dev)
+    _lib.check(lib.hp_csr_stats(_ptr(offsets), m, _ptr(stats), _stream()))
+    max_q = int(stats[1].item()) if m > 0 else 0
+    cap = max(SAMPLE_STAGE_PER_RAY * m, 1 << 16)
+    nb = c_size(0)
+    _lib.check(lib.hp_sample_workspace_bytes(m, total, max_q, cap, ctypes.byref(p),
+                                             ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
+    r_off = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    t_end = torch.empty(max(m, 0), dtype=torch.float64, device=dev)
+    col = colors.contiguous() if want else None
+    ncol = int(col.shape[0]) if want else 0
+    common = (_ptr(offsets), m, _ptr(ids), _ptr(t), _ptr(dist), total, max_q, _ptr(slopes),
+              ctypes.byref(p), _ptr(col) if want else ctypes.c_void_p(0), ncol, cap)
+    _lib.check(lib.hp_sample_run(*common, _ptr(r_off), _ptr(t_end), _ptr(ws), nb.value,
+                                 _stream()))
+    R = int(r_off[m].item())
+    i64 = dict(dtype=torch.int64, device=dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    r_id = torch.empty(R, **i64)
+    outs = [torch.empty(R, **f64) for _ in range(5)]
+    r_color = torch.empty((R, 3), **f64) if want else torch.zeros((0, 3), **f64)
+    _lib.check(lib.hp_sample_emit(*common, _ptr(r_off), R, _ptr(r_id), *[_ptr(o) for o in outs],
+                                  _ptr(r_color) if want else ctypes.c_void_p(0), _ptr(ws),
+                                  nb.value, _stream()))
+    return (r_off, r_id, *outs, r_color, t_end)
+
+
+def primary_surface(r_off: torch.Tensor, r_id: torch.Tensor, r_t: torch.Tensor):
+    """Primary-surface point per ray: (point id or -1, t or NaN)."""
+    lib = _lib.load(require_device=True)
+    m = int(r_off.shape[0]) - 1
+    pid = torch.empty(m, dtype=torch.int64, device=r_off.device)
+    pt = torch.empty(m, dtype=torch.float64, device=r_off.device)
+    _lib.check(lib.hp_primary_surface(_ptr(r_off), m, _ptr(r_id), _ptr(r_t), _ptr(pid),
+                                      _ptr(pt), _stream()))
+    return pid, pt
