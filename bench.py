@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""HashPoint B200 benchmark: rays/s of hash build + per-ray query +
+primary-surface sampling (BASELINE.json metric) on the cfg2 workload.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one frame: build the index of a 1M-point sphere-shell cloud for an
+800x800 view (delta = 0.01 -> 41x41 kernel), query all 640,000 rays, sample
+them (K = 8, eps retention, colours, exact transmittance).  Inputs are
+synthetic (seeded generators of the reference) and resident in HBM when the
+timed region starts; L2 is flushed (256 MB write) between timed steps.  With
+N > 1 (torchrun) the rays are split into contiguous row bands (equal-cost by
+the per-ray scan counts) and every rank runs its band of the same frame; the
+retained samples are gathered to rank 0 with NCCL; the step time is the max
+over ranks.
+
+--impl reference runs the reference algorithm on the host CPU (the C oracle,
+a step-for-step restatement of the reference's numba kernels, all host
+threads) on a strided ray subset of the same frame and extrapolates.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (scene kwargs, (W, H, fov), delta, t_near, t_far)
+    "cfg2": (dict(kind="sphere_surface", n=1_000_000, seed=0, noise=0.005), (800, 800, 40.0), 0.01),
+    "cfg1": (dict(kind="sphere_surface", n=100_000, seed=0, noise=0.005), (200, 200, 40.0), 0.01),
+}
+T_NEAR, T_FAR = 1.0, 10.0
+
+
+def make_workload(name):
+    import paper_2404_14044_b200 as hp
+    scene, (W, H, fov), delta = WORKLOADS[name]
+    cloud = hp.generate_scene(hp.SceneSpec(**scene))
+    cam = hp.scene_camera(W, H, fov_deg=fov)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, T_NEAR, delta),
+                          hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    m = dirs.shape[0]
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius, cfg.use_approx_radius)
+    return dict(name=name, cloud=cloud, cam=cam, cfg=cfg, dirs=dirs, pixels=pixels,
+                t_near=np.full(m, T_NEAR), t_far=np.full(m, T_FAR), slopes=slopes, m=m,
+                delta=delta)
+
+
+def describe(w):
+    c = w["cam"]
+    return (f"{w['name']}: {w['cloud'].count:,}-point sphere shell, {c.width}x{c.height} view, "
+            f"delta={w['delta']} (s={w['cfg'].kernel_size}), t in [{T_NEAR},{T_FAR}], "
+            "SamplerConfig() eps retention K=8 with colours, exact transmittance")
+
+
+def frame_bytes(n, n_in, P, m, Q, R, colors=True):
+    """Algorithmic bytes of one frame."""
+    b_build = 24 * n + 16 * P + 32 * n_in
+    b_query = 64 * m + 16 * P + 32 * n_in + 8 * (m + 1) + 24 * Q + 16 * m
+    b_sample = 8 * (m + 1) + 24 * Q + 8 * m + 8 * (m + 1) + 48 * R + 8 * m + (24 * R if colors else 0)
+    return b_build, b_query, b_sample
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 2 + k and r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_run(w, stride, threads):
+    """Reference algorithm on the host (C oracle): full build, strided rays."""
+    from oracle import oracle as orc
+    cam, cfg, cloud = w["cam"], w["cfg"], w["cloud"]
+    t0 = time.perf_counter()
+    b = orc.build(cloud.positions, cam, cfg.pad)
+    t_build = time.perf_counter() - t0
+    sel = slice(0, None, stride)
+    px = np.ascontiguousarray(w["pixels"][sel])
+    t0 = time.perf_counter()
+    q = orc.query(b["table_start"], b["table_count"], b["slot_x"], b["slot_y"], b["slot_z"],
+                  b["reordered_ids"], cam.width + 2 * cfg.pad, cfg.pad, px[:, 0], px[:, 1],
+                  w["dirs"][sel], cam.origin, w["t_near"][sel], w["t_far"][sel], w["slopes"][sel],
+                  threads=threads)
+    from paper_2404_14044_b200.sampler import SamplerConfig
+    sc = SamplerConfig()
+    orc.sample(*q[:4], w["slopes"][sel], sc.k_neighbors, sc.beta * sc.beta, sc.gamma, True,
+               sc.epsilon, sc.tau_min, cloud.colors, threads=threads)
+    t_sub = time.perf_counter() - t0
+    m_sub = px.shape[0]
+    secs = t_build + (w["m"] / m_sub) * t_sub
+    return w["m"] / secs, dict(t_build_s=t_build, t_subset_s=t_sub, m_sub=m_sub)
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    threads = host_threads()
+    stride = args.cpu_stride
+    vals = []
+    info = None
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_run(w, stride * 4, threads)
+    for _ in range(args.steps):
+        v, info = cpu_run(w, stride, threads)
+        vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "rays/sec (search+primary-surface sampling)",
+        "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * w["m"] / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": describe(w), "rays": w["m"], "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "port",
+                         "sample": f"full build + every {stride}th ray ({info['m_sub']} rays) of the "
+                                   f"frame through query+sample, extrapolated to {w['m']} rays; "
+                                   f"C restatement of the reference kernels (oracle/hp_oracle.c), "
+                                   f"{cpu_model()}"},
+        "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+def row_bands(w, world, rank):
+    """Contiguous ray range of this rank (whole image rows, cost-balanced by
+    the scan count each ray will do; every rank computes the same split)."""
+    from paper_2404_14044_b200.shard import balanced_row_bands
+    lo, hi = balanced_row_bands(w["cloud"].positions, w["cam"], w["cfg"].pad, world)[rank]
+    W = w["cam"].width
+    return lo * W, hi * W
+
+
+def run_ours(args, w, rank, world, dist):
+    import torch
+
+    import paper_2404_14044_b200 as hp
+    from paper_2404_14044_b200 import _lib, device as dv, pipeline
+    from paper_2404_14044_b200.shard import gather_samples
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    r0, r1 = row_bands(w, world, rank) if world > 1 else (0, w["m"])
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    xyz = up(w["cloud"].positions)
+    col = up(w["cloud"].colors)
+    rays = [up(w["pixels"][r0:r1]), up(w["dirs"][r0:r1]), up(w["t_near"][r0:r1]),
+            up(w["t_far"][r0:r1]), up(w["slopes"][r0:r1])]
+    scfg = hp.SamplerConfig()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(timer=None):
+        fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer)
+        if world > 1:
+            gather_samples(fr.samples, dist)
+        return fr
+
+    # parity gate (fairness gate of the reference bench, bench.py:114-134):
+    # refuse to time if the device result differs from the oracle on a subset
+    parity = "skipped"
+    if rank == 0 and not args.no_parity:
+        parity = parity_gate(w, dev)
+    for _ in range(args.warmup):
+        fr = step()
+    torch.cuda.synchronize()
+    times, stage_tot = [], {}
+    launches0 = _lib.launch_count()
+    smi = ClockSampler(dev.index)
+    with smi:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            timer = pipeline.StageTimer()
+            dv.TIMER = timer
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fr = step(timer)
+            e1.record()
+            dv.TIMER = None
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            for k, v in timer.spans().items():
+                stage_tot[k] = stage_tot.get(k, 0.0) + v
+    launches = _lib.launch_count() - launches0
+    ms = statistics.mean(times)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stages = {k: v / args.steps for k, v in stage_tot.items()}
+
+    # end-to-end through the public host-buffer API (pinned host inputs)
+    e2e = None
+    if rank == 0 and not args.no_e2e:
+        e2e = run_e2e(args, w, r0, r1)
+    if rank != 0:
+        return
+    m_total = w["m"]
+    value = m_total / (ms / 1e3)
+    n, P = w["cloud"].count, fr.index.padded_width * fr.index.padded_height
+    Q, R = fr.Q * world, fr.R * world  # per-rank band; exact only at world == 1
+    bb, bq, bs = frame_bytes(n, fr.index.n_in, P, m_total, Q, R)
+    peak, peak_kind = measured_peaks()
+    # dominant kernel: the larger of query fill / sampler run
+    cand = {
+        "k_query_fill": (stages.get("query.fill", 0.0), 24 * Q + 8 * (m_total + 1) + 64 * m_total
+                         + 32 * fr.index.n_in + 4 * (P + 1)),
+        "k_sample": (stages.get("sample.run", 0.0), 8 * (m_total + 1) + 16 * Q + 8 * m_total
+                     + 8 * (m_total + 1) + 8 * m_total),
+        "k_query_count": (stages.get("query.count", 0.0), 64 * m_total + 4 * (P + 1) + 32 * fr.index.n_in
+                          + 24 * m_total),
+    }
+    top = max(cand, key=lambda k: cand[k][0])
+    t_top, b_top = cand[top]
+    achieved = b_top / (t_top / 1e3) / 1e9 if t_top > 0 else 0.0
+    line = {
+        "metric": "rays/sec (search+primary-surface sampling)", "value": value, "unit": "rays/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded reference scene generators)",
+        "config": {"workload": describe(w), "rays": m_total, "n_points": n,
+                   "n_indexed": fr.index.n_in, "Q": Q, "R": R, "P": P,
+                   "l2": "flushed between timed steps (256 MB write)",
+                   "parallelism": f"row bands x{world}" if world > 1 else "single GPU",
+                   "parity_gate": parity},
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_kind},
+        "frame_roofline": {"bytes": bb + bq + bs, "achieved_gbs": (bb + bq + bs) / (ms / 1e3) / 1e9,
+                           "frac": (bb + bq + bs) / (ms / 1e3) / 1e9 / peak},
+        "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "gpu_launches": launches,
+        "clocks": smi.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        v, info = cpu_run(w, args.cpu_stride, host_threads())
+        line["cpu_baseline"] = {"value": v, "unit": "rays/s", "cores": host_threads(), "kind": "port",
+                                "sample": f"full build + every {args.cpu_stride}th ray "
+                                          f"({info['m_sub']} rays) through query+sample, "
+                                          f"extrapolated; oracle/hp_oracle.c; {cpu_model()}"}
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, w, r0, r1):
+    import torch
+
+    from paper_2404_14044_b200 import pipeline
+    from paper_2404_14044_b200.cloud import PointCloud
+    m = r1 - r0
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    cloud = PointCloud(w["cloud"].positions, w["cloud"].colors)
+    host = dict(pixels=pin(w["pixels"][r0:r1]), dirs=pin(w["dirs"][r0:r1]),
+                t_near=pin(w["t_near"][r0:r1]), t_far=pin(w["t_far"][r0:r1]))
+    times, out = [], None
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = pipeline.search_and_sample(cloud, w["cam"], w["cfg"], host["pixels"], host["dirs"],
+                                         host["t_near"], host["t_far"])
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    sec = statistics.mean(times)
+    h2d = (cloud.positions.nbytes + cloud.colors.nbytes + 16 * m + 24 * m + 8 * m + 8 * m + 8 * m)
+    d2h = sum(int(x.nbytes) for x in out)
+    return {"value": m / sec, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": d2h, "api": "paper_2404_14044_b200.pipeline.search_and_sample "
+                                            "(numpy in / numpy out)"}
+
+
+def parity_gate(w, dev):
+    """Device vs oracle on every 53rd ray of the frame (bit-exact ids/t/dist/
+    udf/primary; alpha/w within 1e-12)."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2404_14044_b200 import device as dv
+    from paper_2404_14044_b200.sampler import SamplerConfig
+    sel = slice(0, None, 53)
+    cam, cfg, cloud = w["cam"], w["cfg"], w["cloud"]
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    idx = dv.build(up(cloud.positions), cam, cfg.pad)
+    px = np.ascontiguousarray(w["pixels"][sel])
+    q = dv.query(idx, up(px), up(w["dirs"][sel]), up(w["t_near"][sel]), up(w["t_far"][sel]),
+                 up(w["slopes"][sel]))
+    sc = SamplerConfig()
+    s = dv.sample(q[0], q[1], q[2], q[3], up(w["slopes"][sel]), sc, up(cloud.colors))
+    b = orc.build(cloud.positions, cam, cfg.pad)
+    oq = orc.query(b["table_start"], b["table_count"], b["slot_x"], b["slot_y"], b["slot_z"],
+                   b["reordered_ids"], cam.width + 2 * cfg.pad, cfg.pad, px[:, 0], px[:, 1],
+                   w["dirs"][sel], cam.origin, w["t_near"][sel], w["t_far"][sel], w["slopes"][sel],
+                   threads=host_threads())
+    os_ = orc.sample(*oq[:4], w["slopes"][sel], sc.k_neighbors, sc.beta * sc.beta, sc.gamma, True,
+                     sc.epsilon, sc.tau_min, cloud.colors, threads=host_threads())
+    ok = all(np.array_equal(a.cpu().numpy(), b_) for a, b_ in zip(q, oq))
+    s = [x.cpu().numpy() for x in s]
+    ok &= all(np.array_equal(s[k], os_[k]) for k in range(5))
+    ok &= all(np.allclose(s[k], os_[k], rtol=1e-12, atol=1e-300) for k in (5, 6, 7, 8))
+    if not ok:
+        raise SystemExit("parity gate failed: device results differ from the oracle; not timing")
+    return f"pass (every 53rd ray, {len(px)} rays, Q={len(oq[1])}, R={len(os_[1])})"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--cpu-stride", type=int, default=97)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    w = make_workload(args.workload)
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    run_ours(args, w, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

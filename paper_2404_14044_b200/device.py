@@ -24,6 +24,14 @@ __all__ = ["DeviceIndex", "build", "build_from_table", "query", "sample", "prima
 
 SAMPLE_STAGE_PER_RAY = 8  # staging slots reserved per ray for retained candidates
 
+# Optional per-kernel timer (pipeline.StageTimer); set by the benchmark.
+TIMER = None
+
+
+def _mark(name):
+    if TIMER is not None:
+        TIMER.mark(name)
+
 
 def _ptr(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
@@ -110,11 +118,13 @@ def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
     rx, ry, rz = (torch.empty(cap, **f64) for _ in range(3))
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
     n_in_d = torch.zeros(1, **i64)
+    _mark("build.setup")
     L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid))
     cam = camera_struct(camera)
     _lib.check(lib.hp_build(_ptr(xyz), n, ctypes.byref(cam), pad, _ptr(ts), _ptr(tc), _ptr(rid),
                             _ptr(sx), _ptr(sy), _ptr(sz), L, _ptr(n_in_d), _ptr(ws), nb.value,
                             _stream()))
+    _mark("build.kernels")
     n_in = int(n_in_d.item()) if n > 0 else 0
     return DeviceIndex(camera, pad, wp, hp, n_in, ts, tc, rid[:n_in], sx[:n_in], sy[:n_in],
                        sz[:n_in], row_ptr, rx[:max(n_in, 1)], ry[:max(n_in, 1)],
@@ -166,14 +176,18 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     L = index.layout()
     args = (L, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
+    _mark("query.setup")
     _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), _ptr(ws),
                                   nb.value, _stream()))
+    _mark("query.count")
     total = int(offsets[m].item())
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
+    _mark("query.sync")
     _lib.check(lib.hp_query_fill(*args, _ptr(offsets), total, _ptr(ids), _ptr(t), _ptr(d),
                                  _ptr(ws), nb.value, _stream()))
+    _mark("query.fill")
     return offsets, ids, t, d, probes, scanned
 
 
@@ -219,17 +233,21 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     ncol = int(col.shape[0]) if want else 0
     common = (_ptr(offsets), m, _ptr(ids), _ptr(t), _ptr(dist), total, max_q, _ptr(slopes),
               ctypes.byref(p), _ptr(col) if want else ctypes.c_void_p(0), ncol, cap)
+    _mark("sample.setup")
     _lib.check(lib.hp_sample_run(*common, _ptr(r_off), _ptr(t_end), _ptr(ws), nb.value,
                                  _stream()))
+    _mark("sample.run")
     R = int(r_off[m].item())
     i64 = dict(dtype=torch.int64, device=dev)
     f64 = dict(dtype=torch.float64, device=dev)
     r_id = torch.empty(R, **i64)
     outs = [torch.empty(R, **f64) for _ in range(5)]
     r_color = torch.empty((R, 3), **f64) if want else torch.zeros((0, 3), **f64)
+    _mark("sample.sync")
     _lib.check(lib.hp_sample_emit(*common, _ptr(r_off), R, _ptr(r_id), *[_ptr(o) for o in outs],
                                   _ptr(r_color) if want else ctypes.c_void_p(0), _ptr(ws),
                                   nb.value, _stream()))
+    _mark("sample.emit")
     return (r_off, r_id, *outs, r_color, t_end)
 
 
