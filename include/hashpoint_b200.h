@@ -59,13 +59,16 @@ typedef struct {
  * (within a pixel: ascending original id, as in the reference's slots), with
  * coordinates pre-shifted by the camera origin.  A kernel row of s pixels is
  * then ONE contiguous slot range.  Device arrays; caller-allocated:
- * row_ptr[P+1], rel_x/rel_y/rel_z/point_id[N_in] (capacity n for hp_build). */
+ * row_ptr[P+1], rel_x/rel_y/rel_z/point_id[N_in], relf[4*N_in] (capacity n
+ * for hp_build).  relf holds (x, y, z, e) in float32 for the filter: the
+ * rounded coordinates and the point's error budget e = 2^-18 * |p|_1. */
 typedef struct {
     int32_t* row_ptr;
     double* rel_x;
     double* rel_y;
     double* rel_z;
     int32_t* point_id;
+    float* relf;
 } hp_query_layout;
 
 typedef struct {
@@ -154,6 +157,11 @@ int hp_csr_stats(const int64_t* offsets, int64_t m, int64_t* out2, hp_stream_t s
 /* primary_id[r] = r_id[r_off[r]] or -1; primary_t[r] = r_t[r_off[r]] or NaN. */
 int hp_primary_surface(const int64_t* r_off, int64_t m, const int64_t* r_id, const double* r_t,
                        int64_t* primary_id, double* primary_t, hp_stream_t stream);
+
+/* Sampler path counters since the last reset (diagnostics):
+ * [rays with candidates, fast-path rays, rays whose transmittance was proved 0,
+ *  exactly evaluated candidates, candidates, sum of jstar, -, -]. */
+int hp_sample_debug_counters(int64_t* out8, int reset);
 
 /* Kernel launches issued by this library since load (for bench gpu_launches). */
 int64_t hp_launch_count(void);

@@ -29,7 +29,7 @@ class Camera(ctypes.Structure):
 
 class Layout(ctypes.Structure):
     _fields_ = [("row_ptr", c_p), ("rel_x", c_p), ("rel_y", c_p), ("rel_z", c_p),
-                ("point_id", c_p)]
+                ("point_id", c_p), ("relf", c_p)]
 
 
 class SamplerParams(ctypes.Structure):
@@ -64,6 +64,7 @@ _SIGNATURES = {
                                       c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
     "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "hp_sample_debug_counters": (ctypes.c_int, [c_p, ctypes.c_int]),
 }
 
 EXPORTS = tuple(_SIGNATURES)

@@ -10,6 +10,7 @@
 // padded pixel grid, empty pixels get start 0, and points inside a pixel are
 // ordered by ascending original index.
 #include "hp_common.cuh"
+#include "hp_cone.cuh"
 #include "hp_sortnet.cuh"
 
 namespace hp {
@@ -21,6 +22,7 @@ struct CamDev {
 };
 
 constexpr int kProjThreads = 256;
+
 constexpr int kSmallBucket = 32;
 
 // Bucket (row-major padded pixel) of one point; -1 if not rasterized.
@@ -211,10 +213,12 @@ __global__ void k_gather(int64_t n_cap, const int64_t* __restrict__ n_in_dev, co
         slot_z[s] = z;
         const int32_t l = lin[id];
         const int64_t rm = int64_t(L.row_ptr[l]) + (s - table_start[l]);
-        L.rel_x[rm] = dsub(x, o0);
-        L.rel_y[rm] = dsub(y, o1);
-        L.rel_z[rm] = dsub(z, o2);
+        const double rx = dsub(x, o0), ry = dsub(y, o1), rz = dsub(z, o2);
+        L.rel_x[rm] = rx;
+        L.rel_y[rm] = ry;
+        L.rel_z[rm] = rz;
         L.point_id[rm] = id;
+        reinterpret_cast<float4*>(L.relf)[rm] = filter_point(rx, ry, rz);
     }
 }
 
@@ -237,10 +241,12 @@ __global__ void k_layout_fill(int64_t P, const int64_t* __restrict__ table_start
         if (c == 0) continue;
         const int64_t s0 = table_start[l], r0 = L.row_ptr[l];
         for (int64_t k = lane_id(); k < c; k += 32) {
-            L.rel_x[r0 + k] = dsub(sx[s0 + k], o0);
-            L.rel_y[r0 + k] = dsub(sy[s0 + k], o1);
-            L.rel_z[r0 + k] = dsub(sz[s0 + k], o2);
+            const double rx = dsub(sx[s0 + k], o0), ry = dsub(sy[s0 + k], o1), rz = dsub(sz[s0 + k], o2);
+            L.rel_x[r0 + k] = rx;
+            L.rel_y[r0 + k] = ry;
+            L.rel_z[r0 + k] = rz;
             L.point_id[r0 + k] = int32_t(sid[s0 + k]);
+            reinterpret_cast<float4*>(L.relf)[r0 + k] = filter_point(rx, ry, rz);
         }
     }
 }

@@ -1,4 +1,4 @@
-// hp_query.cu — per-ray cone query over the hash index (two passes).
+// hp_query.cu — per-ray cone query over the hash index.
 //
 // Reference: _kernels.hash_query_batch (_kernels.py:86-157), _cone_test
 // (:22-36), _canonical_sort (:39-73).
@@ -7,27 +7,32 @@
 // pixel (hp_query_layout), so the s pixels of one kernel row are ONE
 // contiguous slot range [row_ptr[y*Wp + u], row_ptr[y*Wp + u + s]).
 //
-// Work decomposition: a CTA owns a GROUP of consecutive rays (up to 32; for
-// ray_grid input these are horizontally adjacent pixels) and streams the
-// union of their kernel rows through shared memory, one padded image row at a
-// time.  Every staged point is cone-tested by every ray of the group whose
-// window covers it (~18 rays for s = 41, G = 32), so L2 traffic is ~1/18 of a
-// per-ray scan.
+// Work decomposition: a CTA owns a GROUP of up to 32 consecutive rays (for
+// ray_grid input: horizontally adjacent pixels) and streams the union of
+// their kernel rows through shared memory, one padded image row at a time.
+// Every staged point is tested by every ray of the group whose window covers
+// it (~18 rays for s = 41), so L2 traffic is ~1/18 of a per-ray scan.
 //
-//   pass 1 (hp_query_count): exact per-ray match count, probes (= s*s) and
-//          scanned (sum of table counts over the window); offsets = scan.
-//   pass 2 (hp_query_fill):  rays regrouped so a group's matches fit in
-//          shared memory; matches are appended per ray, sorted by (t, id)
-//          in shared memory (bucket by t + exact in-bucket rank) and written
-//          once, coalesced.  Rays with more matches than fit are handled by
-//          a global-memory path (in-place sorting network).
+// Cone test: a float32 filter with a rigorous error budget classifies each
+// (ray, point) pair as sure-reject / sure-accept / uncertain (DESIGN.md "fp32
+// filter"); the reference's fp64 test (same operation order, no FMA) decides
+// the uncertain pairs and produces the exact t_proj / dist_perp of accepted
+// ones, so results are bit-identical to the reference.
 //
-// The cone test is fp64 with the reference's operation order and no FMA, so
-// ids, t_proj and dist_perp are bit-identical to the reference.
+//   k_query_count  exact per-ray count, probes (= s*s), scanned; offsets = scan
+//   k_query_fill   same streaming; accepted pairs written (unsorted) into the
+//                  ray's CSR segment
+//   k_query_sort   per ray: (t, id) sort of its segment in shared memory
+//                  (bucket by t + exact in-bucket rank), in place; segments
+//                  longer than the shared buffer use an in-place sorting
+//                  network in global memory
+#include <math_constants.h>
+
 #include <cfloat>
 #include <climits>
 
 #include "hp_common.cuh"
+#include "hp_cone.cuh"
 #include "hp_sortnet.cuh"
 
 namespace hp {
@@ -35,10 +40,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kGroupMax = 32;     // rays per group
-constexpr int kStage = 1024;      // staged points per chunk of a row
-constexpr int kFillCap = 4096;    // matches buffered per fill group
-constexpr int kBucketMax = 2048;  // buckets for the per-ray sort
+constexpr int kGroupMax = 32;  // rays per group
+constexpr int kStageCount = 2048;
+constexpr int kStageFill = 512;
 
 struct Rays {
     const int64_t* pix;
@@ -48,25 +52,6 @@ struct Rays {
     const double* tf;
     const double* slopes;
 };
-
-struct RayParams {
-    int u, v;  // padded window origin (== unpadded pixel)
-    double d0, d1, d2, tn, tf, slope;
-};
-
-// _cone_test (_kernels.py:22-36): t = p.d; reject outside [tn, tf]; reject
-// when |p - t d|^2 > (t * slope)^2.  Returns the exact fp64 t and dist^2.
-__device__ __forceinline__ bool cone_test(double p0, double p1, double p2, const RayParams& r,
-                                          double& t, double& dist2) {
-    t = dadd(dadd(dmul(p0, r.d0), dmul(p1, r.d1)), dmul(p2, r.d2));
-    if (t < r.tn || t > r.tf) return false;
-    const double e0 = dsub(p0, dmul(t, r.d0));
-    const double e1 = dsub(p1, dmul(t, r.d1));
-    const double e2 = dsub(p2, dmul(t, r.d2));
-    dist2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
-    const double rad = dmul(t, r.slope);
-    return !(dist2 > dmul(rad, rad));
-}
 
 __device__ __forceinline__ RayParams load_ray(const Rays& R, int64_t r) {
     RayParams p;
@@ -78,72 +63,19 @@ __device__ __forceinline__ RayParams load_ray(const Rays& R, int64_t r) {
     p.tn = R.tn[r];
     p.tf = R.tf[r];
     p.slope = R.slopes[r];
+    ray_derive(p);
     return p;
 }
 
-// Shared state of one streamed group.
-struct GroupSmem {
+struct GroupHead {
     RayParams ray[kGroupMax];
     int lo[kGroupMax], hi[kGroupMax];  // the ray's slot sub-range in the current row
-    double px[kStage], py[kStage], pz[kStage];
-    int pid[kStage];
-    int stage_lo, stage_hi, u0, u1, v0, v1;
+    int stage_lo[2], stage_hi[2];  // by row parity (no end-of-row barrier needed)
+    int u0, u1, v0, v1;
 };
 
-// Streams the rows of a group; calls visit(ray_slot, slot_index_in_stage, t,
-// dist2) for every accepted (ray, point) pair, on the warp that owns the ray
-// (warp w owns rays w, w+8, ...).  `with_ids` stages point ids as well.
-template <bool kWithIds, class Visit, class RowDone>
-__device__ void stream_group(GroupSmem& S, int G, const hp_query_layout L, int64_t wp, int s,
-                             Visit visit, RowDone row_done) {
-    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-    for (int y = S.v0; y < S.v1; y++) {
-        const int64_t rowbase = int64_t(y) * wp;
-        // each ray's sub-range of this row (rays outside the row: empty)
-        if (tid < G) {
-            const RayParams& r = S.ray[tid];
-            if (y >= r.v && y < r.v + s) {
-                S.lo[tid] = L.row_ptr[rowbase + r.u];
-                S.hi[tid] = L.row_ptr[rowbase + r.u + s];
-            } else {
-                S.lo[tid] = S.hi[tid] = 0;
-            }
-        }
-        if (tid == 0) {
-            S.stage_lo = L.row_ptr[rowbase + S.u0];
-            S.stage_hi = L.row_ptr[rowbase + S.u1];
-        }
-        __syncthreads();
-        const int A = S.stage_lo, B = S.stage_hi;
-        for (int c0 = A; c0 < B; c0 += kStage) {
-            const int c1 = c0 + kStage < B ? c0 + kStage : B;
-            for (int k = c0 + tid; k < c1; k += kThreads) {
-                S.px[k - c0] = L.rel_x[k];
-                S.py[k - c0] = L.rel_y[k];
-                S.pz[k - c0] = L.rel_z[k];
-                if (kWithIds) S.pid[k - c0] = L.point_id[k];
-            }
-            __syncthreads();
-            for (int g = warp; g < G; g += kWarps) {
-                const int lo = max(S.lo[g], c0), hi = min(S.hi[g], c1);
-                if (lo >= hi) continue;
-                const RayParams r = S.ray[g];
-                for (int base = lo; base < hi; base += 32) {
-                    const int k = base + lane;
-                    double t = 0.0, d2 = 0.0;
-                    bool ok = false;
-                    if (k < hi) ok = cone_test(S.px[k - c0], S.py[k - c0], S.pz[k - c0], r, t, d2);
-                    visit(g, k - c0, ok, t, d2);
-                }
-            }
-            __syncthreads();
-        }
-        row_done(y);
-    }
-}
-
 // Group bounding box (padded coordinates) of rays [r0, r0+G).
-__device__ void group_setup(GroupSmem& S, const Rays& R, int64_t r0, int G, int s) {
+__device__ void group_setup(GroupHead& S, const Rays& R, int64_t r0, int G, int s) {
     const int tid = threadIdx.x;
     if (tid < G) S.ray[tid] = load_ray(R, r0 + tid);
     __syncthreads();
@@ -172,112 +104,206 @@ __device__ void group_setup(GroupSmem& S, const Rays& R, int64_t r0, int G, int 
     __syncthreads();
 }
 
+// Streams the kernel rows of a group.  For each staged chunk of a row,
+// stage(c0, c1) loads slots [c0, c1) into shared memory, then every warp
+// calls test(g, k, c0) for the rays g it owns (warp w owns rays w, w+8, ...)
+// over their sub-range, 32 slots at a time (lanes beyond the range get
+// k = -1).  row_done() runs once per row after the ranges are known.
+template <int kStage, class Stage, class Test, class RowDone>
+__device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, Stage stage,
+                             Test test, RowDone row_done) {
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    for (int y = S.v0; y < S.v1; y++) {
+        const int64_t rowbase = int64_t(y) * wp;
+        if (tid < G) {
+            const RayParams& r = S.ray[tid];
+            if (y >= r.v && y < r.v + s) {
+                S.lo[tid] = L.row_ptr[rowbase + r.u];
+                S.hi[tid] = L.row_ptr[rowbase + r.u + s];
+            } else {
+                S.lo[tid] = S.hi[tid] = 0;
+            }
+        }
+        if (tid == 0) {
+            S.stage_lo[y & 1] = L.row_ptr[rowbase + S.u0];
+            S.stage_hi[y & 1] = L.row_ptr[rowbase + S.u1];
+        }
+        __syncthreads();
+        row_done();
+        const int A = S.stage_lo[y & 1], B = S.stage_hi[y & 1];
+        for (int c0 = A; c0 < B; c0 += kStage) {
+            const int c1 = c0 + kStage < B ? c0 + kStage : B;
+            stage(c0, c1);
+            __syncthreads();
+            for (int g = warp; g < G; g += kWarps) {
+                const int lo = max(S.lo[g], c0), hi = min(S.hi[g], c1);
+                for (int base = lo; base < hi; base += 32) {
+                    const int k = base + lane;
+                    test(g, k < hi ? k : -1, c0);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 // ---------------------------------------------------------------- pass 1
+struct CountSmem {
+    GroupHead head;
+    float4 pf[kStageCount];
+    int64_t cnt[kGroupMax], scn[kGroupMax];
+};
+
 __global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int64_t wp, int pad, Rays R,
                                                           int64_t m, int64_t* __restrict__ counts,
                                                           int64_t* __restrict__ probes,
                                                           int64_t* __restrict__ scanned) {
-    __shared__ GroupSmem S;
-    __shared__ int64_t cnt[kGroupMax], scn[kGroupMax];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    CountSmem& S = *reinterpret_cast<CountSmem*>(dyn);
     const int s = 2 * pad + 1;
+    const float4* __restrict__ relf = reinterpret_cast<const float4*>(L.relf);
     for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
         const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
-        if (threadIdx.x < kGroupMax) cnt[threadIdx.x] = scn[threadIdx.x] = 0;
-        group_setup(S, R, r0, G, s);
-        stream_group<false>(
-            S, G, L, wp, s,
-            [&](int g, int, bool ok, double, double) {
-                const unsigned b = __ballot_sync(0xffffffffu, ok);
-                if (lane_id() == 0) cnt[g] += __popc(b);
+        if (threadIdx.x < kGroupMax) S.cnt[threadIdx.x] = S.scn[threadIdx.x] = 0;
+        group_setup(S.head, R, r0, G, s);
+        stream_group<kStageCount>(
+            S.head, G, L, wp, s,
+            [&](int c0, int c1) {
+                for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) S.pf[k - c0] = relf[k];
             },
-            [&](int) {
-                if (threadIdx.x < G) scn[threadIdx.x] += S.hi[threadIdx.x] - S.lo[threadIdx.x];
+            [&](int g, int k, int c0) {
+                int cls = 0;
+                if (k >= 0) {
+                    const RayParams& r = S.head.ray[g];
+                    cls = cone_filter(S.pf[k - c0], r);
+                    if (cls == 2) {
+                        double t, d2;
+                        cls = cone_test(L.rel_x[k], L.rel_y[k], L.rel_z[k], r, t, d2) ? 1 : 0;
+                    }
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
+                if (lane_id() == 0) S.cnt[g] += __popc(b);
+            },
+            [&]() {
+                if (threadIdx.x < G) S.scn[threadIdx.x] += S.head.hi[threadIdx.x] - S.head.lo[threadIdx.x];
             });
         __syncthreads();
         if (threadIdx.x < G) {
-            counts[r0 + threadIdx.x] = cnt[threadIdx.x];
+            counts[r0 + threadIdx.x] = S.cnt[threadIdx.x];
             probes[r0 + threadIdx.x] = int64_t(s) * s;
-            scanned[r0 + threadIdx.x] = scn[threadIdx.x];
+            scanned[r0 + threadIdx.x] = S.scn[threadIdx.x];
         }
         __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------- grouping
-// Greedy split of every 32-ray chunk into fill groups whose total match count
-// fits kFillCap; rays above kFillCap become single "big" groups; groups with
-// no matches are dropped.  Descriptor: x = first ray, y = ray count | big<<8.
-__global__ void k_make_groups(const int64_t* __restrict__ off, int64_t m, int2* __restrict__ groups,
-                              int* __restrict__ ngroups) {
-    const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
-    for (int64_t c = blockIdx.x * int64_t(blockDim.x / 32) + warp_id(); c * 32 < m; c += warps) {
-        if (lane_id() == 0) {
-            int64_t first = c * 32, sum = 0;
-            int n = 0;
-            const int len = int(m - c * 32 < 32 ? m - c * 32 : 32);
-            for (int k = 0; k < len; k++) {
-                const int64_t qk = off[c * 32 + k + 1] - off[c * 32 + k];
-                if (qk > kFillCap) {
-                    if (n && sum) groups[atomicAdd(ngroups, 1)] = make_int2(int(first), n);
-                    groups[atomicAdd(ngroups, 1)] = make_int2(int(c * 32 + k), 1 | (1 << 8));
-                    first = c * 32 + k + 1;
-                    n = 0;
-                    sum = 0;
-                    continue;
-                }
-                if (sum + qk > kFillCap) {
-                    if (sum) groups[atomicAdd(ngroups, 1)] = make_int2(int(first), n);
-                    first = c * 32 + k;
-                    n = 0;
-                    sum = 0;
-                }
-                sum += qk;
-                n++;
-            }
-            if (n && sum) groups[atomicAdd(ngroups, 1)] = make_int2(int(first), n);
-        }
-        __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------- pass 2
 struct FillSmem {
-    double t[kFillCap];
-    double d[kFillCap];
-    int id[kFillCap];
-    unsigned short lst[kFillCap];
-    unsigned short perm[kFillCap];
-    unsigned int bk[kFillCap];  // bucket << 16 | local index
-    int hist[kBucketMax + 1];
-    int base[kGroupMax + 1];  // region of each ray in the buffers
+    GroupHead head;
+    float4 pf[kStageFill];
+    double px[kStageFill], py[kStageFill], pz[kStageFill];
+    int pid[kStageFill];
     int fill[kGroupMax];
-    int64_t out_off[kGroupMax];
+    int64_t off[kGroupMax];
+};
+
+__global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int64_t wp, int pad, Rays R,
+                                                         int64_t m, const int64_t* __restrict__ off,
+                                                         int64_t* __restrict__ out_id, double* __restrict__ out_t,
+                                                         double* __restrict__ out_d) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    FillSmem& S = *reinterpret_cast<FillSmem*>(dyn);
+    const int s = 2 * pad + 1;
+    const float4* __restrict__ relf = reinterpret_cast<const float4*>(L.relf);
+    for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
+        const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
+        // skip groups without matches
+        const int64_t total = off[r0 + G] - off[r0];
+        if (total == 0) continue;
+        if (threadIdx.x < G) {
+            S.fill[threadIdx.x] = 0;
+            S.off[threadIdx.x] = off[r0 + threadIdx.x];
+        }
+        group_setup(S.head, R, r0, G, s);
+        stream_group<kStageFill>(
+            S.head, G, L, wp, s,
+            [&](int c0, int c1) {
+                for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) {
+                    S.pf[k - c0] = relf[k];
+                    S.px[k - c0] = L.rel_x[k];
+                    S.py[k - c0] = L.rel_y[k];
+                    S.pz[k - c0] = L.rel_z[k];
+                    S.pid[k - c0] = L.point_id[k];
+                }
+            },
+            [&](int g, int k, int c0) {
+                int cls = 0;
+                double t = 0.0, d2 = 0.0;
+                if (k >= 0) {
+                    const RayParams& r = S.head.ray[g];
+                    const int i = k - c0;
+                    cls = cone_filter(S.pf[i], r);
+                    if (cls != 0) {
+                        const bool ok = cone_test(S.px[i], S.py[i], S.pz[i], r, t, d2);
+                        if (cls == 2) cls = ok ? 1 : 0;
+                    }
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
+                if (cls == 1) {
+                    const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
+                    out_t[pos] = t;
+                    out_d[pos] = sqrt(d2);
+                    out_id[pos] = S.pid[k - c0];
+                }
+                __syncwarp();
+                if (lane_id() == 0) S.fill[g] += __popc(b);
+                __syncwarp();
+            },
+            [&]() {});
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- sort
+__device__ __forceinline__ bool key_less(double ta, int64_t ia, double tb, int64_t ib) {
+    return ta < tb || (ta == tb && ia < ib);
+}
+
+template <int kCap>
+struct SortSmem {
+    double t[kCap];
+    int id[kCap];  // point ids < 2^31 (hp_build)
+    unsigned int bk[kCap];  // bucket << 16 | local index
+    unsigned short lst[kCap];
+    unsigned short perm[kCap];
+    int hist[kCap + 1];
     unsigned long long tmin, tmax;
     int scan_sh[kWarps + 1];
 };
 
-__device__ __forceinline__ bool key_less(double ta, int ia, double tb, int ib) {
-    return ta < tb || (ta == tb && ia < ib);
-}
-
-// Sort the q matches of one ray (region [b0, b0+q) of the buffers) by
-// (t, id) and write them to the output segment at `off`.  Block-wide.
-__device__ void sort_and_write(FillSmem& F, int b0, int q, int64_t off, int64_t* __restrict__ out_id,
-                               double* __restrict__ out_t, double* __restrict__ out_d) {
+// Sort one ray's segment [off, off+q) by (t, id) in place (q <= kCap).
+template <int kCap>
+__device__ void sort_segment(SortSmem<kCap>& F, int q, int64_t* __restrict__ gid, double* __restrict__ gt,
+                             double* __restrict__ gd) {
+    constexpr int kPer = (kCap + kThreads - 1) / kThreads;
     const int tid = threadIdx.x;
+    for (int e = tid; e < q; e += kThreads) {
+        F.t[e] = gt[e];
+        F.id[e] = int(gid[e]);
+    }
     if (q <= 64) {
-        // direct rank: each element counts the elements ordered before it
+        __syncthreads();
         for (int e = tid; e < q; e += kThreads) {
-            const double te = F.t[b0 + e];
-            const int ie = F.id[b0 + e];
+            const double te = F.t[e];
+            const int ie = F.id[e];
             int rank = 0;
-            for (int k = 0; k < q; k++) rank += key_less(F.t[b0 + k], F.id[b0 + k], te, ie);
-            F.perm[b0 + rank] = (unsigned short)e;
+            for (int k = 0; k < q; k++) rank += key_less(F.t[k], F.id[k], te, ie);
+            F.perm[rank] = (unsigned short)e;
         }
         __syncthreads();
     } else {
         int nb = 64;
-        while (nb < q && nb < kBucketMax) nb <<= 1;
+        while (nb < q && nb < kCap) nb <<= 1;
         if (tid == 0) {
             F.tmin = ~0ull;
             F.tmax = 0ull;
@@ -286,13 +312,14 @@ __device__ void sort_and_write(FillSmem& F, int b0, int q, int64_t off, int64_t*
         __syncthreads();
         unsigned long long lmin = ~0ull, lmax = 0;
         for (int e = tid; e < q; e += kThreads) {
-            const unsigned long long kk = okey(F.t[b0 + e]);
+            const unsigned long long kk = okey(F.t[e]);
             lmin = lmin < kk ? lmin : kk;
             lmax = lmax > kk ? lmax : kk;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long a = __shfl_xor_sync(0xffffffffu, lmin, o), b = __shfl_xor_sync(0xffffffffu, lmax, o);
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lmin, o);
+            const unsigned long long b = __shfl_xor_sync(0xffffffffu, lmax, o);
             lmin = lmin < a ? lmin : a;
             lmax = lmax > b ? lmax : b;
         }
@@ -301,7 +328,6 @@ __device__ void sort_and_write(FillSmem& F, int b0, int q, int64_t off, int64_t*
             atomicMax(&F.tmax, lmax);
         }
         __syncthreads();
-        // okey is invertible: recover the doubles
         const unsigned long long kmin = F.tmin, kmax = F.tmax;
         const double tlo = __longlong_as_double((kmin & 0x8000000000000000ull) ? (kmin & 0x7fffffffffffffffull) : ~kmin);
         const double thi = __longlong_as_double((kmax & 0x8000000000000000ull) ? (kmax & 0x7fffffffffffffffull) : ~kmax);
@@ -310,15 +336,13 @@ __device__ void sort_and_write(FillSmem& F, int b0, int q, int64_t off, int64_t*
         const double scale = span > 0.0 ? fmin(__ddiv_rn(double(nb), span), DBL_MAX) : 0.0;
         for (int e = tid; e < q; e += kThreads) {
             // monotone in t: (t - tlo) and the positive scaling both preserve order
-            const double x = fmin(dmul(dsub(F.t[b0 + e], tlo), scale), double(nb - 1));
+            const double x = fmin(dmul(dsub(F.t[e], tlo), scale), double(nb - 1));
             const int b = int(x);
             const int li = atomicAdd(&F.hist[b], 1);
-            F.bk[b0 + e] = (unsigned(b) << 16) | unsigned(li);
+            F.bk[e] = (unsigned(b) << 16) | unsigned(li);
         }
         __syncthreads();
-        // exclusive scan of hist[0..nb) (nb <= kBucketMax = 8 per thread)
         {
-            constexpr int kPer = kBucketMax / kThreads;
             int v[kPer], acc = 0;
 #pragma unroll
             for (int k = 0; k < kPer; k++) {
@@ -337,140 +361,89 @@ __device__ void sort_and_write(FillSmem& F, int b0, int q, int64_t off, int64_t*
         }
         __syncthreads();
         for (int e = tid; e < q; e += kThreads) {
-            const unsigned bk = F.bk[b0 + e];
-            F.lst[b0 + F.hist[bk >> 16] + (bk & 0xffffu)] = (unsigned short)e;
+            const unsigned bk = F.bk[e];
+            F.lst[F.hist[bk >> 16] + (bk & 0xffffu)] = (unsigned short)e;
         }
         __syncthreads();
         for (int e = tid; e < q; e += kThreads) {
-            const unsigned bk = F.bk[b0 + e];
+            const unsigned bk = F.bk[e];
             const int bs = F.hist[bk >> 16];
             const int be = (int(bk >> 16) + 1 < nb) ? F.hist[(bk >> 16) + 1] : q;
-            const double te = F.t[b0 + e];
-            const int ie = F.id[b0 + e];
+            const double te = F.t[e];
+            const int ie = F.id[e];
             int rank = 0;
             for (int k = bs; k < be; k++) {
-                const int o = F.lst[b0 + k];
-                rank += key_less(F.t[b0 + o], F.id[b0 + o], te, ie);
+                const int o = F.lst[k];
+                rank += key_less(F.t[o], F.id[o], te, ie);
             }
-            F.perm[b0 + bs + rank] = (unsigned short)e;
+            F.perm[bs + rank] = (unsigned short)e;
         }
         __syncthreads();
     }
-    for (int p = tid; p < q; p += kThreads) {
-        const int e = F.perm[b0 + p];
-        out_id[off + p] = F.id[b0 + e];
-        out_t[off + p] = F.t[b0 + e];
-        out_d[off + p] = F.d[b0 + e];
+    // dist: gather in permuted order into registers before overwriting
+    double dv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+        const int p = tid + k * kThreads;
+        if (p < q) dv[k] = gd[F.perm[p]];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+        const int p = tid + k * kThreads;
+        if (p < q) {
+            const int e = F.perm[p];
+            gd[p] = dv[k];
+            gt[p] = F.t[e];
+            gid[p] = F.id[e];
+        }
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int64_t wp, int pad, Rays R,
-                                                         const int64_t* __restrict__ off,
-                                                         const int2* __restrict__ groups,
-                                                         const int* __restrict__ ngroups,
-                                                         int* __restrict__ work, int64_t* __restrict__ out_id,
-                                                         double* __restrict__ out_t, double* __restrict__ out_d) {
-    __shared__ GroupSmem S;
+// Rays with lo_q < q <= kCap (kCap > 0), or q > lo_q with the in-place global
+// network (kCap == 0).
+template <int kCap>
+__global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restrict__ off, int64_t m, int lo_q,
+                                                         int64_t* __restrict__ out_id, double* __restrict__ out_t,
+                                                         double* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char dyn[];
-    FillSmem& F = *reinterpret_cast<FillSmem*>(dyn);
-    __shared__ int gidx;
-    const int s = 2 * pad + 1;
-    const int ng = *ngroups;
-    for (;;) {
-        if (threadIdx.x == 0) gidx = atomicAdd(work, 1);
-        __syncthreads();
-        const int gi = gidx;
-        __syncthreads();
-        if (gi >= ng) break;
-        const int2 gd = groups[gi];
-        const int64_t r0 = gd.x;
-        const int G = gd.y & 0xff;
-        const bool big = (gd.y >> 8) & 1;
-        group_setup(S, R, r0, G, s);
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int g = 0; g < G; g++) {
-                F.base[g] = acc;
-                F.fill[g] = 0;
-                F.out_off[g] = off[r0 + g];
-                acc += int(off[r0 + g + 1] - off[r0 + g]);
-            }
-            F.base[G] = acc;
-        }
-        __syncthreads();
-        if (!big) {
-            stream_group<true>(
-                S, G, L, wp, s,
-                [&](int g, int k, bool ok, double t, double d2) {
-                    const unsigned b = __ballot_sync(0xffffffffu, ok);
-                    if (ok) {
-                        const int pos = F.base[g] + F.fill[g] + __popc(b & ((1u << lane_id()) - 1));
-                        F.t[pos] = t;
-                        F.d[pos] = sqrt(d2);
-                        F.id[pos] = S.pid[k];
-                    }
-                    __syncwarp();
-                    if (lane_id() == 0) F.fill[g] += __popc(b);
-                    __syncwarp();
-                },
-                [&](int) {});
-            __syncthreads();
-            for (int g = 0; g < G; g++) {
-                const int q = F.base[g + 1] - F.base[g];
-                if (q == 0) continue;
-                sort_and_write(F, F.base[g], q, F.out_off[g], out_id, out_t, out_d);
-            }
+    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+        const int64_t o = off[r];
+        const int64_t q = off[r + 1] - o;
+        if (q <= lo_q || q < 2) continue;
+        if constexpr (kCap > 0) {
+            if (q > kCap) continue;
+            sort_segment<kCap>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), out_id + o, out_t + o, out_d + o);
         } else {
-            // one ray with more matches than the shared buffer: append into the
-            // output segment (unsorted), then sort it in place in global memory.
-            const int64_t o = F.out_off[0];
-            stream_group<true>(
-                S, 1, L, wp, s,
-                [&](int, int k, bool ok, double t, double d2) {
-                    const unsigned b = __ballot_sync(0xffffffffu, ok);
-                    if (ok) {
-                        const int64_t pos = o + F.fill[0] + __popc(b & ((1u << lane_id()) - 1));
-                        out_t[pos] = t;
-                        out_d[pos] = sqrt(d2);
-                        out_id[pos] = S.pid[k];
-                    }
-                    __syncwarp();
-                    if (lane_id() == 0) F.fill[0] += __popc(b);
-                    __syncwarp();
-                },
-                [&](int) {});
-            __syncthreads();
-            const int64_t q = off[r0 + 1] - off[r0];
             double* tt = out_t + o;
             double* dd = out_d + o;
             int64_t* ii = out_id + o;
             block_bitonic_sort(
-                q, [&](int64_t a, int64_t b) { return tt[a] < tt[b] || (tt[a] == tt[b] && ii[a] < ii[b]); },
+                q, [&](int64_t a, int64_t b) { return key_less(tt[a], ii[a], tt[b], ii[b]); },
                 [&](int64_t a, int64_t b) {
-                    double x = tt[a]; tt[a] = tt[b]; tt[b] = x;
-                    x = dd[a]; dd[a] = dd[b]; dd[b] = x;
-                    int64_t y = ii[a]; ii[a] = ii[b]; ii[b] = y;
+                    double x = tt[a];
+                    tt[a] = tt[b];
+                    tt[b] = x;
+                    x = dd[a];
+                    dd[a] = dd[b];
+                    dd[b] = x;
+                    const int64_t y = ii[a];
+                    ii[a] = ii[b];
+                    ii[b] = y;
                 });
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
-struct QueryWs {
-    int2* groups;
-    int* ngroups;
-    int* work;
-    void* scan;
-};
+constexpr int kSortSmall = 2048;
+constexpr int kSortLarge = 8192;
 
-QueryWs carve_query(Carver& c, int64_t m) {
-    QueryWs w;
-    w.groups = c.take<int2>(m > 0 ? m : 1);
-    w.ngroups = c.take<int>(1);
-    w.work = c.take<int>(1);
-    w.scan = c.take<char>(scan_workspace_bytes(m + 1));
-    return w;
+template <class K>
+int set_smem(K kernel, size_t bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    return e == cudaSuccess ? HP_OK : cuda_status(e, "cudaFuncSetAttribute");
 }
 
 int check_common(const hp_query_layout& L, int64_t pad, int64_t m) {
@@ -485,15 +458,19 @@ int check_common(const hp_query_layout& L, int64_t pad, int64_t m) {
     return HP_OK;
 }
 
+unsigned group_grid(int64_t m, int per_sm) {
+    const int64_t groups = (m + kGroupMax - 1) / kGroupMax;
+    const int64_t cap = int64_t(kNumSMs) * per_sm;
+    return unsigned(groups < cap ? (groups > 0 ? groups : 1) : cap);
+}
+
 }  // namespace
 }  // namespace hp
 
 using namespace hp;
 
 extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, size_t* bytes) {
-    Carver c(nullptr, 0);
-    carve_query(c, m);
-    *bytes = c.used + 256;
+    *bytes = scan_workspace_bytes(m + 1) + 256;
     (void)pad;
     return HP_OK;
 }
@@ -505,21 +482,23 @@ extern "C" int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t 
                               size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(check_common(layout, pad, m));
     (void)padded_h;
-    Carver c(workspace, workspace_bytes);
-    QueryWs w = carve_query(c, m);
-    if (!c.ok()) {
+    if (workspace_bytes < scan_workspace_bytes(m + 1)) {
         set_error("hp_query_count: workspace too small");
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
     if (m > 0) {
-        const int64_t groups = (m + kGroupMax - 1) / kGroupMax;
-        const unsigned grid = unsigned(groups < 148 * 8 ? groups : 148 * 8);
-        k_query_count<<<grid, kThreads, 0, s>>>(layout, padded_w, int(pad), R, m, offsets, probes, scanned);
+        static bool attr = false;
+        if (!attr) {
+            HP_TRY(set_smem(k_query_count, sizeof(CountSmem)));
+            attr = true;
+        }
+        k_query_count<<<group_grid(m, 6), kThreads, sizeof(CountSmem), s>>>(layout, padded_w, int(pad), R, m,
+                                                                            offsets, probes, scanned);
         HP_CHECK_LAUNCH("k_query_count");
     }
-    HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
+    HP_TRY(exclusive_scan_i64(offsets, offsets, m, workspace, s));
     return HP_OK;
 }
 
@@ -531,28 +510,28 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
                              hp_stream_t stream) {
     HP_TRY(check_common(layout, pad, m));
     (void)padded_h;
+    (void)workspace;
+    (void)workspace_bytes;
     if (m == 0 || total == 0) return HP_OK;
-    Carver c(workspace, workspace_bytes);
-    QueryWs w = carve_query(c, m);
-    if (!c.ok()) {
-        set_error("hp_query_fill: workspace too small");
-        return HP_ESPACE;
-    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
-    if (cudaMemsetAsync(w.ngroups, 0, sizeof(int), s) != cudaSuccess ||
-        cudaMemsetAsync(w.work, 0, sizeof(int), s) != cudaSuccess)
-        return cuda_status(cudaGetLastError(), "hp_query_fill memset");
-    const int64_t chunks = (m + 31) / 32;
-    k_make_groups<<<grid_for(chunks * 32, 256), 256, 0, s>>>(offsets, m, w.groups, w.ngroups);
-    HP_CHECK_LAUNCH("k_make_groups");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_query_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FillSmem)));
+        HP_TRY(set_smem(k_query_fill, sizeof(FillSmem)));
+        HP_TRY(set_smem(k_query_sort<kSortSmall>, sizeof(SortSmem<kSortSmall>)));
+        HP_TRY(set_smem(k_query_sort<kSortLarge>, sizeof(SortSmem<kSortLarge>)));
         attr = true;
     }
-    k_query_fill<<<148 * 2, kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, offsets, w.groups,
-                                                              w.ngroups, w.work, ids, t_proj, dist_perp);
+    k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, m, offsets,
+                                                                      ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_fill");
+    const unsigned g = unsigned(m < int64_t(kNumSMs) * 8 ? m : int64_t(kNumSMs) * 8);
+    k_query_sort<kSortSmall><<<g, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(offsets, m, 0, ids, t_proj, dist_perp);
+    HP_CHECK_LAUNCH("k_query_sort<small>");
+    k_query_sort<kSortLarge><<<kNumSMs, kThreads, sizeof(SortSmem<kSortLarge>), s>>>(offsets, m, kSortSmall, ids,
+                                                                                     t_proj, dist_perp);
+    HP_CHECK_LAUNCH("k_query_sort<large>");
+    k_query_sort<0><<<kNumSMs, kThreads, 0, s>>>(offsets, m, kSortLarge, ids, t_proj, dist_perp);
+    HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
 }

@@ -41,6 +41,10 @@ constexpr int kThreads = 128;
 constexpr int kSmemCap = 2048;  // candidates staged in shared memory per ray
 constexpr int kRetCap = 64;     // retained candidates buffered per ray
 
+// Path counters (rays, fast rays, proved-zero rays, exact evals, candidates,
+// bound evals); read with hp_sample_debug_counters().
+__device__ unsigned long long g_dbg[8];
+
 struct Params {
     int K;
     int eps_mode, want_color, exact_t_end;
@@ -55,6 +59,7 @@ struct Csr {
     const double* slopes;
     const double* colors;
     int64_t m;
+    int64_t max_q;  // longest segment (sizes the per-CTA scratch of long rays)
 };
 
 struct Stage {  // retained candidates between hp_sample_run and hp_sample_emit
@@ -174,7 +179,9 @@ struct RaySmem {
     int nret;
     int stop;
     int jstar;
-    double T;
+    int je, jz;
+    double T, U, dsk, exit_T;
+    int64_t stage_at;
 };
 
 // Per-candidate evaluation: udf, alpha (and colour) of candidate j.
@@ -330,8 +337,99 @@ __device__ void build_blocks(const double* __restrict__ DS, double* __restrict__
     }
 }
 
+// Upper bound of the reference's factor fl(1 - alpha_j) for candidate j
+// (DESIGN.md "sampler: transmittance bound").  Any ksel members of j's pool
+// give a mean distance >= the K-nearest mean, so the udf bound is the mean
+// over the ksel pool members nearest to j in t order, inflated by 1e-12 (which
+// dominates every fp64 rounding of the two sums); alpha is then bounded
+// below with a further 1e-12 margin (covers exp() ulp differences).  All
+// operations used afterwards are monotone, so the chain U_{j+1} = U_j * u_j
+// evaluated in the reference's order dominates its transmittance T_j.
+__device__ double bound_factor(const double* __restrict__ T, const double* __restrict__ DS, int q, int j,
+                               int jstar, double slope, const Params& P) {
+    const double tj = T[j];
+    const double rj = dmul(slope, tj);
+    const bool use_el = j >= jstar;
+    const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
+    double sum = 0.0;
+    int found = 0;
+    int l = j, r = j + 1;
+    while (found < ksel) {
+        int i;
+        if (l < 0) {
+            i = r++;
+        } else if (r >= q) {
+            i = l--;
+        } else if (dsub(tj, T[l]) <= dsub(T[r], tj)) {
+            i = l--;
+        } else {
+            i = r++;
+        }
+        const double di = DS[i];
+        if (use_el && di > rj) continue;
+        const double dt = dsub(T[i], tj);
+        sum = dadd(sum, sqrt(dadd(dmul(dt, dt), dmul(di, di))));
+        found++;
+    }
+    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
+    const double a_lo = dmul(dmul(P.gamma, exp(__ddiv_rn(-dmul(udf_up, udf_up), P.beta2))), 1.0 - 1e-12);
+    return dsub(1.0, a_lo);
+}
+
+// K-th smallest ds over the ray (ds >= 0), from the (ds, i)-sorted 32-blocks:
+// warp 0 pops the smallest block head K times.  Returns +inf if q < K.
+__device__ double kth_smallest_ds(const double* __restrict__ BDS, int q, int K) {
+    if (q < K) return CUDART_INF;
+    const int nblk = (q + 31) >> 5;
+    // each lane owns blocks lane, lane+32, ... ; head pointer per block kept in
+    // registers for up to 4 blocks per lane (q <= 4096), else generic loop
+    int head[4] = {0, 0, 0, 0};
+    double v = 0.0;
+    const int lane = lane_id();
+    for (int k = 0; k < K; k++) {
+        double best = CUDART_INF;
+        int bb = -1;
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            const int b = lane + 32 * s;
+            if (b < nblk) {
+                const int e = (b << 5) + head[s];
+                const int e_end = min((b << 5) + 32, q);
+                if (e < e_end && BDS[e] < best) {
+                    best = BDS[e];
+                    bb = s;
+                }
+            }
+        }
+        // warp argmin (value, lane)
+        double mv = best;
+        int ml = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, mv, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, ml, o);
+            if (ov < mv || (ov == mv && ol < ml)) {
+                mv = ov;
+                ml = ol;
+            }
+        }
+        if (lane == ml && bb >= 0) head[bb]++;
+        v = mv;
+    }
+    return v;
+}
+
 // One ray, block-wide.  mode 0: stage retained candidates; mode 1: write them
 // directly to the outputs at r_off[ray].
+//
+// Fast path (t sorted, ds >= 0, slope >= 0):
+//   1. bound chain U over candidates (cheap factors) -> Je = first j with
+//      U_j < thr (retention is decided before Je) and whether U reaches 0
+//      (then the exact transmittance is exactly 0).
+//   2. exact udf/alpha (block K-nearest search) for j < Je -- or for all j
+//      when the exact t_end is requested and U never reached 0 -- with the
+//      reference's sequential compositing and retention.
+// Slow path: exact evaluation of every candidate with the reference loops.
 template <class BestT>
 __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ray, int mode,
                            double* __restrict__ gscratch_ds, int* __restrict__ gscratch_idx,
@@ -368,16 +466,10 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
     } else {
         T = C.t + lo;
         DS = C.ds + lo;
-        BDS = gscratch_ds + lo;
-        BIDX = gscratch_idx + lo;
+        BDS = gscratch_ds + int64_t(blockIdx.x) * C.max_q;
+        BIDX = gscratch_idx + int64_t(blockIdx.x) * C.max_q;
     }
-    if (tid == 0) {
-        S.flag = (slope >= 0.0 && slope <= DBL_MAX) ? 1 : 0;
-        S.nret = 0;
-        S.stop = 0;
-        S.T = 1.0;
-    }
-    __syncthreads();
+    __syncthreads();  // staged t/ds visible to the whole block
     // fast-path preconditions: t finite and non-decreasing, ds finite and >= 0
     bool ok = true;
     for (int k = tid; k < q; k += kThreads) {
@@ -385,18 +477,32 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
         ok &= (fabs(tk) <= DBL_MAX) && (dk >= 0.0) && (dk <= DBL_MAX);
         if (k + 1 < q) ok &= !(T[k + 1] < tk);
     }
-    if (!__syncthreads_and(ok)) {
-        if (tid == 0) S.flag = 0;
-    }
-    __syncthreads();
-    const bool fast = S.flag != 0;
+    const bool fast = __syncthreads_and(ok) && slope >= 0.0 && slope <= DBL_MAX;
+    const double thr = P.eps_mode ? P.eps : P.tau_min;
     if (fast) {
         build_blocks(DS, BDS, BIDX, q);
-        // jstar: first j with #{ds_i <= slope*t_j} >= K (q if none)
-        if (q >= P.K) {
-            int lo_j = 0, hi_j = q;  // answer in [lo_j, hi_j]
-            while (lo_j < hi_j) {
-                const int mid = (lo_j + hi_j) >> 1;
+        __syncthreads();
+        if (P.K <= 32 && q <= 4096) {
+            if (warp_id() == 0) {
+                const double dsk = kth_smallest_ds(BDS, q, P.K);
+                if (lane_id() == 0) S.dsk = dsk;
+            }
+            __syncthreads();
+            // jstar = first j with slope * t_j >= ds_(K)   (r_j is monotone)
+            if (tid == 0) {
+                int a = 0, b = q;
+                const double dsk = S.dsk;
+                while (a < b) {
+                    const int mid = (a + b) >> 1;
+                    if (dmul(slope, T[mid]) >= dsk) b = mid; else a = mid + 1;
+                }
+                S.jstar = (dsk <= DBL_MAX) ? a : q;
+            }
+        } else {
+            // generic: binary search on j with block-wide counts
+            int a = 0, b = q;
+            while (a < b) {
+                const int mid = (a + b) >> 1;
                 const double rj = dmul(slope, T[mid]);
                 int c = 0;
                 for (int k = tid; k < q; k += kThreads) c += (DS[k] <= rj);
@@ -407,24 +513,74 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
 #pragma unroll
                 for (int w = 0; w < kThreads / 32; w++) tot += S.red[w];
                 __syncthreads();
-                if (tot >= P.K)
-                    hi_j = mid;
-                else
-                    lo_j = mid + 1;
+                if (tot >= P.K) b = mid; else a = mid + 1;
             }
-            if (tid == 0) S.jstar = lo_j;
-        } else if (tid == 0) {
-            S.jstar = q;
+            if (tid == 0) S.jstar = a;
         }
+        if (tid == 0) {
+            S.U = 1.0;
+            S.je = q;
+            S.jz = 0;  // 1 when the bound chain reached exactly 0
+        }
+        __syncthreads();
+        // ---- 1. bound chain
+        const int jstar = S.jstar;
+        for (int c0 = 0; c0 < q; c0 += kThreads) {
+            const int j = c0 + tid;
+            if (j < q) S.ca[tid] = bound_factor(T, DS, q, j, jstar, slope, P);
+            __syncthreads();
+            if (tid == 0) {
+                double U = S.U;
+                int je = S.je, jz = 0;
+                const int c1 = min(c0 + kThreads, q);
+                for (int jj = c0; jj < c1; jj++) {
+                    if (je == q && U < thr) je = jj;
+                    U = dmul(U, S.ca[jj - c0]);
+                    if (U == 0.0) {
+                        jz = 1;
+                        if (je == q && thr > 0.0) je = jj + 1;  // U_{jj+1} = 0 < thr
+                        break;
+                    }
+                }
+                S.U = U;
+                S.je = je;
+                S.jz = jz;
+                S.stop = jz || (!P.exact_t_end && je < q);
+            }
+            __syncthreads();
+            if (S.stop) break;
+        }
+    } else if (tid == 0) {
+        S.je = q;
+        S.jz = 0;
     }
     __syncthreads();
+    // exact region: [0, E)
+    const int je = S.je;
+    const bool proved_zero = fast && S.jz;
+    const int E = (P.exact_t_end && !proved_zero) ? q : je;
     const int jstar = fast ? S.jstar : 0;
+    if (tid == 0 && mode == 0) {
+        atomicAdd(&g_dbg[0], 1ull);
+        atomicAdd(&g_dbg[1], fast ? 1ull : 0ull);
+        atomicAdd(&g_dbg[2], proved_zero ? 1ull : 0ull);
+        atomicAdd(&g_dbg[3], (unsigned long long)E);
+        atomicAdd(&g_dbg[4], (unsigned long long)q);
+        atomicAdd(&g_dbg[5], (unsigned long long)(fast ? S.jstar : -1));
+    }
+    if (tid == 0) {
+        S.nret = 0;
+        S.T = 1.0;
+        S.stop = 0;
+        S.exit_T = -1.0;
+    }
+    __syncthreads();
     const int64_t* ids_ray = C.ids + lo;
     int64_t out_base = 0;
     if (mode == 1) out_base = r_off[ray];
-    for (int c0 = 0; c0 < q; c0 += kThreads) {
+    for (int c0 = 0; c0 < E; c0 += kThreads) {
         const int j = c0 + tid;
-        if (j < q) {
+        if (j < E) {
             double u, a;
             eval_candidate<BestT>(T, DS, BDS, BIDX, q, j, fast, jstar, slope, P, ids_ray, C.colors, u, a,
                                   &S.ccol[3 * tid]);
@@ -436,10 +592,15 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
             // sequential front-to-back compositing (_kernels.py:661-697)
             double Tr = S.T;
             int nret = S.nret;
-            const int c1 = c0 + kThreads < q ? c0 + kThreads : q;
+            const int c1 = min(c0 + kThreads, E);
             int stop = 0;
             for (int jj = c0; jj < c1; jj++) {
                 const int k = jj - c0;
+                if (!P.exact_t_end && Tr < thr) {  // exit mode: retention decided
+                    S.exit_T = Tr;
+                    stop = 1;
+                    break;
+                }
                 const double a = S.ca[k];
                 const double w = dmul(a, Tr);
                 const bool keep = P.eps_mode ? (w >= P.eps) : !(Tr < P.tau_min);
@@ -471,13 +632,6 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
                     nret++;
                 }
                 Tr = dmul(Tr, dsub(1.0, a));
-                // Tr is non-increasing (alpha in [0, gamma], gamma <= 1).
-                const bool ret_done = P.eps_mode ? (Tr < P.eps) : (Tr < P.tau_min);
-                const bool tend_done = P.exact_t_end ? (Tr == 0.0) : true;
-                if (ret_done && tend_done) {
-                    stop = 1;
-                    break;
-                }
             }
             S.T = Tr;
             S.nret = nret;
@@ -490,7 +644,12 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
         if (tid == 0) {
             const int nret = S.nret;
             rcount[ray] = nret;
-            t_end[ray] = S.T;
+            double te;
+            if (P.exact_t_end)
+                te = proved_zero ? 0.0 : S.T;
+            else
+                te = S.exit_T >= 0.0 ? S.exit_T : S.T;
+            t_end[ray] = te;
             int64_t st = -1;
             if (nret > 0 && nret <= kRetCap) {
                 st = atomicAdd(reinterpret_cast<unsigned long long*>(stage_cursor), (unsigned long long)nret);
@@ -501,11 +660,11 @@ __device__ void sample_ray(RaySmem& S, const Csr& C, const Params& P, int64_t ra
             ray_stage[ray] = st;
             if (st < 0) ovf_list[atomicAdd(ovf_n, 1)] = int(ray);
             S.flag = int(st >= 0 && nret > 0);
-            S.jstar = int(st >= 0 ? st : 0);
+            S.stage_at = st >= 0 ? st : 0;
         }
         __syncthreads();
         if (S.flag) {
-            const int64_t st = S.jstar;
+            const int64_t st = S.stage_at;
             for (int k = tid; k < S.nret; k += kThreads) {
                 ST.j[st + k] = S.rj[k];
                 ST.udf[st + k] = S.rudf[k];
@@ -586,7 +745,11 @@ struct SampleWs {
     void* scan;
 };
 
-SampleWs carve_sample(Carver& c, int64_t m, int64_t total, int64_t cap, bool color, bool big) {
+constexpr int kSampleGrid = 148 * 2;
+
+SampleWs carve_sample(Carver& c, int64_t m, int64_t total, int64_t cap, bool color, int64_t max_q) {
+    const bool big = max_q > kSmemCap;
+    (void)total;
     SampleWs w;
     w.rcount = nullptr;
     w.ray_stage = c.take<int64_t>(m > 0 ? m : 1);
@@ -599,13 +762,11 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t total, int64_t cap, bool col
     w.st.alpha = c.take<double>(cap > 0 ? cap : 1);
     w.st.w = c.take<double>(cap > 0 ? cap : 1);
     w.st.col = color ? c.take<double>(3 * (cap > 0 ? cap : 1)) : nullptr;
-    w.gds = big ? c.take<double>(total > 0 ? total : 1) : nullptr;
-    w.gidx = big ? c.take<int>(total > 0 ? total : 1) : nullptr;
+    w.gds = big ? c.take<double>(kSampleGrid * max_q) : nullptr;
+    w.gidx = big ? c.take<int>(kSampleGrid * max_q) : nullptr;
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     return w;
 }
-
-bool needs_big(int64_t max_q) { return max_q > kSmemCap; }
 
 __global__ void k_csr_stats(const int64_t* __restrict__ off, int64_t m, int64_t* __restrict__ out2) {
     int64_t mx = 0;
@@ -643,7 +804,7 @@ int launch_sample(const Csr& C, const Params& P, int mode, const int* list, cons
         cudaFuncSetAttribute(k_sample<BestT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RaySmem)));
         attr = true;
     }
-    k_sample<BestT><<<148 * 2, kThreads, sizeof(RaySmem), s>>>(C, P, mode, list, list_n, w.gds, w.gidx, rcount,
+    k_sample<BestT><<<kSampleGrid, kThreads, sizeof(RaySmem), s>>>(C, P, mode, list, list_n, w.gds, w.gidx, rcount,
                                                                t_end, w.ray_stage, w.stage_cursor, w.st,
                                                                w.ovf_list, w.ovf_n, r_off, O);
     HP_CHECK_LAUNCH("k_sample");
@@ -657,12 +818,12 @@ int dispatch_sample(const Csr& C, const Params& P, int mode, const int* list, co
     return launch_sample<BestDyn>(C, P, mode, list, list_n, w, rcount, t_end, r_off, O, s);
 }
 
-int validate(const hp_sampler_params* p, const double* colors) {
+int validate(const hp_sampler_params* p, const double* colors, int64_t n_colors) {
     if (!p || p->k_neighbors < 1 || p->k_neighbors > HP_MAX_K) {
         set_error("k_neighbors must be in [1, %d] on the device path", HP_MAX_K);
         return HP_EINVAL;
     }
-    if (p->want_color && !colors) {
+    if (p->want_color && !colors && n_colors > 0) {
         set_error("want_color set but colors is NULL");
         return HP_EINVAL;
     }
@@ -680,7 +841,7 @@ extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t max_q
     Carver c(nullptr, 0);
     // the global scratch for long rays is sized by `total` and only exists
     // when some ray has more than kSmemCap candidates
-    carve_sample(c, m, total, stage_capacity, p && p->want_color, needs_big(max_q));
+    carve_sample(c, m, total, stage_capacity, p && p->want_color, max_q);
     *bytes = c.used + 256;
     return HP_OK;
 }
@@ -690,10 +851,9 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
                              const hp_sampler_params* p, const double* colors, int64_t n_colors,
                              int64_t stage_capacity, int64_t* r_off, double* t_end, void* workspace,
                              size_t workspace_bytes, hp_stream_t stream) {
-    HP_TRY(validate(p, colors));
-    (void)n_colors;
+    HP_TRY(validate(p, colors, n_colors));
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, total, stage_capacity, p->want_color, needs_big(max_q));
+    SampleWs w = carve_sample(c, m, total, stage_capacity, p->want_color, max_q);
     if (!c.ok()) {
         set_error("hp_sample_run: workspace too small");
         return HP_ESPACE;
@@ -702,7 +862,7 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
     if (cudaMemsetAsync(w.stage_cursor, 0, sizeof(int64_t), s) != cudaSuccess ||
         cudaMemsetAsync(w.ovf_n, 0, sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_sample_run memset");
-    Csr C{offsets, ids, t, dist, slopes, colors, m};
+    Csr C{offsets, ids, t, dist, slopes, colors, m, max_q};
     Params P = to_params(p);
     Outputs O{};
     if (m > 0) HP_TRY(dispatch_sample(C, P, 0, nullptr, nullptr, w, r_off, t_end, nullptr, O, s));
@@ -716,17 +876,16 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
                               int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id, double* r_t,
                               double* r_dist, double* r_udf, double* r_alpha, double* r_w, double* r_color,
                               void* workspace, size_t workspace_bytes, hp_stream_t stream) {
-    HP_TRY(validate(p, colors));
-    (void)n_colors;
+    HP_TRY(validate(p, colors, n_colors));
     if (R == 0 || m == 0) return HP_OK;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, total, stage_capacity, p->want_color, needs_big(max_q));
+    SampleWs w = carve_sample(c, m, total, stage_capacity, p->want_color, max_q);
     if (!c.ok()) {
         set_error("hp_sample_emit: workspace too small");
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Csr C{offsets, ids, t, dist, slopes, colors, m};
+    Csr C{offsets, ids, t, dist, slopes, colors, m, max_q};
     Params P = to_params(p);
     Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
     k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.ray_stage, w.st, O);
@@ -751,5 +910,16 @@ extern "C" int hp_csr_stats(const int64_t* offsets, int64_t m, int64_t* out2, hp
         return cuda_status(cudaGetLastError(), "hp_csr_stats memset");
     k_csr_stats<<<grid_for(m > 0 ? m : 1, 256, 148 * 4), 256, 0, s>>>(offsets, m, out2);
     HP_CHECK_LAUNCH("k_csr_stats");
+    return HP_OK;
+}
+
+extern "C" int hp_sample_debug_counters(int64_t* out8, int reset) {
+    unsigned long long h[8];
+    if (cudaMemcpyFromSymbol(h, g_dbg, sizeof(h)) != cudaSuccess) return cuda_status(cudaGetLastError(), "dbg");
+    for (int k = 0; k < 8; k++) out8[k] = int64_t(h[k]);
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+    }
     return HP_OK;
 }

@@ -83,15 +83,11 @@ class DeviceIndex:
     rel_y: torch.Tensor
     rel_z: torch.Tensor
     point_id: torch.Tensor      # int32
+    relf: torch.Tensor          # float32 [N_in, 4]: filter copy (x, y, z, error budget)
 
     def layout(self) -> _lib.Layout:
-        L = _lib.Layout()
-        L.row_ptr = _ptr(self.row_ptr)
-        L.rel_x = _ptr(self.rel_x)
-        L.rel_y = _ptr(self.rel_y)
-        L.rel_z = _ptr(self.rel_z)
-        L.point_id = _ptr(self.point_id)
-        return L
+        return _lib.Layout(_ptr(self.row_ptr), _ptr(self.rel_x), _ptr(self.rel_y),
+                           _ptr(self.rel_z), _ptr(self.point_id), _ptr(self.relf))
 
 
 def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
@@ -117,9 +113,10 @@ def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
     row_ptr = torch.empty(P + 1, dtype=torch.int32, device=dev)
     rx, ry, rz = (torch.empty(cap, **f64) for _ in range(3))
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    rf = torch.empty((cap, 4), dtype=torch.float32, device=dev)
     n_in_d = torch.zeros(1, **i64)
     _mark("build.setup")
-    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid))
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf))
     cam = camera_struct(camera)
     _lib.check(lib.hp_build(_ptr(xyz), n, ctypes.byref(cam), pad, _ptr(ts), _ptr(tc), _ptr(rid),
                             _ptr(sx), _ptr(sy), _ptr(sz), L, _ptr(n_in_d), _ptr(ws), nb.value,
@@ -128,7 +125,7 @@ def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
     n_in = int(n_in_d.item()) if n > 0 else 0
     return DeviceIndex(camera, pad, wp, hp, n_in, ts, tc, rid[:n_in], sx[:n_in], sy[:n_in],
                        sz[:n_in], row_ptr, rx[:max(n_in, 1)], ry[:max(n_in, 1)],
-                       rz[:max(n_in, 1)], pid[:max(n_in, 1)])
+                       rz[:max(n_in, 1)], pid[:max(n_in, 1)], rf[:max(n_in, 1)])
 
 
 def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered_ids, camera,
@@ -144,16 +141,17 @@ def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered
     row_ptr = torch.empty(P + 1, dtype=torch.int32, device=dev)
     rx, ry, rz = (torch.empty(cap, dtype=torch.float64, device=dev) for _ in range(3))
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    rf = torch.empty((cap, 4), dtype=torch.float32, device=dev)
     nb = c_size(0)
     _lib.check(lib.hp_layout_workspace_bytes(n_in, wp, hp, ctypes.byref(nb)))
     ws = _workspace(nb.value, dev)
     origin = (ctypes.c_double * 3)(*[float(v) for v in np.asarray(camera.origin)])
-    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid))
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf))
     _lib.check(lib.hp_layout_from_table(_ptr(table_start), _ptr(table_count), _ptr(slot_x),
                                         _ptr(slot_y), _ptr(slot_z), _ptr(reordered_ids), n_in, wp,
                                         hp, origin, L, _ptr(ws), nb.value, _stream()))
     return DeviceIndex(camera, pad, wp, hp, n_in, table_start, table_count, reordered_ids, slot_x,
-                       slot_y, slot_z, row_ptr, rx, ry, rz, pid)
+                       slot_y, slot_z, row_ptr, rx, ry, rz, pid, rf)
 
 
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
