@@ -163,6 +163,13 @@ int hp_primary_surface(const int64_t* r_off, int64_t m, const int64_t* r_id, con
  *  exactly evaluated candidates, candidates, sum of jstar, -, -]. */
 int hp_sample_debug_counters(int64_t* out8, int reset);
 
+/* Per-kernel CUDA-event timing on the launching stream (diagnostics and the
+ * benchmark's roofline): enable, run, then collect per-name summed ms and
+ * launch counts (names newline-separated); collect synchronises and clears. */
+int hp_timing_enable(int on);
+int hp_timing_collect(char* names, int names_len, double* ms, int64_t* counts, int max_entries,
+                      int* n_entries);
+
 /* Kernel launches issued by this library since load (for bench gpu_launches). */
 int64_t hp_launch_count(void);
 

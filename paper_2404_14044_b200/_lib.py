@@ -65,6 +65,9 @@ _SIGNATURES = {
     "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "hp_sample_debug_counters": (ctypes.c_int, [c_p, ctypes.c_int]),
+    "hp_timing_enable": (ctypes.c_int, [ctypes.c_int]),
+    "hp_timing_collect": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, c_p, c_p, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_int)]),
 }
 
 EXPORTS = tuple(_SIGNATURES)
@@ -105,3 +108,21 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(load().hp_launch_count())
+
+
+def timing_enable(on: bool) -> None:
+    check(load().hp_timing_enable(1 if on else 0))
+
+
+def timing_collect() -> dict:
+    """{kernel name: (summed ms, launches)} since the last collect (syncs)."""
+    import numpy as np
+    L = load()
+    names = ctypes.create_string_buffer(4096)
+    ms = np.zeros(64)
+    cnt = np.zeros(64, np.int64)
+    n = ctypes.c_int(0)
+    check(L.hp_timing_collect(names, 4096, ms.ctypes.data_as(c_p), cnt.ctypes.data_as(c_p), 64,
+                              ctypes.byref(n)))
+    keys = names.value.decode().split("\n")[: n.value]
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}

@@ -327,6 +327,7 @@ extern "C" int hp_build(const double* positions, int64_t n, const hp_camera* cam
     cd.half_w = 0.5 * double(cam->width);
     cd.half_h = 0.5 * double(cam->height);
 
+    TimedSpan ts("hp_build", s);
     if (cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * P, s) != cudaSuccess ||
         cudaMemsetAsync(w.big_n, 0, sizeof(int32_t), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_build memset");

@@ -3,6 +3,10 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "hp_common.cuh"
 
@@ -24,6 +28,46 @@ int cuda_status(cudaError_t e, const char* where) {
 }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------ timing
+namespace {
+struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_pool;
+std::vector<Pending> g_open;  // begun, not ended (per nesting level)
+cudaEvent_t take_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+void timing_begin(const char* name, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing) return;
+    Pending p{name, take_event(), take_event()};
+    cudaEventRecord(p.a, s);
+    g_open.push_back(p);
+}
+
+void timing_end(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing || g_open.empty()) return;
+    Pending p = g_open.back();
+    g_open.pop_back();
+    cudaEventRecord(p.b, s);
+    g_pending.push_back(p);
+}
 
 // ------------------------------------------------------------------ scan
 constexpr int kScanThreads = 512;
@@ -116,6 +160,53 @@ int exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, void* 
 }
 
 }  // namespace hp
+
+extern "C" int hp_timing_enable(int on) {
+    std::lock_guard<std::mutex> lk(hp::g_tmu);
+    hp::g_timing = on != 0;
+    return HP_OK;
+}
+
+// Synchronises on the recorded events and returns, per kernel name, the summed
+// milliseconds and launch counts ("name1\nname2\n..." in names).  Clears.
+extern "C" int hp_timing_collect(char* names, int names_len, double* ms, int64_t* counts, int max_entries,
+                                 int* n_entries) {
+    std::lock_guard<std::mutex> lk(hp::g_tmu);
+    std::vector<std::string> keys;
+    std::vector<double> sums;
+    std::vector<int64_t> cnts;
+    for (auto& p : hp::g_pending) {
+        cudaEventSynchronize(p.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, p.a, p.b);
+        size_t k = 0;
+        while (k < keys.size() && keys[k] != p.name) k++;
+        if (k == keys.size()) {
+            keys.push_back(p.name);
+            sums.push_back(0.0);
+            cnts.push_back(0);
+        }
+        sums[k] += t;
+        cnts[k] += 1;
+        hp::g_pool.push_back(p.a);
+        hp::g_pool.push_back(p.b);
+    }
+    hp::g_pending.clear();
+    std::string joined;
+    int n = 0;
+    for (size_t k = 0; k < keys.size() && n < max_entries; k++, n++) {
+        ms[n] = sums[k];
+        counts[n] = cnts[k];
+        joined += keys[k];
+        joined += "\n";
+    }
+    if (names && names_len > 0) {
+        strncpy(names, joined.c_str(), size_t(names_len - 1));
+        names[names_len - 1] = 0;
+    }
+    *n_entries = n;
+    return HP_OK;
+}
 
 extern "C" const char* hp_last_error(void) { return hp::g_err; }
 extern "C" int hp_version(void) { return 1; }

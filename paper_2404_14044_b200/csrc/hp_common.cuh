@@ -16,6 +16,16 @@ void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 
+// Optional per-kernel CUDA-event timing (hp_timing_enable): spans recorded on
+// the launching stream around the named launches, summed per name.
+void timing_begin(const char* name, cudaStream_t s);
+void timing_end(cudaStream_t s);
+struct TimedSpan {
+    cudaStream_t s;
+    TimedSpan(const char* name, cudaStream_t st) : s(st) { timing_begin(name, st); }
+    ~TimedSpan() { timing_end(s); }
+};
+
 #define HP_CHECK_LAUNCH(where)                                                 \
     do {                                                                       \
         ::hp::count_launch();                                                  \

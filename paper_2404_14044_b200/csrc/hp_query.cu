@@ -41,8 +41,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGroupMax = 32;  // rays per group
-constexpr int kStageCount = 2048;
-constexpr int kStageFill = 512;
+constexpr int kStageCount = 512;
+constexpr int kStageFill = 384;
 
 struct Rays {
     const int64_t* pix;
@@ -67,12 +67,33 @@ __device__ __forceinline__ RayParams load_ray(const Rays& R, int64_t r) {
     return p;
 }
 
+constexpr int kRowsMax = 48;  // kernel rows tabulated per batch
+
 struct GroupHead {
     RayParams ray[kGroupMax];
-    int lo[kGroupMax], hi[kGroupMax];  // the ray's slot sub-range in the current row
-    int stage_lo[2], stage_hi[2];  // by row parity (no end-of-row barrier needed)
+    int rlo[kRowsMax][kGroupMax], rhi[kRowsMax][kGroupMax];  // ray sub-range per row
+    int slo[kRowsMax], shi[kRowsMax];                          // staged (union) range per row
     int u0, u1, v0, v1;
 };
+
+// cp.async (LDGSTS) helpers: asynchronous global -> shared copies.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = unsigned(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = unsigned(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = unsigned(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
 // Group bounding box (padded coordinates) of rays [r0, r0+G).
 __device__ void group_setup(GroupHead& S, const Rays& R, int64_t r0, int G, int s) {
@@ -104,45 +125,80 @@ __device__ void group_setup(GroupHead& S, const Rays& R, int64_t r0, int G, int 
     __syncthreads();
 }
 
-// Streams the kernel rows of a group.  For each staged chunk of a row,
-// stage(c0, c1) loads slots [c0, c1) into shared memory, then every warp
-// calls test(g, k, c0) for the rays g it owns (warp w owns rays w, w+8, ...)
-// over their sub-range, 32 slots at a time (lanes beyond the range get
-// k = -1).  row_done() runs once per row after the ranges are known.
-template <int kStage, class Stage, class Test, class RowDone>
-__device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, Stage stage,
-                             Test test, RowDone row_done) {
+// Streams the kernel rows of a group through two shared-memory stages.
+// Rows are processed in batches of kRowsMax: the batch's per-(row, ray) slot
+// sub-ranges are tabulated first (one parallel round of row_ptr loads, each
+// ray's total added to `scanned` via tab(g, hi - lo)), then the batch's
+// chunks (row, [c0, c1)) are staged with cp.async into alternating buffers:
+// chunk i+1 is in flight while chunk i is tested.  issue(buf, c0, c1) issues
+// the copies of slots [c0, c1); test(buf, row, g, k, c0) runs on the warp
+// owning ray g (warp w owns rays w, w+8, ...), 32 slots at a time, with
+// k = -1 for lanes beyond the ray's sub-range.
+template <int kStage, class Issue, class Test, class Tab>
+__device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, Issue issue,
+                             Test test, Tab tab) {
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-    for (int y = S.v0; y < S.v1; y++) {
-        const int64_t rowbase = int64_t(y) * wp;
-        if (tid < G) {
-            const RayParams& r = S.ray[tid];
+    for (int yb = S.v0; yb < S.v1; yb += kRowsMax) {
+        const int nrows = min(kRowsMax, S.v1 - yb);
+        for (int idx = tid; idx < nrows * G; idx += kThreads) {
+            const int row = idx / G, g = idx - row * G;
+            const int y = yb + row;
+            const RayParams& r = S.ray[g];
+            int lo = 0, hi = 0;
             if (y >= r.v && y < r.v + s) {
-                S.lo[tid] = L.row_ptr[rowbase + r.u];
-                S.hi[tid] = L.row_ptr[rowbase + r.u + s];
-            } else {
-                S.lo[tid] = S.hi[tid] = 0;
+                const int64_t base = int64_t(y) * wp + r.u;
+                lo = L.row_ptr[base];
+                hi = L.row_ptr[base + s];
+                tab(g, hi - lo);
             }
+            S.rlo[row][g] = lo;
+            S.rhi[row][g] = hi;
         }
-        if (tid == 0) {
-            S.stage_lo[y & 1] = L.row_ptr[rowbase + S.u0];
-            S.stage_hi[y & 1] = L.row_ptr[rowbase + S.u1];
+        for (int row = tid; row < nrows; row += kThreads) {
+            const int64_t base = int64_t(yb + row) * wp;
+            S.slo[row] = L.row_ptr[base + S.u0];
+            S.shi[row] = L.row_ptr[base + S.u1];
         }
         __syncthreads();
-        row_done();
-        const int A = S.stage_lo[y & 1], B = S.stage_hi[y & 1];
-        for (int c0 = A; c0 < B; c0 += kStage) {
-            const int c1 = c0 + kStage < B ? c0 + kStage : B;
-            stage(c0, c1);
+        // chunk cursor (identical in every thread)
+        int row = 0, c0 = S.slo[0];
+        auto advance = [&](int& rw, int& cc) {
+            cc += kStage;
+            while (rw < nrows && cc >= S.shi[rw]) {
+                rw++;
+                if (rw < nrows) cc = S.slo[rw];
+            }
+        };
+        if (c0 >= S.shi[0]) {  // empty first row(s)
+            c0 -= kStage;
+            advance(row, c0);
+        }
+        int buf = 0;
+        if (row < nrows) issue(0, c0, min(c0 + kStage, S.shi[row]));
+        cp_commit();
+        while (row < nrows) {
+            int nrow = row, nc0 = c0;
+            advance(nrow, nc0);
+            if (nrow < nrows) {
+                issue(buf ^ 1, nc0, min(nc0 + kStage, S.shi[nrow]));
+                cp_commit();
+                cp_wait<1>();
+            } else {
+                cp_wait<0>();
+            }
             __syncthreads();
+            const int c1 = min(c0 + kStage, S.shi[row]);
             for (int g = warp; g < G; g += kWarps) {
-                const int lo = max(S.lo[g], c0), hi = min(S.hi[g], c1);
+                const int lo = max(S.rlo[row][g], c0), hi = min(S.rhi[row][g], c1);
                 for (int base = lo; base < hi; base += 32) {
                     const int k = base + lane;
-                    test(g, k < hi ? k : -1, c0);
+                    test(buf, g, k < hi ? k : -1, c0);
                 }
             }
             __syncthreads();
+            row = nrow;
+            c0 = nc0;
+            buf ^= 1;
         }
     }
 }
@@ -150,8 +206,8 @@ __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64
 // ---------------------------------------------------------------- pass 1
 struct CountSmem {
     GroupHead head;
-    float4 pf[kStageCount];
-    int64_t cnt[kGroupMax], scn[kGroupMax];
+    float4 pf[2][kStageCount];
+    int cnt[kGroupMax], scn[kGroupMax];
 };
 
 __global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int64_t wp, int pad, Rays R,
@@ -168,14 +224,14 @@ __global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int
         group_setup(S.head, R, r0, G, s);
         stream_group<kStageCount>(
             S.head, G, L, wp, s,
-            [&](int c0, int c1) {
-                for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) S.pf[k - c0] = relf[k];
+            [&](int buf, int c0, int c1) {
+                for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) cp_async16(&S.pf[buf][k - c0], relf + k);
             },
-            [&](int g, int k, int c0) {
+            [&](int buf, int g, int k, int c0) {
                 int cls = 0;
                 if (k >= 0) {
                     const RayParams& r = S.head.ray[g];
-                    cls = cone_filter(S.pf[k - c0], r);
+                    cls = cone_filter(S.pf[buf][k - c0], r);
                     if (cls == 2) {
                         double t, d2;
                         cls = cone_test(L.rel_x[k], L.rel_y[k], L.rel_z[k], r, t, d2) ? 1 : 0;
@@ -184,9 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int
                 const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
                 if (lane_id() == 0) S.cnt[g] += __popc(b);
             },
-            [&]() {
-                if (threadIdx.x < G) S.scn[threadIdx.x] += S.head.hi[threadIdx.x] - S.head.lo[threadIdx.x];
-            });
+            [&](int g, int n) { atomicAdd(&S.scn[g], n); });
         __syncthreads();
         if (threadIdx.x < G) {
             counts[r0 + threadIdx.x] = S.cnt[threadIdx.x];
@@ -200,9 +254,9 @@ __global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int
 // ---------------------------------------------------------------- pass 2
 struct FillSmem {
     GroupHead head;
-    float4 pf[kStageFill];
-    double px[kStageFill], py[kStageFill], pz[kStageFill];
-    int pid[kStageFill];
+    float4 pf[2][kStageFill];
+    double px[2][kStageFill], py[2][kStageFill], pz[2][kStageFill];
+    int pid[2][kStageFill];
     int fill[kGroupMax];
     int64_t off[kGroupMax];
 };
@@ -227,24 +281,25 @@ __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int6
         group_setup(S.head, R, r0, G, s);
         stream_group<kStageFill>(
             S.head, G, L, wp, s,
-            [&](int c0, int c1) {
+            [&](int buf, int c0, int c1) {
                 for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) {
-                    S.pf[k - c0] = relf[k];
-                    S.px[k - c0] = L.rel_x[k];
-                    S.py[k - c0] = L.rel_y[k];
-                    S.pz[k - c0] = L.rel_z[k];
-                    S.pid[k - c0] = L.point_id[k];
+                    const int i = k - c0;
+                    cp_async16(&S.pf[buf][i], relf + k);
+                    cp_async8(&S.px[buf][i], L.rel_x + k);
+                    cp_async8(&S.py[buf][i], L.rel_y + k);
+                    cp_async8(&S.pz[buf][i], L.rel_z + k);
+                    cp_async4(&S.pid[buf][i], L.point_id + k);
                 }
             },
-            [&](int g, int k, int c0) {
+            [&](int buf, int g, int k, int c0) {
                 int cls = 0;
                 double t = 0.0, d2 = 0.0;
                 if (k >= 0) {
                     const RayParams& r = S.head.ray[g];
                     const int i = k - c0;
-                    cls = cone_filter(S.pf[i], r);
+                    cls = cone_filter(S.pf[buf][i], r);
                     if (cls != 0) {
-                        const bool ok = cone_test(S.px[i], S.py[i], S.pz[i], r, t, d2);
+                        const bool ok = cone_test(S.px[buf][i], S.py[buf][i], S.pz[buf][i], r, t, d2);
                         if (cls == 2) cls = ok ? 1 : 0;
                     }
                 }
@@ -253,13 +308,13 @@ __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int6
                     const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
                     out_t[pos] = t;
                     out_d[pos] = sqrt(d2);
-                    out_id[pos] = S.pid[k - c0];
+                    out_id[pos] = S.pid[buf][k - c0];
                 }
                 __syncwarp();
                 if (lane_id() == 0) S.fill[g] += __popc(b);
                 __syncwarp();
             },
-            [&]() {});
+            [&](int, int) {});
         __syncthreads();
     }
 }
@@ -401,19 +456,45 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, int64_t* __restrict__ gid
     __syncthreads();
 }
 
-// Rays with lo_q < q <= kCap (kCap > 0), or q > lo_q with the in-place global
-// network (kCap == 0).
+constexpr int kSortSmall = 2048;
+constexpr int kSortLarge = 8192;
+
+// Size classes of rays to sort: [2, kSortSmall], (kSortSmall, kSortLarge], above.
+__global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
+                               int* __restrict__ counts) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        int cls = -1;
+        if (r < m) {
+            const int64_t q = off[r + 1] - off[r];
+            cls = q < 2 ? -1 : (q <= kSortSmall ? 0 : (q <= kSortLarge ? 1 : 2));
+        }
+#pragma unroll
+        for (int c = 0; c < 3; c++) {  // warp-aggregated append
+            const unsigned b = __ballot_sync(0xffffffffu, cls == c);
+            if (!b) continue;
+            int base = 0;
+            if (lane_id() == __ffs(b) - 1) base = atomicAdd(&counts[c], __popc(b));
+            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+            if (cls == c) lists[int64_t(c) * m + base + __popc(b & ((1u << lane_id()) - 1))] = int(r);
+        }
+    }
+}
+
+// Sort the rays of one size class (list of ray ids): in shared memory when
+// kCap > 0, with the in-place global sorting network when kCap == 0.
 template <int kCap>
-__global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restrict__ off, int64_t m, int lo_q,
+__global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restrict__ off, const int* __restrict__ list,
+                                                         const int* __restrict__ list_n,
                                                          int64_t* __restrict__ out_id, double* __restrict__ out_t,
                                                          double* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char dyn[];
-    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+    const int n = *list_n;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+        const int64_t r = list[k];
         const int64_t o = off[r];
         const int64_t q = off[r + 1] - o;
-        if (q <= lo_q || q < 2) continue;
         if constexpr (kCap > 0) {
-            if (q > kCap) continue;
             sort_segment<kCap>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), out_id + o, out_t + o, out_d + o);
         } else {
             double* tt = out_t + o;
@@ -436,9 +517,6 @@ __global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restri
         }
     }
 }
-
-constexpr int kSortSmall = 2048;
-constexpr int kSortLarge = 8192;
 
 template <class K>
 int set_smem(K kernel, size_t bytes) {
@@ -470,7 +548,8 @@ unsigned group_grid(int64_t m, int per_sm) {
 using namespace hp;
 
 extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, size_t* bytes) {
-    *bytes = scan_workspace_bytes(m + 1) + 256;
+    // scan scratch | 3 ray lists of the sort size classes | 3 counts
+    *bytes = scan_workspace_bytes(m + 1) + 256 + sizeof(int) * (3 * (m > 0 ? m : 1) + 64) + 256;
     (void)pad;
     return HP_OK;
 }
@@ -494,7 +573,8 @@ extern "C" int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t 
             HP_TRY(set_smem(k_query_count, sizeof(CountSmem)));
             attr = true;
         }
-        k_query_count<<<group_grid(m, 6), kThreads, sizeof(CountSmem), s>>>(layout, padded_w, int(pad), R, m,
+        TimedSpan ts("k_query_count", s);
+        k_query_count<<<group_grid(m, 7), kThreads, sizeof(CountSmem), s>>>(layout, padded_w, int(pad), R, m,
                                                                             offsets, probes, scanned);
         HP_CHECK_LAUNCH("k_query_count");
     }
@@ -510,9 +590,15 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
                              hp_stream_t stream) {
     HP_TRY(check_common(layout, pad, m));
     (void)padded_h;
-    (void)workspace;
-    (void)workspace_bytes;
     if (m == 0 || total == 0) return HP_OK;
+    Carver cv(workspace, workspace_bytes);
+    cv.take<char>(scan_workspace_bytes(m + 1));
+    int* lists = cv.take<int>(3 * m);
+    int* counts = cv.take<int>(64);
+    if (!cv.ok()) {
+        set_error("hp_query_fill: workspace too small");
+        return HP_ESPACE;
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
     static bool attr = false;
@@ -522,16 +608,24 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
         HP_TRY(set_smem(k_query_sort<kSortLarge>, sizeof(SortSmem<kSortLarge>)));
         attr = true;
     }
-    k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, m, offsets,
-                                                                      ids, t_proj, dist_perp);
-    HP_CHECK_LAUNCH("k_query_fill");
-    const unsigned g = unsigned(m < int64_t(kNumSMs) * 8 ? m : int64_t(kNumSMs) * 8);
-    k_query_sort<kSortSmall><<<g, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(offsets, m, 0, ids, t_proj, dist_perp);
+    {
+        TimedSpan ts("k_query_fill", s);
+        k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, m,
+                                                                          offsets, ids, t_proj, dist_perp);
+        HP_CHECK_LAUNCH("k_query_fill");
+    }
+    TimedSpan ts("k_query_sort", s);
+    if (cudaMemsetAsync(counts, 0, 3 * sizeof(int), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_query_fill memset");
+    k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, counts);
+    HP_CHECK_LAUNCH("k_sort_classes");
+    k_query_sort<kSortSmall><<<kNumSMs * 4, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(offsets, lists, counts,
+                                                                                         ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<small>");
-    k_query_sort<kSortLarge><<<kNumSMs, kThreads, sizeof(SortSmem<kSortLarge>), s>>>(offsets, m, kSortSmall, ids,
-                                                                                     t_proj, dist_perp);
+    k_query_sort<kSortLarge><<<kNumSMs, kThreads, sizeof(SortSmem<kSortLarge>), s>>>(offsets, lists + m, counts + 1,
+                                                                                     ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
-    k_query_sort<0><<<kNumSMs, kThreads, 0, s>>>(offsets, m, kSortLarge, ids, t_proj, dist_perp);
+    k_query_sort<0><<<kNumSMs, kThreads, 0, s>>>(offsets, lists + 2 * m, counts + 2, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
 }

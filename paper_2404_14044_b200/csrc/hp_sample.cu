@@ -659,6 +659,7 @@ Params to_params(const hp_sampler_params* p) {
 template <class BestT>
 int launch_sample(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
                   const Stage& ST, const int64_t* r_off, const Outputs& O, cudaStream_t s) {
+    TimedSpan ts(mode == 0 ? "k_sample" : "k_sample_overflow", s);
     k_sample<BestT><<<kSampleGrid, kThreads, 0, s>>>(C, P, mode, list, list_n, RO, ST, r_off, O);
     HP_CHECK_LAUNCH("k_sample");
     return HP_OK;
@@ -746,8 +747,11 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
     Csr C{offsets, ids, t, dist, slopes, colors, m};
     Params P = to_params(p);
     Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
-    k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.ro.ray_stage, w.st, O);
-    HP_CHECK_LAUNCH("k_emit");
+    {
+        TimedSpan ts("k_emit", s);
+        k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.ro.ray_stage, w.st, O);
+        HP_CHECK_LAUNCH("k_emit");
+    }
     // rays whose retained list did not fit the staging: recompute, write direct
     HP_TRY(dispatch_sample(C, P, 1, w.ro.ovf_list, w.ro.ovf_n, w.ro, w.st, r_off, O, s));
     return HP_OK;
