@@ -32,6 +32,7 @@
 
 #include <cfloat>
 #include <climits>
+#include <cmath>
 
 #include "hp_common.cuh"
 
@@ -51,6 +52,7 @@ struct Params {
     int K;
     int eps_mode, want_color, exact_t_end;
     double beta2, gamma, eps, tau_min;
+    double inv_beta2_up;  // 1 / beta2 rounded up (bound factors only)
 };
 
 struct Csr {
@@ -199,18 +201,21 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
     if (fast) {
         // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
         int l = j, r = j + 1;
+        double tl = tj, tr = r < q ? ldg(T + r) : 0.0;
         while (l >= 0 || r < q) {
+            const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
             int i;
-            if (l < 0) {
-                i = r++;
-            } else if (r >= q) {
-                i = l--;
-            } else if (dsub(tj, ldg(T + l)) <= dsub(ldg(T + r), tj)) {
-                i = l--;
+            double ti;
+            if (go_left) {
+                i = l;
+                ti = tl;
+                if (--l >= 0) tl = ldg(T + l);
             } else {
-                i = r++;
+                i = r;
+                ti = tr;
+                if (++r < q) tr = ldg(T + r);
             }
-            const double dt = dsub(ldg(T + i), tj);
+            const double dt = dsub(ti, tj);
             const double lb = dmul(dt, dt);
             if (lb > kd) break;  // the other side is at least as far
             const double di = ldg(DS + i);
@@ -275,12 +280,14 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
 }
 
 // Upper bound of the reference's factor fl(1 - alpha_j) (DESIGN.md "sampler:
-// transmittance bound").  Any ksel members of j's pool give a mean distance
-// >= the K-nearest mean, so the udf bound is the mean over the ksel pool
-// members nearest to j in t order, inflated by 1e-12 (which dominates every
-// fp64 rounding of the two sums); alpha is then bounded below with a further
-// 1e-12 margin (covers exp() ulp differences).  Every later operation is
-// monotone, so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
+// transmittance bound").  For any ksel members A of j's pool,
+//   sum_{K nearest} sqrt(d2) <= sum_A sqrt(dt^2 + ds^2) <= sum_A (|dt| + ds),
+// so the mean of (|dt| + ds) over the first ksel pool members at or after j
+// in t order (then before j) bounds udf_j from above once inflated by 1e-12
+// (which dominates every fp64 rounding of both sums for K <= 256).  exp is
+// then bounded below in fp32 (argument rounded up, result scaled by
+// 1 - 2^-20 against expf's 2-ulp error).  Every later operation is monotone,
+// so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
 __device__ double bound_factor(const double* __restrict__ T, const double* __restrict__ DS, int q, int j,
                                int jstar, double slope, const Params& P) {
     const double tj = ldg(T + j);
@@ -289,26 +296,22 @@ __device__ double bound_factor(const double* __restrict__ T, const double* __res
     const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
     double sum = 0.0;
     int found = 0;
-    int l = j, r = j + 1;
-    while (found < ksel) {
-        int i;
-        if (l < 0) {
-            i = r++;
-        } else if (r >= q) {
-            i = l--;
-        } else if (dsub(tj, ldg(T + l)) <= dsub(ldg(T + r), tj)) {
-            i = l--;
-        } else {
-            i = r++;
-        }
+    for (int i = j; i < q && found < ksel; i++) {
         const double di = ldg(DS + i);
         if (use_el && di > rj) continue;
-        const double dt = dsub(ldg(T + i), tj);
-        sum = dadd(sum, sqrt(dadd(dmul(dt, dt), dmul(di, di))));
+        sum = dadd(sum, dadd(dsub(ldg(T + i), tj), di));
+        found++;
+    }
+    for (int i = j - 1; found < ksel; i--) {  // the pool has >= ksel members
+        const double di = ldg(DS + i);
+        if (use_el && di > rj) continue;
+        sum = dadd(sum, dadd(dsub(tj, ldg(T + i)), di));
         found++;
     }
     const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
-    const double a_lo = dmul(dmul(P.gamma, exp(__ddiv_rn(-dmul(udf_up, udf_up), P.beta2))), 1.0 - 1e-12);
+    const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
+    const float e = expf(-__double2float_ru(y));
+    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
     return dsub(1.0, a_lo);
 }
 
@@ -653,6 +656,9 @@ Params to_params(const hp_sampler_params* p) {
     P.gamma = p->gamma;
     P.eps = p->eps;
     P.tau_min = p->tau_min;
+    // 1/beta2 rounded toward +inf on the host (fesetround-free): next double up
+    const double r = 1.0 / p->beta2;
+    P.inv_beta2_up = nextafter(r, INFINITY);
     return P;
 }
 
