@@ -107,7 +107,9 @@ int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
                          void* workspace, size_t workspace_bytes, hp_stream_t stream);
 
 /* ---------------- query ---------------- */
-int hp_query_workspace_bytes(int64_t m, int64_t pad, size_t* bytes);
+/* total: Q for hp_query_fill's workspace (it holds the unsorted matches),
+ * 0 for hp_query_count. */
+int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t total, size_t* bytes);
 /* Pass 1.  pixels: int64 [m,2] (u, v) with element stride pixel_stride between
  * rays (2 for an (m,2) array); dirs float64 [m,3]; t_near/t_far/slopes [m];
  * origin_host: the index camera origin (host).  Writes probes/scanned [m]

@@ -324,31 +324,65 @@ __device__ __forceinline__ bool key_less(double ta, int64_t ia, double tb, int64
     return ta < tb || (ta == tb && ia < ib);
 }
 
+constexpr int kCoarse = 256;
+
 template <int kCap>
 struct SortSmem {
     double t[kCap];
-    int id[kCap];  // point ids < 2^31 (hp_build)
-    unsigned int bk[kCap];  // bucket << 16 | local index
+    int id[kCap];           // point ids < 2^31 (hp_build)
+    unsigned int bk[kCap];  // fine bucket << 16 | local index
     unsigned short lst[kCap];
     unsigned short perm[kCap];
     int hist[kCap + 1];
+    int chist[kCoarse + 1];
     unsigned long long tmin, tmax;
-    int scan_sh[kWarps + 1];
+    int scan_sh[33];
 };
 
-// Sort one ray's segment [off, off+q) by (t, id) in place (q <= kCap).
-template <int kCap>
-__device__ void sort_segment(SortSmem<kCap>& F, int q, int64_t* __restrict__ gid, double* __restrict__ gt,
-                             double* __restrict__ gd) {
-    constexpr int kPer = (kCap + kThreads - 1) / kThreads;
+__device__ __forceinline__ double from_okey(unsigned long long k) {
+    return __longlong_as_double((k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k);
+}
+
+// Block-wide exclusive scan of a[0..n) in place (n <= per * blockDim.x).
+template <int kPer>
+__device__ void block_scan_inplace(int* a, int n, int* sh) {
     const int tid = threadIdx.x;
-    for (int e = tid; e < q; e += kThreads) {
-        F.t[e] = gt[e];
-        F.id[e] = int(gid[e]);
+    int v[kPer], acc = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+        const int i = tid * kPer + k;
+        v[k] = i < n ? a[i] : 0;
+        acc += v[k];
+    }
+    int total;
+    int run = block_excl_scan<int>(acc, sh, &total);
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+        const int i = tid * kPer + k;
+        if (i < n) a[i] = run;
+        run += v[k];
+    }
+}
+
+// Sort one ray's q matches by (t, id): read from the fill scratch (st, sid,
+// sd), write the sorted segment to the outputs.  Buckets are equalised: a
+// 256-bin coarse histogram of t over [tmin, tmax] assigns each coarse bin a
+// share of the q fine buckets proportional to its population, and t is
+// placed linearly inside its bin's share.  The map is monotone in t, so
+// buckets are ordered; each element's final position is its bucket start
+// plus its exact (t, id) rank among the (few) members of its bucket.
+template <int kCap, int kT>
+__device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int64_t* __restrict__ sid,
+                             const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
+                             double* __restrict__ gd) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < q; e += kT) {
+        F.t[e] = st[e];
+        F.id[e] = int(sid[e]);
     }
     if (q <= 64) {
         __syncthreads();
-        for (int e = tid; e < q; e += kThreads) {
+        for (int e = tid; e < q; e += kT) {
             const double te = F.t[e];
             const int ie = F.id[e];
             int rank = 0;
@@ -357,70 +391,78 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, int64_t* __restrict__ gid
         }
         __syncthreads();
     } else {
-        int nb = 64;
-        while (nb < q && nb < kCap) nb <<= 1;
+        const int nb = q;  // fine buckets
         if (tid == 0) {
             F.tmin = ~0ull;
             F.tmax = 0ull;
         }
-        for (int k = tid; k <= nb; k += kThreads) F.hist[k] = 0;
+        for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
+        for (int k = tid; k <= nb; k += kT) F.hist[k] = 0;
         __syncthreads();
         unsigned long long lmin = ~0ull, lmax = 0;
-        for (int e = tid; e < q; e += kThreads) {
+        for (int e = tid; e < q; e += kT) {
             const unsigned long long kk = okey(F.t[e]);
             lmin = lmin < kk ? lmin : kk;
             lmax = lmax > kk ? lmax : kk;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lmin, o);
-            const unsigned long long b = __shfl_xor_sync(0xffffffffu, lmax, o);
-            lmin = lmin < a ? lmin : a;
-            lmax = lmax > b ? lmax : b;
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, lmin, o);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, lmax, o);
+            lmin = lmin < x ? lmin : x;
+            lmax = lmax > y ? lmax : y;
         }
         if (lane_id() == 0) {
             atomicMin(&F.tmin, lmin);
             atomicMax(&F.tmax, lmax);
         }
         __syncthreads();
-        const unsigned long long kmin = F.tmin, kmax = F.tmax;
-        const double tlo = __longlong_as_double((kmin & 0x8000000000000000ull) ? (kmin & 0x7fffffffffffffffull) : ~kmin);
-        const double thi = __longlong_as_double((kmax & 0x8000000000000000ull) ? (kmax & 0x7fffffffffffffffull) : ~kmax);
+        const double tlo = from_okey(F.tmin), thi = from_okey(F.tmax);
         const double span = dsub(thi, tlo);
         // capped so that 0 * scale stays 0 when the span is tiny
-        const double scale = span > 0.0 ? fmin(__ddiv_rn(double(nb), span), DBL_MAX) : 0.0;
-        for (int e = tid; e < q; e += kThreads) {
-            // monotone in t: (t - tlo) and the positive scaling both preserve order
-            const double x = fmin(dmul(dsub(F.t[e], tlo), scale), double(nb - 1));
-            const int b = int(x);
-            const int li = atomicAdd(&F.hist[b], 1);
-            F.bk[e] = (unsigned(b) << 16) | unsigned(li);
+        const double cscale = span > 0.0 ? fmin(__ddiv_rn(double(kCoarse), span), DBL_MAX) : 0.0;
+        auto coarse_x = [&](double t) { return fmin(dmul(dsub(t, tlo), cscale), double(kCoarse)); };
+        for (int e = tid; e < q; e += kT) {
+            const int b = min(int(coarse_x(F.t[e])), kCoarse - 1);
+            const unsigned peers = __match_any_sync(__activemask(), b);
+            if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.chist[b], __popc(peers));
         }
         __syncthreads();
-        {
-            int v[kPer], acc = 0;
-#pragma unroll
-            for (int k = 0; k < kPer; k++) {
-                const int i = tid * kPer + k;
-                v[k] = i < nb ? F.hist[i] : 0;
-                acc += v[k];
+        // coarse prefix counts -> first fine bucket of each coarse bin
+        if (tid < 32) {
+            int run = 0;
+            for (int c0 = 0; c0 < kCoarse; c0 += 32) {
+                const int v = F.chist[c0 + tid];
+                const int inc = warp_incl_scan(v);
+                F.chist[c0 + tid] = int((int64_t(run + inc - v) * nb) / q);
+                run += __shfl_sync(0xffffffffu, inc, 31);
             }
-            int total;
-            int run = block_excl_scan<int>(acc, F.scan_sh, &total);
-#pragma unroll
-            for (int k = 0; k < kPer; k++) {
-                const int i = tid * kPer + k;
-                if (i < nb) F.hist[i] = run;
-                run += v[k];
-            }
+            if (tid == 0) F.chist[kCoarse] = nb;
         }
         __syncthreads();
-        for (int e = tid; e < q; e += kThreads) {
+        for (int e = tid; e < q; e += kT) {
+            const double x = coarse_x(F.t[e]);
+            const int b = min(int(x), kCoarse - 1);
+            const int f0 = F.chist[b], width = F.chist[b + 1] - f0;
+            int f = f0;
+            if (width > 1) {
+                // x - b is exact (Sterbenz) and in [0, 1]
+                const int off = int(dmul(dsub(x, double(b)), double(width)));
+                f += min(off, width - 1);
+            }
+            f = min(f, nb - 1);
+            const int li = atomicAdd(&F.hist[f], 1);
+            F.bk[e] = (unsigned(f) << 16) | unsigned(li);
+        }
+        __syncthreads();
+        block_scan_inplace<(kCap + kT - 1) / kT>(F.hist, nb, F.scan_sh);
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
             const unsigned bk = F.bk[e];
             F.lst[F.hist[bk >> 16] + (bk & 0xffffu)] = (unsigned short)e;
         }
         __syncthreads();
-        for (int e = tid; e < q; e += kThreads) {
+        for (int e = tid; e < q; e += kT) {
             const unsigned bk = F.bk[e];
             const int bs = F.hist[bk >> 16];
             const int be = (int(bk >> 16) + 1 < nb) ? F.hist[(bk >> 16) + 1] : q;
@@ -435,31 +477,20 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, int64_t* __restrict__ gid
         }
         __syncthreads();
     }
-    // dist: gather in permuted order into registers before overwriting
-    double dv[kPer];
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int p = tid + k * kThreads;
-        if (p < q) dv[k] = gd[F.perm[p]];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int p = tid + k * kThreads;
-        if (p < q) {
-            const int e = F.perm[p];
-            gd[p] = dv[k];
-            gt[p] = F.t[e];
-            gid[p] = F.id[e];
-        }
+    for (int p = tid; p < q; p += kT) {
+        const int e = F.perm[p];
+        gt[p] = F.t[e];
+        gid[p] = F.id[e];
+        gd[p] = sd[e];
     }
     __syncthreads();
 }
 
 constexpr int kSortSmall = 2048;
 constexpr int kSortLarge = 8192;
+constexpr int kSortLargeThreads = 512;
 
-// Size classes of rays to sort: [2, kSortSmall], (kSortSmall, kSortLarge], above.
+// Size classes of rays to sort: [1, kSortSmall], (kSortSmall, kSortLarge], above.
 __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
                                int* __restrict__ counts) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
@@ -467,7 +498,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q < 2 ? -1 : (q <= kSortSmall ? 0 : (q <= kSortLarge ? 1 : 2));
+            cls = q < 1 ? -1 : (q <= kSortSmall ? 0 : (q <= kSortLarge ? 1 : 2));
         }
 #pragma unroll
         for (int c = 0; c < 3; c++) {  // warp-aggregated append
@@ -481,13 +512,15 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
     }
 }
 
-// Sort the rays of one size class (list of ray ids): in shared memory when
-// kCap > 0, with the in-place global sorting network when kCap == 0.
-template <int kCap>
-__global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restrict__ off, const int* __restrict__ list,
-                                                         const int* __restrict__ list_n,
-                                                         int64_t* __restrict__ out_id, double* __restrict__ out_t,
-                                                         double* __restrict__ out_d) {
+// Sort the rays of one size class (list of ray ids) from the fill scratch
+// into the outputs: in shared memory when kCap > 0; with an in-place sorting
+// network on the scratch then a copy when kCap == 0.
+template <int kCap, int kT>
+__global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int* __restrict__ list,
+                                                   const int* __restrict__ list_n, double* __restrict__ st,
+                                                   int64_t* __restrict__ sid, double* __restrict__ sd,
+                                                   int64_t* __restrict__ out_id, double* __restrict__ out_t,
+                                                   double* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char dyn[];
     const int n = *list_n;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
@@ -495,11 +528,12 @@ __global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restri
         const int64_t o = off[r];
         const int64_t q = off[r + 1] - o;
         if constexpr (kCap > 0) {
-            sort_segment<kCap>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), out_id + o, out_t + o, out_d + o);
+            sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), st + o, sid + o, sd + o,
+                                   out_id + o, out_t + o, out_d + o);
         } else {
-            double* tt = out_t + o;
-            double* dd = out_d + o;
-            int64_t* ii = out_id + o;
+            double* tt = st + o;
+            double* dd = sd + o;
+            int64_t* ii = sid + o;
             block_bitonic_sort(
                 q, [&](int64_t a, int64_t b) { return key_less(tt[a], ii[a], tt[b], ii[b]); },
                 [&](int64_t a, int64_t b) {
@@ -513,6 +547,12 @@ __global__ void __launch_bounds__(kThreads) k_query_sort(const int64_t* __restri
                     ii[a] = ii[b];
                     ii[b] = y;
                 });
+            __syncthreads();
+            for (int64_t p = threadIdx.x; p < q; p += kT) {
+                out_t[o + p] = tt[p];
+                out_d[o + p] = dd[p];
+                out_id[o + p] = ii[p];
+            }
             __syncthreads();
         }
     }
@@ -547,9 +587,26 @@ unsigned group_grid(int64_t m, int per_sm) {
 
 using namespace hp;
 
-extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, size_t* bytes) {
-    // scan scratch | 3 ray lists of the sort size classes | 3 counts
-    *bytes = scan_workspace_bytes(m + 1) + 256 + sizeof(int) * (3 * (m > 0 ? m : 1) + 64) + 256;
+static void carve_fill(Carver& c, int64_t m, int64_t total, int** lists, int** counts, double** st,
+                       int64_t** sid, double** sd) {
+    c.take<char>(scan_workspace_bytes(m + 1));
+    *lists = c.take<int>(3 * (m > 0 ? m : 1));
+    *counts = c.take<int>(64);
+    *st = c.take<double>(total > 0 ? total : 1);
+    *sid = c.take<int64_t>(total > 0 ? total : 1);
+    *sd = c.take<double>(total > 0 ? total : 1);
+}
+
+extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t total, size_t* bytes) {
+    // scan scratch | 3 ray lists of the sort size classes | counts | unsorted
+    // matches (t, id, dist) written by the fill pass (total = Q; 0 for pass 1)
+    Carver c(nullptr, 0);
+    int* l;
+    int* cn;
+    double *st, *sd;
+    int64_t* sid;
+    carve_fill(c, m, total, &l, &cn, &st, &sid, &sd);
+    *bytes = c.used + 256;
     (void)pad;
     return HP_OK;
 }
@@ -592,9 +649,11 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
     (void)padded_h;
     if (m == 0 || total == 0) return HP_OK;
     Carver cv(workspace, workspace_bytes);
-    cv.take<char>(scan_workspace_bytes(m + 1));
-    int* lists = cv.take<int>(3 * m);
-    int* counts = cv.take<int>(64);
+    int* lists;
+    int* counts;
+    double *st, *sd;
+    int64_t* sid;
+    carve_fill(cv, m, total, &lists, &counts, &st, &sid, &sd);
     if (!cv.ok()) {
         set_error("hp_query_fill: workspace too small");
         return HP_ESPACE;
@@ -604,14 +663,14 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
     static bool attr = false;
     if (!attr) {
         HP_TRY(set_smem(k_query_fill, sizeof(FillSmem)));
-        HP_TRY(set_smem(k_query_sort<kSortSmall>, sizeof(SortSmem<kSortSmall>)));
-        HP_TRY(set_smem(k_query_sort<kSortLarge>, sizeof(SortSmem<kSortLarge>)));
+        HP_TRY(set_smem(k_query_sort<kSortSmall, kThreads>, sizeof(SortSmem<kSortSmall>)));
+        HP_TRY(set_smem(k_query_sort<kSortLarge, kSortLargeThreads>, sizeof(SortSmem<kSortLarge>)));
         attr = true;
     }
     {
         TimedSpan ts("k_query_fill", s);
         k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, m,
-                                                                          offsets, ids, t_proj, dist_perp);
+                                                                          offsets, sid, st, sd);
         HP_CHECK_LAUNCH("k_query_fill");
     }
     TimedSpan ts("k_query_sort", s);
@@ -619,13 +678,14 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, counts);
     HP_CHECK_LAUNCH("k_sort_classes");
-    k_query_sort<kSortSmall><<<kNumSMs * 4, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(offsets, lists, counts,
-                                                                                         ids, t_proj, dist_perp);
+    k_query_sort<kSortSmall, kThreads><<<kNumSMs * 4, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
+        offsets, lists, counts, st, sid, sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<small>");
-    k_query_sort<kSortLarge><<<kNumSMs, kThreads, sizeof(SortSmem<kSortLarge>), s>>>(offsets, lists + m, counts + 1,
-                                                                                     ids, t_proj, dist_perp);
+    k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs, kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
+        offsets, lists + m, counts + 1, st, sid, sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
-    k_query_sort<0><<<kNumSMs, kThreads, 0, s>>>(offsets, lists + 2 * m, counts + 2, ids, t_proj, dist_perp);
+    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, lists + 2 * m, counts + 2, st, sid, sd, ids,
+                                                           t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
 }

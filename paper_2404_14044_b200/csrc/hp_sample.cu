@@ -174,13 +174,26 @@ struct BestDyn {
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
+constexpr int kWin = 384;  // candidates of a ray staged in shared memory (per warp)
+
+// The ray's t / ds: the first kWin candidates from the warp's shared-memory
+// window, the rest from global memory (read-only path).
+struct RayView {
+    const double* gt;
+    const double* gd;
+    const double* wt;
+    const double* wd;
+    __device__ __forceinline__ double t(int i) const { return i < kWin ? wt[i] : __ldg(gt + i); }
+    __device__ __forceinline__ double d(int i) const { return i < kWin ? wd[i] : __ldg(gd + i); }
+};
+
 // Exact udf/alpha (and colour) of candidate j (reference _kernels.py:594-660).
 template <class BestT>
-__device__ void eval_exact(const double* __restrict__ T, const double* __restrict__ DS, int q, int j, bool fast,
+__device__ void eval_exact(const RayView& V, int q, int j, bool fast,
                            int jstar, double slope, const Params& P, const int64_t* __restrict__ ids_ray,
                            const double* __restrict__ colors, double& udf, double& alpha, double* col3,
                            unsigned long long& evals) {
-    const double tj = ldg(T + j);
+    const double tj = V.t(j);
     const double rj = dmul(slope, tj);
     bool use_el;
     int ksel;
@@ -189,7 +202,7 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
         ksel = use_el ? P.K : (q < P.K ? q : P.K);
     } else {
         int n_el = 0;
-        for (int i = 0; i < q; i++) n_el += (ldg(DS + i) <= rj);
+        for (int i = 0; i < q; i++) n_el += (V.d(i) <= rj);
         use_el = n_el >= P.K;
         const int pool = use_el ? n_el : q;
         ksel = pool > P.K ? P.K : pool;
@@ -201,7 +214,7 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
     if (fast) {
         // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
         int l = j, r = j + 1;
-        double tl = tj, tr = r < q ? ldg(T + r) : 0.0;
+        double tl = tj, tr = r < q ? V.t(r) : 0.0;
         while (l >= 0 || r < q) {
             const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
             int i;
@@ -209,16 +222,16 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
             if (go_left) {
                 i = l;
                 ti = tl;
-                if (--l >= 0) tl = ldg(T + l);
+                if (--l >= 0) tl = V.t(l);
             } else {
                 i = r;
                 ti = tr;
-                if (++r < q) tr = ldg(T + r);
+                if (++r < q) tr = V.t(r);
             }
             const double dt = dsub(ti, tj);
             const double lb = dmul(dt, dt);
             if (lb > kd) break;  // the other side is at least as far
-            const double di = ldg(DS + i);
+            const double di = V.d(i);
             if (use_el && di > rj) continue;
             const double d2 = dadd(lb, dmul(di, di));
             evals++;
@@ -229,9 +242,9 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
         }
     } else {
         for (int i = 0; i < q; i++) {  // reference loop (_kernels.py:607-620)
-            const double di = ldg(DS + i);
+            const double di = V.d(i);
             if (use_el && di > rj) continue;
-            const double dt = dsub(ldg(T + i), tj);
+            const double dt = dsub(V.t(i), tj);
             const double d2 = dadd(dmul(dt, dt), dmul(di, di));
             evals++;
             if (d2 < kd) {
@@ -288,24 +301,23 @@ __device__ void eval_exact(const double* __restrict__ T, const double* __restric
 // then bounded below in fp32 (argument rounded up, result scaled by
 // 1 - 2^-20 against expf's 2-ulp error).  Every later operation is monotone,
 // so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
-__device__ double bound_factor(const double* __restrict__ T, const double* __restrict__ DS, int q, int j,
-                               int jstar, double slope, const Params& P) {
-    const double tj = ldg(T + j);
+__device__ double bound_factor(const RayView& V, int q, int j, int jstar, double slope, const Params& P) {
+    const double tj = V.t(j);
     const double rj = dmul(slope, tj);
     const bool use_el = j >= jstar;
     const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
     double sum = 0.0;
     int found = 0;
     for (int i = j; i < q && found < ksel; i++) {
-        const double di = ldg(DS + i);
+        const double di = V.d(i);
         if (use_el && di > rj) continue;
-        sum = dadd(sum, dadd(dsub(ldg(T + i), tj), di));
+        sum = dadd(sum, dadd(dsub(V.t(i), tj), di));
         found++;
     }
     for (int i = j - 1; found < ksel; i--) {  // the pool has >= ksel members
-        const double di = ldg(DS + i);
+        const double di = V.d(i);
         if (use_el && di > rj) continue;
-        sum = dadd(sum, dadd(dsub(tj, ldg(T + i)), di));
+        sum = dadd(sum, dadd(dsub(tj, V.t(i)), di));
         found++;
     }
     const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
@@ -340,6 +352,7 @@ __device__ int warp_first_true(int q, Pred pred) {
 }
 
 struct WarpSmem {
+    double wt[kWin], wd[kWin];
     int rj[kRetCap];
     double rudf[kRetCap], ralpha[kRetCap], rw[kRetCap], rcol[kRetCap * 3];
 };
@@ -374,6 +387,10 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
     const bool small_k = P.K <= 8;
     for (int k = lane; k < q; k += 32) {
         const double tk = ldg(T + k), dk = ldg(DS + k);
+        if (k < kWin) {
+            W.wt[k] = tk;
+            W.wd[k] = dk;
+        }
         ok &= (fabs(tk) <= DBL_MAX) && (dk >= 0.0) && (dk <= DBL_MAX);
         if (k + 1 < q) ok &= !(ldg(T + k + 1) < tk);
         if (small_k && dk < top[7]) {  // insert into the lane's sorted top-8
@@ -386,7 +403,8 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
             }
         }
     }
-    const bool fast = __all_sync(0xffffffffu, ok);
+    const bool fast = __all_sync(0xffffffffu, ok);  // also orders the window stores
+    const RayView V{T, DS, W.wt, W.wd};
     int jstar = 0;
     if (fast) {
         double dsk = CUDART_INF;  // K-th smallest ds (inf if q < K)
@@ -413,13 +431,13 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
                     if (lane == ml) h++;
                     dsk = mv;
                 }
-                jstar = warp_first_true(q, [&](int j) { return dmul(slope, ldg(T + j)) >= dsk; });
+                jstar = warp_first_true(q, [&](int j) { return dmul(slope, V.t(j)) >= dsk; });
             } else {
                 // generic K: first j with #{ds_i <= r_j} >= K by counting passes
                 jstar = warp_first_true(q, [&](int j) {
-                    const double rj = dmul(slope, ldg(T + j));
+                    const double rj = dmul(slope, V.t(j));
                     int c = 0;
-                    for (int i = 0; i < q; i++) c += (ldg(DS + i) <= rj);
+                    for (int i = 0; i < q; i++) c += (V.d(i) <= rj);
                     return c >= P.K;
                 });
             }
@@ -436,7 +454,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
         double U = 1.0;
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
-            const double u = j < q ? bound_factor(T, DS, q, j, jstar, slope, P) : 1.0;
+            const double u = j < q ? bound_factor(V, q, j, jstar, slope, P) : 1.0;
             nbound += 32;
             const int n = min(32, q - c0);
             for (int k = 0; k < n; k++) {
@@ -462,7 +480,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
     for (int c0 = 0; c0 < E; c0 += 32) {
         const int j = c0 + lane;
         double u = 0.0, a = 0.0, col[3] = {0.0, 0.0, 0.0};
-        if (j < E) eval_exact<BestT>(T, DS, q, j, fast, jstar, slope, P, ids_ray, C.colors, u, a, col, nexact);
+        if (j < E) eval_exact<BestT>(V, q, j, fast, jstar, slope, P, ids_ray, C.colors, u, a, col, nexact);
         const int n = min(32, E - c0);
         double wmine = 0.0;
         unsigned keep = 0;
@@ -488,8 +506,8 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
             if (mode == 1) {
                 const int64_t o = out_base + pos;
                 O.r_id[o] = ids_ray[jj];
-                O.r_t[o] = ldg(T + jj);
-                O.r_dist[o] = ldg(DS + jj);
+                O.r_t[o] = V.t(jj);
+                O.r_dist[o] = V.d(jj);
                 O.r_udf[o] = u;
                 O.r_alpha[o] = a;
                 O.r_w[o] = wmine;
@@ -564,7 +582,8 @@ template <class BestT>
 __global__ void __launch_bounds__(kThreads, 3) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
                                                      const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
                                                      const int64_t* __restrict__ r_off, Outputs O) {
-    __shared__ WarpSmem W[kWarps];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    WarpSmem* W = reinterpret_cast<WarpSmem*>(dyn);
     const int64_t n = ray_list ? int64_t(*ray_list_n) : C.m;
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t k = int64_t(blockIdx.x) * kWarps + warp_id(); k < n; k += warps) {
@@ -665,8 +684,16 @@ Params to_params(const hp_sampler_params* p) {
 template <class BestT>
 int launch_sample(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
                   const Stage& ST, const int64_t* r_off, const Outputs& O, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(k_sample<BestT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(sizeof(WarpSmem) * kWarps));
+        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(k_sample)");
+        attr = true;
+    }
     TimedSpan ts(mode == 0 ? "k_sample" : "k_sample_overflow", s);
-    k_sample<BestT><<<kSampleGrid, kThreads, 0, s>>>(C, P, mode, list, list_n, RO, ST, r_off, O);
+    k_sample<BestT><<<kSampleGrid, kThreads, sizeof(WarpSmem) * kWarps, s>>>(C, P, mode, list, list_n, RO, ST,
+                                                                             r_off, O);
     HP_CHECK_LAUNCH("k_sample");
     return HP_OK;
 }

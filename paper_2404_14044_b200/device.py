@@ -166,7 +166,7 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     pixels = pixels.contiguous()
     dirs = dirs.contiguous()
     nb = c_size(0)
-    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, ctypes.byref(nb)))
+    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, 0, ctypes.byref(nb)))
     ws = _workspace(nb.value, dev)
     offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
     probes = torch.empty(m, dtype=torch.int64, device=dev)
@@ -179,6 +179,8 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
                                   nb.value, _stream()))
     _mark("query.count")
     total = int(offsets[m].item())
+    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, total, ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
