@@ -379,12 +379,13 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
     const int64_t* ids_ray = C.ids + lo;
     const double thr = P.eps_mode ? P.eps : P.tau_min;
 
-    // ---- pass over the ray: fast-path preconditions + K-th smallest ds (K <= 8)
+    // ---- pass over the ray: fast-path preconditions, shared-memory window,
+    // and the count of candidates within r_0 (use_el holds from j = 0 on when
+    // it reaches K, the common case on dense surfaces)
     bool ok = slope >= 0.0 && slope <= DBL_MAX;
-    double top[8];
-#pragma unroll
-    for (int b = 0; b < 8; b++) top[b] = CUDART_INF;
-    const bool small_k = P.K <= 8;
+    const double r0 = dmul(slope, ldg(T));
+    int c0cnt = 0;
+#pragma unroll 4
     for (int k = lane; k < q; k += 32) {
         const double tk = ldg(T + k), dk = ldg(DS + k);
         if (k < kWin) {
@@ -393,70 +394,72 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
         }
         ok &= (fabs(tk) <= DBL_MAX) && (dk >= 0.0) && (dk <= DBL_MAX);
         if (k + 1 < q) ok &= !(ldg(T + k + 1) < tk);
-        if (small_k && dk < top[7]) {  // insert into the lane's sorted top-8
-            double v = dk;
-#pragma unroll
-            for (int b = 0; b < 8; b++) {
-                const double lo_ = fmin(top[b], v), hi_ = fmax(top[b], v);
-                top[b] = lo_;
-                v = hi_;
-            }
-        }
+        c0cnt += (dk <= r0);
     }
     const bool fast = __all_sync(0xffffffffu, ok);  // also orders the window stores
     const RayView V{T, DS, W.wt, W.wd};
     int jstar = 0;
     if (fast) {
-        double dsk = CUDART_INF;  // K-th smallest ds (inf if q < K)
-        if (q >= P.K) {
-            if (small_k) {
-                // merge the lanes' sorted lists: pop the warp minimum K times
-                int h = 0;
-                for (int k = 0; k < P.K; k++) {
-                    double mine = CUDART_INF;
-#pragma unroll
-                    for (int b = 0; b < 8; b++)
-                        if (b == h) mine = top[b];
-                    double mv = mine;
-                    int ml = lane;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const double ov = __shfl_xor_sync(0xffffffffu, mv, o);
-                        const int ol = __shfl_xor_sync(0xffffffffu, ml, o);
-                        if (ov < mv || (ov == mv && ol < ml)) {
-                            mv = ov;
-                            ml = ol;
-                        }
-                    }
-                    if (lane == ml) h++;
-                    dsk = mv;
-                }
-                jstar = warp_first_true(q, [&](int j) { return dmul(slope, V.t(j)) >= dsk; });
-            } else {
-                // generic K: first j with #{ds_i <= r_j} >= K by counting passes
-                jstar = warp_first_true(q, [&](int j) {
-                    const double rj = dmul(slope, V.t(j));
-                    int c = 0;
-                    for (int i = 0; i < q; i++) c += (V.d(i) <= rj);
-                    return c >= P.K;
-                });
-            }
-        } else {
+        if (warp_sum(c0cnt) >= P.K) {
+            jstar = 0;
+        } else if (q < P.K) {
             jstar = q;
+        } else {
+            // first j with #{ds_i <= slope * t_j} >= K (monotone in j)
+            jstar = warp_first_true(q, [&](int j) {
+                const double rj = dmul(slope, V.t(j));
+                int c = 0;
+                for (int i = 0; i < q; i++) c += (V.d(i) <= rj);
+                return c >= P.K;
+            });
         }
     }
 
     // ---- 1. bound chain (fast path)
+    // Vs bounds the reference's T at the current chunk start.  While it is
+    // far from underflow, the chunk's bounds come from a round-up warp prefix
+    // product: T_{c0+l+1} <= T_{c0} * prod f * (1+u)^(l+1) + (l+1) 2^-1075
+    // (round-to-nearest error <= u|x| + 2^-1075 per step), and prod f <=
+    // prod u (round-up).  Near underflow the sequential round-to-nearest chain
+    // U_{i+1} = U_i * u_i (monotone, dominates T_i) takes over and proves the
+    // exact zero.
     int je = q;  // retention is decided before je
     bool proved_zero = false;
     unsigned long long nbound = 0;
     if (fast) {
-        double U = 1.0;
+        double Vs = 1.0;
+        bool seq = false;
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
             const double u = j < q ? bound_factor(V, q, j, jstar, slope, P) : 1.0;
             nbound += 32;
             const int n = min(32, q - c0);
+            if (!seq) {
+                double Pl = u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double other = __shfl_up_sync(0xffffffffu, Pl, o);
+                    if (lane >= o) Pl = __dmul_ru(Pl, other);
+                }
+                double B = __dmul_ru(__dmul_ru(Vs, Pl), 1.0 + double(lane + 1) * 0x1p-51);
+                B = __dadd_ru(B, double(lane + 1) * 0x1p-1074);
+                if (je == q) {
+                    if (Vs < thr) {
+                        je = c0;
+                    } else {
+                        const unsigned mask = __ballot_sync(0xffffffffu, lane < n && B < thr);
+                        if (mask) je = c0 + __ffs(mask);  // T_{c0+l+1} < thr for the first such l
+                    }
+                }
+                const double Vn = __shfl_sync(0xffffffffu, B, n - 1);
+                if (Vn >= 0x1p-1000) {
+                    Vs = Vn;
+                    if (!P.exact_t_end && je < q) break;
+                    continue;
+                }
+                seq = true;  // redo this chunk sequentially from Vs
+            }
+            double U = Vs;
             for (int k = 0; k < n; k++) {
                 const double uk = __shfl_sync(0xffffffffu, u, k);
                 if (je == q && U < thr) je = c0 + k;
@@ -467,6 +470,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
                     break;
                 }
             }
+            Vs = U;
             if (proved_zero || (!P.exact_t_end && je < q)) break;
         }
     }
