@@ -102,4 +102,103 @@ HP_HD float4 filter_point(double x, double y, double z) {
     return make_float4(fx, fy, fz, e);
 }
 
+// ------------------------------------------------------------------ footprint
+// Which pixels of a ray's s x s window can hold an accepted point.  The cone
+// test accepts p iff t = p.d > 0 and |p - t d| <= slope * t, i.e. iff the
+// angle between p and d is at most atan(slope).  A point's pixel depends only
+// on its direction (U = f (p.R)/(p.F)/pw + W/2, V = -f (p.U)/(p.F)/ph + H/2),
+// and the directions within that angle project to an ellipse on the image
+// plane (when the cone does not reach the image plane's horizon).  Per padded
+// row y the accepted points therefore lie in a column interval, computed here
+// with margins: the half-angle widened by 1e-7 relative (covers the fp64 test's
+// rounding), the row slab widened by 1e-3 pixel (covers rounding of V in the
+// build), one extra column on each side (rounding of U).  tests/native/
+// footprint_check.cu verifies the bound against the reference cone test.
+struct CamFrame {
+    double r[3], u[3], f[3];
+    double focal, pw, ph, half_w, half_h;
+};
+
+struct Footprint {
+    int tight;  // 0: use the full window
+    double dx, dy, dz, c2, amin, amax, bL, bR, bmin, bmax;
+};
+
+// Roots of A x^2 + 2 B x + C = 0 (A != 0), sorted; false when complex.
+HP_HD bool roots2(double A, double B, double C, double& x0, double& x1) {
+    double disc = B * B - A * C;
+    if (!(disc >= 0.0)) return false;
+    const double sq = sqrt(disc);
+    const double r0 = (-B + sq) / A, r1 = (-B - sq) / A;
+    x0 = fmin(r0, r1);
+    x1 = fmax(r0, r1);
+    return true;
+}
+
+HP_HD void footprint_init(Footprint& F, const CamFrame& C, double d0, double d1, double d2, double slope) {
+    F.tight = 0;
+    F.dx = d0 * C.r[0] + d1 * C.r[1] + d2 * C.r[2];
+    F.dy = d0 * C.u[0] + d1 * C.u[1] + d2 * C.u[2];
+    F.dz = d0 * C.f[0] + d1 * C.f[1] + d2 * C.f[2];
+    const double sig = slope * (1.0 + 1e-7) + 1e-12;
+    if (!(sig >= 0.0) || !(sig < 1e3)) return;
+    F.c2 = 1.0 / (1.0 + sig * sig);
+    const double s2 = sig * sig * F.c2;
+    const double dz = F.dz, dx = F.dx, dy = F.dy, f = C.focal;
+    // bounded ellipse with margin: the cone edge at least ~0.6 degree from the horizon
+    if (!(dz > 0.0) || !(dz * dz - s2 > 1e-4)) return;
+    const double A2 = s2 - dz * dz;  // < 0
+    const double k = F.c2 - dy * dy, kp = F.c2 - dx * dx;
+    if (!(k > 0.0) || !(kp > 0.0)) return;
+    if (!roots2(A2, dx * f * dz, f * f * (dz * dz - k), F.amin, F.amax)) return;
+    if (!roots2(A2, dy * f * dz, f * f * (dz * dz - kp), F.bmin, F.bmax)) return;
+    F.bL = dy * (F.amin * dx + f * dz) / k;
+    F.bR = dy * (F.amax * dx + f * dz) / k;
+    F.tight = 1;
+}
+
+// a-interval of the ellipse at height b (empty if outside).
+HP_HD void footprint_a_at(const Footprint& F, const CamFrame& C, double b, double& lo, double& hi) {
+    const double A = F.dx * F.dx - F.c2;  // < 0 when tight
+    const double w = b * F.dy + C.focal * F.dz;
+    const double B = F.dx * w;
+    const double Cq = w * w - F.c2 * (b * b + C.focal * C.focal);
+    double disc = B * B - A * Cq;
+    if (disc < 0.0) disc = 0.0;  // tangency up to rounding
+    const double sq = sqrt(disc);
+    const double r0 = (-B + sq) / A, r1 = (-B - sq) / A;
+    lo = fmin(r0, r1);
+    hi = fmax(r0, r1);
+}
+
+// Padded column interval [x0, x1] of padded row y that can hold accepted
+// points of the ray at unpadded pixel (u, v); false if none.  With a
+// non-tight footprint this is the whole window row.
+HP_HD bool footprint_row(const Footprint& F, const CamFrame& C, int pad, int width, int height, int u, int v,
+                         int y, int& x0, int& x1) {
+    x0 = u;
+    x1 = u + 2 * pad;
+    if (!F.tight) return true;
+    const double vr = double(y - pad);  // unpadded row index
+    const double mb = 1e-3 * C.ph;
+    double bb1 = (0.5 * double(height) - vr - 1.0) * C.ph - mb;
+    double bb2 = (0.5 * double(height) - vr) * C.ph + mb;
+    bb1 = fmax(bb1, F.bmin);
+    bb2 = fmin(bb2, F.bmax);
+    if (bb1 > bb2) return false;
+    double l1, h1, l2, h2;
+    footprint_a_at(F, C, bb1, l1, h1);
+    footprint_a_at(F, C, bb2, l2, h2);
+    const double amin = (F.bL >= bb1 && F.bL <= bb2) ? F.amin : fmin(l1, l2);
+    const double amax = (F.bR >= bb1 && F.bR <= bb2) ? F.amax : fmax(h1, h2);
+    // columns (padded), clamped to the window before converting to int
+    const double lo_win = double(u), hi_win = double(u + 2 * pad);
+    const double c0 = floor(amin / C.pw + 0.5 * double(width)) - 1.0 + double(pad);
+    const double c1 = floor(amax / C.pw + 0.5 * double(width)) + 1.0 + double(pad);
+    if (!(c0 <= hi_win) || !(c1 >= lo_win)) return false;
+    x0 = int(fmax(c0, lo_win));
+    x1 = int(fmin(c1, hi_win));
+    return x0 <= x1;
+}
+
 }  // namespace hp

@@ -71,9 +71,15 @@ constexpr int kRowsMax = 48;  // kernel rows tabulated per batch
 
 struct GroupHead {
     RayParams ray[kGroupMax];
-    int rlo[kRowsMax][kGroupMax], rhi[kRowsMax][kGroupMax];  // ray sub-range per row
+    Footprint fp[kGroupMax];
+    int rlo[kRowsMax][kGroupMax], rhi[kRowsMax][kGroupMax];  // ray's tested sub-range per row
     int slo[kRowsMax], shi[kRowsMax];                          // staged (union) range per row
     int u0, u1, v0, v1;
+};
+
+struct QCam {  // camera frame for the footprint (has_cam == 0: full windows)
+    CamFrame C;
+    int has_cam, width, height;
 };
 
 // cp.async (LDGSTS) helpers: asynchronous global -> shared copies.
@@ -96,9 +102,15 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 // Group bounding box (padded coordinates) of rays [r0, r0+G).
-__device__ void group_setup(GroupHead& S, const Rays& R, int64_t r0, int G, int s) {
+__device__ void group_setup(GroupHead& S, const Rays& R, const QCam& QC, int64_t r0, int G, int s) {
     const int tid = threadIdx.x;
-    if (tid < G) S.ray[tid] = load_ray(R, r0 + tid);
+    if (tid < G) {
+        S.ray[tid] = load_ray(R, r0 + tid);
+        if (QC.has_cam)
+            footprint_init(S.fp[tid], QC.C, S.ray[tid].d0, S.ray[tid].d1, S.ray[tid].d2, S.ray[tid].slope);
+        else
+            S.fp[tid].tight = 0;
+    }
     __syncthreads();
     if (tid < 32) {
         int u0 = INT_MAX, u1 = INT_MIN, v0 = INT_MAX, v1 = INT_MIN;
@@ -135,30 +147,41 @@ __device__ void group_setup(GroupHead& S, const Rays& R, int64_t r0, int G, int 
 // owning ray g (warp w owns rays w, w+8, ...), 32 slots at a time, with
 // k = -1 for lanes beyond the ray's sub-range.
 template <int kStage, class Issue, class Test, class Tab>
-__device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, Issue issue,
-                             Test test, Tab tab) {
+__device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, const QCam& QC,
+                             Issue issue, Test test, Tab tab) {
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    const int pad = (s - 1) / 2;
     for (int yb = S.v0; yb < S.v1; yb += kRowsMax) {
         const int nrows = min(kRowsMax, S.v1 - yb);
+        for (int row = tid; row < nrows; row += kThreads) {
+            S.slo[row] = INT_MAX;
+            S.shi[row] = INT_MIN;
+        }
+        __syncthreads();
         for (int idx = tid; idx < nrows * G; idx += kThreads) {
             const int row = idx / G, g = idx - row * G;
             const int y = yb + row;
             const RayParams& r = S.ray[g];
             int lo = 0, hi = 0;
             if (y >= r.v && y < r.v + s) {
-                const int64_t base = int64_t(y) * wp + r.u;
-                lo = L.row_ptr[base];
-                hi = L.row_ptr[base + s];
-                tab(g, hi - lo);
+                const int64_t base = int64_t(y) * wp;
+                tab(g, L.row_ptr[base + r.u + s] - L.row_ptr[base + r.u]);  // scanned: full window
+                int x0, x1;
+                if (footprint_row(S.fp[g], QC.C, pad, QC.width, QC.height, r.u, r.v, y, x0, x1)) {
+                    lo = L.row_ptr[base + x0];
+                    hi = L.row_ptr[base + x1 + 1];
+                    if (lo < hi) {
+                        atomicMin(&S.slo[row], lo);
+                        atomicMax(&S.shi[row], hi);
+                    }
+                }
             }
             S.rlo[row][g] = lo;
             S.rhi[row][g] = hi;
         }
-        for (int row = tid; row < nrows; row += kThreads) {
-            const int64_t base = int64_t(yb + row) * wp;
-            S.slo[row] = L.row_ptr[base + S.u0];
-            S.shi[row] = L.row_ptr[base + S.u1];
-        }
+        __syncthreads();
+        for (int row = tid; row < nrows; row += kThreads)
+            if (S.slo[row] > S.shi[row]) S.slo[row] = S.shi[row] = 0;  // nothing staged
         __syncthreads();
         // chunk cursor (identical in every thread)
         int row = 0, c0 = S.slo[0];
@@ -210,7 +233,7 @@ struct CountSmem {
     int cnt[kGroupMax], scn[kGroupMax];
 };
 
-__global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int64_t wp, int pad, Rays R,
+__global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
                                                           int64_t m, int64_t* __restrict__ counts,
                                                           int64_t* __restrict__ probes,
                                                           int64_t* __restrict__ scanned) {
@@ -221,9 +244,9 @@ __global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int
     for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
         const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
         if (threadIdx.x < kGroupMax) S.cnt[threadIdx.x] = S.scn[threadIdx.x] = 0;
-        group_setup(S.head, R, r0, G, s);
+        group_setup(S.head, R, QC, r0, G, s);
         stream_group<kStageCount>(
-            S.head, G, L, wp, s,
+            S.head, G, L, wp, s, QC,
             [&](int buf, int c0, int c1) {
                 for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) cp_async16(&S.pf[buf][k - c0], relf + k);
             },
@@ -261,7 +284,7 @@ struct FillSmem {
     int64_t off[kGroupMax];
 };
 
-__global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int64_t wp, int pad, Rays R,
+__global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
                                                          int64_t m, const int64_t* __restrict__ off,
                                                          int64_t* __restrict__ out_id, double* __restrict__ out_t,
                                                          double* __restrict__ out_d) {
@@ -278,9 +301,9 @@ __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int6
             S.fill[threadIdx.x] = 0;
             S.off[threadIdx.x] = off[r0 + threadIdx.x];
         }
-        group_setup(S.head, R, r0, G, s);
+        group_setup(S.head, R, QC, r0, G, s);
         stream_group<kStageFill>(
-            S.head, G, L, wp, s,
+            S.head, G, L, wp, s, QC,
             [&](int buf, int c0, int c1) {
                 for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) {
                     const int i = k - c0;
@@ -564,6 +587,26 @@ int set_smem(K kernel, size_t bytes) {
     return e == cudaSuccess ? HP_OK : cuda_status(e, "cudaFuncSetAttribute");
 }
 
+QCam make_qcam(const hp_camera* cam) {
+    QCam q{};
+    q.has_cam = cam != nullptr;
+    if (cam) {
+        for (int k = 0; k < 3; k++) {
+            q.C.r[k] = cam->right[k];
+            q.C.u[k] = cam->up[k];
+            q.C.f[k] = cam->forward[k];
+        }
+        q.C.focal = cam->focal_length;
+        q.C.pw = cam->pixel_width;
+        q.C.ph = cam->pixel_height;
+        q.C.half_w = 0.5 * double(cam->width);
+        q.C.half_h = 0.5 * double(cam->height);
+        q.width = int(cam->width);
+        q.height = int(cam->height);
+    }
+    return q;
+}
+
 int check_common(const hp_query_layout& L, int64_t pad, int64_t m) {
     if (pad < 0 || m < 0 || !L.row_ptr) {
         set_error("hp_query: invalid arguments");
@@ -611,7 +654,8 @@ extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t total, s
     return HP_OK;
 }
 
-extern "C" int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t padded_h, int64_t pad,
+extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
+                              int64_t pad,
                               const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                               const double* t_near, const double* t_far, const double* slopes, int64_t m,
                               int64_t* offsets, int64_t* probes, int64_t* scanned, void* workspace,
@@ -624,6 +668,7 @@ extern "C" int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t 
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
+    const QCam QC = make_qcam(cam);
     if (m > 0) {
         static bool attr = false;
         if (!attr) {
@@ -631,7 +676,7 @@ extern "C" int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t 
             attr = true;
         }
         TimedSpan ts("k_query_count", s);
-        k_query_count<<<group_grid(m, 7), kThreads, sizeof(CountSmem), s>>>(layout, padded_w, int(pad), R, m,
+        k_query_count<<<group_grid(m, 7), kThreads, sizeof(CountSmem), s>>>(layout, padded_w, int(pad), R, QC, m,
                                                                             offsets, probes, scanned);
         HP_CHECK_LAUNCH("k_query_count");
     }
@@ -639,7 +684,8 @@ extern "C" int hp_query_count(hp_query_layout layout, int64_t padded_w, int64_t 
     return HP_OK;
 }
 
-extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t padded_h, int64_t pad,
+extern "C" int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
+                             int64_t pad,
                              const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                              const double* t_near, const double* t_far, const double* slopes, int64_t m,
                              const int64_t* offsets, int64_t total, int64_t* ids, double* t_proj,
@@ -660,6 +706,7 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
+    const QCam QC = make_qcam(cam);
     static bool attr = false;
     if (!attr) {
         HP_TRY(set_smem(k_query_fill, sizeof(FillSmem)));
@@ -669,7 +716,7 @@ extern "C" int hp_query_fill(hp_query_layout layout, int64_t padded_w, int64_t p
     }
     {
         TimedSpan ts("k_query_fill", s);
-        k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, m,
+        k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m,
                                                                           offsets, sid, st, sd);
         HP_CHECK_LAUNCH("k_query_fill");
     }

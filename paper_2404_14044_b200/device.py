@@ -155,7 +155,7 @@ def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered
 
 
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
-          t_far: torch.Tensor, slopes: torch.Tensor):
+          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True):
     """_kernels.hash_query_batch on the device (reference _kernels.py:86-157).
 
     Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors.
@@ -172,7 +172,8 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     probes = torch.empty(m, dtype=torch.int64, device=dev)
     scanned = torch.empty(m, dtype=torch.int64, device=dev)
     L = index.layout()
-    args = (L, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
+    cam = ctypes.byref(camera_struct(index.camera)) if footprint else None
+    args = (L, cam, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
     _mark("query.setup")
     _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), _ptr(ws),

@@ -75,3 +75,39 @@ def test_layout_from_reference_table_equals_build():
     q2 = dv.query(idx2, *rays)
     for a, b in zip(q1, q2):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", gu.case_names())
+def test_cone_footprint_is_transparent(name):
+    """Testing only footprint pixels gives exactly the full-window result."""
+    cloud, cam, cfg, samplers, idx, rays = _dev_case(name)
+    a = dv.query(idx, *rays, footprint=True)
+    b = dv.query(idx, *rays, footprint=False)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+def test_footprint_on_wide_rotated_camera():
+    """Wide field of view, rotated off-origin camera, large delta."""
+    import paper_2404_14044_b200 as hp
+    cloud = hp.generate_scene(hp.SceneSpec("uniform_box", n=40_000, seed=8, extent=3.0))
+    cam = hp.scene_camera(96, 64, fov_deg=110, origin=(0.7, -0.4, 0.3), target=(0.2, 0.1, 4.0),
+                          up=(0.3, 1.0, 0.1))
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.05), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    m = dirs.shape[0]
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    idx = dv.build(up(cloud.positions), cam, cfg.pad)
+    rays = (up(pixels), up(dirs), up(np.full(m, 0.5)), up(np.full(m, 9.0)), up(slopes))
+    a = dv.query(idx, *rays, footprint=True)
+    b = dv.query(idx, *rays, footprint=False)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    ob = orc.build(cloud.positions, cam, cfg.pad)
+    oq = orc.query(ob["table_start"], ob["table_count"], ob["slot_x"], ob["slot_y"], ob["slot_z"],
+                   ob["reordered_ids"], cam.width + 2 * cfg.pad, cfg.pad, pixels[:, 0], pixels[:, 1],
+                   dirs, cam.origin, np.full(m, 0.5), np.full(m, 9.0), slopes)
+    for x, y in zip(a, oq):
+        np.testing.assert_array_equal(x.cpu().numpy(), y)
