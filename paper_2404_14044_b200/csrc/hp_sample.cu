@@ -96,6 +96,7 @@ __device__ __forceinline__ bool kless(double d2a, int ia, double d2b, int ib) {
 // ascending by (d2, i).
 template <int MAXK>
 struct Best {
+    static constexpr int kMax = MAXK;
     double d[MAXK];
     int i[MAXK];
     __device__ __forceinline__ void init() {
@@ -118,6 +119,23 @@ struct Best {
 #pragma unroll
         for (int b = 0; b < MAXK; b++)
             if (b < ksel) f(d[b], i[b]);
+    }
+    // full list (ksel == MAXK): branch-free compare-shift network; the caller
+    // guarantees (nd, ni) < the last entry.
+    __device__ __forceinline__ void insert_full(double nd, int ni) {
+#pragma unroll
+        for (int b = MAXK - 1; b >= 1; --b) {
+            const bool shift = kless(nd, ni, d[b - 1], i[b - 1]);
+            const bool here = !shift && kless(nd, ni, d[b], i[b]);
+            const double db = shift ? d[b - 1] : (here ? nd : d[b]);
+            const int ib = shift ? i[b - 1] : (here ? ni : i[b]);
+            d[b] = db;
+            i[b] = ib;
+        }
+        if (kless(nd, ni, d[0], i[0])) {
+            d[0] = nd;
+            i[0] = ni;
+        }
     }
     // caller guarantees (nd, ni) < the current ksel-th entry
     __device__ __forceinline__ void insert(int ksel, double nd, int ni) {
@@ -144,6 +162,7 @@ struct Best {
 
 // Large-K variant: arrays in local memory, dynamic loops.
 struct BestDyn {
+    static constexpr int kMax = HP_MAX_K;
     double d[HP_MAX_K];
     int i[HP_MAX_K];
     __device__ void init() {
@@ -160,6 +179,7 @@ struct BestDyn {
     __device__ void for_each(int ksel, F f) const {
         for (int b = 0; b < ksel; b++) f(d[b], i[b]);
     }
+    __device__ void insert_full(double nd, int ni) { insert(HP_MAX_K, nd, ni); }
     __device__ void insert(int ksel, double nd, int ni) {
         int b = ksel - 1;
         while (b > 0 && kless(nd, ni, d[b - 1], i[b - 1])) {
@@ -211,6 +231,8 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
     best.init();
     double kd = CUDART_INF;
     int ki = INT_MAX;
+    constexpr int kMaxK = BestT::kMax;
+    const bool full = ksel == kMaxK;
     if (fast) {
         // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
         int l = j, r = j + 1;
@@ -236,8 +258,14 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
             const double d2 = dadd(lb, dmul(di, di));
             evals++;
             if (kless(d2, i, kd, ki)) {
-                best.insert(ksel, d2, i);
-                best.kth(ksel, kd, ki);
+                if (full) {
+                    best.insert_full(d2, i);
+                    kd = best.d[kMaxK - 1];
+                    ki = best.i[kMaxK - 1];
+                } else {
+                    best.insert(ksel, d2, i);
+                    best.kth(ksel, kd, ki);
+                }
             }
         }
     } else {
