@@ -284,10 +284,23 @@ struct FillSmem {
     int64_t off[kGroupMax];
 };
 
+template <int kCap>
+struct SortSmem;
+template <int kCap, int kT>
+__device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int* __restrict__ sid,
+                             const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
+                             double* __restrict__ gd);
+constexpr int kSortSmall = 2048;
+
+// Fill + sort: stream a group's rows, append accepted pairs (unsorted) to the
+// rays' scratch segments, then immediately sort the group's rays with
+// q <= kSortSmall from the scratch (still L2-resident) into the outputs.
+// Longer rays are left to k_query_sort.
 __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
                                                          int64_t m, const int64_t* __restrict__ off,
-                                                         int64_t* __restrict__ out_id, double* __restrict__ out_t,
-                                                         double* __restrict__ out_d) {
+                                                         int* __restrict__ sc_id, double* __restrict__ sc_t,
+                                                         double* __restrict__ sc_d, int64_t* __restrict__ out_id,
+                                                         double* __restrict__ out_t, double* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char dyn[];
     FillSmem& S = *reinterpret_cast<FillSmem*>(dyn);
     const int s = 2 * pad + 1;
@@ -329,9 +342,9 @@ __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int6
                 const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
                 if (cls == 1) {
                     const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
-                    out_t[pos] = t;
-                    out_d[pos] = sqrt(d2);
-                    out_id[pos] = S.pid[buf][k - c0];
+                    sc_t[pos] = t;
+                    sc_d[pos] = sqrt(d2);
+                    sc_id[pos] = S.pid[buf][k - c0];
                 }
                 __syncwarp();
                 if (lane_id() == 0) S.fill[g] += __popc(b);
@@ -339,6 +352,13 @@ __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int6
             },
             [&](int, int) {});
         __syncthreads();
+        for (int g = 0; g < G; g++) {
+            const int64_t o = off[r0 + g];
+            const int64_t q = off[r0 + g + 1] - o;
+            if (q < 1 || q > kSortSmall) continue;
+            sort_segment<kSortSmall, kThreads>(*reinterpret_cast<SortSmem<kSortSmall>*>(dyn), int(q), sc_t + o,
+                                               sc_id + o, sc_d + o, out_id + o, out_t + o, out_d + o);
+        }
     }
 }
 
@@ -395,13 +415,13 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
 // buckets are ordered; each element's final position is its bucket start
 // plus its exact (t, id) rank among the (few) members of its bucket.
 template <int kCap, int kT>
-__device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int64_t* __restrict__ sid,
+__device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int* __restrict__ sid,
                              const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
                              double* __restrict__ gd) {
     const int tid = threadIdx.x;
     for (int e = tid; e < q; e += kT) {
         F.t[e] = st[e];
-        F.id[e] = int(sid[e]);
+        F.id[e] = sid[e];
     }
     if (q <= 64) {
         __syncthreads();
@@ -509,7 +529,6 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
     __syncthreads();
 }
 
-constexpr int kSortSmall = 2048;
 constexpr int kSortLarge = 8192;
 constexpr int kSortLargeThreads = 512;
 
@@ -521,7 +540,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q < 1 ? -1 : (q <= kSortSmall ? 0 : (q <= kSortLarge ? 1 : 2));
+            cls = q <= kSortSmall ? -1 : (q <= kSortLarge ? 1 : 2);  // small rays: sorted by k_query_fill
         }
 #pragma unroll
         for (int c = 0; c < 3; c++) {  // warp-aggregated append
@@ -541,7 +560,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
 template <int kCap, int kT>
 __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int* __restrict__ list,
                                                    const int* __restrict__ list_n, double* __restrict__ st,
-                                                   int64_t* __restrict__ sid, double* __restrict__ sd,
+                                                   int* __restrict__ sid, double* __restrict__ sd,
                                                    int64_t* __restrict__ out_id, double* __restrict__ out_t,
                                                    double* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char dyn[];
@@ -556,7 +575,7 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
         } else {
             double* tt = st + o;
             double* dd = sd + o;
-            int64_t* ii = sid + o;
+            int* ii = sid + o;
             block_bitonic_sort(
                 q, [&](int64_t a, int64_t b) { return key_less(tt[a], ii[a], tt[b], ii[b]); },
                 [&](int64_t a, int64_t b) {
@@ -566,7 +585,7 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
                     x = dd[a];
                     dd[a] = dd[b];
                     dd[b] = x;
-                    const int64_t y = ii[a];
+                    const int y = ii[a];
                     ii[a] = ii[b];
                     ii[b] = y;
                 });
@@ -580,6 +599,9 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
         }
     }
 }
+
+constexpr size_t kFillSmemBytes =
+    sizeof(FillSmem) > sizeof(SortSmem<kSortSmall>) ? sizeof(FillSmem) : sizeof(SortSmem<kSortSmall>);
 
 template <class K>
 int set_smem(K kernel, size_t bytes) {
@@ -630,13 +652,13 @@ unsigned group_grid(int64_t m, int per_sm) {
 
 using namespace hp;
 
-static void carve_fill(Carver& c, int64_t m, int64_t total, int** lists, int** counts, double** st,
-                       int64_t** sid, double** sd) {
+static void carve_fill(Carver& c, int64_t m, int64_t total, int** lists, int** counts, double** st, int** sid,
+                       double** sd) {
     c.take<char>(scan_workspace_bytes(m + 1));
     *lists = c.take<int>(3 * (m > 0 ? m : 1));
     *counts = c.take<int>(64);
     *st = c.take<double>(total > 0 ? total : 1);
-    *sid = c.take<int64_t>(total > 0 ? total : 1);
+    *sid = c.take<int>(total > 0 ? total : 1);
     *sd = c.take<double>(total > 0 ? total : 1);
 }
 
@@ -647,7 +669,7 @@ extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t total, s
     int* l;
     int* cn;
     double *st, *sd;
-    int64_t* sid;
+    int* sid;
     carve_fill(c, m, total, &l, &cn, &st, &sid, &sd);
     *bytes = c.used + 256;
     (void)pad;
@@ -698,7 +720,7 @@ extern "C" int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64
     int* lists;
     int* counts;
     double *st, *sd;
-    int64_t* sid;
+    int* sid;
     carve_fill(cv, m, total, &lists, &counts, &st, &sid, &sd);
     if (!cv.ok()) {
         set_error("hp_query_fill: workspace too small");
@@ -709,15 +731,14 @@ extern "C" int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64
     const QCam QC = make_qcam(cam);
     static bool attr = false;
     if (!attr) {
-        HP_TRY(set_smem(k_query_fill, sizeof(FillSmem)));
-        HP_TRY(set_smem(k_query_sort<kSortSmall, kThreads>, sizeof(SortSmem<kSortSmall>)));
+        HP_TRY(set_smem(k_query_fill, kFillSmemBytes));
         HP_TRY(set_smem(k_query_sort<kSortLarge, kSortLargeThreads>, sizeof(SortSmem<kSortLarge>)));
         attr = true;
     }
     {
         TimedSpan ts("k_query_fill", s);
-        k_query_fill<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m,
-                                                                          offsets, sid, st, sd);
+        k_query_fill<<<group_grid(m, 4), kThreads, kFillSmemBytes, s>>>(layout, padded_w, int(pad), R, QC, m,
+                                                                        offsets, sid, st, sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_fill");
     }
     TimedSpan ts("k_query_sort", s);
@@ -725,9 +746,6 @@ extern "C" int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, counts);
     HP_CHECK_LAUNCH("k_sort_classes");
-    k_query_sort<kSortSmall, kThreads><<<kNumSMs * 4, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
-        offsets, lists, counts, st, sid, sd, ids, t_proj, dist_perp);
-    HP_CHECK_LAUNCH("k_query_sort<small>");
     k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs, kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
         offsets, lists + m, counts + 1, st, sid, sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
