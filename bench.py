@@ -341,10 +341,13 @@ def run_e2e(args, w, r0, r1):
     import torch
 
     from paper_2404_14044_b200 import pipeline
-    from paper_2404_14044_b200.cloud import PointCloud
     m = r1 - r0
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    cloud = PointCloud(w["cloud"].positions, w["cloud"].colors)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+
+    class PinnedCloud:  # PointCloud-like view over pinned host tensors
+        positions = pin(w["cloud"].positions)
+        colors = pin(w["cloud"].colors)
+    cloud = PinnedCloud()
     host = dict(pixels=pin(w["pixels"][r0:r1]), dirs=pin(w["dirs"][r0:r1]),
                 t_near=pin(w["t_near"][r0:r1]), t_far=pin(w["t_far"][r0:r1]))
     times, out = [], None
@@ -357,7 +360,8 @@ def run_e2e(args, w, r0, r1):
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     sec = statistics.mean(times)
-    h2d = (cloud.positions.nbytes + cloud.colors.nbytes + 16 * m + 24 * m + 8 * m + 8 * m + 8 * m)
+    h2d = (cloud.positions.numel() * 8 + cloud.colors.numel() * 8 + 16 * m + 24 * m + 8 * m + 8 * m
+           + 8 * m)
     d2h = sum(int(x.nbytes) for x in out)
     return {"value": m / sec, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": d2h, "api": "paper_2404_14044_b200.pipeline.search_and_sample "

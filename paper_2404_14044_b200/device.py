@@ -11,7 +11,6 @@ Q after the query count pass, R after the sampler), as in the two-phase C ABI.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -62,28 +61,36 @@ def camera_struct(camera) -> _lib.Camera:
     return c
 
 
-@dataclass
 class DeviceIndex:
     """Hash index in HBM: the reference's HashIndex arrays plus the row-major
-    query layout (origin-relative fp64 coordinates, int32 ids, row pointers)."""
+    query layout (origin-relative fp64 coordinates, int32 ids, row pointers,
+    fp32 filter copy).  Arrays are allocated with capacity n; N_in is read
+    from the device only when first needed (no synchronisation in build)."""
 
-    camera: object
-    pad: int
-    padded_width: int
-    padded_height: int
-    n_in: int
-    table_start: torch.Tensor   # int64 [P]
-    table_count: torch.Tensor   # int64 [P]
-    reordered_ids: torch.Tensor  # int64 [N_in]
-    slot_x: torch.Tensor
-    slot_y: torch.Tensor
-    slot_z: torch.Tensor
-    row_ptr: torch.Tensor       # int32 [P+1]
-    rel_x: torch.Tensor
-    rel_y: torch.Tensor
-    rel_z: torch.Tensor
-    point_id: torch.Tensor      # int32
-    relf: torch.Tensor          # float32 [N_in, 4]: filter copy (x, y, z, error budget)
+    def __init__(self, camera, pad, padded_width, padded_height, n_in_dev, table_start, table_count,
+                 reordered_ids, slot_x, slot_y, slot_z, row_ptr, rel_x, rel_y, rel_z, point_id, relf,
+                 n_in=None):
+        self.camera = camera
+        self.pad = pad
+        self.padded_width = padded_width
+        self.padded_height = padded_height
+        self._n_in_dev = n_in_dev
+        self._n_in = n_in
+        self.table_start, self.table_count = table_start, table_count
+        self._rid, self._sx, self._sy, self._sz = reordered_ids, slot_x, slot_y, slot_z
+        self.row_ptr, self.rel_x, self.rel_y, self.rel_z = row_ptr, rel_x, rel_y, rel_z
+        self.point_id, self.relf = point_id, relf
+
+    @property
+    def n_in(self) -> int:
+        if self._n_in is None:
+            self._n_in = int(self._n_in_dev.item())
+        return self._n_in
+
+    reordered_ids = property(lambda self: self._rid[: self.n_in])
+    slot_x = property(lambda self: self._sx[: self.n_in])
+    slot_y = property(lambda self: self._sy[: self.n_in])
+    slot_z = property(lambda self: self._sz[: self.n_in])
 
     def layout(self) -> _lib.Layout:
         return _lib.Layout(_ptr(self.row_ptr), _ptr(self.rel_x), _ptr(self.rel_y),
@@ -122,10 +129,8 @@ def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
                             _ptr(sx), _ptr(sy), _ptr(sz), L, _ptr(n_in_d), _ptr(ws), nb.value,
                             _stream()))
     _mark("build.kernels")
-    n_in = int(n_in_d.item()) if n > 0 else 0
-    return DeviceIndex(camera, pad, wp, hp, n_in, ts, tc, rid[:n_in], sx[:n_in], sy[:n_in],
-                       sz[:n_in], row_ptr, rx[:max(n_in, 1)], ry[:max(n_in, 1)],
-                       rz[:max(n_in, 1)], pid[:max(n_in, 1)], rf[:max(n_in, 1)])
+    return DeviceIndex(camera, pad, wp, hp, n_in_d, ts, tc, rid, sx, sy, sz, row_ptr, rx, ry, rz,
+                       pid, rf, n_in=0 if n == 0 else None)
 
 
 def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered_ids, camera,
@@ -150,8 +155,8 @@ def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered
     _lib.check(lib.hp_layout_from_table(_ptr(table_start), _ptr(table_count), _ptr(slot_x),
                                         _ptr(slot_y), _ptr(slot_z), _ptr(reordered_ids), n_in, wp,
                                         hp, origin, L, _ptr(ws), nb.value, _stream()))
-    return DeviceIndex(camera, pad, wp, hp, n_in, table_start, table_count, reordered_ids, slot_x,
-                       slot_y, slot_z, row_ptr, rx, ry, rz, pid, rf)
+    return DeviceIndex(camera, pad, wp, hp, None, table_start, table_count, reordered_ids, slot_x,
+                       slot_y, slot_z, row_ptr, rx, ry, rz, pid, rf, n_in=n_in)
 
 
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
@@ -220,9 +225,7 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     total = int(ids.numel())
     want = colors is not None
     p = sampler_params(cfg, want, exact_t_end)
-    stats = torch.empty(2, dtype=torch.int64, device=dev)
-    _lib.check(lib.hp_csr_stats(_ptr(offsets), m, _ptr(stats), _stream()))
-    max_q = int(stats[1].item()) if m > 0 else 0
+    max_q = 0  # the device sampler needs no per-length scratch
     cap = max(SAMPLE_STAGE_PER_RAY * m, 1 << 16)
     nb = c_size(0)
     _lib.check(lib.hp_sample_workspace_bytes(m, total, max_q, cap, ctypes.byref(p),

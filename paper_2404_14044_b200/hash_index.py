@@ -97,14 +97,14 @@ class HashIndex:
     reference are copied to the host lazily, once.
     """
 
-    __slots__ = ("points", "camera", "config", "pad", "point_touches", "device", "_host")
+    __slots__ = ("points", "camera", "config", "pad", "_touch_n", "device", "_host")
 
     def __init__(self, points, camera, config, dev: device.DeviceIndex):
         object.__setattr__(self, "points", points)
         object.__setattr__(self, "camera", camera)
         object.__setattr__(self, "config", config)
         object.__setattr__(self, "pad", int(dev.pad))
-        object.__setattr__(self, "point_touches", int(points.count) + 2 * int(dev.n_in))
+        object.__setattr__(self, "_touch_n", int(points.count))
         object.__setattr__(self, "device", dev)
         object.__setattr__(self, "_host", {})
 
@@ -119,6 +119,11 @@ class HashIndex:
                                      .cpu().numpy())
             return host[name]
         raise AttributeError(name)
+
+    @property
+    def point_touches(self) -> int:
+        """Per-point visits of the three build passes: n + 2 N_in (hash_index.py:189)."""
+        return self._touch_n + 2 * int(self.device.n_in)
 
     @property
     def padded_width(self) -> int:

@@ -78,20 +78,36 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
                       exact_t_end: bool = True):
     """Host arrays in, host arrays out: build the index for ``camera``, query
     the rays and run primary-surface sampling.  Returns the numpy 9-tuple of
-    ``sample_batch_arrays`` (reference sampler.py:196-217)."""
+    ``sample_batch_arrays`` (reference sampler.py:196-217).
+
+    Inputs may be numpy arrays or (preferably pinned) CPU torch tensors.  The
+    device build is enqueued first; the host-side slopes (numpy, bit-identical
+    to the reference's ``radius_slopes``) are computed while it runs; results
+    come back through pinned buffers with one synchronisation.
+    """
     dev = torch.device("cuda", torch.cuda.current_device())
-    pixels = np.ascontiguousarray(pixels, dtype=np.int64).reshape(-1, 2)
-    m = pixels.shape[0]
-    slopes = radius_slopes(camera, pixels, search_cfg.kernel_radius, search_cfg.use_approx_radius)
 
-    def up(a, dt, shape=None):
-        t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
-        return t.to(dev, non_blocking=True) if shape is None else t.to(dev).view(*shape)
+    def up(a, dt):
+        if isinstance(a, torch.Tensor):
+            return a.to(device=dev, dtype=dt, non_blocking=True)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt, non_blocking=True)
 
-    xyz = up(cloud.positions, np.float64)
-    col = up(cloud.colors, np.float64) if (with_colors and cloud.colors is not None) else None
-    fr = frame_device(xyz, col, camera, search_cfg, up(pixels, np.int64), up(dirs, np.float64),
-                      up(np.broadcast_to(t_near, (m,)), np.float64),
-                      up(np.broadcast_to(t_far, (m,)), np.float64), up(slopes, np.float64),
-                      sampler_cfg, exact_t_end)
-    return tuple(x.cpu().numpy() for x in fr.samples)
+    xyz = up(cloud.positions, torch.float64)
+    col = up(cloud.colors, torch.float64) if (with_colors and cloud.colors is not None) else None
+    idx = device.build(xyz, camera, search_cfg.pad)          # async on the stream
+    px_host = pixels.numpy() if isinstance(pixels, torch.Tensor) else np.asarray(pixels)
+    px_host = np.ascontiguousarray(px_host, dtype=np.int64).reshape(-1, 2)
+    m = px_host.shape[0]
+    slopes = radius_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius)
+    pix_d = up(pixels, torch.int64).view(m, 2)
+    dirs_d = up(dirs, torch.float64).view(m, 3)
+    tn = up(np.broadcast_to(np.asarray(t_near, np.float64), (m,)), torch.float64)
+    tf = up(np.broadcast_to(np.asarray(t_far, np.float64), (m,)), torch.float64)
+    sl = up(slopes, torch.float64)
+    q = device.query(idx, pix_d, dirs_d, tn, tf, sl)
+    s = device.sample(q[0], q[1], q[2], q[3], sl, sampler_cfg or SamplerConfig(), col, exact_t_end)
+    outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
+    for o, x in zip(outs, s):
+        o.copy_(x, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return tuple(o.numpy() for o in outs)
