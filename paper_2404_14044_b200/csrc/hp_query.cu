@@ -373,8 +373,9 @@ template <int kCap>
 struct SortSmem {
     double t[kCap];
     int id[kCap];           // point ids < 2^31 (hp_build)
-    unsigned int bk[kCap];  // fine bucket << 16 | local index
+    unsigned int bk[2 * kCap];  // fine bucket << 16 | local index; later the sorted dist (8 B each)
     unsigned short lst[kCap];
+    unsigned short perm[kCap];
     int hist[kCap + 1];
     int chist[kCoarse + 1];
     unsigned long long tmin, tmax;
@@ -431,10 +432,29 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
             dv[k] = sd[e];
         }
     }
-    auto emit = [&](int k, int e, int pos) {
-        gt[pos] = F.t[e];
-        gid[pos] = F.id[e];
-        gd[pos] = dv[k];
+    // final (coalesced) write: position p takes element perm[p]; the dist
+    // values are parked at their final position in `dpos` (aliases the bucket
+    // arrays, dead by then)
+    double* dpos = reinterpret_cast<double*>(F.bk);
+    int pos[kPer];
+    auto finish = [&]() {
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPer; k++) {
+            const int e = tid + k * kT;
+            if (e < q) {
+                F.perm[pos[k]] = (unsigned short)e;
+                dpos[pos[k]] = dv[k];
+            }
+        }
+        __syncthreads();
+        for (int p = tid; p < q; p += kT) {
+            const int e = F.perm[p];
+            gt[p] = F.t[e];
+            gid[p] = F.id[e];
+            gd[p] = dpos[p];
+        }
+        __syncthreads();
     };
     if (q <= 64) {
         __syncthreads();
@@ -446,9 +466,9 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
             const int ie = F.id[e];
             int rank = 0;
             for (int j = 0; j < q; j++) rank += key_less(F.t[j], F.id[j], te, ie);
-            emit(k, e, rank);
+            pos[k] = rank;
         }
-        __syncthreads();
+        finish();
         return;
     }
     const int nb = q;  // fine buckets
@@ -554,9 +574,9 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
                 rank += key_less(F.t[o], F.id[o], te, ie);
             }
         }
-        emit(k, e, bs + rank);
+        pos[k] = bs + rank;
     }
-    __syncthreads();
+    finish();
 }
 
 constexpr int kSortLarge = 8192;
