@@ -372,8 +372,9 @@ constexpr int kCoarse = 256;
 template <int kCap>
 struct SortSmem {
     double t[kCap];
+    double d[kCap];         // dist, staged with t/id (no gather at the end)
     int id[kCap];           // point ids < 2^31 (hp_build)
-    unsigned int bk[2 * kCap];  // fine bucket << 16 | local index; later the sorted dist (8 B each)
+    unsigned int bk[kCap];  // fine bucket << 16 | local index
     unsigned short lst[kCap];
     unsigned short perm[kCap];
     int hist[kCap + 1];
@@ -418,165 +419,118 @@ template <int kCap, int kT>
 __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int* __restrict__ sid,
                              const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
                              double* __restrict__ gd) {
-    // Thread tid owns elements e = tid + k*kT: it keeps their dist in
-    // registers and writes all three outputs at the element's final rank.
-    constexpr int kPer = (kCap + kT - 1) / kT;
     const int tid = threadIdx.x;
-    double dv[kPer];
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int e = tid + k * kT;
-        if (e < q) {
-            F.t[e] = st[e];
-            F.id[e] = sid[e];
-            dv[k] = sd[e];
-        }
+    for (int e = tid; e < q; e += kT) {
+        F.t[e] = st[e];
+        F.d[e] = sd[e];
+        F.id[e] = sid[e];
     }
-    // final (coalesced) write: position p takes element perm[p]; the dist
-    // values are parked at their final position in `dpos` (aliases the bucket
-    // arrays, dead by then)
-    double* dpos = reinterpret_cast<double*>(F.bk);
-    int pos[kPer];
-    auto finish = [&]() {
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kPer; k++) {
-            const int e = tid + k * kT;
-            if (e < q) {
-                F.perm[pos[k]] = (unsigned short)e;
-                dpos[pos[k]] = dv[k];
-            }
-        }
-        __syncthreads();
-        for (int p = tid; p < q; p += kT) {
-            const int e = F.perm[p];
-            gt[p] = F.t[e];
-            gid[p] = F.id[e];
-            gd[p] = dpos[p];
-        }
-        __syncthreads();
-    };
     if (q <= 64) {
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kPer; k++) {
-            const int e = tid + k * kT;
-            if (e >= q) continue;
+        for (int e = tid; e < q; e += kT) {
             const double te = F.t[e];
             const int ie = F.id[e];
             int rank = 0;
-            for (int j = 0; j < q; j++) rank += key_less(F.t[j], F.id[j], te, ie);
-            pos[k] = rank;
+            for (int k = 0; k < q; k++) rank += key_less(F.t[k], F.id[k], te, ie);
+            F.perm[rank] = (unsigned short)e;
         }
-        finish();
-        return;
-    }
-    const int nb = q;  // fine buckets
-    if (tid == 0) {
-        F.tmin = ~0ull;
-        F.tmax = 0ull;
-    }
-    for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
-    for (int k = tid; k <= nb; k += kT) F.hist[k] = 0;
-    __syncthreads();
-    unsigned long long lmin = ~0ull, lmax = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int e = tid + k * kT;
-        if (e < q) {
+        __syncthreads();
+    } else {
+        const int nb = q;  // fine buckets
+        if (tid == 0) {
+            F.tmin = ~0ull;
+            F.tmax = 0ull;
+        }
+        for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
+        for (int k = tid; k <= nb; k += kT) F.hist[k] = 0;
+        __syncthreads();
+        unsigned long long lmin = ~0ull, lmax = 0;
+        for (int e = tid; e < q; e += kT) {
             const unsigned long long kk = okey(F.t[e]);
             lmin = lmin < kk ? lmin : kk;
             lmax = lmax > kk ? lmax : kk;
         }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long x = __shfl_xor_sync(0xffffffffu, lmin, o);
-        const unsigned long long y = __shfl_xor_sync(0xffffffffu, lmax, o);
-        lmin = lmin < x ? lmin : x;
-        lmax = lmax > y ? lmax : y;
-    }
-    if (lane_id() == 0) {
-        atomicMin(&F.tmin, lmin);
-        atomicMax(&F.tmax, lmax);
-    }
-    __syncthreads();
-    const double tlo = from_okey(F.tmin), thi = from_okey(F.tmax);
-    const double span = dsub(thi, tlo);
-    // capped so that 0 * scale stays 0 when the span is tiny
-    const double cscale = span > 0.0 ? fmin(__ddiv_rn(double(kCoarse), span), DBL_MAX) : 0.0;
-    auto coarse_x = [&](double t) { return fmin(dmul(dsub(t, tlo), cscale), double(kCoarse)); };
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int e = tid + k * kT;
-        const bool in = e < q;
-        const int b = in ? min(int(coarse_x(F.t[e])), kCoarse - 1) : -1;
-        const unsigned act = __ballot_sync(0xffffffffu, in);
-        if (in) {
-            const unsigned peers = __match_any_sync(act, b);
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, lmin, o);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, lmax, o);
+            lmin = lmin < x ? lmin : x;
+            lmax = lmax > y ? lmax : y;
+        }
+        if (lane_id() == 0) {
+            atomicMin(&F.tmin, lmin);
+            atomicMax(&F.tmax, lmax);
+        }
+        __syncthreads();
+        const double tlo = from_okey(F.tmin), thi = from_okey(F.tmax);
+        const double span = dsub(thi, tlo);
+        // capped so that 0 * scale stays 0 when the span is tiny
+        const double cscale = span > 0.0 ? fmin(__ddiv_rn(double(kCoarse), span), DBL_MAX) : 0.0;
+        auto coarse_x = [&](double t) { return fmin(dmul(dsub(t, tlo), cscale), double(kCoarse)); };
+        for (int e = tid; e < q; e += kT) {
+            const int b = min(int(coarse_x(F.t[e])), kCoarse - 1);
+            const unsigned peers = __match_any_sync(__activemask(), b);
             if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.chist[b], __popc(peers));
         }
-    }
-    __syncthreads();
-    // coarse prefix counts -> first fine bucket of each coarse bin
-    if (tid < 32) {
-        int run = 0;
-        for (int c0 = 0; c0 < kCoarse; c0 += 32) {
-            const int v = F.chist[c0 + tid];
-            const int inc = warp_incl_scan(v);
-            F.chist[c0 + tid] = int((int64_t(run + inc - v) * nb) / q);
-            run += __shfl_sync(0xffffffffu, inc, 31);
-        }
-        if (tid == 0) F.chist[kCoarse] = nb;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int e = tid + k * kT;
-        if (e >= q) continue;
-        const double x = coarse_x(F.t[e]);
-        const int b = min(int(x), kCoarse - 1);
-        const int f0 = F.chist[b], width = F.chist[b + 1] - f0;
-        int f = f0;
-        if (width > 1) {
-            // x - b is exact (Sterbenz) and in [0, 1]
-            const int off = int(dmul(dsub(x, double(b)), double(width)));
-            f += min(off, width - 1);
-        }
-        f = min(f, nb - 1);
-        const int li = atomicAdd(&F.hist[f], 1);
-        F.bk[e] = (unsigned(f) << 16) | unsigned(li);
-    }
-    __syncthreads();
-    block_scan_inplace<kPer>(F.hist, nb, F.scan_sh);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int e = tid + k * kT;
-        if (e >= q) continue;
-        const unsigned bk = F.bk[e];
-        F.lst[F.hist[bk >> 16] + (bk & 0xffffu)] = (unsigned short)e;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int e = tid + k * kT;
-        if (e >= q) continue;
-        const unsigned bk = F.bk[e];
-        const int bs = F.hist[bk >> 16];
-        const int be = (int(bk >> 16) + 1 < nb) ? F.hist[(bk >> 16) + 1] : q;
-        int rank = 0;
-        if (be - bs > 1) {
-            const double te = F.t[e];
-            const int ie = F.id[e];
-            for (int j = bs; j < be; j++) {
-                const int o = F.lst[j];
-                rank += key_less(F.t[o], F.id[o], te, ie);
+        __syncthreads();
+        // coarse prefix counts -> first fine bucket of each coarse bin
+        if (tid < 32) {
+            int run = 0;
+            for (int c0 = 0; c0 < kCoarse; c0 += 32) {
+                const int v = F.chist[c0 + tid];
+                const int inc = warp_incl_scan(v);
+                F.chist[c0 + tid] = int((int64_t(run + inc - v) * nb) / q);
+                run += __shfl_sync(0xffffffffu, inc, 31);
             }
+            if (tid == 0) F.chist[kCoarse] = nb;
         }
-        pos[k] = bs + rank;
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
+            const double x = coarse_x(F.t[e]);
+            const int b = min(int(x), kCoarse - 1);
+            const int f0 = F.chist[b], width = F.chist[b + 1] - f0;
+            int f = f0;
+            if (width > 1) {
+                // x - b is exact (Sterbenz) and in [0, 1]
+                const int off = int(dmul(dsub(x, double(b)), double(width)));
+                f += min(off, width - 1);
+            }
+            f = min(f, nb - 1);
+            const int li = atomicAdd(&F.hist[f], 1);
+            F.bk[e] = (unsigned(f) << 16) | unsigned(li);
+        }
+        __syncthreads();
+        block_scan_inplace<(kCap + kT - 1) / kT>(F.hist, nb, F.scan_sh);
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
+            const unsigned bk = F.bk[e];
+            F.lst[F.hist[bk >> 16] + (bk & 0xffffu)] = (unsigned short)e;
+        }
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
+            const unsigned bk = F.bk[e];
+            const int bs = F.hist[bk >> 16];
+            const int be = (int(bk >> 16) + 1 < nb) ? F.hist[(bk >> 16) + 1] : q;
+            int rank = 0;
+            if (be - bs > 1) {
+                const double te = F.t[e];
+                const int ie = F.id[e];
+                for (int k = bs; k < be; k++) {
+                    const int o = F.lst[k];
+                    rank += key_less(F.t[o], F.id[o], te, ie);
+                }
+            }
+            F.perm[bs + rank] = (unsigned short)e;
+        }
+        __syncthreads();
     }
-    finish();
+    for (int p = tid; p < q; p += kT) {
+        const int e = F.perm[p];
+        gt[p] = F.t[e];
+        gid[p] = F.id[e];
+        gd[p] = F.d[e];
+    }
+    __syncthreads();
 }
 
 constexpr int kSortLarge = 8192;
@@ -787,7 +741,7 @@ extern "C" int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64
     }
     {
         TimedSpan ts("k_query_fill", s);
-        k_query_fill<<<group_grid(m, 4), kThreads, kFillSmemBytes, s>>>(layout, padded_w, int(pad), R, QC, m,
+        k_query_fill<<<group_grid(m, 3), kThreads, kFillSmemBytes, s>>>(layout, padded_w, int(pad), R, QC, m,
                                                                         offsets, sid, st, sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_fill");
     }
