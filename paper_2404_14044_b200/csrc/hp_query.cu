@@ -533,7 +533,7 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
     __syncthreads();
 }
 
-constexpr int kSortLarge = 8192;
+constexpr int kSortLarge = 4096;
 constexpr int kSortLargeThreads = 512;
 
 // Size classes of rays to sort: [1, kSortSmall], (kSortSmall, kSortLarge], above.
