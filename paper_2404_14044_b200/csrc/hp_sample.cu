@@ -329,15 +329,6 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
 // then bounded below in fp32 (argument rounded up, result scaled by
 // 1 - 2^-20 against expf's 2-ulp error).  Every later operation is monotone,
 // so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
-// u >= fl(1 - alpha) from an upper bound `sum` of the reference's udf sum.
-__device__ __forceinline__ double bound_from_sum(double sum, int ksel, const Params& P) {
-    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
-    const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
-    const float e = expf(-__double2float_ru(y));
-    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
-    return dsub(1.0, a_lo);
-}
-
 __device__ double bound_factor(const RayView& V, int q, int j, int jstar, double slope, const Params& P) {
     const double tj = V.t(j);
     const double rj = dmul(slope, tj);
@@ -357,7 +348,11 @@ __device__ double bound_factor(const RayView& V, int q, int j, int jstar, double
         sum = dadd(sum, dadd(dsub(tj, V.t(i)), di));
         found++;
     }
-    return bound_from_sum(sum, ksel, P);
+    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
+    const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
+    const float e = expf(-__double2float_ru(y));
+    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
+    return dsub(1.0, a_lo);
 }
 
 // Warp: first j in [0, q) with pred(j) (monotone false..true); q if none.
@@ -464,36 +459,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
         bool seq = false;
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
-            double u = 1.0;
-            {
-                // Chunk-shared bound: when use_el is the same for the whole chunk,
-                // the first ksel pool members among the chunk's own candidates
-                // (pool taken at r_{c0}, the chunk's smallest radius) belong to
-                // every lane's pool, and by the triangle inequality
-                //   |t_i - t_j| <= |t_i - t_m| + |t_m - t_j|
-                // udf_j <= (S + ksel |t_m - t_j|) / ksel with S = sum_i (|t_i - t_m| + ds_i).
-                const int cend = min(c0 + 32, q);
-                const bool el0 = c0 >= jstar;
-                bool done = false;
-                if (el0 || cend <= jstar) {
-                    const int ksel = el0 ? P.K : (q < P.K ? q : P.K);
-                    const double tjl = j < q ? V.t(j) : 0.0, dsl = j < q ? V.d(j) : 0.0;
-                    const double rc0 = dmul(slope, V.t(c0));
-                    const bool memb = j < q && (!el0 || dsl <= rc0);
-                    const unsigned mask = __ballot_sync(0xffffffffu, memb);
-                    if (__popc(mask) >= ksel) {
-                        const bool take = memb && __popc(mask & ((1u << lane) - 1)) < ksel;
-                        const double tm = __shfl_sync(0xffffffffu, tjl, __ffs(mask) - 1);
-                        const double S = warp_sum(take ? dadd(fabs(dsub(tjl, tm)), dsl) : 0.0);
-                        if (j < q) {
-                            const double sum = dadd(S, dmul(double(ksel), fabs(dsub(tm, tjl))));
-                            u = bound_from_sum(sum, ksel, P);
-                        }
-                        done = true;
-                    }
-                }
-                if (!done && j < q) u = bound_factor(V, q, j, jstar, slope, P);
-            }
+            const double u = j < q ? bound_factor(V, q, j, jstar, slope, P) : 1.0;
             nbound += 32;
             const int n = min(32, q - c0);
             if (!seq) {
