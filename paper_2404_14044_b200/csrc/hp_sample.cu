@@ -194,7 +194,7 @@ struct BestDyn {
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
-constexpr int kWin = 256;  // candidates of a ray staged in shared memory (per warp)
+constexpr int kWin = 384;  // candidates of a ray staged in shared memory (per warp)
 
 // The ray's t / ds: the first kWin candidates from the warp's shared-memory
 // window, the rest from global memory (read-only path).
@@ -611,7 +611,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
 }
 
 template <class BestT>
-__global__ void __launch_bounds__(kThreads, 4) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
+__global__ void __launch_bounds__(kThreads, 3) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
                                                      const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
                                                      const int64_t* __restrict__ r_off, Outputs O) {
     extern __shared__ __align__(16) unsigned char dyn[];

@@ -132,10 +132,13 @@ def retain(candidates: list, config: SamplerConfig) -> list:
 
 
 # ---------------------------------------------------------------- device path
+_NP = {torch.int64: np.int64, torch.float64: np.float64}
+
+
 def _to_dev(a, dt, dev):
     if isinstance(a, torch.Tensor):
         return a.to(device=dev, dtype=dt).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=_NP[dt])).to(dev)
 
 
 def sample_batch_device(offsets, ids, t_proj, dist_perp, slopes, sampler_cfg: SamplerConfig,
