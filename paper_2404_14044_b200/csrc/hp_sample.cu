@@ -234,12 +234,27 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
     constexpr int kMaxK = BestT::kMax;
     const bool full = ksel == kMaxK;
     if (fast) {
-        // outward from j in t order, both sides per step (two independent
-        // chains); a side stops once (t_i - t_j)^2 > K-th best (later
-        // candidates on that side are at least as far -- rounding is monotone)
-        auto consider = [&](int i, double lb) {
+        // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
+        int l = j, r = j + 1;
+        double tl = tj, tr = r < q ? V.t(r) : 0.0;
+        while (l >= 0 || r < q) {
+            const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
+            int i;
+            double ti;
+            if (go_left) {
+                i = l;
+                ti = tl;
+                if (--l >= 0) tl = V.t(l);
+            } else {
+                i = r;
+                ti = tr;
+                if (++r < q) tr = V.t(r);
+            }
+            const double dt = dsub(ti, tj);
+            const double lb = dmul(dt, dt);
+            if (lb > kd) break;  // the other side is at least as far
             const double di = V.d(i);
-            if (use_el && di > rj) return;
+            if (use_el && di > rj) continue;
             const double d2 = dadd(lb, dmul(di, di));
             evals++;
             if (kless(d2, i, kd, ki)) {
@@ -252,26 +267,6 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
                     best.kth(ksel, kd, ki);
                 }
             }
-        };
-        consider(j, 0.0);  // t_j - t_j = 0 exactly
-        int l = j - 1, r = j + 1;
-        bool lgo = l >= 0, rgo = r < q;
-        while (lgo || rgo) {
-            double lbl = 0.0, lbr = 0.0;
-            if (lgo) {
-                const double dt = dsub(V.t(l), tj);
-                lbl = dmul(dt, dt);
-                lgo = !(lbl > kd);
-            }
-            if (rgo) {
-                const double dt = dsub(V.t(r), tj);
-                lbr = dmul(dt, dt);
-                rgo = !(lbr > kd);
-            }
-            if (lgo) consider(l, lbl);
-            if (rgo) consider(r, lbr);
-            if (lgo) lgo = --l >= 0;
-            if (rgo) rgo = ++r < q;
         }
     } else {
         for (int i = 0; i < q; i++) {  // reference loop (_kernels.py:607-620)
