@@ -668,7 +668,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
 }
 
 template <class BestT>
-__global__ void __launch_bounds__(kThreads) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
+__global__ void __launch_bounds__(kThreads, 3) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
                                                      const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
                                                      const int64_t* __restrict__ r_off, Outputs O) {
     extern __shared__ __align__(16) unsigned char dyn[];
