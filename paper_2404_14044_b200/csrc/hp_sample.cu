@@ -194,8 +194,7 @@ struct BestDyn {
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
-constexpr int kWin = 320;  // candidates of a ray staged in shared memory (per warp)
-constexpr int kSortedBlocks = 8;  // leading 32-blocks kept sorted by (ds, i) (per warp)
+constexpr int kWin = 384;  // candidates of a ray staged in shared memory (per warp)
 
 // The ray's t / ds: the first kWin candidates from the warp's shared-memory
 // window, the rest from global memory (read-only path).
@@ -204,9 +203,6 @@ struct RayView {
     const double* gd;
     const double* wt;
     const double* wd;
-    const double* bds;          // blocks [0, nsb): ds sorted ascending within each block
-    const unsigned short* bidx;  // ... and the candidate index of each entry
-    int nsb;
     __device__ __forceinline__ double t(int i) const { return i < kWin ? wt[i] : __ldg(gt + i); }
     __device__ __forceinline__ double d(int i) const { return i < kWin ? wd[i] : __ldg(gd + i); }
 };
@@ -238,13 +234,28 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
     constexpr int kMaxK = BestT::kMax;
     const bool full = ksel == kMaxK;
     if (fast) {
-        // Blocks of 32 consecutive (in t) candidates, visited outward from
-        // j's block in order of the lower bound (t_edge - t_j)^2; inside a
-        // (ds, i)-sorted block the scan stops once ds^2 (a lower bound of d2)
-        // exceeds the K-th best; blocks beyond the sorted ones are scanned
-        // whole.  Selection by the (d2, i) key makes the visiting order
-        // irrelevant to the result.
-        auto consider = [&](int i, double d2) {
+        // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
+        int l = j, r = j + 1;
+        double tl = tj, tr = r < q ? V.t(r) : 0.0;
+        while (l >= 0 || r < q) {
+            const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
+            int i;
+            double ti;
+            if (go_left) {
+                i = l;
+                ti = tl;
+                if (--l >= 0) tl = V.t(l);
+            } else {
+                i = r;
+                ti = tr;
+                if (++r < q) tr = V.t(r);
+            }
+            const double dt = dsub(ti, tj);
+            const double lb = dmul(dt, dt);
+            if (lb > kd) break;  // the other side is at least as far
+            const double di = V.d(i);
+            if (use_el && di > rj) continue;
+            const double d2 = dadd(lb, dmul(di, di));
             evals++;
             if (kless(d2, i, kd, ki)) {
                 if (full) {
@@ -256,46 +267,6 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
                     best.kth(ksel, kd, ki);
                 }
             }
-        };
-        auto scan_block = [&](int b) {
-            const int e0 = b << 5, e1 = min(e0 + 32, q);
-            if (b < V.nsb) {
-                for (int e = e0; e < e1; e++) {
-                    const double di = V.bds[e];
-                    if (use_el && di > rj) break;
-                    const double di2 = dmul(di, di);
-                    if (di2 > kd) break;
-                    const int i = V.bidx[e];
-                    const double dt = dsub(V.t(i), tj);
-                    consider(i, dadd(dmul(dt, dt), di2));
-                }
-            } else {
-                for (int i = e0; i < e1; i++) {
-                    const double di = V.d(i);
-                    if (use_el && di > rj) continue;
-                    const double dt = dsub(V.t(i), tj);
-                    consider(i, dadd(dmul(dt, dt), dmul(di, di)));
-                }
-            }
-        };
-        const int nblk = (q + 31) >> 5;
-        const int B = j >> 5;
-        scan_block(B);
-        int left = B - 1, right = B + 1;
-        while (left >= 0 || right < nblk) {
-            double lbl = CUDART_INF, lbr = CUDART_INF;
-            if (left >= 0) {
-                const double dt = dsub(V.t((left << 5) + 31), tj);
-                lbl = dmul(dt, dt);
-            }
-            if (right < nblk) {
-                const double dt = dsub(V.t(right << 5), tj);
-                lbr = dmul(dt, dt);
-            }
-            const bool goleft = lbl <= lbr;
-            if (!((goleft ? lbl : lbr) <= kd)) break;
-            if (goleft) scan_block(left--);
-            else scan_block(right++);
         }
     } else {
         for (int i = 0; i < q; i++) {  // reference loop (_kernels.py:607-620)
@@ -410,8 +381,6 @@ __device__ int warp_first_true(int q, Pred pred) {
 
 struct WarpSmem {
     double wt[kWin], wd[kWin];
-    double bds[kSortedBlocks * 32];
-    unsigned short bidx[kSortedBlocks * 32];
     int rj[kRetCap];
     double rudf[kRetCap], ralpha[kRetCap], rw[kRetCap], rcol[kRetCap * 3];
 };
@@ -456,33 +425,7 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
         c0cnt += (dk <= r0);
     }
     const bool fast = __all_sync(0xffffffffu, ok);  // also orders the window stores
-    const int nsb = fast ? min(kSortedBlocks, (min(q, kWin) + 31) >> 5) : 0;
-    for (int b = 0; b < nsb; b++) {  // sort block b by (ds, i): bitonic over the lanes
-        const int e = (b << 5) + lane;
-        double k = e < q ? W.wd[e] : CUDART_INF;
-        int id = e < q ? e : INT_MAX;
-#pragma unroll
-        for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                const double ok2 = __shfl_xor_sync(0xffffffffu, k, stride);
-                const int oid = __shfl_xor_sync(0xffffffffu, id, stride);
-                const bool ascending = (lane & size) == 0;
-                const bool lower = (lane & stride) == 0;
-                const bool take = (lower == ascending) ? kless(ok2, oid, k, id) : kless(k, id, ok2, oid);
-                if (take) {
-                    k = ok2;
-                    id = oid;
-                }
-            }
-        }
-        if (e < q) {
-            W.bds[e] = k;
-            W.bidx[e] = (unsigned short)id;
-        }
-    }
-    __syncwarp();
-    const RayView V{T, DS, W.wt, W.wd, W.bds, W.bidx, nsb};
+    const RayView V{T, DS, W.wt, W.wd};
     int jstar = 0;
     if (fast) {
         if (warp_sum(c0cnt) >= P.K) {
