@@ -203,8 +203,9 @@ struct RayView {
     const double* gd;
     const double* wt;
     const double* wd;
-    __device__ __forceinline__ double t(int i) const { return i < kWin ? wt[i] : __ldg(gt + i); }
-    __device__ __forceinline__ double d(int i) const { return i < kWin ? wd[i] : __ldg(gd + i); }
+    int win;  // staged prefix length (0: everything from global memory)
+    __device__ __forceinline__ double t(int i) const { return i < win ? wt[i] : __ldg(gt + i); }
+    __device__ __forceinline__ double d(int i) const { return i < win ? wd[i] : __ldg(gd + i); }
 };
 
 // Exact udf/alpha (and colour) of candidate j (reference _kernels.py:594-660).
@@ -385,47 +386,38 @@ struct WarpSmem {
     double rudf[kRetCap], ralpha[kRetCap], rw[kRetCap], rcol[kRetCap * 3];
 };
 
-// One ray per warp.  mode 0: stage retained candidates; mode 1: write them
-// directly to the outputs at r_off[ray] (rays whose staging overflowed).
-template <class BestT>
-__device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t ray, int mode, const RayOut& RO,
-                           const Stage& ST, const int64_t* __restrict__ r_off, const Outputs& O) {
+// ---- plan (k_sample_plan): one warp per ray, no shared memory.
+// Fast-path preconditions, j* (first j where use_el holds), and the bound
+// chain: je (retention is decided before je) and whether the reference's
+// transmittance provably underflows to exactly 0.  plan[ray] =
+// (jstar, je, flags: 1 fast | 2 proved_zero, q).
+__device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __restrict__ plan) {
     const int lane = lane_id();
     const int64_t lo = C.off[ray];
     const int q = int(C.off[ray + 1] - lo);
     if (q == 0) {
-        if (mode == 0 && lane == 0) {
-            RO.rcount[ray] = 0;
-            RO.t_end[ray] = 1.0;
-            RO.ray_stage[ray] = 0;
-        }
+        if (lane == 0) plan[ray] = make_int4(0, 0, 0, 0);
         return;
     }
     const double slope = C.slopes[ray];
     const double* T = C.t + lo;
     const double* DS = C.ds + lo;
-    const int64_t* ids_ray = C.ids + lo;
     const double thr = P.eps_mode ? P.eps : P.tau_min;
+    const RayView V{T, DS, nullptr, nullptr, 0};
 
-    // ---- pass over the ray: fast-path preconditions, shared-memory window,
-    // and the count of candidates within r_0 (use_el holds from j = 0 on when
-    // it reaches K, the common case on dense surfaces)
+    // fast-path preconditions + count of candidates within r_0 (use_el holds
+    // from j = 0 when it reaches K, the common case on dense surfaces)
     bool ok = slope >= 0.0 && slope <= DBL_MAX;
     const double r0 = dmul(slope, ldg(T));
     int c0cnt = 0;
 #pragma unroll 4
     for (int k = lane; k < q; k += 32) {
         const double tk = ldg(T + k), dk = ldg(DS + k);
-        if (k < kWin) {
-            W.wt[k] = tk;
-            W.wd[k] = dk;
-        }
         ok &= (fabs(tk) <= DBL_MAX) && (dk >= 0.0) && (dk <= DBL_MAX);
         if (k + 1 < q) ok &= !(ldg(T + k + 1) < tk);
         c0cnt += (dk <= r0);
     }
-    const bool fast = __all_sync(0xffffffffu, ok);  // also orders the window stores
-    const RayView V{T, DS, W.wt, W.wd};
+    const bool fast = __all_sync(0xffffffffu, ok);
     int jstar = 0;
     if (fast) {
         if (warp_sum(c0cnt) >= P.K) {
@@ -442,7 +434,6 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
             });
         }
     }
-
     // ---- 1. bound chain (fast path)
     // Vs bounds the reference's T at the current chunk start.  While it is
     // far from underflow, the chunk's bounds come from a round-up warp prefix
@@ -502,7 +493,47 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
             if (proved_zero || (!P.exact_t_end && je < q)) break;
         }
     }
+    if (lane == 0) {
+        plan[ray] = make_int4(jstar, je, (fast ? 1 : 0) | (proved_zero ? 2 : 0), q);
+        atomicAdd(&g_dbg[5], nbound);
+    }
+}
+
+// One ray per warp (k_sample).  mode 0: stage retained candidates; mode 1:
+// write them directly to the outputs at r_off[ray] (rays whose staging
+// overflowed).  Evaluates the exact region [0, E) given by the plan.
+template <class BestT>
+__device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t ray, int mode, const RayOut& RO,
+                           const Stage& ST, const int64_t* __restrict__ r_off, const Outputs& O,
+                           const int4* __restrict__ plan) {
+    const int lane = lane_id();
+    const int64_t lo = C.off[ray];
+    const int q = int(C.off[ray + 1] - lo);
+    if (q == 0) {
+        if (mode == 0 && lane == 0) {
+            RO.rcount[ray] = 0;
+            RO.t_end[ray] = 1.0;
+            RO.ray_stage[ray] = 0;
+        }
+        return;
+    }
+    const double slope = C.slopes[ray];
+    const double* T = C.t + lo;
+    const double* DS = C.ds + lo;
+    const int64_t* ids_ray = C.ids + lo;
+    const double thr = P.eps_mode ? P.eps : P.tau_min;
+    const int4 pl = plan[ray];
+    const int jstar = pl.x, je = pl.y;
+    const bool fast = pl.z & 1, proved_zero = (pl.z >> 1) & 1;
+    const unsigned long long nbound = 0;
     const int E = (!fast || (P.exact_t_end && !proved_zero)) ? q : je;
+    const int win = min(q, kWin);
+    for (int k = lane; k < win; k += 32) {
+        W.wt[k] = ldg(T + k);
+        W.wd[k] = ldg(DS + k);
+    }
+    __syncwarp();
+    const RayView V{T, DS, W.wt, W.wd, win};
 
     // ---- 2. exact region [0, E): reference compositing and retention
     double Tr = 1.0, exit_T = -1.0;
@@ -610,17 +641,24 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan) {
+    const int64_t warps = int64_t(gridDim.x) * kWarps;
+    for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
+        plan_ray(C, P, ray, plan);
+}
+
 template <class BestT>
 __global__ void __launch_bounds__(kThreads, 3) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
                                                      const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
-                                                     const int64_t* __restrict__ r_off, Outputs O) {
+                                                     const int64_t* __restrict__ r_off, Outputs O,
+                                                     const int4* __restrict__ plan) {
     extern __shared__ __align__(16) unsigned char dyn[];
     WarpSmem* W = reinterpret_cast<WarpSmem*>(dyn);
     const int64_t n = ray_list ? int64_t(*ray_list_n) : C.m;
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t k = int64_t(blockIdx.x) * kWarps + warp_id(); k < n; k += warps) {
         const int64_t ray = ray_list ? int64_t(ray_list[k]) : k;
-        sample_ray<BestT>(W[warp_id()], C, P, ray, mode, RO, ST, r_off, O);
+        sample_ray<BestT>(W[warp_id()], C, P, ray, mode, RO, ST, r_off, O, plan);
     }
 }
 
@@ -676,6 +714,7 @@ __global__ void k_csr_stats(const int64_t* __restrict__ off, int64_t m, int64_t*
 struct SampleWs {
     RayOut ro;
     Stage st;
+    int4* plan;
     void* scan;
 };
 
@@ -693,6 +732,7 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t cap, bool color) {
     w.st.alpha = c.take<double>(cap > 0 ? cap : 1);
     w.st.w = c.take<double>(cap > 0 ? cap : 1);
     w.st.col = color ? c.take<double>(3 * (cap > 0 ? cap : 1)) : nullptr;
+    w.plan = c.take<int4>(m > 0 ? m : 1);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     return w;
 }
@@ -715,7 +755,7 @@ Params to_params(const hp_sampler_params* p) {
 
 template <class BestT>
 int launch_sample(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
-                  const Stage& ST, const int64_t* r_off, const Outputs& O, cudaStream_t s) {
+                  const Stage& ST, const int64_t* r_off, const Outputs& O, int4* plan, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         const cudaError_t e = cudaFuncSetAttribute(k_sample<BestT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -723,18 +763,23 @@ int launch_sample(const Csr& C, const Params& P, int mode, const int* list, cons
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(k_sample)");
         attr = true;
     }
+    if (mode == 0) {
+        TimedSpan ts("k_sample_plan", s);
+        k_sample_plan<<<kNumSMs * 8, kThreads, 0, s>>>(C, P, plan);
+        HP_CHECK_LAUNCH("k_sample_plan");
+    }
     TimedSpan ts(mode == 0 ? "k_sample" : "k_sample_overflow", s);
     k_sample<BestT><<<kSampleGrid, kThreads, sizeof(WarpSmem) * kWarps, s>>>(C, P, mode, list, list_n, RO, ST,
-                                                                             r_off, O);
+                                                                             r_off, O, plan);
     HP_CHECK_LAUNCH("k_sample");
     return HP_OK;
 }
 
 int dispatch_sample(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
-                    const Stage& ST, const int64_t* r_off, const Outputs& O, cudaStream_t s) {
-    if (P.K <= 8) return launch_sample<Best<8>>(C, P, mode, list, list_n, RO, ST, r_off, O, s);
-    if (P.K <= 32) return launch_sample<Best<32>>(C, P, mode, list, list_n, RO, ST, r_off, O, s);
-    return launch_sample<BestDyn>(C, P, mode, list, list_n, RO, ST, r_off, O, s);
+                    const Stage& ST, const int64_t* r_off, const Outputs& O, int4* plan, cudaStream_t s) {
+    if (P.K <= 8) return launch_sample<Best<8>>(C, P, mode, list, list_n, RO, ST, r_off, O, plan, s);
+    if (P.K <= 32) return launch_sample<Best<32>>(C, P, mode, list, list_n, RO, ST, r_off, O, plan, s);
+    return launch_sample<BestDyn>(C, P, mode, list, list_n, RO, ST, r_off, O, plan, s);
 }
 
 int validate(const hp_sampler_params* p, const double* colors, int64_t n_colors) {
@@ -787,7 +832,7 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
     RayOut RO = w.ro;
     RO.rcount = r_off;
     RO.t_end = t_end;
-    if (m > 0) HP_TRY(dispatch_sample(C, P, 0, nullptr, nullptr, RO, w.st, nullptr, Outputs{}, s));
+    if (m > 0) HP_TRY(dispatch_sample(C, P, 0, nullptr, nullptr, RO, w.st, nullptr, Outputs{}, w.plan, s));
     HP_TRY(exclusive_scan_i64(r_off, r_off, m, w.scan, s));
     return HP_OK;
 }
@@ -818,7 +863,7 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
         HP_CHECK_LAUNCH("k_emit");
     }
     // rays whose retained list did not fit the staging: recompute, write direct
-    HP_TRY(dispatch_sample(C, P, 1, w.ro.ovf_list, w.ro.ovf_n, w.ro, w.st, r_off, O, s));
+    HP_TRY(dispatch_sample(C, P, 1, w.ro.ovf_list, w.ro.ovf_n, w.ro, w.st, r_off, O, w.plan, s));
     return HP_OK;
 }
 
