@@ -134,23 +134,29 @@ int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64_t padded_w
                   hp_stream_t stream);
 
 /* ---------------- sample ---------------- */
-/* max_q: longest per-ray segment of the CSR (hp_csr_stats); rays longer than
- * the shared-memory capacity use global scratch sized from `total`. */
-int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t max_q, int64_t stage_capacity,
+/* exact_capacity: slots for candidates evaluated exactly (udf/alpha/colour
+ * scratch, one thread per candidate).  stage_capacity: slots for retained
+ * candidates staged between run and emit (rays that do not fit are
+ * recomputed by emit). */
+int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity, int64_t stage_capacity,
                               const hp_sampler_params* p, size_t* bytes);
 /* Pass 1 over the query CSR (offsets [m+1], ids/t/dist [total], slopes [m],
  * colors float64 [n_colors,3] or NULL).  Writes t_end [m] and r_off [m+1]
- * (r_off[m] = R).  Retained candidates are staged in the workspace. */
+ * (r_off[m] = R).  Retained candidates are staged in the workspace.
+ * Synchronises `stream` once to read the number of exactly evaluated
+ * candidates; if it exceeds exact_capacity, returns HP_ESPACE and stores the
+ * required capacity in *exact_needed (host pointer, may be NULL) so the
+ * caller can grow the workspace and call again. */
 int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
-                  const double* dist, int64_t total, int64_t max_q, const double* slopes,
+                  const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
                   const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                  int64_t stage_capacity, int64_t* r_off, double* t_end, void* workspace,
-                  size_t workspace_bytes, hp_stream_t stream);
+                  int64_t stage_capacity, int64_t* r_off, double* t_end, int64_t* exact_needed,
+                  void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Pass 2: write the R retained candidates (R = r_off[m], host value) in ray
  * order: r_id int64, r_t/r_dist/r_udf/r_alpha/r_w float64 [R], r_color
  * float64 [R,3] (may be NULL without colors). */
 int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
-                   const double* dist, int64_t total, int64_t max_q, const double* slopes,
+                   const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
                    const hp_sampler_params* p, const double* colors, int64_t n_colors,
                    int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id,
                    double* r_t, double* r_dist, double* r_udf, double* r_alpha, double* r_w,

@@ -16,6 +16,7 @@ HP_EINVAL = -1
 
 c_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
+HP_ESPACE = -3  # hashpoint_b200.h
 c_i32 = ctypes.c_int32
 c_f64 = ctypes.c_double
 c_size = ctypes.c_size_t
@@ -59,7 +60,7 @@ _SIGNATURES = {
                                                  ctypes.POINTER(c_size)]),
     "hp_sample_run": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
                                      ctypes.POINTER(SamplerParams), c_p, c_i64, c_i64, c_p, c_p,
-                                     c_p, c_size, c_p]),
+                                     ctypes.POINTER(c_i64), c_p, c_size, c_p]),
     "hp_sample_emit": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
                                       ctypes.POINTER(SamplerParams), c_p, c_i64, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),

@@ -194,18 +194,12 @@ struct BestDyn {
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
-constexpr int kWin = 384;  // candidates of a ray staged in shared memory (per warp)
-
-// The ray's t / ds: the first kWin candidates from the warp's shared-memory
-// window, the rest from global memory (read-only path).
+// One ray's t / ds segment of the query CSR (read-only path).
 struct RayView {
     const double* gt;
     const double* gd;
-    const double* wt;
-    const double* wd;
-    int win;  // staged prefix length (0: everything from global memory)
-    __device__ __forceinline__ double t(int i) const { return i < win ? wt[i] : __ldg(gt + i); }
-    __device__ __forceinline__ double d(int i) const { return i < win ? wd[i] : __ldg(gd + i); }
+    __device__ __forceinline__ double t(int i) const { return __ldg(gt + i); }
+    __device__ __forceinline__ double d(int i) const { return __ldg(gd + i); }
 };
 
 // Exact udf/alpha (and colour) of candidate j (reference _kernels.py:594-660).
@@ -381,7 +375,6 @@ __device__ int warp_first_true(int q, Pred pred) {
 }
 
 struct WarpSmem {
-    double wt[kWin], wd[kWin];
     int rj[kRetCap];
     double rudf[kRetCap], ralpha[kRetCap], rw[kRetCap], rcol[kRetCap * 3];
 };
@@ -391,19 +384,23 @@ struct WarpSmem {
 // chain: je (retention is decided before je) and whether the reference's
 // transmittance provably underflows to exactly 0.  plan[ray] =
 // (jstar, je, flags: 1 fast | 2 proved_zero, q).
-__device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __restrict__ plan) {
+__device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __restrict__ plan,
+                         int64_t* __restrict__ ecnt) {
     const int lane = lane_id();
     const int64_t lo = C.off[ray];
     const int q = int(C.off[ray + 1] - lo);
     if (q == 0) {
-        if (lane == 0) plan[ray] = make_int4(0, 0, 0, 0);
+        if (lane == 0) {
+            plan[ray] = make_int4(0, 0, 0, 0);
+            ecnt[ray] = 0;
+        }
         return;
     }
     const double slope = C.slopes[ray];
     const double* T = C.t + lo;
     const double* DS = C.ds + lo;
     const double thr = P.eps_mode ? P.eps : P.tau_min;
-    const RayView V{T, DS, nullptr, nullptr, 0};
+    const RayView V{T, DS};
 
     // fast-path preconditions + count of candidates within r_0 (use_el holds
     // from j = 0 when it reaches K, the common case on dense surfaces)
@@ -495,20 +492,74 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     }
     if (lane == 0) {
         plan[ray] = make_int4(jstar, je, (fast ? 1 : 0) | (proved_zero ? 2 : 0), q);
+        // exact region [0, E): everything unless retention is decided before je
+        // and (exact t_end) the transmittance is proved to reach exactly 0
+        ecnt[ray] = (!fast || (P.exact_t_end && !proved_zero)) ? q : je;
         atomicAdd(&g_dbg[5], nbound);
     }
 }
 
-// One ray per warp (k_sample).  mode 0: stage retained candidates; mode 1:
-// write them directly to the outputs at r_off[ray] (rays whose staging
-// overflowed).  Evaluates the exact region [0, E) given by the plan.
+__global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan,
+                                                          int64_t* __restrict__ ecnt) {
+    const int64_t warps = int64_t(gridDim.x) * kWarps;
+    for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
+        plan_ray(C, P, ray, plan, ecnt);
+}
+
+// candidate slot -> ray (warp per ray)
+__global__ void k_sample_expand(int64_t m, const int64_t* __restrict__ eoff, int* __restrict__ cand_ray) {
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t ray = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); ray < m; ray += warps) {
+        const int64_t a = eoff[ray], b = eoff[ray + 1];
+        for (int64_t k = a + lane_id(); k < b; k += 32) cand_ray[k] = int(ray);
+    }
+}
+
+struct Exact {  // per exact candidate (flat over all rays)
+    double* udf;
+    double* alpha;
+    double* col;  // [n, 3]
+    int* ray;
+    int64_t cap;
+};
+
+// One thread per exact candidate (all lanes busy regardless of how few
+// candidates a ray needs): exact udf / alpha / colour of candidate j of ray.
 template <class BestT>
-__device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t ray, int mode, const RayOut& RO,
+__global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
+                                                           const int64_t* __restrict__ eoff, Exact X) {
+    const int64_t n = eoff[C.m];
+    unsigned long long evals = 0;
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
+        const int ray = X.ray[c];
+        const int j = int(c - eoff[ray]);
+        const int4 pl = plan[ray];
+        const int64_t lo = C.off[ray];
+        const int q = pl.w;
+        const RayView V{C.t + lo, C.ds + lo};
+        double u, a, col[3] = {0.0, 0.0, 0.0};
+        eval_exact<BestT>(V, q, j, pl.z & 1, pl.x, C.slopes[ray], P, C.ids + lo, C.colors, u, a, col, evals);
+        X.udf[c] = u;
+        X.alpha[c] = a;
+        if (P.want_color) {
+            X.col[3 * c] = col[0];
+            X.col[3 * c + 1] = col[1];
+            X.col[3 * c + 2] = col[2];
+        }
+    }
+    evals = warp_sum(evals);
+    if (lane_id() == 0 && evals) atomicAdd(&g_dbg[3], evals);
+}
+
+// One warp per ray: the reference's sequential compositing over the exact
+// region (_kernels.py:661-697), retention, transmittance.  mode 0: stage the
+// retained candidates; mode 1: write them to the outputs at r_off[ray].
+__device__ void retain_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t ray, int mode, const RayOut& RO,
                            const Stage& ST, const int64_t* __restrict__ r_off, const Outputs& O,
-                           const int4* __restrict__ plan) {
+                           const int4* __restrict__ plan, const int64_t* __restrict__ eoff, const Exact& X) {
     const int lane = lane_id();
-    const int64_t lo = C.off[ray];
-    const int q = int(C.off[ray + 1] - lo);
+    const int4 pl = plan[ray];
+    const int q = pl.w;
     if (q == 0) {
         if (mode == 0 && lane == 0) {
             RO.rcount[ray] = 0;
@@ -517,33 +568,17 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
         }
         return;
     }
-    const double slope = C.slopes[ray];
-    const double* T = C.t + lo;
-    const double* DS = C.ds + lo;
-    const int64_t* ids_ray = C.ids + lo;
-    const double thr = P.eps_mode ? P.eps : P.tau_min;
-    const int4 pl = plan[ray];
-    const int jstar = pl.x, je = pl.y;
     const bool fast = pl.z & 1, proved_zero = (pl.z >> 1) & 1;
-    const unsigned long long nbound = 0;
-    const int E = (!fast || (P.exact_t_end && !proved_zero)) ? q : je;
-    const int win = min(q, kWin);
-    for (int k = lane; k < win; k += 32) {
-        W.wt[k] = ldg(T + k);
-        W.wd[k] = ldg(DS + k);
-    }
-    __syncwarp();
-    const RayView V{T, DS, W.wt, W.wd, win};
-
-    // ---- 2. exact region [0, E): reference compositing and retention
+    const double thr = P.eps_mode ? P.eps : P.tau_min;
+    const int64_t lo = C.off[ray];
+    const int64_t e0 = eoff[ray];
+    const int E = int(eoff[ray + 1] - e0);
     double Tr = 1.0, exit_T = -1.0;
     int nret = 0;
-    unsigned long long nexact = 0;
     const int64_t out_base = mode == 1 ? r_off[ray] : 0;
     for (int c0 = 0; c0 < E; c0 += 32) {
         const int j = c0 + lane;
-        double u = 0.0, a = 0.0, col[3] = {0.0, 0.0, 0.0};
-        if (j < E) eval_exact<BestT>(V, q, j, fast, jstar, slope, P, ids_ray, C.colors, u, a, col, nexact);
+        const double a = j < E ? X.alpha[e0 + j] : 0.0;
         const int n = min(32, E - c0);
         double wmine = 0.0;
         unsigned keep = 0;
@@ -561,46 +596,44 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
             if (lane == k) wmine = w;
             Tr = dmul(Tr, dsub(1.0, ak));
         }
-        // write the kept lanes in order
         const bool mine = (keep >> lane) & 1u;
         const int pos = nret + __popc(keep & ((1u << lane) - 1));
         if (mine) {
-            const int jj = c0 + lane;
+            const int64_t c = e0 + j;
             if (mode == 1) {
                 const int64_t o = out_base + pos;
-                O.r_id[o] = ids_ray[jj];
-                O.r_t[o] = V.t(jj);
-                O.r_dist[o] = V.d(jj);
-                O.r_udf[o] = u;
+                O.r_id[o] = C.ids[lo + j];
+                O.r_t[o] = C.t[lo + j];
+                O.r_dist[o] = C.ds[lo + j];
+                O.r_udf[o] = X.udf[c];
                 O.r_alpha[o] = a;
                 O.r_w[o] = wmine;
                 if (P.want_color) {
-                    O.r_color[3 * o] = col[0];
-                    O.r_color[3 * o + 1] = col[1];
-                    O.r_color[3 * o + 2] = col[2];
+                    O.r_color[3 * o] = X.col[3 * c];
+                    O.r_color[3 * o + 1] = X.col[3 * c + 1];
+                    O.r_color[3 * o + 2] = X.col[3 * c + 2];
                 }
             } else if (pos < kRetCap) {
-                W.rj[pos] = jj;
-                W.rudf[pos] = u;
+                W.rj[pos] = j;
+                W.rudf[pos] = X.udf[c];
                 W.ralpha[pos] = a;
                 W.rw[pos] = wmine;
-                W.rcol[3 * pos] = col[0];
-                W.rcol[3 * pos + 1] = col[1];
-                W.rcol[3 * pos + 2] = col[2];
+                if (P.want_color) {
+                    W.rcol[3 * pos] = X.col[3 * c];
+                    W.rcol[3 * pos + 1] = X.col[3 * c + 1];
+                    W.rcol[3 * pos + 2] = X.col[3 * c + 2];
+                }
             }
         }
         nret += __popc(keep);
         if (stop) break;
     }
     if (mode == 0) {
-        nexact = warp_sum(nexact);
         if (lane == 0) {
             atomicAdd(&g_dbg[0], 1ull);
             atomicAdd(&g_dbg[1], fast ? 1ull : 0ull);
             atomicAdd(&g_dbg[2], proved_zero ? 1ull : 0ull);
-            atomicAdd(&g_dbg[3], nexact);
             atomicAdd(&g_dbg[4], (unsigned long long)q);
-            atomicAdd(&g_dbg[5], nbound);
         }
         double te;
         if (P.exact_t_end)
@@ -641,24 +674,17 @@ __device__ void sample_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan) {
-    const int64_t warps = int64_t(gridDim.x) * kWarps;
-    for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
-        plan_ray(C, P, ray, plan);
-}
-
-template <class BestT>
-__global__ void __launch_bounds__(kThreads, 3) k_sample(Csr C, Params P, int mode, const int* __restrict__ ray_list,
-                                                     const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
-                                                     const int64_t* __restrict__ r_off, Outputs O,
-                                                     const int4* __restrict__ plan) {
-    extern __shared__ __align__(16) unsigned char dyn[];
-    WarpSmem* W = reinterpret_cast<WarpSmem*>(dyn);
+__global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, int mode, const int* __restrict__ ray_list,
+                                                            const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
+                                                            const int64_t* __restrict__ r_off, Outputs O,
+                                                            const int4* __restrict__ plan,
+                                                            const int64_t* __restrict__ eoff, Exact X) {
+    __shared__ WarpSmem W[kWarps];
     const int64_t n = ray_list ? int64_t(*ray_list_n) : C.m;
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t k = int64_t(blockIdx.x) * kWarps + warp_id(); k < n; k += warps) {
         const int64_t ray = ray_list ? int64_t(ray_list[k]) : k;
-        sample_ray<BestT>(W[warp_id()], C, P, ray, mode, RO, ST, r_off, O, plan);
+        retain_ray(W[warp_id()], C, P, ray, mode, RO, ST, r_off, O, plan, eoff, X);
     }
 }
 
@@ -715,10 +741,12 @@ struct SampleWs {
     RayOut ro;
     Stage st;
     int4* plan;
+    int64_t* eoff;  // [m + 1] exact-candidate offsets
+    Exact x;
     void* scan;
 };
 
-SampleWs carve_sample(Carver& c, int64_t m, int64_t cap, bool color) {
+SampleWs carve_sample(Carver& c, int64_t m, int64_t cap, int64_t xcap, bool color) {
     SampleWs w;
     w.ro.rcount = nullptr;
     w.ro.t_end = nullptr;
@@ -733,6 +761,13 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t cap, bool color) {
     w.st.w = c.take<double>(cap > 0 ? cap : 1);
     w.st.col = color ? c.take<double>(3 * (cap > 0 ? cap : 1)) : nullptr;
     w.plan = c.take<int4>(m > 0 ? m : 1);
+    w.eoff = c.take<int64_t>(m + 1);
+    const int64_t xc = xcap > 0 ? xcap : 1;
+    w.x.cap = xcap;
+    w.x.udf = c.take<double>(xc);
+    w.x.alpha = c.take<double>(xc);
+    w.x.col = color ? c.take<double>(3 * xc) : nullptr;
+    w.x.ray = c.take<int>(xc);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     return w;
 }
@@ -753,33 +788,55 @@ Params to_params(const hp_sampler_params* p) {
     return P;
 }
 
+// Plan (warp per ray) -> scan of the exact-region sizes -> (host reads the
+// total) -> expand (slot -> ray) -> exact evaluation (thread per candidate).
 template <class BestT>
-int launch_sample(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
-                  const Stage& ST, const int64_t* r_off, const Outputs& O, int4* plan, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(k_sample<BestT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(sizeof(WarpSmem) * kWarps));
-        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(k_sample)");
-        attr = true;
-    }
-    if (mode == 0) {
+int launch_exact(const Csr& C, const Params& P, SampleWs& w, int64_t* needed, cudaStream_t s) {
+    {
         TimedSpan ts("k_sample_plan", s);
-        k_sample_plan<<<kNumSMs * 8, kThreads, 0, s>>>(C, P, plan);
+        k_sample_plan<<<kNumSMs * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff);
         HP_CHECK_LAUNCH("k_sample_plan");
     }
-    TimedSpan ts(mode == 0 ? "k_sample" : "k_sample_overflow", s);
-    k_sample<BestT><<<kSampleGrid, kThreads, sizeof(WarpSmem) * kWarps, s>>>(C, P, mode, list, list_n, RO, ST,
-                                                                             r_off, O, plan);
-    HP_CHECK_LAUNCH("k_sample");
+    HP_TRY(exclusive_scan_i64(w.eoff, w.eoff, C.m, w.scan, s));
+    int64_t n = 0;
+    cudaError_t e = cudaMemcpyAsync(&n, w.eoff + C.m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "hp_sample_run: exact count");
+    if (needed) *needed = n;
+    if (n > w.x.cap) {
+        set_error("hp_sample_run: %lld exact candidates exceed exact_capacity %lld", (long long)n,
+                  (long long)w.x.cap);
+        return HP_ESPACE;
+    }
+    if (n == 0) return HP_OK;
+    {
+        TimedSpan ts("k_sample_expand", s);
+        k_sample_expand<<<kNumSMs * 8, 256, 0, s>>>(C.m, w.eoff, w.x.ray);
+        HP_CHECK_LAUNCH("k_sample_expand");
+    }
+    {
+        TimedSpan ts("k_sample_exact", s);
+        const int64_t blocks = (n + kThreads - 1) / kThreads;
+        k_sample_exact<BestT><<<int(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16), kThreads, 0, s>>>(C, P, w.plan,
+                                                                                                     w.eoff, w.x);
+        HP_CHECK_LAUNCH("k_sample_exact");
+    }
     return HP_OK;
 }
 
-int dispatch_sample(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
-                    const Stage& ST, const int64_t* r_off, const Outputs& O, int4* plan, cudaStream_t s) {
-    if (P.K <= 8) return launch_sample<Best<8>>(C, P, mode, list, list_n, RO, ST, r_off, O, plan, s);
-    if (P.K <= 32) return launch_sample<Best<32>>(C, P, mode, list, list_n, RO, ST, r_off, O, plan, s);
-    return launch_sample<BestDyn>(C, P, mode, list, list_n, RO, ST, r_off, O, plan, s);
+int dispatch_exact(const Csr& C, const Params& P, SampleWs& w, int64_t* needed, cudaStream_t s) {
+    if (P.K <= 8) return launch_exact<Best<8>>(C, P, w, needed, s);
+    if (P.K <= 32) return launch_exact<Best<32>>(C, P, w, needed, s);
+    return launch_exact<BestDyn>(C, P, w, needed, s);
+}
+
+int launch_retain(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
+                  const SampleWs& w, const int64_t* r_off, const Outputs& O, cudaStream_t s) {
+    TimedSpan ts(mode == 0 ? "k_sample_retain" : "k_sample_overflow", s);
+    k_sample_retain<<<kSampleGrid, kThreads, 0, s>>>(C, P, mode, list, list_n, RO, w.st, r_off, O, w.plan, w.eoff,
+                                                     w.x);
+    HP_CHECK_LAUNCH("k_sample_retain");
+    return HP_OK;
 }
 
 int validate(const hp_sampler_params* p, const double* colors, int64_t n_colors) {
@@ -799,26 +856,25 @@ int validate(const hp_sampler_params* p, const double* colors, int64_t n_colors)
 
 using namespace hp;
 
-extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t max_q, int64_t stage_capacity,
-                                         const hp_sampler_params* p, size_t* bytes) {
+extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity,
+                                         int64_t stage_capacity, const hp_sampler_params* p, size_t* bytes) {
     Carver c(nullptr, 0);
-    carve_sample(c, m, stage_capacity, p && p->want_color);
+    carve_sample(c, m, stage_capacity, exact_capacity, p && p->want_color);
     *bytes = c.used + 256;
     (void)total;
-    (void)max_q;
     return HP_OK;
 }
 
 extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
-                             const double* dist, int64_t total, int64_t max_q, const double* slopes,
+                             const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
                              const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                             int64_t stage_capacity, int64_t* r_off, double* t_end, void* workspace,
-                             size_t workspace_bytes, hp_stream_t stream) {
+                             int64_t stage_capacity, int64_t* r_off, double* t_end, int64_t* exact_needed,
+                             void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
-    (void)max_q;
+    if (exact_needed) *exact_needed = 0;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, stage_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, stage_capacity, exact_capacity, p->want_color);
     if (!c.ok()) {
         set_error("hp_sample_run: workspace too small");
         return HP_ESPACE;
@@ -832,23 +888,25 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
     RayOut RO = w.ro;
     RO.rcount = r_off;
     RO.t_end = t_end;
-    if (m > 0) HP_TRY(dispatch_sample(C, P, 0, nullptr, nullptr, RO, w.st, nullptr, Outputs{}, w.plan, s));
+    if (m > 0) {
+        HP_TRY(dispatch_exact(C, P, w, exact_needed, s));
+        HP_TRY(launch_retain(C, P, 0, nullptr, nullptr, RO, w, nullptr, Outputs{}, s));
+    }
     HP_TRY(exclusive_scan_i64(r_off, r_off, m, w.scan, s));
     return HP_OK;
 }
 
 extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
-                              const double* dist, int64_t total, int64_t max_q, const double* slopes,
-                              const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                              int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id, double* r_t,
+                              const double* dist, int64_t total, int64_t exact_capacity,
+                              const double* slopes, const hp_sampler_params* p, const double* colors,
+                              int64_t n_colors, int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id, double* r_t,
                               double* r_dist, double* r_udf, double* r_alpha, double* r_w, double* r_color,
                               void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
-    (void)max_q;
     if (R == 0 || m == 0) return HP_OK;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, stage_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, stage_capacity, exact_capacity, p->want_color);
     if (!c.ok()) {
         set_error("hp_sample_emit: workspace too small");
         return HP_ESPACE;
@@ -863,7 +921,7 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
         HP_CHECK_LAUNCH("k_emit");
     }
     // rays whose retained list did not fit the staging: recompute, write direct
-    HP_TRY(dispatch_sample(C, P, 1, w.ro.ovf_list, w.ro.ovf_n, w.ro, w.st, r_off, O, w.plan, s));
+    HP_TRY(launch_retain(C, P, 1, w.ro.ovf_list, w.ro.ovf_n, w.ro, w, r_off, O, s));
     return HP_OK;
 }
 
