@@ -324,6 +324,14 @@ __device__ void eval_exact(const RayView& V, int q, int j, bool fast,
 // then bounded below in fp32 (argument rounded up, result scaled by
 // 1 - 2^-20 against expf's 2-ulp error).  Every later operation is monotone,
 // so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
+__device__ __forceinline__ double factor_from_sum(double sum, int ksel, const Params& P) {
+    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
+    const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
+    const float e = expf(-__double2float_ru(y));
+    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
+    return dsub(1.0, a_lo);
+}
+
 __device__ double bound_factor(const RayView& V, int q, int j, int jstar, double slope, const Params& P) {
     const double tj = V.t(j);
     const double rj = dmul(slope, tj);
@@ -343,11 +351,28 @@ __device__ double bound_factor(const RayView& V, int q, int j, int jstar, double
         sum = dadd(sum, dadd(dsub(tj, V.t(i)), di));
         found++;
     }
-    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
-    const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
-    const float e = expf(-__double2float_ru(y));
-    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
-    return dsub(1.0, a_lo);
+    return factor_from_sum(sum, ksel, P);
+}
+
+// Same bound with the members taken from the warp's ring of the last 64
+// candidates (K <= 32): the ksel candidates ending at j (or [0, ksel) for
+// j < ksel - 1).  Returns a negative value when a member is not in j's pool
+// (the caller then uses bound_factor).
+__device__ __forceinline__ double bound_factor_ring(const double* rt, const double* rd, int q, int j, double tj,
+                                                    int jstar, double slope, const Params& P) {
+    const bool use_el = j >= jstar;
+    const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
+    const double rj = dmul(slope, tj);
+    const int i0 = j >= ksel - 1 ? j - ksel + 1 : 0;
+    double sum = 0.0;
+    bool ok = true;
+    for (int k = 0; k < ksel; k++) {
+        const int i = (i0 + k) & 63;
+        const double di = rd[i];
+        ok &= !(use_el && di > rj);
+        sum = dadd(sum, dadd(fabs(dsub(rt[i], tj)), di));
+    }
+    return ok ? factor_from_sum(sum, ksel, P) : -1.0;
 }
 
 // Warp: first j in [0, q) with pred(j) (monotone false..true); q if none.
@@ -385,7 +410,7 @@ struct WarpSmem {
 // transmittance provably underflows to exactly 0.  plan[ray] =
 // (jstar, je, flags: 1 fast | 2 proved_zero, q).
 __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __restrict__ plan,
-                         int64_t* __restrict__ ecnt) {
+                         int64_t* __restrict__ ecnt, double* __restrict__ rt, double* __restrict__ rd) {
     const int lane = lane_id();
     const int64_t lo = C.off[ray];
     const int q = int(C.off[ray + 1] - lo);
@@ -447,7 +472,22 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
         bool seq = false;
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
-            const double u = j < q ? bound_factor(V, q, j, jstar, slope, P) : 1.0;
+            double u = 1.0;
+            if (P.K <= 32) {
+                const double tj = j < q ? ldg(T + j) : 0.0;
+                __syncwarp();
+                rt[j & 63] = tj;
+                rd[j & 63] = j < q ? ldg(DS + j) : 0.0;
+                __syncwarp();
+                if (j < q) {
+                    u = (j >= P.K - 1 || c0 + 32 >= min(q, P.K))
+                            ? bound_factor_ring(rt, rd, q, j, tj, jstar, slope, P)
+                            : -1.0;
+                    if (u < 0.0) u = bound_factor(V, q, j, jstar, slope, P);
+                }
+            } else if (j < q) {
+                u = bound_factor(V, q, j, jstar, slope, P);
+            }
             nbound += 32;
             const int n = min(32, q - c0);
             if (!seq) {
@@ -501,9 +541,10 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
 
 __global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan,
                                                           int64_t* __restrict__ ecnt) {
+    __shared__ double ring[kWarps][2][64];  // last 64 candidates' t / ds per warp
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
-        plan_ray(C, P, ray, plan, ecnt);
+        plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1]);
 }
 
 // candidate slot -> ray (warp per ray)
