@@ -420,11 +420,14 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
                              const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
                              double* __restrict__ gd) {
     const int tid = threadIdx.x;
+    // all of the segment's loads in flight at once (L2-resident scratch)
     for (int e = tid; e < q; e += kT) {
-        F.t[e] = st[e];
-        F.d[e] = sd[e];
-        F.id[e] = sid[e];
+        cp_async8(&F.t[e], st + e);
+        cp_async8(&F.d[e], sd + e);
+        cp_async4(&F.id[e], sid + e);
     }
+    cp_commit();
+    cp_wait<0>();
     if (q <= 64) {
         __syncthreads();
         for (int e = tid; e < q; e += kT) {
