@@ -135,14 +135,13 @@ int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64_t padded_w
 
 /* ---------------- sample ---------------- */
 /* exact_capacity: slots for candidates evaluated exactly (udf/alpha/colour
- * scratch, one thread per candidate).  stage_capacity: slots for retained
- * candidates staged between run and emit (rays that do not fit are
- * recomputed by emit). */
-int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity, int64_t stage_capacity,
+ * scratch, one thread per candidate; the retained candidates are kept there,
+ * compacted, between run and emit). */
+int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity,
                               const hp_sampler_params* p, size_t* bytes);
 /* Pass 1 over the query CSR (offsets [m+1], ids/t/dist [total], slopes [m],
  * colors float64 [n_colors,3] or NULL).  Writes t_end [m] and r_off [m+1]
- * (r_off[m] = R).  Retained candidates are staged in the workspace.
+ * (r_off[m] = R).  Retained candidates are kept in the workspace for emit.
  * Synchronises `stream` once to read the number of exactly evaluated
  * candidates; if it exceeds exact_capacity, returns HP_ESPACE and stores the
  * required capacity in *exact_needed (host pointer, may be NULL) so the
@@ -150,7 +149,7 @@ int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity, 
 int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                   const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
                   const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                  int64_t stage_capacity, int64_t* r_off, double* t_end, int64_t* exact_needed,
+                  int64_t* r_off, double* t_end, int64_t* exact_needed,
                   void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Pass 2: write the R retained candidates (R = r_off[m], host value) in ray
  * order: r_id int64, r_t/r_dist/r_udf/r_alpha/r_w float64 [R], r_color
@@ -158,7 +157,7 @@ int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const d
 int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                    const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
                    const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                   int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id,
+                   const int64_t* r_off, int64_t R, int64_t* r_id,
                    double* r_t, double* r_dist, double* r_udf, double* r_alpha, double* r_w,
                    double* r_color, void* workspace, size_t workspace_bytes,
                    hp_stream_t stream);

@@ -41,7 +41,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRetCap = 32;  // retained candidates buffered per ray (per warp)
 constexpr int kSampleGrid = kNumSMs * 4;
 
 // Path counters: rays, fast rays, proved-zero rays, exact evaluations,
@@ -65,27 +64,14 @@ struct Csr {
     int64_t m;
 };
 
-struct Stage {  // retained candidates between hp_sample_run and hp_sample_emit
-    int32_t* j;
-    double* udf;
-    double* alpha;
-    double* w;
-    double* col;  // [cap, 3]
-    int64_t cap;
-};
-
 struct Outputs {
     int64_t* r_id;
     double *r_t, *r_dist, *r_udf, *r_alpha, *r_w, *r_color;
 };
 
-struct RayOut {  // per-ray bookkeeping written by pass 1
-    int64_t* rcount;     // retained count (scanned into r_off)
+struct RayOut {  // per-ray results of pass 1
+    int64_t* rcount;  // retained count (scanned into r_off)
     double* t_end;
-    int64_t* ray_stage;  // staging start, -1 = recompute in pass 2
-    int64_t* stage_cursor;
-    int* ovf_list;
-    int* ovf_n;
 };
 
 __device__ __forceinline__ bool kless(double d2a, int ia, double d2b, int ib) {
@@ -399,10 +385,6 @@ __device__ int warp_first_true(int q, Pred pred) {
     return mask ? a + __ffs(mask) - 1 : b;
 }
 
-struct WarpSmem {
-    int rj[kRetCap];
-    double rudf[kRetCap], ralpha[kRetCap], rw[kRetCap], rcol[kRetCap * 3];
-};
 
 // ---- plan (k_sample_plan): one warp per ray, no shared memory.
 // Fast-path preconditions, j* (first j where use_el holds), and the bound
@@ -556,9 +538,14 @@ __global__ void k_sample_expand(int64_t m, const int64_t* __restrict__ eoff, int
     }
 }
 
-struct Exact {  // per exact candidate (flat over all rays)
+// Per exact candidate, flat over all rays (ray r owns slots [eoff[r],
+// eoff[r+1])).  After k_sample_retain the first rcount[r] slots of each ray
+// hold its retained candidates, compacted in place: ray[] then holds the
+// candidate's index j within the ray and w[] its weight.
+struct Exact {
     double* udf;
     double* alpha;
+    double* w;
     double* col;  // [n, 3]
     int* ray;
     int64_t cap;
@@ -593,30 +580,28 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
 }
 
 // One warp per ray: the reference's sequential compositing over the exact
-// region (_kernels.py:661-697), retention, transmittance.  mode 0: stage the
-// retained candidates; mode 1: write them to the outputs at r_off[ray].
-__device__ void retain_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t ray, int mode, const RayOut& RO,
-                           const Stage& ST, const int64_t* __restrict__ r_off, const Outputs& O,
+// region (_kernels.py:661-697), retention, transmittance.  Retained
+// candidates are compacted to the front of the ray's exact slots (a retained
+// candidate's position never exceeds its index, and every lane reads its
+// chunk before any lane writes).
+__device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const RayOut& RO,
                            const int4* __restrict__ plan, const int64_t* __restrict__ eoff, const Exact& X) {
     const int lane = lane_id();
     const int4 pl = plan[ray];
     const int q = pl.w;
     if (q == 0) {
-        if (mode == 0 && lane == 0) {
+        if (lane == 0) {
             RO.rcount[ray] = 0;
             RO.t_end[ray] = 1.0;
-            RO.ray_stage[ray] = 0;
         }
         return;
     }
     const bool fast = pl.z & 1, proved_zero = (pl.z >> 1) & 1;
     const double thr = P.eps_mode ? P.eps : P.tau_min;
-    const int64_t lo = C.off[ray];
     const int64_t e0 = eoff[ray];
     const int E = int(eoff[ray + 1] - e0);
     double Tr = 1.0, exit_T = -1.0;
     int nret = 0;
-    const int64_t out_base = mode == 1 ? r_off[ray] : 0;
     for (int c0 = 0; c0 < E; c0 += 32) {
         const int j = c0 + lane;
         const double a = j < E ? X.alpha[e0 + j] : 0.0;
@@ -637,118 +622,71 @@ __device__ void retain_ray(WarpSmem& W, const Csr& C, const Params& P, int64_t r
             if (lane == k) wmine = w;
             Tr = dmul(Tr, dsub(1.0, ak));
         }
-        const bool mine = (keep >> lane) & 1u;
-        const int pos = nret + __popc(keep & ((1u << lane) - 1));
-        if (mine) {
-            const int64_t c = e0 + j;
-            if (mode == 1) {
-                const int64_t o = out_base + pos;
-                O.r_id[o] = C.ids[lo + j];
-                O.r_t[o] = C.t[lo + j];
-                O.r_dist[o] = C.ds[lo + j];
-                O.r_udf[o] = X.udf[c];
-                O.r_alpha[o] = a;
-                O.r_w[o] = wmine;
-                if (P.want_color) {
-                    O.r_color[3 * o] = X.col[3 * c];
-                    O.r_color[3 * o + 1] = X.col[3 * c + 1];
-                    O.r_color[3 * o + 2] = X.col[3 * c + 2];
-                }
-            } else if (pos < kRetCap) {
-                W.rj[pos] = j;
-                W.rudf[pos] = X.udf[c];
-                W.ralpha[pos] = a;
-                W.rw[pos] = wmine;
-                if (P.want_color) {
-                    W.rcol[3 * pos] = X.col[3 * c];
-                    W.rcol[3 * pos + 1] = X.col[3 * c + 1];
-                    W.rcol[3 * pos + 2] = X.col[3 * c + 2];
-                }
+        if (keep) {
+            const bool mine = (keep >> lane) & 1u;
+            const int64_t dst = e0 + nret + __popc(keep & ((1u << lane) - 1));
+            double u = 0.0, c[3] = {0.0, 0.0, 0.0};
+            if (mine) {
+                u = X.udf[e0 + j];
+                if (P.want_color)
+                    for (int x = 0; x < 3; x++) c[x] = X.col[3 * (e0 + j) + x];
             }
+            __syncwarp();
+            if (mine) {
+                X.udf[dst] = u;
+                X.alpha[dst] = a;
+                X.w[dst] = wmine;
+                X.ray[dst] = j;
+                if (P.want_color)
+                    for (int x = 0; x < 3; x++) X.col[3 * dst + x] = c[x];
+            }
+            __syncwarp();
         }
         nret += __popc(keep);
         if (stop) break;
     }
-    if (mode == 0) {
-        if (lane == 0) {
-            atomicAdd(&g_dbg[0], 1ull);
-            atomicAdd(&g_dbg[1], fast ? 1ull : 0ull);
-            atomicAdd(&g_dbg[2], proved_zero ? 1ull : 0ull);
-            atomicAdd(&g_dbg[4], (unsigned long long)q);
-        }
+    if (lane == 0) {
+        atomicAdd(&g_dbg[0], 1ull);
+        atomicAdd(&g_dbg[1], fast ? 1ull : 0ull);
+        atomicAdd(&g_dbg[2], proved_zero ? 1ull : 0ull);
+        atomicAdd(&g_dbg[4], (unsigned long long)q);
         double te;
         if (P.exact_t_end)
             te = (fast && proved_zero) ? 0.0 : Tr;
         else
             te = exit_T >= 0.0 ? exit_T : Tr;
-        long long st = 0;
-        if (lane == 0) {
-            RO.rcount[ray] = nret;
-            RO.t_end[ray] = te;
-            st = -1;
-            if (nret > 0 && nret <= kRetCap) {
-                st = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(RO.stage_cursor),
-                                          (unsigned long long)nret);
-                if (st + nret > ST.cap) st = -1;
-            } else if (nret == 0) {
-                st = 0;
-            }
-            RO.ray_stage[ray] = st;
-            if (st < 0) RO.ovf_list[atomicAdd(RO.ovf_n, 1)] = int(ray);
-        }
-        st = __shfl_sync(0xffffffffu, st, 0);
-        __syncwarp();
-        if (st >= 0 && nret > 0) {
-            for (int k = lane; k < nret; k += 32) {
-                ST.j[st + k] = W.rj[k];
-                ST.udf[st + k] = W.rudf[k];
-                ST.alpha[st + k] = W.ralpha[k];
-                ST.w[st + k] = W.rw[k];
-                if (P.want_color) {
-                    ST.col[3 * (st + k)] = W.rcol[3 * k];
-                    ST.col[3 * (st + k) + 1] = W.rcol[3 * k + 1];
-                    ST.col[3 * (st + k) + 2] = W.rcol[3 * k + 2];
-                }
-            }
-        }
-        __syncwarp();
+        RO.rcount[ray] = nret;
+        RO.t_end[ray] = te;
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, int mode, const int* __restrict__ ray_list,
-                                                            const int* __restrict__ ray_list_n, RayOut RO, Stage ST,
-                                                            const int64_t* __restrict__ r_off, Outputs O,
-                                                            const int4* __restrict__ plan,
+__global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, RayOut RO, const int4* __restrict__ plan,
                                                             const int64_t* __restrict__ eoff, Exact X) {
-    __shared__ WarpSmem W[kWarps];
-    const int64_t n = ray_list ? int64_t(*ray_list_n) : C.m;
     const int64_t warps = int64_t(gridDim.x) * kWarps;
-    for (int64_t k = int64_t(blockIdx.x) * kWarps + warp_id(); k < n; k += warps) {
-        const int64_t ray = ray_list ? int64_t(ray_list[k]) : k;
-        retain_ray(W[warp_id()], C, P, ray, mode, RO, ST, r_off, O, plan, eoff, X);
-    }
+    for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
+        retain_ray(C, P, ray, RO, plan, eoff, X);
 }
 
-// Copy staged retained candidates to the outputs (ray order).
-__global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const int64_t* __restrict__ ray_stage,
-                       Stage ST, Outputs O) {
+// Copy the compacted retained candidates to the outputs (ray order).
+__global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const int64_t* __restrict__ eoff,
+                       Exact X, Outputs O) {
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); r < C.m; r += warps) {
-        const int64_t o = r_off[r], n = r_off[r + 1] - o, st = ray_stage[r];
-        if (n == 0 || st < 0) continue;
-        const int64_t lo = C.off[r];
+        const int64_t o = r_off[r], n = r_off[r + 1] - o;
+        if (n == 0) continue;
+        const int64_t lo = C.off[r], st = eoff[r];
         for (int64_t k = lane_id(); k < n; k += 32) {
-            const int64_t j = lo + ST.j[st + k];
+            const int64_t j = lo + X.ray[st + k];
             O.r_id[o + k] = C.ids[j];
             O.r_t[o + k] = C.t[j];
             O.r_dist[o + k] = C.ds[j];
-            O.r_udf[o + k] = ST.udf[st + k];
-            O.r_alpha[o + k] = ST.alpha[st + k];
-            O.r_w[o + k] = ST.w[st + k];
+            O.r_udf[o + k] = X.udf[st + k];
+            O.r_alpha[o + k] = X.alpha[st + k];
+            O.r_w[o + k] = X.w[st + k];
             if (P.want_color) {
-                O.r_color[3 * (o + k)] = ST.col[3 * (st + k)];
-                O.r_color[3 * (o + k) + 1] = ST.col[3 * (st + k) + 1];
-                O.r_color[3 * (o + k) + 2] = ST.col[3 * (st + k) + 2];
+                O.r_color[3 * (o + k)] = X.col[3 * (st + k)];
+                O.r_color[3 * (o + k) + 1] = X.col[3 * (st + k) + 1];
+                O.r_color[3 * (o + k) + 2] = X.col[3 * (st + k) + 2];
             }
         }
     }
@@ -779,34 +717,21 @@ __global__ void k_csr_stats(const int64_t* __restrict__ off, int64_t m, int64_t*
 }
 
 struct SampleWs {
-    RayOut ro;
-    Stage st;
     int4* plan;
     int64_t* eoff;  // [m + 1] exact-candidate offsets
     Exact x;
     void* scan;
 };
 
-SampleWs carve_sample(Carver& c, int64_t m, int64_t cap, int64_t xcap, bool color) {
+SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color) {
     SampleWs w;
-    w.ro.rcount = nullptr;
-    w.ro.t_end = nullptr;
-    w.ro.ray_stage = c.take<int64_t>(m > 0 ? m : 1);
-    w.ro.stage_cursor = c.take<int64_t>(1);
-    w.ro.ovf_list = c.take<int>(m > 0 ? m : 1);
-    w.ro.ovf_n = c.take<int>(1);
-    w.st.cap = cap;
-    w.st.j = c.take<int32_t>(cap > 0 ? cap : 1);
-    w.st.udf = c.take<double>(cap > 0 ? cap : 1);
-    w.st.alpha = c.take<double>(cap > 0 ? cap : 1);
-    w.st.w = c.take<double>(cap > 0 ? cap : 1);
-    w.st.col = color ? c.take<double>(3 * (cap > 0 ? cap : 1)) : nullptr;
     w.plan = c.take<int4>(m > 0 ? m : 1);
     w.eoff = c.take<int64_t>(m + 1);
     const int64_t xc = xcap > 0 ? xcap : 1;
     w.x.cap = xcap;
     w.x.udf = c.take<double>(xc);
     w.x.alpha = c.take<double>(xc);
+    w.x.w = c.take<double>(xc);
     w.x.col = color ? c.take<double>(3 * xc) : nullptr;
     w.x.ray = c.take<int>(xc);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
@@ -871,11 +796,9 @@ int dispatch_exact(const Csr& C, const Params& P, SampleWs& w, int64_t* needed, 
     return launch_exact<BestDyn>(C, P, w, needed, s);
 }
 
-int launch_retain(const Csr& C, const Params& P, int mode, const int* list, const int* list_n, const RayOut& RO,
-                  const SampleWs& w, const int64_t* r_off, const Outputs& O, cudaStream_t s) {
-    TimedSpan ts(mode == 0 ? "k_sample_retain" : "k_sample_overflow", s);
-    k_sample_retain<<<kSampleGrid, kThreads, 0, s>>>(C, P, mode, list, list_n, RO, w.st, r_off, O, w.plan, w.eoff,
-                                                     w.x);
+int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleWs& w, cudaStream_t s) {
+    TimedSpan ts("k_sample_retain", s);
+    k_sample_retain<<<kSampleGrid, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
     HP_CHECK_LAUNCH("k_sample_retain");
     return HP_OK;
 }
@@ -898,9 +821,9 @@ int validate(const hp_sampler_params* p, const double* colors, int64_t n_colors)
 using namespace hp;
 
 extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity,
-                                         int64_t stage_capacity, const hp_sampler_params* p, size_t* bytes) {
+                                         const hp_sampler_params* p, size_t* bytes) {
     Carver c(nullptr, 0);
-    carve_sample(c, m, stage_capacity, exact_capacity, p && p->want_color);
+    carve_sample(c, m, exact_capacity, p && p->want_color);
     *bytes = c.used + 256;
     (void)total;
     return HP_OK;
@@ -908,30 +831,24 @@ extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact
 
 extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                              const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
-                             const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                             int64_t stage_capacity, int64_t* r_off, double* t_end, int64_t* exact_needed,
-                             void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+                             const hp_sampler_params* p, const double* colors, int64_t n_colors, int64_t* r_off,
+                             double* t_end, int64_t* exact_needed, void* workspace, size_t workspace_bytes,
+                             hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
     if (exact_needed) *exact_needed = 0;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, stage_capacity, exact_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
     if (!c.ok()) {
         set_error("hp_sample_run: workspace too small");
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(w.ro.stage_cursor, 0, sizeof(int64_t), s) != cudaSuccess ||
-        cudaMemsetAsync(w.ro.ovf_n, 0, sizeof(int), s) != cudaSuccess)
-        return cuda_status(cudaGetLastError(), "hp_sample_run memset");
     Csr C{offsets, ids, t, dist, slopes, colors, m};
     Params P = to_params(p);
-    RayOut RO = w.ro;
-    RO.rcount = r_off;
-    RO.t_end = t_end;
     if (m > 0) {
         HP_TRY(dispatch_exact(C, P, w, exact_needed, s));
-        HP_TRY(launch_retain(C, P, 0, nullptr, nullptr, RO, w, nullptr, Outputs{}, s));
+        HP_TRY(launch_retain(C, P, RayOut{r_off, t_end}, w, s));
     }
     HP_TRY(exclusive_scan_i64(r_off, r_off, m, w.scan, s));
     return HP_OK;
@@ -940,14 +857,14 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
 extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                               const double* dist, int64_t total, int64_t exact_capacity,
                               const double* slopes, const hp_sampler_params* p, const double* colors,
-                              int64_t n_colors, int64_t stage_capacity, const int64_t* r_off, int64_t R, int64_t* r_id, double* r_t,
+                              int64_t n_colors, const int64_t* r_off, int64_t R, int64_t* r_id, double* r_t,
                               double* r_dist, double* r_udf, double* r_alpha, double* r_w, double* r_color,
                               void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
     if (R == 0 || m == 0) return HP_OK;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, stage_capacity, exact_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
     if (!c.ok()) {
         set_error("hp_sample_emit: workspace too small");
         return HP_ESPACE;
@@ -956,13 +873,9 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
     Csr C{offsets, ids, t, dist, slopes, colors, m};
     Params P = to_params(p);
     Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
-    {
-        TimedSpan ts("k_emit", s);
-        k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.ro.ray_stage, w.st, O);
-        HP_CHECK_LAUNCH("k_emit");
-    }
-    // rays whose retained list did not fit the staging: recompute, write direct
-    HP_TRY(launch_retain(C, P, 1, w.ro.ovf_list, w.ro.ovf_n, w.ro, w, r_off, O, s));
+    TimedSpan ts("k_emit", s);
+    k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    HP_CHECK_LAUNCH("k_emit");
     return HP_OK;
 }
 

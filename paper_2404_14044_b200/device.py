@@ -19,9 +19,8 @@ from . import _lib
 from ._lib import c_i64, c_size
 
 __all__ = ["DeviceIndex", "build", "build_from_table", "query", "sample", "primary_surface",
-           "SAMPLE_STAGE_PER_RAY", "SAMPLE_EXACT_PER_RAY"]
+           "SAMPLE_EXACT_PER_RAY"]
 
-SAMPLE_STAGE_PER_RAY = 8  # staging slots reserved per ray for retained candidates
 SAMPLE_EXACT_PER_RAY = 16  # initial exact-candidate scratch per ray (grown on demand)
 
 # Optional per-kernel timer (pipeline.StageTimer); set by the benchmark.
@@ -226,7 +225,6 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     total = int(ids.numel())
     want = colors is not None
     p = sampler_params(cfg, want, exact_t_end)
-    cap = max(SAMPLE_STAGE_PER_RAY * m, 1 << 16)
     exact_cap = max(SAMPLE_EXACT_PER_RAY * m, 1 << 16)
     r_off = torch.empty(m + 1, dtype=torch.int64, device=dev)
     t_end = torch.empty(max(m, 0), dtype=torch.float64, device=dev)
@@ -236,12 +234,11 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     _mark("sample.setup")
     for _ in range(2):
         nb = c_size(0)
-        _lib.check(lib.hp_sample_workspace_bytes(m, total, exact_cap, cap, ctypes.byref(p),
+        _lib.check(lib.hp_sample_workspace_bytes(m, total, exact_cap, ctypes.byref(p),
                                                  ctypes.byref(nb)))
         ws = _workspace(nb.value, dev)
         common = (_ptr(offsets), m, _ptr(ids), _ptr(t), _ptr(dist), total, exact_cap,
-                  _ptr(slopes), ctypes.byref(p), _ptr(col) if want else ctypes.c_void_p(0), ncol,
-                  cap)
+                  _ptr(slopes), ctypes.byref(p), _ptr(col) if want else ctypes.c_void_p(0), ncol)
         rc = lib.hp_sample_run(*common, _ptr(r_off), _ptr(t_end), ctypes.byref(needed), _ptr(ws),
                                nb.value, _stream())
         if rc == _lib.HP_ESPACE and needed.value > exact_cap:

@@ -41,7 +41,7 @@ def test_workspace_size_queries_are_host_only():
     assert L.hp_build_workspace_bytes(1000, 64, 48, ctypes.byref(nb)) == 0 and nb.value > 0
     assert L.hp_query_workspace_bytes(4096, 5, 100000, ctypes.byref(nb)) == 0 and nb.value > 0
     p = _lib.SamplerParams(8, 1, 1, 1, 0.02, 0.9, 1e-4, 0.01)
-    assert L.hp_sample_workspace_bytes(4096, 100000, 3000, 32768, ctypes.byref(p),
+    assert L.hp_sample_workspace_bytes(4096, 100000, 32768, ctypes.byref(p),
                                        ctypes.byref(nb)) == 0 and nb.value > 0
 
 
