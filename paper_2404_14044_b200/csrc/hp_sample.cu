@@ -798,7 +798,9 @@ int dispatch_exact(const Csr& C, const Params& P, SampleWs& w, int64_t* needed, 
 
 int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleWs& w, cudaStream_t s) {
     TimedSpan ts("k_sample_retain", s);
-    k_sample_retain<<<kSampleGrid, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
+    // one ray per warp: as many warps in flight as the SMs hold (latency-bound)
+    const int64_t blocks = (C.m + kWarps - 1) / kWarps;
+    k_sample_retain<<<int(blocks < (1 << 30) ? blocks : (1 << 30)), kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
     HP_CHECK_LAUNCH("k_sample_retain");
     return HP_OK;
 }
