@@ -107,30 +107,31 @@ int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
                          void* workspace, size_t workspace_bytes, hp_stream_t stream);
 
 /* ---------------- query ---------------- */
-/* total: Q for hp_query_fill's workspace (it holds the unsorted matches),
- * 0 for hp_query_count. */
-int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t total, size_t* bytes);
-/* Pass 1.  cam: the index camera (host struct; NULL tests every pixel of the
- * s x s window, otherwise only pixels whose directions can lie inside the
- * ray's cone -- same result, fewer tests).  pixels: int64 [m,2] (u, v) with
- * element stride pixel_stride between rays (2 for an (m,2) array); dirs
- * float64 [m,3]; t_near/t_far/slopes [m].  Writes probes/scanned [m] (int64,
- * over the full window as the reference) and offsets [m+1] (int64 CSR
- * offsets; offsets[m] = Q). */
+/* capacity: scratch slots for the unsorted matches (hp_query_count reports
+ * the number it needs). */
+int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t capacity, size_t* bytes);
+/* Pass 1 (the streaming pass).  cam: the index camera (host struct; NULL
+ * tests every pixel of the s x s window, otherwise only pixels whose
+ * directions can lie inside the ray's cone -- same result, fewer tests).
+ * pixels: int64 [m,2] (u, v) with element stride pixel_stride between rays (2
+ * for an (m,2) array); dirs float64 [m,3]; t_near/t_far/slopes [m].  Writes
+ * probes/scanned [m] (int64, over the full window as the reference) and
+ * offsets [m+1] (int64 CSR offsets; offsets[m] = Q); the accepted matches are
+ * kept, unsorted, in the workspace.  Synchronises `stream` once to size that
+ * scratch: if it needs more than `capacity` slots, returns HP_ESPACE with the
+ * requirement in *needed (host pointer, may be NULL) and the caller retries
+ * with a larger workspace. */
 int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
                    int64_t pad,
                    const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                    const double* t_near, const double* t_far, const double* slopes, int64_t m,
-                   int64_t* offsets, int64_t* probes, int64_t* scanned, void* workspace,
-                   size_t workspace_bytes, hp_stream_t stream);
-/* Pass 2.  Same inputs + offsets from pass 1 and total = Q (host value).
- * Fills ids int64 [Q], t_proj / dist_perp float64 [Q], sorted by (t, id) per ray. */
-int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
-                  int64_t pad,
-                  const int64_t* pixels, int64_t pixel_stride, const double* dirs,
-                  const double* t_near, const double* t_far, const double* slopes, int64_t m,
-                  const int64_t* offsets, int64_t total, int64_t* ids, double* t_proj,
-                  double* dist_perp, void* workspace, size_t workspace_bytes,
+                   int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
+                   int64_t* needed, void* workspace, size_t workspace_bytes, hp_stream_t stream);
+/* Pass 2: sort each ray's matches by (t, id) from the workspace of pass 1
+ * (same buffer, same capacity) into ids int64 [Q], t_proj / dist_perp
+ * float64 [Q] (total = Q = offsets[m], host value). */
+int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, int64_t* ids, double* t_proj,
+                  double* dist_perp, int64_t capacity, void* workspace, size_t workspace_bytes,
                   hp_stream_t stream);
 
 /* ---------------- sample ---------------- */

@@ -226,93 +226,67 @@ __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64
     }
 }
 
-// ---------------------------------------------------------------- pass 1
-struct CountSmem {
-    GroupHead head;
-    float4 pf[2][kStageCount];
-    int cnt[kGroupMax], scn[kGroupMax];
-};
-
-__global__ void __launch_bounds__(kThreads) k_query_count(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
-                                                          int64_t m, int64_t* __restrict__ counts,
-                                                          int64_t* __restrict__ probes,
-                                                          int64_t* __restrict__ scanned) {
-    extern __shared__ __align__(16) unsigned char dyn[];
-    CountSmem& S = *reinterpret_cast<CountSmem*>(dyn);
+// ---------------------------------------------------------------- pass 0
+// Per-ray upper bound of the matches: the number of slots the streaming pass
+// will test for the ray (its footprint rows, exactly as stream_group
+// tabulates them).  Places each ray's unsorted-match scratch segment.
+__global__ void __launch_bounds__(kThreads) k_query_bound(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
+                                                          int64_t m, int64_t* __restrict__ bound) {
+    __shared__ GroupHead head;
+    __shared__ int acc[kGroupMax];
     const int s = 2 * pad + 1;
-    const float4* __restrict__ relf = reinterpret_cast<const float4*>(L.relf);
     for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
         const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
-        if (threadIdx.x < kGroupMax) S.cnt[threadIdx.x] = S.scn[threadIdx.x] = 0;
-        group_setup(S.head, R, QC, r0, G, s);
-        stream_group<kStageCount>(
-            S.head, G, L, wp, s, QC,
-            [&](int buf, int c0, int c1) {
-                for (int k = c0 + int(threadIdx.x); k < c1; k += kThreads) cp_async16(&S.pf[buf][k - c0], relf + k);
-            },
-            [&](int buf, int g, int k, int c0) {
-                int cls = 0;
-                if (k >= 0) {
-                    const RayParams& r = S.head.ray[g];
-                    cls = cone_filter(S.pf[buf][k - c0], r);
-                    if (cls == 2) {
-                        double t, d2;
-                        cls = cone_test(L.rel_x[k], L.rel_y[k], L.rel_z[k], r, t, d2) ? 1 : 0;
-                    }
-                }
-                const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
-                if (lane_id() == 0) S.cnt[g] += __popc(b);
-            },
-            [&](int g, int n) { atomicAdd(&S.scn[g], n); });
-        __syncthreads();
-        if (threadIdx.x < G) {
-            counts[r0 + threadIdx.x] = S.cnt[threadIdx.x];
-            probes[r0 + threadIdx.x] = int64_t(s) * s;
-            scanned[r0 + threadIdx.x] = S.scn[threadIdx.x];
+        if (threadIdx.x < kGroupMax) acc[threadIdx.x] = 0;
+        group_setup(head, R, QC, r0, G, s);
+        for (int idx = threadIdx.x; idx < s * G; idx += kThreads) {
+            const int row = idx / G, g = idx - row * G;
+            const RayParams& r = head.ray[g];
+            const int y = r.v + row;
+            int x0, x1;
+            if (footprint_row(head.fp[g], QC.C, pad, QC.width, QC.height, r.u, r.v, y, x0, x1)) {
+                const int64_t base = int64_t(y) * wp;
+                const int n = L.row_ptr[base + x1 + 1] - L.row_ptr[base + x0];
+                if (n > 0) atomicAdd(&acc[g], n);
+            }
         }
+        __syncthreads();
+        if (threadIdx.x < G) bound[r0 + threadIdx.x] = acc[threadIdx.x];
         __syncthreads();
     }
 }
 
-// ---------------------------------------------------------------- pass 2
+// ---------------------------------------------------------------- pass 1
 struct FillSmem {
     GroupHead head;
     float4 pf[2][kStageFill];
     double px[2][kStageFill], py[2][kStageFill], pz[2][kStageFill];
     int pid[2][kStageFill];
-    int fill[kGroupMax];
+    int fill[kGroupMax], scn[kGroupMax];
     int64_t off[kGroupMax];
 };
 
-template <int kCap>
-struct SortSmem;
-template <int kCap, int kT>
-__device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int* __restrict__ sid,
-                             const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
-                             double* __restrict__ gd);
 constexpr int kSortSmall = 2048;
 
-// Fill + sort: stream a group's rows, append accepted pairs (unsorted) to the
-// rays' scratch segments, then immediately sort the group's rays with
-// q <= kSortSmall from the scratch (still L2-resident) into the outputs.
-// Longer rays are left to k_query_sort.
-__global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
-                                                         int64_t m, const int64_t* __restrict__ off,
+// Pass 1 (the only streaming pass): stream a group's rows and append the
+// accepted pairs (t, id, dist), unsorted, to each ray's scratch segment at
+// soff[r] (capacity from k_query_bound); write the exact count, probes and
+// scanned of every ray.
+__global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
+                                                         int64_t m, const int64_t* __restrict__ soff,
                                                          int* __restrict__ sc_id, double* __restrict__ sc_t,
-                                                         double* __restrict__ sc_d, int64_t* __restrict__ out_id,
-                                                         double* __restrict__ out_t, double* __restrict__ out_d) {
+                                                         double* __restrict__ sc_d, int64_t* __restrict__ counts,
+                                                         int64_t* __restrict__ probes, int64_t* __restrict__ scanned) {
     extern __shared__ __align__(16) unsigned char dyn[];
     FillSmem& S = *reinterpret_cast<FillSmem*>(dyn);
     const int s = 2 * pad + 1;
     const float4* __restrict__ relf = reinterpret_cast<const float4*>(L.relf);
     for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
         const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
-        // skip groups without matches
-        const int64_t total = off[r0 + G] - off[r0];
-        if (total == 0) continue;
         if (threadIdx.x < G) {
             S.fill[threadIdx.x] = 0;
-            S.off[threadIdx.x] = off[r0 + threadIdx.x];
+            S.scn[threadIdx.x] = 0;
+            S.off[threadIdx.x] = soff[r0 + threadIdx.x];
         }
         group_setup(S.head, R, QC, r0, G, s);
         stream_group<kStageFill>(
@@ -350,15 +324,14 @@ __global__ void __launch_bounds__(kThreads) k_query_fill(hp_query_layout L, int6
                 if (lane_id() == 0) S.fill[g] += __popc(b);
                 __syncwarp();
             },
-            [&](int, int) {});
+            [&](int g, int n) { atomicAdd(&S.scn[g], n); });
         __syncthreads();
-        for (int g = 0; g < G; g++) {
-            const int64_t o = off[r0 + g];
-            const int64_t q = off[r0 + g + 1] - o;
-            if (q < 1 || q > kSortSmall) continue;
-            sort_segment<kSortSmall, kThreads>(*reinterpret_cast<SortSmem<kSortSmall>*>(dyn), int(q), sc_t + o,
-                                               sc_id + o, sc_d + o, out_id + o, out_t + o, out_d + o);
+        if (threadIdx.x < G) {
+            counts[r0 + threadIdx.x] = S.fill[threadIdx.x];
+            probes[r0 + threadIdx.x] = int64_t(s) * s;
+            scanned[r0 + threadIdx.x] = S.scn[threadIdx.x];
         }
+        __syncthreads();
     }
 }
 
@@ -547,7 +520,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q <= kSortSmall ? -1 : (q <= kSortLarge ? 1 : 2);  // small rays: sorted by k_query_fill
+            cls = q == 0 ? -1 : (q <= kSortSmall ? 0 : (q <= kSortLarge ? 1 : 2));
         }
 #pragma unroll
         for (int c = 0; c < 3; c++) {  // warp-aggregated append
@@ -561,11 +534,12 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
     }
 }
 
-// Sort the rays of one size class (list of ray ids) from the fill scratch
-// into the outputs: in shared memory when kCap > 0; with an in-place sorting
-// network on the scratch then a copy when kCap == 0.
+// Sort the rays of one size class (list of ray ids) from the scratch (ray r
+// at soff[r]) into the outputs (at off[r]): in shared memory when kCap > 0;
+// with an in-place sorting network on the scratch then a copy when kCap == 0.
 template <int kCap, int kT>
-__global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int* __restrict__ list,
+__global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int64_t* __restrict__ soff,
+                                                   const int* __restrict__ list,
                                                    const int* __restrict__ list_n, double* __restrict__ st,
                                                    int* __restrict__ sid, double* __restrict__ sd,
                                                    int64_t* __restrict__ out_id, double* __restrict__ out_t,
@@ -574,15 +548,15 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
     const int n = *list_n;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
         const int64_t r = list[k];
-        const int64_t o = off[r];
+        const int64_t o = off[r], so = soff[r];
         const int64_t q = off[r + 1] - o;
         if constexpr (kCap > 0) {
-            sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), st + o, sid + o, sd + o,
+            sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), st + so, sid + so, sd + so,
                                    out_id + o, out_t + o, out_d + o);
         } else {
-            double* tt = st + o;
-            double* dd = sd + o;
-            int* ii = sid + o;
+            double* tt = st + so;
+            double* dd = sd + so;
+            int* ii = sid + so;
             block_bitonic_sort(
                 q, [&](int64_t a, int64_t b) { return key_less(tt[a], ii[a], tt[b], ii[b]); },
                 [&](int64_t a, int64_t b) {
@@ -607,8 +581,6 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
     }
 }
 
-constexpr size_t kFillSmemBytes =
-    sizeof(FillSmem) > sizeof(SortSmem<kSortSmall>) ? sizeof(FillSmem) : sizeof(SortSmem<kSortSmall>);
 
 template <class K>
 int set_smem(K kernel, size_t bytes) {
@@ -659,39 +631,49 @@ unsigned group_grid(int64_t m, int per_sm) {
 
 using namespace hp;
 
-static void carve_fill(Carver& c, int64_t m, int64_t total, int** lists, int** counts, double** st, int** sid,
-                       double** sd) {
-    c.take<char>(scan_workspace_bytes(m + 1));
-    *lists = c.take<int>(3 * (m > 0 ? m : 1));
-    *counts = c.take<int>(64);
-    *st = c.take<double>(total > 0 ? total : 1);
-    *sid = c.take<int>(total > 0 ? total : 1);
-    *sd = c.take<double>(total > 0 ? total : 1);
+// workspace: scan scratch | scratch offsets soff [m+1] | 3 ray lists of the
+// sort size classes | class counts | unsorted matches (t, id, dist) x capacity
+struct QueryWs {
+    void* scan;
+    int64_t* soff;
+    int* lists;
+    int* counts;
+    double* st;
+    int* sid;
+    double* sd;
+};
+
+static QueryWs carve_query(Carver& c, int64_t m, int64_t cap) {
+    QueryWs w;
+    w.scan = c.take<char>(scan_workspace_bytes(m + 1));
+    w.soff = c.take<int64_t>(m + 1);
+    w.lists = c.take<int>(3 * (m > 0 ? m : 1));
+    w.counts = c.take<int>(64);
+    w.st = c.take<double>(cap > 0 ? cap : 1);
+    w.sid = c.take<int>(cap > 0 ? cap : 1);
+    w.sd = c.take<double>(cap > 0 ? cap : 1);
+    return w;
 }
 
-extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t total, size_t* bytes) {
-    // scan scratch | 3 ray lists of the sort size classes | counts | unsorted
-    // matches (t, id, dist) written by the fill pass (total = Q; 0 for pass 1)
+extern "C" int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t capacity, size_t* bytes) {
     Carver c(nullptr, 0);
-    int* l;
-    int* cn;
-    double *st, *sd;
-    int* sid;
-    carve_fill(c, m, total, &l, &cn, &st, &sid, &sd);
+    carve_query(c, m, capacity);
     *bytes = c.used + 256;
     (void)pad;
     return HP_OK;
 }
 
 extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
-                              int64_t pad,
-                              const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                              int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                               const double* t_near, const double* t_far, const double* slopes, int64_t m,
-                              int64_t* offsets, int64_t* probes, int64_t* scanned, void* workspace,
-                              size_t workspace_bytes, hp_stream_t stream) {
+                              int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
+                              int64_t* needed, void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(check_common(layout, pad, m));
     (void)padded_h;
-    if (workspace_bytes < scan_workspace_bytes(m + 1)) {
+    if (needed) *needed = 0;
+    Carver cv(workspace, workspace_bytes);
+    QueryWs w = carve_query(cv, m, capacity);
+    if (!cv.ok()) {
         set_error("hp_query_count: workspace too small");
         return HP_ESPACE;
     }
@@ -699,65 +681,73 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
     Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
     const QCam QC = make_qcam(cam);
     if (m > 0) {
+        {
+            TimedSpan ts("k_query_bound", s);
+            k_query_bound<<<group_grid(m, 8), kThreads, 0, s>>>(layout, padded_w, int(pad), R, QC, m, w.soff);
+            HP_CHECK_LAUNCH("k_query_bound");
+        }
+        HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
+        int64_t need = 0;
+        cudaError_t e = cudaMemcpyAsync(&need, w.soff + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_status(e, "hp_query_count: bound");
+        if (needed) *needed = need;
+        if (need > capacity) {
+            set_error("hp_query_count: %lld scratch slots needed, capacity %lld", (long long)need,
+                      (long long)capacity);
+            return HP_ESPACE;
+        }
         static bool attr = false;
         if (!attr) {
-            HP_TRY(set_smem(k_query_count, sizeof(CountSmem)));
+            HP_TRY(set_smem(k_query_scan, sizeof(FillSmem)));
             attr = true;
         }
-        TimedSpan ts("k_query_count", s);
-        k_query_count<<<group_grid(m, 7), kThreads, sizeof(CountSmem), s>>>(layout, padded_w, int(pad), R, QC, m,
-                                                                            offsets, probes, scanned);
-        HP_CHECK_LAUNCH("k_query_count");
+        TimedSpan ts("k_query_scan", s);
+        k_query_scan<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
+                                                                         w.sid, w.st, w.sd, offsets, probes, scanned);
+        HP_CHECK_LAUNCH("k_query_scan");
     }
-    HP_TRY(exclusive_scan_i64(offsets, offsets, m, workspace, s));
+    HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
     return HP_OK;
 }
 
-extern "C" int hp_query_fill(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
-                             int64_t pad,
-                             const int64_t* pixels, int64_t pixel_stride, const double* dirs,
-                             const double* t_near, const double* t_far, const double* slopes, int64_t m,
-                             const int64_t* offsets, int64_t total, int64_t* ids, double* t_proj,
-                             double* dist_perp, void* workspace, size_t workspace_bytes,
+extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, int64_t* ids, double* t_proj,
+                             double* dist_perp, int64_t capacity, void* workspace, size_t workspace_bytes,
                              hp_stream_t stream) {
-    HP_TRY(check_common(layout, pad, m));
-    (void)padded_h;
+    if (m < 0 || total < 0) {
+        set_error("hp_query_fill: invalid arguments");
+        return HP_EINVAL;
+    }
     if (m == 0 || total == 0) return HP_OK;
     Carver cv(workspace, workspace_bytes);
-    int* lists;
-    int* counts;
-    double *st, *sd;
-    int* sid;
-    carve_fill(cv, m, total, &lists, &counts, &st, &sid, &sd);
+    QueryWs w = carve_query(cv, m, capacity);
     if (!cv.ok()) {
         set_error("hp_query_fill: workspace too small");
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
-    const QCam QC = make_qcam(cam);
     static bool attr = false;
     if (!attr) {
-        HP_TRY(set_smem(k_query_fill, kFillSmemBytes));
+        HP_TRY(set_smem(k_query_sort<kSortSmall, kThreads>, sizeof(SortSmem<kSortSmall>)));
         HP_TRY(set_smem(k_query_sort<kSortLarge, kSortLargeThreads>, sizeof(SortSmem<kSortLarge>)));
         attr = true;
     }
-    {
-        TimedSpan ts("k_query_fill", s);
-        k_query_fill<<<group_grid(m, 3), kThreads, kFillSmemBytes, s>>>(layout, padded_w, int(pad), R, QC, m,
-                                                                        offsets, sid, st, sd, ids, t_proj, dist_perp);
-        HP_CHECK_LAUNCH("k_query_fill");
-    }
-    TimedSpan ts("k_query_sort", s);
-    if (cudaMemsetAsync(counts, 0, 3 * sizeof(int), s) != cudaSuccess)
+    if (cudaMemsetAsync(w.counts, 0, 3 * sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
-    k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, counts);
+    k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, w.lists, w.counts);
     HP_CHECK_LAUNCH("k_sort_classes");
+    {
+        TimedSpan ts("k_query_sort", s);
+        k_query_sort<kSortSmall, kThreads><<<kNumSMs * 3, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
+            offsets, w.soff, w.lists, w.counts, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
+        HP_CHECK_LAUNCH("k_query_sort<small>");
+    }
+    TimedSpan ts("k_query_sort_large", s);
     k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs, kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
-        offsets, lists + m, counts + 1, st, sid, sd, ids, t_proj, dist_perp);
+        offsets, w.soff, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
-    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, lists + 2 * m, counts + 2, st, sid, sd, ids,
-                                                           t_proj, dist_perp);
+    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.lists + 2 * m, w.counts + 2, w.st,
+                                                           w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
 }

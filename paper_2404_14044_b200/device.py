@@ -21,6 +21,9 @@ from ._lib import c_i64, c_size
 __all__ = ["DeviceIndex", "build", "build_from_table", "query", "sample", "primary_surface",
            "SAMPLE_EXACT_PER_RAY"]
 
+# match-scratch capacity of the last query per device (slots), reused so a
+# steady stream of frames sizes its workspace once
+_QUERY_CAP: dict = {}
 SAMPLE_EXACT_PER_RAY = 16  # initial exact-candidate scratch per ray (grown on demand)
 
 # Optional per-kernel timer (pipeline.StageTimer); set by the benchmark.
@@ -171,8 +174,6 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     pixels = pixels.contiguous()
     dirs = dirs.contiguous()
     nb = c_size(0)
-    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, 0, ctypes.byref(nb)))
-    ws = _workspace(nb.value, dev)
     offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
     probes = torch.empty(m, dtype=torch.int64, device=dev)
     scanned = torch.empty(m, dtype=torch.int64, device=dev)
@@ -180,19 +181,28 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     cam = ctypes.byref(camera_struct(index.camera)) if footprint else None
     args = (L, cam, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
+    needed = c_i64(0)
+    cap = _QUERY_CAP.get(dev, 0)
     _mark("query.setup")
-    _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), _ptr(ws),
-                                  nb.value, _stream()))
+    for _ in range(2):
+        _lib.check(lib.hp_query_workspace_bytes(m, index.pad, cap, ctypes.byref(nb)))
+        ws = _workspace(nb.value, dev)
+        rc = lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap,
+                                ctypes.byref(needed), _ptr(ws), nb.value, _stream())
+        if rc == _lib.HP_ESPACE and needed.value > cap:
+            cap = int(needed.value * 1.0625) + 1024   # grow the match scratch once (and remember)
+            _QUERY_CAP[dev] = cap
+            continue
+        _lib.check(rc)
+        break
     _mark("query.count")
     total = int(offsets[m].item())
-    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, total, ctypes.byref(nb)))
-    ws = _workspace(nb.value, dev)
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
     _mark("query.sync")
-    _lib.check(lib.hp_query_fill(*args, _ptr(offsets), total, _ptr(ids), _ptr(t), _ptr(d),
-                                 _ptr(ws), nb.value, _stream()))
+    _lib.check(lib.hp_query_fill(_ptr(offsets), m, total, _ptr(ids), _ptr(t), _ptr(d), cap, _ptr(ws),
+                                 nb.value, _stream()))
     _mark("query.fill")
     return offsets, ids, t, d, probes, scanned
 
