@@ -267,6 +267,7 @@ struct FillSmem {
 };
 
 constexpr int kSortSmall = 2048;
+constexpr int kSortTiny = 1024;
 
 // Pass 1 (the only streaming pass): stream a group's rows and append the
 // accepted pairs (t, id, dist), unsorted, to each ray's scratch segment at
@@ -510,9 +511,10 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
 }
 
 constexpr int kSortLarge = 4096;
-constexpr int kSortLargeThreads = 512;
+constexpr int kSortLargeThreads = 1024;
 
-// Size classes of rays to sort: [1, kSortSmall], (kSortSmall, kSortLarge], above.
+// Size classes of rays to sort: [1, kSortTiny], (kSortTiny, kSortSmall],
+// (kSortSmall, kSortLarge], above.
 __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
                                int* __restrict__ counts) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
@@ -520,10 +522,10 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q == 0 ? -1 : (q <= kSortSmall ? 0 : (q <= kSortLarge ? 1 : 2));
+            cls = q == 0 ? -1 : (q <= kSortTiny ? 0 : (q <= kSortSmall ? 1 : (q <= kSortLarge ? 2 : 3)));
         }
 #pragma unroll
-        for (int c = 0; c < 3; c++) {  // warp-aggregated append
+        for (int c = 0; c < 4; c++) {  // warp-aggregated append
             const unsigned b = __ballot_sync(0xffffffffu, cls == c);
             if (!b) continue;
             int base = 0;
@@ -647,7 +649,7 @@ static QueryWs carve_query(Carver& c, int64_t m, int64_t cap) {
     QueryWs w;
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     w.soff = c.take<int64_t>(m + 1);
-    w.lists = c.take<int>(3 * (m > 0 ? m : 1));
+    w.lists = c.take<int>(4 * (m > 0 ? m : 1));
     w.counts = c.take<int>(64);
     w.st = c.take<double>(cap > 0 ? cap : 1);
     w.sid = c.take<int>(cap > 0 ? cap : 1);
@@ -728,25 +730,29 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     static bool attr = false;
     if (!attr) {
+        HP_TRY(set_smem(k_query_sort<kSortTiny, kThreads>, sizeof(SortSmem<kSortTiny>)));
         HP_TRY(set_smem(k_query_sort<kSortSmall, kThreads>, sizeof(SortSmem<kSortSmall>)));
         HP_TRY(set_smem(k_query_sort<kSortLarge, kSortLargeThreads>, sizeof(SortSmem<kSortLarge>)));
         attr = true;
     }
-    if (cudaMemsetAsync(w.counts, 0, 3 * sizeof(int), s) != cudaSuccess)
+    if (cudaMemsetAsync(w.counts, 0, 4 * sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, w.lists, w.counts);
     HP_CHECK_LAUNCH("k_sort_classes");
     {
         TimedSpan ts("k_query_sort", s);
-        k_query_sort<kSortSmall, kThreads><<<kNumSMs * 3, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
+        k_query_sort<kSortTiny, kThreads><<<kNumSMs * 6, kThreads, sizeof(SortSmem<kSortTiny>), s>>>(
             offsets, w.soff, w.lists, w.counts, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
+        HP_CHECK_LAUNCH("k_query_sort<tiny>");
+        k_query_sort<kSortSmall, kThreads><<<kNumSMs * 3, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
+            offsets, w.soff, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_sort<small>");
     }
     TimedSpan ts("k_query_sort_large", s);
     k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs, kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
-        offsets, w.soff, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
+        offsets, w.soff, w.lists + 2 * m, w.counts + 2, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
-    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.lists + 2 * m, w.counts + 2, w.st,
+    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.lists + 3 * m, w.counts + 3, w.st,
                                                            w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
