@@ -226,6 +226,15 @@ __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64
     }
 }
 
+// Order-preserving uint32 key of a float (and back).
+__device__ __forceinline__ unsigned fkey(float x) {
+    const unsigned u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float from_fkey(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 // ---------------------------------------------------------------- pass 0
 // Per-ray upper bound of the matches: the number of slots the streaming pass
 // will test for the ray (its footprint rows, exactly as stream_group
@@ -263,6 +272,7 @@ struct FillSmem {
     double px[2][kStageFill], py[2][kStageFill], pz[2][kStageFill];
     int pid[2][kStageFill];
     int fill[kGroupMax], scn[kGroupMax];
+    unsigned tmin[kGroupMax], tmax[kGroupMax];  // fkey bounds of the accepted t (for the sort)
     int64_t off[kGroupMax];
 };
 
@@ -276,7 +286,8 @@ constexpr int kSortTiny = 1024;
 __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
                                                          int64_t m, const int64_t* __restrict__ soff,
                                                          int* __restrict__ sc_id, double* __restrict__ sc_t,
-                                                         double* __restrict__ sc_d, int64_t* __restrict__ counts,
+                                                         double* __restrict__ sc_d, uint2* __restrict__ tmm,
+                                                         int64_t* __restrict__ counts,
                                                          int64_t* __restrict__ probes, int64_t* __restrict__ scanned) {
     extern __shared__ __align__(16) unsigned char dyn[];
     FillSmem& S = *reinterpret_cast<FillSmem*>(dyn);
@@ -287,6 +298,8 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
         if (threadIdx.x < G) {
             S.fill[threadIdx.x] = 0;
             S.scn[threadIdx.x] = 0;
+            S.tmin[threadIdx.x] = 0xffffffffu;
+            S.tmax[threadIdx.x] = 0u;
             S.off[threadIdx.x] = soff[r0 + threadIdx.x];
         }
         group_setup(S.head, R, QC, r0, G, s);
@@ -315,19 +328,31 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
                     }
                 }
                 const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
-                if (cls == 1) {
-                    const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
-                    sc_t[pos] = t;
-                    sc_d[pos] = sqrt(d2);
-                    sc_id[pos] = S.pid[buf][k - c0];
+                if (b) {
+                    unsigned lo = 0xffffffffu, hi = 0u;
+                    if (cls == 1) {
+                        const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
+                        sc_t[pos] = t;
+                        sc_d[pos] = sqrt(d2);
+                        sc_id[pos] = S.pid[buf][k - c0];
+                        lo = fkey(__double2float_rd(t));
+                        hi = fkey(__double2float_ru(t));
+                    }
+                    lo = __reduce_min_sync(0xffffffffu, lo);
+                    hi = __reduce_max_sync(0xffffffffu, hi);
+                    __syncwarp();
+                    if (lane_id() == 0) {  // ray g belongs to this warp alone
+                        S.fill[g] += __popc(b);
+                        S.tmin[g] = min(S.tmin[g], lo);
+                        S.tmax[g] = max(S.tmax[g], hi);
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
-                if (lane_id() == 0) S.fill[g] += __popc(b);
-                __syncwarp();
             },
             [&](int g, int n) { atomicAdd(&S.scn[g], n); });
         __syncthreads();
         if (threadIdx.x < G) {
+            tmm[r0 + threadIdx.x] = make_uint2(S.tmin[threadIdx.x], S.tmax[threadIdx.x]);
             counts[r0 + threadIdx.x] = S.fill[threadIdx.x];
             probes[r0 + threadIdx.x] = int64_t(s) * s;
             scanned[r0 + threadIdx.x] = S.scn[threadIdx.x];
@@ -353,7 +378,6 @@ struct SortSmem {
     unsigned short perm[kCap];
     int hist[kCap + 1];
     int chist[kCoarse + 1];
-    unsigned long long tmin, tmax;
     int scan_sh[33];
 };
 
@@ -390,20 +414,24 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
 // buckets are ordered; each element's final position is its bucket start
 // plus its exact (t, id) rank among the (few) members of its bucket.
 template <int kCap, int kT>
-__device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict__ st, const int* __restrict__ sid,
-                             const double* __restrict__ sd, int64_t* __restrict__ gid, double* __restrict__ gt,
-                             double* __restrict__ gd) {
+__device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* __restrict__ st,
+                             const int* __restrict__ sid, const double* __restrict__ sd, int64_t* __restrict__ gid,
+                             double* __restrict__ gt, double* __restrict__ gd) {
     const int tid = threadIdx.x;
-    // all of the segment's loads in flight at once (L2-resident scratch)
+    // all of the segment's loads in flight at once
     for (int e = tid; e < q; e += kT) {
         cp_async8(&F.t[e], st + e);
         cp_async8(&F.d[e], sd + e);
         cp_async4(&F.id[e], sid + e);
     }
     cp_commit();
+    if (q > 64) {
+        for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
+        for (int k = tid; k <= q; k += kT) F.hist[k] = 0;
+    }
     cp_wait<0>();
+    __syncthreads();
     if (q <= 64) {
-        __syncthreads();
         for (int e = tid; e < q; e += kT) {
             const double te = F.t[e];
             const int ie = F.id[e];
@@ -414,32 +442,9 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, const double* __restrict_
         __syncthreads();
     } else {
         const int nb = q;  // fine buckets
-        if (tid == 0) {
-            F.tmin = ~0ull;
-            F.tmax = 0ull;
-        }
-        for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
-        for (int k = tid; k <= nb; k += kT) F.hist[k] = 0;
-        __syncthreads();
-        unsigned long long lmin = ~0ull, lmax = 0;
-        for (int e = tid; e < q; e += kT) {
-            const unsigned long long kk = okey(F.t[e]);
-            lmin = lmin < kk ? lmin : kk;
-            lmax = lmax > kk ? lmax : kk;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long x = __shfl_xor_sync(0xffffffffu, lmin, o);
-            const unsigned long long y = __shfl_xor_sync(0xffffffffu, lmax, o);
-            lmin = lmin < x ? lmin : x;
-            lmax = lmax > y ? lmax : y;
-        }
-        if (lane_id() == 0) {
-            atomicMin(&F.tmin, lmin);
-            atomicMax(&F.tmax, lmax);
-        }
-        __syncthreads();
-        const double tlo = from_okey(F.tmin), thi = from_okey(F.tmax);
+        // float bounds of the segment's t, from the streaming pass (any
+        // monotone bucket map gives the same order: exact in-bucket ranks)
+        const double tlo = double(from_fkey(mm.x)), thi = double(from_fkey(mm.y));
         const double span = dsub(thi, tlo);
         // capped so that 0 * scale stays 0 when the span is tiny
         const double cscale = span > 0.0 ? fmin(__ddiv_rn(double(kCoarse), span), DBL_MAX) : 0.0;
@@ -541,7 +546,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
 // with an in-place sorting network on the scratch then a copy when kCap == 0.
 template <int kCap, int kT>
 __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int64_t* __restrict__ soff,
-                                                   const int* __restrict__ list,
+                                                   const uint2* __restrict__ tmm, const int* __restrict__ list,
                                                    const int* __restrict__ list_n, double* __restrict__ st,
                                                    int* __restrict__ sid, double* __restrict__ sd,
                                                    int64_t* __restrict__ out_id, double* __restrict__ out_t,
@@ -553,7 +558,7 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
         const int64_t o = off[r], so = soff[r];
         const int64_t q = off[r + 1] - o;
         if constexpr (kCap > 0) {
-            sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), st + so, sid + so, sd + so,
+            sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), tmm[r], st + so, sid + so, sd + so,
                                    out_id + o, out_t + o, out_d + o);
         } else {
             double* tt = st + so;
@@ -638,6 +643,7 @@ using namespace hp;
 struct QueryWs {
     void* scan;
     int64_t* soff;
+    uint2* tmm;
     int* lists;
     int* counts;
     double* st;
@@ -649,6 +655,7 @@ static QueryWs carve_query(Carver& c, int64_t m, int64_t cap) {
     QueryWs w;
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     w.soff = c.take<int64_t>(m + 1);
+    w.tmm = c.take<uint2>(m > 0 ? m : 1);
     w.lists = c.take<int>(4 * (m > 0 ? m : 1));
     w.counts = c.take<int>(64);
     w.st = c.take<double>(cap > 0 ? cap : 1);
@@ -706,7 +713,8 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
         }
         TimedSpan ts("k_query_scan", s);
         k_query_scan<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
-                                                                         w.sid, w.st, w.sd, offsets, probes, scanned);
+                                                                         w.sid, w.st, w.sd, w.tmm, offsets, probes,
+                                                                         scanned);
         HP_CHECK_LAUNCH("k_query_scan");
     }
     HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
@@ -742,17 +750,17 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     {
         TimedSpan ts("k_query_sort", s);
         k_query_sort<kSortTiny, kThreads><<<kNumSMs * 6, kThreads, sizeof(SortSmem<kSortTiny>), s>>>(
-            offsets, w.soff, w.lists, w.counts, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
+            offsets, w.soff, w.tmm, w.lists, w.counts, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_sort<tiny>");
         k_query_sort<kSortSmall, kThreads><<<kNumSMs * 3, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
-            offsets, w.soff, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
+            offsets, w.soff, w.tmm, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_sort<small>");
     }
     TimedSpan ts("k_query_sort_large", s);
     k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs, kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
-        offsets, w.soff, w.lists + 2 * m, w.counts + 2, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
+        offsets, w.soff, w.tmm, w.lists + 2 * m, w.counts + 2, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
-    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.lists + 3 * m, w.counts + 3, w.st,
+    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, w.lists + 3 * m, w.counts + 3, w.st,
                                                            w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
