@@ -371,12 +371,16 @@ constexpr int kCoarse = 256;
 template <int kCap>
 struct SortSmem {
     double t[kCap];
-    double d[kCap];         // dist, staged with t/id (no gather at the end)
-    int id[kCap];           // point ids < 2^31 (hp_build)
-    unsigned int bk[kCap];  // fine bucket << 16 | local index
+    int id[kCap];  // point ids < 2^31 (hp_build)
+    union {
+        struct {
+            unsigned int bk[kCap];  // fine bucket << 16 | local index
+            int hist[kCap + 1];
+        };
+        double d[kCap];  // dist, loaded once the ranks are known
+    };
     unsigned short lst[kCap];
     unsigned short perm[kCap];
-    int hist[kCap + 1];
     int chist[kCoarse + 1];
     int scan_sh[33];
 };
@@ -421,7 +425,6 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* _
     // all of the segment's loads in flight at once
     for (int e = tid; e < q; e += kT) {
         cp_async8(&F.t[e], st + e);
-        cp_async8(&F.d[e], sd + e);
         cp_async4(&F.id[e], sid + e);
     }
     cp_commit();
@@ -506,17 +509,22 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* _
         }
         __syncthreads();
     }
+    // dist into the (now free) bucket arrays, in flight while t / id go out
+    for (int e = tid; e < q; e += kT) cp_async8(&F.d[e], sd + e);
+    cp_commit();
     for (int p = tid; p < q; p += kT) {
         const int e = F.perm[p];
         gt[p] = F.t[e];
         gid[p] = F.id[e];
-        gd[p] = F.d[e];
     }
+    cp_wait<0>();
+    __syncthreads();
+    for (int p = tid; p < q; p += kT) gd[p] = F.d[F.perm[p]];
     __syncthreads();
 }
 
 constexpr int kSortLarge = 4096;
-constexpr int kSortLargeThreads = 1024;
+constexpr int kSortLargeThreads = 512;
 
 // Size classes of rays to sort: [1, kSortTiny], (kSortTiny, kSortSmall],
 // (kSortSmall, kSortLarge], above.
@@ -588,6 +596,17 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
     }
 }
 
+
+// Resident CTAs per SM of a kernel at its block size / dynamic smem (>= 1).
+template <class K>
+int resident(K kernel, int threads, size_t smem) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = 1;
+    }
+    return n;
+}
 
 template <class K>
 int set_smem(K kernel, size_t bytes) {
@@ -737,10 +756,15 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     static bool attr = false;
+    static int occ[3];
     if (!attr) {
         HP_TRY(set_smem(k_query_sort<kSortTiny, kThreads>, sizeof(SortSmem<kSortTiny>)));
         HP_TRY(set_smem(k_query_sort<kSortSmall, kThreads>, sizeof(SortSmem<kSortSmall>)));
         HP_TRY(set_smem(k_query_sort<kSortLarge, kSortLargeThreads>, sizeof(SortSmem<kSortLarge>)));
+        occ[0] = resident(k_query_sort<kSortTiny, kThreads>, kThreads, sizeof(SortSmem<kSortTiny>));
+        occ[1] = resident(k_query_sort<kSortSmall, kThreads>, kThreads, sizeof(SortSmem<kSortSmall>));
+        occ[2] = resident(k_query_sort<kSortLarge, kSortLargeThreads>, kSortLargeThreads,
+                          sizeof(SortSmem<kSortLarge>));
         attr = true;
     }
     if (cudaMemsetAsync(w.counts, 0, 4 * sizeof(int), s) != cudaSuccess)
@@ -749,15 +773,15 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     HP_CHECK_LAUNCH("k_sort_classes");
     {
         TimedSpan ts("k_query_sort", s);
-        k_query_sort<kSortTiny, kThreads><<<kNumSMs * 6, kThreads, sizeof(SortSmem<kSortTiny>), s>>>(
+        k_query_sort<kSortTiny, kThreads><<<kNumSMs * occ[0], kThreads, sizeof(SortSmem<kSortTiny>), s>>>(
             offsets, w.soff, w.tmm, w.lists, w.counts, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_sort<tiny>");
-        k_query_sort<kSortSmall, kThreads><<<kNumSMs * 3, kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
+        k_query_sort<kSortSmall, kThreads><<<kNumSMs * occ[1], kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
             offsets, w.soff, w.tmm, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
         HP_CHECK_LAUNCH("k_query_sort<small>");
     }
     TimedSpan ts("k_query_sort_large", s);
-    k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs, kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
+    k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs * occ[2], kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
         offsets, w.soff, w.tmm, w.lists + 2 * m, w.counts + 2, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<large>");
     k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, w.lists + 3 * m, w.counts + 3, w.st,
