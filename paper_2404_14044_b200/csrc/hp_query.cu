@@ -276,8 +276,6 @@ struct FillSmem {
     int64_t off[kGroupMax];
 };
 
-constexpr int kSortSmall = 2048;
-constexpr int kSortTiny = 1024;
 
 // Pass 1 (the only streaming pass): stream a group's rows and append the
 // accepted pairs (t, id, dist), unsorted, to each ray's scratch segment at
@@ -526,8 +524,11 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* _
 constexpr int kSortLarge = 4096;
 constexpr int kSortLargeThreads = 512;
 
-// Size classes of rays to sort: [1, kSortTiny], (kSortTiny, kSortSmall],
-// (kSortSmall, kSortLarge], above.
+// Size classes of rays to sort (by match count): shared-memory sorts with
+// capacities kSortCap (smaller capacity = more resident CTAs), then the
+// global-memory class above kSortLarge.
+constexpr int kSortClasses = 3;
+__constant__ int kSortCap[kSortClasses] = {1024, 2048, 4096};
 __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
                                int* __restrict__ counts) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
@@ -535,10 +536,13 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q == 0 ? -1 : (q <= kSortTiny ? 0 : (q <= kSortSmall ? 1 : (q <= kSortLarge ? 2 : 3)));
+            cls = q == 0 ? -1 : kSortClasses;
+#pragma unroll
+            for (int c = kSortClasses - 1; c >= 0; c--)
+                if (q <= kSortCap[c]) cls = c;
         }
 #pragma unroll
-        for (int c = 0; c < 4; c++) {  // warp-aggregated append
+        for (int c = 0; c <= kSortClasses; c++) {  // warp-aggregated append
             const unsigned b = __ballot_sync(0xffffffffu, cls == c);
             if (!b) continue;
             int base = 0;
@@ -657,8 +661,9 @@ unsigned group_grid(int64_t m, int per_sm) {
 
 using namespace hp;
 
-// workspace: scan scratch | scratch offsets soff [m+1] | 3 ray lists of the
-// sort size classes | class counts | unsorted matches (t, id, dist) x capacity
+// workspace: scan scratch | scratch offsets soff [m+1] | per-ray float t
+// bounds | ray lists of the sort size classes | class counts | unsorted
+// matches (t, id, dist) x capacity
 struct QueryWs {
     void* scan;
     int64_t* soff;
@@ -670,12 +675,37 @@ struct QueryWs {
     double* sd;
 };
 
+struct SortArgs {
+    const int64_t* offsets;
+    QueryWs w;
+    int64_t m;
+    int64_t* ids;
+    double* t;
+    double* d;
+};
+
+// One shared-memory size class: grid = SMs x resident CTAs (occupancy API).
+template <int kCap, int kT>
+static int launch_sort(const SortArgs& A, int cls, cudaStream_t s) {
+    static int occ = 0;
+    if (!occ) {
+        HP_TRY(set_smem(k_query_sort<kCap, kT>, sizeof(SortSmem<kCap>)));
+        occ = resident(k_query_sort<kCap, kT>, kT, sizeof(SortSmem<kCap>));
+    }
+    k_query_sort<kCap, kT><<<kNumSMs * occ, kT, sizeof(SortSmem<kCap>), s>>>(
+        A.offsets, A.w.soff, A.w.tmm, A.w.lists + int64_t(cls) * A.m, A.w.counts + cls, A.w.st, A.w.sid, A.w.sd,
+        A.ids, A.t, A.d);
+    HP_CHECK_LAUNCH("k_query_sort");
+    return HP_OK;
+}
+
+
 static QueryWs carve_query(Carver& c, int64_t m, int64_t cap) {
     QueryWs w;
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     w.soff = c.take<int64_t>(m + 1);
     w.tmm = c.take<uint2>(m > 0 ? m : 1);
-    w.lists = c.take<int>(4 * (m > 0 ? m : 1));
+    w.lists = c.take<int>((kSortClasses + 1) * (m > 0 ? m : 1));
     w.counts = c.take<int>(64);
     w.st = c.take<double>(cap > 0 ? cap : 1);
     w.sid = c.take<int>(cap > 0 ? cap : 1);
@@ -755,37 +785,21 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    static bool attr = false;
-    static int occ[3];
-    if (!attr) {
-        HP_TRY(set_smem(k_query_sort<kSortTiny, kThreads>, sizeof(SortSmem<kSortTiny>)));
-        HP_TRY(set_smem(k_query_sort<kSortSmall, kThreads>, sizeof(SortSmem<kSortSmall>)));
-        HP_TRY(set_smem(k_query_sort<kSortLarge, kSortLargeThreads>, sizeof(SortSmem<kSortLarge>)));
-        occ[0] = resident(k_query_sort<kSortTiny, kThreads>, kThreads, sizeof(SortSmem<kSortTiny>));
-        occ[1] = resident(k_query_sort<kSortSmall, kThreads>, kThreads, sizeof(SortSmem<kSortSmall>));
-        occ[2] = resident(k_query_sort<kSortLarge, kSortLargeThreads>, kSortLargeThreads,
-                          sizeof(SortSmem<kSortLarge>));
-        attr = true;
-    }
-    if (cudaMemsetAsync(w.counts, 0, 4 * sizeof(int), s) != cudaSuccess)
+    if (cudaMemsetAsync(w.counts, 0, (kSortClasses + 1) * sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, w.lists, w.counts);
     HP_CHECK_LAUNCH("k_sort_classes");
+    const SortArgs A{offsets, w, m, ids, t_proj, dist_perp};
     {
         TimedSpan ts("k_query_sort", s);
-        k_query_sort<kSortTiny, kThreads><<<kNumSMs * occ[0], kThreads, sizeof(SortSmem<kSortTiny>), s>>>(
-            offsets, w.soff, w.tmm, w.lists, w.counts, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
-        HP_CHECK_LAUNCH("k_query_sort<tiny>");
-        k_query_sort<kSortSmall, kThreads><<<kNumSMs * occ[1], kThreads, sizeof(SortSmem<kSortSmall>), s>>>(
-            offsets, w.soff, w.tmm, w.lists + m, w.counts + 1, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
-        HP_CHECK_LAUNCH("k_query_sort<small>");
+        HP_TRY((launch_sort<1024, kThreads>(A, 0, s)));
+        HP_TRY((launch_sort<2048, kThreads>(A, 1, s)));
     }
     TimedSpan ts("k_query_sort_large", s);
-    k_query_sort<kSortLarge, kSortLargeThreads><<<kNumSMs * occ[2], kSortLargeThreads, sizeof(SortSmem<kSortLarge>), s>>>(
-        offsets, w.soff, w.tmm, w.lists + 2 * m, w.counts + 2, w.st, w.sid, w.sd, ids, t_proj, dist_perp);
-    HP_CHECK_LAUNCH("k_query_sort<large>");
-    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, w.lists + 3 * m, w.counts + 3, w.st,
-                                                           w.sid, w.sd, ids, t_proj, dist_perp);
+    HP_TRY((launch_sort<kSortLarge, kSortLargeThreads>(A, 2, s)));
+    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, w.lists + kSortClasses * m,
+                                                           w.counts + kSortClasses, w.st, w.sid, w.sd, ids, t_proj,
+                                                           dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");
     return HP_OK;
 }
