@@ -128,6 +128,22 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(span):
+    """DRAM bytes (read + write) of one occurrence of a timing span, from the
+    committed `ncu --set full` summary of the same bench command
+    (profiles/*_ncu_full.json, scripts/ncu_summary.py); None if absent."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            sp = json.load(open(f))["spans"].get(span)
+        except Exception:
+            continue
+        if sp:
+            return float(sp["dram_bytes"]), os.path.relpath(f, ROOT)
+    return None, None
+
+
 # --------------------------------------------------------------------------- CPU legs
 def cpu_run(w, stride, threads):
     """Reference algorithm on the host (C oracle): full build, strided rays."""
@@ -309,6 +325,7 @@ def run_ours(args, w, rank, world, dist):
     t_top = kern[top][0] / max(kern[top][1], 1)
     b_top = kbytes[top] / max(kern[top][1], 1)
     achieved = b_top / (t_top / 1e3) / 1e9 if t_top > 0 else 0.0
+    traffic, traffic_src = ncu_traffic(top)
     line = {
         "metric": "rays/sec (search+primary-surface sampling)", "value": value, "unit": "rays/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -320,7 +337,8 @@ def run_ours(args, w, rank, world, dist):
                    "parallelism": f"row bands x{world}" if world > 1 else "single GPU",
                    "parity_gate": parity},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes": b_top, "traffic_source": traffic_src,
                      "peak_source": peak_kind},
         "frame_roofline": {"bytes": bb + bq + bs, "achieved_gbs": (bb + bq + bs) / (ms / 1e3) / 1e9,
                            "frac": (bb + bq + bs) / (ms / 1e3) / 1e9 / peak},

@@ -1,0 +1,25 @@
+"""Per-kernel share of one bench frame from an ncu launch list
+(--metrics gpu__time_duration.sum --csv; bench.py --steps 1 --warmup 1, so the
+second half of the list is the timed frame)."""
+import collections
+import csv
+import sys
+
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+h = rows[0]
+ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+launch = []
+for r in rows[1:]:
+    name = r[ki].replace("<unnamed>::", "").replace("(anonymous namespace)::", "").replace("void ", "")
+    name = name.replace("hp::", "").split("(")[0]
+    launch.append((name, float(r[vi].replace(",", ""))))
+frame = launch[len(launch) // 2:]
+s = sum(v for _, v in frame)
+agg = collections.Counter()
+for nm, v in frame:
+    agg[nm] += v
+out = [f"frame = second half of the launch list: {len(frame)} launches, {s / 1e6:.3f} ms serialised "
+       f"(ncu, cold caches, --clock-control none)"]
+for k, v in agg.most_common():
+    out.append(f"{k[:60]:60s} {v / 1e3:9.1f} us {100 * v / s:6.1f}%")
+print("\n".join(out))
