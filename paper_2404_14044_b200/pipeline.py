@@ -19,7 +19,31 @@ from . import device
 from .geometry import radius_slopes
 from .sampler import SamplerConfig
 
-__all__ = ["FrameResult", "frame_device", "search_and_sample", "StageTimer"]
+__all__ = ["FrameResult", "frame_device", "search_and_sample", "StageTimer", "host_slopes"]
+
+_POOL = None
+
+
+def host_slopes(camera, pixels: np.ndarray, kernel_radius: float, approx: bool = False,
+                chunk: int = 1 << 16) -> np.ndarray:
+    """``radius_slopes`` over ray chunks on a host thread pool (numpy releases
+    the GIL inside its ufunc loops).  Every element goes through the same
+    elementwise expression, so the result is bit-identical to one call."""
+    global _POOL
+    m = pixels.shape[0]
+    if m <= chunk:
+        return radius_slopes(camera, pixels, kernel_radius, approx)
+    if _POOL is None:
+        import concurrent.futures
+        import os
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
+    out = np.empty(m, dtype=np.float64)
+
+    def run(a):
+        out[a:a + chunk] = radius_slopes(camera, pixels[a:a + chunk], kernel_radius, approx)
+
+    list(_POOL.map(run, range(0, m, chunk)))
+    return out
 
 
 class StageTimer:
@@ -81,9 +105,10 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     ``sample_batch_arrays`` (reference sampler.py:196-217).
 
     Inputs may be numpy arrays or (preferably pinned) CPU torch tensors.  The
-    device build is enqueued first; the host-side slopes (numpy, bit-identical
-    to the reference's ``radius_slopes``) are computed while it runs; results
-    come back through pinned buffers with one synchronisation.
+    device build and the ray uploads are enqueued first; the host-side slopes
+    (numpy on a thread pool, bit-identical to the reference's
+    ``radius_slopes``) are computed while they run; results come back through
+    pinned buffers with one synchronisation.
     """
     dev = torch.device("cuda", torch.cuda.current_device())
 
@@ -98,11 +123,16 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     px_host = pixels.numpy() if isinstance(pixels, torch.Tensor) else np.asarray(pixels)
     px_host = np.ascontiguousarray(px_host, dtype=np.int64).reshape(-1, 2)
     m = px_host.shape[0]
-    slopes = radius_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius)
-    pix_d = up(pixels, torch.int64).view(m, 2)
+    pix_d = up(pixels, torch.int64).view(m, 2)               # copies overlap the host slopes
     dirs_d = up(dirs, torch.float64).view(m, 3)
-    tn = up(np.broadcast_to(np.asarray(t_near, np.float64), (m,)), torch.float64)
-    tf = up(np.broadcast_to(np.asarray(t_far, np.float64), (m,)), torch.float64)
+
+    def per_ray(a):
+        if isinstance(a, torch.Tensor) and a.numel() == m:
+            return up(a.reshape(m), torch.float64)
+        return up(np.broadcast_to(np.asarray(a, np.float64), (m,)), torch.float64)
+
+    tn, tf = per_ray(t_near), per_ray(t_far)
+    slopes = host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius)
     sl = up(slopes, torch.float64)
     q = device.query(idx, pix_d, dirs_d, tn, tf, sl)
     s = device.sample(q[0], q[1], q[2], q[3], sl, sampler_cfg or SamplerConfig(), col, exact_t_end)
