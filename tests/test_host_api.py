@@ -210,3 +210,15 @@ class TestScenes:
             hp.SceneSpec("nope")
         with pytest.raises(ValueError):
             hp.SceneSpec("uniform_box", n=-1)
+
+
+def test_threaded_host_slopes_are_bit_identical():
+    import paper_2404_14044_b200 as hp
+    from paper_2404_14044_b200 import pipeline
+    from paper_2404_14044_b200.geometry import radius_slopes
+    cam = hp.scene_camera(320, 240, fov_deg=60, origin=(0.3, -0.2, 0.1), target=(0.0, 0.1, 4.0))
+    dirs, pix = hp.ray_grid(cam)
+    for approx in (False, True):
+        a = radius_slopes(cam, pix, 0.0137, approx)
+        b = pipeline.host_slopes(cam, pix, 0.0137, approx, chunk=4096)
+        assert a.tobytes() == b.tobytes()
