@@ -129,10 +129,15 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
                    int64_t* needed, void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Pass 2: sort each ray's matches by (t, id) from the workspace of pass 1
  * (same buffer, same capacity) into ids int64 [Q], t_proj / dist_perp
- * float64 [Q] (total = Q = offsets[m], host value). */
+ * float64 [Q] (total = Q = offsets[m], host value).
+ * facts (optional, int32 [m], NULL to skip; needs the query's slopes [m]):
+ * per ray -1 (unknown) or, when every t / dist of the sorted segment is
+ * finite with dist >= 0, the count #{dist <= slopes[r] * t_0}.  Passing them
+ * to hp_sample_run for this exact CSR spares the sampler its full pass over
+ * the CSR. */
 int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, int64_t* ids, double* t_proj,
-                  double* dist_perp, int64_t capacity, void* workspace, size_t workspace_bytes,
-                  hp_stream_t stream);
+                  double* dist_perp, const double* slopes, int32_t* facts, int64_t capacity,
+                  void* workspace, size_t workspace_bytes, hp_stream_t stream);
 
 /* ---------------- sample ---------------- */
 /* exact_capacity: slots for candidates evaluated exactly (udf/alpha/colour
@@ -146,9 +151,11 @@ int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity,
  * Synchronises `stream` once to read the number of exactly evaluated
  * candidates; if it exceeds exact_capacity, returns HP_ESPACE and stores the
  * required capacity in *exact_needed (host pointer, may be NULL) so the
- * caller can grow the workspace and call again. */
+ * caller can grow the workspace and call again.  query_facts: NULL, or the
+ * facts hp_query_fill wrote for exactly this CSR and these slopes. */
 int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                   const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
+                  const int32_t* query_facts,
                   const hp_sampler_params* p, const double* colors, int64_t n_colors,
                   int64_t* r_off, double* t_end, int64_t* exact_needed,
                   void* workspace, size_t workspace_bytes, hp_stream_t stream);

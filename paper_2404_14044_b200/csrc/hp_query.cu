@@ -381,6 +381,7 @@ struct SortSmem {
     unsigned short perm[kCap];
     int chist[kCoarse + 1];
     int scan_sh[33];
+    int fcount, fbad;  // per-ray facts for the sampler (see sort_segment)
 };
 
 __device__ __forceinline__ double from_okey(unsigned long long k) {
@@ -418,8 +419,9 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
 template <int kCap, int kT>
 __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* __restrict__ st,
                              const int* __restrict__ sid, const double* __restrict__ sd, int64_t* __restrict__ gid,
-                             double* __restrict__ gt, double* __restrict__ gd) {
+                             double* __restrict__ gt, double* __restrict__ gd, double slope, int* fact) {
     const int tid = threadIdx.x;
+    if (tid == 0) F.fcount = F.fbad = 0;
     // all of the segment's loads in flight at once
     for (int e = tid; e < q; e += kT) {
         cp_async8(&F.t[e], st + e);
@@ -510,15 +512,36 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* _
     // dist into the (now free) bucket arrays, in flight while t / id go out
     for (int e = tid; e < q; e += kT) cp_async8(&F.d[e], sd + e);
     cp_commit();
+    // Facts for the sampler's fast path (hp_sample_run, query_facts): the
+    // segment is sorted by construction; record whether every t / dist is
+    // finite with dist >= 0, and #{dist <= slope * t_0} (its r_0 count).
+    bool bad = false;
     for (int p = tid; p < q; p += kT) {
         const int e = F.perm[p];
-        gt[p] = F.t[e];
+        const double te = F.t[e];
+        gt[p] = te;
         gid[p] = F.id[e];
+        bad |= !(fabs(te) <= DBL_MAX);
     }
     cp_wait<0>();
     __syncthreads();
-    for (int p = tid; p < q; p += kT) gd[p] = F.d[F.perm[p]];
+    if (fact) {
+        const double r0 = dmul(slope, F.t[F.perm[0]]);
+        int cnt = 0;
+        for (int p = tid; p < q; p += kT) {
+            const double d = F.d[F.perm[p]];
+            gd[p] = d;
+            bad |= !(d >= 0.0) || !(d <= DBL_MAX);
+            cnt += d <= r0;
+        }
+        cnt = warp_sum(cnt);
+        if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(&F.fbad, 1);
+        if (lane_id() == 0 && cnt) atomicAdd(&F.fcount, cnt);
+    } else {
+        for (int p = tid; p < q; p += kT) gd[p] = F.d[F.perm[p]];
+    }
     __syncthreads();
+    if (fact && tid == 0) *fact = F.fbad ? -1 : F.fcount;
 }
 
 constexpr int kSortLarge = 4096;
@@ -536,10 +559,11 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q == 0 ? -1 : kSortClasses;
+            cls = kSortClasses;
 #pragma unroll
             for (int c = kSortClasses - 1; c >= 0; c--)
                 if (q <= kSortCap[c]) cls = c;
+            if (q == 0) cls = -1;  // nothing to sort
         }
 #pragma unroll
         for (int c = 0; c <= kSortClasses; c++) {  // warp-aggregated append
@@ -558,7 +582,8 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
 // with an in-place sorting network on the scratch then a copy when kCap == 0.
 template <int kCap, int kT>
 __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int64_t* __restrict__ soff,
-                                                   const uint2* __restrict__ tmm, const int* __restrict__ list,
+                                                   const uint2* __restrict__ tmm, const double* slopes, int* facts,
+                                                   const int* __restrict__ list,
                                                    const int* __restrict__ list_n, double* __restrict__ st,
                                                    int* __restrict__ sid, double* __restrict__ sd,
                                                    int64_t* __restrict__ out_id, double* __restrict__ out_t,
@@ -570,8 +595,11 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
         const int64_t o = off[r], so = soff[r];
         const int64_t q = off[r + 1] - o;
         if constexpr (kCap > 0) {
+            // (plain loads under the branch: the .nc path may be speculated)
+            double slope = 0.0;
+            if (facts) slope = __ldcg(slopes + r);
             sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), tmm[r], st + so, sid + so, sd + so,
-                                   out_id + o, out_t + o, out_d + o);
+                                   out_id + o, out_t + o, out_d + o, slope, facts ? facts + r : nullptr);
         } else {
             double* tt = st + so;
             double* dd = sd + so;
@@ -682,6 +710,8 @@ struct SortArgs {
     int64_t* ids;
     double* t;
     double* d;
+    const double* slopes;
+    int* facts;
 };
 
 // One shared-memory size class: grid = SMs x resident CTAs (occupancy API).
@@ -693,7 +723,7 @@ static int launch_sort(const SortArgs& A, int cls, cudaStream_t s) {
         occ = resident(k_query_sort<kCap, kT>, kT, sizeof(SortSmem<kCap>));
     }
     k_query_sort<kCap, kT><<<kNumSMs * occ, kT, sizeof(SortSmem<kCap>), s>>>(
-        A.offsets, A.w.soff, A.w.tmm, A.w.lists + int64_t(cls) * A.m, A.w.counts + cls, A.w.st, A.w.sid, A.w.sd,
+        A.offsets, A.w.soff, A.w.tmm, A.slopes, A.facts, A.w.lists + int64_t(cls) * A.m, A.w.counts + cls, A.w.st, A.w.sid, A.w.sd,
         A.ids, A.t, A.d);
     HP_CHECK_LAUNCH("k_query_sort");
     return HP_OK;
@@ -771,12 +801,19 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
 }
 
 extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, int64_t* ids, double* t_proj,
-                             double* dist_perp, int64_t capacity, void* workspace, size_t workspace_bytes,
-                             hp_stream_t stream) {
+                             double* dist_perp, const double* slopes, int32_t* facts, int64_t capacity,
+                             void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     if (m < 0 || total < 0) {
         set_error("hp_query_fill: invalid arguments");
         return HP_EINVAL;
     }
+    if (facts && !slopes) {
+        set_error("hp_query_fill: facts need the query's slopes");
+        return HP_EINVAL;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (facts && m > 0 && cudaMemsetAsync(facts, 0xff, size_t(m) * sizeof(int32_t), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_query_fill memset");  // -1: unknown
     if (m == 0 || total == 0) return HP_OK;
     Carver cv(workspace, workspace_bytes);
     QueryWs w = carve_query(cv, m, capacity);
@@ -784,12 +821,11 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
         set_error("hp_query_fill: workspace too small");
         return HP_ESPACE;
     }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(w.counts, 0, (kSortClasses + 1) * sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     k_sort_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, w.lists, w.counts);
     HP_CHECK_LAUNCH("k_sort_classes");
-    const SortArgs A{offsets, w, m, ids, t_proj, dist_perp};
+    const SortArgs A{offsets, w, m, ids, t_proj, dist_perp, slopes, facts};
     {
         TimedSpan ts("k_query_sort", s);
         HP_TRY((launch_sort<1024, kThreads>(A, 0, s)));
@@ -797,7 +833,8 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     }
     TimedSpan ts("k_query_sort_large", s);
     HP_TRY((launch_sort<kSortLarge, kSortLargeThreads>(A, 2, s)));
-    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, w.lists + kSortClasses * m,
+    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, nullptr, nullptr,
+                                                           w.lists + kSortClasses * m,
                                                            w.counts + kSortClasses, w.st, w.sid, w.sd, ids, t_proj,
                                                            dist_perp);
     HP_CHECK_LAUNCH("k_query_sort<global>");

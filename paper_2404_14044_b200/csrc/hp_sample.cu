@@ -62,6 +62,7 @@ struct Csr {
     const double* slopes;
     const double* colors;
     int64_t m;
+    const int32_t* facts;  // optional per-ray facts from hp_query_fill (NULL: compute)
 };
 
 struct Outputs {
@@ -412,14 +413,19 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     // fast-path preconditions + count of candidates within r_0 (use_el holds
     // from j = 0 when it reaches K, the common case on dense surfaces)
     bool ok = slope >= 0.0 && slope <= DBL_MAX;
-    const double r0 = dmul(slope, ldg(T));
     int c0cnt = 0;
+    const int fact = C.facts ? C.facts[ray] : -1;
+    if (fact >= 0) {  // the query's sort established the preconditions
+        c0cnt = lane == 0 ? fact : 0;
+    } else {
+        const double r0 = dmul(slope, ldg(T));
 #pragma unroll 4
-    for (int k = lane; k < q; k += 32) {
-        const double tk = ldg(T + k), dk = ldg(DS + k);
-        ok &= (fabs(tk) <= DBL_MAX) && (dk >= 0.0) && (dk <= DBL_MAX);
-        if (k + 1 < q) ok &= !(ldg(T + k + 1) < tk);
-        c0cnt += (dk <= r0);
+        for (int k = lane; k < q; k += 32) {
+            const double tk = ldg(T + k), dk = ldg(DS + k);
+            ok &= (fabs(tk) <= DBL_MAX) && (dk >= 0.0) && (dk <= DBL_MAX);
+            if (k + 1 < q) ok &= !(ldg(T + k + 1) < tk);
+            c0cnt += (dk <= r0);
+        }
     }
     const bool fast = __all_sync(0xffffffffu, ok);
     int jstar = 0;
@@ -833,7 +839,7 @@ extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact
 
 extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                              const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
-                             const hp_sampler_params* p, const double* colors, int64_t n_colors, int64_t* r_off,
+                             const int32_t* query_facts, const hp_sampler_params* p, const double* colors, int64_t n_colors, int64_t* r_off,
                              double* t_end, int64_t* exact_needed, void* workspace, size_t workspace_bytes,
                              hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
@@ -846,7 +852,7 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Csr C{offsets, ids, t, dist, slopes, colors, m};
+    Csr C{offsets, ids, t, dist, slopes, colors, m, query_facts};
     Params P = to_params(p);
     if (m > 0) {
         HP_TRY(dispatch_exact(C, P, w, exact_needed, s));
@@ -872,7 +878,7 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
         return HP_ESPACE;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Csr C{offsets, ids, t, dist, slopes, colors, m};
+    Csr C{offsets, ids, t, dist, slopes, colors, m, nullptr};
     Params P = to_params(p);
     Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
     TimedSpan ts("k_emit", s);

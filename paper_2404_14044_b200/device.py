@@ -163,10 +163,12 @@ def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered
 
 
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
-          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True):
+          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True, facts: bool = False):
     """_kernels.hash_query_batch on the device (reference _kernels.py:86-157).
 
-    Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors.
+    Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors
+    (+ the per-ray sampler facts, int32 [m], with ``facts=True``; pass them to
+    :func:`sample` together with this CSR and these slopes).
     """
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
@@ -201,9 +203,14 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
     _mark("query.sync")
-    _lib.check(lib.hp_query_fill(_ptr(offsets), m, total, _ptr(ids), _ptr(t), _ptr(d), cap, _ptr(ws),
-                                 nb.value, _stream()))
+    fa = torch.empty(m, dtype=torch.int32, device=dev) if facts else None
+    _lib.check(lib.hp_query_fill(_ptr(offsets), m, total, _ptr(ids), _ptr(t), _ptr(d),
+                                 _ptr(slopes) if facts else ctypes.c_void_p(0),
+                                 _ptr(fa) if facts else ctypes.c_void_p(0), cap, _ptr(ws), nb.value,
+                                 _stream()))
     _mark("query.fill")
+    if facts:
+        return offsets, ids, t, d, probes, scanned, fa
     return offsets, ids, t, d, probes, scanned
 
 
@@ -222,12 +229,15 @@ def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerPara
 
 def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torch.Tensor,
            slopes: torch.Tensor, cfg, colors: torch.Tensor | None = None,
-           exact_t_end: bool = True):
+           exact_t_end: bool = True, facts: torch.Tensor | None = None):
     """_kernels.sample_batch on the device (reference _kernels.py:552-700).
 
     Returns (r_off, r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color, t_end).
     ``exact_t_end=False`` stops each ray once retention is decided and reports
     the transmittance at that point instead of over all candidates.
+    ``facts``: the per-ray facts :func:`query` returned with this very CSR and
+    these slopes (lets the sampler skip its full precondition pass); results
+    are identical with or without them.
     """
     lib = _lib.load(require_device=True)
     dev = offsets.device
@@ -249,7 +259,8 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
         ws = _workspace(nb.value, dev)
         common = (_ptr(offsets), m, _ptr(ids), _ptr(t), _ptr(dist), total, exact_cap,
                   _ptr(slopes), ctypes.byref(p), _ptr(col) if want else ctypes.c_void_p(0), ncol)
-        rc = lib.hp_sample_run(*common, _ptr(r_off), _ptr(t_end), ctypes.byref(needed), _ptr(ws),
+        run_args = common[:8] + (_ptr(facts) if facts is not None else ctypes.c_void_p(0),) + common[8:]
+        rc = lib.hp_sample_run(*run_args, _ptr(r_off), _ptr(t_end), ctypes.byref(needed), _ptr(ws),
                                nb.value, _stream())
         if rc == _lib.HP_ESPACE and needed.value > exact_cap:
             exact_cap = int(needed.value)   # grow the exact-candidate scratch once

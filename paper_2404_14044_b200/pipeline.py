@@ -90,11 +90,11 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
     mark("start")
     idx = device.build(xyz, camera, search_cfg.pad)
     mark("build")
-    q = device.query(idx, pixels, dirs, t_near, t_far, slopes)
+    q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True)
     mark("query")
-    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end)
+    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
-    return FrameResult(idx, q, s)
+    return FrameResult(idx, q[:6], s)
 
 
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
@@ -134,8 +134,9 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     tn, tf = per_ray(t_near), per_ray(t_far)
     slopes = host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius)
     sl = up(slopes, torch.float64)
-    q = device.query(idx, pix_d, dirs_d, tn, tf, sl)
-    s = device.sample(q[0], q[1], q[2], q[3], sl, sampler_cfg or SamplerConfig(), col, exact_t_end)
+    q = device.query(idx, pix_d, dirs_d, tn, tf, sl, facts=True)
+    s = device.sample(q[0], q[1], q[2], q[3], sl, sampler_cfg or SamplerConfig(), col, exact_t_end,
+                      facts=q[6])
     outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
     for o, x in zip(outs, s):
         o.copy_(x, non_blocking=True)

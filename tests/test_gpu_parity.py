@@ -111,3 +111,20 @@ def test_footprint_on_wide_rotated_camera():
                    dirs, cam.origin, np.full(m, 0.5), np.full(m, 9.0), slopes)
     for x, y in zip(a, oq):
         np.testing.assert_array_equal(x.cpu().numpy(), y)
+
+
+@pytest.mark.parametrize("name", gu.case_names())
+@pytest.mark.parametrize("exact_t_end", [True, False])
+def test_query_facts_do_not_change_samples(name, exact_t_end):
+    """The sampler's fast path fed by the query's per-ray facts gives the
+    same arrays as the sampler computing its own preconditions."""
+    cloud, cam, cfg, samplers, idx, rays = _dev_case(name)
+    q = dv.query(idx, *rays, facts=True)
+    assert all(torch.equal(a, b) for a, b in zip(q[:6], dv.query(idx, *rays)))
+    colors = torch.from_numpy(cloud.colors).cuda()
+    for sname in samplers:
+        sc = gu.sampler_config(sname)
+        a = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, colors, exact_t_end=exact_t_end, facts=q[6])
+        b = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, colors, exact_t_end=exact_t_end)
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
