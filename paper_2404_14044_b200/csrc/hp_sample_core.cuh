@@ -1,0 +1,404 @@
+// hp_sample_core.cuh — the sampler's per-candidate arithmetic, shared by the
+// standalone sampler (hp_sample.cu) and the query sort's fused sampling
+// epilogue (hp_query.cu).  Reference: _kernels.sample_batch
+// (_kernels.py:552-700); exactness arguments in DESIGN.md §6.
+#pragma once
+#include <math_constants.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "hp_common.cuh"
+
+namespace hp {
+namespace {
+
+struct Params {
+    int K;
+    int eps_mode, want_color, exact_t_end;
+    double beta2, gamma, eps, tau_min;
+    double inv_beta2_up;  // 1 / beta2 rounded up (bound factors only)
+};
+
+__device__ __forceinline__ bool kless(double d2a, int ia, double d2b, int ib) {
+    return d2a < d2b || (d2a == d2b && ia < ib);
+}
+
+// K-best list in registers (MAXK compile-time, ksel <= MAXK at runtime),
+// ascending by (d2, i).
+template <int MAXK>
+struct Best {
+    static constexpr int kMax = MAXK;
+    double d[MAXK];
+    int i[MAXK];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int b = 0; b < MAXK; b++) {
+            d[b] = CUDART_INF;
+            i[b] = INT_MAX;
+        }
+    }
+    __device__ __forceinline__ void kth(int ksel, double& kd, int& ki) const {
+#pragma unroll
+        for (int b = 0; b < MAXK; b++)
+            if (b == ksel - 1) {
+                kd = d[b];
+                ki = i[b];
+            }
+    }
+    template <class F>
+    __device__ __forceinline__ void for_each(int ksel, F f) const {
+#pragma unroll
+        for (int b = 0; b < MAXK; b++)
+            if (b < ksel) f(d[b], i[b]);
+    }
+    // full list (ksel == MAXK): branch-free compare-shift network; the caller
+    // guarantees (nd, ni) < the last entry.
+    __device__ __forceinline__ void insert_full(double nd, int ni) {
+#pragma unroll
+        for (int b = MAXK - 1; b >= 1; --b) {
+            const bool shift = kless(nd, ni, d[b - 1], i[b - 1]);
+            const bool here = !shift && kless(nd, ni, d[b], i[b]);
+            const double db = shift ? d[b - 1] : (here ? nd : d[b]);
+            const int ib = shift ? i[b - 1] : (here ? ni : i[b]);
+            d[b] = db;
+            i[b] = ib;
+        }
+        if (kless(nd, ni, d[0], i[0])) {
+            d[0] = nd;
+            i[0] = ni;
+        }
+    }
+    // caller guarantees (nd, ni) < the current ksel-th entry
+    __device__ __forceinline__ void insert(int ksel, double nd, int ni) {
+        bool placed = false;
+#pragma unroll
+        for (int b = MAXK - 1; b >= 1; --b) {
+            if (b < ksel && !placed) {
+                if (kless(nd, ni, d[b - 1], i[b - 1])) {
+                    d[b] = d[b - 1];
+                    i[b] = i[b - 1];
+                } else {
+                    d[b] = nd;
+                    i[b] = ni;
+                    placed = true;
+                }
+            }
+        }
+        if (!placed) {
+            d[0] = nd;
+            i[0] = ni;
+        }
+    }
+};
+
+// Large-K variant: arrays in local memory, dynamic loops.
+struct BestDyn {
+    static constexpr int kMax = HP_MAX_K;
+    double d[HP_MAX_K];
+    int i[HP_MAX_K];
+    __device__ void init() {
+        for (int b = 0; b < HP_MAX_K; b++) {
+            d[b] = CUDART_INF;
+            i[b] = INT_MAX;
+        }
+    }
+    __device__ void kth(int ksel, double& kd, int& ki) const {
+        kd = d[ksel - 1];
+        ki = i[ksel - 1];
+    }
+    template <class F>
+    __device__ void for_each(int ksel, F f) const {
+        for (int b = 0; b < ksel; b++) f(d[b], i[b]);
+    }
+    __device__ void insert_full(double nd, int ni) { insert(HP_MAX_K, nd, ni); }
+    __device__ void insert(int ksel, double nd, int ni) {
+        int b = ksel - 1;
+        while (b > 0 && kless(nd, ni, d[b - 1], i[b - 1])) {
+            d[b] = d[b - 1];
+            i[b] = i[b - 1];
+            b--;
+        }
+        d[b] = nd;
+        i[b] = ni;
+    }
+};
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+// One ray's t / ds segment of the query CSR (read-only path).
+struct RayView {
+    const double* gt;
+    const double* gd;
+    __device__ __forceinline__ double t(int i) const { return __ldg(gt + i); }
+    __device__ __forceinline__ double d(int i) const { return __ldg(gd + i); }
+};
+
+// Exact udf/alpha (and colour) of candidate j (reference _kernels.py:594-660).
+template <class BestT, class View>
+__device__ void eval_exact(const View& V, int q, int j, bool fast,
+                           int jstar, double slope, const Params& P, const int64_t* __restrict__ ids_ray,
+                           const double* __restrict__ colors, double& udf, double& alpha, double* col3,
+                           unsigned long long& evals) {
+    const double tj = V.t(j);
+    const double rj = dmul(slope, tj);
+    bool use_el;
+    int ksel;
+    if (fast) {
+        use_el = j >= jstar;
+        ksel = use_el ? P.K : (q < P.K ? q : P.K);
+    } else {
+        int n_el = 0;
+        for (int i = 0; i < q; i++) n_el += (V.d(i) <= rj);
+        use_el = n_el >= P.K;
+        const int pool = use_el ? n_el : q;
+        ksel = pool > P.K ? P.K : pool;
+    }
+    BestT best;
+    best.init();
+    double kd = CUDART_INF;
+    int ki = INT_MAX;
+    constexpr int kMaxK = BestT::kMax;
+    const bool full = ksel == kMaxK;
+    if (fast) {
+        // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
+        int l = j, r = j + 1;
+        double tl = tj, tr = r < q ? V.t(r) : 0.0;
+        while (l >= 0 || r < q) {
+            const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
+            int i;
+            double ti;
+            if (go_left) {
+                i = l;
+                ti = tl;
+                if (--l >= 0) tl = V.t(l);
+            } else {
+                i = r;
+                ti = tr;
+                if (++r < q) tr = V.t(r);
+            }
+            const double dt = dsub(ti, tj);
+            const double lb = dmul(dt, dt);
+            if (lb > kd) break;  // the other side is at least as far
+            const double di = V.d(i);
+            if (use_el && di > rj) continue;
+            const double d2 = dadd(lb, dmul(di, di));
+            evals++;
+            if (kless(d2, i, kd, ki)) {
+                if (full) {
+                    best.insert_full(d2, i);
+                    kd = best.d[kMaxK - 1];
+                    ki = best.i[kMaxK - 1];
+                } else {
+                    best.insert(ksel, d2, i);
+                    best.kth(ksel, kd, ki);
+                }
+            }
+        }
+    } else {
+        for (int i = 0; i < q; i++) {  // reference loop (_kernels.py:607-620)
+            const double di = V.d(i);
+            if (use_el && di > rj) continue;
+            const double dt = dsub(V.t(i), tj);
+            const double d2 = dadd(dmul(dt, dt), dmul(di, di));
+            evals++;
+            if (d2 < kd) {
+                best.insert(ksel, d2, i);
+                best.kth(ksel, kd, ki);
+            }
+        }
+    }
+    double acc = 0.0;
+    best.for_each(ksel, [&](double d2, int) { acc = dadd(acc, sqrt(d2)); });
+    udf = __ddiv_rn(acc, double(ksel));
+    alpha = dmul(P.gamma, exp(__ddiv_rn(-dmul(udf, udf), P.beta2)));
+    if (P.want_color) {
+        int nz = 0;
+        best.for_each(ksel, [&](double d2, int) { nz += (d2 == 0.0); });
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+        if (nz > 0) {
+            best.for_each(ksel, [&](double d2, int i) {
+                if (d2 != 0.0) return;
+                const int64_t pid = ids_ray[i];
+                c0 = dadd(c0, colors[3 * pid]);
+                c1 = dadd(c1, colors[3 * pid + 1]);
+                c2 = dadd(c2, colors[3 * pid + 2]);
+            });
+            c0 = __ddiv_rn(c0, double(nz));
+            c1 = __ddiv_rn(c1, double(nz));
+            c2 = __ddiv_rn(c2, double(nz));
+        } else {
+            double wsum = 0.0;
+            best.for_each(ksel, [&](double d2, int i) {
+                const double wgt = __ddiv_rn(1.0, sqrt(d2));
+                const int64_t pid = ids_ray[i];
+                c0 = dadd(c0, dmul(wgt, colors[3 * pid]));
+                c1 = dadd(c1, dmul(wgt, colors[3 * pid + 1]));
+                c2 = dadd(c2, dmul(wgt, colors[3 * pid + 2]));
+                wsum = dadd(wsum, wgt);
+            });
+            c0 = __ddiv_rn(c0, wsum);
+            c1 = __ddiv_rn(c1, wsum);
+            c2 = __ddiv_rn(c2, wsum);
+        }
+        col3[0] = c0;
+        col3[1] = c1;
+        col3[2] = c2;
+    }
+}
+
+// Upper bound of the reference's factor fl(1 - alpha_j) (DESIGN.md "sampler:
+// transmittance bound").  For any ksel members A of j's pool,
+//   sum_{K nearest} sqrt(d2) <= sum_A sqrt(dt^2 + ds^2) <= sum_A (|dt| + ds),
+// so the mean of (|dt| + ds) over the first ksel pool members at or after j
+// in t order (then before j) bounds udf_j from above once inflated by 1e-12
+// (which dominates every fp64 rounding of both sums for K <= 256).  exp is
+// then bounded below in fp32 (argument rounded up, result scaled by
+// 1 - 2^-20 against expf's 2-ulp error).  Every later operation is monotone,
+// so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
+__device__ __forceinline__ double factor_from_sum(double sum, int ksel, const Params& P) {
+    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
+    const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
+    const float e = expf(-__double2float_ru(y));
+    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
+    return dsub(1.0, a_lo);
+}
+
+template <class View>
+__device__ double bound_factor(const View& V, int q, int j, int jstar, double slope, const Params& P) {
+    const double tj = V.t(j);
+    const double rj = dmul(slope, tj);
+    const bool use_el = j >= jstar;
+    const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
+    double sum = 0.0;
+    int found = 0;
+    for (int i = j; i < q && found < ksel; i++) {
+        const double di = V.d(i);
+        if (use_el && di > rj) continue;
+        sum = dadd(sum, dadd(dsub(V.t(i), tj), di));
+        found++;
+    }
+    for (int i = j - 1; found < ksel; i--) {  // the pool has >= ksel members
+        const double di = V.d(i);
+        if (use_el && di > rj) continue;
+        sum = dadd(sum, dadd(dsub(tj, V.t(i)), di));
+        found++;
+    }
+    return factor_from_sum(sum, ksel, P);
+}
+
+// Same bound with the members taken from the warp's ring of the last 64
+// candidates (K <= 32): the ksel candidates ending at j (or [0, ksel) for
+// j < ksel - 1).  Returns a negative value when a member is not in j's pool
+// (the caller then uses bound_factor).
+__device__ __forceinline__ double bound_factor_ring(const double* rt, const double* rd, int q, int j, double tj,
+                                                    int jstar, double slope, const Params& P) {
+    const bool use_el = j >= jstar;
+    const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
+    const double rj = dmul(slope, tj);
+    const int i0 = j >= ksel - 1 ? j - ksel + 1 : 0;
+    double sum = 0.0;
+    bool ok = true;
+    for (int k = 0; k < ksel; k++) {
+        const int i = (i0 + k) & 63;
+        const double di = rd[i];
+        ok &= !(use_el && di > rj);
+        sum = dadd(sum, dadd(fabs(dsub(rt[i], tj)), di));
+    }
+    return ok ? factor_from_sum(sum, ksel, P) : -1.0;
+}
+
+// Warp: first j in [0, q) with pred(j) (monotone false..true); q if none.
+template <class Pred>
+__device__ int warp_first_true(int q, Pred pred) {
+    int a = 0, b = q;  // answer in [a, b]
+    const int lane = lane_id();
+    while (b - a > 32) {
+        const int stride = (b - a + 31) / 32;
+        const int j = a + lane * stride;
+        const bool p = j < b && pred(j);
+        const unsigned mask = __ballot_sync(0xffffffffu, p);
+        const unsigned valid = __ballot_sync(0xffffffffu, j < b);
+        if (mask == 0) {
+            a = a + (31 - __clz(valid)) * stride + 1;
+        } else {
+            const int f = __ffs(mask) - 1;
+            b = a + f * stride;
+            if (f > 0) a = a + (f - 1) * stride + 1;
+        }
+    }
+    const int j = a + lane;
+    const unsigned mask = __ballot_sync(0xffffffffu, j < b && pred(j));
+    return mask ? a + __ffs(mask) - 1 : b;
+}
+
+
+// ---- bound chain (DESIGN.md §6 "Early exit with an exact transmittance").
+// Vs bounds the reference's T at the current chunk start.  While it is far
+// from underflow, the chunk's bounds come from a round-up warp prefix
+// product: T_{c0+l+1} <= T_{c0} * prod f * (1+u)^(l+1) + (l+1) 2^-1075
+// (round-to-nearest error <= u|x| + 2^-1075 per step), and prod f <= prod u
+// (round-up).  Near underflow the sequential round-to-nearest chain
+// U_{i+1} = U_i * u_i (monotone, dominates T_i) takes over and proves the
+// exact zero.  je: retention is decided before je.
+struct Chain {
+    double Vs = 1.0;
+    bool seq = false;
+    int je = 0;
+    bool proved_zero = false;
+};
+
+// Warp-uniform step over the bound factors u (one per lane, 1.0 beyond the
+// ray) of candidates [c0, c0 + n).  Returns true when the chain is finished.
+__device__ __forceinline__ bool chain_chunk(Chain& S, double u, int c0, int n, int q, double thr, const Params& P) {
+    const int lane = lane_id();
+    if (!S.seq) {
+        double Pl = u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double other = __shfl_up_sync(0xffffffffu, Pl, o);
+            if (lane >= o) Pl = __dmul_ru(Pl, other);
+        }
+        double B = __dmul_ru(__dmul_ru(S.Vs, Pl), 1.0 + double(lane + 1) * 0x1p-51);
+        B = __dadd_ru(B, double(lane + 1) * 0x1p-1074);
+        if (S.je == q) {
+            if (S.Vs < thr) {
+                S.je = c0;
+            } else {
+                const unsigned mask = __ballot_sync(0xffffffffu, lane < n && B < thr);
+                if (mask) S.je = c0 + __ffs(mask);  // T_{c0+l+1} < thr for the first such l
+            }
+        }
+        const double Vn = __shfl_sync(0xffffffffu, B, n - 1);
+        if (Vn >= 0x1p-1000) {
+            S.Vs = Vn;
+            return !P.exact_t_end && S.je < q;
+        }
+        S.seq = true;  // redo this chunk sequentially from Vs
+    }
+    double U = S.Vs;
+    for (int k = 0; k < n; k++) {
+        const double uk = __shfl_sync(0xffffffffu, u, k);
+        if (S.je == q && U < thr) S.je = c0 + k;
+        U = dmul(U, uk);
+        if (U == 0.0) {
+            S.proved_zero = true;
+            if (S.je == q && thr > 0.0) S.je = c0 + k + 1;  // U_{j+1} = 0 < thr
+            break;
+        }
+    }
+    S.Vs = U;
+    return S.proved_zero || (!P.exact_t_end && S.je < q);
+}
+
+// One ray's t / ds held in shared memory (sorted), for the fused epilogue.
+struct SmemView {
+    const double* st;
+    const double* sd;
+    __device__ __forceinline__ double t(int i) const { return st[i]; }
+    __device__ __forceinline__ double d(int i) const { return sd[i]; }
+};
+
+}  // namespace
+}  // namespace hp
