@@ -39,13 +39,19 @@ struct Best {
             i[b] = INT_MAX;
         }
     }
+    // d[ksel - 1] as a select chain: an equality test lets the compiler turn
+    // the loop into one indexed load, which demotes the list to local memory.
     __device__ __forceinline__ void kth(int ksel, double& kd, int& ki) const {
+        double x = d[0];
+        int y = i[0];
 #pragma unroll
-        for (int b = 0; b < MAXK; b++)
-            if (b == ksel - 1) {
-                kd = d[b];
-                ki = i[b];
-            }
+        for (int b = 1; b < MAXK; b++) {
+            const bool in = b < ksel;
+            x = in ? d[b] : x;
+            y = in ? i[b] : y;
+        }
+        kd = x;
+        ki = y;
     }
     template <class F>
     __device__ __forceinline__ void for_each(int ksel, F f) const {
