@@ -217,6 +217,12 @@ def run_reference(args, w, rank, world):
 
 
 # --------------------------------------------------------------------------- GPU leg
+def local_device():
+    import torch
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
+
+
+
 def row_bands(w, world, rank):
     """Contiguous ray range of this rank (whole image rows, cost-balanced by
     the scan count each ray will do; every rank computes the same split)."""
@@ -233,7 +239,7 @@ def run_ours(args, w, rank, world, dist):
     from paper_2404_14044_b200 import _lib, device as dv, pipeline
     from paper_2404_14044_b200.shard import gather_samples
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     r0, r1 = row_bands(w, world, rank) if world > 1 else (0, w["m"])
     up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
@@ -292,40 +298,47 @@ def run_ours(args, w, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     stages = {k: v / args.steps for k, v in stage_tot.items()}
+    QR_total = (fr.Q, fr.R)
+    if dist is not None:  # whole-job candidate / sample counts
+        qr = torch.tensor([fr.Q, fr.R], device=dev, dtype=torch.int64)
+        dist.all_reduce(qr)
+        QR_total = (int(qr[0]), int(qr[1]))
 
-    # end-to-end through the public host-buffer API (pinned host inputs)
+    # end-to-end through the public host-buffer API (pinned host inputs); at
+    # N > 1 every rank runs its band concurrently, max time over ranks
     e2e = None
-    if rank == 0 and not args.no_e2e:
-        e2e = run_e2e(args, w, r0, r1)
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, r0, r1, dist)
     if rank != 0:
         return
     m_total = w["m"]
     value = m_total / (ms / 1e3)
     n, P = w["cloud"].count, fr.index.padded_width * fr.index.padded_height
-    Q, R = fr.Q * world, fr.R * world  # per-rank band; exact only at world == 1
+    Q, R = QR_total
     bb, bq, bs = frame_bytes(n, fr.index.n_in, P, m_total, Q, R)
     peak, peak_kind = measured_peaks()
-    # per-kernel algorithmic bytes per frame (inputs read once, outputs written once)
+    # per-kernel algorithmic bytes of this rank's frame (inputs read once,
+    # outputs written once).  Sort classes by the match counts.
     n_in = fr.index.n_in
-    # per-kernel algorithmic bytes per frame (inputs read once, outputs written
-    # once).  Sort classes by the rays' match counts.
+    m_loc, q_loc, r_loc = r1 - r0, fr.Q, fr.R
     qs = np.diff(fr.query[0].cpu().numpy())
     cls = {"k_query_sort": (qs > 0) & (qs <= 2048), "k_query_sort_large": qs > 2048}
     kbytes = {
         "hp_build": 24 * n + 16 * P + 32 * n_in + 4 * (P + 1) + 44 * n_in,
-        "k_query_bound": 64 * m_total + 4 * (P + 1) + 8 * m_total,
-        "k_query_scan": 64 * m_total + 4 * (P + 1) + 44 * n_in + 20 * Q + 32 * m_total,
-        "k_sample_plan": 8 * (m_total + 1) + 16 * Q + 8 * m_total + 24 * m_total,
-        "k_emit": 8 * (m_total + 1) + 52 * R + 24 * R + 72 * R,
+        "k_query_bound": 64 * m_loc + 4 * (P + 1) + 8 * m_loc,
+        "k_query_scan": 64 * m_loc + 4 * (P + 1) + 44 * n_in + 20 * q_loc + 32 * m_loc,
+        "k_sample_plan": 8 * (m_loc + 1) + 16 * q_loc + 8 * m_loc + 24 * m_loc,
+        "k_emit": 8 * (m_loc + 1) + 52 * r_loc + 24 * r_loc + 72 * r_loc,
     }
     for k, sel in cls.items():  # read the unsorted matches (20 B), write the CSR (24 B)
-        kbytes[k] = 44 * int(qs[sel].sum()) * world + 24 * int(sel.sum()) * world
+        kbytes[k] = 44 * int(qs[sel].sum()) + 24 * int(sel.sum())
     kern = {k: (v / args.steps, c // args.steps) for k, (v, c) in kern_tot.items()}
     top = max((k for k in kern if k in kbytes), key=lambda k: kern[k][0])
     t_top = kern[top][0] / max(kern[top][1], 1)
     b_top = kbytes[top] / max(kern[top][1], 1)
     achieved = b_top / (t_top / 1e3) / 1e9 if t_top > 0 else 0.0
-    traffic, traffic_src = ncu_traffic(top)
+    # the committed ncu capture is of the default command (cfg2, 1 GPU)
+    traffic, traffic_src = ncu_traffic(top) if (args.workload == "cfg2" and world == 1) else (None, None)
     line = {
         "metric": "rays/sec (search+primary-surface sampling)", "value": value, "unit": "rays/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -360,7 +373,7 @@ def run_ours(args, w, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
-def run_e2e(args, w, r0, r1):
+def run_e2e(args, w, r0, r1, dist=None):
     import torch
 
     from paper_2404_14044_b200 import pipeline
@@ -375,6 +388,8 @@ def run_e2e(args, w, r0, r1):
                 t_near=pin(w["t_near"][r0:r1]), t_far=pin(w["t_far"][r0:r1]))
     times, out = [], None
     for i in range(args.warmup + args.steps):
+        if dist is not None:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = pipeline.search_and_sample(cloud, w["cam"], w["cfg"], host["pixels"], host["dirs"],
@@ -386,9 +401,16 @@ def run_e2e(args, w, r0, r1):
     h2d = (cloud.positions.numel() * 8 + cloud.colors.numel() * 8 + 16 * m + 24 * m + 8 * m + 8 * m
            + 8 * m)
     d2h = sum(int(x.nbytes) for x in out)
-    return {"value": m / sec, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": d2h, "api": "paper_2404_14044_b200.pipeline.search_and_sample "
-                                            "(numpy in / numpy out)"}
+    if dist is not None:  # whole job: slowest rank's time, bytes of all ranks
+        dev = torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([sec, h2d, d2h], device=dev, dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        sec, h2d, d2h = float(mx[0]), float(t[1]), float(t[2])
+    return {"value": w["m"] / sec, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "api": "paper_2404_14044_b200.pipeline.search_and_sample "
+                                                  "(numpy in / numpy out; per rank: its row band)"}
 
 
 def parity_gate(w, dev):
@@ -446,8 +468,10 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        # HP_DIST_BACKEND=gloo: functional check of the N > 1 path on a box
+        # with fewer GPUs than ranks (no NCCL); never used for a bench number
+        dist.init_process_group(os.environ.get("HP_DIST_BACKEND", "nccl"))
     run_ours(args, w, rank, world, dist)
     if dist is not None:
         dist.destroy_process_group()
