@@ -178,9 +178,10 @@ int hp_csr_stats(const int64_t* offsets, int64_t m, int64_t* out2, hp_stream_t s
 int hp_primary_surface(const int64_t* r_off, int64_t m, const int64_t* r_id, const double* r_t,
                        int64_t* primary_id, double* primary_t, hp_stream_t stream);
 
-/* Sampler path counters since the last reset (diagnostics):
+/* Sampler path counters since the last reset (diagnostics; all zero unless
+ * the library is built with -DHP_DEBUG_COUNTERS, e.g. `make DEBUG=1`):
  * [rays with candidates, fast-path rays, rays whose transmittance was proved 0,
- *  exactly evaluated candidates, candidates, sum of jstar, -, -]. */
+ *  K-NN distance evaluations, candidates, bound factors evaluated, -, -]. */
 int hp_sample_debug_counters(int64_t* out8, int reset);
 
 /* Per-kernel CUDA-event timing on the launching stream (diagnostics and the

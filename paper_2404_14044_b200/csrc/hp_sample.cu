@@ -46,7 +46,14 @@ constexpr int kSampleGrid = kNumSMs * 4;
 
 // Path counters: rays, fast rays, proved-zero rays, exact evaluations,
 // candidates, bound evaluations.  Read with hp_sample_debug_counters().
+// Compiled in with -DHP_DEBUG_COUNTERS only: same-address global atomics per
+// ray serialise in L2 and cost ~0.5 ms per cfg2 frame.
 __device__ unsigned long long g_dbg[8];
+#ifdef HP_DEBUG_COUNTERS
+#define HP_DBG_ADD(k, v) atomicAdd(&g_dbg[k], (unsigned long long)(v))
+#else
+#define HP_DBG_ADD(k, v) ((void)0)
+#endif
 
 
 struct Csr {
@@ -163,7 +170,7 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
         // exact region [0, E): everything unless retention is decided before je
         // and (exact t_end) the transmittance is proved to reach exactly 0
         ecnt[ray] = (!fast || (P.exact_t_end && !proved_zero)) ? q : je;
-        atomicAdd(&g_dbg[5], nbound);
+        HP_DBG_ADD(5, nbound);
     }
 }
 
@@ -221,8 +228,10 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
             X.col[3 * c + 2] = col[2];
         }
     }
+#ifdef HP_DEBUG_COUNTERS
     evals = warp_sum(evals);
-    if (lane_id() == 0 && evals) atomicAdd(&g_dbg[3], evals);
+    if (lane_id() == 0 && evals) HP_DBG_ADD(3, evals);
+#endif
 }
 
 // One warp per ray: the reference's sequential compositing over the exact
@@ -292,10 +301,10 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
         if (stop) break;
     }
     if (lane == 0) {
-        atomicAdd(&g_dbg[0], 1ull);
-        atomicAdd(&g_dbg[1], fast ? 1ull : 0ull);
-        atomicAdd(&g_dbg[2], proved_zero ? 1ull : 0ull);
-        atomicAdd(&g_dbg[4], (unsigned long long)q);
+        HP_DBG_ADD(0, 1);
+        HP_DBG_ADD(1, fast ? 1 : 0);
+        HP_DBG_ADD(2, proved_zero ? 1 : 0);
+        HP_DBG_ADD(4, q);
         double te;
         if (P.exact_t_end)
             te = (fast && proved_zero) ? 0.0 : Tr;

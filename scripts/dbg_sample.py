@@ -1,4 +1,4 @@
-"""Diagnostics: sampler path counters and per-stage timing on a workload."""
+"""Diagnostics: sampler path counters and per-stage timing on a workload (counters need `make -C paper_2404_14044_b200/csrc DEBUG=1`)."""
 import ctypes, sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
