@@ -106,6 +106,14 @@ int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
                          int64_t padded_h, const double* origin_host, hp_query_layout layout,
                          void* workspace, size_t workspace_bytes, hp_stream_t stream);
 
+/* ---------------- host helpers ---------------- */
+/* Per-ray search-radius slopes on host threads (replaces the vectorised
+ * geometry.radius_slopes, reference geometry.py:249-260): same expression
+ * order and libm calls as numpy, bit-identical; pixels int64 [m,2] with
+ * element stride pixel_stride between rays; slopes float64 [m] (host). */
+int hp_radius_slopes_host(const hp_camera* cam, const int64_t* pixels, int64_t pixel_stride, int64_t m,
+                          double kernel_radius, int approx, double* slopes, int threads);
+
 /* ---------------- query ---------------- */
 /* capacity: scratch slots for the unsorted matches (hp_query_count reports
  * the number it needs). */

@@ -1,0 +1,53 @@
+// hp_host.cpp — host-side helpers of the path that stay on the CPU by design.
+//
+// hp_radius_slopes_host: the reference's vectorised radius_slopes
+// (geometry.py:249-260) with the same operation order and
+// the same libm calls numpy makes (sqrt; hypot from glibc), so the values are
+// bit-identical to `radius_slopes` in numpy; compiled without FP contraction.
+// Kept on the host on purpose: hypot is not correctly rounded, so a device
+// version could differ in the last bit.  Runs on host threads.
+#include <cmath>
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+#include "../../include/hashpoint_b200.h"
+
+namespace {
+
+void slopes_range(const hp_camera& c, const int64_t* pix, int64_t stride, double kr, int approx, double* out,
+                  int64_t a, int64_t b) {
+    const double f = c.focal_length;
+    const double hw = 0.5 * double(c.width), hh = 0.5 * double(c.height);
+    const double fkr = f * kr;
+    const double ff = f * f;
+    for (int64_t r = a; r < b; r++) {
+        // _plane_offsets: (u + 0.5 - 0.5 * W) * pixel_width (left to right)
+        const double ox = ((double(pix[r * stride]) + 0.5) - hw) * c.pixel_width;
+        const double oy = ((double(pix[r * stride + 1]) + 0.5) - hh) * c.pixel_height;
+        const double a2 = ox * ox + oy * oy;
+        const double ae2 = ff + a2;
+        out[r] = approx ? fkr / ae2 : fkr / (std::sqrt(ae2) * std::hypot(std::sqrt(a2) - kr, f));
+    }
+}
+
+}  // namespace
+
+extern "C" int hp_radius_slopes_host(const hp_camera* cam, const int64_t* pixels, int64_t pixel_stride, int64_t m,
+                                     double kernel_radius, int approx, double* slopes, int threads) {
+    if (!cam || m < 0 || (m > 0 && (!pixels || !slopes))) return HP_EINVAL;
+    if (threads < 1) threads = 1;
+    const int64_t per = (m + threads - 1) / threads;
+    if (threads == 1 || m < 4096) {
+        slopes_range(*cam, pixels, pixel_stride, kernel_radius, approx, slopes, 0, m);
+        return HP_OK;
+    }
+    std::vector<std::thread> pool;
+    for (int k = 0; k < threads; k++) {
+        const int64_t a = k * per, b = std::min<int64_t>(m, a + per);
+        if (a >= b) break;
+        pool.emplace_back(slopes_range, std::cref(*cam), pixels, pixel_stride, kernel_radius, approx, slopes, a, b);
+    }
+    for (auto& t : pool) t.join();
+    return HP_OK;
+}

@@ -10,39 +10,34 @@ numpy out) used for the end-to-end number.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import device
-from .geometry import radius_slopes
 from .sampler import SamplerConfig
 
 __all__ = ["FrameResult", "frame_device", "search_and_sample", "StageTimer", "host_slopes"]
 
-_POOL = None
-
 
 def host_slopes(camera, pixels: np.ndarray, kernel_radius: float, approx: bool = False,
-                chunk: int = 1 << 16) -> np.ndarray:
-    """``radius_slopes`` over ray chunks on a host thread pool (numpy releases
-    the GIL inside its ufunc loops).  Every element goes through the same
-    elementwise expression, so the result is bit-identical to one call."""
-    global _POOL
-    m = pixels.shape[0]
-    if m <= chunk:
-        return radius_slopes(camera, pixels, kernel_radius, approx)
-    if _POOL is None:
-        import concurrent.futures
-        import os
-        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
-    out = np.empty(m, dtype=np.float64)
-
-    def run(a):
-        out[a:a + chunk] = radius_slopes(camera, pixels[a:a + chunk], kernel_radius, approx)
-
-    list(_POOL.map(run, range(0, m, chunk)))
+                out: np.ndarray | None = None, threads: int | None = None) -> np.ndarray:
+    """``radius_slopes`` on host threads through the library
+    (hp_radius_slopes_host: same expression order and libm calls as numpy,
+    bit-identical).  ``out`` may be a (pinned) float64 buffer of m values."""
+    import os
+    lib = device._lib.load(require_device=False)
+    px = np.ascontiguousarray(pixels, dtype=np.int64).reshape(-1, 2)
+    m = px.shape[0]
+    if out is None:
+        out = np.empty(m, dtype=np.float64)
+    threads = threads or min(16, os.cpu_count() or 1)
+    device._lib.check(lib.hp_radius_slopes_host(ctypes.byref(device.camera_struct(camera)),
+                                                px.ctypes.data_as(ctypes.c_void_p), 2, m,
+                                                float(kernel_radius), 1 if approx else 0,
+                                                out.ctypes.data_as(ctypes.c_void_p), int(threads)))
     return out
 
 
@@ -106,7 +101,7 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
 
     Inputs may be numpy arrays or (preferably pinned) CPU torch tensors.  The
     device build and the ray uploads are enqueued first; the host-side slopes
-    (numpy on a thread pool, bit-identical to the reference's
+    (host threads in the library, bit-identical to the reference's
     ``radius_slopes``) are computed while they run; results come back through
     pinned buffers with one synchronisation.
     """
@@ -132,8 +127,10 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
         return up(np.broadcast_to(np.asarray(a, np.float64), (m,)), torch.float64)
 
     tn, tf = per_ray(t_near), per_ray(t_far)
-    slopes = host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius)
-    sl = up(slopes, torch.float64)
+    sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
+    host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius,
+                out=sl_host.numpy())
+    sl = sl_host.to(dev, non_blocking=True)
     q = device.query(idx, pix_d, dirs_d, tn, tf, sl, facts=True)
     s = device.sample(q[0], q[1], q[2], q[3], sl, sampler_cfg or SamplerConfig(), col, exact_t_end,
                       facts=q[6])

@@ -212,7 +212,7 @@ class TestScenes:
             hp.SceneSpec("uniform_box", n=-1)
 
 
-def test_threaded_host_slopes_are_bit_identical():
+def test_native_host_slopes_are_bit_identical():
     import paper_2404_14044_b200 as hp
     from paper_2404_14044_b200 import pipeline
     from paper_2404_14044_b200.geometry import radius_slopes
@@ -220,5 +220,6 @@ def test_threaded_host_slopes_are_bit_identical():
     dirs, pix = hp.ray_grid(cam)
     for approx in (False, True):
         a = radius_slopes(cam, pix, 0.0137, approx)
-        b = pipeline.host_slopes(cam, pix, 0.0137, approx, chunk=4096)
-        assert a.tobytes() == b.tobytes()
+        for threads in (1, 7):
+            b = pipeline.host_slopes(cam, pix, 0.0137, approx, threads=threads)
+            assert a.tobytes() == b.tobytes()
