@@ -36,10 +36,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (scene kwargs, (W, H, fov), delta, t_near, t_far)
+    # name: (scene kwargs, (W, H, fov), delta)
     "cfg2": (dict(kind="sphere_surface", n=1_000_000, seed=0, noise=0.005), (800, 800, 40.0), 0.01),
     "cfg1": (dict(kind="sphere_surface", n=100_000, seed=0, noise=0.005), (200, 200, 40.0), 0.01),
+    # dense large scene, smallest delta of the sweep: Q ~ 4.3e9 does not fit
+    # one GPU's memory in one pass -> ray-chunk streaming (pipeline)
+    "cfg4": (dict(kind="sphere_surface", n=10_000_000, seed=0, noise=0.005), (1920, 1080, 40.0), 0.005),
 }
+# rays checked against the oracle before timing / timed on the host CPU
+PARITY_STRIDE = {"cfg1": 53, "cfg2": 53, "cfg4": 4999}
+CPU_STRIDE = {"cfg1": 97, "cfg2": 97, "cfg4": 20011}
 T_NEAR, T_FAR = 1.0, 10.0
 
 
@@ -321,7 +327,7 @@ def run_ours(args, w, rank, world, dist):
     # outputs written once).  Sort classes by the match counts.
     n_in = fr.index.n_in
     m_loc, q_loc, r_loc = r1 - r0, fr.Q, fr.R
-    qs = np.diff(fr.query[0].cpu().numpy())
+    qs = np.diff(fr.query[0].cpu().numpy()) if fr.query is not None else np.zeros(0, np.int64)
     cls = {"k_query_sort": (qs > 0) & (qs <= 2048), "k_query_sort_large": qs > 2048}
     kbytes = {
         "hp_build": 24 * n + 16 * P + 32 * n_in + 4 * (P + 1) + 44 * n_in,
@@ -348,6 +354,7 @@ def run_ours(args, w, rank, world, dist):
                    "n_indexed": fr.index.n_in, "Q": Q, "R": R, "P": P,
                    "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"row bands x{world}" if world > 1 else "single GPU",
+                   "ray_chunks": fr.chunks,
                    "parity_gate": parity},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -414,14 +421,14 @@ def run_e2e(args, w, r0, r1, dist=None):
 
 
 def parity_gate(w, dev):
-    """Device vs oracle on every 53rd ray of the frame (bit-exact ids/t/dist/
+    """Device vs oracle on every k-th ray of the frame (PARITY_STRIDE) (bit-exact ids/t/dist/
     udf/primary; alpha/w within 1e-12)."""
     import torch
 
     from oracle import oracle as orc
     from paper_2404_14044_b200 import device as dv
     from paper_2404_14044_b200.sampler import SamplerConfig
-    sel = slice(0, None, 53)
+    sel = slice(0, None, PARITY_STRIDE.get(w["name"], 53))
     cam, cfg, cloud = w["cam"], w["cfg"], w["cloud"]
     up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     idx = dv.build(up(cloud.positions), cam, cfg.pad)
@@ -443,7 +450,8 @@ def parity_gate(w, dev):
     ok &= all(np.allclose(s[k], os_[k], rtol=1e-12, atol=1e-300) for k in (5, 6, 7, 8))
     if not ok:
         raise SystemExit("parity gate failed: device results differ from the oracle; not timing")
-    return f"pass (every 53rd ray, {len(px)} rays, Q={len(oq[1])}, R={len(os_[1])})"
+    return (f"pass (every {PARITY_STRIDE.get(w['name'], 53)}th ray, {len(px)} rays, Q={len(oq[1])}, "
+            f"R={len(os_[1])})")
 
 
 def main():
@@ -453,7 +461,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
-    ap.add_argument("--cpu-stride", type=int, default=97)
+    ap.add_argument("--cpu-stride", type=int, default=None,
+                    help="every k-th ray for the CPU legs (default per workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
@@ -461,6 +470,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     w = make_workload(args.workload)
+    if args.cpu_stride is None:
+        args.cpu_stride = CPU_STRIDE.get(args.workload, 97)
     if args.impl == "reference":
         run_reference(args, w, rank, world)
         return

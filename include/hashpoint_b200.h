@@ -135,6 +135,14 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
                    const double* t_near, const double* t_far, const double* slopes, int64_t m,
                    int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
                    int64_t* needed, void* workspace, size_t workspace_bytes, hp_stream_t stream);
+/* Upper bounds of the match counts (the slots pass 1 will test per ray),
+ * exclusive-scanned into bound_off [m+1] (bound_off[m] = the scratch pass 1
+ * needs).  Lets a caller split a frame into ray chunks that fit memory.
+ * workspace: >= hp_query_workspace_bytes(m, pad, 0). */
+int hp_query_bounds(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
+                    int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                    const double* t_near, const double* t_far, const double* slopes, int64_t m,
+                    int64_t* bound_off, void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Pass 2: sort each ray's matches by (t, id) from the workspace of pass 1
  * (same buffer, same capacity) into ids int64 [Q], t_proj / dist_perp
  * float64 [Q] (total = Q = offsets[m], host value).

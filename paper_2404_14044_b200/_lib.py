@@ -55,6 +55,8 @@ _SIGNATURES = {
     "hp_query_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
                                       ctypes.POINTER(c_i64), c_p, c_size, c_p]),
+    "hp_query_bounds": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
+                                       c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_size, c_p]),
     "hp_query_fill": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
     "hp_sample_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64,
                                                  ctypes.POINTER(SamplerParams),

@@ -416,16 +416,21 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
 // placed linearly inside its bin's share.  The map is monotone in t, so
 // buckets are ordered; each element's final position is its bucket start
 // plus its exact (t, id) rank among the (few) members of its bucket.
-template <int kCap, int kT>
-__device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* __restrict__ st,
-                             const int* __restrict__ sid, const double* __restrict__ sd, int64_t* __restrict__ gid,
-                             double* __restrict__ gt, double* __restrict__ gd, double slope, int* fact) {
+// IdT: int32 (the match scratch) or int64 (in place in the output arrays,
+// for the parts of split rays: every input is in shared memory before the
+// corresponding output is written).
+template <int kCap, int kT, class IdT>
+__device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* st, const IdT* sid,
+                             const double* sd, int64_t* gid, double* gt, double* gd, double slope, int* fact) {
     const int tid = threadIdx.x;
     if (tid == 0) F.fcount = F.fbad = 0;
     // all of the segment's loads in flight at once
     for (int e = tid; e < q; e += kT) {
         cp_async8(&F.t[e], st + e);
-        cp_async4(&F.id[e], sid + e);
+        if constexpr (sizeof(IdT) == 4)
+            cp_async4(&F.id[e], sid + e);
+        else
+            F.id[e] = int(sid[e]);
     }
     cp_commit();
     if (q > 64) {
@@ -544,14 +549,12 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* _
     if (fact && tid == 0) *fact = F.fbad ? -1 : F.fcount;
 }
 
-constexpr int kSortLarge = 4096;
-constexpr int kSortLargeThreads = 512;
-
 // Size classes of rays to sort (by match count): shared-memory sorts with
-// capacities kSortCap (smaller capacity = more resident CTAs), then the
-// global-memory class above kSortLarge.
-constexpr int kSortClasses = 3;
-__constant__ int kSortCap[kSortClasses] = {1024, 2048, 4096};
+// capacities kSortCap (smaller capacity = more resident CTAs), then the rays
+// above kSortHuge, split into parts (k_query_split).
+constexpr int kSortClasses = 4;
+__constant__ int kSortCap[kSortClasses] = {1024, 2048, 4096, 8192};
+constexpr int kSortHuge = 8192;  // above: split into t-ordered parts of <= kSortHuge (k_query_split)
 __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
                                int* __restrict__ counts) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
@@ -578,8 +581,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
 }
 
 // Sort the rays of one size class (list of ray ids) from the scratch (ray r
-// at soff[r]) into the outputs (at off[r]): in shared memory when kCap > 0;
-// with an in-place sorting network on the scratch then a copy when kCap == 0.
+// at soff[r]) into the outputs (at off[r]) in shared memory.
 template <int kCap, int kT>
 __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int64_t* __restrict__ soff,
                                                    const uint2* __restrict__ tmm, const double* slopes, int* facts,
@@ -594,18 +596,131 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
         const int64_t r = list[k];
         const int64_t o = off[r], so = soff[r];
         const int64_t q = off[r + 1] - o;
-        if constexpr (kCap > 0) {
-            // (plain loads under the branch: the .nc path may be speculated)
-            double slope = 0.0;
-            if (facts) slope = __ldcg(slopes + r);
-            sort_segment<kCap, kT>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), tmm[r], st + so, sid + so, sd + so,
-                                   out_id + o, out_t + o, out_d + o, slope, facts ? facts + r : nullptr);
+        // (plain loads under the branch: the .nc path may be speculated)
+        double slope = 0.0;
+        if (facts) slope = __ldcg(slopes + r);
+        sort_segment<kCap, kT, int>(*reinterpret_cast<SortSmem<kCap>*>(dyn), int(q), tmm[r], st + so, sid + so,
+                                    sd + so, out_id + o, out_t + o, out_d + o, slope, facts ? facts + r : nullptr);
+    }
+}
+
+// ---------------------------------------------------------------- huge rays
+// Rays with more than kSortHuge matches: one CTA per ray splits the ray's
+// matches into t-ordered parts of <= kSortHuge (a 2048-bin linear histogram
+// of t over the ray's float bounds, bins grouped greedily), scattering them
+// into the ray's output segment part by part; every part is then sorted in
+// place in shared memory (k_query_sort_parts).  Parts are disjoint, ordered
+// t ranges (the bin map is monotone), so sorted parts = sorted ray.  A single
+// bin above kSortHuge (near-equal t) becomes a part sorted by a CTA network.
+constexpr int kSplitBins = 2048;
+constexpr int kSplitThreads = 1024;
+constexpr int kMaxParts = 512;
+
+struct Part {
+    int64_t start;  // absolute position in the output arrays
+    int size;
+    unsigned lo, hi;  // fkey bounds of the part's t
+};
+
+struct SplitSmem {
+    int hist[kSplitBins + 1];
+    int cur[kSplitBins];
+    unsigned short bin_part[kSplitBins];
+    int pstart[kMaxParts + 1];
+    unsigned plo[kMaxParts], phi[kMaxParts];
+    int scan_sh[33];
+    int np, slot;
+};
+
+__global__ void __launch_bounds__(kSplitThreads) k_query_split(
+    const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm,
+    const int* __restrict__ list, const int* __restrict__ list_n, const double* __restrict__ st,
+    const int* __restrict__ sid, const double* __restrict__ sd, int64_t* __restrict__ out_id,
+    double* __restrict__ out_t, double* __restrict__ out_d, Part* __restrict__ parts, int* __restrict__ parts_n,
+    int parts_cap) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    SplitSmem& S = *reinterpret_cast<SplitSmem*>(dyn);
+    const int tid = threadIdx.x;
+    const int n = *list_n;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+        const int64_t r = list[k];
+        const int64_t o = off[r], so = soff[r];
+        const int q = int(off[r + 1] - o);
+        const double tlo = double(from_fkey(tmm[r].x)), thi = double(nextafterf(from_fkey(tmm[r].y), CUDART_INF_F));
+        const double span = dsub(thi, tlo);
+        const double scale = span > 0.0 ? fmin(__ddiv_rn(double(kSplitBins), span), DBL_MAX) : 0.0;
+        auto bin = [&](double t) { return min(int(fmin(dmul(dsub(t, tlo), scale), double(kSplitBins))), kSplitBins - 1); };
+        for (int b = tid; b <= kSplitBins; b += kSplitThreads) S.hist[b] = 0;
+        __syncthreads();
+        for (int e = tid; e < q; e += kSplitThreads) {
+            const int b = bin(st[so + e]);
+            const unsigned peers = __match_any_sync(__activemask(), b);
+            if (lane_id() == __ffs(peers) - 1) atomicAdd(&S.hist[b], __popc(peers));
+        }
+        __syncthreads();
+        block_scan_inplace<(kSplitBins + kSplitThreads - 1) / kSplitThreads>(S.hist, kSplitBins, S.scan_sh);
+        __syncthreads();
+        if (tid == 0) {  // greedy grouping of consecutive bins into parts
+            int np = 0, pst = 0;
+            S.pstart[0] = 0;
+            for (int b = 0; b < kSplitBins; b++) {
+                const int bs = S.hist[b], be = b + 1 < kSplitBins ? S.hist[b + 1] : q;
+                if (be - pst > kSortHuge && bs > pst && np + 1 < kMaxParts) {  // close the part before b
+                    S.pstart[++np] = bs;
+                    pst = bs;
+                }
+                S.bin_part[b] = (unsigned short)np;
+            }
+            S.pstart[++np] = q;
+            S.np = np;
+            S.slot = atomicAdd(parts_n, np);
+        }
+        for (int p = tid; p < kMaxParts; p += kSplitThreads) {
+            S.plo[p] = 0xffffffffu;
+            S.phi[p] = 0u;
+        }
+        for (int b = tid; b < kSplitBins; b += kSplitThreads) S.cur[b] = S.hist[b];
+        __syncthreads();
+        for (int e = tid; e < q; e += kSplitThreads) {
+            const double t = st[so + e];
+            const int b = bin(t);
+            const int pos = atomicAdd(&S.cur[b], 1);
+            out_t[o + pos] = t;
+            out_id[o + pos] = sid[so + e];
+            out_d[o + pos] = sd[so + e];
+            const int p = S.bin_part[b];
+            atomicMin(&S.plo[p], fkey(__double2float_rd(t)));
+            atomicMax(&S.phi[p], fkey(__double2float_ru(t)));
+        }
+        __syncthreads();
+        for (int p = tid; p < S.np; p += kSplitThreads) {
+            const int slot = S.slot + p;
+            if (slot < parts_cap)
+                parts[slot] = Part{o + S.pstart[p], S.pstart[p + 1] - S.pstart[p], S.plo[p], S.phi[p]};
+        }
+        __syncthreads();
+    }
+}
+
+// Sort the parts in place in the output arrays: shared memory for parts of
+// <= kCap, a CTA sorting network in global memory for the larger ones.
+template <int kCap, int kT>
+__global__ void __launch_bounds__(kT) k_query_sort_parts(const Part* __restrict__ parts,
+                                                         const int* __restrict__ parts_n, int parts_cap,
+                                                         int64_t* out_id, double* out_t, double* out_d) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int n = min(*parts_n, parts_cap);
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+        const Part P = parts[k];
+        int64_t* ii = out_id + P.start;
+        double* tt = out_t + P.start;
+        double* dd = out_d + P.start;
+        if (P.size <= kCap) {
+            sort_segment<kCap, kT, int64_t>(*reinterpret_cast<SortSmem<kCap>*>(dyn), P.size,
+                                            make_uint2(P.lo, P.hi), tt, ii, dd, ii, tt, dd, 0.0, nullptr);
         } else {
-            double* tt = st + so;
-            double* dd = sd + so;
-            int* ii = sid + so;
             block_bitonic_sort(
-                q, [&](int64_t a, int64_t b) { return key_less(tt[a], ii[a], tt[b], ii[b]); },
+                P.size, [&](int64_t a, int64_t b) { return key_less(tt[a], ii[a], tt[b], ii[b]); },
                 [&](int64_t a, int64_t b) {
                     double x = tt[a];
                     tt[a] = tt[b];
@@ -613,16 +728,10 @@ __global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ o
                     x = dd[a];
                     dd[a] = dd[b];
                     dd[b] = x;
-                    const int y = ii[a];
+                    const int64_t y = ii[a];
                     ii[a] = ii[b];
                     ii[b] = y;
                 });
-            __syncthreads();
-            for (int64_t p = threadIdx.x; p < q; p += kT) {
-                out_t[o + p] = tt[p];
-                out_d[o + p] = dd[p];
-                out_id[o + p] = ii[p];
-            }
             __syncthreads();
         }
     }
@@ -701,6 +810,9 @@ struct QueryWs {
     double* st;
     int* sid;
     double* sd;
+    Part* parts;  // t-ordered parts of the rays above kSortHuge
+    int* parts_n;
+    int parts_cap;
 };
 
 struct SortArgs {
@@ -740,6 +852,11 @@ static QueryWs carve_query(Carver& c, int64_t m, int64_t cap) {
     w.st = c.take<double>(cap > 0 ? cap : 1);
     w.sid = c.take<int>(cap > 0 ? cap : 1);
     w.sd = c.take<double>(cap > 0 ? cap : 1);
+    // parts: consecutive parts of a ray hold > kSortHuge matches together
+    const int64_t pc = 2 * (cap > 0 ? cap : 0) / kSortHuge + m + 64;
+    w.parts_cap = int(pc < INT_MAX ? pc : INT_MAX);
+    w.parts = c.take<Part>(w.parts_cap);
+    w.parts_n = c.take<int>(1);
     return w;
 }
 
@@ -832,11 +949,45 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
         HP_TRY((launch_sort<2048, kThreads>(A, 1, s)));
     }
     TimedSpan ts("k_query_sort_large", s);
-    HP_TRY((launch_sort<kSortLarge, kSortLargeThreads>(A, 2, s)));
-    k_query_sort<0, kThreads><<<kNumSMs, kThreads, 0, s>>>(offsets, w.soff, w.tmm, nullptr, nullptr,
-                                                           w.lists + kSortClasses * m,
-                                                           w.counts + kSortClasses, w.st, w.sid, w.sd, ids, t_proj,
-                                                           dist_perp);
-    HP_CHECK_LAUNCH("k_query_sort<global>");
+    HP_TRY((launch_sort<4096, 512>(A, 2, s)));
+    HP_TRY((launch_sort<kSortHuge, 1024>(A, 3, s)));
+    // rays above kSortHuge: split into t-ordered parts, sort the parts in place
+    static int occ_parts = 0;
+    if (!occ_parts) {
+        HP_TRY(set_smem(k_query_split, sizeof(SplitSmem)));
+        HP_TRY(set_smem(k_query_sort_parts<kSortHuge, 1024>, sizeof(SortSmem<kSortHuge>)));
+        occ_parts = resident(k_query_sort_parts<kSortHuge, 1024>, 1024, sizeof(SortSmem<kSortHuge>));
+    }
+    if (cudaMemsetAsync(w.parts_n, 0, sizeof(int), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_query_fill memset");
+    k_query_split<<<kNumSMs, kSplitThreads, sizeof(SplitSmem), s>>>(
+        offsets, w.soff, w.tmm, w.lists + kSortClasses * m, w.counts + kSortClasses, w.st, w.sid, w.sd, ids, t_proj,
+        dist_perp, w.parts, w.parts_n, w.parts_cap);
+    HP_CHECK_LAUNCH("k_query_split");
+    k_query_sort_parts<kSortHuge, 1024><<<kNumSMs * occ_parts, 1024, sizeof(SortSmem<kSortHuge>), s>>>(
+        w.parts, w.parts_n, w.parts_cap, ids, t_proj, dist_perp);
+    HP_CHECK_LAUNCH("k_query_sort_parts");
+    return HP_OK;
+}
+
+extern "C" int hp_query_bounds(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
+                               int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                               const double* t_near, const double* t_far, const double* slopes, int64_t m,
+                               int64_t* bound_off, void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+    HP_TRY(check_common(layout, pad, m));
+    (void)padded_h;
+    if (workspace_bytes < scan_workspace_bytes(m + 1)) {
+        set_error("hp_query_bounds: workspace too small");
+        return HP_ESPACE;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (m > 0) {
+        const Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
+        const QCam QC = make_qcam(cam);
+        TimedSpan ts("k_query_bound", s);
+        k_query_bound<<<group_grid(m, 8), kThreads, 0, s>>>(layout, padded_w, int(pad), R, QC, m, bound_off);
+        HP_CHECK_LAUNCH("k_query_bound");
+    }
+    HP_TRY(exclusive_scan_i64(bound_off, bound_off, m, workspace, s));
     return HP_OK;
 }

@@ -18,8 +18,8 @@ import torch
 from . import _lib
 from ._lib import c_i64, c_size
 
-__all__ = ["DeviceIndex", "build", "build_from_table", "query", "sample", "primary_surface",
-           "SAMPLE_EXACT_PER_RAY"]
+__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "sample",
+           "primary_surface", "MatchBudgetExceeded", "SAMPLE_EXACT_PER_RAY"]
 
 # match-scratch capacity of the last query per device (slots), reused so a
 # steady stream of frames sizes its workspace once
@@ -162,13 +162,44 @@ def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered
                        slot_y, slot_z, row_ptr, rx, ry, rz, pid, rf, n_in=n_in)
 
 
+class MatchBudgetExceeded(RuntimeError):
+    """The query's match scratch would exceed ``max_scratch`` slots."""
+
+    def __init__(self, needed: int, budget: int):
+        super().__init__(f"query needs {needed} match slots, budget {budget}")
+        self.needed = needed
+        self.budget = budget
+
+
+def query_bounds(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
+                 t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True) -> torch.Tensor:
+    """Exclusive scan of the per-ray match upper bounds (hp_query_bounds),
+    int64 [m+1]; used to split a frame into ray chunks that fit memory."""
+    lib = _lib.load(require_device=True)
+    dev = index.table_start.device
+    m = int(pixels.shape[0])
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    nb = c_size(0)
+    _lib.check(lib.hp_query_workspace_bytes(m, index.pad, 0, ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
+    out = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    cam = ctypes.byref(camera_struct(index.camera)) if footprint else None
+    _lib.check(lib.hp_query_bounds(index.layout(), cam, index.padded_width, index.padded_height, index.pad,
+                                   _ptr(pixels), 2, _ptr(dirs), _ptr(t_near), _ptr(t_far), _ptr(slopes), m,
+                                   _ptr(out), _ptr(ws), nb.value, _stream()))
+    return out
+
+
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
-          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True, facts: bool = False):
+          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True, facts: bool = False,
+          max_scratch: int | None = None):
     """_kernels.hash_query_batch on the device (reference _kernels.py:86-157).
 
     Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors
     (+ the per-ray sampler facts, int32 [m], with ``facts=True``; pass them to
-    :func:`sample` together with this CSR and these slopes).
+    :func:`sample` together with this CSR and these slopes).  With
+    ``max_scratch`` a frame needing more match slots raises
+    :class:`MatchBudgetExceeded` before any CSR is written.
     """
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
@@ -185,6 +216,8 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
     needed = c_i64(0)
     cap = _QUERY_CAP.get(dev, 0)
+    if max_scratch is not None:
+        cap = min(cap, int(max_scratch))
     _mark("query.setup")
     for _ in range(2):
         _lib.check(lib.hp_query_workspace_bytes(m, index.pad, cap, ctypes.byref(nb)))
@@ -192,8 +225,12 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
         rc = lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap,
                                 ctypes.byref(needed), _ptr(ws), nb.value, _stream())
         if rc == _lib.HP_ESPACE and needed.value > cap:
+            if max_scratch is not None and needed.value > max_scratch:
+                raise MatchBudgetExceeded(int(needed.value), int(max_scratch))
             cap = int(needed.value * 1.0625) + 1024   # grow the match scratch once (and remember)
-            _QUERY_CAP[dev] = cap
+            if max_scratch is not None:
+                cap = min(cap, int(max_scratch))
+            _QUERY_CAP[dev] = max(cap, _QUERY_CAP.get(dev, 0))
             continue
         _lib.check(rc)
         break

@@ -64,37 +64,108 @@ class StageTimer:
 @dataclass
 class FrameResult:
     index: device.DeviceIndex
-    query: tuple
+    query: tuple | None      # the query CSR (None when the frame ran in ray chunks)
     samples: tuple
-
-    @property
-    def Q(self) -> int:
-        return int(self.query[1].numel())
+    Q: int = 0
+    chunks: int = 1
 
     @property
     def R(self) -> int:
         return int(self.samples[1].numel())
 
 
+# bytes of device memory per match slot of one query + sample pass: unsorted
+# scratch 20 + CSR 24 + sampler scratch (bounded) -- sizing ray chunks
+BYTES_PER_MATCH = 56
+
+
+_BUDGET: dict = {}
+
+
+def match_budget(fraction: float = 0.8) -> int:
+    """Match slots one pass may use: a fraction of the device memory free at
+    the first call (cached per device: cudaMemGetInfo costs milliseconds)."""
+    dev = torch.cuda.current_device()
+    if dev not in _BUDGET:
+        free, _ = torch.cuda.mem_get_info()
+        free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()  # torch's cached blocks
+        _BUDGET[dev] = max(int(free * fraction) // BYTES_PER_MATCH, 1 << 20)
+    return _BUDGET[dev]
+
+
+def _concat_samples(parts):
+    """Concatenate per-chunk sampler 9-tuples (offsets rebased)."""
+    if len(parts) == 1:
+        return parts[0]
+    offs, base = [parts[0][0][:1]], 0
+    for p in parts:
+        offs.append(p[0][1:] + base)
+        base += int(p[1].numel())
+    out = [torch.cat(offs)]
+    for k in range(1, 9):
+        out.append(torch.cat([p[k] for p in parts]))
+    return tuple(out)
+
+
 def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_cfg, pixels,
                  dirs, t_near, t_far, slopes, sampler_cfg: SamplerConfig | None = None,
-                 exact_t_end: bool = True, timer: StageTimer | None = None) -> FrameResult:
-    """build -> query -> sample, all on the device (CUDA tensors in and out)."""
-    sampler_cfg = sampler_cfg or SamplerConfig()
+                 exact_t_end: bool = True, timer: StageTimer | None = None,
+                 max_matches: int | None = None) -> FrameResult:
+    """build -> query -> sample, all on the device (CUDA tensors in and out).
+
+    A frame whose query would need more than ``max_matches`` match slots
+    (default: :func:`match_budget`) runs in ray chunks (ray-chunk
+    streaming): the per-ray bounds split the rays, each chunk is queried and
+    sampled in turn, and only the retained samples are kept.  Results are
+    identical (rays are independent)."""
     mark = timer.mark if timer is not None else (lambda name: None)
     mark("start")
     idx = device.build(xyz, camera, search_cfg.pad)
     mark("build")
-    q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True)
+    return _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg or SamplerConfig(),
+                         exact_t_end, max_matches, mark)
+
+
+def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
+                  mark=lambda name: None) -> FrameResult:
+    budget = int(max_matches) if max_matches is not None else match_budget()
+    try:
+        q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
+    except device.MatchBudgetExceeded:
+        return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
+                              exact_t_end, budget, mark)
     mark("query")
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
-    return FrameResult(idx, q[:6], s)
+    return FrameResult(idx, q[:6], s, Q=int(q[1].numel()))
+
+
+def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end,
+                   budget, mark):
+    bo = device.query_bounds(idx, pixels, dirs, t_near, t_far, slopes).cpu().numpy()
+    m = bo.shape[0] - 1
+    cuts = [0]
+    while cuts[-1] < m:
+        a = cuts[-1]
+        b = int(np.searchsorted(bo, bo[a] + budget, side="right")) - 1
+        if b <= a:
+            raise device.MatchBudgetExceeded(int(bo[a + 1] - bo[a]), budget)
+        cuts.append(min(b, m))
+    parts, Q = [], 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        q = device.query(idx, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b], slopes[a:b], facts=True)
+        parts.append(device.sample(q[0], q[1], q[2], q[3], slopes[a:b], sampler_cfg, colors,
+                                   exact_t_end, facts=q[6]))
+        Q += int(q[1].numel())
+        del q
+    mark("query")
+    mark("sample")
+    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts))
 
 
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
                       sampler_cfg: SamplerConfig | None = None, with_colors: bool = True,
-                      exact_t_end: bool = True):
+                      exact_t_end: bool = True, max_matches: int | None = None):
     """Host arrays in, host arrays out: build the index for ``camera``, query
     the rays and run primary-surface sampling.  Returns the numpy 9-tuple of
     ``sample_batch_arrays`` (reference sampler.py:196-217).
@@ -131,9 +202,8 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius,
                 out=sl_host.numpy())
     sl = sl_host.to(dev, non_blocking=True)
-    q = device.query(idx, pix_d, dirs_d, tn, tf, sl, facts=True)
-    s = device.sample(q[0], q[1], q[2], q[3], sl, sampler_cfg or SamplerConfig(), col, exact_t_end,
-                      facts=q[6])
+    s = _query_sample(idx, col, pix_d, dirs_d, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
+                      max_matches).samples
     outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
     for o, x in zip(outs, s):
         o.copy_(x, non_blocking=True)

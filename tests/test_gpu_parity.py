@@ -128,3 +128,25 @@ def test_query_facts_do_not_change_samples(name, exact_t_end):
         b = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, colors, exact_t_end=exact_t_end)
         for x, y in zip(a, b):
             assert torch.equal(x, y)
+
+
+def test_ray_chunked_frame_equals_single_pass():
+    """pipeline.frame_device split into ray chunks (match budget forced
+    small) returns exactly the single-pass samples."""
+    import paper_2404_14044_b200 as hp
+    from paper_2404_14044_b200 import pipeline
+    cloud = hp.generate_scene(hp.SceneSpec("sphere_surface", n=60_000, seed=2, noise=0.005))
+    cam = hp.scene_camera(96, 80, fov_deg=40)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.01), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    m = dirs.shape[0]
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    args = (up(cloud.positions), up(cloud.colors), cam, cfg, up(pixels), up(dirs), up(np.full(m, 1.0)),
+            up(np.full(m, 10.0)), up(slopes))
+    one = pipeline.frame_device(*args)
+    assert one.chunks == 1
+    many = pipeline.frame_device(*args, max_matches=max(one.Q // 7, 1))
+    assert many.chunks >= 7 and many.Q == one.Q and many.query is None
+    for a, b in zip(one.samples, many.samples):
+        assert torch.equal(a, b)
