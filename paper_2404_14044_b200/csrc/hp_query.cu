@@ -660,37 +660,71 @@ __global__ void __launch_bounds__(kSplitThreads) k_query_split(
         __syncthreads();
         block_scan_inplace<(kSplitBins + kSplitThreads - 1) / kSplitThreads>(S.hist, kSplitBins, S.scan_sh);
         __syncthreads();
-        if (tid == 0) {  // greedy grouping of consecutive bins into parts
-            int np = 0, pst = 0;
-            S.pstart[0] = 0;
-            for (int b = 0; b < kSplitBins; b++) {
-                const int bs = S.hist[b], be = b + 1 < kSplitBins ? S.hist[b + 1] : q;
-                if (be - pst > kSortHuge && bs > pst && np + 1 < kMaxParts) {  // close the part before b
-                    S.pstart[++np] = bs;
-                    pst = bs;
-                }
-                S.bin_part[b] = (unsigned short)np;
+        // parts: bin b joins part floor(start_b / (kSortHuge / 2)) (a part holds
+        // at most kSortHuge / 2 + its last bin's matches), renumbered densely
+        constexpr int kHalf = kSortHuge / 2;
+        int flag[(kSplitBins + kSplitThreads - 1) / kSplitThreads];
+#pragma unroll
+        for (int k = 0; k < (kSplitBins + kSplitThreads - 1) / kSplitThreads; k++) {
+            const int b = tid * ((kSplitBins + kSplitThreads - 1) / kSplitThreads) + k;
+            flag[k] = b < kSplitBins && (b == 0 || S.hist[b] / kHalf != S.hist[b - 1] / kHalf);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < (kSplitBins + kSplitThreads - 1) / kSplitThreads; k++) {
+            const int b = tid * ((kSplitBins + kSplitThreads - 1) / kSplitThreads) + k;
+            if (b < kSplitBins) S.cur[b] = flag[k];
+        }
+        __syncthreads();
+        int nparts;
+        {
+            int v[(kSplitBins + kSplitThreads - 1) / kSplitThreads], acc = 0;
+#pragma unroll
+            for (int k = 0; k < (kSplitBins + kSplitThreads - 1) / kSplitThreads; k++) {
+                const int b = tid * ((kSplitBins + kSplitThreads - 1) / kSplitThreads) + k;
+                v[k] = b < kSplitBins ? S.cur[b] : 0;
+                acc += v[k];
             }
-            S.pstart[++np] = q;
+            int run = block_excl_scan<int>(acc, S.scan_sh, &nparts);
+#pragma unroll
+            for (int k = 0; k < (kSplitBins + kSplitThreads - 1) / kSplitThreads; k++) {
+                const int b = tid * ((kSplitBins + kSplitThreads - 1) / kSplitThreads) + k;
+                run += v[k];
+                if (b < kSplitBins) {
+                    const int p = min(run - 1, kMaxParts - 1);
+                    S.bin_part[b] = (unsigned short)p;
+                    if (v[k] && run - 1 < kMaxParts) {
+                        S.pstart[p] = S.hist[b];
+                        // t bounds of the part from its first bin's lower edge (any
+                        // bounds keep the part sort's bucket map monotone)
+                        S.plo[p] = fkey(__double2float_rd(tlo + double(b) / scale));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int np = min(nparts, kMaxParts);
             S.np = np;
+            S.pstart[np] = q;
             S.slot = atomicAdd(parts_n, np);
         }
-        for (int p = tid; p < kMaxParts; p += kSplitThreads) {
-            S.plo[p] = 0xffffffffu;
-            S.phi[p] = 0u;
-        }
+        __syncthreads();
+        for (int p = tid; p < S.np; p += kSplitThreads) S.phi[p] = p + 1 < S.np ? S.plo[p + 1] : tmm[r].y;
         for (int b = tid; b < kSplitBins; b += kSplitThreads) S.cur[b] = S.hist[b];
         __syncthreads();
         for (int e = tid; e < q; e += kSplitThreads) {
             const double t = st[so + e];
             const int b = bin(t);
-            const int pos = atomicAdd(&S.cur[b], 1);
+            const unsigned peers = __match_any_sync(__activemask(), b);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (lane_id() == leader) base = atomicAdd(&S.cur[b], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            const int pos = base + __popc(peers & ((1u << lane_id()) - 1));
             out_t[o + pos] = t;
             out_id[o + pos] = sid[so + e];
             out_d[o + pos] = sd[so + e];
-            const int p = S.bin_part[b];
-            atomicMin(&S.plo[p], fkey(__double2float_rd(t)));
-            atomicMax(&S.phi[p], fkey(__double2float_ru(t)));
         }
         __syncthreads();
         for (int p = tid; p < S.np; p += kSplitThreads) {
@@ -950,7 +984,10 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     }
     TimedSpan ts("k_query_sort_large", s);
     HP_TRY((launch_sort<4096, 512>(A, 2, s)));
-    HP_TRY((launch_sort<kSortHuge, 1024>(A, 3, s)));
+    {
+        TimedSpan t8("k_query_sort_8192", s);
+        HP_TRY((launch_sort<kSortHuge, 1024>(A, 3, s)));
+    }
     // rays above kSortHuge: split into t-ordered parts, sort the parts in place
     static int occ_parts = 0;
     if (!occ_parts) {
@@ -960,6 +997,7 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     }
     if (cudaMemsetAsync(w.parts_n, 0, sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
+    TimedSpan tsp("k_query_split", s);
     k_query_split<<<kNumSMs, kSplitThreads, sizeof(SplitSmem), s>>>(
         offsets, w.soff, w.tmm, w.lists + kSortClasses * m, w.counts + kSortClasses, w.st, w.sid, w.sd, ids, t_proj,
         dist_perp, w.parts, w.parts_n, w.parts_cap);
