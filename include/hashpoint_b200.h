@@ -125,16 +125,16 @@ int hp_query_workspace_bytes(int64_t m, int64_t pad, int64_t capacity, size_t* b
  * for an (m,2) array); dirs float64 [m,3]; t_near/t_far/slopes [m].  Writes
  * probes/scanned [m] (int64, over the full window as the reference) and
  * offsets [m+1] (int64 CSR offsets; offsets[m] = Q); the accepted matches are
- * kept, unsorted, in the workspace.  Synchronises `stream` once to size that
- * scratch: if it needs more than `capacity` slots, returns HP_ESPACE with the
- * requirement in *needed (host pointer, may be NULL) and the caller retries
- * with a larger workspace. */
+ * kept, unsorted, in the workspace (capacity slots).  No host round trip: if
+ * the frame needs more than `capacity` slots nothing else is written and
+ * offsets[m] = -(slots needed); the caller, which reads offsets[m] anyway to
+ * allocate the outputs, grows the workspace and calls again. */
 int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
                    int64_t pad,
                    const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                    const double* t_near, const double* t_far, const double* slopes, int64_t m,
                    int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
-                   int64_t* needed, void* workspace, size_t workspace_bytes, hp_stream_t stream);
+                   void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Upper bounds of the match counts (the slots pass 1 will test per ray),
  * exclusive-scanned into bound_off [m+1] (bound_off[m] = the scratch pass 1
  * needs).  Lets a caller split a frame into ray chunks that fit memory.
@@ -164,16 +164,15 @@ int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity,
 /* Pass 1 over the query CSR (offsets [m+1], ids/t/dist [total], slopes [m],
  * colors float64 [n_colors,3] or NULL).  Writes t_end [m] and r_off [m+1]
  * (r_off[m] = R).  Retained candidates are kept in the workspace for emit.
- * Synchronises `stream` once to read the number of exactly evaluated
- * candidates; if it exceeds exact_capacity, returns HP_ESPACE and stores the
- * required capacity in *exact_needed (host pointer, may be NULL) so the
- * caller can grow the workspace and call again.  query_facts: NULL, or the
- * facts hp_query_fill wrote for exactly this CSR and these slopes. */
+ * No host round trip: if the exactly evaluated candidates exceed
+ * exact_capacity, r_off[m] = -(slots needed) and the caller grows the
+ * workspace and calls again.  query_facts: NULL, or the facts hp_query_fill
+ * wrote for exactly this CSR and these slopes. */
 int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                   const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
                   const int32_t* query_facts,
                   const hp_sampler_params* p, const double* colors, int64_t n_colors,
-                  int64_t* r_off, double* t_end, int64_t* exact_needed,
+                  int64_t* r_off, double* t_end,
                   void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Pass 2: write the R retained candidates (R = r_off[m], host value) in ray
  * order: r_id int64, r_t/r_dist/r_udf/r_alpha/r_w float64 [R], r_color

@@ -54,7 +54,7 @@ _SIGNATURES = {
     "hp_query_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
     "hp_query_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
-                                      ctypes.POINTER(c_i64), c_p, c_size, c_p]),
+                                      c_p, c_size, c_p]),
     "hp_query_bounds": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                        c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_size, c_p]),
     "hp_query_fill": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
@@ -63,7 +63,7 @@ _SIGNATURES = {
                                                  ctypes.POINTER(c_size)]),
     "hp_sample_run": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p, c_p,
                                      ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_p,
-                                     ctypes.POINTER(c_i64), c_p, c_size, c_p]),
+                                     c_p, c_size, c_p]),
     "hp_sample_emit": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
                                       ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),

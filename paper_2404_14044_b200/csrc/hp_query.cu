@@ -235,6 +235,11 @@ __device__ __forceinline__ float from_fkey(unsigned k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
+// offsets[m] = -(scratch slots needed) when the caller's capacity is short
+__global__ void k_mark_overflow(const int64_t* __restrict__ need_at, int64_t capacity, int64_t* __restrict__ total) {
+    if (*need_at > capacity) *total = -*need_at;
+}
+
 // ---------------------------------------------------------------- pass 0
 // Per-ray upper bound of the matches: the number of slots the streaming pass
 // will test for the ray (its footprint rows, exactly as stream_group
@@ -286,9 +291,11 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
                                                          int* __restrict__ sc_id, double* __restrict__ sc_t,
                                                          double* __restrict__ sc_d, uint2* __restrict__ tmm,
                                                          int64_t* __restrict__ counts,
-                                                         int64_t* __restrict__ probes, int64_t* __restrict__ scanned) {
+                                                         int64_t* __restrict__ probes, int64_t* __restrict__ scanned,
+                                                         int64_t capacity) {
     extern __shared__ __align__(16) unsigned char dyn[];
     FillSmem& S = *reinterpret_cast<FillSmem*>(dyn);
+    if (soff[m] > capacity) return;  // scratch too small: hp_query_count reports it in offsets[m]
     const int s = 2 * pad + 1;
     const float4* __restrict__ relf = reinterpret_cast<const float4*>(L.relf);
     for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
@@ -906,10 +913,9 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
                               int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                               const double* t_near, const double* t_far, const double* slopes, int64_t m,
                               int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
-                              int64_t* needed, void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+                              void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(check_common(layout, pad, m));
     (void)padded_h;
-    if (needed) *needed = 0;
     Carver cv(workspace, workspace_bytes);
     QueryWs w = carve_query(cv, m, capacity);
     if (!cv.ok()) {
@@ -926,16 +932,6 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
             HP_CHECK_LAUNCH("k_query_bound");
         }
         HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
-        int64_t need = 0;
-        cudaError_t e = cudaMemcpyAsync(&need, w.soff + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) return cuda_status(e, "hp_query_count: bound");
-        if (needed) *needed = need;
-        if (need > capacity) {
-            set_error("hp_query_count: %lld scratch slots needed, capacity %lld", (long long)need,
-                      (long long)capacity);
-            return HP_ESPACE;
-        }
         static bool attr = false;
         if (!attr) {
             HP_TRY(set_smem(k_query_scan, sizeof(FillSmem)));
@@ -944,10 +940,14 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
         TimedSpan ts("k_query_scan", s);
         k_query_scan<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
                                                                          w.sid, w.st, w.sd, w.tmm, offsets, probes,
-                                                                         scanned);
+                                                                         scanned, capacity);
         HP_CHECK_LAUNCH("k_query_scan");
     }
     HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
+    if (m > 0) {
+        k_mark_overflow<<<1, 1, 0, s>>>(w.soff + m, capacity, offsets + m);
+        HP_CHECK_LAUNCH("k_mark_overflow");
+    }
     return HP_OK;
 }
 

@@ -182,8 +182,14 @@ __global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4*
         plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1]);
 }
 
+// r_off[m] = -(exact slots needed) when the caller's capacity is short
+__global__ void k_mark_exact_overflow(const int64_t* __restrict__ need_at, int64_t cap, int64_t* __restrict__ total) {
+    if (*need_at > cap) *total = -*need_at;
+}
+
 // candidate slot -> ray (warp per ray)
-__global__ void k_sample_expand(int64_t m, const int64_t* __restrict__ eoff, int* __restrict__ cand_ray) {
+__global__ void k_sample_expand(int64_t m, const int64_t* __restrict__ eoff, int* __restrict__ cand_ray, int64_t cap) {
+    if (eoff[m] > cap) return;  // exact scratch too small (hp_sample_run reports it in r_off[m])
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t ray = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); ray < m; ray += warps) {
         const int64_t a = eoff[ray], b = eoff[ray + 1];
@@ -210,6 +216,7 @@ template <class BestT>
 __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
                                                            const int64_t* __restrict__ eoff, Exact X) {
     const int64_t n = eoff[C.m];
+    if (n > X.cap) return;
     unsigned long long evals = 0;
     for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
         const int ray = X.ray[c];
@@ -317,6 +324,7 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
 
 __global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, RayOut RO, const int4* __restrict__ plan,
                                                             const int64_t* __restrict__ eoff, Exact X) {
+    if (eoff[C.m] > X.cap) return;
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
         retain_ray(C, P, ray, RO, plan, eoff, X);
@@ -412,43 +420,32 @@ Params to_params(const hp_sampler_params* p) {
 // Plan (warp per ray) -> scan of the exact-region sizes -> (host reads the
 // total) -> expand (slot -> ray) -> exact evaluation (thread per candidate).
 template <class BestT>
-int launch_exact(const Csr& C, const Params& P, SampleWs& w, int64_t* needed, cudaStream_t s) {
+int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     {
         TimedSpan ts("k_sample_plan", s);
         k_sample_plan<<<kNumSMs * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff);
         HP_CHECK_LAUNCH("k_sample_plan");
     }
     HP_TRY(exclusive_scan_i64(w.eoff, w.eoff, C.m, w.scan, s));
-    int64_t n = 0;
-    cudaError_t e = cudaMemcpyAsync(&n, w.eoff + C.m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_status(e, "hp_sample_run: exact count");
-    if (needed) *needed = n;
-    if (n > w.x.cap) {
-        set_error("hp_sample_run: %lld exact candidates exceed exact_capacity %lld", (long long)n,
-                  (long long)w.x.cap);
-        return HP_ESPACE;
-    }
-    if (n == 0) return HP_OK;
+    // no host round trip: the kernels read the exact-region total on the
+    // device and do nothing if it exceeds the capacity (reported in r_off[m])
     {
         TimedSpan ts("k_sample_expand", s);
-        k_sample_expand<<<kNumSMs * 8, 256, 0, s>>>(C.m, w.eoff, w.x.ray);
+        k_sample_expand<<<kNumSMs * 8, 256, 0, s>>>(C.m, w.eoff, w.x.ray, w.x.cap);
         HP_CHECK_LAUNCH("k_sample_expand");
     }
     {
         TimedSpan ts("k_sample_exact", s);
-        const int64_t blocks = (n + kThreads - 1) / kThreads;
-        k_sample_exact<BestT><<<int(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16), kThreads, 0, s>>>(C, P, w.plan,
-                                                                                                     w.eoff, w.x);
+        k_sample_exact<BestT><<<kNumSMs * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
         HP_CHECK_LAUNCH("k_sample_exact");
     }
     return HP_OK;
 }
 
-int dispatch_exact(const Csr& C, const Params& P, SampleWs& w, int64_t* needed, cudaStream_t s) {
-    if (P.K <= 8) return launch_exact<Best<8>>(C, P, w, needed, s);
-    if (P.K <= 32) return launch_exact<Best<32>>(C, P, w, needed, s);
-    return launch_exact<BestDyn>(C, P, w, needed, s);
+int dispatch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
+    if (P.K <= 8) return launch_exact<Best<8>>(C, P, w, s);
+    if (P.K <= 32) return launch_exact<Best<32>>(C, P, w, s);
+    return launch_exact<BestDyn>(C, P, w, s);
 }
 
 int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleWs& w, cudaStream_t s) {
@@ -488,12 +485,11 @@ extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact
 
 extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
                              const double* dist, int64_t total, int64_t exact_capacity, const double* slopes,
-                             const int32_t* query_facts, const hp_sampler_params* p, const double* colors, int64_t n_colors, int64_t* r_off,
-                             double* t_end, int64_t* exact_needed, void* workspace, size_t workspace_bytes,
-                             hp_stream_t stream) {
+                             const int32_t* query_facts, const hp_sampler_params* p, const double* colors,
+                             int64_t n_colors, int64_t* r_off, double* t_end, void* workspace,
+                             size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
-    if (exact_needed) *exact_needed = 0;
     Carver c(workspace, workspace_bytes);
     SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
     if (!c.ok()) {
@@ -504,10 +500,14 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
     Csr C{offsets, ids, t, dist, slopes, colors, m, query_facts};
     Params P = to_params(p);
     if (m > 0) {
-        HP_TRY(dispatch_exact(C, P, w, exact_needed, s));
+        HP_TRY(dispatch_exact(C, P, w, s));
         HP_TRY(launch_retain(C, P, RayOut{r_off, t_end}, w, s));
     }
     HP_TRY(exclusive_scan_i64(r_off, r_off, m, w.scan, s));
+    if (m > 0) {
+        k_mark_exact_overflow<<<1, 1, 0, s>>>(w.eoff + m, exact_capacity, r_off + m);
+        HP_CHECK_LAUNCH("k_mark_exact_overflow");
+    }
     return HP_OK;
 }
 

@@ -214,7 +214,6 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     cam = ctypes.byref(camera_struct(index.camera)) if footprint else None
     args = (L, cam, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
-    needed = c_i64(0)
     cap = _QUERY_CAP.get(dev, 0)
     if max_scratch is not None:
         cap = min(cap, int(max_scratch))
@@ -222,20 +221,19 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     for _ in range(2):
         _lib.check(lib.hp_query_workspace_bytes(m, index.pad, cap, ctypes.byref(nb)))
         ws = _workspace(nb.value, dev)
-        rc = lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap,
-                                ctypes.byref(needed), _ptr(ws), nb.value, _stream())
-        if rc == _lib.HP_ESPACE and needed.value > cap:
-            if max_scratch is not None and needed.value > max_scratch:
-                raise MatchBudgetExceeded(int(needed.value), int(max_scratch))
-            cap = int(needed.value * 1.0625) + 1024   # grow the match scratch once (and remember)
-            if max_scratch is not None:
-                cap = min(cap, int(max_scratch))
-            _QUERY_CAP[dev] = max(cap, _QUERY_CAP.get(dev, 0))
-            continue
-        _lib.check(rc)
-        break
-    _mark("query.count")
-    total = int(offsets[m].item())
+        _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap, _ptr(ws),
+                                      nb.value, _stream()))
+        _mark("query.count")
+        total = int(offsets[m].item())
+        if total >= 0:
+            break
+        needed = -total  # scratch too small: nothing was written, grow it once (and remember)
+        if max_scratch is not None and needed > max_scratch:
+            raise MatchBudgetExceeded(needed, int(max_scratch))
+        cap = int(needed * 1.0625) + 1024
+        if max_scratch is not None:
+            cap = min(cap, int(max_scratch))
+        _QUERY_CAP[dev] = max(cap, _QUERY_CAP.get(dev, 0))
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
@@ -287,7 +285,6 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     t_end = torch.empty(max(m, 0), dtype=torch.float64, device=dev)
     col = colors.contiguous() if want else None
     ncol = int(col.shape[0]) if want else 0
-    needed = c_i64(0)
     _mark("sample.setup")
     for _ in range(2):
         nb = c_size(0)
@@ -297,15 +294,12 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
         common = (_ptr(offsets), m, _ptr(ids), _ptr(t), _ptr(dist), total, exact_cap,
                   _ptr(slopes), ctypes.byref(p), _ptr(col) if want else ctypes.c_void_p(0), ncol)
         run_args = common[:8] + (_ptr(facts) if facts is not None else ctypes.c_void_p(0),) + common[8:]
-        rc = lib.hp_sample_run(*run_args, _ptr(r_off), _ptr(t_end), ctypes.byref(needed), _ptr(ws),
-                               nb.value, _stream())
-        if rc == _lib.HP_ESPACE and needed.value > exact_cap:
-            exact_cap = int(needed.value)   # grow the exact-candidate scratch once
-            continue
-        _lib.check(rc)
-        break
-    _mark("sample.run")
-    R = int(r_off[m].item())
+        _lib.check(lib.hp_sample_run(*run_args, _ptr(r_off), _ptr(t_end), _ptr(ws), nb.value, _stream()))
+        _mark("sample.run")
+        R = int(r_off[m].item())
+        if R >= 0:
+            break
+        exact_cap = int(-R * 1.0625) + 1024   # exact scratch too small: grow it once
     i64 = dict(dtype=torch.int64, device=dev)
     f64 = dict(dtype=torch.float64, device=dev)
     r_id = torch.empty(R, **i64)
