@@ -146,9 +146,9 @@ __device__ void group_setup(GroupHead& S, const Rays& R, const QCam& QC, int64_t
 // the copies of slots [c0, c1); test(buf, row, g, k, c0) runs on the warp
 // owning ray g (warp w owns rays w, w+8, ...), 32 slots at a time, with
 // k = -1 for lanes beyond the ray's sub-range.
-template <int kStage, class Issue, class Test, class Tab>
+template <int kStage, class Issue, class Test, class Tab, class Done>
 __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, const QCam& QC,
-                             Issue issue, Test test, Tab tab) {
+                             Issue issue, Test test, Tab tab, Done done) {
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
     const int pad = (s - 1) / 2;
     for (int yb = S.v0; yb < S.v1; yb += kRowsMax) {
@@ -217,6 +217,7 @@ __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64
                     const int k = base + lane;
                     test(buf, g, k < hi ? k : -1, c0);
                 }
+                if (lo < hi) done(g);  // warp-uniform: end of ray g's slots in this chunk
             }
             __syncthreads();
             row = nrow;
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
             S.off[threadIdx.x] = soff[r0 + threadIdx.x];
         }
         group_setup(S.head, R, QC, r0, G, s);
+        unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's t bounds for the current ray
         stream_group<kStageFill>(
             S.head, G, L, wp, s, QC,
             [&](int buf, int c0, int c1) {
@@ -333,28 +335,29 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
                     }
                 }
                 const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
-                if (b) {
-                    unsigned lo = 0xffffffffu, hi = 0u;
-                    if (cls == 1) {
-                        const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
-                        sc_t[pos] = t;
-                        sc_d[pos] = sqrt(d2);
-                        sc_id[pos] = S.pid[buf][k - c0];
-                        lo = fkey(__double2float_rd(t));
-                        hi = fkey(__double2float_ru(t));
-                    }
-                    lo = __reduce_min_sync(0xffffffffu, lo);
-                    hi = __reduce_max_sync(0xffffffffu, hi);
-                    __syncwarp();
-                    if (lane_id() == 0) {  // ray g belongs to this warp alone
-                        S.fill[g] += __popc(b);
-                        S.tmin[g] = min(S.tmin[g], lo);
-                        S.tmax[g] = max(S.tmax[g], hi);
-                    }
-                    __syncwarp();
+                if (cls == 1) {
+                    const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
+                    sc_t[pos] = t;
+                    sc_d[pos] = sqrt(d2);
+                    sc_id[pos] = S.pid[buf][k - c0];
+                    lmin = min(lmin, fkey(__double2float_rd(t)));
+                    lmax = max(lmax, fkey(__double2float_ru(t)));
                 }
+                __syncwarp();
+                if (lane_id() == 0) S.fill[g] += __popc(b);  // ray g belongs to this warp alone
+                __syncwarp();
             },
-            [&](int g, int n) { atomicAdd(&S.scn[g], n); });
+            [&](int g, int n) { atomicAdd(&S.scn[g], n); },
+            [&](int g) {  // per-lane t bounds of ray g's matches in this chunk -> the ray's
+                const unsigned lo = __reduce_min_sync(0xffffffffu, lmin);
+                const unsigned hi = __reduce_max_sync(0xffffffffu, lmax);
+                if (lane_id() == 0) {
+                    S.tmin[g] = min(S.tmin[g], lo);
+                    S.tmax[g] = max(S.tmax[g], hi);
+                }
+                lmin = 0xffffffffu;
+                lmax = 0u;
+            });
         __syncthreads();
         if (threadIdx.x < G) {
             tmm[r0 + threadIdx.x] = make_uint2(S.tmin[threadIdx.x], S.tmax[threadIdx.x]);
