@@ -593,7 +593,7 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t m, int* 
 // Sort the rays of one size class (list of ray ids) from the scratch (ray r
 // at soff[r]) into the outputs (at off[r]) in shared memory.
 template <int kCap, int kT>
-__global__ void __launch_bounds__(kT) k_query_sort(const int64_t* __restrict__ off, const int64_t* __restrict__ soff,
+__global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_query_sort(const int64_t* __restrict__ off, const int64_t* __restrict__ soff,
                                                    const uint2* __restrict__ tmm, const double* slopes, int* facts,
                                                    const int* __restrict__ list,
                                                    const int* __restrict__ list_n, double* __restrict__ st,
@@ -983,7 +983,7 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
     {
         TimedSpan ts("k_query_sort", s);
         HP_TRY((launch_sort<1024, kThreads>(A, 0, s)));
-        HP_TRY((launch_sort<2048, kThreads>(A, 1, s)));
+        HP_TRY((launch_sort<2048, 512>(A, 1, s)));
     }
     TimedSpan ts("k_query_sort_large", s);
     HP_TRY((launch_sort<4096, 512>(A, 2, s)));
