@@ -215,6 +215,8 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     args = (L, cam, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
     cap = _QUERY_CAP.get(dev, 0)
+    if cap > 4096 * max(m, 1):  # remembered from a much larger frame: let this one size itself
+        cap = 0
     if max_scratch is not None:
         cap = min(cap, int(max_scratch))
     _mark("query.setup")
@@ -233,7 +235,7 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
         cap = int(needed * 1.0625) + 1024
         if max_scratch is not None:
             cap = min(cap, int(max_scratch))
-        _QUERY_CAP[dev] = max(cap, _QUERY_CAP.get(dev, 0))
+        _QUERY_CAP[dev] = cap
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
