@@ -150,3 +150,23 @@ def test_ray_chunked_frame_equals_single_pass():
     assert many.chunks >= 7 and many.Q == one.Q and many.query is None
     for a, b in zip(one.samples, many.samples):
         assert torch.equal(a, b)
+
+
+def test_degenerate_frames():
+    """No rays, rays that hit nothing, an empty cloud: the chained device
+    path returns empty / all-zero results without launching garbage."""
+    import paper_2404_14044_b200 as hp
+    from paper_2404_14044_b200 import pipeline
+    cam = hp.scene_camera(16, 12, fov_deg=40)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.01), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    far = hp.generate_scene(hp.SceneSpec("uniform_box", n=500, seed=1, center=(0.0, 0.0, 50.0), extent=1.0))
+    empty = np.zeros((0, 3))
+    for pos, m in ((far.positions, dirs.shape[0]), (empty, dirs.shape[0]), (far.positions, 0)):
+        fr = pipeline.frame_device(up(pos), None, cam, cfg, up(pixels[:m]), up(dirs[:m]),
+                                   up(np.full(m, 1.0)), up(np.full(m, 10.0)), up(slopes[:m]))
+        r_off, r_id, *_, t_end = fr.samples
+        assert fr.Q == 0 and r_id.numel() == 0 and r_off.numel() == m + 1
+        assert torch.all(r_off == 0) and torch.all(t_end == 1.0)
