@@ -462,13 +462,17 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* s
         const int nb = q;  // fine buckets
         // float bounds of the segment's t, from the streaming pass (any
         // monotone bucket map gives the same order: exact in-bucket ranks)
-        const double tlo = double(from_fkey(mm.x)), thi = double(from_fkey(mm.y));
-        const double span = dsub(thi, tlo);
+        // The map is computed in fp32 (each step is monotone under round to
+        // nearest: float(t), - tlo, * scale, fminf), once per element; the
+        // coarse coordinate is kept in bk[] for the fine pass.
+        const float tlo = from_fkey(mm.x), thi = from_fkey(mm.y);
+        const float span = thi - tlo;
         // capped so that 0 * scale stays 0 when the span is tiny
-        const double cscale = span > 0.0 ? fmin(__ddiv_rn(double(kCoarse), span), DBL_MAX) : 0.0;
-        auto coarse_x = [&](double t) { return fmin(dmul(dsub(t, tlo), cscale), double(kCoarse)); };
+        const float cscale = span > 0.0f ? fminf(float(kCoarse) / span, FLT_MAX) : 0.0f;
         for (int e = tid; e < q; e += kT) {
-            const int b = min(int(coarse_x(F.t[e])), kCoarse - 1);
+            const float x = fminf((__double2float_rn(F.t[e]) - tlo) * cscale, float(kCoarse));
+            F.bk[e] = __float_as_uint(x);
+            const int b = min(int(x), kCoarse - 1);
             const unsigned peers = __match_any_sync(__activemask(), b);
             if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.chist[b], __popc(peers));
         }
@@ -486,13 +490,13 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* s
         }
         __syncthreads();
         for (int e = tid; e < q; e += kT) {
-            const double x = coarse_x(F.t[e]);
+            const float x = __uint_as_float(F.bk[e]);
             const int b = min(int(x), kCoarse - 1);
             const int f0 = F.chist[b], width = F.chist[b + 1] - f0;
             int f = f0;
             if (width > 1) {
                 // x - b is exact (Sterbenz) and in [0, 1]
-                const int off = int(dmul(dsub(x, double(b)), double(width)));
+                const int off = int((x - float(b)) * float(width));
                 f += min(off, width - 1);
             }
             f = min(f, nb - 1);
