@@ -127,14 +127,16 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
 
 
 def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
-                  mark=lambda name: None) -> FrameResult:
+                  mark=lambda name: None, before_sample=lambda: None) -> FrameResult:
     budget = int(max_matches) if max_matches is not None else match_budget()
     try:
         q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
     except device.MatchBudgetExceeded:
+        before_sample()
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                               exact_t_end, budget, mark)
     mark("query")
+    before_sample()
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
     return FrameResult(idx, q[:6], s, Q=int(q[1].numel()))
@@ -183,27 +185,36 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
             return a.to(device=dev, dtype=dt, non_blocking=True)
         return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt, non_blocking=True)
 
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(main)
     xyz = up(cloud.positions, torch.float64)
-    col = up(cloud.colors, torch.float64) if (with_colors and cloud.colors is not None) else None
     idx = device.build(xyz, camera, search_cfg.pad)          # async on the stream
     px_host = pixels.numpy() if isinstance(pixels, torch.Tensor) else np.asarray(pixels)
     px_host = np.ascontiguousarray(px_host, dtype=np.int64).reshape(-1, 2)
     m = px_host.shape[0]
-    pix_d = up(pixels, torch.int64).view(m, 2)               # copies overlap the host slopes
-    dirs_d = up(dirs, torch.float64).view(m, 3)
 
     def per_ray(a):
         if isinstance(a, torch.Tensor) and a.numel() == m:
             return up(a.reshape(m), torch.float64)
         return up(np.broadcast_to(np.asarray(a, np.float64), (m,)), torch.float64)
 
-    tn, tf = per_ray(t_near), per_ray(t_far)
+    with torch.cuda.stream(side):  # ray uploads overlap the build and the host slopes
+        pix_d = up(pixels, torch.int64).view(m, 2)
+        dirs_d = up(dirs, torch.float64).view(m, 3)
+        tn, tf = per_ray(t_near), per_ray(t_far)
     sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
     host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius,
                 out=sl_host.numpy())
-    sl = sl_host.to(dev, non_blocking=True)
+    with torch.cuda.stream(side):
+        sl = sl_host.to(dev, non_blocking=True)
+        rays_ready = side.record_event()
+        # colours are needed by the sampler only: their upload overlaps the query
+        col = up(cloud.colors, torch.float64) if (with_colors and cloud.colors is not None) else None
+        cols_ready = side.record_event()
+    main.wait_event(rays_ready)
     s = _query_sample(idx, col, pix_d, dirs_d, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
-                      max_matches).samples
+                      max_matches, before_sample=lambda: main.wait_event(cols_ready)).samples
     outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
     for o, x in zip(outs, s):
         o.copy_(x, non_blocking=True)

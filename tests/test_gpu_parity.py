@@ -170,3 +170,17 @@ def test_degenerate_frames():
         r_off, r_id, *_, t_end = fr.samples
         assert fr.Q == 0 and r_id.numel() == 0 and r_off.numel() == m + 1
         assert torch.all(r_off == 0) and torch.all(t_end == 1.0)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "small_sphere_surface", "orbit_planes", "empty"])
+def test_search_and_sample_host_api_matches_goldens(name):
+    """The public host-buffer pipeline (numpy in / numpy out, side-stream
+    uploads, host slopes in the library) reproduces the reference goldens."""
+    from paper_2404_14044_b200 import pipeline
+    if name not in gu.case_names():
+        pytest.skip(f"no golden case {name}")
+    g = gu.load(name)
+    _, cloud, cam, cfg, tn, tf, stride, samplers = gu.get_case(name)
+    pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)
+    out = pipeline.search_and_sample(cloud, cam, cfg, pixels, dirs, t_near, t_far)
+    gu.check_sample(g, "sample_default_", out, g["rows"], check_t_end=True)
