@@ -80,6 +80,13 @@ BYTES_PER_MATCH = 56
 
 
 _BUDGET: dict = {}
+_SIDE: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream(device=dev)
+    return _SIDE[dev]
 
 
 def match_budget(fraction: float = 0.8) -> int:
@@ -186,7 +193,7 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
         return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt, non_blocking=True)
 
     main = torch.cuda.current_stream()
-    side = torch.cuda.Stream()
+    side = _side_stream(dev)  # persistent: the caching allocator pools blocks per stream
     side.wait_stream(main)
     xyz = up(cloud.positions, torch.float64)
     idx = device.build(xyz, camera, search_cfg.pad)          # async on the stream
