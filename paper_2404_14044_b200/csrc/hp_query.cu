@@ -19,13 +19,16 @@
 // the uncertain pairs and produces the exact t_proj / dist_perp of accepted
 // ones, so results are bit-identical to the reference.
 //
-//   k_query_count  exact per-ray count, probes (= s*s), scanned; offsets = scan
-//   k_query_fill   same streaming; accepted pairs written (unsorted) into the
-//                  ray's CSR segment
-//   k_query_sort   per ray: (t, id) sort of its segment in shared memory
-//                  (bucket by t + exact in-bucket rank), in place; segments
-//                  longer than the shared buffer use an in-place sorting
-//                  network in global memory
+//   k_query_bound  per-ray upper bound of the matches (footprint slots):
+//                  scanned into the rays' scratch offsets
+//   k_query_scan   the one streaming pass: accepted pairs (t, id, dist) are
+//                  appended unsorted to the ray's scratch segment; exact
+//                  counts (-> CSR offsets), probes, scanned, float t bounds
+//   k_query_sort   per ray (size classes): (t, id) sort of its segment in
+//                  shared memory (equalised buckets of t + exact in-bucket
+//                  rank) into the CSR; rays above the largest class are
+//                  split into t-ordered parts first (k_query_split)
+// (hp_query_count = bound + scan, hp_query_fill = sort)
 #include <math_constants.h>
 
 #include <cfloat>
@@ -41,7 +44,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGroupMax = 32;  // rays per group
-constexpr int kStageCount = 512;
 constexpr int kStageFill = 384;
 
 struct Rays {
@@ -394,9 +396,6 @@ struct SortSmem {
     int fcount, fbad;  // per-ray facts for the sampler (see sort_segment)
 };
 
-__device__ __forceinline__ double from_okey(unsigned long long k) {
-    return __longlong_as_double((k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k);
-}
 
 // Block-wide exclusive scan of a[0..n) in place (n <= per * blockDim.x).
 template <int kPer>

@@ -42,7 +42,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kSampleGrid = kNumSMs * 4;
 
 // Path counters: rays, fast rays, proved-zero rays, exact evaluations,
 // candidates, bound evaluations.  Read with hp_sample_debug_counters().
