@@ -14,18 +14,29 @@
 //   retention: eps mode keeps w_j >= eps; tau mode keeps the prefix while
 //   T (before j) >= tau_min.
 //
-// One WARP per ray (no block barriers; the ray's t/ds are read through L1),
-// with these exact reformulations:
+// Kernels (hp_sample_run / hp_sample_emit):
+//   k_sample_plan    warp per ray: fast-path preconditions (or the query's
+//                    facts), j*, and a monotone upper bound of the reference's
+//                    transmittance (bound factors from window members, a
+//                    shared-memory ring of the last 64 candidates) -> the
+//                    exact region [0, E): E = je, the index where retention is
+//                    decided, when the product is proved to reach exactly 0
+//                    (or in exit mode), else q
+//   k_sample_expand  exact slot -> ray
+//   k_sample_exact   thread per exact candidate: K nearest, udf, alpha, colour
+//   k_sample_retain  warp per ray: the reference's sequential compositing
+//                    over [0, E), retention (compacted in place), t_end
+//   k_emit           retained candidates -> the output CSR
+// Exact reformulations:
 //   * use_el(j) = (#{ds_i <= r_j} >= K) = (ds_(K) <= r_j) is monotone in j
-//     when t is sorted and slope >= 0: one pass finds the K-th smallest ds and
-//     a search over j finds the first j where it holds.
-//   * exact K-nearest search expands outward from j in t order and stops when
-//     (t_edge - t_j)^2 > the K-th best d2; selection key (d2, i) reproduces the
-//     reference's strict-< insertion.
-//   * only candidates before the retention decision need the exact alpha; a
-//     cheap monotone upper bound of the reference's transmittance (bound
-//     factors from any K pool members) locates that point and, in exact-t_end
-//     mode, proves when the reference's product underflows to exactly 0.
+//     when t is sorted and slope >= 0: a search over j finds the first j
+//     where it holds.
+//   * the exact K-nearest search expands outward from j in t order and stops
+//     when (t_edge - t_j)^2 > the K-th best d2; selection key (d2, i)
+//     reproduces the reference's strict-< insertion.
+//   * only candidates before the retention decision need the exact alpha;
+//     the bound locates that point and, in exact-t_end mode, proves when the
+//     reference's product underflows to exactly 0.
 // Rays violating the preconditions (unsorted t, negative/NaN values) take the
 // reference's direct loops, still on the device.
 #include <math_constants.h>
