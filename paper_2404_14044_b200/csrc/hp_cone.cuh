@@ -46,14 +46,23 @@ struct RayParams {
 
 // _cone_test (_kernels.py:22-36): t = p.d; reject outside [tn, tf]; reject
 // when |p - t d|^2 > (t * slope)^2.  Returns the exact fp64 t and dist^2.
+// t = p.d and |p - t d|^2 in the reference's operation order (no FMA); the
+// query sort recomputes dist^2 from the same p, t and d (bit-identical).
+HP_HD double cone_t(double p0, double p1, double p2, double d0, double d1, double d2) {
+    return cadd(cadd(cmul(p0, d0), cmul(p1, d1)), cmul(p2, d2));
+}
+HP_HD double cone_dist2(double p0, double p1, double p2, double t, double d0, double d1, double d2) {
+    const double e0 = csub(p0, cmul(t, d0));
+    const double e1 = csub(p1, cmul(t, d1));
+    const double e2 = csub(p2, cmul(t, d2));
+    return cadd(cadd(cmul(e0, e0), cmul(e1, e1)), cmul(e2, e2));
+}
+
 HP_HD bool cone_test(double p0, double p1, double p2, const RayParams& r,
                                           double& t, double& dist2) {
-    t = cadd(cadd(cmul(p0, r.d0), cmul(p1, r.d1)), cmul(p2, r.d2));
+    t = cone_t(p0, p1, p2, r.d0, r.d1, r.d2);
     if (t < r.tn || t > r.tf) return false;
-    const double e0 = csub(p0, cmul(t, r.d0));
-    const double e1 = csub(p1, cmul(t, r.d1));
-    const double e2 = csub(p2, cmul(t, r.d2));
-    dist2 = cadd(cadd(cmul(e0, e0), cmul(e1, e1)), cmul(e2, e2));
+    dist2 = cone_dist2(p0, p1, p2, t, r.d0, r.d1, r.d2);
     const double rad = cmul(t, r.slope);
     return !(dist2 > cmul(rad, rad));
 }
