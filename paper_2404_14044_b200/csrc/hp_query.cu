@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
                 if (cls == 1) {
                     const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
                     sc_t[pos] = t;
-                    sc_d[pos] = sqrt(d2);
+                    sc_d[pos] = d2;  // dist^2: the sort takes the square root
                     sc_id[pos] = S.pid[buf][k - c0];
                     lmin = min(lmin, fkey(__double2float_rd(t)));
                     lmax = max(lmax, fkey(__double2float_ru(t)));
@@ -547,7 +547,7 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* s
         const double r0 = dmul(slope, F.t[F.perm[0]]);
         int cnt = 0;
         for (int p = tid; p < q; p += kT) {
-            const double d = F.d[F.perm[p]];
+            const double d = sqrt(F.d[F.perm[p]]);
             gd[p] = d;
             bad |= !(d >= 0.0) || !(d <= DBL_MAX);
             cnt += d <= r0;
@@ -556,7 +556,7 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* s
         if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(&F.fbad, 1);
         if (lane_id() == 0 && cnt) atomicAdd(&F.fcount, cnt);
     } else {
-        for (int p = tid; p < q; p += kT) gd[p] = F.d[F.perm[p]];
+        for (int p = tid; p < q; p += kT) gd[p] = sqrt(F.d[F.perm[p]]);
     }
     __syncthreads();
     if (fact && tid == 0) *fact = F.fbad ? -1 : F.fcount;
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_query_split(
             const int pos = base + __popc(peers & ((1u << lane_id()) - 1));
             out_t[o + pos] = t;
             out_id[o + pos] = sid[so + e];
-            out_d[o + pos] = sd[so + e];
+            out_d[o + pos] = sd[so + e];  // dist^2 until the part sort
         }
         __syncthreads();
         for (int p = tid; p < S.np; p += kSplitThreads) {
@@ -779,6 +779,8 @@ __global__ void __launch_bounds__(kT) k_query_sort_parts(const Part* __restrict_
                     ii[a] = ii[b];
                     ii[b] = y;
                 });
+            __syncthreads();
+            for (int64_t p = threadIdx.x; p < P.size; p += kT) dd[p] = sqrt(dd[p]);  // dist^2 -> dist
             __syncthreads();
         }
     }
