@@ -169,25 +169,37 @@ __device__ void eval_exact(const View& V, int q, int j, bool fast,
     const bool full = ksel == kMaxK;
     if (fast) {
         // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
+        // (t, ds) of the next candidate on each side are loaded one step ahead
         int l = j, r = j + 1;
-        double tl = tj, tr = r < q ? V.t(r) : 0.0;
+        double tl = tj, dl = V.d(j), tr = 0.0, dr = 0.0;
+        if (r < q) {
+            tr = V.t(r);
+            dr = V.d(r);
+        }
         while (l >= 0 || r < q) {
             const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
             int i;
-            double ti;
+            double ti, di;
             if (go_left) {
                 i = l;
                 ti = tl;
-                if (--l >= 0) tl = V.t(l);
+                di = dl;
+                if (--l >= 0) {
+                    tl = V.t(l);
+                    dl = V.d(l);
+                }
             } else {
                 i = r;
                 ti = tr;
-                if (++r < q) tr = V.t(r);
+                di = dr;
+                if (++r < q) {
+                    tr = V.t(r);
+                    dr = V.d(r);
+                }
             }
             const double dt = dsub(ti, tj);
             const double lb = dmul(dt, dt);
             if (lb > kd) break;  // the other side is at least as far
-            const double di = V.d(i);
             if (use_el && di > rj) continue;
             const double d2 = dadd(lb, dmul(di, di));
             evals++;
