@@ -151,14 +151,19 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     if (fast) {
         Chain S;
         S.je = q;
+        // this lane's (t, ds) of the current chunk, loaded one chunk ahead
+        double tn = lane < q ? ldg(T + lane) : 0.0, dn = lane < q ? ldg(DS + lane) : 0.0;
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
             double u = 1.0;
             if (P.K <= 32) {
-                const double tj = j < q ? ldg(T + j) : 0.0;
+                const double tj = tn, dj = dn;
+                const int jn = j + 32;
+                tn = jn < q ? ldg(T + jn) : 0.0;
+                dn = jn < q ? ldg(DS + jn) : 0.0;
                 __syncwarp();
                 rt[j & 63] = tj;
-                rd[j & 63] = j < q ? ldg(DS + j) : 0.0;
+                rd[j & 63] = dj;
                 __syncwarp();
                 if (j < q) {
                     u = (j >= P.K - 1 || c0 + 32 >= min(q, P.K))
