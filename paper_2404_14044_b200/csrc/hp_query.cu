@@ -878,11 +878,11 @@ struct SortArgs {
 // One shared-memory size class: grid = SMs x resident CTAs (occupancy API).
 template <int kCap, int kT>
 static int launch_sort(const SortArgs& A, int cls, cudaStream_t s) {
-    static int occ = 0;
-    if (!occ) {
-        HP_TRY(set_smem(k_query_sort<kCap, kT>, sizeof(SortSmem<kCap>)));
-        occ = resident(k_query_sort<kCap, kT>, kT, sizeof(SortSmem<kCap>));
-    }
+    // once per process (thread-safe initialisation); a failure shows at launch
+    static const int occ = [] {
+        set_smem(k_query_sort<kCap, kT>, sizeof(SortSmem<kCap>));
+        return resident(k_query_sort<kCap, kT>, kT, sizeof(SortSmem<kCap>));
+    }();
     k_query_sort<kCap, kT><<<kNumSMs * occ, kT, sizeof(SortSmem<kCap>), s>>>(
         A.offsets, A.w.soff, A.w.tmm, A.slopes, A.facts, A.w.lists + int64_t(cls) * A.m, A.w.counts + cls, A.w.st, A.w.sid, A.w.sd,
         A.ids, A.t, A.d);
@@ -940,11 +940,8 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
             HP_CHECK_LAUNCH("k_query_bound");
         }
         HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
-        static bool attr = false;
-        if (!attr) {
-            HP_TRY(set_smem(k_query_scan, sizeof(FillSmem)));
-            attr = true;
-        }
+        static const int attr = set_smem(k_query_scan, sizeof(FillSmem));  // once (thread-safe)
+        (void)attr;
         TimedSpan ts("k_query_scan", s);
         k_query_scan<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
                                                                          w.sid, w.st, w.sd, w.tmm, offsets, probes,
@@ -997,12 +994,11 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
         HP_TRY((launch_sort<kSortHuge, 1024>(A, 3, s)));
     }
     // rays above kSortHuge: split into t-ordered parts, sort the parts in place
-    static int occ_parts = 0;
-    if (!occ_parts) {
-        HP_TRY(set_smem(k_query_split, sizeof(SplitSmem)));
-        HP_TRY(set_smem(k_query_sort_parts<kSortHuge, 1024>, sizeof(SortSmem<kSortHuge>)));
-        occ_parts = resident(k_query_sort_parts<kSortHuge, 1024>, 1024, sizeof(SortSmem<kSortHuge>));
-    }
+    static const int occ_parts = [] {  // once (thread-safe)
+        set_smem(k_query_split, sizeof(SplitSmem));
+        set_smem(k_query_sort_parts<kSortHuge, 1024>, sizeof(SortSmem<kSortHuge>));
+        return resident(k_query_sort_parts<kSortHuge, 1024>, 1024, sizeof(SortSmem<kSortHuge>));
+    }();
     if (cudaMemsetAsync(w.parts_n, 0, sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     TimedSpan tsp("k_query_split", s);
