@@ -27,3 +27,11 @@ for n in (2, 4, 8):
     times = [timed(*bench.row_bands(w, n, k)) for k in range(n)]
     tm = max(times)
     print("N=%d band ms min %.3f max %.3f -> est %.1f M rays/s, efficiency %.2f" % (n, min(times), tm, w["m"] / tm / 1e3, t1 / (n * tm)))
+if len(sys.argv) > 2:  # per-band detail at N = argv[2]
+    from paper_2404_14044_b200.shard import row_costs
+    n = int(sys.argv[2])
+    rc = row_costs(w["cloud"].positions, w["cam"], w["cfg"].pad)
+    for k in range(n):
+        r0, r1 = bench.row_bands(w, n, k)
+        W = w["cam"].width
+        print("band", k, "rows", r0 // W, r1 // W, "cost %.3e" % rc[r0 // W:r1 // W].sum(), "ms %.3f" % timed(r0, r1))
