@@ -425,6 +425,96 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
 // placed linearly inside its bin's share.  The map is monotone in t, so
 // buckets are ordered; each element's final position is its bucket start
 // plus its exact (t, id) rank among the (few) members of its bucket.
+// The (t, id) order of q elements staged in shared memory -> perm[0, q):
+// q <= 64 by direct ranks; else an equalised bucket map of t (256-bin coarse
+// histogram over the float bounds [tlo, thi] -> q fine buckets allotted in
+// proportion -> linear inside a bin; fp32, every step monotone) and an exact
+// rank inside each bucket.  hist needs kCap + 1 entries; chist kCoarse + 1
+// (both zeroed by the caller when q > 64).  Ends with a barrier.
+template <int kCap, int kT>
+__device__ void rank_segment(int q, float tlo, float thi, const double* t, const int* id, unsigned* bk, int* hist,
+                             unsigned short* lst, unsigned short* perm, int* chist, int* scan_sh) {
+    const int tid = threadIdx.x;
+    if (q <= 64) {
+        for (int e = tid; e < q; e += kT) {
+            const double te = t[e];
+            const int ie = id[e];
+            int rank = 0;
+            for (int k = 0; k < q; k++) rank += key_less(t[k], id[k], te, ie);
+            perm[rank] = (unsigned short)e;
+        }
+        __syncthreads();
+    } else {
+        const int nb = q;  // fine buckets
+        // float bounds of the segment's t, from the streaming pass (any
+        // monotone bucket map gives the same order: exact in-bucket ranks)
+        // The map is computed in fp32 (each step is monotone under round to
+        // nearest: float(t), - tlo, * scale, fminf), once per element; the
+        // coarse coordinate is kept in bk[] for the fine pass.
+        const float span = thi - tlo;
+        // capped so that 0 * scale stays 0 when the span is tiny
+        const float cscale = span > 0.0f ? fminf(float(kCoarse) / span, FLT_MAX) : 0.0f;
+        for (int e = tid; e < q; e += kT) {
+            const float x = fminf((__double2float_rn(t[e]) - tlo) * cscale, float(kCoarse));
+            bk[e] = __float_as_uint(x);
+            const int b = min(int(x), kCoarse - 1);
+            const unsigned peers = __match_any_sync(__activemask(), b);
+            if (lane_id() == __ffs(peers) - 1) atomicAdd(&chist[b], __popc(peers));
+        }
+        __syncthreads();
+        // coarse prefix counts -> first fine bucket of each coarse bin
+        if (tid < 32) {
+            int run = 0;
+            for (int c0 = 0; c0 < kCoarse; c0 += 32) {
+                const int v = chist[c0 + tid];
+                const int inc = warp_incl_scan(v);
+                chist[c0 + tid] = int((int64_t(run + inc - v) * nb) / q);
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (tid == 0) chist[kCoarse] = nb;
+        }
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
+            const float x = __uint_as_float(bk[e]);
+            const int b = min(int(x), kCoarse - 1);
+            const int f0 = chist[b], width = chist[b + 1] - f0;
+            int f = f0;
+            if (width > 1) {
+                // x - b is exact (Sterbenz) and in [0, 1]
+                const int off = int((x - float(b)) * float(width));
+                f += min(off, width - 1);
+            }
+            f = min(f, nb - 1);
+            const int li = atomicAdd(&hist[f], 1);
+            bk[e] = (unsigned(f) << 16) | unsigned(li);
+        }
+        __syncthreads();
+        block_scan_inplace<(kCap + kT - 1) / kT>(hist, nb, scan_sh);
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
+            const unsigned be_k = bk[e];
+            lst[hist[be_k >> 16] + (be_k & 0xffffu)] = (unsigned short)e;
+        }
+        __syncthreads();
+        for (int e = tid; e < q; e += kT) {
+            const unsigned be_k = bk[e];
+            const int bs = hist[be_k >> 16];
+            const int be = (int(be_k >> 16) + 1 < nb) ? hist[(be_k >> 16) + 1] : q;
+            int rank = 0;
+            if (be - bs > 1) {
+                const double te = t[e];
+                const int ie = id[e];
+                for (int k = bs; k < be; k++) {
+                    const int o = lst[k];
+                    rank += key_less(t[o], id[o], te, ie);
+                }
+            }
+            perm[bs + rank] = (unsigned short)e;
+        }
+        __syncthreads();
+    }
+}
+
 // IdT: int32 (the match scratch) or int64 (in place in the output arrays,
 // for the parts of split rays: every input is in shared memory before the
 // corresponding output is written).
@@ -448,85 +538,8 @@ __device__ void sort_segment(SortSmem<kCap>& F, int q, uint2 mm, const double* s
     }
     cp_wait<0>();
     __syncthreads();
-    if (q <= 64) {
-        for (int e = tid; e < q; e += kT) {
-            const double te = F.t[e];
-            const int ie = F.id[e];
-            int rank = 0;
-            for (int k = 0; k < q; k++) rank += key_less(F.t[k], F.id[k], te, ie);
-            F.perm[rank] = (unsigned short)e;
-        }
-        __syncthreads();
-    } else {
-        const int nb = q;  // fine buckets
-        // float bounds of the segment's t, from the streaming pass (any
-        // monotone bucket map gives the same order: exact in-bucket ranks)
-        // The map is computed in fp32 (each step is monotone under round to
-        // nearest: float(t), - tlo, * scale, fminf), once per element; the
-        // coarse coordinate is kept in bk[] for the fine pass.
-        const float tlo = from_fkey(mm.x), thi = from_fkey(mm.y);
-        const float span = thi - tlo;
-        // capped so that 0 * scale stays 0 when the span is tiny
-        const float cscale = span > 0.0f ? fminf(float(kCoarse) / span, FLT_MAX) : 0.0f;
-        for (int e = tid; e < q; e += kT) {
-            const float x = fminf((__double2float_rn(F.t[e]) - tlo) * cscale, float(kCoarse));
-            F.bk[e] = __float_as_uint(x);
-            const int b = min(int(x), kCoarse - 1);
-            const unsigned peers = __match_any_sync(__activemask(), b);
-            if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.chist[b], __popc(peers));
-        }
-        __syncthreads();
-        // coarse prefix counts -> first fine bucket of each coarse bin
-        if (tid < 32) {
-            int run = 0;
-            for (int c0 = 0; c0 < kCoarse; c0 += 32) {
-                const int v = F.chist[c0 + tid];
-                const int inc = warp_incl_scan(v);
-                F.chist[c0 + tid] = int((int64_t(run + inc - v) * nb) / q);
-                run += __shfl_sync(0xffffffffu, inc, 31);
-            }
-            if (tid == 0) F.chist[kCoarse] = nb;
-        }
-        __syncthreads();
-        for (int e = tid; e < q; e += kT) {
-            const float x = __uint_as_float(F.bk[e]);
-            const int b = min(int(x), kCoarse - 1);
-            const int f0 = F.chist[b], width = F.chist[b + 1] - f0;
-            int f = f0;
-            if (width > 1) {
-                // x - b is exact (Sterbenz) and in [0, 1]
-                const int off = int((x - float(b)) * float(width));
-                f += min(off, width - 1);
-            }
-            f = min(f, nb - 1);
-            const int li = atomicAdd(&F.hist[f], 1);
-            F.bk[e] = (unsigned(f) << 16) | unsigned(li);
-        }
-        __syncthreads();
-        block_scan_inplace<(kCap + kT - 1) / kT>(F.hist, nb, F.scan_sh);
-        __syncthreads();
-        for (int e = tid; e < q; e += kT) {
-            const unsigned bk = F.bk[e];
-            F.lst[F.hist[bk >> 16] + (bk & 0xffffu)] = (unsigned short)e;
-        }
-        __syncthreads();
-        for (int e = tid; e < q; e += kT) {
-            const unsigned bk = F.bk[e];
-            const int bs = F.hist[bk >> 16];
-            const int be = (int(bk >> 16) + 1 < nb) ? F.hist[(bk >> 16) + 1] : q;
-            int rank = 0;
-            if (be - bs > 1) {
-                const double te = F.t[e];
-                const int ie = F.id[e];
-                for (int k = bs; k < be; k++) {
-                    const int o = F.lst[k];
-                    rank += key_less(F.t[o], F.id[o], te, ie);
-                }
-            }
-            F.perm[bs + rank] = (unsigned short)e;
-        }
-        __syncthreads();
-    }
+    rank_segment<kCap, kT>(q, from_fkey(mm.x), from_fkey(mm.y), F.t, F.id, F.bk, F.hist, F.lst, F.perm, F.chist,
+                           F.scan_sh);
     // dist into the (now free) bucket arrays, in flight while t / id go out
     for (int e = tid; e < q; e += kT) cp_async8(&F.d[e], sd + e);
     cp_commit();
