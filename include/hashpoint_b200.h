@@ -135,6 +135,27 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
                    const double* t_near, const double* t_far, const double* slopes, int64_t m,
                    int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
                    void* workspace, size_t workspace_bytes, hp_stream_t stream);
+/* Prefix mode (callers that only want samples): instead of hp_query_fill,
+ * sort in place, at the front of each ray's match scratch, the ray's
+ * smallest-t matches -- all of them when it has <= want, else everything up
+ * to the histogram bin where the count reaches `want` (<= 2048) -- and
+ * record the sampler's facts over ALL its matches.  plen [m] receives each
+ * prefix length; the view gives the (device) arrays of the prefixes: ray r
+ * at start[r], t float64, ids int32, dist float64.  cut_t / cut_d [m]
+ * receive the smallest t and dist of the matches left out (+inf when none;
+ * every left-out t is strictly above the prefix's last t).
+ * hp_sample_run_prefix consumes them. */
+typedef struct hp_query_prefix_view {
+    const int64_t* start; /* [m] */
+    const double* t;
+    const int32_t* ids;
+    const double* dist;
+} hp_query_prefix_view;
+int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, const double* slopes,
+                    int32_t* facts, int32_t* plen, double* cut_t, double* cut_d, int64_t capacity,
+                    void* workspace, size_t workspace_bytes, hp_query_prefix_view* view,
+                    hp_stream_t stream);
+
 /* Upper bounds of the match counts (the slots pass 1 will test per ray),
  * exclusive-scanned into bound_off [m+1] (bound_off[m] = the scratch pass 1
  * needs).  Lets a caller split a frame into ray chunks that fit memory.
@@ -184,6 +205,33 @@ int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const 
                    double* r_t, double* r_dist, double* r_udf, double* r_alpha, double* r_w,
                    double* r_color, void* workspace, size_t workspace_bytes,
                    hp_stream_t stream);
+
+/* Prefix mode: the sampler over hp_query_prefix's sorted prefixes (offsets
+ * = the full match counts from hp_query_count, query_facts = the prefix
+ * call's facts).  Results are those of hp_sample_run on the full CSR for
+ * every ray not flagged; flagged [m+1] receives 1 for a ray whose work may
+ * reach past its prefix (its r_off count is 0, its t_end NaN: run it through
+ * the full path) and flagged[m] = the number of such rays. */
+typedef struct hp_sample_prefix {
+    const int64_t* start;  /* [m] */
+    const int32_t* length; /* [m] */
+    const int32_t* ids;
+    const double* t;
+    const double* dist;
+    const double* cut_t;   /* [m] */
+    const double* cut_d;   /* [m] */
+} hp_sample_prefix;
+int hp_sample_run_prefix(const int64_t* offsets, int64_t m, const hp_sample_prefix* prefix,
+                         int64_t exact_capacity, const double* slopes, const int32_t* query_facts,
+                         const hp_sampler_params* p, const double* colors, int64_t n_colors,
+                         int64_t* r_off, double* t_end, int32_t* flagged, void* workspace,
+                         size_t workspace_bytes, hp_stream_t stream);
+int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp_sample_prefix* prefix,
+                          int64_t exact_capacity, const double* slopes, const hp_sampler_params* p,
+                          const double* colors, int64_t n_colors, const int64_t* r_off, int64_t R,
+                          int64_t* r_id, double* r_t, double* r_dist, double* r_udf, double* r_alpha,
+                          double* r_w, double* r_color, void* workspace, size_t workspace_bytes,
+                          hp_stream_t stream);
 
 /* out2[0] = offsets[m] (total), out2[1] = max_r (offsets[r+1] - offsets[r]).
  * Device int64[2]. */

@@ -39,6 +39,15 @@ class SamplerParams(ctypes.Structure):
                 ("tau_min", c_f64)]
 
 
+class PrefixView(ctypes.Structure):
+    _fields_ = [("start", c_p), ("t", c_p), ("ids", c_p), ("dist", c_p)]
+
+
+class SamplePrefix(ctypes.Structure):
+    _fields_ = [("start", c_p), ("length", c_p), ("ids", c_p), ("t", c_p), ("dist", c_p),
+                ("cut_t", c_p), ("cut_d", c_p)]
+
+
 _SIGNATURES = {
     "hp_last_error": (ctypes.c_char_p, []),
     "hp_version": (ctypes.c_int, []),
@@ -55,6 +64,8 @@ _SIGNATURES = {
     "hp_query_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
                                       c_p, c_size, c_p]),
+    "hp_query_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.c_int32, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
+                                       c_size, ctypes.POINTER(PrefixView), c_p]),
     "hp_query_bounds": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                        c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_size, c_p]),
     "hp_query_fill": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
@@ -67,6 +78,12 @@ _SIGNATURES = {
     "hp_sample_emit": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
                                       ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
+    "hp_sample_run_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(SamplePrefix), c_i64, c_p, c_p,
+                                            ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_p, c_p, c_p,
+                                            c_size, c_p]),
+    "hp_sample_emit_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(SamplePrefix), c_i64, c_p,
+                                             ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_i64,
+                                             c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
     "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "hp_sample_debug_counters": (ctypes.c_int, [c_p, ctypes.c_int]),

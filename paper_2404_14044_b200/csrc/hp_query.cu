@@ -630,6 +630,176 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
     }
 }
 
+
+// ---------------------------------------------------------------- prefix sort
+// For callers that only want samples (pipeline.search_and_sample): each ray's
+// smallest-t matches -- everything through the 2048-bin histogram bin where
+// the count reaches `want` (at most kCap) -- sorted by (t, id) in place at the
+// front of the ray's match scratch (t, id, dist), plus the sampler's facts
+// over ALL the ray's matches, and two cuts for the matches left out: their
+// smallest t (every one is strictly above the prefix's last t) and their
+// smallest dist.  The sampler runs on these prefixes and flags a ray whose
+// work would reach past its prefix (hp_sample_run prefix mode).
+constexpr int kPrefixCap = 2048;
+constexpr int kPrefixThreads = 512;
+constexpr int kSelBins = 2048;
+
+struct PrefixSmem {
+    double t[kPrefixCap];
+    double d2[kPrefixCap];
+    int id[kPrefixCap];
+    unsigned bk[kPrefixCap];
+    int hist[kSelBins + 1];  // selection histogram, then the fine buckets
+    unsigned short lst[kPrefixCap], perm[kPrefixCap];
+    int chist[kCoarse + 1];
+    int scan_sh[33];
+    unsigned long long cut_t, cut_d2;  // order keys of the left-out minima
+    int cnt, bsel, fcount, fbad;
+};
+
+__device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving key
+    const unsigned long long b = __double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+    return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
+}
+
+__global__ void __launch_bounds__(kPrefixThreads) k_query_prefix(
+    const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm, int64_t m,
+    int want, const double* __restrict__ slopes, int* __restrict__ facts, int* __restrict__ plen,
+    double* __restrict__ cut_t, double* __restrict__ cut_d, double* st, int* sid, double* sd) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    PrefixSmem& F = *reinterpret_cast<PrefixSmem*>(dyn);
+    constexpr int kT = kPrefixThreads;
+    const int tid = threadIdx.x;
+    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+        const int64_t so = soff[r];
+        const int q = int(off[r + 1] - off[r]);
+        if (q == 0) {
+            if (tid == 0) {
+                plen[r] = 0;
+                facts[r] = -1;
+                cut_t[r] = cut_d[r] = CUDART_INF;
+            }
+            continue;
+        }
+        const float tlo = from_fkey(tmm[r].x), thi = from_fkey(tmm[r].y);
+        const float span = thi - tlo;
+        const float sel_scale = span > 0.0f ? fminf(float(kSelBins) / span, FLT_MAX) : 0.0f;
+        auto sel_bin = [&](double t) {
+            return min(int(fminf((__double2float_rn(t) - tlo) * sel_scale, float(kSelBins))), kSelBins - 1);
+        };
+        const bool all = q <= want;
+        int bsel = kSelBins - 1, L = q;
+        if (!all) {
+            for (int k = tid; k <= kSelBins; k += kT) F.hist[k] = 0;
+            if (tid == 0) F.bsel = kSelBins;
+            __syncthreads();
+            for (int e = tid; e < q; e += kT) {
+                const int b = sel_bin(st[so + e]);
+                const unsigned peers = __match_any_sync(__activemask(), b);
+                if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.hist[b], __popc(peers));
+            }
+            __syncthreads();
+            block_scan_inplace<(kSelBins + kT - 1) / kT>(F.hist, kSelBins, F.scan_sh);
+            if (tid == 0) F.hist[kSelBins] = q;
+            __syncthreads();
+            // first bin whose cumulative count reaches `want`, within kPrefixCap
+            for (int b = tid; b < kSelBins; b += kT)
+                if (F.hist[b + 1] >= want) atomicMin(&F.bsel, b);
+            __syncthreads();
+            bsel = F.bsel;
+            L = F.hist[bsel + 1];
+            if (L > kPrefixCap) {  // that bin alone overflows: stop before it
+                bsel -= 1;
+                L = bsel >= 0 ? F.hist[bsel + 1] : 0;
+            }
+        }
+        // stage the selected matches (the smallest L by t) in shared memory
+        if (tid == 0) F.cnt = 0;
+        for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
+        __syncthreads();
+        for (int k = tid; k <= L; k += kT) F.hist[k] = 0;
+        for (int e0 = 0; e0 < q; e0 += kT) {
+            const int e = e0 + tid;
+            bool in = false;
+            double t = 0.0;
+            if (e < q) {
+                t = st[so + e];
+                in = all || sel_bin(t) <= bsel;
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, in);
+            int base = 0;
+            if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) {
+                const int slot = base + __popc(b & ((1u << lane_id()) - 1));
+                F.t[slot] = t;
+                F.id[slot] = sid[so + e];
+                F.d2[slot] = sd[so + e];
+            }
+        }
+        __syncthreads();
+        if (L > 0) {  // bounds of the selected t (any bounds keep the map monotone)
+            const float hi = all ? thi : tlo + float(bsel + 1) / sel_scale;
+            rank_segment<kPrefixCap, kT>(L, tlo, hi, F.t, F.id, F.bk, F.hist, F.lst, F.perm, F.chist, F.scan_sh);
+        }
+        // facts over all q matches and the cuts of the left-out ones (before
+        // the prefix overwrites the scratch)
+        if (tid == 0) {
+            F.fcount = F.fbad = 0;
+            F.cut_t = F.cut_d2 = ~0ull;
+        }
+        __syncthreads();
+        const double slope = __ldcg(slopes + r);
+        const double r0 = L > 0 ? dmul(slope, F.t[F.perm[0]]) : 0.0;
+        int cnt = 0;
+        bool bad = false;
+        unsigned long long kt = ~0ull, kd = ~0ull;
+        for (int e = tid; e < q; e += kT) {
+            const double te = st[so + e], d2 = sd[so + e];
+            const double d = sqrt(d2);
+            bad |= !(fabs(te) <= DBL_MAX) || !(d >= 0.0) || !(d <= DBL_MAX);
+            cnt += d <= r0;
+            if (!all && sel_bin(te) > bsel) {
+                kt = min(kt, dkey(te));
+                kd = min(kd, dkey(d2));
+            }
+        }
+        cnt = warp_sum(cnt);
+        const bool anybad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            kt = min(kt, __shfl_xor_sync(0xffffffffu, kt, o));
+            kd = min(kd, __shfl_xor_sync(0xffffffffu, kd, o));
+        }
+        if (lane_id() == 0) {
+            if (anybad) atomicOr(&F.fbad, 1);
+            if (cnt) atomicAdd(&F.fcount, cnt);
+            if (kt != ~0ull) {
+                atomicMin(&F.cut_t, kt);
+                atomicMin(&F.cut_d2, kd);
+            }
+        }
+        __syncthreads();
+        for (int p = tid; p < L; p += kT) {  // the sorted prefix, in place
+            const int e = F.perm[p];
+            st[so + p] = F.t[e];
+            sid[so + p] = F.id[e];
+            sd[so + p] = sqrt(F.d2[e]);
+        }
+        if (tid == 0) {
+            plen[r] = L;
+            facts[r] = (F.fbad || L == 0) ? -1 : F.fcount;
+            const bool rest = F.cut_t != ~0ull;
+            cut_t[r] = rest ? dkey_inv(F.cut_t) : CUDART_INF;
+            cut_d[r] = rest ? sqrt(dkey_inv(F.cut_d2)) : CUDART_INF;
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- huge rays
 // Rays with more than kSortHuge matches: one CTA per ray splits the ray's
 // matches into t-ordered parts of <= kSortHuge (a 2048-bin linear histogram
@@ -1044,5 +1214,39 @@ extern "C" int hp_query_bounds(hp_query_layout layout, const hp_camera* cam, int
         HP_CHECK_LAUNCH("k_query_bound");
     }
     HP_TRY(exclusive_scan_i64(bound_off, bound_off, m, workspace, s));
+    return HP_OK;
+}
+
+extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, const double* slopes,
+                               int32_t* facts, int32_t* plen, double* cut_t, double* cut_d, int64_t capacity,
+                               void* workspace, size_t workspace_bytes, hp_query_prefix_view* view,
+                               hp_stream_t stream) {
+    if (m < 0 || want < 1 || want > kPrefixCap || !slopes || !facts || !plen || !cut_t || !cut_d) {
+        set_error("hp_query_prefix: invalid arguments (1 <= want <= %d)", kPrefixCap);
+        return HP_EINVAL;
+    }
+    Carver cv(workspace, workspace_bytes);
+    QueryWs w = carve_query(cv, m, capacity);
+    if (!cv.ok()) {
+        set_error("hp_query_prefix: workspace too small");
+        return HP_ESPACE;
+    }
+    if (view) {
+        view->start = w.soff;
+        view->t = w.st;
+        view->ids = w.sid;
+        view->dist = w.sd;
+    }
+    if (m == 0) return HP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static const int occ = [] {  // once (thread-safe)
+        set_smem(k_query_prefix, sizeof(PrefixSmem));
+        return resident(k_query_prefix, kPrefixThreads, sizeof(PrefixSmem));
+    }();
+    TimedSpan ts("k_query_prefix", s);
+    k_query_prefix<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
+                                                                             facts, plen, cut_t, cut_d, w.st, w.sid,
+                                                                             w.sd);
+    HP_CHECK_LAUNCH("k_query_prefix");
     return HP_OK;
 }

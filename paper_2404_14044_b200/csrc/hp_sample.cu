@@ -75,6 +75,19 @@ struct Csr {
     const double* colors;
     int64_t m;
     const int32_t* facts;  // optional per-ray facts from hp_query_fill (NULL: compute)
+    // prefix mode (hp_query_prefix; start == NULL: CSR mode).  Ray r's
+    // candidates are the first len[r] of its off[r+1] - off[r] matches, at
+    // start[r]; the rest all have t >= cut_t[r] and dist >= cut_d[r].
+    const int64_t* start;
+    const int32_t* len;
+    const int32_t* ids32;
+    const double* cut_t;
+    const double* cut_d;
+    int32_t* flag;  // [m + 1]: 1 = the ray needs its full CSR; flag[m] = count
+    __device__ __forceinline__ int64_t lo(int64_t r) const { return start ? start[r] : off[r]; }
+    __device__ __forceinline__ int n(int64_t r) const { return start ? len[r] : int(off[r + 1] - off[r]); }
+    __device__ __forceinline__ int qtrue(int64_t r) const { return int(off[r + 1] - off[r]); }
+    __device__ __forceinline__ int64_t id(int64_t k) const { return ids32 ? int64_t(ids32[k]) : ids[k]; }
 };
 
 struct Outputs {
@@ -95,8 +108,22 @@ struct RayOut {  // per-ray results of pass 1
 __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __restrict__ plan,
                          int64_t* __restrict__ ecnt, double* __restrict__ rt, double* __restrict__ rd) {
     const int lane = lane_id();
-    const int64_t lo = C.off[ray];
-    const int q = int(C.off[ray + 1] - lo);
+    const int64_t lo = C.lo(ray);
+    const int q = C.n(ray);  // candidates present (prefix mode: the prefix)
+    const int qt = C.start ? C.qtrue(ray) : q;
+    const bool partial = q < qt;
+    const int fact = C.facts ? C.facts[ray] : -1;
+    // prefix mode: a ray whose work may reach past its prefix is flagged for
+    // the full path (no facts, or a prefix shorter than K)
+    auto flag_out = [&]() {
+        if (lane == 0) {
+            plan[ray] = make_int4(0, 0, 0, 0);
+            ecnt[ray] = 0;
+            C.flag[ray] = 1;
+        }
+    };
+    if (partial && (fact < 0 || q < P.K)) return flag_out();
+    if (C.start && lane == 0) C.flag[ray] = 0;
     if (q == 0) {
         if (lane == 0) {
             plan[ray] = make_int4(0, 0, 0, 0);
@@ -114,7 +141,6 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     // from j = 0 when it reaches K, the common case on dense surfaces)
     bool ok = slope >= 0.0 && slope <= DBL_MAX;
     int c0cnt = 0;
-    const int fact = C.facts ? C.facts[ray] : -1;
     if (fact >= 0) {  // the query's sort established the preconditions
         c0cnt = lane == 0 ? fact : 0;
     } else {
@@ -128,11 +154,12 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
         }
     }
     const bool fast = __all_sync(0xffffffffu, ok);
+    if (partial && !fast) return flag_out();
     int jstar = 0;
     if (fast) {
         if (warp_sum(c0cnt) >= P.K) {
             jstar = 0;
-        } else if (q < P.K) {
+        } else if (qt < P.K) {
             jstar = q;
         } else {
             // first j with #{ds_i <= slope * t_j} >= K (monotone in j)
@@ -142,6 +169,9 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
                 for (int i = 0; i < q; i++) c += (V.d(i) <= rj);
                 return c >= P.K;
             });
+            // prefix counts are the full counts while r_j < cut_d (the
+            // left-out matches are all farther out); beyond, unknown
+            if (partial && jstar > 0 && !(dmul(slope, V.t(jstar - 1)) < __ldg(C.cut_d + ray))) return flag_out();
         }
     }
     // ---- 1. bound chain (fast path): chain_chunk over 32 candidates at a time
@@ -180,6 +210,9 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
         je = S.je;
         proved_zero = S.proved_zero;
     }
+    // prefix mode: retention (and, exact t_end, the zero) must be decided
+    // inside the prefix
+    if (partial && (je == q || (P.exact_t_end && !proved_zero))) return flag_out();
     if (lane == 0) {
         plan[ray] = make_int4(jstar, je, (fast ? 1 : 0) | (proved_zero ? 2 : 0), q);
         // exact region [0, E): everything unless retention is decided before je
@@ -237,11 +270,20 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
         const int ray = X.ray[c];
         const int j = int(c - eoff[ray]);
         const int4 pl = plan[ray];
-        const int64_t lo = C.off[ray];
+        const int64_t lo = C.lo(ray);
         const int q = pl.w;
         const RayView V{C.t + lo, C.ds + lo};
         double u, a, col[3] = {0.0, 0.0, 0.0};
-        eval_exact<BestT>(V, q, j, pl.z & 1, pl.x, C.slopes[ray], P, C.ids + lo, C.colors, u, a, col, evals);
+        bool ok = true;
+        if (C.start) {
+            const int qt = C.qtrue(ray);
+            ok = eval_exact<BestT>(V, q, qt, q < qt ? __ldg(C.cut_t + ray) : CUDART_INF, j, pl.z & 1, pl.x,
+                                   C.slopes[ray], P, C.ids32 + lo, C.colors, u, a, col, evals);
+        } else {
+            eval_exact<BestT>(V, q, q, CUDART_INF, j, pl.z & 1, pl.x, C.slopes[ray], P, C.ids + lo, C.colors, u, a,
+                              col, evals);
+        }
+        if (!ok) C.flag[ray] = 1;
         X.udf[c] = u;
         X.alpha[c] = a;
         if (P.want_color) {
@@ -266,6 +308,14 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
     const int lane = lane_id();
     const int4 pl = plan[ray];
     const int q = pl.w;
+    if (C.start && C.flag[ray]) {  // left to the full path
+        if (lane == 0) {
+            RO.rcount[ray] = 0;
+            RO.t_end[ray] = CUDART_NAN;
+            atomicAdd(C.flag + C.m, 1);
+        }
+        return;
+    }
     if (q == 0) {
         if (lane == 0) {
             RO.rcount[ray] = 0;
@@ -352,10 +402,10 @@ __global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const
     for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); r < C.m; r += warps) {
         const int64_t o = r_off[r], n = r_off[r + 1] - o;
         if (n == 0) continue;
-        const int64_t lo = C.off[r], st = eoff[r];
+        const int64_t lo = C.lo(r), st = eoff[r];
         for (int64_t k = lane_id(); k < n; k += 32) {
             const int64_t j = lo + X.ray[st + k];
-            O.r_id[o + k] = C.ids[j];
+            O.r_id[o + k] = C.id(j);
             O.r_t[o + k] = C.t[j];
             O.r_dist[o + k] = C.ds[j];
             O.r_udf[o + k] = X.udf[st + k];
@@ -523,6 +573,72 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
         k_mark_exact_overflow<<<1, 1, 0, s>>>(w.eoff + m, exact_capacity, r_off + m);
         HP_CHECK_LAUNCH("k_mark_exact_overflow");
     }
+    return HP_OK;
+}
+
+// Prefix mode (hp_query_prefix): the same passes over each ray's sorted
+// prefix; rays whose work may reach past it are flagged instead.
+extern "C" int hp_sample_run_prefix(const int64_t* offsets, int64_t m, const hp_sample_prefix* pre,
+                                    int64_t exact_capacity, const double* slopes, const int32_t* query_facts,
+                                    const hp_sampler_params* p, const double* colors, int64_t n_colors,
+                                    int64_t* r_off, double* t_end, int32_t* flagged, void* workspace,
+                                    size_t workspace_bytes, hp_stream_t stream) {
+    HP_TRY(validate(p, colors, n_colors));
+    if (!pre || !pre->start || !pre->length || !pre->ids || !pre->t || !pre->dist || !pre->cut_t || !pre->cut_d ||
+        !query_facts || !flagged) {
+        set_error("hp_sample_run_prefix: the prefix arrays, facts and flagged are required");
+        return HP_EINVAL;
+    }
+    Carver c(workspace, workspace_bytes);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
+    if (!c.ok()) {
+        set_error("hp_sample_run_prefix: workspace too small");
+        return HP_ESPACE;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(flagged + m, 0, sizeof(int32_t), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_sample_run_prefix memset");
+    Csr C{offsets, nullptr, pre->t, pre->dist, slopes, colors, m, query_facts,
+          pre->start, pre->length, pre->ids, pre->cut_t, pre->cut_d, flagged};
+    Params P = to_params(p);
+    if (m > 0) {
+        HP_TRY(dispatch_exact(C, P, w, s));
+        HP_TRY(launch_retain(C, P, RayOut{r_off, t_end}, w, s));
+    }
+    HP_TRY(exclusive_scan_i64(r_off, r_off, m, w.scan, s));
+    if (m > 0) {
+        k_mark_exact_overflow<<<1, 1, 0, s>>>(w.eoff + m, exact_capacity, r_off + m);
+        HP_CHECK_LAUNCH("k_mark_exact_overflow");
+    }
+    return HP_OK;
+}
+
+extern "C" int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp_sample_prefix* pre,
+                                     int64_t exact_capacity, const double* slopes, const hp_sampler_params* p,
+                                     const double* colors, int64_t n_colors, const int64_t* r_off, int64_t R,
+                                     int64_t* r_id, double* r_t, double* r_dist, double* r_udf, double* r_alpha,
+                                     double* r_w, double* r_color, void* workspace, size_t workspace_bytes,
+                                     hp_stream_t stream) {
+    HP_TRY(validate(p, colors, n_colors));
+    if (!pre) {
+        set_error("hp_sample_emit_prefix: prefix is NULL");
+        return HP_EINVAL;
+    }
+    if (R == 0 || m == 0) return HP_OK;
+    Carver c(workspace, workspace_bytes);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
+    if (!c.ok()) {
+        set_error("hp_sample_emit_prefix: workspace too small");
+        return HP_ESPACE;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Csr C{offsets, nullptr, pre->t, pre->dist, slopes, colors, m, nullptr,
+          pre->start, pre->length, pre->ids, pre->cut_t, pre->cut_d, nullptr};
+    Params P = to_params(p);
+    Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
+    TimedSpan ts("k_emit", s);
+    k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    HP_CHECK_LAUNCH("k_emit");
     return HP_OK;
 }
 

@@ -142,18 +142,22 @@ struct RayView {
 };
 
 // Exact udf/alpha (and colour) of candidate j (reference _kernels.py:594-660).
-template <class BestT, class View>
-__device__ void eval_exact(const View& V, int q, int j, bool fast,
-                           int jstar, double slope, const Params& P, const int64_t* __restrict__ ids_ray,
+// q candidates are present of the ray's qt (prefix mode: q < qt, the others
+// all at t >= tcut, fast path only).  Returns false when the K nearest may
+// lie past the prefix (the ray then takes the full path).
+template <class BestT, class View, class IdT>
+__device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, bool fast,
+                           int jstar, double slope, const Params& P, const IdT* __restrict__ ids_ray,
                            const double* __restrict__ colors, double& udf, double& alpha, double* col3,
                            unsigned long long& evals) {
     const double tj = V.t(j);
     const double rj = dmul(slope, tj);
+    const bool partial = q < qt;
     bool use_el;
     int ksel;
     if (fast) {
         use_el = j >= jstar;
-        ksel = use_el ? P.K : (q < P.K ? q : P.K);
+        ksel = use_el ? P.K : (qt < P.K ? qt : P.K);
     } else {
         int n_el = 0;
         for (int i = 0; i < q; i++) n_el += (V.d(i) <= rj);
@@ -170,14 +174,17 @@ __device__ void eval_exact(const View& V, int q, int j, bool fast,
     if (fast) {
         // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
         // (t, ds) of the next candidate on each side are loaded one step ahead
+        // prefix mode: past the prefix, the cut stands in for the next
+        // candidate on the right (a lower bound of its t)
         int l = j, r = j + 1;
-        double tl = tj, dl = V.d(j), tr = 0.0, dr = 0.0;
+        const int rend = partial ? q + 1 : q;
+        double tl = tj, dl = V.d(j), tr = tcut, dr = 0.0;
         if (r < q) {
             tr = V.t(r);
             dr = V.d(r);
         }
-        while (l >= 0 || r < q) {
-            const bool go_left = l >= 0 && (r >= q || dsub(tj, tl) <= dsub(tr, tj));
+        while (l >= 0 || r < rend) {
+            const bool go_left = l >= 0 && (r >= rend || dsub(tj, tl) <= dsub(tr, tj));
             int i;
             double ti, di;
             if (go_left) {
@@ -189,12 +196,19 @@ __device__ void eval_exact(const View& V, int q, int j, bool fast,
                     dl = V.d(l);
                 }
             } else {
+                if (r == q) {  // the cut: every left-out match is at least this far
+                    const double dc = dsub(tcut, tj);
+                    if (dmul(dc, dc) > kd) break;
+                    return false;
+                }
                 i = r;
                 ti = tr;
                 di = dr;
                 if (++r < q) {
                     tr = V.t(r);
                     dr = V.d(r);
+                } else {
+                    tr = tcut;
                 }
             }
             const double dt = dsub(ti, tj);
@@ -264,6 +278,7 @@ __device__ void eval_exact(const View& V, int q, int j, bool fast,
         col3[1] = c1;
         col3[2] = c2;
     }
+    return true;
 }
 
 // Upper bound of the reference's factor fl(1 - alpha_j) (DESIGN.md "sampler:

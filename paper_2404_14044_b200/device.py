@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import c_i64, c_size
 
-__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "sample",
+__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "query_prefix", "sample", "sample_prefix", "merge_flagged",
            "primary_surface", "MatchBudgetExceeded", "SAMPLE_EXACT_PER_RAY"]
 
 # match-scratch capacity of the last query per device (slots), reused so a
@@ -190,22 +190,12 @@ def query_bounds(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
     return out
 
 
-def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
-          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True, facts: bool = False,
-          max_scratch: int | None = None):
-    """_kernels.hash_query_batch on the device (reference _kernels.py:86-157).
-
-    Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors
-    (+ the per-ray sampler facts, int32 [m], with ``facts=True``; pass them to
-    :func:`sample` together with this CSR and these slopes).  With
-    ``max_scratch`` a frame needing more match slots raises
-    :class:`MatchBudgetExceeded` before any CSR is written.
-    """
+def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
+    """hp_query_count with the workspace sized (retrying once); returns
+    (offsets, probes, scanned, total, workspace, workspace bytes, capacity)."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
     m = int(pixels.shape[0])
-    pixels = pixels.contiguous()
-    dirs = dirs.contiguous()
     nb = c_size(0)
     offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
     probes = torch.empty(m, dtype=torch.int64, device=dev)
@@ -236,6 +226,26 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
         if max_scratch is not None:
             cap = min(cap, int(max_scratch))
         _QUERY_CAP[dev] = cap
+    return offsets, probes, scanned, total, ws, nb.value, cap
+
+
+def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
+          t_far: torch.Tensor, slopes: torch.Tensor, footprint: bool = True, facts: bool = False,
+          max_scratch: int | None = None):
+    """_kernels.hash_query_batch on the device (reference _kernels.py:86-157).
+
+    Returns (offsets, ids, t_proj, dist_perp, probes, scanned) as CUDA tensors
+    (+ the per-ray sampler facts, int32 [m], with ``facts=True``; pass them to
+    :func:`sample` together with this CSR and these slopes).  With
+    ``max_scratch`` a frame needing more match slots raises
+    :class:`MatchBudgetExceeded` before any CSR is written.
+    """
+    lib = _lib.load(require_device=True)
+    dev = index.table_start.device
+    m = int(pixels.shape[0])
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    offsets, probes, scanned, total, ws, nb, cap = _count(index, pixels, dirs, t_near, t_far, slopes,
+                                                          footprint, max_scratch)
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
@@ -243,12 +253,68 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     fa = torch.empty(m, dtype=torch.int32, device=dev) if facts else None
     _lib.check(lib.hp_query_fill(_ptr(offsets), m, total, _ptr(ids), _ptr(t), _ptr(d),
                                  _ptr(slopes) if facts else ctypes.c_void_p(0),
-                                 _ptr(fa) if facts else ctypes.c_void_p(0), cap, _ptr(ws), nb.value,
-                                 _stream()))
+                                 _ptr(fa) if facts else ctypes.c_void_p(0), cap, _ptr(ws), nb, _stream()))
     _mark("query.fill")
     if facts:
         return offsets, ids, t, d, probes, scanned, fa
     return offsets, ids, t, d, probes, scanned
+
+
+class QueryPrefix:
+    """Result of :func:`query_prefix`: the full match counts (``offsets``)
+    and, per ray, the (t, id)-sorted head of its matches inside the query
+    workspace (``start``, ``length``; ``t``, ``ids`` int32, ``dist``), the
+    smallest t / dist of the matches left out (``cut_t``, ``cut_d``), and
+    the sampler's facts over all matches.  Keeps the workspace alive."""
+
+    def __init__(self, offsets, probes, scanned, start, length, t, ids, dist, cut_t, cut_d, facts, ws):
+        self.offsets, self.probes, self.scanned = offsets, probes, scanned
+        self.start, self.length, self.t, self.ids, self.dist = start, length, t, ids, dist
+        self.cut_t, self.cut_d, self.facts = cut_t, cut_d, facts
+        self._ws = ws
+
+    def struct(self) -> _lib.SamplePrefix:
+        sp = _lib.SamplePrefix()
+        sp.start, sp.length, sp.ids = self.start.data_ptr(), self.length.data_ptr(), self.ids.data_ptr()
+        sp.t, sp.dist = self.t.data_ptr(), self.dist.data_ptr()
+        sp.cut_t, sp.cut_d = self.cut_t.data_ptr(), self.cut_d.data_ptr()
+        return sp
+
+
+PREFIX_WANT = 512
+
+
+def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
+                 t_far: torch.Tensor, slopes: torch.Tensor, want: int = PREFIX_WANT, footprint: bool = True,
+                 max_scratch: int | None = None) -> QueryPrefix:
+    """The query for callers that only want samples (hp_query_prefix): each
+    ray's smallest-t matches sorted in place, no CSR of all matches."""
+    lib = _lib.load(require_device=True)
+    dev = index.table_start.device
+    m = int(pixels.shape[0])
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    offsets, probes, scanned, total, ws, nb, cap = _count(index, pixels, dirs, t_near, t_far, slopes,
+                                                          footprint, max_scratch)
+    fa = torch.empty(m, dtype=torch.int32, device=dev)
+    plen = torch.empty(m, dtype=torch.int32, device=dev)
+    cut = torch.empty((2, m), dtype=torch.float64, device=dev)
+    view = _lib.PrefixView()
+    _lib.check(lib.hp_query_prefix(_ptr(offsets), m, int(want), _ptr(slopes), _ptr(fa), _ptr(plen),
+                                   _ptr(cut[0]), _ptr(cut[1]), cap, _ptr(ws), nb, ctypes.byref(view),
+                                   _stream()))
+    _mark("query.prefix")
+
+    def wrap(ptr, dtype, n):  # device view into the workspace (kept alive by QueryPrefix)
+        if n == 0 or not ptr:
+            return torch.empty(0, dtype=dtype, device=dev)
+        off = ptr - ws.data_ptr()
+        return ws[off:off + n * torch.empty(0, dtype=dtype).element_size()].view(dtype)
+
+    pre = QueryPrefix(offsets, probes, scanned, wrap(view.start, torch.int64, m), plen,
+                      wrap(view.t, torch.float64, cap), wrap(view.ids, torch.int32, cap),
+                      wrap(view.dist, torch.float64, cap), cut[0], cut[1], fa, ws)
+    pre.total = total
+    return pre
 
 
 def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerParams:
@@ -313,6 +379,97 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
                                   nb.value, _stream()))
     _mark("sample.emit")
     return (r_off, r_id, *outs, r_color, t_end)
+
+
+def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Tensor | None = None,
+                  exact_t_end: bool = False):
+    """:func:`sample` over :func:`query_prefix`'s prefixes
+    (hp_sample_run_prefix / hp_sample_emit_prefix).
+
+    Returns (r_off, r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color, t_end,
+    flagged, n_flagged): for every ray with ``flagged[r] == 0`` the results
+    are :func:`sample`'s on the full CSR; a flagged ray (its work may reach
+    past its prefix) has no retained candidates and t_end NaN here and must
+    be run through the full path (:func:`sample_rays_prefix` does that).
+    """
+    lib = _lib.load(require_device=True)
+    dev = pre.offsets.device
+    m = int(pre.offsets.shape[0]) - 1
+    want = colors is not None
+    p = sampler_params(cfg, want, exact_t_end)
+    exact_cap = max(SAMPLE_EXACT_PER_RAY * m, 1 << 16)
+    r_off = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    t_end = torch.empty(max(m, 0), dtype=torch.float64, device=dev)
+    flagged = torch.empty(m + 1, dtype=torch.int32, device=dev)
+    col = colors.contiguous() if want else None
+    ncol = int(col.shape[0]) if want else 0
+    sp = pre.struct()
+    colp = _ptr(col) if want else ctypes.c_void_p(0)
+    for _ in range(2):
+        nb = c_size(0)
+        _lib.check(lib.hp_sample_workspace_bytes(m, 0, exact_cap, ctypes.byref(p), ctypes.byref(nb)))
+        ws = _workspace(nb.value, dev)
+        _lib.check(lib.hp_sample_run_prefix(_ptr(pre.offsets), m, ctypes.byref(sp), exact_cap, _ptr(slopes),
+                                            _ptr(pre.facts), ctypes.byref(p), colp, ncol, _ptr(r_off),
+                                            _ptr(t_end), _ptr(flagged), _ptr(ws), nb.value, _stream()))
+        _mark("sample.run")
+        R = int(r_off[m].item())
+        if R >= 0:
+            break
+        exact_cap = int(-R * 1.0625) + 1024   # exact scratch too small: grow it once
+    n_flagged = int(flagged[m].item())
+    i64 = dict(dtype=torch.int64, device=dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    r_id = torch.empty(R, **i64)
+    outs = [torch.empty(R, **f64) for _ in range(5)]
+    r_color = torch.empty((R, 3), **f64) if want else torch.zeros((0, 3), **f64)
+    _lib.check(lib.hp_sample_emit_prefix(_ptr(pre.offsets), m, ctypes.byref(sp), exact_cap, _ptr(slopes),
+                                         ctypes.byref(p), colp, ncol, _ptr(r_off), R, _ptr(r_id),
+                                         *[_ptr(o) for o in outs], _ptr(r_color) if want else ctypes.c_void_p(0),
+                                         _ptr(ws), nb.value, _stream()))
+    _mark("sample.emit")
+    return (r_off, r_id, *outs, r_color, t_end, flagged[:m], n_flagged)
+
+
+def merge_flagged(main, flagged: torch.Tensor, sub):
+    """Splice the full-path samples ``sub`` of the flagged rays into the
+    prefix-mode samples ``main`` (both (r_off, r_id, r_t, r_dist, r_udf,
+    r_alpha, r_w, r_color, t_end)); flagged rays hold no candidates in main."""
+    r_off, *rows, r_color, t_end = main
+    s_off, *s_rows, s_color, s_tend = sub
+    dev = r_off.device
+    m = int(r_off.shape[0]) - 1
+    sel = torch.nonzero(flagged, as_tuple=True)[0]
+    counts = r_off[1:] - r_off[:-1]
+    counts[sel] = s_off[1:] - s_off[:-1]
+    off = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=off[1:])
+    R = int(off[m].item())
+
+    def dst(src_off, rays):  # destination row of every source row
+        n = src_off[1:] - src_off[:-1]
+        k = int(src_off[-1].item()) if src_off.numel() > 1 else 0
+        ray = torch.repeat_interleave(rays, n, output_size=k)
+        pos = torch.arange(k, device=dev) - torch.repeat_interleave(src_off[:-1], n, output_size=k)
+        return off[ray] + pos
+
+    d_main = dst(r_off, torch.arange(m, device=dev))
+    d_sub = dst(s_off, sel)
+    out = []
+    colored = r_color.shape[0] == rows[0].shape[0] and s_color.shape[0] == s_rows[0].shape[0]
+    for a, b in zip(rows + [r_color], s_rows + [s_color]):
+        if a.dim() == 2 and not colored:
+            out.append(torch.zeros((0, 3), dtype=a.dtype, device=dev))
+            continue
+        o = torch.empty((R,) + tuple(a.shape[1:]), dtype=a.dtype, device=dev)
+        if a.shape[0]:
+            o[d_main] = a
+        if b.shape[0]:
+            o[d_sub] = b
+        out.append(o)
+    te = t_end.clone()
+    te[sel] = s_tend
+    return (off, *out[:-1], out[-1], te)
 
 
 def primary_surface(r_off: torch.Tensor, r_id: torch.Tensor, r_t: torch.Tensor):

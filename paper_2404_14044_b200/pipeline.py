@@ -11,6 +11,7 @@ numpy out) used for the end-to-end number.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -68,6 +69,7 @@ class FrameResult:
     samples: tuple
     Q: int = 0
     chunks: int = 1
+    flagged: int = 0         # prefix mode: rays re-run through the full query
 
     @property
     def R(self) -> int:
@@ -133,9 +135,35 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
                          exact_t_end, max_matches, mark)
 
 
+# Frames that only want samples sort each ray's head of matches only
+# (device.query_prefix + device.sample_prefix); rays whose sampling may reach
+# past the head re-run through the full query.  HP_PREFIX=0 turns it off.
+PREFIX = os.environ.get("HP_PREFIX", "1") != "0"
+
+
 def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
-                  mark=lambda name: None, before_sample=lambda: None) -> FrameResult:
+                  mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None) -> FrameResult:
     budget = int(max_matches) if max_matches is not None else match_budget()
+    if PREFIX if prefix is None else prefix:
+        try:
+            pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes, max_scratch=budget)
+        except device.MatchBudgetExceeded:
+            before_sample()
+            return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
+                                  exact_t_end, budget, mark)
+        mark("query")
+        before_sample()
+        *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
+        Q = pre.total
+        del pre
+        if n_flagged:
+            sel = torch.nonzero(flagged, as_tuple=True)[0]
+            q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
+            sub = device.sample(q[0], q[1], q[2], q[3], slopes[sel], sampler_cfg, colors, exact_t_end,
+                                facts=q[6])
+            s = device.merge_flagged(tuple(s), flagged, sub)
+        mark("sample")
+        return FrameResult(idx, None, tuple(s), Q=Q, flagged=n_flagged)
     try:
         q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
     except device.MatchBudgetExceeded:

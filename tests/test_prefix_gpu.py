@@ -1,0 +1,167 @@
+"""hp_query_prefix: each ray's sorted prefix is exactly the first ``plen``
+entries of the full (t, id)-sorted CSR (bit for bit), it is closed under t
+(the next match has a strictly larger t), it holds at least ``min(q, want)``
+matches unless one selection bin alone overflows the prefix capacity, and the
+sampler facts equal the full query's.
+
+Reference behaviour being preserved: _kernels.hash_query_batch
+(_kernels.py:86-157) sorts every ray's matches by (t, id); a prefix of that
+order is what _kernels.sample_batch (_kernels.py:552-700) walks first.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_util as gu
+import paper_2404_14044_b200 as hp
+from paper_2404_14044_b200 import device as dv
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_prefix(q, p, want):
+    off = q[0].cpu().numpy()
+    ids, t, d = (x.cpu().numpy() for x in q[1:4])
+    fa = q[6].cpu().numpy()
+    np.testing.assert_array_equal(p.offsets.cpu().numpy(), off)
+    np.testing.assert_array_equal(p.facts.cpu().numpy(), fa)
+    start = p.start.cpu().numpy()
+    plen = p.length.cpu().numpy()
+    pt, pid, pd = p.t.cpu().numpy(), p.ids.cpu().numpy(), p.dist.cpu().numpy()
+    counts = np.diff(off)
+    assert np.all(plen <= counts)
+    short = plen < np.minimum(counts, want)
+    for r in np.flatnonzero(counts):
+        a, n, s = off[r], plen[r], start[r]
+        np.testing.assert_array_equal(pt[s:s + n], t[a:a + n])
+        np.testing.assert_array_equal(pid[s:s + n].astype(np.int64), ids[a:a + n])
+        np.testing.assert_array_equal(pd[s:s + n], d[a:a + n])
+        if n < counts[r] and n > 0:
+            assert t[a + n] > t[a + n - 1]
+        if short[r]:  # only when a single selection bin holds more than the cap
+            assert n < want
+    return plen, counts
+
+
+@pytest.mark.parametrize("name", gu.case_names())
+@pytest.mark.parametrize("want", [1, 7, 64, 512])
+def test_prefix_is_the_sorted_csr_head(name, want):
+    _, cloud, cam, cfg, tn, tf, stride, _ = gu.get_case(name)
+    dev = torch.device("cuda")
+    idx = dv.build(torch.from_numpy(cloud.positions).to(dev), cam, cfg.pad)
+    pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    rays = (up(pixels), up(dirs), up(t_near), up(t_far), up(slopes))
+    q = dv.query(idx, *rays, facts=True)
+    p = dv.query_prefix(idx, *rays, want=want)
+    _check_prefix(q, p, want)
+
+
+def test_prefix_on_dense_rays():
+    """q up to thousands per ray: the prefix is selected by histogram, not
+    the whole segment."""
+    cloud = hp.generate_scene(hp.SceneSpec("parallel_planes", n=60_000, seed=3, plane_count=3,
+                                           plane_gap=0.05, extent=0.8, noise=0.01))
+    cam = hp.scene_camera(48, 40, fov_deg=14)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.04), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    dirs, pixels = dirs[::11], pixels[::11]
+    tn, tf = np.full(len(dirs), 1.0), np.full(len(dirs), 10.0)
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    idx = dv.build(up(cloud.positions), cam, cfg.pad)
+    rays = (up(pixels), up(dirs), up(tn), up(tf), up(slopes))
+    q = dv.query(idx, *rays, facts=True)
+    for want in (16, 300, 1024):
+        p = dv.query_prefix(idx, *rays, want=want)
+        plen, counts = _check_prefix(q, p, want)
+        assert (counts > want).sum() > 10
+        assert np.all(plen[counts > want] >= want)
+
+
+def _prefix_frame(idx, rays, sc, colors, exact_t_end, want):
+    """prefix-mode sampling with the flagged rays re-run on the full path"""
+    pre = dv.query_prefix(idx, *rays, want=want)
+    *s, flagged, n_flagged = dv.sample_prefix(pre, rays[4], sc, colors, exact_t_end)
+    fl = flagged.cpu().numpy()
+    assert int(fl.sum()) == n_flagged
+    cnt = np.diff(s[0].cpu().numpy())
+    assert np.all(cnt[fl == 1] == 0)
+    if n_flagged:
+        sel = torch.nonzero(flagged, as_tuple=True)[0]
+        q = dv.query(idx, *[r[sel] for r in rays], facts=True)
+        sub = dv.sample(q[0], q[1], q[2], q[3], rays[4][sel], sc, colors, exact_t_end, facts=q[6])
+        s = dv.merge_flagged(tuple(s), flagged, sub)
+    return s, n_flagged
+
+
+def _assert_same(a, b):
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x.cpu().numpy(), y.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", gu.case_names())
+@pytest.mark.parametrize("exact_t_end", [True, False])
+@pytest.mark.parametrize("want", [1, 9, 512])
+def test_prefix_sampling_equals_full(name, exact_t_end, want):
+    _, cloud, cam, cfg, tn, tf, stride, samplers = gu.get_case(name)
+    dev = torch.device("cuda")
+    idx = dv.build(torch.from_numpy(cloud.positions).to(dev), cam, cfg.pad)
+    pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    rays = (up(pixels), up(dirs), up(t_near), up(t_far), up(slopes))
+    q = dv.query(idx, *rays, facts=True)
+    colors = torch.from_numpy(cloud.colors).cuda()
+    for sname in samplers:
+        sc = gu.sampler_config(sname)
+        for col in ((colors, None) if sname == "default" else (colors,)):
+            full = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, col, exact_t_end=exact_t_end, facts=q[6])
+            got, _ = _prefix_frame(idx, rays, sc, col, exact_t_end, want)
+            _assert_same(got, full)
+
+
+@pytest.mark.parametrize("k,mode,gamma", [(8, "epsilon", 0.9), (40, "epsilon", 0.5), (3, "tau", 0.3)])
+@pytest.mark.parametrize("exact_t_end", [True, False])
+def test_prefix_sampling_on_dense_rays(k, mode, gamma, exact_t_end):
+    cloud = hp.generate_scene(hp.SceneSpec("parallel_planes", n=60_000, seed=3, plane_count=3,
+                                           plane_gap=0.05, extent=0.8, noise=0.01))
+    cam = hp.scene_camera(48, 40, fov_deg=14)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.04), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    dirs, pixels = dirs[::5], pixels[::5]
+    tn, tf = np.full(len(dirs), 1.0), np.full(len(dirs), 10.0)
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    idx = dv.build(up(cloud.positions), cam, cfg.pad)
+    rays = (up(pixels), up(dirs), up(tn), up(tf), up(slopes))
+    q = dv.query(idx, *rays, facts=True)
+    sc = hp.SamplerConfig(k_neighbors=k, retention_mode=mode, gamma=gamma)
+    colors = torch.from_numpy(cloud.colors).cuda()
+    full = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, colors, exact_t_end=exact_t_end, facts=q[6])
+    seen = []
+    for want in (16, 64, 512):
+        got, nf = _prefix_frame(idx, rays, sc, colors, exact_t_end, want)
+        _assert_same(got, full)
+        seen.append(nf)
+    assert seen[0] > 0  # the small heads do send rays to the full path
+
+
+@pytest.mark.parametrize("exact_t_end", [True, False])
+def test_pipeline_prefix_frame_equals_full_frame(exact_t_end):
+    from paper_2404_14044_b200 import pipeline
+    _, cloud, cam, cfg, tn, tf, stride, _ = gu.get_case("cfg1")
+    dev = torch.device("cuda")
+    xyz = torch.from_numpy(cloud.positions).to(dev)
+    col = torch.from_numpy(cloud.colors).to(dev)
+    pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    rays = (up(pixels), up(dirs), up(t_near), up(t_far), up(slopes))
+    idx = dv.build(xyz, cam, cfg.pad)
+    sc = hp.SamplerConfig()
+    a = pipeline._query_sample(idx, col, *rays, sc, exact_t_end, None, prefix=True)
+    b = pipeline._query_sample(idx, col, *rays, sc, exact_t_end, None, prefix=False)
+    _assert_same(a.samples, b.samples)
+    assert a.Q == b.Q
