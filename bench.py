@@ -448,7 +448,7 @@ def run_ours(args, w, rank, world, dist):
                    "n_indexed": fr.index.n_in, "Q": Q, "R": R, "P": P,
                    "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"row bands x{world}" if world > 1 else "single GPU",
-                   "ray_chunks": fr.chunks,
+                   "ray_chunks": fr.chunks, "prefix_mode": pipeline.PREFIX, "prefix_flagged_rays": fr.flagged,
                    "parity_gate": parity},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

@@ -138,8 +138,8 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
 /* Prefix mode (callers that only want samples): instead of hp_query_fill,
  * sort in place, at the front of each ray's match scratch, the ray's
  * smallest-t matches -- all of them when it has <= want, else everything up
- * to the histogram bin where the count reaches `want` (<= 2048) -- and
- * record the sampler's facts over ALL its matches.  plen [m] receives each
+ * to the histogram bin where the count reaches `want` (<= 1024) -- and
+ * record the sampler's facts over that prefix.  plen [m] receives each
  * prefix length; the view gives the (device) arrays of the prefixes: ray r
  * at start[r], t float64, ids int32, dist float64.  cut_t / cut_d [m]
  * receive the smallest t and dist of the matches left out (+inf when none;

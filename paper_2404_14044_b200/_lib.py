@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhp_b200.so")
+# HP_LIB: an alternative build of the same ABI (A/B measurements only)
+LIB_PATH = os.environ.get("HP_LIB") or os.path.join(_HERE, "libhp_b200.so")
 
 HP_EINVAL = -1
 

@@ -632,25 +632,31 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
 
 
 // ---------------------------------------------------------------- prefix sort
-// For callers that only want samples (pipeline.search_and_sample): each ray's
-// smallest-t matches -- everything through the 2048-bin histogram bin where
-// the count reaches `want` (at most kCap) -- sorted by (t, id) in place at the
-// front of the ray's match scratch (t, id, dist), plus the sampler's facts
-// over ALL the ray's matches, and two cuts for the matches left out: their
-// smallest t (every one is strictly above the prefix's last t) and their
-// smallest dist.  The sampler runs on these prefixes and flags a ray whose
-// work would reach past its prefix (hp_sample_run prefix mode).
-constexpr int kPrefixCap = 2048;
-constexpr int kPrefixThreads = 512;
-constexpr int kSelBins = 2048;
+// For callers that only want samples (pipeline frames): each ray's
+// smallest-t matches -- everything through the histogram bin where the count
+// reaches `want` (at most kPrefixCap) -- sorted by (t, id) in place at the
+// front of the ray's match scratch (t, id, dist), the sampler's facts over
+// that prefix, and two cuts for the matches left out: their smallest t
+// (every one is strictly above the prefix's last t) and their smallest dist.
+// The sampler runs on these prefixes and flags a ray whose work would reach
+// past its prefix (hp_sample_run_prefix).
+#ifndef HP_PREFIX_U
+#define HP_PREFIX_U 2
+#endif
+#ifndef HP_PREFIX_MINB
+#define HP_PREFIX_MINB 0
+#endif
+constexpr int kPrefixCap = 1024;
+constexpr int kPrefixThreads = 256;
 
+template <int kCap>
 struct PrefixSmem {
-    double t[kPrefixCap];
-    double d2[kPrefixCap];
-    int id[kPrefixCap];
-    unsigned bk[kPrefixCap];
-    int hist[kSelBins + 1];  // selection histogram, then the fine buckets
-    unsigned short lst[kPrefixCap], perm[kPrefixCap];
+    double t[kCap];
+    double d2[kCap];
+    int id[kCap];
+    unsigned bk[kCap];
+    int hist[kCap + 1];  // selection histogram (kCap bins), then the fine buckets
+    unsigned short lst[kCap], perm[kCap];
     int chist[kCoarse + 1];
     int scan_sh[33];
     unsigned long long cut_t, cut_d2;  // order keys of the left-out minima
@@ -665,13 +671,19 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
 }
 
-__global__ void __launch_bounds__(kPrefixThreads) k_query_prefix(
+// Passes per ray: [q > want] a kCap-bin histogram of t -> the bin where the
+// count reaches want; staging (selected -> shared memory; the others give the
+// cuts and the finiteness check); rank_segment; write-out with the facts
+// counted over the prefix (a prefix count >= K implies the full one; the
+// sampler checks the cuts before trusting a smaller one).
+template <int kCap, int kT>
+__global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
     const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm, int64_t m,
     int want, const double* __restrict__ slopes, int* __restrict__ facts, int* __restrict__ plen,
     double* __restrict__ cut_t, double* __restrict__ cut_d, double* st, int* sid, double* sd) {
     extern __shared__ __align__(16) unsigned char dyn[];
-    PrefixSmem& F = *reinterpret_cast<PrefixSmem*>(dyn);
-    constexpr int kT = kPrefixThreads;
+    PrefixSmem<kCap>& F = *reinterpret_cast<PrefixSmem<kCap>*>(dyn);
+    constexpr int kBins = kCap;
     const int tid = threadIdx.x;
     for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
         const int64_t so = soff[r];
@@ -686,88 +698,98 @@ __global__ void __launch_bounds__(kPrefixThreads) k_query_prefix(
         }
         const float tlo = from_fkey(tmm[r].x), thi = from_fkey(tmm[r].y);
         const float span = thi - tlo;
-        const float sel_scale = span > 0.0f ? fminf(float(kSelBins) / span, FLT_MAX) : 0.0f;
+        const float sel_scale = span > 0.0f ? fminf(float(kBins) / span, FLT_MAX) : 0.0f;
         auto sel_bin = [&](double t) {
-            return min(int(fminf((__double2float_rn(t) - tlo) * sel_scale, float(kSelBins))), kSelBins - 1);
+            return min(int(fminf((__double2float_rn(t) - tlo) * sel_scale, float(kBins))), kBins - 1);
         };
         const bool all = q <= want;
-        int bsel = kSelBins - 1, L = q;
+        int bsel = kBins - 1, L = q;
+        if (tid == 0) {
+            F.cnt = F.fcount = F.fbad = 0;
+            F.cut_t = F.cut_d2 = ~0ull;
+        }
+        // the ray's matches in chunks of kU per thread, every load of a chunk
+        // in flight at once (a ray of <= kChunk matches stays in registers
+        // from the histogram to the staging)
+        constexpr int kU = HP_PREFIX_U, kChunk = kT * kU;
+        double tv[kU], dv[kU];
+        int iv[kU];
+        const bool single = q <= kChunk;
+        auto load_chunk = [&](int c0, bool full) {
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const int e = c0 + u * kT + tid;
+                if (e < q) {
+                    tv[u] = st[so + e];
+                    if (full) {
+                        dv[u] = sd[so + e];
+                        iv[u] = sid[so + e];
+                    }
+                }
+            }
+        };
+        if (single) load_chunk(0, true);
         if (!all) {
-            for (int k = tid; k <= kSelBins; k += kT) F.hist[k] = 0;
-            if (tid == 0) F.bsel = kSelBins;
+            for (int k = tid; k <= kBins; k += kT) F.hist[k] = 0;
+            if (tid == 0) F.bsel = kBins;
             __syncthreads();
-            for (int e = tid; e < q; e += kT) {
-                const int b = sel_bin(st[so + e]);
-                const unsigned peers = __match_any_sync(__activemask(), b);
-                if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.hist[b], __popc(peers));
+            for (int c0 = 0; c0 < q; c0 += kChunk) {
+                if (!single) load_chunk(c0, false);
+#pragma unroll
+                for (int u = 0; u < kU; u++) {
+                    const int e = c0 + u * kT + tid;
+                    const int b = e < q ? sel_bin(tv[u]) : kBins;
+                    const unsigned peers = __match_any_sync(0xffffffffu, b);
+                    if (e < q && lane_id() == __ffs(peers) - 1) atomicAdd(&F.hist[b], __popc(peers));
+                }
             }
             __syncthreads();
-            block_scan_inplace<(kSelBins + kT - 1) / kT>(F.hist, kSelBins, F.scan_sh);
-            if (tid == 0) F.hist[kSelBins] = q;
+            block_scan_inplace<(kBins + kT - 1) / kT>(F.hist, kBins, F.scan_sh);
+            if (tid == 0) F.hist[kBins] = q;
             __syncthreads();
-            // first bin whose cumulative count reaches `want`, within kPrefixCap
-            for (int b = tid; b < kSelBins; b += kT)
+            // first bin whose cumulative count reaches `want`
+            for (int b = tid; b < kBins; b += kT)
                 if (F.hist[b + 1] >= want) atomicMin(&F.bsel, b);
             __syncthreads();
             bsel = F.bsel;
             L = F.hist[bsel + 1];
-            if (L > kPrefixCap) {  // that bin alone overflows: stop before it
+            if (L > kCap) {  // that bin alone overflows: stop before it
                 bsel -= 1;
                 L = bsel >= 0 ? F.hist[bsel + 1] : 0;
             }
         }
-        // stage the selected matches (the smallest L by t) in shared memory
-        if (tid == 0) F.cnt = 0;
         for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
         __syncthreads();
-        for (int k = tid; k <= L; k += kT) F.hist[k] = 0;
-        for (int e0 = 0; e0 < q; e0 += kT) {
-            const int e = e0 + tid;
-            bool in = false;
-            double t = 0.0;
-            if (e < q) {
-                t = st[so + e];
-                in = all || sel_bin(t) <= bsel;
-            }
-            const unsigned b = __ballot_sync(0xffffffffu, in);
-            int base = 0;
-            if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (in) {
-                const int slot = base + __popc(b & ((1u << lane_id()) - 1));
-                F.t[slot] = t;
-                F.id[slot] = sid[so + e];
-                F.d2[slot] = sd[so + e];
-            }
-        }
-        __syncthreads();
-        if (L > 0) {  // bounds of the selected t (any bounds keep the map monotone)
-            const float hi = all ? thi : tlo + float(bsel + 1) / sel_scale;
-            rank_segment<kPrefixCap, kT>(L, tlo, hi, F.t, F.id, F.bk, F.hist, F.lst, F.perm, F.chist, F.scan_sh);
-        }
-        // facts over all q matches and the cuts of the left-out ones (before
-        // the prefix overwrites the scratch)
-        if (tid == 0) {
-            F.fcount = F.fbad = 0;
-            F.cut_t = F.cut_d2 = ~0ull;
-        }
-        __syncthreads();
-        const double slope = __ldcg(slopes + r);
-        const double r0 = L > 0 ? dmul(slope, F.t[F.perm[0]]) : 0.0;
-        int cnt = 0;
+        // stage the selected matches (the smallest L by t); the others give
+        // the cuts; every value is checked finite
         bool bad = false;
         unsigned long long kt = ~0ull, kd = ~0ull;
-        for (int e = tid; e < q; e += kT) {
-            const double te = st[so + e], d2 = sd[so + e];
-            const double d = sqrt(d2);
-            bad |= !(fabs(te) <= DBL_MAX) || !(d >= 0.0) || !(d <= DBL_MAX);
-            cnt += d <= r0;
-            if (!all && sel_bin(te) > bsel) {
-                kt = min(kt, dkey(te));
-                kd = min(kd, dkey(d2));
+        for (int c0 = 0; c0 < q; c0 += kChunk) {
+            if (!single) load_chunk(c0, true);
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const int e = c0 + u * kT + tid;
+                bool in = false;
+                if (e < q) {
+                    in = all || sel_bin(tv[u]) <= bsel;
+                    bad |= !(fabs(tv[u]) <= DBL_MAX) || !(dv[u] >= 0.0) || !(dv[u] <= DBL_MAX);
+                    if (!in) {
+                        kt = min(kt, dkey(tv[u]));
+                        kd = min(kd, dkey(dv[u]));
+                    }
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, in);
+                int base = 0;
+                if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (in) {
+                    const int slot = base + __popc(b & ((1u << lane_id()) - 1));
+                    F.t[slot] = tv[u];
+                    F.id[slot] = iv[u];
+                    F.d2[slot] = dv[u];
+                }
             }
         }
-        cnt = warp_sum(cnt);
         const bool anybad = __any_sync(0xffffffffu, bad);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -776,19 +798,31 @@ __global__ void __launch_bounds__(kPrefixThreads) k_query_prefix(
         }
         if (lane_id() == 0) {
             if (anybad) atomicOr(&F.fbad, 1);
-            if (cnt) atomicAdd(&F.fcount, cnt);
             if (kt != ~0ull) {
                 atomicMin(&F.cut_t, kt);
                 atomicMin(&F.cut_d2, kd);
             }
         }
+        for (int k = tid; k <= L; k += kT) F.hist[k] = 0;
         __syncthreads();
-        for (int p = tid; p < L; p += kT) {  // the sorted prefix, in place
+        if (L > 0) {  // bounds of the selected t (any bounds keep the map monotone)
+            const float hi = all ? thi : tlo + float(bsel + 1) / sel_scale;
+            rank_segment<kCap, kT>(L, tlo, hi, F.t, F.id, F.bk, F.hist, F.lst, F.perm, F.chist, F.scan_sh);
+        }
+        // the sorted prefix, in place (the ray's matches were all read above)
+        const double r0 = L > 0 ? dmul(__ldcg(slopes + r), F.t[F.perm[0]]) : 0.0;
+        int cnt = 0;
+        for (int p = tid; p < L; p += kT) {
             const int e = F.perm[p];
+            const double d = sqrt(F.d2[e]);
             st[so + p] = F.t[e];
             sid[so + p] = F.id[e];
-            sd[so + p] = sqrt(F.d2[e]);
+            sd[so + p] = d;
+            cnt += d <= r0;
         }
+        cnt = warp_sum(cnt);
+        if (lane_id() == 0 && cnt) atomicAdd(&F.fcount, cnt);
+        __syncthreads();
         if (tid == 0) {
             plen[r] = L;
             facts[r] = (F.fbad || L == 0) ? -1 : F.fcount;
@@ -1221,7 +1255,7 @@ extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, 
                                int32_t* facts, int32_t* plen, double* cut_t, double* cut_d, int64_t capacity,
                                void* workspace, size_t workspace_bytes, hp_query_prefix_view* view,
                                hp_stream_t stream) {
-    if (m < 0 || want < 1 || want > kPrefixCap || !slopes || !facts || !plen || !cut_t || !cut_d) {
+    if (m < 0 || want < 1 || want > kPrefixCap || (m > 0 && (!slopes || !facts || !plen || !cut_t || !cut_d))) {
         set_error("hp_query_prefix: invalid arguments (1 <= want <= %d)", kPrefixCap);
         return HP_EINVAL;
     }
@@ -1239,12 +1273,13 @@ extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, 
     }
     if (m == 0) return HP_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    constexpr auto kern = k_query_prefix<kPrefixCap, kPrefixThreads>;
     static const int occ = [] {  // once (thread-safe)
-        set_smem(k_query_prefix, sizeof(PrefixSmem));
-        return resident(k_query_prefix, kPrefixThreads, sizeof(PrefixSmem));
+        set_smem(kern, sizeof(PrefixSmem<kPrefixCap>));
+        return resident(kern, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>));
     }();
     TimedSpan ts("k_query_prefix", s);
-    k_query_prefix<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
+    kern<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
                                                                              facts, plen, cut_t, cut_d, w.st, w.sid,
                                                                              w.sd);
     HP_CHECK_LAUNCH("k_query_prefix");

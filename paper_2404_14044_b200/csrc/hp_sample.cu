@@ -584,8 +584,7 @@ extern "C" int hp_sample_run_prefix(const int64_t* offsets, int64_t m, const hp_
                                     int64_t* r_off, double* t_end, int32_t* flagged, void* workspace,
                                     size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
-    if (!pre || !pre->start || !pre->length || !pre->ids || !pre->t || !pre->dist || !pre->cut_t || !pre->cut_d ||
-        !query_facts || !flagged) {
+    if (!pre || !flagged || (m > 0 && (!pre->start || !pre->length || !pre->cut_t || !pre->cut_d || !query_facts))) {
         set_error("hp_sample_run_prefix: the prefix arrays, facts and flagged are required");
         return HP_EINVAL;
     }

@@ -11,6 +11,7 @@ Q after the query count pass, R after the sampler), as in the two-phase C ABI.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -281,7 +282,7 @@ class QueryPrefix:
         return sp
 
 
-PREFIX_WANT = 512
+PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "512"))  # head length the sampler usually needs
 
 
 def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,

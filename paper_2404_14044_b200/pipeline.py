@@ -76,9 +76,11 @@ class FrameResult:
         return int(self.samples[1].numel())
 
 
-# bytes of device memory per match slot of one query + sample pass: unsorted
-# scratch 20 + CSR 24 + sampler scratch (bounded) -- sizing ray chunks
+# bytes of device memory per match slot of one query + sample pass, for
+# sizing ray chunks: unsorted scratch 20 + CSR 24 + sampler scratch (bounded);
+# prefix mode keeps only the scratch
 BYTES_PER_MATCH = 56
+BYTES_PER_MATCH_PREFIX = 24
 
 
 _BUDGET: dict = {}
@@ -91,15 +93,15 @@ def _side_stream(dev) -> torch.cuda.Stream:
     return _SIDE[dev]
 
 
-def match_budget(fraction: float = 0.8) -> int:
+def match_budget(fraction: float = 0.8, bytes_per_match: int = BYTES_PER_MATCH) -> int:
     """Match slots one pass may use: a fraction of the device memory free at
     the first call (cached per device: cudaMemGetInfo costs milliseconds)."""
     dev = torch.cuda.current_device()
     if dev not in _BUDGET:
         free, _ = torch.cuda.mem_get_info()
         free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()  # torch's cached blocks
-        _BUDGET[dev] = max(int(free * fraction) // BYTES_PER_MATCH, 1 << 20)
-    return _BUDGET[dev]
+        _BUDGET[dev] = int(free * fraction)
+    return max(_BUDGET[dev] // bytes_per_match, 1 << 20)
 
 
 def _concat_samples(parts):
@@ -141,44 +143,53 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
 PREFIX = os.environ.get("HP_PREFIX", "1") != "0"
 
 
+def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end):
+    """Sample over the prefixes of ``pre``; rays whose sampling may reach past
+    their head re-run through the full query.  (samples 9-tuple, Q, flagged)"""
+    *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
+    Q = pre.total
+    if n_flagged:
+        sel = torch.nonzero(flagged, as_tuple=True)[0]
+        q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
+        sub = device.sample(q[0], q[1], q[2], q[3], slopes[sel], sampler_cfg, colors, exact_t_end, facts=q[6])
+        del q
+        s = device.merge_flagged(tuple(s), flagged, sub)
+    return tuple(s), Q, n_flagged
+
+
+def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end):
+    pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes)
+    return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end)
+
+
 def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
                   mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None) -> FrameResult:
-    budget = int(max_matches) if max_matches is not None else match_budget()
-    if PREFIX if prefix is None else prefix:
-        try:
-            pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes, max_scratch=budget)
-        except device.MatchBudgetExceeded:
-            before_sample()
-            return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                                  exact_t_end, budget, mark)
-        mark("query")
-        before_sample()
-        *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
-        Q = pre.total
-        del pre
-        if n_flagged:
-            sel = torch.nonzero(flagged, as_tuple=True)[0]
-            q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
-            sub = device.sample(q[0], q[1], q[2], q[3], slopes[sel], sampler_cfg, colors, exact_t_end,
-                                facts=q[6])
-            s = device.merge_flagged(tuple(s), flagged, sub)
-        mark("sample")
-        return FrameResult(idx, None, tuple(s), Q=Q, flagged=n_flagged)
+    prefix = PREFIX if prefix is None else prefix
+    budget = int(max_matches) if max_matches is not None else match_budget(
+        bytes_per_match=BYTES_PER_MATCH_PREFIX if prefix else BYTES_PER_MATCH)
     try:
-        q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
+        if prefix:
+            pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes, max_scratch=budget)
+        else:
+            q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
     except device.MatchBudgetExceeded:
         before_sample()
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                              exact_t_end, budget, mark)
+                              exact_t_end, budget, mark, prefix)
     mark("query")
     before_sample()
+    if prefix:
+        s, Q, n_flagged = _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
+                                         exact_t_end)
+        mark("sample")
+        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged)
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
     return FrameResult(idx, q[:6], s, Q=int(q[1].numel()))
 
 
 def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end,
-                   budget, mark):
+                   budget, mark, prefix=False):
     bo = device.query_bounds(idx, pixels, dirs, t_near, t_far, slopes).cpu().numpy()
     m = bo.shape[0] - 1
     cuts = [0]
@@ -188,8 +199,15 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
         if b <= a:
             raise device.MatchBudgetExceeded(int(bo[a + 1] - bo[a]), budget)
         cuts.append(min(b, m))
-    parts, Q = [], 0
+    parts, Q, nf = [], 0, 0
     for a, b in zip(cuts[:-1], cuts[1:]):
+        if prefix:
+            s, q_n, f_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
+                                       slopes[a:b], sampler_cfg, exact_t_end)
+            parts.append(s)
+            Q += q_n
+            nf += f_n
+            continue
         q = device.query(idx, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b], slopes[a:b], facts=True)
         parts.append(device.sample(q[0], q[1], q[2], q[3], slopes[a:b], sampler_cfg, colors,
                                    exact_t_end, facts=q[6]))
@@ -197,7 +215,7 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
         del q
     mark("query")
     mark("sample")
-    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts))
+    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf)
 
 
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
