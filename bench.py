@@ -432,6 +432,10 @@ def run_ours(args, w, rank, world, dist):
     }
     for k, sel in cls.items():  # read the unsorted matches (20 B), write the CSR (24 B)
         kbytes[k] = 44 * int(qs[sel].sum()) + 24 * int(sel.sum())
+    plen = int(fr.prefix_len.item()) if fr.prefix_len is not None else 0
+    # prefix mode: read the unsorted matches (20 B), write the sorted heads
+    # (t, id32, dist: 20 B), per ray offsets/soff/t-bounds in, length/facts/cuts out
+    kbytes["k_query_prefix"] = 20 * q_loc + 20 * plen + 56 * m_loc
     kern = {k: (v / args.steps, c // args.steps) for k, (v, c) in kern_tot.items()}
     top = max((k for k in kern if k in kbytes), key=lambda k: kern[k][0])
     t_top = kern[top][0] / max(kern[top][1], 1)
@@ -455,7 +459,12 @@ def run_ours(args, w, rank, world, dist):
                      "algorithmic_bytes": b_top, "traffic_source": traffic_src,
                      "peak_source": peak_kind},
         "frame_roofline": {"bytes": bb + bq + bs, "achieved_gbs": (bb + bq + bs) / (ms / 1e3) / 1e9,
-                           "frac": (bb + bq + bs) / (ms / 1e3) / 1e9 / peak},
+                           "frac": (bb + bq + bs) / (ms / 1e3) / 1e9 / peak,
+                           # a path that never materialises the query CSR,
+                           # reported beside B_frame, not divided by it
+                           "b_fused": 24 * n + 64 * fr.index.n_in + 32 * P + 96 * m_total + 48 * R
+                           if fr.query is None and pipeline.PREFIX else None,
+                           "prefix_len": plen if fr.prefix_len is not None else None},
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "kernels_ms": {k: round(v[0], 4) for k, v in sorted(kern.items(), key=lambda x: -x[1][0])},
         "kernels_gbs": {k: round(kbytes[k] / (kern[k][0] / 1e3) / 1e9, 1) for k in kern if k in kbytes

@@ -70,6 +70,7 @@ class FrameResult:
     Q: int = 0
     chunks: int = 1
     flagged: int = 0         # prefix mode: rays re-run through the full query
+    prefix_len: object = None  # prefix mode: device tensor, total prefix length (sum over rays)
 
     @property
     def R(self) -> int:
@@ -143,11 +144,15 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
 PREFIX = os.environ.get("HP_PREFIX", "1") != "0"
 
 
+_PREFIX_LEN: list = []  # prefix lengths of the passes of the current frame (device scalars)
+
+
 def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end):
     """Sample over the prefixes of ``pre``; rays whose sampling may reach past
     their head re-run through the full query.  (samples 9-tuple, Q, flagged)"""
     *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
     Q = pre.total
+    _PREFIX_LEN.append(pre.length.sum())
     if n_flagged:
         sel = torch.nonzero(flagged, as_tuple=True)[0]
         q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
@@ -179,10 +184,11 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
     mark("query")
     before_sample()
     if prefix:
+        _PREFIX_LEN.clear()
         s, Q, n_flagged = _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                                          exact_t_end)
         mark("sample")
-        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged)
+        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, prefix_len=_PREFIX_LEN.pop())
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
     return FrameResult(idx, q[:6], s, Q=int(q[1].numel()))
@@ -200,6 +206,7 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
             raise device.MatchBudgetExceeded(int(bo[a + 1] - bo[a]), budget)
         cuts.append(min(b, m))
     parts, Q, nf = [], 0, 0
+    _PREFIX_LEN.clear()
     for a, b in zip(cuts[:-1], cuts[1:]):
         if prefix:
             s, q_n, f_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
@@ -215,7 +222,9 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
         del q
     mark("query")
     mark("sample")
-    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf)
+    plen = sum(_PREFIX_LEN) if (prefix and _PREFIX_LEN) else None
+    _PREFIX_LEN.clear()
+    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf, prefix_len=plen)
 
 
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
