@@ -110,9 +110,20 @@ int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
 /* Per-ray search-radius slopes on host threads (replaces the vectorised
  * geometry.radius_slopes, reference geometry.py:249-260): same expression
  * order and libm calls as numpy, bit-identical; pixels int64 [m,2] with
- * element stride pixel_stride between rays; slopes float64 [m] (host). */
+ * element stride pixel_stride between rays, or NULL for the camera's ray
+ * grid (ray k = pixel (k % width, k / width)); slopes float64 [m] (host). */
 int hp_radius_slopes_host(const hp_camera* cam, const int64_t* pixels, int64_t pixel_stride, int64_t m,
                           double kernel_radius, int approx, double* slopes, int threads);
+
+/* The camera's ray grid on the device (replaces geometry.ray_grid,
+ * geometry.py:289-306, bit-identical): rows [row0, row0 + rows) of the image,
+ * ray k = (row0 * width + k) in row-major order.  dirs float64 [m,3] unit
+ * directions through the pixel centres; pixels int64 [m,2] (u, v) or NULL;
+ * t_near / t_far [m] filled with the given values, or NULL.
+ * m = rows * cam->width. */
+int hp_ray_grid(const hp_camera* cam, int64_t row0, int64_t rows, double* dirs, int64_t* pixels,
+                double t_near_value, double t_far_value, double* t_near, double* t_far,
+                hp_stream_t stream);
 
 /* ---------------- query ---------------- */
 /* capacity: scratch slots for the unsorted matches (hp_query_count reports

@@ -22,9 +22,12 @@ void slopes_range(const hp_camera& c, const int64_t* pix, int64_t stride, double
     const double fkr = f * kr;
     const double ff = f * f;
     for (int64_t r = a; r < b; r++) {
+        // pixels NULL: the ray grid, ray r = pixel (r % W, r / W)
+        const int64_t pu = pix ? pix[r * stride] : r % c.width;
+        const int64_t pv = pix ? pix[r * stride + 1] : r / c.width;
         // _plane_offsets: (u + 0.5 - 0.5 * W) * pixel_width (left to right)
-        const double ox = ((double(pix[r * stride]) + 0.5) - hw) * c.pixel_width;
-        const double oy = ((double(pix[r * stride + 1]) + 0.5) - hh) * c.pixel_height;
+        const double ox = ((double(pu) + 0.5) - hw) * c.pixel_width;
+        const double oy = ((double(pv) + 0.5) - hh) * c.pixel_height;
         const double a2 = ox * ox + oy * oy;
         const double ae2 = ff + a2;
         out[r] = approx ? fkr / ae2 : fkr / (std::sqrt(ae2) * std::hypot(std::sqrt(a2) - kr, f));
@@ -35,7 +38,7 @@ void slopes_range(const hp_camera& c, const int64_t* pix, int64_t stride, double
 
 extern "C" int hp_radius_slopes_host(const hp_camera* cam, const int64_t* pixels, int64_t pixel_stride, int64_t m,
                                      double kernel_radius, int approx, double* slopes, int threads) {
-    if (!cam || m < 0 || (m > 0 && (!pixels || !slopes))) return HP_EINVAL;
+    if (!cam || m < 0 || (m > 0 && !slopes) || (!pixels && m > cam->width * cam->height)) return HP_EINVAL;
     if (threads < 1) threads = 1;
     const int64_t per = (m + threads - 1) / threads;
     if (threads == 1 || m < 4096) {

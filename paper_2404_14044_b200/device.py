@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._lib import c_i64, c_size
 
-__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "query_prefix", "sample", "sample_prefix", "merge_flagged",
+__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "query_prefix", "sample", "sample_prefix", "merge_flagged", "ray_grid",
            "primary_surface", "MatchBudgetExceeded", "SAMPLE_EXACT_PER_RAY"]
 
 # match-scratch capacity of the last query per device (slots), reused so a
@@ -471,6 +471,27 @@ def merge_flagged(main, flagged: torch.Tensor, sub):
     te = t_end.clone()
     te[sel] = s_tend
     return (off, *out[:-1], out[-1], te)
+
+
+def ray_grid(camera, dev=None, row0: int = 0, rows: int | None = None, t_near: float | None = None,
+             t_far: float | None = None):
+    """geometry.ray_grid on the device (hp_ray_grid, bit-identical to numpy;
+    reference geometry.py:289-306): (dirs f64 [m,3], pixels i64 [m,2]) for
+    image rows [row0, row0 + rows), plus t_near / t_far [m] filled with the
+    given scalars (None when not given)."""
+    lib = _lib.load(require_device=True)
+    dev = dev or torch.device("cuda", torch.cuda.current_device())
+    rows = int(camera.height) - row0 if rows is None else int(rows)
+    m = rows * int(camera.width)
+    dirs = torch.empty((m, 3), dtype=torch.float64, device=dev)
+    pixels = torch.empty((m, 2), dtype=torch.int64, device=dev)
+    tn = torch.empty(m, dtype=torch.float64, device=dev) if t_near is not None else None
+    tf = torch.empty(m, dtype=torch.float64, device=dev) if t_far is not None else None
+    _lib.check(lib.hp_ray_grid(ctypes.byref(camera_struct(camera)), int(row0), rows, _ptr(dirs), _ptr(pixels),
+                               float(t_near or 0.0), float(t_far or 0.0),
+                               _ptr(tn) if tn is not None else ctypes.c_void_p(0),
+                               _ptr(tf) if tf is not None else ctypes.c_void_p(0), _stream()))
+    return dirs, pixels, tn, tf
 
 
 def primary_surface(r_off: torch.Tensor, r_id: torch.Tensor, r_t: torch.Tensor):

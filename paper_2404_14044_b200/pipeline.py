@@ -20,23 +20,28 @@ import torch
 from . import device
 from .sampler import SamplerConfig
 
-__all__ = ["FrameResult", "frame_device", "search_and_sample", "StageTimer", "host_slopes"]
+__all__ = ["FrameResult", "frame_device", "search_and_sample", "search_and_sample_view", "StageTimer",
+           "host_slopes"]
 
 
-def host_slopes(camera, pixels: np.ndarray, kernel_radius: float, approx: bool = False,
+def host_slopes(camera, pixels: np.ndarray | None, kernel_radius: float, approx: bool = False,
                 out: np.ndarray | None = None, threads: int | None = None) -> np.ndarray:
     """``radius_slopes`` on host threads through the library
     (hp_radius_slopes_host: same expression order and libm calls as numpy,
-    bit-identical).  ``out`` may be a (pinned) float64 buffer of m values."""
-    import os
+    bit-identical).  ``pixels=None``: the camera's whole ray grid (row-major,
+    as ``ray_grid``).  ``out`` may be a (pinned) float64 buffer of m values."""
     lib = device._lib.load(require_device=False)
-    px = np.ascontiguousarray(pixels, dtype=np.int64).reshape(-1, 2)
-    m = px.shape[0]
+    if pixels is None:
+        px, m = None, int(camera.width) * int(camera.height)
+    else:
+        px = np.ascontiguousarray(pixels, dtype=np.int64).reshape(-1, 2)
+        m = px.shape[0]
     if out is None:
         out = np.empty(m, dtype=np.float64)
     threads = threads or min(16, os.cpu_count() or 1)
     device._lib.check(lib.hp_radius_slopes_host(ctypes.byref(device.camera_struct(camera)),
-                                                px.ctypes.data_as(ctypes.c_void_p), 2, m,
+                                                px.ctypes.data_as(ctypes.c_void_p) if px is not None
+                                                else ctypes.c_void_p(0), 2, m,
                                                 float(kernel_radius), 1 if approx else 0,
                                                 out.ctypes.data_as(ctypes.c_void_p), int(threads)))
     return out
@@ -276,6 +281,47 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
         cols_ready = side.record_event()
     main.wait_event(rays_ready)
     s = _query_sample(idx, col, pix_d, dirs_d, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
+                      max_matches, before_sample=lambda: main.wait_event(cols_ready)).samples
+    outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
+    for o, x in zip(outs, s):
+        o.copy_(x, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return tuple(o.numpy() for o in outs)
+
+
+def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: float,
+                           sampler_cfg: SamplerConfig | None = None, with_colors: bool = True,
+                           exact_t_end: bool = True, max_matches: int | None = None):
+    """A whole view: the camera's ray grid (``ray_grid(camera)``, every pixel,
+    row-major, scalar t_near / t_far -- the reference CLI's
+    ``generate_rays`` + renderer ``_prepare``, cli.py:127-162,
+    renderer.py:113-125) generated on the device (hp_ray_grid, bit-identical
+    to numpy), then build -> query -> sample as :func:`search_and_sample`.
+    Only the cloud (and its colours) go up; returns the numpy 9-tuple of
+    ``sample_batch_arrays``."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def up(a):
+        if isinstance(a, torch.Tensor):
+            return a.to(device=dev, dtype=torch.float64, non_blocking=True)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=torch.float64, non_blocking=True)
+
+    main = torch.cuda.current_stream()
+    side = _side_stream(dev)
+    side.wait_stream(main)
+    xyz = up(cloud.positions)
+    idx = device.build(xyz, camera, search_cfg.pad)
+    dirs, pixels, tn, tf = device.ray_grid(camera, dev, t_near=t_near, t_far=t_far)
+    m = int(dirs.shape[0])
+    sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
+    host_slopes(camera, None, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
+    with torch.cuda.stream(side):
+        sl = sl_host.to(dev, non_blocking=True)
+        rays_ready = side.record_event()
+        col = up(cloud.colors) if (with_colors and cloud.colors is not None) else None
+        cols_ready = side.record_event()
+    main.wait_event(rays_ready)
+    s = _query_sample(idx, col, pixels, dirs, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
                       max_matches, before_sample=lambda: main.wait_event(cols_ready)).samples
     outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
     for o, x in zip(outs, s):

@@ -223,3 +223,5 @@ def test_native_host_slopes_are_bit_identical():
         for threads in (1, 7):
             b = pipeline.host_slopes(cam, pix, 0.0137, approx, threads=threads)
             assert a.tobytes() == b.tobytes()
+            g = pipeline.host_slopes(cam, None, 0.0137, approx, threads=threads)  # the ray grid
+            assert a.tobytes() == g.tobytes()
