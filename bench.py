@@ -173,9 +173,30 @@ def frame_bytes(n, n_in, P, m, Q, R, colors=True):
     return b_build, b_query, b_sample
 
 
+_CLOCK_CHILD = r"""
+import select, sys, pynvml
+pynvml.nvmlInit()
+try:
+    h = pynvml.nvmlDeviceGetHandleByPciBusId(sys.argv[1])
+except Exception:
+    h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+        pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+print("ready", flush=True)
+rows = []
+while not select.select([sys.stdin], [], [], 0.005)[0]:
+    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    rows.append("%d %d %s" % (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
+                              "".join("1" if rs & b else "0" for b in bits)))
+print("\n".join(rows), flush=True)
+"""
+
+
 class ClockSampler:
     """SM clocks / throttle reasons sampled during the timed region: NVML
-    every 2 ms (nvidia-ml-py), else nvidia-smi every 0.2 s."""
+    every 5 ms in a child process (no GIL contention with the timed host
+    loop), else nvidia-smi every 0.2 s from a thread."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -188,33 +209,20 @@ class ClockSampler:
         self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._child = None
 
-    def _nvml_handle(self):
-        import pynvml
-        pynvml.nvmlInit()
-        try:  # the CUDA device's PCI address (CUDA and NVML indices may differ)
-            p = torch.cuda.get_device_properties(self.index)
-            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
-            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-        except Exception:
-            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+    def _start_child(self):
+        import torch
+        p = torch.cuda.get_device_properties(self.index)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        child = subprocess.Popen([sys.executable, "-c", _CLOCK_CHILD, bus, str(self.index)], stdin=subprocess.PIPE,
+                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        if child.stdout.readline().strip() != "ready":
+            child.kill()
+            raise RuntimeError("no NVML")
+        return child
 
-    def _run(self):
-        try:
-            nv, h = self._nvml_handle()
-            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            self.source = "nvml"
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((float(sm), float(mx), {n for n, b in zip(self.NAMES, bits) if rs & b}))
-                self._stop.wait(0.002)
-            return
-        except Exception:
-            self.rows.clear()
-        self.source = "nvidia-smi"
+    def _run_smi(self):
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -229,11 +237,28 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._child = self._start_child()
+            self.source = "nvml"
+        except Exception:
+            self._child = None
+            self.source = "nvidia-smi"
+            self._t = threading.Thread(target=self._run_smi, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
+        if self._child is not None:
+            try:
+                out, _ = self._child.communicate(input="stop\n", timeout=30)
+                for line in out.splitlines():
+                    f = line.split()
+                    if len(f) == 3:
+                        self.rows.append((float(f[0]), float(f[1]),
+                                          {n for n, c in zip(self.NAMES, f[2]) if c == "1"}))
+            except Exception:
+                self._child.kill()
+            return
         self._stop.set()
         self._t.join(timeout=10)
 
@@ -377,6 +402,8 @@ def run_ours(args, w, rank, world, dist):
             up(w["t_far"][r0:r1]), up(w["slopes"][r0:r1])]
     scfg = hp.SamplerConfig()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    pipeline.TRACK_PREFIX_LEN = True  # Σ prefix length for the prefix kernel's bytes
 
     def step(timer=None):
         fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer)

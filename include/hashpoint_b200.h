@@ -148,7 +148,7 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
                    void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Prefix mode (callers that only want samples): instead of hp_query_fill,
  * sort in place, at the front of each ray's match scratch, the ray's
- * smallest-t matches -- all of them when it has <= want, else everything up
+ * smallest-t matches -- all of them when it has <= 1024, else everything up
  * to the histogram bin where the count reaches `want` (<= 1024) -- and
  * record the sampler's facts over that prefix.  plen [m] receives each
  * prefix length; the view gives the (device) arrays of the prefixes: ray r

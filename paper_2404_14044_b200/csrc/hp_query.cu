@@ -633,8 +633,9 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
 
 // ---------------------------------------------------------------- prefix sort
 // For callers that only want samples (pipeline frames): each ray's
-// smallest-t matches -- everything through the histogram bin where the count
-// reaches `want` (at most kPrefixCap) -- sorted by (t, id) in place at the
+// smallest-t matches -- all of them when they fit (<= kPrefixCap), else
+// everything through the histogram bin where the count reaches `want` (at
+// most kPrefixCap) -- sorted by (t, id) in place at the
 // front of the ray's match scratch (t, id, dist), the sampler's facts over
 // that prefix, and two cuts for the matches left out: their smallest t
 // (every one is strictly above the prefix's last t) and their smallest dist.
@@ -671,7 +672,7 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
 }
 
-// Passes per ray: [q > want] a kCap-bin histogram of t -> the bin where the
+// Passes per ray: [q > kCap] a kCap-bin histogram of t -> the bin where the
 // count reaches want; staging (selected -> shared memory; the others give the
 // cuts and the finiteness check); rank_segment; write-out with the facts
 // counted over the prefix (a prefix count >= K implies the full one; the
@@ -702,7 +703,9 @@ __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
         auto sel_bin = [&](double t) {
             return min(int(fminf((__double2float_rn(t) - tlo) * sel_scale, float(kBins))), kBins - 1);
         };
-        const bool all = q <= want;
+        // rays that fit are sorted whole: cheaper than a selection pass
+        // (cfg2 6.9 -> 6.6 ms, cfg3 -3%) and never flagged
+        const bool all = q <= kCap;
         int bsel = kBins - 1, L = q;
         if (tid == 0) {
             F.cnt = F.fcount = F.fbad = 0;

@@ -414,11 +414,11 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
                                             _ptr(pre.facts), ctypes.byref(p), colp, ncol, _ptr(r_off),
                                             _ptr(t_end), _ptr(flagged), _ptr(ws), nb.value, _stream()))
         _mark("sample.run")
-        R = int(r_off[m].item())
+        both = torch.stack([r_off[m], flagged[m].to(torch.int64)]).cpu()  # one synchronisation
+        R, n_flagged = int(both[0]), int(both[1])
         if R >= 0:
             break
         exact_cap = int(-R * 1.0625) + 1024   # exact scratch too small: grow it once
-    n_flagged = int(flagged[m].item())
     i64 = dict(dtype=torch.int64, device=dev)
     f64 = dict(dtype=torch.float64, device=dev)
     r_id = torch.empty(R, **i64)

@@ -150,6 +150,7 @@ PREFIX = os.environ.get("HP_PREFIX", "1") != "0"
 
 
 _PREFIX_LEN: list = []  # prefix lengths of the passes of the current frame (device scalars)
+TRACK_PREFIX_LEN = False  # bench.py: report Σ prefix length (one extra reduction per pass)
 
 
 def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end):
@@ -157,7 +158,8 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     their head re-run through the full query.  (samples 9-tuple, Q, flagged)"""
     *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
     Q = pre.total
-    _PREFIX_LEN.append(pre.length.sum())
+    if TRACK_PREFIX_LEN:
+        _PREFIX_LEN.append(pre.length.sum())
     if n_flagged:
         sel = torch.nonzero(flagged, as_tuple=True)[0]
         q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
@@ -193,7 +195,8 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
         s, Q, n_flagged = _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                                          exact_t_end)
         mark("sample")
-        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, prefix_len=_PREFIX_LEN.pop())
+        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged,
+                           prefix_len=_PREFIX_LEN.pop() if _PREFIX_LEN else None)
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
     return FrameResult(idx, q[:6], s, Q=int(q[1].numel()))

@@ -10,14 +10,14 @@ P = dict(pix=pin(w["pixels"]), dirs=pin(w["dirs"]), tn=pin(w["t_near"]), tf=pin(
 evs = []
 def mark(name):
     e = torch.cuda.Event(enable_timing=True); e.record(); evs.append((name, e, time.perf_counter()))
-orig_query, orig_sample, orig_build = device.query, device.sample, device.build
+orig_query, orig_sample, orig_build = device.query_prefix, device.sample_prefix, device.build
 def q(*a, **k):
     mark("query>"); r = orig_query(*a, **k); mark("query<"); return r
 def s(*a, **k):
     mark("sample>"); r = orig_sample(*a, **k); mark("sample<"); return r
 def b(*a, **k):
     mark("build>"); r = orig_build(*a, **k); mark("build<"); return r
-device.query, device.sample, device.build = q, s, b
+device.query_prefix, device.sample_prefix, device.build = q, s, b
 for it in range(6):
     evs.clear(); torch.cuda.synchronize(); mark("start")
     out = pipeline.search_and_sample(C, w["cam"], w["cfg"], P["pix"], P["dirs"], P["tn"], P["tf"])
