@@ -205,9 +205,9 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
     cam = ctypes.byref(camera_struct(index.camera)) if footprint else None
     args = (L, cam, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2, _ptr(dirs),
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
-    cap = _QUERY_CAP.get(dev, 0)
-    if cap > 4096 * max(m, 1):  # remembered from a much larger frame: let this one size itself
-        cap = 0
+    # the frame size seen so far, but no more than a generous per-ray guess for
+    # a much smaller query (e.g. the re-run of a frame's flagged rays)
+    cap = min(_QUERY_CAP.get(dev, 0), 16384 * max(m, 1))
     if max_scratch is not None:
         cap = min(cap, int(max_scratch))
     _mark("query.setup")
@@ -226,7 +226,8 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
         cap = int(needed * 1.0625) + 1024
         if max_scratch is not None:
             cap = min(cap, int(max_scratch))
-        _QUERY_CAP[dev] = cap
+        if cap > _QUERY_CAP.get(dev, 0):  # only grow: a small query (e.g. the re-run of a
+            _QUERY_CAP[dev] = cap         # frame's flagged rays) must not shrink the frame's size
     return offsets, probes, scanned, total, ws, nb.value, cap
 
 
@@ -432,30 +433,32 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
     return (r_off, r_id, *outs, r_color, t_end, flagged[:m], n_flagged)
 
 
-def merge_flagged(main, flagged: torch.Tensor, sub):
+def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = None):
     """Splice the full-path samples ``sub`` of the flagged rays into the
     prefix-mode samples ``main`` (both (r_off, r_id, r_t, r_dist, r_udf,
-    r_alpha, r_w, r_color, t_end)); flagged rays hold no candidates in main."""
+    r_alpha, r_w, r_color, t_end)); flagged rays hold no candidates in main.
+    ``sel``: the flagged ray indices if the caller has them already."""
     r_off, *rows, r_color, t_end = main
     s_off, *s_rows, s_color, s_tend = sub
     dev = r_off.device
     m = int(r_off.shape[0]) - 1
-    sel = torch.nonzero(flagged, as_tuple=True)[0]
+    if sel is None:
+        sel = torch.nonzero(flagged, as_tuple=True)[0]
     counts = r_off[1:] - r_off[:-1]
     counts[sel] = s_off[1:] - s_off[:-1]
     off = torch.zeros(m + 1, dtype=torch.int64, device=dev)
     torch.cumsum(counts, 0, out=off[1:])
-    R = int(off[m].item())
+    R_main, R_sub = int(rows[0].shape[0]), int(s_rows[0].shape[0])  # host values: no synchronisation
+    R = R_main + R_sub  # flagged rays hold nothing in main
 
-    def dst(src_off, rays):  # destination row of every source row
+    def dst(src_off, rays, k):  # destination row of every source row
         n = src_off[1:] - src_off[:-1]
-        k = int(src_off[-1].item()) if src_off.numel() > 1 else 0
         ray = torch.repeat_interleave(rays, n, output_size=k)
         pos = torch.arange(k, device=dev) - torch.repeat_interleave(src_off[:-1], n, output_size=k)
         return off[ray] + pos
 
-    d_main = dst(r_off, torch.arange(m, device=dev))
-    d_sub = dst(s_off, sel)
+    d_main = dst(r_off, torch.arange(m, device=dev), R_main)
+    d_sub = dst(s_off, sel, R_sub)
     out = []
     colored = r_color.shape[0] == rows[0].shape[0] and s_color.shape[0] == s_rows[0].shape[0]
     for a, b in zip(rows + [r_color], s_rows + [s_color]):

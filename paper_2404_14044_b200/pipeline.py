@@ -165,7 +165,7 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
         q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
         sub = device.sample(q[0], q[1], q[2], q[3], slopes[sel], sampler_cfg, colors, exact_t_end, facts=q[6])
         del q
-        s = device.merge_flagged(tuple(s), flagged, sub)
+        s = device.merge_flagged(tuple(s), flagged, sub, sel)
     return tuple(s), Q, n_flagged
 
 
