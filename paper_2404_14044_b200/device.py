@@ -207,7 +207,7 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
             _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
     # the frame size seen so far, but no more than a generous per-ray guess for
     # a much smaller query (e.g. the re-run of a frame's flagged rays)
-    cap = min(_QUERY_CAP.get(dev, 0), 16384 * max(m, 1))
+    cap = min(_QUERY_CAP.get(dev, 0), 4096 * max(m, 1))
     if max_scratch is not None:
         cap = min(cap, int(max_scratch))
     _mark("query.setup")
