@@ -24,6 +24,8 @@
  *   hp_sample_run /     _kernels.sample_batch        _kernels.py:552-700
  *   hp_sample_emit        (two-phase for the same reason; R unknown)
  *   hp_primary_surface  derived: first retained candidate per ray
+ *   hp_ray_grid         geometry.ray_grid            geometry.py:289-306
+ *   hp_render           renderer.render_volume / render_knp renderer.py:138-185
  */
 #ifndef HASHPOINT_B200_H
 #define HASHPOINT_B200_H
@@ -243,6 +245,20 @@ int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp_sample_pre
                           int64_t* r_id, double* r_t, double* r_dist, double* r_udf, double* r_alpha,
                           double* r_w, double* r_color, void* workspace, size_t workspace_bytes,
                           hp_stream_t stream);
+
+/* ---------------- render (consumer of the samples) ---------------- */
+/* Colour / depth of each ray's pixel from its retained samples (replaces the
+ * per-ray loops of renderer.render_volume / render_knp, renderer.py:138-185).
+ * mode 0 volume (uses r_alpha, r_color [R,3], t_far), 1 knp (uses r_dist,
+ * r_id, point_colors [n,3], knp_k >= 1).  pixels int64 [m,2] (stride),
+ * background: host double[3].  color [H,W,3] / depth [H,W] are written only
+ * at the rays' pixels (the caller fills the blank image); several rays on
+ * one pixel: the last ray wins.  owner: int32 [H*W] scratch. */
+int hp_render(int mode, const int64_t* r_off, int64_t m, const int64_t* r_id, const double* r_t,
+              const double* r_dist, const double* r_alpha, const double* r_color,
+              const double* point_colors, const int64_t* pixels, int64_t pixel_stride,
+              const double* t_far, int32_t knp_k, const double* background, int64_t width,
+              int64_t height, int32_t* owner, double* color, double* depth, hp_stream_t stream);
 
 /* out2[0] = offsets[m] (total), out2[1] = max_r (offsets[r+1] - offsets[r]).
  * Device int64[2]. */

@@ -69,6 +69,8 @@ _SIGNATURES = {
                                        c_size, ctypes.POINTER(PrefixView), c_p]),
     "hp_ray_grid": (ctypes.c_int, [ctypes.POINTER(Camera), c_i64, c_i64, c_p, c_p, ctypes.c_double,
                                    ctypes.c_double, c_p, c_p, c_p]),
+    "hp_render": (ctypes.c_int, [ctypes.c_int, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
+                                 ctypes.c_int32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p]),
     "hp_query_bounds": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                        c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_size, c_p]),
     "hp_query_fill": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),

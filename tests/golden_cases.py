@@ -90,3 +90,26 @@ def rays_for(camera, t_near, t_far, stride=1):
     dirs, pixels = dirs[::stride], pixels[::stride]
     m = dirs.shape[0]
     return pixels, dirs, np.full(m, t_near), np.full(m, t_far)
+
+
+# render configurations: (tag, mode, background, knp_k, sampler)
+RENDERS = [
+    ("vol", "volume", (0.0, 0.0, 0.0), 8, "default"),
+    ("vol_bg_tau", "volume", (0.2, 0.5, 1.0), 8, "tau"),
+    ("knp", "knp_blend", (0.0, 0.0, 0.0), 8, "default"),
+    ("knp3_bg", "knp_blend", (0.1, 0.1, 0.1), 3, "k3_g05"),
+    ("knp1", "knp_blend", (1.0, 1.0, 1.0), 1, "default"),
+]
+
+
+def render_cases():
+    """Yield (name, cloud, camera, search_config, t_near, t_far, render configs) for the
+    renderer goldens (reference renderer.py:138-192 over generate_rays)."""
+    byname = {c[0]: c for c in cases()}
+    for name in ("small_sphere_surface", "orbit_planes", "dup_planes", "edge_points"):
+        _, cloud, cam, cfg, tn, tf, _, _ = byname[name]
+        yield name, cloud, cam, cfg, tn, tf, RENDERS
+    # constant colour: every hit pixel renders exactly that colour (test_acceptance.py:349-362)
+    _, cloud, cam, cfg, tn, tf, _, _ = byname["small_parallel_planes"]
+    const = PointCloud(cloud.positions, np.tile([0.25, 0.5, 0.75], (cloud.count, 1)))
+    yield "const_planes", const, cam, cfg, tn, tf, RENDERS[:3]
