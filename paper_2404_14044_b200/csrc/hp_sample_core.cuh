@@ -1,6 +1,6 @@
-// hp_sample_core.cuh — the sampler's per-candidate arithmetic, shared by the
-// standalone sampler (hp_sample.cu) and the query sort's fused sampling
-// epilogue (hp_query.cu).  Reference: _kernels.sample_batch
+// hp_sample_core.cuh — the sampler's per-candidate arithmetic (K-nearest
+// search, udf / alpha / colour, bound factors, bound chain) used by the
+// sampler kernels in hp_sample.cu.  Reference: _kernels.sample_batch
 // (_kernels.py:552-700); exactness arguments in DESIGN.md §6.
 #pragma once
 #include <math_constants.h>
@@ -424,14 +424,6 @@ __device__ __forceinline__ bool chain_chunk(Chain& S, double u, int c0, int n, i
     S.Vs = U;
     return S.proved_zero || (!P.exact_t_end && S.je < q);
 }
-
-// One ray's t / ds held in shared memory (sorted), for the fused epilogue.
-struct SmemView {
-    const double* st;
-    const double* sd;
-    __device__ __forceinline__ double t(int i) const { return st[i]; }
-    __device__ __forceinline__ double d(int i) const { return sd[i]; }
-};
 
 }  // namespace
 }  // namespace hp
