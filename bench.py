@@ -403,8 +403,6 @@ def run_ours(args, w, rank, world, dist):
     scfg = hp.SamplerConfig()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    pipeline.TRACK_PREFIX_LEN = True  # Σ prefix length for the prefix kernel's bytes
-
     def step(timer=None):
         fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer)
         if world > 1:
@@ -461,6 +459,10 @@ def run_ours(args, w, rank, world, dist):
 
     # end-to-end through the public host-buffer API (pinned host inputs); at
     # N > 1 every rank runs its band concurrently, max time over ranks
+    # one more (untimed) frame for the prefix kernel's bytes: Σ prefix length
+    pipeline.TRACK_PREFIX_LEN = True
+    plen_fr = step()
+    pipeline.TRACK_PREFIX_LEN = False
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, w, r0, r1, dist)
@@ -487,7 +489,7 @@ def run_ours(args, w, rank, world, dist):
     }
     for k, sel in cls.items():  # read the unsorted matches (20 B), write the CSR (24 B)
         kbytes[k] = 44 * int(qs[sel].sum()) + 24 * int(sel.sum())
-    plen = int(fr.prefix_len.item()) if fr.prefix_len is not None else 0
+    plen = int(plen_fr.prefix_len.item()) if plen_fr.prefix_len is not None else 0
     # prefix mode: read the unsorted matches (20 B), write the sorted heads
     # (t, id32, dist: 20 B), per ray offsets/soff/t-bounds in, length/facts/cuts out
     kbytes["k_query_prefix"] = 20 * q_loc + 20 * plen + 56 * m_loc
@@ -507,7 +509,7 @@ def run_ours(args, w, rank, world, dist):
                    "n_indexed": fr.index.n_in, "Q": Q, "R": R, "P": P,
                    "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"row bands x{world}" if world > 1 else "single GPU",
-                   "ray_chunks": fr.chunks, "prefix_mode": pipeline.PREFIX, "prefix_flagged_rays": fr.flagged,
+                   "ray_chunks": fr.chunks, "prefix_mode": fr.prefix, "prefix_flagged_rays": fr.flagged,
                    "parity_gate": parity},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -518,8 +520,8 @@ def run_ours(args, w, rank, world, dist):
                            # a path that never materialises the query CSR,
                            # reported beside B_frame, not divided by it
                            "b_fused": 24 * n + 64 * fr.index.n_in + 32 * P + 96 * m_total + 48 * R
-                           if fr.query is None and pipeline.PREFIX else None,
-                           "prefix_len": plen if fr.prefix_len is not None else None},
+                           if fr.prefix else None,
+                           "prefix_len": plen if plen_fr.prefix_len is not None else None},
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "kernels_ms": {k: round(v[0], 4) for k, v in sorted(kern.items(), key=lambda x: -x[1][0])},
         "kernels_gbs": {k: round(kbytes[k] / (kern[k][0] / 1e3) / 1e9, 1) for k in kern if k in kbytes

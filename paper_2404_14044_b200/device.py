@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._lib import c_i64, c_size
 
-__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "query_prefix", "sample", "sample_prefix", "merge_flagged", "ray_grid",
+__all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "query_prefix", "query_frame", "sample", "sample_prefix", "merge_flagged", "ray_grid",
            "primary_surface", "MatchBudgetExceeded", "SAMPLE_EXACT_PER_RAY"]
 
 # match-scratch capacity of the last query per device (slots), reused so a
@@ -191,9 +191,11 @@ def query_bounds(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
     return out
 
 
-def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
+def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, long_cut=None):
     """hp_query_count with the workspace sized (retrying once); returns
-    (offsets, probes, scanned, total, workspace, workspace bytes, capacity)."""
+    (offsets, probes, scanned, total, workspace, workspace bytes, capacity,
+    long_total): long_total = the matches of rays with more than ``long_cut``
+    (read with the total, one synchronisation; None without ``long_cut``)."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
     m = int(pixels.shape[0])
@@ -217,7 +219,13 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
         _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap, _ptr(ws),
                                       nb.value, _stream()))
         _mark("query.count")
-        total = int(offsets[m].item())
+        long_total = None
+        if long_cut is not None and m > 0:
+            qd = offsets[1:] - offsets[:-1]
+            both = torch.stack([offsets[m], torch.where(qd > long_cut, qd, 0).sum()]).cpu()
+            total, long_total = int(both[0]), int(both[1])
+        else:
+            total = int(offsets[m].item())
         if total >= 0:
             break
         needed = -total  # scratch too small: nothing was written, grow it once (and remember)
@@ -228,7 +236,7 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
             cap = min(cap, int(max_scratch))
         if cap > _QUERY_CAP.get(dev, 0):  # only grow: a small query (e.g. the re-run of a
             _QUERY_CAP[dev] = cap         # frame's flagged rays) must not shrink the frame's size
-    return offsets, probes, scanned, total, ws, nb.value, cap
+    return offsets, probes, scanned, total, ws, nb.value, cap, long_total
 
 
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
@@ -242,12 +250,17 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
     ``max_scratch`` a frame needing more match slots raises
     :class:`MatchBudgetExceeded` before any CSR is written.
     """
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    return _fill(index, _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch), slopes,
+                 facts)
+
+
+def _fill(index, counted, slopes, facts):
+    """hp_query_fill after :func:`_count`: the (t, id)-sorted CSR."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
-    m = int(pixels.shape[0])
-    pixels, dirs = pixels.contiguous(), dirs.contiguous()
-    offsets, probes, scanned, total, ws, nb, cap = _count(index, pixels, dirs, t_near, t_far, slopes,
-                                                          footprint, max_scratch)
+    offsets, probes, scanned, total, ws, nb, cap, _ = counted
+    m = int(offsets.shape[0]) - 1
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
     d = torch.empty(total, dtype=torch.float64, device=dev)
@@ -291,12 +304,17 @@ def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
                  max_scratch: int | None = None) -> QueryPrefix:
     """The query for callers that only want samples (hp_query_prefix): each
     ray's smallest-t matches sorted in place, no CSR of all matches."""
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    return _prefix(index, _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch), slopes,
+                   want)
+
+
+def _prefix(index, counted, slopes, want=PREFIX_WANT) -> QueryPrefix:
+    """hp_query_prefix after :func:`_count`."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
-    m = int(pixels.shape[0])
-    pixels, dirs = pixels.contiguous(), dirs.contiguous()
-    offsets, probes, scanned, total, ws, nb, cap = _count(index, pixels, dirs, t_near, t_far, slopes,
-                                                          footprint, max_scratch)
+    offsets, probes, scanned, total, ws, nb, cap, _ = counted
+    m = int(offsets.shape[0]) - 1
     fa = torch.empty(m, dtype=torch.int32, device=dev)
     plen = torch.empty(m, dtype=torch.int32, device=dev)
     cut = torch.empty((2, m), dtype=torch.float64, device=dev)
@@ -317,6 +335,27 @@ def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
                       wrap(view.dist, torch.float64, cap), cut[0], cut[1], fa, ws)
     pre.total = total
     return pre
+
+
+# Prefix mode pays off when long rays (more matches than the prefix kernel
+# sorts whole) carry a good share of the frame's matches (cfg2: most; cfg3
+# planes at q <= 1114: almost none, and the size-class sorts are faster there)
+PREFIX_CAP = 1024
+PREFIX_AUTO_SHARE = 0.25
+
+
+def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix: bool | None = None,
+                max_scratch: int | None = None, want: int = PREFIX_WANT):
+    """Count, then either the prefix sort (returns a :class:`QueryPrefix`) or
+    the full CSR with facts (returns the 7-tuple of :func:`query`).
+    ``prefix=None`` decides from the count: prefix mode when rays of more
+    than PREFIX_CAP matches hold more than PREFIX_AUTO_SHARE of them."""
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    c = _count(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch,
+               long_cut=PREFIX_CAP if prefix is None else None)
+    if prefix is None:
+        prefix = c[3] > 0 and c[7] > PREFIX_AUTO_SHARE * c[3]
+    return _prefix(index, c, slopes, want) if prefix else _fill(index, c, slopes, True)
 
 
 def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerParams:

@@ -75,6 +75,7 @@ class FrameResult:
     Q: int = 0
     chunks: int = 1
     flagged: int = 0         # prefix mode: rays re-run through the full query
+    prefix: bool = False     # the frame ran in prefix mode
     prefix_len: object = None  # prefix mode: device tensor, total prefix length (sum over rays)
 
     @property
@@ -144,9 +145,12 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
 
 
 # Frames that only want samples sort each ray's head of matches only
-# (device.query_prefix + device.sample_prefix); rays whose sampling may reach
-# past the head re-run through the full query.  HP_PREFIX=0 turns it off.
-PREFIX = os.environ.get("HP_PREFIX", "1") != "0"
+# (device.query_prefix + device.sample_prefix) when long rays dominate the
+# frame (device.query_frame decides from the counts); rays whose sampling
+# may reach past the head re-run through the full query.
+# HP_PREFIX=1 forces prefix mode, HP_PREFIX=0 turns it off, default: auto.
+_PREFIX_ENV = os.environ.get("HP_PREFIX", "auto")
+PREFIX = None if _PREFIX_ENV == "auto" else _PREFIX_ENV != "0"
 
 
 _PREFIX_LEN: list = []  # prefix lengths of the passes of the current frame (device scalars)
@@ -176,26 +180,28 @@ def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, 
 
 def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
                   mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None) -> FrameResult:
+    """query -> sample of one frame on the device.  ``prefix``: True / False
+    forces the mode, None (default: the HP_PREFIX setting, auto) lets
+    device.query_frame pick it from the counts."""
     prefix = PREFIX if prefix is None else prefix
     budget = int(max_matches) if max_matches is not None else match_budget(
-        bytes_per_match=BYTES_PER_MATCH_PREFIX if prefix else BYTES_PER_MATCH)
+        bytes_per_match=BYTES_PER_MATCH if prefix is False else BYTES_PER_MATCH_PREFIX)
     try:
-        if prefix:
-            pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes, max_scratch=budget)
-        else:
-            q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
+        q = device.query_frame(idx, pixels, dirs, t_near, t_far, slopes, prefix=prefix, max_scratch=budget)
     except device.MatchBudgetExceeded:
+        # too big for one pass: ray chunks (prefix mode unless turned off --
+        # such frames are dominated by long rays)
         before_sample()
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                              exact_t_end, budget, mark, prefix)
+                              exact_t_end, budget, mark, prefix is not False)
     mark("query")
     before_sample()
-    if prefix:
+    if isinstance(q, device.QueryPrefix):
         _PREFIX_LEN.clear()
-        s, Q, n_flagged = _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
+        s, Q, n_flagged = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                                          exact_t_end)
         mark("sample")
-        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged,
+        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, prefix=True,
                            prefix_len=_PREFIX_LEN.pop() if _PREFIX_LEN else None)
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
@@ -232,7 +238,8 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
     mark("sample")
     plen = sum(_PREFIX_LEN) if (prefix and _PREFIX_LEN) else None
     _PREFIX_LEN.clear()
-    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf, prefix_len=plen)
+    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf, prefix=prefix,
+                       prefix_len=plen)
 
 
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
