@@ -173,12 +173,15 @@ def test_degenerate_frames():
 
 
 @pytest.mark.parametrize("name", ["cfg1", "small_sphere_surface", "orbit_planes", "empty"])
-def test_search_and_sample_host_api_matches_goldens(name):
+@pytest.mark.parametrize("mode", [None, True, False])
+def test_search_and_sample_host_api_matches_goldens(name, mode, monkeypatch):
     """The public host-buffer pipeline (numpy in / numpy out, side-stream
-    uploads, host slopes in the library) reproduces the reference goldens."""
+    uploads, host slopes in the library) reproduces the reference goldens in
+    every frame mode (auto, prefix, full CSR)."""
     from paper_2404_14044_b200 import pipeline
     if name not in gu.case_names():
         pytest.skip(f"no golden case {name}")
+    monkeypatch.setattr(pipeline, "PREFIX", mode)
     g = gu.load(name)
     _, cloud, cam, cfg, tn, tf, stride, samplers = gu.get_case(name)
     pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)
