@@ -60,18 +60,21 @@ struct Best {
             if (b < ksel) f(d[b], i[b]);
     }
     // full list (ksel == MAXK): branch-free compare-shift network; the caller
-    // guarantees (nd, ni) < the last entry.
+    // guarantees (nd, ni) < the last entry.  One comparison per slot: keys
+    // are unique (ids differ) and the list is sorted, so lt[b] = (entry b <
+    // new) is true exactly below the insertion point.
     __device__ __forceinline__ void insert_full(double nd, int ni) {
+        bool lt[MAXK];
+#pragma unroll
+        for (int b = 0; b < MAXK; b++) lt[b] = kless(d[b], i[b], nd, ni);
 #pragma unroll
         for (int b = MAXK - 1; b >= 1; --b) {
-            const bool shift = kless(nd, ni, d[b - 1], i[b - 1]);
-            const bool here = !shift && kless(nd, ni, d[b], i[b]);
-            const double db = shift ? d[b - 1] : (here ? nd : d[b]);
-            const int ib = shift ? i[b - 1] : (here ? ni : i[b]);
-            d[b] = db;
-            i[b] = ib;
+            const bool shift = !lt[b - 1];
+            const bool here = lt[b - 1] && !lt[b];
+            d[b] = shift ? d[b - 1] : (here ? nd : d[b]);
+            i[b] = shift ? i[b - 1] : (here ? ni : i[b]);
         }
-        if (kless(nd, ni, d[0], i[0])) {
+        if (!lt[0]) {
             d[0] = nd;
             i[0] = ni;
         }
