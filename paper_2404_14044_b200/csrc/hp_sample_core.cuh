@@ -225,6 +225,11 @@ __device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, boo
                     best.insert_full(d2, i);
                     kd = best.d[kMaxK - 1];
                     ki = best.i[kMaxK - 1];
+                } else if (kMaxK <= 8) {
+                    // small register list: the branch-free network over all
+                    // slots (what it pushes past slot ksel - 1 is never read)
+                    best.insert_full(d2, i);
+                    best.kth(ksel, kd, ki);
                 } else {
                     best.insert(ksel, d2, i);
                     best.kth(ksel, kd, ki);
