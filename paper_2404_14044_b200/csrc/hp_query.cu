@@ -84,25 +84,6 @@ struct QCam {  // camera frame for the footprint (has_cam == 0: full windows)
     int has_cam, width, height;
 };
 
-// cp.async (LDGSTS) helpers: asynchronous global -> shared copies.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = unsigned(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned s = unsigned(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-    const unsigned s = unsigned(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 // Group bounding box (padded coordinates) of rays [r0, r0+G).
 __device__ void group_setup(GroupHead& S, const Rays& R, const QCam& QC, int64_t r0, int G, int s) {
     const int tid = threadIdx.x;

@@ -53,6 +53,12 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef HP_PLAN_CPASYNC
+#define HP_PLAN_CPASYNC 1
+#endif
+// plan ring: the last 64 candidates (bound factors, K <= 32), + two chunks
+// in flight with cp.async
+constexpr int kRing = HP_PLAN_CPASYNC ? 128 : 64;
 
 // Path counters: rays, fast rays, proved-zero rays, exact evaluations,
 // candidates, bound evaluations.  Read with hp_sample_debug_counters().
@@ -181,23 +187,45 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     if (fast) {
         Chain S;
         S.je = q;
+#if HP_PLAN_CPASYNC
+        // the ring is filled by cp.async two chunks ahead (no registers held
+        // across the chunk; the chunk's own work does not cover a DRAM trip)
+        auto fetch = [&](int c) {
+            const int jj = c + lane;
+            if (P.K <= 32 && jj < q) {
+                cp_async8(&rt[jj & (kRing - 1)], T + jj);
+                cp_async8(&rd[jj & (kRing - 1)], DS + jj);
+            }
+            cp_commit();
+        };
+        fetch(0);
+        fetch(32);
+#else
         // this lane's (t, ds) of the current chunk, loaded one chunk ahead
         double tn = lane < q ? ldg(T + lane) : 0.0, dn = lane < q ? ldg(DS + lane) : 0.0;
+#endif
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
             double u = 1.0;
             if (P.K <= 32) {
+#if HP_PLAN_CPASYNC
+                cp_wait<1>();  // chunk c0 has landed
+                __syncwarp();
+                const double tj = j < q ? rt[j & (kRing - 1)] : 0.0;
+                fetch(c0 + 64);  // its slots are outside this chunk's and the next one's windows
+#else
                 const double tj = tn, dj = dn;
                 const int jn = j + 32;
                 tn = jn < q ? ldg(T + jn) : 0.0;
                 dn = jn < q ? ldg(DS + jn) : 0.0;
                 __syncwarp();
-                rt[j & 63] = tj;
-                rd[j & 63] = dj;
+                rt[j & (kRing - 1)] = tj;
+                rd[j & (kRing - 1)] = dj;
                 __syncwarp();
+#endif
                 if (j < q) {
                     u = (j >= P.K - 1 || c0 + 32 >= min(q, P.K))
-                            ? bound_factor_ring(rt, rd, q, j, tj, jstar, slope, P)
+                            ? bound_factor_ring<kRing>(rt, rd, q, j, tj, jstar, slope, P)
                             : -1.0;
                     if (u < 0.0) u = bound_factor(V, q, j, jstar, slope, P);
                 }
@@ -207,6 +235,10 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
             nbound += 32;
             if (chain_chunk(S, u, c0, min(32, q - c0), q, thr, P)) break;
         }
+#if HP_PLAN_CPASYNC
+        cp_wait<0>();  // nothing may land in the ring once the next ray uses it
+        __syncwarp();
+#endif
         je = S.je;
         proved_zero = S.proved_zero;
     }
@@ -224,7 +256,7 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
 
 __global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan,
                                                           int64_t* __restrict__ ecnt) {
-    __shared__ double ring[kWarps][2][64];  // last 64 candidates' t / ds per warp
+    __shared__ double ring[kWarps][2][kRing];  // recent candidates' t / ds per warp
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
         plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1]);

@@ -333,6 +333,7 @@ __device__ double bound_factor(const View& V, int q, int j, int jstar, double sl
 // candidates (K <= 32): the ksel candidates ending at j (or [0, ksel) for
 // j < ksel - 1).  Returns a negative value when a member is not in j's pool
 // (the caller then uses bound_factor).
+template <int kRingSize>
 __device__ __forceinline__ double bound_factor_ring(const double* rt, const double* rd, int q, int j, double tj,
                                                     int jstar, double slope, const Params& P) {
     const bool use_el = j >= jstar;
@@ -342,7 +343,7 @@ __device__ __forceinline__ double bound_factor_ring(const double* rt, const doub
     double sum = 0.0;
     bool ok = true;
     for (int k = 0; k < ksel; k++) {
-        const int i = (i0 + k) & 63;
+        const int i = (i0 + k) & (kRingSize - 1);
         const double di = rd[i];
         ok &= !(use_el && di > rj);
         sum = dadd(sum, dadd(fabs(dsub(rt[i], tj)), di));
