@@ -56,9 +56,12 @@ constexpr int kWarps = kThreads / 32;
 #ifndef HP_PLAN_CPASYNC
 #define HP_PLAN_CPASYNC 1
 #endif
-// plan ring: the last 64 candidates (bound factors, K <= 32), + two chunks
-// in flight with cp.async
-constexpr int kRing = HP_PLAN_CPASYNC ? 128 : 64;
+#ifndef HP_PLAN_AHEAD
+#define HP_PLAN_AHEAD 2  // chunks in flight
+#endif
+// plan ring: the last 64 candidates (bound factors, K <= 32) + the chunks in
+// flight with cp.async
+constexpr int kRing = HP_PLAN_CPASYNC ? (HP_PLAN_AHEAD <= 2 ? 128 : 256) : 64;
 
 // Path counters: rays, fast rays, proved-zero rays, exact evaluations,
 // candidates, bound evaluations.  Read with hp_sample_debug_counters().
@@ -198,8 +201,8 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
             }
             cp_commit();
         };
-        fetch(0);
-        fetch(32);
+#pragma unroll
+        for (int a = 0; a < HP_PLAN_AHEAD; a++) fetch(32 * a);
 #else
         // this lane's (t, ds) of the current chunk, loaded one chunk ahead
         double tn = lane < q ? ldg(T + lane) : 0.0, dn = lane < q ? ldg(DS + lane) : 0.0;
@@ -209,10 +212,10 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
             double u = 1.0;
             if (P.K <= 32) {
 #if HP_PLAN_CPASYNC
-                cp_wait<1>();  // chunk c0 has landed
+                cp_wait<HP_PLAN_AHEAD - 1>();  // chunk c0 has landed
                 __syncwarp();
                 const double tj = j < q ? rt[j & (kRing - 1)] : 0.0;
-                fetch(c0 + 64);  // its slots are outside this chunk's and the next one's windows
+                fetch(c0 + 32 * HP_PLAN_AHEAD);  // its slots are outside the windows still to be read
 #else
                 const double tj = tn, dj = dn;
                 const int jn = j + 32;
