@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
 #define HP_PREFIX_U 2
 #endif
 #ifndef HP_PREFIX_MINB
-#define HP_PREFIX_MINB 0
+#define HP_PREFIX_MINB 6  // 40 registers: 6 CTAs per SM (the shared-memory limit)
 #endif
 constexpr int kPrefixCap = 1024;
 constexpr int kPrefixThreads = 256;
@@ -712,7 +712,16 @@ __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
                 }
             }
         };
-        if (single) load_chunk(0, true);
+        if (all) {  // the whole segment straight into shared memory, every load in flight
+            for (int e = tid; e < q; e += kT) {
+                cp_async8(&F.t[e], st + so + e);
+                cp_async4(&F.id[e], sid + so + e);
+                cp_async8(&F.d2[e], sd + so + e);
+            }
+            cp_commit();
+        } else if (single) {
+            load_chunk(0, true);
+        }
         if (!all) {
             for (int k = tid; k <= kBins; k += kT) F.hist[k] = 0;
             if (tid == 0) F.bsel = kBins;
@@ -743,12 +752,19 @@ __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
             }
         }
         for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
+        cp_wait<0>();
         __syncthreads();
         // stage the selected matches (the smallest L by t); the others give
         // the cuts; every value is checked finite
         bool bad = false;
         unsigned long long kt = ~0ull, kd = ~0ull;
-        for (int c0 = 0; c0 < q; c0 += kChunk) {
+        if (all) {
+            for (int e = tid; e < q; e += kT) {
+                const double te = F.t[e], d2 = F.d2[e];
+                bad |= !(fabs(te) <= DBL_MAX) || !(d2 >= 0.0) || !(d2 <= DBL_MAX);
+            }
+        }
+        for (int c0 = 0; c0 < (all ? 0 : q); c0 += kChunk) {
             if (!single) load_chunk(c0, true);
 #pragma unroll
             for (int u = 0; u < kU; u++) {
