@@ -93,7 +93,7 @@ def run_views(args, rank, world, dist):
     import torch
 
     import paper_2404_14044_b200 as hp
-    from paper_2404_14044_b200 import pipeline
+    from paper_2404_14044_b200 import _lib, pipeline
     dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     cloud, views = make_views(args.views)
@@ -115,7 +115,9 @@ def run_views(args, rank, world, dist):
 
     for _ in range(args.warmup):
         step()
-    times = []
+    times, kern_tot = [], {}
+    _lib.timing_enable(True)
+    _lib.timing_collect()
     smi = ClockSampler(dev.index)
     with smi:
         for _ in range(args.steps):
@@ -129,6 +131,10 @@ def run_views(args, rank, world, dist):
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+            for k, (v, c) in _lib.timing_collect().items():
+                a0, b0 = kern_tot.get(k, (0.0, 0))
+                kern_tot[k] = (a0 + v, b0 + c)
+    _lib.timing_enable(False)
     ms = statistics.mean(times)
     qr = (Q, R)
     if dist is not None:
@@ -153,6 +159,7 @@ def run_views(args, rank, world, dist):
                    "rays": m_total, "views": len(views), "Q": qr[0], "R": qr[1],
                    "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"views x{world}" if world > 1 else "single GPU"},
+        "kernels_ms": {k: round(v / args.steps, 3) for k, (v, _) in sorted(kern_tot.items(), key=lambda x: -x[1][0])},
         "clocks": smi.summary(),
     }
     print(json.dumps(line), flush=True)
