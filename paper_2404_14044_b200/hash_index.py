@@ -148,8 +148,10 @@ def build(points: PointCloud, camera: Camera, config: SearchConfig) -> HashIndex
     if max(camera.width + 2 * pad, camera.height + 2 * pad) > 0xFFFF:
         raise ValueError("padded image exceeds 16-bit pixel coordinates")
     _lib.load(require_device=True)
-    xyz = torch.from_numpy(np.ascontiguousarray(points.positions, dtype=np.float64))
-    dev = device.build(xyz.to(_device(), non_blocking=False), camera, pad)
+    pos = np.ascontiguousarray(points.positions, dtype=np.float64)
+    if not pos.flags.writeable:  # frozen cloud arrays: torch wants a writable buffer to wrap
+        pos = pos.copy()
+    dev = device.build(torch.from_numpy(pos).to(_device(), non_blocking=False), camera, pad)
     return HashIndex(points, camera, config, dev)
 
 

@@ -112,3 +112,39 @@ def test_volume_sample_weights_host_helper():
         RenderConfig(knp_k=0)
     with pytest.raises(ValueError):
         RenderConfig(background=(2.0, 0.0, 0.0))
+
+
+@pytest.mark.gpu
+def test_c8_renderer_consistency_on_device():
+    """Reference acceptance C8 (test_acceptance.py:321-366) through the device
+    renderer: with every candidate kept (epsilon = 0) the density-derived
+    volume weights reproduce the sampler's occlusion weights, so a constant-
+    colour scene on a black background renders to (sum of the ray's sampler
+    weights) x colour within 1e-9; knp blending renders that colour exactly."""
+    import paper_2404_14044_b200 as hp
+    from paper_2404_14044_b200 import renderer
+    from paper_2404_14044_b200.cloud import PointCloud
+    from paper_2404_14044_b200.hash_index import _pack_rays
+    colour = np.array([0.3, 0.6, 0.9])
+    base = hp.generate_scene(hp.SceneSpec("parallel_planes", n=9000, seed=13, plane_count=2, plane_gap=0.8,
+                                          noise=0.15))
+    cloud = PointCloud(base.positions, np.tile(colour, (base.count, 1)))
+    cam = hp.scene_camera(40, 30, fov_deg=35)
+    cfg = hp.SearchConfig.for_camera(cam, scale=2.0)
+    index = hp.build(cloud, cam, cfg)
+    rays = hp.generate_rays(cam, 1.0, 10.0)
+    sc = hp.SamplerConfig(epsilon=0.0)
+    img = renderer.render_volume(index, rays, cfg, sc, renderer.RenderConfig(mode="volume"))
+    pixels, dirs, tn, tf = _pack_rays(rays)
+    q = hp.query_batch_arrays(index, pixels, dirs, tn, tf, cfg)
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius, cfg.use_approx_radius)
+    s = hp.sample_batch_arrays(q[0], q[1], q[2], q[3], slopes, sc)
+    r_off, r_w = s[0], s[6]
+    wsum = np.array([r_w[r_off[i]:r_off[i + 1]].sum() for i in range(len(rays))])
+    hit = np.diff(r_off) > 0
+    assert hit.sum() > 500
+    got = img.color[pixels[:, 1], pixels[:, 0]]
+    np.testing.assert_allclose(got, wsum[:, None] * colour, rtol=0, atol=1e-9)
+    knp = renderer.render_knp(index, rays, cfg, sc)
+    np.testing.assert_allclose(knp.color[pixels[hit, 1], pixels[hit, 0]], np.tile(colour, (hit.sum(), 1)),
+                               rtol=0, atol=1e-6)
