@@ -631,6 +631,84 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
 constexpr int kPrefixCap = 1024;
 constexpr int kPrefixThreads = 256;
 
+#ifndef HP_PREFIX_SELECT
+#define HP_PREFIX_SELECT 1  // selection histograms of long rays in a separate warp-per-ray pass
+#endif
+
+// The selection map of a ray (shared by k_prefix_select and k_query_prefix:
+// the same float operations, so both see the same bins).
+struct SelMap {
+    float tlo, scale;
+    __device__ __forceinline__ SelMap(uint2 mm, int bins) {
+        tlo = from_fkey(mm.x);
+        const float span = from_fkey(mm.y) - tlo;
+        scale = span > 0.0f ? fminf(float(bins) / span, FLT_MAX) : 0.0f;
+    }
+    __device__ __forceinline__ int bin(double t, int bins) const {
+        return min(int(fminf((__double2float_rn(t) - tlo) * scale, float(bins))), bins - 1);
+    }
+};
+
+// Selection of the long rays (more than kCap matches), one warp per ray
+// (many rays in flight: this pass is a plain stream over t): a kBins-bin
+// histogram of t -> the first bin where the running count reaches want
+// (the one before it if that bin alone overflows kCap), and the count up
+// to it.  sel[r] = (bin, count).
+template <int kBins, int kCap>
+__global__ void __launch_bounds__(128) k_prefix_select(const int64_t* __restrict__ off,
+                                                       const int64_t* __restrict__ soff,
+                                                       const uint2* __restrict__ tmm, int64_t m, int want,
+                                                       const double* __restrict__ st, int2* __restrict__ sel) {
+    __shared__ int hist[4][kBins];
+    int* H = hist[warp_id()];
+    const int lane = lane_id();
+    const int64_t warps = int64_t(gridDim.x) * 4;
+    for (int64_t r = int64_t(blockIdx.x) * 4 + warp_id(); r < m; r += warps) {
+        const int q = int(off[r + 1] - off[r]);
+        if (q <= kCap) continue;
+        const int64_t so = soff[r];
+        const SelMap M(tmm[r], kBins);
+        for (int k = lane; k < kBins; k += 32) H[k] = 0;
+        __syncwarp();
+        for (int e0 = 0; e0 < q; e0 += 128) {  // four loads per lane in flight
+            double tv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * 32 + lane;
+                tv[u] = e < q ? st[so + e] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (e0 + u * 32 + lane < q) atomicAdd(&H[M.bin(tv[u], kBins)], 1);
+        }
+        __syncwarp();
+        constexpr int kPer = kBins / 32;  // lane owns bins [lane * kPer, lane * kPer + kPer)
+        int sum = 0;
+#pragma unroll 8
+        for (int k = 0; k < kPer; k++) sum += H[lane * kPer + k];
+        const int incl = warp_incl_scan(sum);
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= want);
+        const int owner = __ffs(hit) - 1;  // exists: the total q > kCap >= want
+        if (lane == owner) {
+            int c = incl - sum, b = lane * kPer;
+            for (int k = 0; k < kPer; k++) {
+                c += H[lane * kPer + k];
+                if (c >= want) {
+                    b = lane * kPer + k;
+                    break;
+                }
+            }
+            int L = c;
+            if (L > kCap) {  // that bin alone overflows: stop before it
+                L -= H[b];
+                b -= 1;
+            }
+            sel[r] = make_int2(b, L);
+        }
+        __syncwarp();
+    }
+}
+
 template <int kCap>
 struct PrefixSmem {
     double t[kCap];
@@ -662,7 +740,8 @@ template <int kCap, int kT>
 __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
     const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm, int64_t m,
     int want, const double* __restrict__ slopes, int* __restrict__ facts, int* __restrict__ plen,
-    double* __restrict__ cut_t, double* __restrict__ cut_d, double* st, int* sid, double* sd) {
+    double* __restrict__ cut_t, double* __restrict__ cut_d, double* st, int* sid, double* sd,
+    const int2* __restrict__ sel) {
     extern __shared__ __align__(16) unsigned char dyn[];
     PrefixSmem<kCap>& F = *reinterpret_cast<PrefixSmem<kCap>*>(dyn);
     constexpr int kBins = kCap;
@@ -679,11 +758,9 @@ __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
             continue;
         }
         const float tlo = from_fkey(tmm[r].x), thi = from_fkey(tmm[r].y);
-        const float span = thi - tlo;
-        const float sel_scale = span > 0.0f ? fminf(float(kBins) / span, FLT_MAX) : 0.0f;
-        auto sel_bin = [&](double t) {
-            return min(int(fminf((__double2float_rn(t) - tlo) * sel_scale, float(kBins))), kBins - 1);
-        };
+        const SelMap M(tmm[r], kBins);
+        const float sel_scale = M.scale;
+        auto sel_bin = [&](double t) { return M.bin(t, kBins); };
         // rays that fit are sorted whole: cheaper than a selection pass
         // (cfg2 6.9 -> 6.6 ms, cfg3 -3%) and never flagged
         const bool all = q <= kCap;
@@ -722,7 +799,11 @@ __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
         } else if (single) {
             load_chunk(0, true);
         }
-        if (!all) {
+        if (!all && sel) {  // selected by k_prefix_select
+            const int2 sv = sel[r];
+            bsel = sv.x;
+            L = sv.y;
+        } else if (!all) {
             for (int k = tid; k <= kBins; k += kT) F.hist[k] = 0;
             if (tid == 0) F.bsel = kBins;
             __syncthreads();
@@ -1278,10 +1359,21 @@ extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, 
         set_smem(kern, sizeof(PrefixSmem<kPrefixCap>));
         return resident(kern, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>));
     }();
+    int2* sel = nullptr;
+#if HP_PREFIX_SELECT
+    sel = reinterpret_cast<int2*>(w.lists);  // (unused by prefix mode otherwise; >= 2m ints)
+    {
+        constexpr auto kselect = k_prefix_select<kPrefixCap, kPrefixCap>;
+        static const int occ_sel = resident(kselect, 128, 0);  // once (thread-safe)
+        TimedSpan tss("k_prefix_select", s);
+        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.tmm, m, want, w.st, sel);
+        HP_CHECK_LAUNCH("k_prefix_select");
+    }
+#endif
     TimedSpan ts("k_query_prefix", s);
     kern<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
                                                                              facts, plen, cut_t, cut_d, w.st, w.sid,
-                                                                             w.sd);
+                                                                             w.sd, sel);
     HP_CHECK_LAUNCH("k_query_prefix");
     return HP_OK;
 }
