@@ -731,11 +731,13 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
 }
 
-// Passes per ray: [q > kCap] a kCap-bin histogram of t -> the bin where the
-// count reaches want; staging (selected -> shared memory; the others give the
-// cuts and the finiteness check); rank_segment; write-out with the facts
-// counted over the prefix (a prefix count >= K implies the full one; the
-// sampler checks the cuts before trusting a smaller one).
+// Per ray (one CTA): a ray of <= kCap matches is staged whole with cp.async;
+// a longer one gets its selected bin from k_prefix_select (sel; without it,
+// a kCap-bin histogram pass here) and is staged through registers (selected
+// -> shared memory; the others give the cuts and the finiteness check);
+// then rank_segment and the write-out, in place, with the facts counted over
+// the prefix (a prefix count >= K implies the full one; the sampler checks
+// the cuts before trusting a smaller one).
 template <int kCap, int kT>
 __global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
     const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm, int64_t m,
