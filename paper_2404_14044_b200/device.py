@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import c_i64, c_size
+from ._lib import c_size
 
 __all__ = ["DeviceIndex", "build", "build_from_table", "query", "query_bounds", "query_prefix", "query_frame", "sample", "sample_prefix", "merge_flagged", "ray_grid",
            "primary_surface", "MatchBudgetExceeded", "SAMPLE_EXACT_PER_RAY"]

@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import device, pipeline
-from .geometry import Ray, SearchConfig, radius_slopes
+from .geometry import SearchConfig, radius_slopes
 from .hash_index import HashIndex, _check_config, _check_rays, _pack_rays
 from .sampler import SamplerConfig
 
