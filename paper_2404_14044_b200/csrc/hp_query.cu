@@ -709,6 +709,41 @@ __global__ void __launch_bounds__(128) k_prefix_select(const int64_t* __restrict
     }
 }
 
+#ifndef HP_PREFIX_SMALL
+#define HP_PREFIX_SMALL 1  // rays of <= kPrefixSmall matches go to a smaller, denser CTA configuration
+#endif
+constexpr int kPrefixSmall = 512;
+
+// Prefix-mode ray classes: list 0 = rays of 1..kSmall matches, list 1 = the
+// longer ones (warp-aggregated appends); empty rays get their outputs here.
+template <int kSmall>
+__global__ void k_prefix_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
+                                 int* __restrict__ counts, int* __restrict__ plen, int* __restrict__ facts,
+                                 double* __restrict__ cut_t, double* __restrict__ cut_d) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        int cls = -1;
+        if (r < m) {
+            const int64_t q = off[r + 1] - off[r];
+            cls = q == 0 ? -1 : (q <= kSmall ? 0 : 1);
+            if (q == 0) {
+                plen[r] = 0;
+                facts[r] = -1;
+                cut_t[r] = cut_d[r] = CUDART_INF;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            const unsigned b = __ballot_sync(0xffffffffu, cls == c);
+            if (!b) continue;
+            int base = 0;
+            if (lane_id() == __ffs(b) - 1) base = atomicAdd(&counts[c], __popc(b));
+            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+            if (cls == c) lists[int64_t(c) * m + base + __popc(b & ((1u << lane_id()) - 1))] = int(r);
+        }
+    }
+}
+
 template <int kCap>
 struct PrefixSmem {
     double t[kCap];
@@ -739,16 +774,18 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 // the prefix (a prefix count >= K implies the full one; the sampler checks
 // the cuts before trusting a smaller one).
 template <int kCap, int kT>
-__global__ void __launch_bounds__(kT, HP_PREFIX_MINB) k_query_prefix(
+__global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_PREFIX_MINB) k_query_prefix(
     const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm, int64_t m,
     int want, const double* __restrict__ slopes, int* __restrict__ facts, int* __restrict__ plen,
     double* __restrict__ cut_t, double* __restrict__ cut_d, double* st, int* sid, double* sd,
-    const int2* __restrict__ sel) {
+    const int2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n) {
     extern __shared__ __align__(16) unsigned char dyn[];
     PrefixSmem<kCap>& F = *reinterpret_cast<PrefixSmem<kCap>*>(dyn);
     constexpr int kBins = kCap;
     const int tid = threadIdx.x;
-    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+    const int64_t nr = list ? int64_t(*list_n) : m;  // this launch's rays (a class list, or all)
+    for (int64_t k = blockIdx.x; k < nr; k += gridDim.x) {
+        const int64_t r = list ? int64_t(list[k]) : k;
         const int64_t so = soff[r];
         const int q = int(off[r + 1] - off[r]);
         if (q == 0) {
@@ -1372,10 +1409,39 @@ extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, 
         HP_CHECK_LAUNCH("k_prefix_select");
     }
 #endif
+    const int* list_small = nullptr;
+    const int* list_big = nullptr;
+    const int* n_small = nullptr;
+    const int* n_big = nullptr;
+#if HP_PREFIX_SMALL
+    {
+        int* lists = w.lists + 2 * m;  // after sel (2m ints); the region holds 5m
+        if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "hp_query_prefix memset");
+        k_prefix_classes<kPrefixSmall><<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, w.counts, plen, facts,
+                                                                        cut_t, cut_d);
+        HP_CHECK_LAUNCH("k_prefix_classes");
+        list_small = lists;
+        list_big = lists + m;
+        n_small = w.counts;
+        n_big = w.counts + 1;
+    }
+    constexpr auto ksmall = k_query_prefix<kPrefixSmall, 128>;
+    static const int occ_small = [] {  // once (thread-safe)
+        set_smem(ksmall, sizeof(PrefixSmem<kPrefixSmall>));
+        return resident(ksmall, 128, sizeof(PrefixSmem<kPrefixSmall>));
+    }();
+#endif
     TimedSpan ts("k_query_prefix", s);
+#if HP_PREFIX_SMALL
+    ksmall<<<kNumSMs * occ_small, 128, sizeof(PrefixSmem<kPrefixSmall>), s>>>(
+        offsets, w.soff, w.tmm, m, want, slopes, facts, plen, cut_t, cut_d, w.st, w.sid, w.sd, nullptr, list_small,
+        n_small);
+    HP_CHECK_LAUNCH("k_query_prefix small");
+#endif
     kern<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
                                                                              facts, plen, cut_t, cut_d, w.st, w.sid,
-                                                                             w.sd, sel);
+                                                                             w.sd, sel, list_big, n_big);
     HP_CHECK_LAUNCH("k_query_prefix");
     return HP_OK;
 }
