@@ -21,7 +21,7 @@ SPANS = {
     "k_query_sort": ["k_query_sort<1024, 256>", "k_query_sort<2048, 512>"],
     "k_query_sort_large": ["k_query_sort<4096, 512>", "k_query_sort<8192, 1024>", "k_query_split",
                            "k_query_sort_parts<8192, 1024>"],
-    "k_query_prefix": ["k_query_prefix<1024, 256>"],
+    "k_query_prefix": ["k_query_prefix<512, 128>", "k_query_prefix<1024, 256>"],
     "k_prefix_select": ["k_prefix_select<1024, 1024>"],
     "k_sample_plan": ["k_sample_plan"],
     "k_sample_exact": ["k_sample_exact"],
