@@ -631,10 +631,6 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
 constexpr int kPrefixCap = 1024;
 constexpr int kPrefixThreads = 256;
 
-#ifndef HP_PREFIX_SELECT
-#define HP_PREFIX_SELECT 1  // selection histograms of long rays in a separate warp-per-ray pass
-#endif
-
 // The selection map of a ray (shared by k_prefix_select and k_query_prefix:
 // the same float operations, so both see the same bins).
 struct SelMap {
@@ -658,12 +654,15 @@ template <int kBins, int kCap>
 __global__ void __launch_bounds__(128) k_prefix_select(const int64_t* __restrict__ off,
                                                        const int64_t* __restrict__ soff,
                                                        const uint2* __restrict__ tmm, int64_t m, int want,
-                                                       const double* __restrict__ st, int2* __restrict__ sel) {
+                                                       const double* __restrict__ st, int2* __restrict__ sel,
+                                                       const int* __restrict__ list, const int* __restrict__ list_n) {
     __shared__ int hist[4][kBins];
     int* H = hist[warp_id()];
     const int lane = lane_id();
     const int64_t warps = int64_t(gridDim.x) * 4;
-    for (int64_t r = int64_t(blockIdx.x) * 4 + warp_id(); r < m; r += warps) {
+    const int64_t nr = list ? int64_t(*list_n) : m;  // candidate rays (a class list, or all)
+    for (int64_t k = int64_t(blockIdx.x) * 4 + warp_id(); k < nr; k += warps) {
+        const int64_t r = list ? int64_t(list[k]) : k;
         const int q = int(off[r + 1] - off[r]);
         if (q <= kCap) continue;
         const int64_t so = soff[r];
@@ -709,10 +708,7 @@ __global__ void __launch_bounds__(128) k_prefix_select(const int64_t* __restrict
     }
 }
 
-#ifndef HP_PREFIX_SMALL
-#define HP_PREFIX_SMALL 1  // rays of <= kPrefixSmall matches go to a smaller, denser CTA configuration
-#endif
-constexpr int kPrefixSmall = 512;
+constexpr int kPrefixSmall = 512;  // rays up to this go to a smaller, denser CTA configuration
 
 // Prefix-mode ray classes: list 0 = rays of 1..kSmall matches, list 1 = the
 // longer ones (warp-aggregated appends); empty rays get their outputs here.
@@ -1398,50 +1394,39 @@ extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, 
         set_smem(kern, sizeof(PrefixSmem<kPrefixCap>));
         return resident(kern, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>));
     }();
-    int2* sel = nullptr;
-#if HP_PREFIX_SELECT
-    sel = reinterpret_cast<int2*>(w.lists);  // (unused by prefix mode otherwise; >= 2m ints)
+    // classes: rays of 1..kPrefixSmall matches / longer ones (the empty rays'
+    // outputs are written here)
+    int* lists = w.lists + 2 * m;  // after sel (2m ints); the region holds 5m
+    const int* list_small = lists;
+    const int* list_big = lists + m;
+    if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_query_prefix memset");
+    k_prefix_classes<kPrefixSmall><<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, w.counts, plen, facts, cut_t,
+                                                                    cut_d);
+    HP_CHECK_LAUNCH("k_prefix_classes");
+    // the selected bin of every ray longer than kPrefixCap (warp per ray)
+    int2* sel = reinterpret_cast<int2*>(w.lists);  // (unused by prefix mode otherwise; 2m ints)
     {
         constexpr auto kselect = k_prefix_select<kPrefixCap, kPrefixCap>;
         static const int occ_sel = resident(kselect, 128, 0);  // once (thread-safe)
         TimedSpan tss("k_prefix_select", s);
-        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.tmm, m, want, w.st, sel);
+        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.tmm, m, want, w.st, sel, list_big,
+                                                  w.counts + 1);
         HP_CHECK_LAUNCH("k_prefix_select");
-    }
-#endif
-    const int* list_small = nullptr;
-    const int* list_big = nullptr;
-    const int* n_small = nullptr;
-    const int* n_big = nullptr;
-#if HP_PREFIX_SMALL
-    {
-        int* lists = w.lists + 2 * m;  // after sel (2m ints); the region holds 5m
-        if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
-            return cuda_status(cudaGetLastError(), "hp_query_prefix memset");
-        k_prefix_classes<kPrefixSmall><<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, w.counts, plen, facts,
-                                                                        cut_t, cut_d);
-        HP_CHECK_LAUNCH("k_prefix_classes");
-        list_small = lists;
-        list_big = lists + m;
-        n_small = w.counts;
-        n_big = w.counts + 1;
     }
     constexpr auto ksmall = k_query_prefix<kPrefixSmall, 128>;
     static const int occ_small = [] {  // once (thread-safe)
         set_smem(ksmall, sizeof(PrefixSmem<kPrefixSmall>));
         return resident(ksmall, 128, sizeof(PrefixSmem<kPrefixSmall>));
     }();
-#endif
     TimedSpan ts("k_query_prefix", s);
-#if HP_PREFIX_SMALL
     ksmall<<<kNumSMs * occ_small, 128, sizeof(PrefixSmem<kPrefixSmall>), s>>>(
         offsets, w.soff, w.tmm, m, want, slopes, facts, plen, cut_t, cut_d, w.st, w.sid, w.sd, nullptr, list_small,
-        n_small);
+        w.counts);
     HP_CHECK_LAUNCH("k_query_prefix small");
-#endif
     kern<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
                                                                              facts, plen, cut_t, cut_d, w.st, w.sid,
-                                                                             w.sd, sel, list_big, n_big);
+                                                                             w.sd, sel, list_big, w.counts + 1);
     HP_CHECK_LAUNCH("k_query_prefix");
     return HP_OK;
 }
