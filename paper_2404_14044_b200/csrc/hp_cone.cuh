@@ -71,7 +71,13 @@ HP_HD bool cone_test(double p0, double p1, double p2, const RayParams& r,
 // band eps = e * max(1, slope) + 2^-22 * t_far bounds |t32 - t64| and the
 // error of the fp32 perpendicular distance (derivation in DESIGN.md).
 // Returns 0 = reject, 1 = accept, 2 = decide in fp64.
-HP_HD int cone_filter(const float4 P, const RayParams& r) {
+// The filter's float terms of a ray (held in registers across a run of slots).
+struct RayF {
+    float f0, f1, f2, ftn, ftf, fslope, eps_ray, smax;
+};
+HP_HD RayF ray_f(const RayParams& r) { return RayF{r.f0, r.f1, r.f2, r.ftn, r.ftf, r.fslope, r.eps_ray, r.smax}; }
+
+HP_HD int cone_filter(const float4 P, const RayF& r) {
     const float eps = fmaf(P.w, r.smax, r.eps_ray);
     const float t = fmaf(P.z, r.f2, fmaf(P.y, r.f1, P.x * r.f0));
     if (t < r.ftn - eps || t > r.ftf + eps) return 0;
@@ -85,6 +91,7 @@ HP_HD int cone_filter(const float4 P, const RayParams& r) {
     if (t_in && lo > 0.0f && d2 < lo * lo * (1.0f - 0x1p-20f)) return 1;
     return 2;
 }
+HP_HD int cone_filter(const float4 P, const RayParams& r) { return cone_filter(P, ray_f(r)); }
 
 
 // Ray parameters derived once per ray (float copies, filter band terms).

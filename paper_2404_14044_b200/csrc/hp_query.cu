@@ -126,9 +126,9 @@ __device__ void group_setup(GroupHead& S, const Rays& R, const QCam& QC, int64_t
 // ray's total added to `scanned` via tab(g, hi - lo)), then the batch's
 // chunks (row, [c0, c1)) are staged with cp.async into alternating buffers:
 // chunk i+1 is in flight while chunk i is tested.  issue(buf, c0, c1) issues
-// the copies of slots [c0, c1); test(buf, row, g, k, c0) runs on the warp
-// owning ray g (warp w owns rays w, w+8, ...), 32 slots at a time, with
-// k = -1 for lanes beyond the ray's sub-range.
+// the copies of slots [c0, c1); test(buf, g, lo, hi, c0) runs on the warp
+// owning ray g (warp w owns rays w, w+8, ...) over the ray's non-empty slot
+// sub-range [lo, hi) of the chunk staged at c0.
 template <int kStage, class Issue, class Test, class Tab, class Done>
 __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64_t wp, int s, const QCam& QC,
                              Issue issue, Test test, Tab tab, Done done) {
@@ -196,11 +196,10 @@ __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64
             const int c1 = min(c0 + kStage, S.shi[row]);
             for (int g = warp; g < G; g += kWarps) {
                 const int lo = max(S.rlo[row][g], c0), hi = min(S.rhi[row][g], c1);
-                for (int base = lo; base < hi; base += 32) {
-                    const int k = base + lane;
-                    test(buf, g, k < hi ? k : -1, c0);
+                if (lo < hi) {  // warp-uniform
+                    test(buf, g, lo, hi, c0);
+                    done(g);  // end of ray g's slots in this chunk
                 }
-                if (lo < hi) done(g);  // warp-uniform: end of ray g's slots in this chunk
             }
             __syncthreads();
             row = nrow;
@@ -305,29 +304,38 @@ __global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int6
                     cp_async4(&S.pid[buf][i], L.point_id + k);
                 }
             },
-            [&](int buf, int g, int k, int c0) {
-                int cls = 0;
-                double t = 0.0, d2 = 0.0;
-                if (k >= 0) {
-                    const RayParams& r = S.head.ray[g];
-                    const int i = k - c0;
-                    cls = cone_filter(S.pf[buf][i], r);
-                    if (cls != 0) {
-                        const bool ok = cone_test(S.px[buf][i], S.py[buf][i], S.pz[buf][i], r, t, d2);
-                        if (cls == 2) cls = ok ? 1 : 0;
+            [&](int buf, int g, int lo, int hi, int c0) {
+                // the ray's filter terms, output offset and fill count stay in
+                // registers for the whole run (shared-memory stores in the loop
+                // would otherwise force a re-load per slot)
+                const RayParams& r = S.head.ray[g];
+                const RayF rf = ray_f(r);
+                const int64_t off = S.off[g];
+                int fill = S.fill[g];
+                for (int base = lo; base < hi; base += 32) {
+                    const int k = base + lane_id();
+                    int cls = 0;
+                    double t = 0.0, d2 = 0.0;
+                    if (k < hi) {
+                        const int i = k - c0;
+                        cls = cone_filter(S.pf[buf][i], rf);
+                        if (cls != 0) {
+                            const bool ok = cone_test(S.px[buf][i], S.py[buf][i], S.pz[buf][i], r, t, d2);
+                            if (cls == 2) cls = ok ? 1 : 0;
+                        }
                     }
+                    const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
+                    if (cls == 1) {
+                        const int64_t pos = off + fill + __popc(b & ((1u << lane_id()) - 1));
+                        sc_t[pos] = t;
+                        sc_d[pos] = d2;  // dist^2: the sort takes the square root
+                        sc_id[pos] = S.pid[buf][k - c0];
+                        lmin = min(lmin, fkey(__double2float_rd(t)));
+                        lmax = max(lmax, fkey(__double2float_ru(t)));
+                    }
+                    fill += __popc(b);
                 }
-                const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
-                if (cls == 1) {
-                    const int64_t pos = S.off[g] + S.fill[g] + __popc(b & ((1u << lane_id()) - 1));
-                    sc_t[pos] = t;
-                    sc_d[pos] = d2;  // dist^2: the sort takes the square root
-                    sc_id[pos] = S.pid[buf][k - c0];
-                    lmin = min(lmin, fkey(__double2float_rd(t)));
-                    lmax = max(lmax, fkey(__double2float_ru(t)));
-                }
-                __syncwarp();
-                if (lane_id() == 0) S.fill[g] += __popc(b);  // ray g belongs to this warp alone
+                if (lane_id() == 0) S.fill[g] = fill;  // ray g belongs to this warp alone
                 __syncwarp();
             },
             [&](int g, int n) { atomicAdd(&S.scn[g], n); },
