@@ -44,7 +44,13 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGroupMax = 32;  // rays per group
-constexpr int kStageFill = 384;
+#ifndef HP_STAGE_FILL
+#define HP_STAGE_FILL 384
+#endif
+#ifndef HP_SCAN_MINB
+#define HP_SCAN_MINB 0
+#endif
+constexpr int kStageFill = HP_STAGE_FILL;
 
 struct Rays {
     const int64_t* pix;
@@ -269,7 +275,7 @@ struct FillSmem {
 // accepted pairs (t, id, dist), unsorted, to each ray's scratch segment at
 // soff[r] (capacity from k_query_bound); write the exact count, probes and
 // scanned of every ray.
-__global__ void __launch_bounds__(kThreads) k_query_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
+__global__ void __launch_bounds__(kThreads, HP_SCAN_MINB) k_query_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
                                                          int64_t m, const int64_t* __restrict__ soff,
                                                          int* __restrict__ sc_id, double* __restrict__ sc_t,
                                                          double* __restrict__ sc_d, uint2* __restrict__ tmm,
@@ -1284,7 +1290,7 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
         static const int attr = set_smem(k_query_scan, sizeof(FillSmem));  // once (thread-safe)
         (void)attr;
         TimedSpan ts("k_query_scan", s);
-        k_query_scan<<<group_grid(m, 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
+        k_query_scan<<<group_grid(m, HP_SCAN_MINB ? HP_SCAN_MINB : 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
                                                                          w.sid, w.st, w.sd, w.tmm, offsets, probes,
                                                                          scanned, capacity);
         HP_CHECK_LAUNCH("k_query_scan");
