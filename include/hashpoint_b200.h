@@ -21,6 +21,8 @@
  *   hp_query_fill         (+ _cone_test :22-36, _canonical_sort :39-73);
  *                       two-phase because Q is unknown before the call
  *                       (the reference grows its buffers, :141-151)
+ *   hp_head_count /     hash_query_batch -> sample_batch chained as in
+ *   hp_head_sort          renderer.py:119-124 (the sampler's heads only)
  *   hp_sample_run /     _kernels.sample_batch        _kernels.py:552-700
  *   hp_sample_emit        (two-phase for the same reason; R unknown)
  *   hp_primary_surface  derived: first retained candidate per ray
@@ -63,7 +65,10 @@ typedef struct {
  * then ONE contiguous slot range.  Device arrays; caller-allocated:
  * row_ptr[P+1], rel_x/rel_y/rel_z/point_id[N_in], relf[4*N_in] (capacity n
  * for hp_build).  relf holds (x, y, z, e) in float32 for the filter: the
- * rounded coordinates and the point's error budget e = 2^-18 * |p|_1. */
+ * rounded coordinates and the point's error budget e = 2^-18 * |p|_1.
+ * rel4[4*N_in] holds the same point as one 32-byte record (x, y, z, id as
+ * int64 bits) so that a single sector gather gives the exact coordinates of
+ * a slot (the head sort recomputes t / dist from it). */
 typedef struct {
     int32_t* row_ptr;
     double* rel_x;
@@ -71,6 +76,7 @@ typedef struct {
     double* rel_z;
     int32_t* point_id;
     float* relf;
+    double* rel4;
 } hp_query_layout;
 
 typedef struct {
@@ -148,26 +154,31 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
                    const double* t_near, const double* t_far, const double* slopes, int64_t m,
                    int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
                    void* workspace, size_t workspace_bytes, hp_stream_t stream);
-/* Prefix mode (callers that only want samples): instead of hp_query_fill,
- * sort in place, at the front of each ray's match scratch, the ray's
- * smallest-t matches -- all of them when it has <= 1024, else everything up
- * to the histogram bin where the count reaches `want` (<= 1024) -- and
- * record the sampler's facts over that prefix.  plen [m] receives each
- * prefix length; the view gives the (device) arrays of the prefixes: ray r
- * at start[r], t float64, ids int32, dist float64.  cut_t / cut_d [m]
- * receive the smallest t and dist of the matches left out (+inf when none;
- * every left-out t is strictly above the prefix's last t).
- * hp_sample_run_prefix consumes them. */
-typedef struct hp_query_prefix_view {
-    const int64_t* start; /* [m] */
-    const double* t;
-    const int32_t* ids;
-    const double* dist;
-} hp_query_prefix_view;
-int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, const double* slopes,
-                    int32_t* facts, int32_t* plen, double* cut_t, double* cut_d, int64_t capacity,
-                    void* workspace, size_t workspace_bytes, hp_query_prefix_view* view,
-                    hp_stream_t stream);
+/* Heads (callers that only want samples; replaces hash_query_batch ->
+ * sample_batch as chained by renderer.py:119-124): per ray, the head of its
+ * matches in (t, id) order -- all of them when it has <= 1024, else the
+ * smallest-t matches up to a cut near the `want`-th (<= 1024) -- without the
+ * full match list.  hp_head_count is the streaming pass (same arguments and
+ * probes / scanned / offsets outputs as hp_query_count, offsets[m] = Q or
+ * -(slots needed) when `capacity` is short); it keeps 8 bytes per match in
+ * the workspace and writes head_off [m+1] = the exclusive scan of
+ * min(q, 1024) (head_off[m] = the head arrays' capacity).  hp_head_sort
+ * writes each ray's head at head_off[r]: head_t / head_dist float64,
+ * head_ids int32 (same workspace and capacity), plen [m] = the head length,
+ * facts [m] (as hp_query_fill's, over the head; -1 when unknown), and cut_t /
+ * cut_d [m] = lower bounds of the t / dist of every match left out (+inf when
+ * none).  hp_sample_run_prefix consumes them. */
+int hp_head_workspace_bytes(int64_t m, int64_t capacity, size_t* bytes);
+int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
+                  int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                  const double* t_near, const double* t_far, const double* slopes, int64_t m,
+                  int64_t* offsets, int64_t* head_off, int64_t* probes, int64_t* scanned,
+                  int64_t capacity, void* workspace, size_t workspace_bytes, hp_stream_t stream);
+int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
+                 const int64_t* offsets, const int64_t* head_off, int32_t want, double* head_t,
+                 int32_t* head_ids, double* head_dist, int32_t* plen, int32_t* facts, double* cut_t,
+                 double* cut_d, int64_t capacity, void* workspace, size_t workspace_bytes,
+                 hp_stream_t stream);
 
 /* Upper bounds of the match counts (the slots pass 1 will test per ray),
  * exclusive-scanned into bound_off [m+1] (bound_off[m] = the scratch pass 1
@@ -219,9 +230,9 @@ int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const 
                    double* r_color, void* workspace, size_t workspace_bytes,
                    hp_stream_t stream);
 
-/* Prefix mode: the sampler over hp_query_prefix's sorted prefixes (offsets
- * = the full match counts from hp_query_count, query_facts = the prefix
- * call's facts).  Results are those of hp_sample_run on the full CSR for
+/* Prefix mode: the sampler over hp_head_sort's heads (offsets = the full
+ * match counts from hp_head_count, query_facts = hp_head_sort's facts,
+ * prefix = {head_off, plen, head_ids, head_t, head_dist, cut_t, cut_d}).  Results are those of hp_sample_run on the full CSR for
  * every ray not flagged; flagged [m+1] receives 1 for a ray whose work may
  * reach past its prefix (its r_off count is 0, its t_end NaN: run it through
  * the full path) and flagged[m] = the number of such rays. */

@@ -31,17 +31,13 @@ class Camera(ctypes.Structure):
 
 class Layout(ctypes.Structure):
     _fields_ = [("row_ptr", c_p), ("rel_x", c_p), ("rel_y", c_p), ("rel_z", c_p),
-                ("point_id", c_p), ("relf", c_p)]
+                ("point_id", c_p), ("relf", c_p), ("rel4", c_p)]
 
 
 class SamplerParams(ctypes.Structure):
     _fields_ = [("k_neighbors", c_i32), ("eps_mode", c_i32), ("want_color", c_i32),
                 ("exact_t_end", c_i32), ("beta2", c_f64), ("gamma", c_f64), ("eps", c_f64),
                 ("tau_min", c_f64)]
-
-
-class PrefixView(ctypes.Structure):
-    _fields_ = [("start", c_p), ("t", c_p), ("ids", c_p), ("dist", c_p)]
 
 
 class SamplePrefix(ctypes.Structure):
@@ -65,8 +61,12 @@ _SIGNATURES = {
     "hp_query_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
                                       c_p, c_size, c_p]),
-    "hp_query_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.c_int32, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
-                                       c_size, ctypes.POINTER(PrefixView), c_p]),
+    "hp_head_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_head_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
+                                     c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_i64,
+                                     c_p, c_size, c_p]),
+    "hp_head_sort": (ctypes.c_int, [Layout, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, c_p, c_p, c_p, c_p,
+                                    c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
     "hp_ray_grid": (ctypes.c_int, [ctypes.POINTER(Camera), c_i64, c_i64, c_p, c_p, ctypes.c_double,
                                    ctypes.c_double, c_p, c_p, c_p]),
     "hp_render": (ctypes.c_int, [ctypes.c_int, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,

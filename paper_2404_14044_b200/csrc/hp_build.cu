@@ -194,6 +194,12 @@ __global__ void __launch_bounds__(512) k_big_bucket_order(const int64_t* __restr
     }
 }
 
+// One 32-byte record per slot: (x, y, z) origin-relative and the id (int64 bits).
+__device__ __forceinline__ void store_rel4(double* rel4, int64_t k, double x, double y, double z, int32_t id) {
+    double4* p = reinterpret_cast<double4*>(rel4) + k;
+    *p = make_double4(x, y, z, __longlong_as_double((long long)id));
+}
+
 // Slot gather (reference HashIndex slot_x/y/z, reordered_ids) and the
 // row-major query layout (origin-relative coordinates).
 __global__ void k_gather(int64_t n_cap, const int64_t* __restrict__ n_in_dev, const double* __restrict__ xyz,
@@ -219,6 +225,7 @@ __global__ void k_gather(int64_t n_cap, const int64_t* __restrict__ n_in_dev, co
         L.rel_z[rm] = rz;
         L.point_id[rm] = id;
         reinterpret_cast<float4*>(L.relf)[rm] = filter_point(rx, ry, rz);
+        store_rel4(L.rel4, rm, rx, ry, rz, id);
     }
 }
 
@@ -247,6 +254,7 @@ __global__ void k_layout_fill(int64_t P, const int64_t* __restrict__ table_start
             L.rel_z[r0 + k] = rz;
             L.point_id[r0 + k] = int32_t(sid[s0 + k]);
             reinterpret_cast<float4*>(L.relf)[r0 + k] = filter_point(rx, ry, rz);
+            store_rel4(L.rel4, r0 + k, rx, ry, rz, int32_t(sid[s0 + k]));
         }
     }
 }

@@ -77,9 +77,12 @@ struct RayF {
 };
 HP_HD RayF ray_f(const RayParams& r) { return RayF{r.f0, r.f1, r.f2, r.ftn, r.ftf, r.fslope, r.eps_ray, r.smax}; }
 
-HP_HD int cone_filter(const float4 P, const RayF& r) {
-    const float eps = fmaf(P.w, r.smax, r.eps_ray);
-    const float t = fmaf(P.z, r.f2, fmaf(P.y, r.f1, P.x * r.f0));
+// cone_filter that also hands back the float t and band eps: for an accepted
+// pair |t - t64| <= eps (the band covers the t error bound with a wide
+// margin), so t - eps rounded down is a lower bound of the exact t.
+HP_HD int cone_filter_te(const float4 P, const RayF& r, float& t, float& eps) {
+    eps = fmaf(P.w, r.smax, r.eps_ray);
+    t = fmaf(P.z, r.f2, fmaf(P.y, r.f1, P.x * r.f0));
     if (t < r.ftn - eps || t > r.ftf + eps) return 0;
     const float ex = fmaf(-t, r.f0, P.x), ey = fmaf(-t, r.f1, P.y), ez = fmaf(-t, r.f2, P.z);
     const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
@@ -90,6 +93,10 @@ HP_HD int cone_filter(const float4 P, const RayF& r) {
     const bool t_in = (t >= r.ftn + eps) && (t <= r.ftf - eps);
     if (t_in && lo > 0.0f && d2 < lo * lo * (1.0f - 0x1p-20f)) return 1;
     return 2;
+}
+HP_HD int cone_filter(const float4 P, const RayF& r) {
+    float t, eps;
+    return cone_filter_te(P, r, t, eps);
 }
 HP_HD int cone_filter(const float4 P, const RayParams& r) { return cone_filter(P, ray_f(r)); }
 

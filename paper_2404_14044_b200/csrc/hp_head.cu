@@ -1,0 +1,726 @@
+// hp_head.cu — the query for callers that only want samples: per ray, the
+// head of its matches in (t, id) order, without materialising its full match
+// list.
+//
+// Reference: the chained hash_query_batch (_kernels.py:86-157; cone test
+// :22-36, canonical order :39-73) -> sample_batch (:552-700) of the renderer
+// (renderer.py:119-124).  The sampler only ever reads a head of each ray's t
+// order (hp_sample.cu, prefix mode), so the query keeps, per accepted
+// (ray, point) pair, 8 bytes -- a lower bound of the exact t as an
+// order-preserving float key and the pair's layout slot -- instead of the
+// 20-byte exact (t, id, dist) record, and recomputes the exact values only for
+// the head, from the L2-resident layout, with the reference's own expression
+// (bit-identical: cone_t / cone_dist2 of hp_cone.cuh).
+//
+//   k_query_bound  (hp_query_core.cuh) per-ray footprint bound -> scratch offsets
+//   k_head_scan    the streaming pass: a CTA owns a group of <= 32 adjacent
+//                  rays and streams the union of their footprint rows through
+//                  shared memory, fp32 copies only (16 B per point), staged by
+//                  1-D bulk copies (cp.async.bulk + mbarrier); the fp32 filter
+//                  settles almost every pair; the few uncertain pairs are
+//                  deferred per warp and decided in batches by the exact fp64
+//                  test (coordinates gathered from rel4).  Accepted pairs ->
+//                  (key, slot) appended to the ray's scratch segment.
+//   k_head_classes / k_head_select (long rays: warp per ray, key histogram ->
+//                  the key cut K_c) / k_head_sort (one CTA per ray: stage the
+//                  selected slots, gather + exact t / dist^2, trim the band
+//                  above the cut, exact (t, id) rank, write the head).
+//
+// Exactness (DESIGN.md §6 "Heads"): every key is a lower bound of its pair's
+// exact t (sure accepts: RD(t32 - eps) with |t32 - t64| <= eps; fp64-decided
+// pairs: RD(t64)).  A long ray keeps the pairs with key <= K_c whose exact t is
+// below T_c = float(K_c + 1); every pair left out has t >= T_c (key > K_c, or
+// trimmed), so the head is exactly a prefix of the ray's (t, id) order.  The
+// cuts handed to the sampler are lower bounds of the left-out t and dist
+// (hp_sample.cu only relies on "every left-out t >= cut_t, dist >= cut_d").
+#include "hp_query_core.cuh"
+
+namespace hp {
+namespace {
+
+constexpr int kHeadCap = 1024;   // longest head; rays up to this are sorted whole
+constexpr int kHeadSmall = 512;  // rays up to this: a smaller, denser CTA configuration
+#ifndef HP_HEAD_STAGE
+#define HP_HEAD_STAGE 512
+#endif
+constexpr int kStage = HP_HEAD_STAGE;  // slots per staged chunk (16 B each)
+#ifndef HP_HEAD_MINB
+#define HP_HEAD_MINB 5
+#endif
+
+// ---------------------------------------------------------------- bulk copies
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n HP_MBAR_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra HP_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+
+// ---------------------------------------------------------------- scan
+// stream_group (hp_query.cu) with the chunks staged by bulk copies: thread 0
+// arms the buffer's mbarrier and issues one copy of the chunk's contiguous
+// slot range; every thread waits on the barrier's phase (tracked in `phase`,
+// bit b = parity of buffer b's next completion).  Chunk i + 1 is in flight
+// while chunk i is tested.
+template <class Issue, class Test, class Tab, class Done>
+__device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, unsigned& phase, int G, const hp_query_layout L,
+                                  int64_t wp, int s, const QCam& QC, Issue issue, Test test, Tab tab, Done done) {
+    const int tid = threadIdx.x, warp = warp_id();
+    const int pad = (s - 1) / 2;
+    for (int yb = S.v0; yb < S.v1; yb += kRowsMax) {
+        const int nrows = min(kRowsMax, S.v1 - yb);
+        for (int row = tid; row < nrows; row += kThreads) {
+            S.slo[row] = INT_MAX;
+            S.shi[row] = INT_MIN;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < nrows * G; idx += kThreads) {
+            const int row = idx / G, g = idx - row * G;
+            const int y = yb + row;
+            const RayParams& r = S.ray[g];
+            int lo = 0, hi = 0;
+            if (y >= r.v && y < r.v + s) {
+                const int64_t base = int64_t(y) * wp;
+                tab(g, L.row_ptr[base + r.u + s] - L.row_ptr[base + r.u]);  // scanned: full window
+                int x0, x1;
+                if (footprint_row(S.fp[g], QC.C, pad, QC.width, QC.height, r.u, r.v, y, x0, x1)) {
+                    lo = L.row_ptr[base + x0];
+                    hi = L.row_ptr[base + x1 + 1];
+                    if (lo < hi) {
+                        atomicMin(&S.slo[row], lo);
+                        atomicMax(&S.shi[row], hi);
+                    }
+                }
+            }
+            S.rlo[row][g] = lo;
+            S.rhi[row][g] = hi;
+        }
+        __syncthreads();
+        for (int row = tid; row < nrows; row += kThreads)
+            if (S.slo[row] > S.shi[row]) S.slo[row] = S.shi[row] = 0;  // nothing staged
+        __syncthreads();
+        int row = 0, c0 = S.slo[0];
+        auto advance = [&](int& rw, int& cc) {
+            cc += kStage;
+            while (rw < nrows && cc >= S.shi[rw]) {
+                rw++;
+                if (rw < nrows) cc = S.slo[rw];
+            }
+        };
+        if (c0 >= S.shi[0]) {  // empty first row(s)
+            c0 -= kStage;
+            advance(row, c0);
+        }
+        int buf = 0;
+        if (row < nrows && tid == 0) issue(0, c0, min(c0 + kStage, S.shi[row]));
+        while (row < nrows) {
+            int nrow = row, nc0 = c0;
+            advance(nrow, nc0);
+            if (nrow < nrows && tid == 0) issue(buf ^ 1, nc0, min(nc0 + kStage, S.shi[nrow]));
+            mbar_wait(&bar[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
+            const int c1 = min(c0 + kStage, S.shi[row]);
+            for (int g = warp; g < G; g += kWarps) {
+                const int lo = max(S.rlo[row][g], c0), hi = min(S.rhi[row][g], c1);
+                if (lo < hi) {  // warp-uniform
+                    test(buf, g, lo, hi, c0);
+                    done(g);
+                }
+            }
+            __syncthreads();  // buffer `buf` is refilled two chunks later
+            row = nrow;
+            c0 = nc0;
+            buf ^= 1;
+        }
+    }
+}
+
+struct HeadScanSmem {
+    GroupHead head;
+    float4 pf[2][kStage];
+    uint64_t bar[2];
+    int fill[kGroupMax], scn[kGroupMax], bad[kGroupMax];
+    unsigned kmin[kGroupMax], kmax[kGroupMax];
+    int64_t off[kGroupMax];
+    int dq[kWarps][64];  // deferred (uncertain) slots of the warp's current ray run
+};
+
+// Per-ray results of the scan: key bounds of the accepted pairs, and whether
+// an fp64-decided pair had a non-finite t or dist^2 (the sampler's facts).
+struct RayMeta {
+    unsigned kmin, kmax;
+    int bad, pad_;
+};
+
+__global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
+    k_head_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC, int64_t m, const int64_t* __restrict__ soff,
+                unsigned* __restrict__ sc_key, int* __restrict__ sc_slot, RayMeta* __restrict__ meta,
+                int64_t* __restrict__ counts, int64_t* __restrict__ hcount, int64_t* __restrict__ probes,
+                int64_t* __restrict__ scanned, int64_t capacity) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    HeadScanSmem& S = *reinterpret_cast<HeadScanSmem*>(dyn);
+    if (soff[m] > capacity) return;  // scratch too small: reported in offsets[m]
+    const int s = 2 * pad + 1;
+    const int lane = lane_id(), warp = warp_id();
+    const double4* __restrict__ rel4 = reinterpret_cast<const double4*>(L.rel4);
+    if (threadIdx.x == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
+        const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
+        if (threadIdx.x < G) {
+            S.fill[threadIdx.x] = 0;
+            S.scn[threadIdx.x] = 0;
+            S.bad[threadIdx.x] = 0;
+            S.kmin[threadIdx.x] = 0xffffffffu;
+            S.kmax[threadIdx.x] = 0u;
+            S.off[threadIdx.x] = soff[r0 + threadIdx.x];
+        }
+        group_setup(S.head, R, QC, r0, G, s);
+        unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's key bounds for the current ray
+        int lbad = 0;
+        stream_group_bulk(
+            S.head, S.bar, phase, G, L, wp, s, QC,
+            [&](int buf, int c0, int c1) {
+                const unsigned bytes = unsigned(c1 - c0) * 16u;
+                mbar_arrive_tx(&S.bar[buf], bytes);
+                bulk_g2s(&S.pf[buf][0], L.relf + 4 * int64_t(c0), bytes, &S.bar[buf]);
+            },
+            [&](int buf, int g, int lo, int hi, int c0) {
+                const RayParams& rp = S.head.ray[g];
+                const RayF rf = ray_f(rp);
+                const int64_t off = S.off[g];
+                int fill = S.fill[g];
+                int* dq = S.dq[warp];
+                int nq = 0;  // deferred pairs (warp-uniform)
+                // the deferred pairs, 32 at a time on all lanes: gather the exact
+                // coordinates, the reference's fp64 test, append the accepted
+                auto flush = [&](int n) {
+                    __syncwarp();
+                    int k = -1;
+                    bool ok = false;
+                    double t = 0.0, d2 = 0.0;
+                    if (lane < n) {
+                        k = dq[lane];
+                        const double4 a = rel4[k];
+                        ok = cone_test(a.x, a.y, a.z, rp, t, d2);
+                    }
+                    const unsigned b = __ballot_sync(0xffffffffu, ok);
+                    if (ok) {
+                        const int64_t pos = off + fill + __popc(b & lanemask_lt());
+                        const unsigned key = fkey(__double2float_rd(t));
+                        sc_key[pos] = key;
+                        sc_slot[pos] = k;
+                        lmin = min(lmin, key);
+                        lmax = max(lmax, key);
+                        lbad |= !(fabs(t) <= DBL_MAX) || !(d2 <= DBL_MAX);
+                    }
+                    fill += __popc(b);
+                    __syncwarp();
+                    if (n < nq && lane < nq - n) dq[lane] = dq[n + lane];  // the rest (< 32) to the front
+                    __syncwarp();
+                    nq -= n;
+                };
+                for (int base = lo; base < hi; base += 32) {
+                    const int k = base + lane;
+                    int cls = 0;
+                    float tf = 0.0f, eps = 0.0f;
+                    if (k < hi) cls = cone_filter_te(S.pf[buf][k - c0], rf, tf, eps);
+                    const unsigned acc = __ballot_sync(0xffffffffu, cls == 1);
+                    if (cls == 1) {
+                        const int64_t pos = off + fill + __popc(acc & lanemask_lt());
+                        const unsigned key = fkey(__fsub_rd(tf, eps));
+                        sc_key[pos] = key;
+                        sc_slot[pos] = k;
+                        lmin = min(lmin, key);
+                        lmax = max(lmax, key);
+                    }
+                    fill += __popc(acc);
+                    const unsigned unc = __ballot_sync(0xffffffffu, cls == 2);
+                    if (unc) {
+                        if (cls == 2) dq[nq + __popc(unc & lanemask_lt())] = k;
+                        nq += __popc(unc);
+                        if (nq >= 32) flush(32);
+                    }
+                }
+                if (nq > 0) flush(nq);
+                if (lane == 0) S.fill[g] = fill;  // ray g belongs to this warp alone
+                __syncwarp();
+            },
+            [&](int g, int n) { atomicAdd(&S.scn[g], n); },
+            [&](int g) {
+                const unsigned lo = __reduce_min_sync(0xffffffffu, lmin);
+                const unsigned hi = __reduce_max_sync(0xffffffffu, lmax);
+                const bool anybad = __any_sync(0xffffffffu, lbad);
+                if (lane == 0) {
+                    S.kmin[g] = min(S.kmin[g], lo);
+                    S.kmax[g] = max(S.kmax[g], hi);
+                    if (anybad) S.bad[g] = 1;
+                }
+                lmin = 0xffffffffu;
+                lmax = 0u;
+                lbad = 0;
+            });
+        __syncthreads();
+        if (threadIdx.x < G) {
+            const int64_t r = r0 + threadIdx.x;
+            const int q = S.fill[threadIdx.x];
+            meta[r] = RayMeta{S.kmin[threadIdx.x], S.kmax[threadIdx.x], S.bad[threadIdx.x], 0};
+            counts[r] = q;
+            hcount[r] = q < kHeadCap ? q : kHeadCap;
+            probes[r] = int64_t(s) * s;
+            scanned[r] = S.scn[threadIdx.x];
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- classes
+// list 0: rays of 1..kHeadSmall matches, list 1: the longer ones; the empty
+// rays' outputs are written here.
+__global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
+                               int* __restrict__ counts, int* __restrict__ plen, int* __restrict__ facts,
+                               double* __restrict__ cut_t, double* __restrict__ cut_d) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        int cls = -1;
+        if (r < m) {
+            const int64_t q = off[r + 1] - off[r];
+            cls = q == 0 ? -1 : (q <= kHeadSmall ? 0 : 1);
+            if (q == 0) {
+                plen[r] = 0;
+                facts[r] = -1;
+                cut_t[r] = cut_d[r] = CUDART_INF;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            const unsigned b = __ballot_sync(0xffffffffu, cls == c);
+            if (!b) continue;
+            int base = 0;
+            if (lane_id() == __ffs(b) - 1) base = atomicAdd(&counts[c], __popc(b));
+            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+            if (cls == c) lists[int64_t(c) * m + base + __popc(b & lanemask_lt())] = int(r);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- selection
+// Rays of more than kHeadCap matches, one warp per ray (a plain stream over
+// the 4-byte keys, many rays in flight): a histogram of the keys over
+// [kmin, kmax] in bins of 2^sh consecutive keys (the smallest sh giving at
+// most kBins bins) -> the first bin b where the running count reaches `want`
+// (b - 1 if that bin alone would overflow kHeadCap) -> the key cut K_c = the
+// largest key of bin b: sel[r] = (K_c, #{key <= K_c}).  No cut (b < 0):
+// K_c = kmin - 1, count 0.
+template <int kBins>
+__global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__ off,
+                                                     const int64_t* __restrict__ soff,
+                                                     const RayMeta* __restrict__ meta, int want,
+                                                     const unsigned* __restrict__ sc_key, uint2* __restrict__ sel,
+                                                     const int* __restrict__ list, const int* __restrict__ list_n) {
+    __shared__ int hist[4][kBins];
+    int* H = hist[warp_id()];
+    const int lane = lane_id();
+    const int64_t warps = int64_t(gridDim.x) * 4;
+    const int64_t nr = *list_n;
+    for (int64_t k = int64_t(blockIdx.x) * 4 + warp_id(); k < nr; k += warps) {
+        const int64_t r = list[k];
+        const int q = int(off[r + 1] - off[r]);
+        if (q <= kHeadCap) continue;
+        const int64_t so = soff[r];
+        const RayMeta M = meta[r];
+        const unsigned span1 = M.kmax - M.kmin;  // span - 1
+        int sh = 0;
+        while ((span1 >> sh) >= unsigned(kBins)) sh++;
+        for (int b = lane; b < kBins; b += 32) H[b] = 0;
+        __syncwarp();
+        for (int e0 = 0; e0 < q; e0 += 128) {  // four loads per lane in flight
+            unsigned kv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * 32 + lane;
+                kv[u] = e < q ? sc_key[so + e] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (e0 + u * 32 + lane < q)
+                    atomicAdd(&H[(kv[u] - M.kmin) >> sh], 1);
+        }
+        __syncwarp();
+        constexpr int kPer = kBins / 32;  // lane owns bins [lane * kPer, lane * kPer + kPer)
+        int sum = 0;
+#pragma unroll 8
+        for (int b = 0; b < kPer; b++) sum += H[lane * kPer + b];
+        const int incl = warp_incl_scan(sum);
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= want);
+        const int owner = __ffs(hit) - 1;  // exists: q > kHeadCap >= want
+        if (lane == owner) {
+            int c = incl - sum, b = lane * kPer;
+            for (int j = 0; j < kPer; j++) {
+                c += H[lane * kPer + j];
+                if (c >= want) {
+                    b = lane * kPer + j;
+                    break;
+                }
+            }
+            if (c > kHeadCap) {  // that bin alone overflows: stop before it
+                c -= H[b];
+                b -= 1;
+            }
+            // largest key of bin b (keys above kmax do not occur)
+            const unsigned long long kc = (unsigned long long)M.kmin + ((unsigned long long)(b + 1) << sh) - 1ull;
+            sel[r] = make_uint2(unsigned(kc < M.kmax ? kc : M.kmax), unsigned(c));
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- head sort
+template <int kCap>
+struct HeadSmem {
+    double t[kCap];
+    double d2[kCap];
+    int id[kCap];
+    union {
+        int slot[kCap];    // staged slots (read before the ranking)
+        unsigned bk[kCap]; // rank_segment's bucket words
+    };
+    int hist[kCap + 1];
+    unsigned short lst[kCap], perm[kCap];
+    int chist[kCoarse + 1];
+    int scan_sh[33];
+    unsigned long long cut_t, cut_d2;  // order keys of the trimmed pairs' minima
+    unsigned kout, thi;                // smallest left-out key; fkey of the largest float(t) staged
+    int cnt, keep, fcount, fbad;
+};
+
+// One CTA per ray: a ray of <= kCap matches is staged whole (its slots by
+// cp.async); a longer one streams its keys and stages the slots of the pairs
+// with key <= K_c.  Then the exact t / dist^2 of every staged pair from its
+// rel4 record (the reference's expression), the long rays' trim (t >= T_c
+// moves to the left-out side), the exact (t, id) rank, and the write-out of
+// the head at hoff[r] with the sampler's facts and cuts.
+template <int kCap, int kT>
+__global__ void __launch_bounds__(kT, kT == 128 ? 12 : 6) k_head_sort(
+    hp_query_layout L, const double* __restrict__ dirs, const double* __restrict__ slopes,
+    const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const int64_t* __restrict__ hoff,
+    const RayMeta* __restrict__ meta, const unsigned* __restrict__ sc_key, const int* __restrict__ sc_slot,
+    const uint2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n,
+    double* __restrict__ head_t, int* __restrict__ head_id, double* __restrict__ head_d, int* __restrict__ plen,
+    int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    HeadSmem<kCap>& F = *reinterpret_cast<HeadSmem<kCap>*>(dyn);
+    const double4* __restrict__ rel4 = reinterpret_cast<const double4*>(L.rel4);
+    const int tid = threadIdx.x;
+    const int nr = *list_n;
+    for (int k = blockIdx.x; k < nr; k += gridDim.x) {
+        const int64_t r = list[k];
+        const int64_t so = soff[r];
+        const int q = int(off[r + 1] - off[r]);
+        const RayMeta M = meta[r];
+        const bool all = q <= kCap;
+        if (tid == 0) {
+            F.cnt = F.keep = F.fcount = 0;
+            F.fbad = M.bad;
+            F.cut_t = F.cut_d2 = ~0ull;
+            F.kout = 0xffffffffu;
+            F.thi = 0u;
+        }
+        unsigned kc = 0xffffffffu;
+        if (all) {  // every slot in flight at once
+            for (int e = tid; e < q; e += kT) cp_async4(&F.slot[e], sc_slot + so + e);
+            cp_commit();
+        } else {
+            kc = sel[r].x;
+        }
+        for (int j = tid; j <= kCoarse; j += kT) F.chist[j] = 0;
+        for (int j = tid; j <= kCap; j += kT) F.hist[j] = 0;
+        __syncthreads();
+        if (!all) {  // stream the keys (4 per thread in flight); stage the selected slots
+            unsigned kout = 0xffffffffu;
+            for (int e0 = 0; e0 < q; e0 += 4 * kT) {
+                unsigned kv[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int e = e0 + u * kT + tid;
+                    kv[u] = e < q ? sc_key[so + e] : 0xffffffffu;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int e = e0 + u * kT + tid;
+                    const bool in = e < q && kv[u] <= kc;
+                    if (e < q && !in) kout = min(kout, kv[u]);
+                    const unsigned b = __ballot_sync(0xffffffffu, in);
+                    int base = 0;
+                    if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (in) F.slot[base + __popc(b & lanemask_lt())] = sc_slot[so + e];
+                }
+            }
+            kout = __reduce_min_sync(0xffffffffu, kout);
+            if (lane_id() == 0 && kout != 0xffffffffu) atomicMin(&F.kout, kout);
+        }
+        cp_wait<0>();
+        __syncthreads();
+        const int S = all ? q : F.cnt;  // staged pairs
+        // exact t / dist^2 of the staged pairs; long rays keep t < T_c
+        const double d0 = dirs[3 * r], d1 = dirs[3 * r + 1], d2v = dirs[3 * r + 2];
+        const double Tc = (all || kc == 0xffffffffu) ? CUDART_INF : double(from_fkey(kc + 1u));
+        unsigned long long mt = ~0ull, md = ~0ull;
+        unsigned thi = 0u;
+        bool bad = false;
+        for (int e0 = 0; e0 < S; e0 += kT) {
+            const int e = e0 + tid;
+            bool keep = false;
+            double t = 0.0, dd = 0.0;
+            int id = 0;
+            if (e < S) {
+                const double4 a = rel4[F.slot[e]];
+                t = cone_t(a.x, a.y, a.z, d0, d1, d2v);
+                dd = cone_dist2(a.x, a.y, a.z, t, d0, d1, d2v);
+                id = int(__double_as_longlong(a.w));
+                keep = t < Tc;
+                if (!keep) {
+                    mt = min(mt, dkey(t));
+                    md = min(md, dkey(dd));
+                }
+            }
+            int pos = e;
+            if (!all) {  // compact the kept pairs (order is irrelevant: ranked below)
+                const unsigned b = __ballot_sync(0xffffffffu, keep);
+                int base = 0;
+                if (lane_id() == 0 && b) base = atomicAdd(&F.keep, __popc(b));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                pos = base + __popc(b & lanemask_lt());
+            }
+            if (keep) {
+                F.t[pos] = t;
+                F.d2[pos] = dd;
+                F.id[pos] = id;
+                thi = max(thi, fkey(__double2float_rn(t)));
+                bad |= !(fabs(t) <= DBL_MAX) || !(dd <= DBL_MAX);
+            }
+        }
+        thi = __reduce_max_sync(0xffffffffu, thi);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mt = min(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+            md = min(md, __shfl_xor_sync(0xffffffffu, md, o));
+        }
+        const bool anybad = __any_sync(0xffffffffu, bad);
+        if (lane_id() == 0) {
+            atomicMax(&F.thi, thi);
+            if (anybad) atomicOr(&F.fbad, 1);
+            if (mt != ~0ull) {
+                atomicMin(&F.cut_t, mt);
+                atomicMin(&F.cut_d2, md);
+            }
+        }
+        __syncthreads();  // every slot read (bk may now be overwritten)
+        const int Lh = all ? q : F.keep;
+        if (Lh > 0)
+            rank_segment<kCap, kT>(Lh, from_fkey(M.kmin), from_fkey(F.thi), F.t, F.id, F.bk, F.hist, F.lst, F.perm,
+                                   F.chist, F.scan_sh);
+        const int64_t ho = hoff[r];
+        const double r0 = Lh > 0 ? dmul(__ldg(slopes + r), F.t[F.perm[0]]) : 0.0;
+        int cnt = 0;
+        for (int p = tid; p < Lh; p += kT) {
+            const int e = F.perm[p];
+            const double d = sqrt(F.d2[e]);
+            head_t[ho + p] = F.t[e];
+            head_id[ho + p] = F.id[e];
+            head_d[ho + p] = d;
+            cnt += d <= r0;
+        }
+        cnt = warp_sum(cnt);
+        if (lane_id() == 0 && cnt) atomicAdd(&F.fcount, cnt);
+        __syncthreads();
+        if (tid == 0) {
+            plen[r] = Lh;
+            facts[r] = (F.fbad || Lh == 0) ? -1 : F.fcount;
+            // lower bounds of the left-out t / dist: a pair never staged has
+            // t >= its key (> K_c) and an unknown dist (0); a trimmed pair's are exact
+            const bool unstaged = !all && F.kout != 0xffffffffu;
+            const bool trimmed = F.cut_t != ~0ull;
+            double ct = CUDART_INF, cd = CUDART_INF;
+            if (unstaged) {
+                ct = double(from_fkey(F.kout));
+                cd = 0.0;
+            }
+            if (trimmed) {
+                ct = fmin(ct, dkey_inv(F.cut_t));
+                cd = fmin(cd, sqrt(dkey_inv(F.cut_d2)));
+            }
+            cut_t[r] = ct;
+            cut_d[r] = cd;
+        }
+        __syncthreads();
+    }
+}
+
+struct HeadWs {
+    void* scan;
+    int64_t* soff;
+    RayMeta* meta;
+    int* lists;
+    int* counts;
+    uint2* sel;
+    unsigned* key;
+    int* slot;
+};
+
+HeadWs carve_head(Carver& c, int64_t m, int64_t cap) {
+    HeadWs w;
+    const int64_t mm = m > 0 ? m : 1;
+    w.scan = c.take<char>(scan_workspace_bytes(m + 1));
+    w.soff = c.take<int64_t>(m + 1);
+    w.meta = c.take<RayMeta>(mm);
+    w.lists = c.take<int>(2 * mm);
+    w.counts = c.take<int>(64);
+    w.sel = c.take<uint2>(mm);
+    w.key = c.take<unsigned>(cap > 0 ? cap : 1);
+    w.slot = c.take<int>(cap > 0 ? cap : 1);
+    return w;
+}
+
+}  // namespace
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" int hp_head_workspace_bytes(int64_t m, int64_t capacity, size_t* bytes) {
+    Carver c(nullptr, 0);
+    carve_head(c, m, capacity);
+    *bytes = c.used + 256;
+    return HP_OK;
+}
+
+extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
+                             int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
+                             const double* t_near, const double* t_far, const double* slopes, int64_t m,
+                             int64_t* offsets, int64_t* head_off, int64_t* probes, int64_t* scanned,
+                             int64_t capacity, void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+    HP_TRY(check_common(layout, pad, m));
+    (void)padded_h;
+    if (!layout.rel4 || !layout.relf || !head_off) {
+        set_error("hp_head_count: the layout's relf / rel4 and head_off are required");
+        return HP_EINVAL;
+    }
+    if (capacity > INT32_MAX) {  // layout slots are int32; the scratch is indexed by int64
+        capacity = INT32_MAX;
+    }
+    Carver cv(workspace, workspace_bytes);
+    HeadWs w = carve_head(cv, m, capacity);
+    if (!cv.ok()) {
+        set_error("hp_head_count: workspace too small");
+        return HP_ESPACE;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
+    const QCam QC = make_qcam(cam);
+    if (m > 0) {
+        {
+            TimedSpan ts("k_query_bound", s);
+            k_query_bound<<<group_grid(m, 8), kThreads, 0, s>>>(layout, padded_w, int(pad), R, QC, m, w.soff);
+            HP_CHECK_LAUNCH("k_query_bound");
+        }
+        HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
+        static const int occ = [] {  // once (thread-safe)
+            set_smem(k_head_scan, sizeof(HeadScanSmem));
+            return resident(k_head_scan, kThreads, sizeof(HeadScanSmem));
+        }();
+        TimedSpan ts("k_head_scan", s);
+        k_head_scan<<<group_grid(m, occ), kThreads, sizeof(HeadScanSmem), s>>>(
+            layout, padded_w, int(pad), R, QC, m, w.soff, w.key, w.slot, w.meta, offsets, head_off, probes, scanned,
+            capacity);
+        HP_CHECK_LAUNCH("k_head_scan");
+    }
+    HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
+    HP_TRY(exclusive_scan_i64(head_off, head_off, m, w.scan, s));
+    if (m > 0) {
+        k_mark_overflow<<<1, 1, 0, s>>>(w.soff + m, capacity, offsets + m);
+        HP_CHECK_LAUNCH("k_mark_overflow");
+    }
+    return HP_OK;
+}
+
+extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
+                            const int64_t* offsets, const int64_t* head_off, int32_t want, double* head_t,
+                            int32_t* head_ids, double* head_dist, int32_t* plen, int32_t* facts, double* cut_t,
+                            double* cut_d, int64_t capacity, void* workspace, size_t workspace_bytes,
+                            hp_stream_t stream) {
+    if (m < 0 || want < 1 || want > kHeadCap ||
+        (m > 0 && (!dirs || !slopes || !facts || !plen || !cut_t || !cut_d || !layout.rel4))) {
+        set_error("hp_head_sort: invalid arguments (1 <= want <= %d)", kHeadCap);
+        return HP_EINVAL;
+    }
+    if (capacity > INT32_MAX) capacity = INT32_MAX;
+    Carver cv(workspace, workspace_bytes);
+    HeadWs w = carve_head(cv, m, capacity);
+    if (!cv.ok()) {
+        set_error("hp_head_sort: workspace too small");
+        return HP_ESPACE;
+    }
+    if (m == 0) return HP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_head_sort memset");
+    const int* list_small = w.lists;
+    const int* list_big = w.lists + m;
+    k_head_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, w.lists, w.counts, plen, facts, cut_t, cut_d);
+    HP_CHECK_LAUNCH("k_head_classes");
+    {
+        constexpr auto kselect = k_head_select<kHeadCap>;
+        static const int occ_sel = resident(kselect, 128, 0);  // once (thread-safe)
+        TimedSpan ts("k_head_select", s);
+        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.meta, want, w.key, w.sel, list_big,
+                                                  w.counts + 1);
+        HP_CHECK_LAUNCH("k_head_select");
+    }
+    constexpr auto ksmall = k_head_sort<kHeadSmall, 128>;
+    constexpr auto kbig = k_head_sort<kHeadCap, 256>;
+    static const int occ_small = [] {
+        set_smem(ksmall, sizeof(HeadSmem<kHeadSmall>));
+        return resident(ksmall, 128, sizeof(HeadSmem<kHeadSmall>));
+    }();
+    static const int occ_big = [] {
+        set_smem(kbig, sizeof(HeadSmem<kHeadCap>));
+        return resident(kbig, 256, sizeof(HeadSmem<kHeadCap>));
+    }();
+    TimedSpan ts("k_head_sort", s);
+    ksmall<<<kNumSMs * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
+        layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts, head_t,
+        head_ids, head_dist, plen, facts, cut_t, cut_d);
+    HP_CHECK_LAUNCH("k_head_sort small");
+    kbig<<<kNumSMs * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
+        layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big, w.counts + 1,
+        head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
+    HP_CHECK_LAUNCH("k_head_sort");
+    return HP_OK;
+}

@@ -36,14 +36,12 @@
 
 #include "hp_common.cuh"
 #include "hp_cone.cuh"
+#include "hp_query_core.cuh"
 #include "hp_sortnet.cuh"
 
 namespace hp {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kGroupMax = 32;  // rays per group
 #ifndef HP_STAGE_FILL
 #define HP_STAGE_FILL 384
 #endif
@@ -52,79 +50,6 @@ constexpr int kGroupMax = 32;  // rays per group
 #endif
 constexpr int kStageFill = HP_STAGE_FILL;
 
-struct Rays {
-    const int64_t* pix;
-    int64_t pstride;
-    const double* dirs;
-    const double* tn;
-    const double* tf;
-    const double* slopes;
-};
-
-__device__ __forceinline__ RayParams load_ray(const Rays& R, int64_t r) {
-    RayParams p;
-    p.u = int(R.pix[r * R.pstride]);
-    p.v = int(R.pix[r * R.pstride + 1]);
-    p.d0 = R.dirs[3 * r];
-    p.d1 = R.dirs[3 * r + 1];
-    p.d2 = R.dirs[3 * r + 2];
-    p.tn = R.tn[r];
-    p.tf = R.tf[r];
-    p.slope = R.slopes[r];
-    ray_derive(p);
-    return p;
-}
-
-constexpr int kRowsMax = 48;  // kernel rows tabulated per batch
-
-struct GroupHead {
-    RayParams ray[kGroupMax];
-    Footprint fp[kGroupMax];
-    int rlo[kRowsMax][kGroupMax], rhi[kRowsMax][kGroupMax];  // ray's tested sub-range per row
-    int slo[kRowsMax], shi[kRowsMax];                          // staged (union) range per row
-    int u0, u1, v0, v1;
-};
-
-struct QCam {  // camera frame for the footprint (has_cam == 0: full windows)
-    CamFrame C;
-    int has_cam, width, height;
-};
-
-// Group bounding box (padded coordinates) of rays [r0, r0+G).
-__device__ void group_setup(GroupHead& S, const Rays& R, const QCam& QC, int64_t r0, int G, int s) {
-    const int tid = threadIdx.x;
-    if (tid < G) {
-        S.ray[tid] = load_ray(R, r0 + tid);
-        if (QC.has_cam)
-            footprint_init(S.fp[tid], QC.C, S.ray[tid].d0, S.ray[tid].d1, S.ray[tid].d2, S.ray[tid].slope);
-        else
-            S.fp[tid].tight = 0;
-    }
-    __syncthreads();
-    if (tid < 32) {
-        int u0 = INT_MAX, u1 = INT_MIN, v0 = INT_MAX, v1 = INT_MIN;
-        if (tid < G) {
-            u0 = S.ray[tid].u;
-            u1 = S.ray[tid].u + s;
-            v0 = S.ray[tid].v;
-            v1 = S.ray[tid].v + s;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            u0 = min(u0, __shfl_xor_sync(0xffffffffu, u0, o));
-            u1 = max(u1, __shfl_xor_sync(0xffffffffu, u1, o));
-            v0 = min(v0, __shfl_xor_sync(0xffffffffu, v0, o));
-            v1 = max(v1, __shfl_xor_sync(0xffffffffu, v1, o));
-        }
-        if (tid == 0) {
-            S.u0 = u0;
-            S.u1 = u1;
-            S.v0 = v0;
-            S.v1 = v1;
-        }
-    }
-    __syncthreads();
-}
 
 // Streams the kernel rows of a group through two shared-memory stages.
 // Rows are processed in batches of kRowsMax: the batch's per-(row, ray) slot
@@ -215,49 +140,6 @@ __device__ void stream_group(GroupHead& S, int G, const hp_query_layout L, int64
     }
 }
 
-// Order-preserving uint32 key of a float (and back).
-__device__ __forceinline__ unsigned fkey(float x) {
-    const unsigned u = __float_as_uint(x);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float from_fkey(unsigned k) {
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-
-// offsets[m] = -(scratch slots needed) when the caller's capacity is short
-__global__ void k_mark_overflow(const int64_t* __restrict__ need_at, int64_t capacity, int64_t* __restrict__ total) {
-    if (*need_at > capacity) *total = -*need_at;
-}
-
-// ---------------------------------------------------------------- pass 0
-// Per-ray upper bound of the matches: the number of slots the streaming pass
-// will test for the ray (its footprint rows, exactly as stream_group
-// tabulates them).  Places each ray's unsorted-match scratch segment.
-__global__ void __launch_bounds__(kThreads) k_query_bound(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC,
-                                                          int64_t m, int64_t* __restrict__ bound) {
-    __shared__ GroupHead head;
-    __shared__ int acc[kGroupMax];
-    const int s = 2 * pad + 1;
-    for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
-        const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
-        if (threadIdx.x < kGroupMax) acc[threadIdx.x] = 0;
-        group_setup(head, R, QC, r0, G, s);
-        for (int idx = threadIdx.x; idx < s * G; idx += kThreads) {
-            const int row = idx / G, g = idx - row * G;
-            const RayParams& r = head.ray[g];
-            const int y = r.v + row;
-            int x0, x1;
-            if (footprint_row(head.fp[g], QC.C, pad, QC.width, QC.height, r.u, r.v, y, x0, x1)) {
-                const int64_t base = int64_t(y) * wp;
-                const int n = L.row_ptr[base + x1 + 1] - L.row_ptr[base + x0];
-                if (n > 0) atomicAdd(&acc[g], n);
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < G) bound[r0 + threadIdx.x] = acc[threadIdx.x];
-        __syncthreads();
-    }
-}
 
 // ---------------------------------------------------------------- pass 1
 struct FillSmem {
@@ -367,11 +249,6 @@ __global__ void __launch_bounds__(kThreads, HP_SCAN_MINB) k_query_scan(hp_query_
 }
 
 // ---------------------------------------------------------------- sort
-__device__ __forceinline__ bool key_less(double ta, int64_t ia, double tb, int64_t ib) {
-    return ta < tb || (ta == tb && ia < ib);
-}
-
-constexpr int kCoarse = 256;
 
 template <int kCap>
 struct SortSmem {
@@ -391,124 +268,6 @@ struct SortSmem {
     int fcount, fbad;  // per-ray facts for the sampler (see sort_segment)
 };
 
-
-// Block-wide exclusive scan of a[0..n) in place (n <= per * blockDim.x).
-template <int kPer>
-__device__ void block_scan_inplace(int* a, int n, int* sh) {
-    const int tid = threadIdx.x;
-    int v[kPer], acc = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int i = tid * kPer + k;
-        v[k] = i < n ? a[i] : 0;
-        acc += v[k];
-    }
-    int total;
-    int run = block_excl_scan<int>(acc, sh, &total);
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-        const int i = tid * kPer + k;
-        if (i < n) a[i] = run;
-        run += v[k];
-    }
-}
-
-// Sort one ray's q matches by (t, id): read from the fill scratch (st, sid,
-// sd), write the sorted segment to the outputs.  Buckets are equalised: a
-// 256-bin coarse histogram of t over [tmin, tmax] assigns each coarse bin a
-// share of the q fine buckets proportional to its population, and t is
-// placed linearly inside its bin's share.  The map is monotone in t, so
-// buckets are ordered; each element's final position is its bucket start
-// plus its exact (t, id) rank among the (few) members of its bucket.
-// The (t, id) order of q elements staged in shared memory -> perm[0, q):
-// q <= 64 by direct ranks; else an equalised bucket map of t (256-bin coarse
-// histogram over the float bounds [tlo, thi] -> q fine buckets allotted in
-// proportion -> linear inside a bin; fp32, every step monotone) and an exact
-// rank inside each bucket.  hist needs kCap + 1 entries; chist kCoarse + 1
-// (both zeroed by the caller when q > 64).  Ends with a barrier.
-template <int kCap, int kT>
-__device__ void rank_segment(int q, float tlo, float thi, const double* t, const int* id, unsigned* bk, int* hist,
-                             unsigned short* lst, unsigned short* perm, int* chist, int* scan_sh) {
-    const int tid = threadIdx.x;
-    if (q <= 64) {
-        for (int e = tid; e < q; e += kT) {
-            const double te = t[e];
-            const int ie = id[e];
-            int rank = 0;
-            for (int k = 0; k < q; k++) rank += key_less(t[k], id[k], te, ie);
-            perm[rank] = (unsigned short)e;
-        }
-        __syncthreads();
-    } else {
-        const int nb = q;  // fine buckets
-        // float bounds of the segment's t, from the streaming pass (any
-        // monotone bucket map gives the same order: exact in-bucket ranks)
-        // The map is computed in fp32 (each step is monotone under round to
-        // nearest: float(t), - tlo, * scale, fminf), once per element; the
-        // coarse coordinate is kept in bk[] for the fine pass.
-        const float span = thi - tlo;
-        // capped so that 0 * scale stays 0 when the span is tiny
-        const float cscale = span > 0.0f ? fminf(float(kCoarse) / span, FLT_MAX) : 0.0f;
-        for (int e = tid; e < q; e += kT) {
-            const float x = fminf((__double2float_rn(t[e]) - tlo) * cscale, float(kCoarse));
-            bk[e] = __float_as_uint(x);
-            const int b = min(int(x), kCoarse - 1);
-            const unsigned peers = __match_any_sync(__activemask(), b);
-            if (lane_id() == __ffs(peers) - 1) atomicAdd(&chist[b], __popc(peers));
-        }
-        __syncthreads();
-        // coarse prefix counts -> first fine bucket of each coarse bin
-        if (tid < 32) {
-            int run = 0;
-            for (int c0 = 0; c0 < kCoarse; c0 += 32) {
-                const int v = chist[c0 + tid];
-                const int inc = warp_incl_scan(v);
-                chist[c0 + tid] = int((int64_t(run + inc - v) * nb) / q);
-                run += __shfl_sync(0xffffffffu, inc, 31);
-            }
-            if (tid == 0) chist[kCoarse] = nb;
-        }
-        __syncthreads();
-        for (int e = tid; e < q; e += kT) {
-            const float x = __uint_as_float(bk[e]);
-            const int b = min(int(x), kCoarse - 1);
-            const int f0 = chist[b], width = chist[b + 1] - f0;
-            int f = f0;
-            if (width > 1) {
-                // x - b is exact (Sterbenz) and in [0, 1]
-                const int off = int((x - float(b)) * float(width));
-                f += min(off, width - 1);
-            }
-            f = min(f, nb - 1);
-            const int li = atomicAdd(&hist[f], 1);
-            bk[e] = (unsigned(f) << 16) | unsigned(li);
-        }
-        __syncthreads();
-        block_scan_inplace<(kCap + kT - 1) / kT>(hist, nb, scan_sh);
-        __syncthreads();
-        for (int e = tid; e < q; e += kT) {
-            const unsigned be_k = bk[e];
-            lst[hist[be_k >> 16] + (be_k & 0xffffu)] = (unsigned short)e;
-        }
-        __syncthreads();
-        for (int e = tid; e < q; e += kT) {
-            const unsigned be_k = bk[e];
-            const int bs = hist[be_k >> 16];
-            const int be = (int(be_k >> 16) + 1 < nb) ? hist[(be_k >> 16) + 1] : q;
-            int rank = 0;
-            if (be - bs > 1) {
-                const double te = t[e];
-                const int ie = id[e];
-                for (int k = bs; k < be; k++) {
-                    const int o = lst[k];
-                    rank += key_less(t[o], id[o], te, ie);
-                }
-            }
-            perm[bs + rank] = (unsigned short)e;
-        }
-        __syncthreads();
-    }
-}
 
 // IdT: int32 (the match scratch) or int64 (in place in the output arrays,
 // for the parts of split rays: every input is in shared memory before the
@@ -625,344 +384,6 @@ __global__ void __launch_bounds__(kT, (kCap == 2048 && kT == 512) ? 4 : 0) k_que
     }
 }
 
-
-// ---------------------------------------------------------------- prefix sort
-// For callers that only want samples (pipeline frames): each ray's
-// smallest-t matches -- all of them when they fit (<= kPrefixCap), else
-// everything through the histogram bin where the count reaches `want` (at
-// most kPrefixCap) -- sorted by (t, id) in place at the
-// front of the ray's match scratch (t, id, dist), the sampler's facts over
-// that prefix, and two cuts for the matches left out: their smallest t
-// (every one is strictly above the prefix's last t) and their smallest dist.
-// The sampler runs on these prefixes and flags a ray whose work would reach
-// past its prefix (hp_sample_run_prefix).
-#ifndef HP_PREFIX_U
-#define HP_PREFIX_U 2
-#endif
-#ifndef HP_PREFIX_MINB
-#define HP_PREFIX_MINB 6  // 40 registers: 6 CTAs per SM (the shared-memory limit)
-#endif
-constexpr int kPrefixCap = 1024;
-constexpr int kPrefixThreads = 256;
-
-// The selection map of a ray (shared by k_prefix_select and k_query_prefix:
-// the same float operations, so both see the same bins).
-struct SelMap {
-    float tlo, scale;
-    __device__ __forceinline__ SelMap(uint2 mm, int bins) {
-        tlo = from_fkey(mm.x);
-        const float span = from_fkey(mm.y) - tlo;
-        scale = span > 0.0f ? fminf(float(bins) / span, FLT_MAX) : 0.0f;
-    }
-    __device__ __forceinline__ int bin(double t, int bins) const {
-        return min(int(fminf((__double2float_rn(t) - tlo) * scale, float(bins))), bins - 1);
-    }
-};
-
-// Selection of the long rays (more than kCap matches), one warp per ray
-// (many rays in flight: this pass is a plain stream over t): a kBins-bin
-// histogram of t -> the first bin where the running count reaches want
-// (the one before it if that bin alone overflows kCap), and the count up
-// to it.  sel[r] = (bin, count).
-template <int kBins, int kCap>
-__global__ void __launch_bounds__(128) k_prefix_select(const int64_t* __restrict__ off,
-                                                       const int64_t* __restrict__ soff,
-                                                       const uint2* __restrict__ tmm, int64_t m, int want,
-                                                       const double* __restrict__ st, int2* __restrict__ sel,
-                                                       const int* __restrict__ list, const int* __restrict__ list_n) {
-    __shared__ int hist[4][kBins];
-    int* H = hist[warp_id()];
-    const int lane = lane_id();
-    const int64_t warps = int64_t(gridDim.x) * 4;
-    const int64_t nr = list ? int64_t(*list_n) : m;  // candidate rays (a class list, or all)
-    for (int64_t k = int64_t(blockIdx.x) * 4 + warp_id(); k < nr; k += warps) {
-        const int64_t r = list ? int64_t(list[k]) : k;
-        const int q = int(off[r + 1] - off[r]);
-        if (q <= kCap) continue;
-        const int64_t so = soff[r];
-        const SelMap M(tmm[r], kBins);
-        for (int k = lane; k < kBins; k += 32) H[k] = 0;
-        __syncwarp();
-        for (int e0 = 0; e0 < q; e0 += 128) {  // four loads per lane in flight
-            double tv[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int e = e0 + u * 32 + lane;
-                tv[u] = e < q ? st[so + e] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (e0 + u * 32 + lane < q) atomicAdd(&H[M.bin(tv[u], kBins)], 1);
-        }
-        __syncwarp();
-        constexpr int kPer = kBins / 32;  // lane owns bins [lane * kPer, lane * kPer + kPer)
-        int sum = 0;
-#pragma unroll 8
-        for (int k = 0; k < kPer; k++) sum += H[lane * kPer + k];
-        const int incl = warp_incl_scan(sum);
-        const unsigned hit = __ballot_sync(0xffffffffu, incl >= want);
-        const int owner = __ffs(hit) - 1;  // exists: the total q > kCap >= want
-        if (lane == owner) {
-            int c = incl - sum, b = lane * kPer;
-            for (int k = 0; k < kPer; k++) {
-                c += H[lane * kPer + k];
-                if (c >= want) {
-                    b = lane * kPer + k;
-                    break;
-                }
-            }
-            int L = c;
-            if (L > kCap) {  // that bin alone overflows: stop before it
-                L -= H[b];
-                b -= 1;
-            }
-            sel[r] = make_int2(b, L);
-        }
-        __syncwarp();
-    }
-}
-
-constexpr int kPrefixSmall = 512;  // rays up to this go to a smaller, denser CTA configuration
-
-// Prefix-mode ray classes: list 0 = rays of 1..kSmall matches, list 1 = the
-// longer ones (warp-aggregated appends); empty rays get their outputs here.
-template <int kSmall>
-__global__ void k_prefix_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
-                                 int* __restrict__ counts, int* __restrict__ plen, int* __restrict__ facts,
-                                 double* __restrict__ cut_t, double* __restrict__ cut_d) {
-    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
-         r += int64_t(gridDim.x) * blockDim.x) {
-        int cls = -1;
-        if (r < m) {
-            const int64_t q = off[r + 1] - off[r];
-            cls = q == 0 ? -1 : (q <= kSmall ? 0 : 1);
-            if (q == 0) {
-                plen[r] = 0;
-                facts[r] = -1;
-                cut_t[r] = cut_d[r] = CUDART_INF;
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 2; c++) {
-            const unsigned b = __ballot_sync(0xffffffffu, cls == c);
-            if (!b) continue;
-            int base = 0;
-            if (lane_id() == __ffs(b) - 1) base = atomicAdd(&counts[c], __popc(b));
-            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
-            if (cls == c) lists[int64_t(c) * m + base + __popc(b & ((1u << lane_id()) - 1))] = int(r);
-        }
-    }
-}
-
-template <int kCap>
-struct PrefixSmem {
-    double t[kCap];
-    double d2[kCap];
-    int id[kCap];
-    unsigned bk[kCap];
-    int hist[kCap + 1];  // selection histogram (kCap bins), then the fine buckets
-    unsigned short lst[kCap], perm[kCap];
-    int chist[kCoarse + 1];
-    int scan_sh[33];
-    unsigned long long cut_t, cut_d2;  // order keys of the left-out minima
-    int cnt, bsel, fcount, fbad;
-};
-
-__device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving key
-    const unsigned long long b = __double_as_longlong(x);
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double dkey_inv(unsigned long long k) {
-    return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
-}
-
-// Per ray (one CTA): a ray of <= kCap matches is staged whole with cp.async;
-// a longer one gets its selected bin from k_prefix_select (sel; without it,
-// a kCap-bin histogram pass here) and is staged through registers (selected
-// -> shared memory; the others give the cuts and the finiteness check);
-// then rank_segment and the write-out, in place, with the facts counted over
-// the prefix (a prefix count >= K implies the full one; the sampler checks
-// the cuts before trusting a smaller one).
-template <int kCap, int kT>
-__global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_PREFIX_MINB) k_query_prefix(
-    const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const uint2* __restrict__ tmm, int64_t m,
-    int want, const double* __restrict__ slopes, int* __restrict__ facts, int* __restrict__ plen,
-    double* __restrict__ cut_t, double* __restrict__ cut_d, double* st, int* sid, double* sd,
-    const int2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n) {
-    extern __shared__ __align__(16) unsigned char dyn[];
-    PrefixSmem<kCap>& F = *reinterpret_cast<PrefixSmem<kCap>*>(dyn);
-    constexpr int kBins = kCap;
-    const int tid = threadIdx.x;
-    const int64_t nr = list ? int64_t(*list_n) : m;  // this launch's rays (a class list, or all)
-    for (int64_t k = blockIdx.x; k < nr; k += gridDim.x) {
-        const int64_t r = list ? int64_t(list[k]) : k;
-        const int64_t so = soff[r];
-        const int q = int(off[r + 1] - off[r]);
-        if (q == 0) {
-            if (tid == 0) {
-                plen[r] = 0;
-                facts[r] = -1;
-                cut_t[r] = cut_d[r] = CUDART_INF;
-            }
-            continue;
-        }
-        const float tlo = from_fkey(tmm[r].x), thi = from_fkey(tmm[r].y);
-        const SelMap M(tmm[r], kBins);
-        const float sel_scale = M.scale;
-        auto sel_bin = [&](double t) { return M.bin(t, kBins); };
-        // rays that fit are sorted whole: cheaper than a selection pass
-        // (cfg2 6.9 -> 6.6 ms, cfg3 -3%) and never flagged
-        const bool all = q <= kCap;
-        int bsel = kBins - 1, L = q;
-        if (tid == 0) {
-            F.cnt = F.fcount = F.fbad = 0;
-            F.cut_t = F.cut_d2 = ~0ull;
-        }
-        // the ray's matches in chunks of kU per thread, every load of a chunk
-        // in flight at once (a ray of <= kChunk matches stays in registers
-        // from the histogram to the staging)
-        constexpr int kU = HP_PREFIX_U, kChunk = kT * kU;
-        double tv[kU], dv[kU];
-        int iv[kU];
-        const bool single = q <= kChunk;
-        auto load_chunk = [&](int c0, bool full) {
-#pragma unroll
-            for (int u = 0; u < kU; u++) {
-                const int e = c0 + u * kT + tid;
-                if (e < q) {
-                    tv[u] = st[so + e];
-                    if (full) {
-                        dv[u] = sd[so + e];
-                        iv[u] = sid[so + e];
-                    }
-                }
-            }
-        };
-        if (all) {  // the whole segment straight into shared memory, every load in flight
-            for (int e = tid; e < q; e += kT) {
-                cp_async8(&F.t[e], st + so + e);
-                cp_async4(&F.id[e], sid + so + e);
-                cp_async8(&F.d2[e], sd + so + e);
-            }
-            cp_commit();
-        } else if (single) {
-            load_chunk(0, true);
-        }
-        if (!all && sel) {  // selected by k_prefix_select
-            const int2 sv = sel[r];
-            bsel = sv.x;
-            L = sv.y;
-        } else if (!all) {
-            for (int k = tid; k <= kBins; k += kT) F.hist[k] = 0;
-            if (tid == 0) F.bsel = kBins;
-            __syncthreads();
-            for (int c0 = 0; c0 < q; c0 += kChunk) {
-                if (!single) load_chunk(c0, false);
-#pragma unroll
-                for (int u = 0; u < kU; u++) {
-                    const int e = c0 + u * kT + tid;
-                    const int b = e < q ? sel_bin(tv[u]) : kBins;
-                    const unsigned peers = __match_any_sync(0xffffffffu, b);
-                    if (e < q && lane_id() == __ffs(peers) - 1) atomicAdd(&F.hist[b], __popc(peers));
-                }
-            }
-            __syncthreads();
-            block_scan_inplace<(kBins + kT - 1) / kT>(F.hist, kBins, F.scan_sh);
-            if (tid == 0) F.hist[kBins] = q;
-            __syncthreads();
-            // first bin whose cumulative count reaches `want`
-            for (int b = tid; b < kBins; b += kT)
-                if (F.hist[b + 1] >= want) atomicMin(&F.bsel, b);
-            __syncthreads();
-            bsel = F.bsel;
-            L = F.hist[bsel + 1];
-            if (L > kCap) {  // that bin alone overflows: stop before it
-                bsel -= 1;
-                L = bsel >= 0 ? F.hist[bsel + 1] : 0;
-            }
-        }
-        for (int k = tid; k <= kCoarse; k += kT) F.chist[k] = 0;
-        cp_wait<0>();
-        __syncthreads();
-        // stage the selected matches (the smallest L by t); the others give
-        // the cuts; every value is checked finite
-        bool bad = false;
-        unsigned long long kt = ~0ull, kd = ~0ull;
-        if (all) {
-            for (int e = tid; e < q; e += kT) {
-                const double te = F.t[e], d2 = F.d2[e];
-                bad |= !(fabs(te) <= DBL_MAX) || !(d2 >= 0.0) || !(d2 <= DBL_MAX);
-            }
-        }
-        for (int c0 = 0; c0 < (all ? 0 : q); c0 += kChunk) {
-            if (!single) load_chunk(c0, true);
-#pragma unroll
-            for (int u = 0; u < kU; u++) {
-                const int e = c0 + u * kT + tid;
-                bool in = false;
-                if (e < q) {
-                    in = all || sel_bin(tv[u]) <= bsel;
-                    bad |= !(fabs(tv[u]) <= DBL_MAX) || !(dv[u] >= 0.0) || !(dv[u] <= DBL_MAX);
-                    if (!in) {
-                        kt = min(kt, dkey(tv[u]));
-                        kd = min(kd, dkey(dv[u]));
-                    }
-                }
-                const unsigned b = __ballot_sync(0xffffffffu, in);
-                int base = 0;
-                if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (in) {
-                    const int slot = base + __popc(b & ((1u << lane_id()) - 1));
-                    F.t[slot] = tv[u];
-                    F.id[slot] = iv[u];
-                    F.d2[slot] = dv[u];
-                }
-            }
-        }
-        const bool anybad = __any_sync(0xffffffffu, bad);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            kt = min(kt, __shfl_xor_sync(0xffffffffu, kt, o));
-            kd = min(kd, __shfl_xor_sync(0xffffffffu, kd, o));
-        }
-        if (lane_id() == 0) {
-            if (anybad) atomicOr(&F.fbad, 1);
-            if (kt != ~0ull) {
-                atomicMin(&F.cut_t, kt);
-                atomicMin(&F.cut_d2, kd);
-            }
-        }
-        for (int k = tid; k <= L; k += kT) F.hist[k] = 0;
-        __syncthreads();
-        if (L > 0) {  // bounds of the selected t (any bounds keep the map monotone)
-            const float hi = all ? thi : tlo + float(bsel + 1) / sel_scale;
-            rank_segment<kCap, kT>(L, tlo, hi, F.t, F.id, F.bk, F.hist, F.lst, F.perm, F.chist, F.scan_sh);
-        }
-        // the sorted prefix, in place (the ray's matches were all read above)
-        const double r0 = L > 0 ? dmul(__ldcg(slopes + r), F.t[F.perm[0]]) : 0.0;
-        int cnt = 0;
-        for (int p = tid; p < L; p += kT) {
-            const int e = F.perm[p];
-            const double d = sqrt(F.d2[e]);
-            st[so + p] = F.t[e];
-            sid[so + p] = F.id[e];
-            sd[so + p] = d;
-            cnt += d <= r0;
-        }
-        cnt = warp_sum(cnt);
-        if (lane_id() == 0 && cnt) atomicAdd(&F.fcount, cnt);
-        __syncthreads();
-        if (tid == 0) {
-            plen[r] = L;
-            facts[r] = (F.fbad || L == 0) ? -1 : F.fcount;
-            const bool rest = F.cut_t != ~0ull;
-            cut_t[r] = rest ? dkey_inv(F.cut_t) : CUDART_INF;
-            cut_d[r] = rest ? sqrt(dkey_inv(F.cut_d2)) : CUDART_INF;
-        }
-        __syncthreads();
-    }
-}
 
 // ---------------------------------------------------------------- huge rays
 // Rays with more than kSortHuge matches: one CTA per ray splits the ray's
@@ -1133,61 +554,6 @@ __global__ void __launch_bounds__(kT) k_query_sort_parts(const Part* __restrict_
     }
 }
 
-
-// Resident CTAs per SM of a kernel at its block size / dynamic smem (>= 1).
-template <class K>
-int resident(K kernel, int threads, size_t smem) {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) {
-        cudaGetLastError();
-        n = 1;
-    }
-    return n;
-}
-
-template <class K>
-int set_smem(K kernel, size_t bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    return e == cudaSuccess ? HP_OK : cuda_status(e, "cudaFuncSetAttribute");
-}
-
-QCam make_qcam(const hp_camera* cam) {
-    QCam q{};
-    q.has_cam = cam != nullptr;
-    if (cam) {
-        for (int k = 0; k < 3; k++) {
-            q.C.r[k] = cam->right[k];
-            q.C.u[k] = cam->up[k];
-            q.C.f[k] = cam->forward[k];
-        }
-        q.C.focal = cam->focal_length;
-        q.C.pw = cam->pixel_width;
-        q.C.ph = cam->pixel_height;
-        q.C.half_w = 0.5 * double(cam->width);
-        q.C.half_h = 0.5 * double(cam->height);
-        q.width = int(cam->width);
-        q.height = int(cam->height);
-    }
-    return q;
-}
-
-int check_common(const hp_query_layout& L, int64_t pad, int64_t m) {
-    if (pad < 0 || m < 0 || !L.row_ptr) {
-        set_error("hp_query: invalid arguments");
-        return HP_EINVAL;
-    }
-    if (2 * pad + 1 > 0xFFFF) {
-        set_error("hp_query: kernel too large");
-        return HP_EINVAL;
-    }
-    return HP_OK;
-}
-
-unsigned group_grid(int64_t m, int per_sm) {
-    const int64_t groups = (m + kGroupMax - 1) / kGroupMax;
-    const int64_t cap = int64_t(kNumSMs) * per_sm;
-    return unsigned(groups < cap ? (groups > 0 ? groups : 1) : cap);
-}
 
 }  // namespace
 }  // namespace hp
@@ -1381,66 +747,3 @@ extern "C" int hp_query_bounds(hp_query_layout layout, const hp_camera* cam, int
     return HP_OK;
 }
 
-extern "C" int hp_query_prefix(const int64_t* offsets, int64_t m, int32_t want, const double* slopes,
-                               int32_t* facts, int32_t* plen, double* cut_t, double* cut_d, int64_t capacity,
-                               void* workspace, size_t workspace_bytes, hp_query_prefix_view* view,
-                               hp_stream_t stream) {
-    if (m < 0 || want < 1 || want > kPrefixCap || (m > 0 && (!slopes || !facts || !plen || !cut_t || !cut_d))) {
-        set_error("hp_query_prefix: invalid arguments (1 <= want <= %d)", kPrefixCap);
-        return HP_EINVAL;
-    }
-    Carver cv(workspace, workspace_bytes);
-    QueryWs w = carve_query(cv, m, capacity);
-    if (!cv.ok()) {
-        set_error("hp_query_prefix: workspace too small");
-        return HP_ESPACE;
-    }
-    if (view) {
-        view->start = w.soff;
-        view->t = w.st;
-        view->ids = w.sid;
-        view->dist = w.sd;
-    }
-    if (m == 0) return HP_OK;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    constexpr auto kern = k_query_prefix<kPrefixCap, kPrefixThreads>;
-    static const int occ = [] {  // once (thread-safe)
-        set_smem(kern, sizeof(PrefixSmem<kPrefixCap>));
-        return resident(kern, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>));
-    }();
-    // classes: rays of 1..kPrefixSmall matches / longer ones (the empty rays'
-    // outputs are written here)
-    int* lists = w.lists + 2 * m;  // after sel (2m ints); the region holds 5m
-    const int* list_small = lists;
-    const int* list_big = lists + m;
-    if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
-        return cuda_status(cudaGetLastError(), "hp_query_prefix memset");
-    k_prefix_classes<kPrefixSmall><<<grid_for(m, 256), 256, 0, s>>>(offsets, m, lists, w.counts, plen, facts, cut_t,
-                                                                    cut_d);
-    HP_CHECK_LAUNCH("k_prefix_classes");
-    // the selected bin of every ray longer than kPrefixCap (warp per ray)
-    int2* sel = reinterpret_cast<int2*>(w.lists);  // (unused by prefix mode otherwise; 2m ints)
-    {
-        constexpr auto kselect = k_prefix_select<kPrefixCap, kPrefixCap>;
-        static const int occ_sel = resident(kselect, 128, 0);  // once (thread-safe)
-        TimedSpan tss("k_prefix_select", s);
-        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.tmm, m, want, w.st, sel, list_big,
-                                                  w.counts + 1);
-        HP_CHECK_LAUNCH("k_prefix_select");
-    }
-    constexpr auto ksmall = k_query_prefix<kPrefixSmall, 128>;
-    static const int occ_small = [] {  // once (thread-safe)
-        set_smem(ksmall, sizeof(PrefixSmem<kPrefixSmall>));
-        return resident(ksmall, 128, sizeof(PrefixSmem<kPrefixSmall>));
-    }();
-    TimedSpan ts("k_query_prefix", s);
-    ksmall<<<kNumSMs * occ_small, 128, sizeof(PrefixSmem<kPrefixSmall>), s>>>(
-        offsets, w.soff, w.tmm, m, want, slopes, facts, plen, cut_t, cut_d, w.st, w.sid, w.sd, nullptr, list_small,
-        w.counts);
-    HP_CHECK_LAUNCH("k_query_prefix small");
-    kern<<<kNumSMs * occ, kPrefixThreads, sizeof(PrefixSmem<kPrefixCap>), s>>>(offsets, w.soff, w.tmm, m, want, slopes,
-                                                                             facts, plen, cut_t, cut_d, w.st, w.sid,
-                                                                             w.sd, sel, list_big, w.counts + 1);
-    HP_CHECK_LAUNCH("k_query_prefix");
-    return HP_OK;
-}

@@ -73,7 +73,7 @@ class DeviceIndex:
 
     def __init__(self, camera, pad, padded_width, padded_height, n_in_dev, table_start, table_count,
                  reordered_ids, slot_x, slot_y, slot_z, row_ptr, rel_x, rel_y, rel_z, point_id, relf,
-                 n_in=None):
+                 rel4, n_in=None):
         self.camera = camera
         self.pad = pad
         self.padded_width = padded_width
@@ -83,7 +83,7 @@ class DeviceIndex:
         self.table_start, self.table_count = table_start, table_count
         self._rid, self._sx, self._sy, self._sz = reordered_ids, slot_x, slot_y, slot_z
         self.row_ptr, self.rel_x, self.rel_y, self.rel_z = row_ptr, rel_x, rel_y, rel_z
-        self.point_id, self.relf = point_id, relf
+        self.point_id, self.relf, self.rel4 = point_id, relf, rel4
 
     @property
     def n_in(self) -> int:
@@ -98,7 +98,7 @@ class DeviceIndex:
 
     def layout(self) -> _lib.Layout:
         return _lib.Layout(_ptr(self.row_ptr), _ptr(self.rel_x), _ptr(self.rel_y),
-                           _ptr(self.rel_z), _ptr(self.point_id), _ptr(self.relf))
+                           _ptr(self.rel_z), _ptr(self.point_id), _ptr(self.relf), _ptr(self.rel4))
 
 
 def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
@@ -125,16 +125,17 @@ def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
     rx, ry, rz = (torch.empty(cap, **f64) for _ in range(3))
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
     rf = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    r4 = torch.empty((cap, 4), **f64)
     n_in_d = torch.zeros(1, **i64)
     _mark("build.setup")
-    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf))
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf), _ptr(r4))
     cam = camera_struct(camera)
     _lib.check(lib.hp_build(_ptr(xyz), n, ctypes.byref(cam), pad, _ptr(ts), _ptr(tc), _ptr(rid),
                             _ptr(sx), _ptr(sy), _ptr(sz), L, _ptr(n_in_d), _ptr(ws), nb.value,
                             _stream()))
     _mark("build.kernels")
     return DeviceIndex(camera, pad, wp, hp, n_in_d, ts, tc, rid, sx, sy, sz, row_ptr, rx, ry, rz,
-                       pid, rf, n_in=0 if n == 0 else None)
+                       pid, rf, r4, n_in=0 if n == 0 else None)
 
 
 def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered_ids, camera,
@@ -151,16 +152,17 @@ def build_from_table(table_start, table_count, slot_x, slot_y, slot_z, reordered
     rx, ry, rz = (torch.empty(cap, dtype=torch.float64, device=dev) for _ in range(3))
     pid = torch.empty(cap, dtype=torch.int32, device=dev)
     rf = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    r4 = torch.empty((cap, 4), dtype=torch.float64, device=dev)
     nb = c_size(0)
     _lib.check(lib.hp_layout_workspace_bytes(n_in, wp, hp, ctypes.byref(nb)))
     ws = _workspace(nb.value, dev)
     origin = (ctypes.c_double * 3)(*[float(v) for v in np.asarray(camera.origin)])
-    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf))
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf), _ptr(r4))
     _lib.check(lib.hp_layout_from_table(_ptr(table_start), _ptr(table_count), _ptr(slot_x),
                                         _ptr(slot_y), _ptr(slot_z), _ptr(reordered_ids), n_in, wp,
                                         hp, origin, L, _ptr(ws), nb.value, _stream()))
     return DeviceIndex(camera, pad, wp, hp, None, table_start, table_count, reordered_ids, slot_x,
-                       slot_y, slot_z, row_ptr, rx, ry, rz, pid, rf, n_in=n_in)
+                       slot_y, slot_z, row_ptr, rx, ry, rz, pid, rf, r4, n_in=n_in)
 
 
 class MatchBudgetExceeded(RuntimeError):
@@ -191,11 +193,9 @@ def query_bounds(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
     return out
 
 
-def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, long_cut=None):
+def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
     """hp_query_count with the workspace sized (retrying once); returns
-    (offsets, probes, scanned, total, workspace, workspace bytes, capacity,
-    long_total): long_total = the matches of rays with more than ``long_cut``
-    (read with the total, one synchronisation; None without ``long_cut``)."""
+    (offsets, probes, scanned, total, workspace, workspace bytes, capacity)."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
     m = int(pixels.shape[0])
@@ -219,13 +219,7 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, l
         _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap, _ptr(ws),
                                       nb.value, _stream()))
         _mark("query.count")
-        long_total = None
-        if long_cut is not None and m > 0:
-            qd = offsets[1:] - offsets[:-1]
-            both = torch.stack([offsets[m], torch.where(qd > long_cut, qd, 0).sum()]).cpu()
-            total, long_total = int(both[0]), int(both[1])
-        else:
-            total = int(offsets[m].item())
+        total = int(offsets[m].item())
         if total >= 0:
             break
         needed = -total  # scratch too small: nothing was written, grow it once (and remember)
@@ -236,7 +230,7 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, l
             cap = min(cap, int(max_scratch))
         if cap > _QUERY_CAP.get(dev, 0):  # only grow: a small query (e.g. the re-run of a
             _QUERY_CAP[dev] = cap         # frame's flagged rays) must not shrink the frame's size
-    return offsets, probes, scanned, total, ws, nb.value, cap, long_total
+    return offsets, probes, scanned, total, ws, nb.value, cap
 
 
 def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
@@ -259,7 +253,7 @@ def _fill(index, counted, slopes, facts):
     """hp_query_fill after :func:`_count`: the (t, id)-sorted CSR."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
-    offsets, probes, scanned, total, ws, nb, cap, _ = counted
+    offsets, probes, scanned, total, ws, nb, cap = counted
     m = int(offsets.shape[0]) - 1
     ids = torch.empty(total, dtype=torch.int64, device=dev)
     t = torch.empty(total, dtype=torch.float64, device=dev)
@@ -277,10 +271,10 @@ def _fill(index, counted, slopes, facts):
 
 class QueryPrefix:
     """Result of :func:`query_prefix`: the full match counts (``offsets``)
-    and, per ray, the (t, id)-sorted head of its matches inside the query
-    workspace (``start``, ``length``; ``t``, ``ids`` int32, ``dist``), the
-    smallest t / dist of the matches left out (``cut_t``, ``cut_d``), and
-    the sampler's facts over all matches.  Keeps the workspace alive."""
+    and, per ray, the (t, id)-sorted head of its matches (``start``,
+    ``length``; ``t``, ``ids`` int32, ``dist``), lower bounds of the t / dist
+    of the matches left out (``cut_t``, ``cut_d``), and the sampler's facts
+    over the head.  Keeps the query workspace alive."""
 
     def __init__(self, offsets, probes, scanned, start, length, t, ids, dist, cut_t, cut_d, facts, ws):
         self.offsets, self.probes, self.scanned = offsets, probes, scanned
@@ -297,65 +291,91 @@ class QueryPrefix:
 
 
 PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "512"))  # head length the sampler usually needs
+HEAD_CAP = 1024  # longest head (hp_head.cu kHeadCap)
+
+
+def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
+    """hp_head_count with the workspace sized (retrying once); returns
+    (offsets, head_off, probes, scanned, Q, head capacity, workspace, bytes,
+    capacity) -- Q and the head capacity read in one synchronisation."""
+    lib = _lib.load(require_device=True)
+    dev = index.table_start.device
+    m = int(pixels.shape[0])
+    nb = c_size(0)
+    offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    head_off = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    probes = torch.empty(m, dtype=torch.int64, device=dev)
+    scanned = torch.empty(m, dtype=torch.int64, device=dev)
+    cam = ctypes.byref(camera_struct(index.camera)) if footprint else None
+    args = (index.layout(), cam, index.padded_width, index.padded_height, index.pad, _ptr(pixels), 2,
+            _ptr(dirs), _ptr(t_near), _ptr(t_far), _ptr(slopes), m)
+    cap = min(_QUERY_CAP.get(dev, 0), 4096 * max(m, 1))
+    if max_scratch is not None:
+        cap = min(cap, int(max_scratch))
+    _mark("query.setup")
+    for _ in range(2):
+        _lib.check(lib.hp_head_workspace_bytes(m, cap, ctypes.byref(nb)))
+        ws = _workspace(nb.value, dev)
+        _lib.check(lib.hp_head_count(*args, _ptr(offsets), _ptr(head_off), _ptr(probes), _ptr(scanned), cap,
+                                     _ptr(ws), nb.value, _stream()))
+        _mark("query.count")
+        both = torch.stack([offsets[m], head_off[m]]).cpu()  # one synchronisation
+        total, hcap = int(both[0]), int(both[1])
+        if total >= 0:
+            break
+        needed = -total
+        if max_scratch is not None and needed > max_scratch:
+            raise MatchBudgetExceeded(needed, int(max_scratch))
+        cap = int(needed * 1.0625) + 1024
+        if max_scratch is not None:
+            cap = min(cap, int(max_scratch))
+        if cap > _QUERY_CAP.get(dev, 0):
+            _QUERY_CAP[dev] = cap
+    return offsets, head_off, probes, scanned, total, hcap, ws, nb.value, cap
 
 
 def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
                  t_far: torch.Tensor, slopes: torch.Tensor, want: int = PREFIX_WANT, footprint: bool = True,
                  max_scratch: int | None = None) -> QueryPrefix:
-    """The query for callers that only want samples (hp_query_prefix): each
-    ray's smallest-t matches sorted in place, no CSR of all matches."""
+    """The query for callers that only want samples (hp_head_count +
+    hp_head_sort): each ray's head of matches in (t, id) order, without the
+    CSR of all matches."""
     pixels, dirs = pixels.contiguous(), dirs.contiguous()
-    return _prefix(index, _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch), slopes,
-                   want)
+    return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch), dirs,
+                 slopes, want)
 
 
-def _prefix(index, counted, slopes, want=PREFIX_WANT) -> QueryPrefix:
-    """hp_query_prefix after :func:`_count`."""
+def _head(index, counted, dirs, slopes, want=PREFIX_WANT) -> QueryPrefix:
+    """hp_head_sort after :func:`_count_head`."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
-    offsets, probes, scanned, total, ws, nb, cap, _ = counted
+    offsets, head_off, probes, scanned, total, hcap, ws, nb, cap = counted
     m = int(offsets.shape[0]) - 1
     fa = torch.empty(m, dtype=torch.int32, device=dev)
     plen = torch.empty(m, dtype=torch.int32, device=dev)
     cut = torch.empty((2, m), dtype=torch.float64, device=dev)
-    view = _lib.PrefixView()
-    _lib.check(lib.hp_query_prefix(_ptr(offsets), m, int(want), _ptr(slopes), _ptr(fa), _ptr(plen),
-                                   _ptr(cut[0]), _ptr(cut[1]), cap, _ptr(ws), nb, ctypes.byref(view),
-                                   _stream()))
+    ht = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
+    hd = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
+    hi = torch.empty(max(hcap, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(offsets), _ptr(head_off),
+                                int(want), _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa), _ptr(cut[0]),
+                                _ptr(cut[1]), cap, _ptr(ws), nb, _stream()))
     _mark("query.prefix")
-
-    def wrap(ptr, dtype, n):  # device view into the workspace (kept alive by QueryPrefix)
-        if n == 0 or not ptr:
-            return torch.empty(0, dtype=dtype, device=dev)
-        off = ptr - ws.data_ptr()
-        return ws[off:off + n * torch.empty(0, dtype=dtype).element_size()].view(dtype)
-
-    pre = QueryPrefix(offsets, probes, scanned, wrap(view.start, torch.int64, m), plen,
-                      wrap(view.t, torch.float64, cap), wrap(view.ids, torch.int32, cap),
-                      wrap(view.dist, torch.float64, cap), cut[0], cut[1], fa, ws)
+    pre = QueryPrefix(offsets, probes, scanned, head_off[:m], plen, ht, hi, hd, cut[0], cut[1], fa, ws)
     pre.total = total
     return pre
 
 
-# Prefix mode pays off when long rays (more matches than the prefix kernel
-# sorts whole) carry a good share of the frame's matches (cfg2: most; cfg3
-# planes at q <= 1114: almost none, and the size-class sorts are faster there)
-PREFIX_CAP = 1024
-PREFIX_AUTO_SHARE = 0.25
-
-
 def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix: bool | None = None,
                 max_scratch: int | None = None, want: int = PREFIX_WANT):
-    """Count, then either the prefix sort (returns a :class:`QueryPrefix`) or
-    the full CSR with facts (returns the 7-tuple of :func:`query`).
-    ``prefix=None`` decides from the count: prefix mode when rays of more
-    than PREFIX_CAP matches hold more than PREFIX_AUTO_SHARE of them."""
+    """The query of a sampling frame: the heads (``prefix`` True or None;
+    returns a :class:`QueryPrefix`) or the full CSR with facts (``prefix``
+    False; returns the 7-tuple of :func:`query`)."""
     pixels, dirs = pixels.contiguous(), dirs.contiguous()
-    c = _count(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch,
-               long_cut=PREFIX_CAP if prefix is None else None)
-    if prefix is None:
-        prefix = c[3] > 0 and c[7] > PREFIX_AUTO_SHARE * c[3]
-    return _prefix(index, c, slopes, want) if prefix else _fill(index, c, slopes, True)
+    if prefix is False:
+        return _fill(index, _count(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), slopes, True)
+    return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), dirs, slopes,
+                 want)
 
 
 def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerParams:

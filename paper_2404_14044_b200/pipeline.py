@@ -85,9 +85,9 @@ class FrameResult:
 
 # bytes of device memory per match slot of one query + sample pass, for
 # sizing ray chunks: unsorted scratch 20 + CSR 24 + sampler scratch (bounded);
-# prefix mode keeps only the scratch
+# head mode: (key, slot) scratch 8 + at most one 20-byte head entry
 BYTES_PER_MATCH = 56
-BYTES_PER_MATCH_PREFIX = 24
+BYTES_PER_MATCH_PREFIX = 28
 
 
 _BUDGET: dict = {}
@@ -144,50 +144,64 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
                          exact_t_end, max_matches, mark)
 
 
-# Frames that only want samples sort each ray's head of matches only
-# (device.query_prefix + device.sample_prefix: no query CSR); rays whose
-# sampling may reach past the head re-run through the full query.  Measured
-# at least as fast as the full-CSR path on every workload (cfg2 -10%, cfg3
-# -10%, cfg4 -44%, cfg1 equal), with 24 instead of 56 bytes per match slot.
-# HP_PREFIX=0 uses the full CSR, HP_PREFIX=auto picks per frame from the
-# counts (device.query_frame).
+# Frames that only want samples keep 8 bytes per match and sort each ray's
+# head only (device.query_prefix = hp_head_count + hp_head_sort, then
+# device.sample_prefix: no query CSR); rays whose sampling may reach past the
+# head re-run through the full query.  HP_PREFIX=0 uses the full CSR.
 _PREFIX_ENV = os.environ.get("HP_PREFIX", "1")
-PREFIX = None if _PREFIX_ENV == "auto" else _PREFIX_ENV != "0"
+PREFIX = _PREFIX_ENV != "0"
 
 
 _PREFIX_LEN: list = []  # prefix lengths of the passes of the current frame (device scalars)
 TRACK_PREFIX_LEN = False  # bench.py: report Σ prefix length (one extra reduction per pass)
 
 
-def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end):
-    """Sample over the prefixes of ``pre``; rays whose sampling may reach past
-    their head re-run through the full query.  (samples 9-tuple, Q, flagged)"""
+def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None):
+    """Sample over the heads of ``pre``; rays whose sampling may reach past
+    their head re-run through the full query (within ``budget`` full-path
+    match slots -- default: from the free memory -- in ray chunks when they
+    need more).  (samples 9-tuple, Q, flagged)"""
     *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
     Q = pre.total
     if TRACK_PREFIX_LEN:
         _PREFIX_LEN.append(pre.length.sum())
+    # the heads and their workspace are no longer needed (sample_prefix copied its outputs)
+    pre.t = pre.ids = pre.dist = pre._ws = None
     if n_flagged:
         sel = torch.nonzero(flagged, as_tuple=True)[0]
-        q = device.query(idx, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], facts=True)
-        sub = device.sample(q[0], q[1], q[2], q[3], slopes[sel], sampler_cfg, colors, exact_t_end, facts=q[6])
-        del q
+        sub = _full_rays(idx, colors, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], sampler_cfg,
+                         exact_t_end, budget)
         s = device.merge_flagged(tuple(s), flagged, sub, sel)
     return tuple(s), Q, n_flagged
 
 
-def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end):
+def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget):
+    """Full-CSR query + sample of a set of rays, in ray chunks of at most
+    ``budget`` match slots."""
+    if budget is None:
+        budget = match_budget(bytes_per_match=BYTES_PER_MATCH)
+    try:
+        q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
+    except device.MatchBudgetExceeded:
+        return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget,
+                              lambda name: None, prefix=False).samples
+    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
+    del q
+    return s
+
+
+def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None):
     pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes)
-    return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end)
+    return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget)
 
 
 def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
                   mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None) -> FrameResult:
-    """query -> sample of one frame on the device.  ``prefix``: True / False
-    forces the mode, None (default: the HP_PREFIX setting, auto) lets
-    device.query_frame pick it from the counts."""
+    """query -> sample of one frame on the device.  ``prefix``: True (heads)
+    / False (full CSR); None: the HP_PREFIX setting."""
     prefix = PREFIX if prefix is None else prefix
     budget = int(max_matches) if max_matches is not None else match_budget(
-        bytes_per_match=BYTES_PER_MATCH if prefix is False else BYTES_PER_MATCH_PREFIX)
+        bytes_per_match=BYTES_PER_MATCH_PREFIX if prefix else BYTES_PER_MATCH)
     try:
         q = device.query_frame(idx, pixels, dirs, t_near, t_far, slopes, prefix=prefix, max_scratch=budget)
     except device.MatchBudgetExceeded:
@@ -195,13 +209,13 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
         # such frames are dominated by long rays)
         before_sample()
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                              exact_t_end, budget, mark, prefix is not False)
+                              exact_t_end, budget, mark, prefix is not False, max_matches)
     mark("query")
     before_sample()
     if isinstance(q, device.QueryPrefix):
         _PREFIX_LEN.clear()
         s, Q, n_flagged = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                                         exact_t_end)
+                                         exact_t_end, max_matches)
         mark("sample")
         return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, prefix=True,
                            prefix_len=_PREFIX_LEN.pop() if _PREFIX_LEN else None)
@@ -211,7 +225,7 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
 
 
 def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end,
-                   budget, mark, prefix=False):
+                   budget, mark, prefix=False, rerun_budget=None):
     bo = device.query_bounds(idx, pixels, dirs, t_near, t_far, slopes).cpu().numpy()
     m = bo.shape[0] - 1
     cuts = [0]
@@ -226,7 +240,7 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
     for a, b in zip(cuts[:-1], cuts[1:]):
         if prefix:
             s, q_n, f_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
-                                       slopes[a:b], sampler_cfg, exact_t_end)
+                                       slopes[a:b], sampler_cfg, exact_t_end, rerun_budget)
             parts.append(s)
             Q += q_n
             nf += f_n
