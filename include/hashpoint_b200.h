@@ -156,8 +156,9 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
                    void* workspace, size_t workspace_bytes, hp_stream_t stream);
 /* Heads (callers that only want samples; replaces hash_query_batch ->
  * sample_batch as chained by renderer.py:119-124): per ray, the head of its
- * matches in (t, id) order -- all of them when it has <= 1024, else the
- * smallest-t matches up to a cut near the `want`-th (<= 1024) -- without the
+ * matches in (t, id) order -- all of them when it has few, else the
+ * smallest-t matches up to a cut near the `want`-th (want <= whole <= 1024:
+ * rays of at most `whole` matches are sorted whole) -- without the
  * full match list.  hp_head_count is the streaming pass (same arguments and
  * probes / scanned / offsets outputs as hp_query_count, offsets[m] = Q or
  * -(slots needed) when `capacity` is short); it keeps 8 bytes per match in
@@ -175,7 +176,7 @@ int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w
                   int64_t* offsets, int64_t* head_off, int64_t* probes, int64_t* scanned,
                   int64_t capacity, void* workspace, size_t workspace_bytes, hp_stream_t stream);
 int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
-                 const int64_t* offsets, const int64_t* head_off, int32_t want, double* head_t,
+                 const int64_t* offsets, const int64_t* head_off, int32_t want, int32_t whole, double* head_t,
                  int32_t* head_ids, double* head_dist, int32_t* plen, int32_t* facts, double* cut_t,
                  double* cut_d, int64_t capacity, void* workspace, size_t workspace_bytes,
                  hp_stream_t stream);

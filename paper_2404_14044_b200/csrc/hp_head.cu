@@ -45,7 +45,10 @@ constexpr int kHeadSmall = 512;  // rays up to this: a smaller, denser CTA confi
 #endif
 constexpr int kStage = HP_HEAD_STAGE;  // slots per staged chunk (16 B each)
 #ifndef HP_HEAD_MINB
-#define HP_HEAD_MINB 5
+#define HP_HEAD_MINB 4
+#endif
+#ifndef HP_HEAD_SORT_MINB
+#define HP_HEAD_SORT_MINB 6
 #endif
 
 // ---------------------------------------------------------------- bulk copies
@@ -301,9 +304,10 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
 }
 
 // ---------------------------------------------------------------- classes
-// list 0: rays of 1..kHeadSmall matches, list 1: the longer ones; the empty
-// rays' outputs are written here.
-__global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int* __restrict__ lists,
+// list 0: rays of 1..min(kHeadSmall, whole) matches (sorted whole by the
+// small configuration), list 1: the longer ones; the empty rays' outputs are
+// written here.
+__global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int whole, int* __restrict__ lists,
                                int* __restrict__ counts, int* __restrict__ plen, int* __restrict__ facts,
                                double* __restrict__ cut_t, double* __restrict__ cut_d) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
@@ -311,7 +315,7 @@ __global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int* 
         int cls = -1;
         if (r < m) {
             const int64_t q = off[r + 1] - off[r];
-            cls = q == 0 ? -1 : (q <= kHeadSmall ? 0 : 1);
+            cls = q == 0 ? -1 : (q <= min(kHeadSmall, whole) ? 0 : 1);
             if (q == 0) {
                 plen[r] = 0;
                 facts[r] = -1;
@@ -341,7 +345,7 @@ __global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int* 
 template <int kBins>
 __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__ off,
                                                      const int64_t* __restrict__ soff,
-                                                     const RayMeta* __restrict__ meta, int want,
+                                                     const RayMeta* __restrict__ meta, int want, int whole,
                                                      const unsigned* __restrict__ sc_key, uint2* __restrict__ sel,
                                                      const int* __restrict__ list, const int* __restrict__ list_n) {
     __shared__ int hist[4][kBins];
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
     for (int64_t k = int64_t(blockIdx.x) * 4 + warp_id(); k < nr; k += warps) {
         const int64_t r = list[k];
         const int q = int(off[r + 1] - off[r]);
-        if (q <= kHeadCap) continue;
+        if (q <= whole) continue;
         const int64_t so = soff[r];
         const RayMeta M = meta[r];
         const unsigned span1 = M.kmax - M.kmin;  // span - 1
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
         for (int b = 0; b < kPer; b++) sum += H[lane * kPer + b];
         const int incl = warp_incl_scan(sum);
         const unsigned hit = __ballot_sync(0xffffffffu, incl >= want);
-        const int owner = __ffs(hit) - 1;  // exists: q > kHeadCap >= want
+        const int owner = __ffs(hit) - 1;  // exists: q > whole >= want
         if (lane == owner) {
             int c = incl - sum, b = lane * kPer;
             for (int j = 0; j < kPer; j++) {
@@ -415,7 +419,7 @@ struct HeadSmem {
     unsigned short lst[kCap], perm[kCap];
     int chist[kCoarse + 1];
     int scan_sh[33];
-    unsigned long long cut_t, cut_d2;  // order keys of the trimmed pairs' minima
+    unsigned long long cut_d2;         // order key of the trimmed pairs' smallest dist^2
     unsigned kout, thi;                // smallest left-out key; fkey of the largest float(t) staged
     int cnt, keep, fcount, fbad;
 };
@@ -427,11 +431,11 @@ struct HeadSmem {
 // moves to the left-out side), the exact (t, id) rank, and the write-out of
 // the head at hoff[r] with the sampler's facts and cuts.
 template <int kCap, int kT>
-__global__ void __launch_bounds__(kT, kT == 128 ? 12 : 6) k_head_sort(
+__global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head_sort(
     hp_query_layout L, const double* __restrict__ dirs, const double* __restrict__ slopes,
     const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const int64_t* __restrict__ hoff,
     const RayMeta* __restrict__ meta, const unsigned* __restrict__ sc_key, const int* __restrict__ sc_slot,
-    const uint2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n,
+    const uint2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n, int whole,
     double* __restrict__ head_t, int* __restrict__ head_id, double* __restrict__ head_d, int* __restrict__ plen,
     int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d) {
     extern __shared__ __align__(16) unsigned char dyn[];
@@ -444,23 +448,27 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : 6) k_head_sort(
         const int64_t so = soff[r];
         const int q = int(off[r + 1] - off[r]);
         const RayMeta M = meta[r];
-        const bool all = q <= kCap;
+        const bool all = q <= whole;
+        unsigned kc = 0xffffffffu;
+        int S = q;  // pairs to stage
+        if (!all) {
+            const uint2 sv = sel[r];
+            kc = sv.x;
+            S = int(sv.y);
+        }
         if (tid == 0) {
             F.cnt = F.keep = F.fcount = 0;
             F.fbad = M.bad;
-            F.cut_t = F.cut_d2 = ~0ull;
+            F.cut_d2 = ~0ull;
             F.kout = 0xffffffffu;
             F.thi = 0u;
         }
-        unsigned kc = 0xffffffffu;
         if (all) {  // every slot in flight at once
             for (int e = tid; e < q; e += kT) cp_async4(&F.slot[e], sc_slot + so + e);
             cp_commit();
-        } else {
-            kc = sel[r].x;
         }
         for (int j = tid; j <= kCoarse; j += kT) F.chist[j] = 0;
-        for (int j = tid; j <= kCap; j += kT) F.hist[j] = 0;
+        for (int j = tid; j <= S; j += kT) F.hist[j] = 0;
         __syncthreads();
         if (!all) {  // stream the keys (4 per thread in flight); stage the selected slots
             unsigned kout = 0xffffffffu;
@@ -488,93 +496,75 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : 6) k_head_sort(
         }
         cp_wait<0>();
         __syncthreads();
-        const int S = all ? q : F.cnt;  // staged pairs
-        // exact t / dist^2 of the staged pairs; long rays keep t < T_c
+        // exact t / dist^2 / id of every staged pair; long rays keep t < T_c
+        // (the trimmed pairs, t >= T_c, end up last in the order below)
         const double d0 = dirs[3 * r], d1 = dirs[3 * r + 1], d2v = dirs[3 * r + 2];
         const double Tc = (all || kc == 0xffffffffu) ? CUDART_INF : double(from_fkey(kc + 1u));
-        unsigned long long mt = ~0ull, md = ~0ull;
         unsigned thi = 0u;
-        bool bad = false;
-        for (int e0 = 0; e0 < S; e0 += kT) {
-            const int e = e0 + tid;
-            bool keep = false;
-            double t = 0.0, dd = 0.0;
-            int id = 0;
-            if (e < S) {
-                const double4 a = rel4[F.slot[e]];
-                t = cone_t(a.x, a.y, a.z, d0, d1, d2v);
-                dd = cone_dist2(a.x, a.y, a.z, t, d0, d1, d2v);
-                id = int(__double_as_longlong(a.w));
-                keep = t < Tc;
-                if (!keep) {
-                    mt = min(mt, dkey(t));
-                    md = min(md, dkey(dd));
-                }
-            }
-            int pos = e;
-            if (!all) {  // compact the kept pairs (order is irrelevant: ranked below)
-                const unsigned b = __ballot_sync(0xffffffffu, keep);
-                int base = 0;
-                if (lane_id() == 0 && b) base = atomicAdd(&F.keep, __popc(b));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                pos = base + __popc(b & lanemask_lt());
-            }
-            if (keep) {
-                F.t[pos] = t;
-                F.d2[pos] = dd;
-                F.id[pos] = id;
-                thi = max(thi, fkey(__double2float_rn(t)));
-                bad |= !(fabs(t) <= DBL_MAX) || !(dd <= DBL_MAX);
-            }
+        int nkeep = 0;
+        for (int e = tid; e < S; e += kT) {
+            const double4 a = rel4[F.slot[e]];
+            const double t = cone_t(a.x, a.y, a.z, d0, d1, d2v);
+            F.t[e] = t;
+            F.d2[e] = cone_dist2(a.x, a.y, a.z, t, d0, d1, d2v);
+            F.id[e] = int(__double_as_longlong(a.w));
+            nkeep += t < Tc;
+            thi = max(thi, fkey(__double2float_rn(t)));
         }
         thi = __reduce_max_sync(0xffffffffu, thi);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mt = min(mt, __shfl_xor_sync(0xffffffffu, mt, o));
-            md = min(md, __shfl_xor_sync(0xffffffffu, md, o));
-        }
-        const bool anybad = __any_sync(0xffffffffu, bad);
+        nkeep = warp_sum(nkeep);
         if (lane_id() == 0) {
             atomicMax(&F.thi, thi);
-            if (anybad) atomicOr(&F.fbad, 1);
-            if (mt != ~0ull) {
-                atomicMin(&F.cut_t, mt);
-                atomicMin(&F.cut_d2, md);
-            }
+            if (nkeep) atomicAdd(&F.keep, nkeep);
         }
         __syncthreads();  // every slot read (bk may now be overwritten)
-        const int Lh = all ? q : F.keep;
-        if (Lh > 0)
-            rank_segment<kCap, kT>(Lh, from_fkey(M.kmin), from_fkey(F.thi), F.t, F.id, F.bk, F.hist, F.lst, F.perm,
+        if (S > 0)
+            rank_segment<kCap, kT>(S, from_fkey(M.kmin), from_fkey(F.thi), F.t, F.id, F.bk, F.hist, F.lst, F.perm,
                                    F.chist, F.scan_sh);
+        const int Lh = F.keep;
         const int64_t ho = hoff[r];
         const double r0 = Lh > 0 ? dmul(__ldg(slopes + r), F.t[F.perm[0]]) : 0.0;
         int cnt = 0;
-        for (int p = tid; p < Lh; p += kT) {
+        bool bad = false;
+        unsigned long long md = ~0ull;
+        for (int p = tid; p < S; p += kT) {
             const int e = F.perm[p];
-            const double d = sqrt(F.d2[e]);
-            head_t[ho + p] = F.t[e];
-            head_id[ho + p] = F.id[e];
-            head_d[ho + p] = d;
-            cnt += d <= r0;
+            const double t = F.t[e], dd = F.d2[e];
+            if (p < Lh) {
+                const double d = sqrt(dd);
+                head_t[ho + p] = t;
+                head_id[ho + p] = F.id[e];
+                head_d[ho + p] = d;
+                cnt += d <= r0;
+                bad |= !(fabs(t) <= DBL_MAX) || !(dd <= DBL_MAX);
+            } else {
+                md = min(md, dkey(dd));
+            }
         }
         cnt = warp_sum(cnt);
-        if (lane_id() == 0 && cnt) atomicAdd(&F.fcount, cnt);
+        const bool anybad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) md = min(md, __shfl_xor_sync(0xffffffffu, md, o));
+        if (lane_id() == 0) {
+            if (cnt) atomicAdd(&F.fcount, cnt);
+            if (anybad) atomicOr(&F.fbad, 1);
+            if (md != ~0ull) atomicMin(&F.cut_d2, md);
+        }
         __syncthreads();
         if (tid == 0) {
             plen[r] = Lh;
             facts[r] = (F.fbad || Lh == 0) ? -1 : F.fcount;
             // lower bounds of the left-out t / dist: a pair never staged has
-            // t >= its key (> K_c) and an unknown dist (0); a trimmed pair's are exact
+            // t >= its key (> K_c) and an unknown dist (0); a trimmed pair's
+            // are exact (the smallest trimmed t is the next in order)
             const bool unstaged = !all && F.kout != 0xffffffffu;
-            const bool trimmed = F.cut_t != ~0ull;
             double ct = CUDART_INF, cd = CUDART_INF;
             if (unstaged) {
                 ct = double(from_fkey(F.kout));
                 cd = 0.0;
             }
-            if (trimmed) {
-                ct = fmin(ct, dkey_inv(F.cut_t));
+            if (Lh < S) {
+                ct = fmin(ct, F.t[F.perm[Lh]]);
                 cd = fmin(cd, sqrt(dkey_inv(F.cut_d2)));
             }
             cut_t[r] = ct;
@@ -671,13 +661,14 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
 }
 
 extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
-                            const int64_t* offsets, const int64_t* head_off, int32_t want, double* head_t,
+                            const int64_t* offsets, const int64_t* head_off, int32_t want, int32_t whole,
+                            double* head_t,
                             int32_t* head_ids, double* head_dist, int32_t* plen, int32_t* facts, double* cut_t,
                             double* cut_d, int64_t capacity, void* workspace, size_t workspace_bytes,
                             hp_stream_t stream) {
-    if (m < 0 || want < 1 || want > kHeadCap ||
+    if (m < 0 || want < 1 || want > kHeadCap || whole < want || whole > kHeadCap ||
         (m > 0 && (!dirs || !slopes || !facts || !plen || !cut_t || !cut_d || !layout.rel4))) {
-        set_error("hp_head_sort: invalid arguments (1 <= want <= %d)", kHeadCap);
+        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d)", kHeadCap);
         return HP_EINVAL;
     }
     if (capacity > INT32_MAX) capacity = INT32_MAX;
@@ -693,13 +684,14 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         return cuda_status(cudaGetLastError(), "hp_head_sort memset");
     const int* list_small = w.lists;
     const int* list_big = w.lists + m;
-    k_head_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, w.lists, w.counts, plen, facts, cut_t, cut_d);
+    k_head_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, whole, w.lists, w.counts, plen, facts, cut_t,
+                                                    cut_d);
     HP_CHECK_LAUNCH("k_head_classes");
     {
         constexpr auto kselect = k_head_select<kHeadCap>;
         static const int occ_sel = resident(kselect, 128, 0);  // once (thread-safe)
         TimedSpan ts("k_head_select", s);
-        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.meta, want, w.key, w.sel, list_big,
+        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.meta, want, whole, w.key, w.sel, list_big,
                                                   w.counts + 1);
         HP_CHECK_LAUNCH("k_head_select");
     }
@@ -715,12 +707,13 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     }();
     TimedSpan ts("k_head_sort", s);
     ksmall<<<kNumSMs * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
-        layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts, head_t,
+        layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts, whole,
+        head_t,
         head_ids, head_dist, plen, facts, cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_sort small");
     kbig<<<kNumSMs * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
         layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big, w.counts + 1,
-        head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
+        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_sort");
     return HP_OK;
 }

@@ -290,8 +290,10 @@ class QueryPrefix:
         return sp
 
 
-PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "512"))  # head length the sampler usually needs
+PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "400"))  # head length the sampler usually needs
 HEAD_CAP = 1024  # longest head (hp_head.cu kHeadCap)
+# rays of at most this many matches are sorted whole; longer ones are cut near PREFIX_WANT
+HEAD_WHOLE = int(os.environ.get("HP_HEAD_WHOLE", "1024"))
 
 
 def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
@@ -336,16 +338,16 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
 
 def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
                  t_far: torch.Tensor, slopes: torch.Tensor, want: int = PREFIX_WANT, footprint: bool = True,
-                 max_scratch: int | None = None) -> QueryPrefix:
+                 max_scratch: int | None = None, whole: int | None = None) -> QueryPrefix:
     """The query for callers that only want samples (hp_head_count +
     hp_head_sort): each ray's head of matches in (t, id) order, without the
     CSR of all matches."""
     pixels, dirs = pixels.contiguous(), dirs.contiguous()
     return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch), dirs,
-                 slopes, want)
+                 slopes, want, whole)
 
 
-def _head(index, counted, dirs, slopes, want=PREFIX_WANT) -> QueryPrefix:
+def _head(index, counted, dirs, slopes, want=PREFIX_WANT, whole=None) -> QueryPrefix:
     """hp_head_sort after :func:`_count_head`."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
@@ -357,8 +359,9 @@ def _head(index, counted, dirs, slopes, want=PREFIX_WANT) -> QueryPrefix:
     ht = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hd = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hi = torch.empty(max(hcap, 1), dtype=torch.int32, device=dev)
+    whole = max(int(want), min(HEAD_WHOLE if whole is None else int(whole), HEAD_CAP))
     _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(offsets), _ptr(head_off),
-                                int(want), _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa), _ptr(cut[0]),
+                                int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa), _ptr(cut[0]),
                                 _ptr(cut[1]), cap, _ptr(ws), nb, _stream()))
     _mark("query.prefix")
     pre = QueryPrefix(offsets, probes, scanned, head_off[:m], plen, ht, hi, hd, cut[0], cut[1], fa, ws)

@@ -57,7 +57,8 @@ def _check_prefix(q, p, want):
 
 @pytest.mark.parametrize("name", gu.case_names())
 @pytest.mark.parametrize("want", [1, 7, 64, 512])
-def test_prefix_is_the_sorted_csr_head(name, want):
+@pytest.mark.parametrize("whole", ["want", 1024])
+def test_prefix_is_the_sorted_csr_head(name, want, whole):
     _, cloud, cam, cfg, tn, tf, stride, _ = gu.get_case(name)
     dev = torch.device("cuda")
     idx = dv.build(torch.from_numpy(cloud.positions).to(dev), cam, cfg.pad)
@@ -65,7 +66,7 @@ def test_prefix_is_the_sorted_csr_head(name, want):
     up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     rays = (up(pixels), up(dirs), up(t_near), up(t_far), up(slopes))
     q = dv.query(idx, *rays, facts=True)
-    p = dv.query_prefix(idx, *rays, want=want)
+    p = dv.query_prefix(idx, *rays, want=want, whole=want if whole == "want" else whole)
     _check_prefix(q, p, want)
 
 
@@ -85,17 +86,17 @@ def test_prefix_on_dense_rays():
     idx = dv.build(up(cloud.positions), cam, cfg.pad)
     rays = (up(pixels), up(dirs), up(tn), up(tf), up(slopes))
     q = dv.query(idx, *rays, facts=True)
-    for want in (16, 300, 700):
-        p = dv.query_prefix(idx, *rays, want=want)
+    for want, whole in ((16, 16), (16, 1024), (300, 300), (300, 640), (700, 700)):
+        p = dv.query_prefix(idx, *rays, want=want, whole=whole)
         plen, counts = _check_prefix(q, p, want)
         assert (counts > want).sum() > 10
         # the head reaches ~want (a trim at the key cut may leave it a little short)
         assert np.mean(plen[counts > want] >= 0.75 * want) > 0.9
 
 
-def _prefix_frame(idx, rays, sc, colors, exact_t_end, want):
+def _prefix_frame(idx, rays, sc, colors, exact_t_end, want, whole=None):
     """prefix-mode sampling with the flagged rays re-run on the full path"""
-    pre = dv.query_prefix(idx, *rays, want=want)
+    pre = dv.query_prefix(idx, *rays, want=want, whole=whole)
     *s, flagged, n_flagged = dv.sample_prefix(pre, rays[4], sc, colors, exact_t_end)
     fl = flagged.cpu().numpy()
     assert int(fl.sum()) == n_flagged
@@ -117,7 +118,8 @@ def _assert_same(a, b):
 @pytest.mark.parametrize("name", gu.case_names())
 @pytest.mark.parametrize("exact_t_end", [True, False])
 @pytest.mark.parametrize("want", [1, 9, 512])
-def test_prefix_sampling_equals_full(name, exact_t_end, want):
+@pytest.mark.parametrize("whole", ["want", 1024])
+def test_prefix_sampling_equals_full(name, exact_t_end, want, whole):
     _, cloud, cam, cfg, tn, tf, stride, samplers = gu.get_case(name)
     dev = torch.device("cuda")
     idx = dv.build(torch.from_numpy(cloud.positions).to(dev), cam, cfg.pad)
@@ -130,7 +132,7 @@ def test_prefix_sampling_equals_full(name, exact_t_end, want):
         sc = gu.sampler_config(sname)
         for col in ((colors, None) if sname == "default" else (colors,)):
             full = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, col, exact_t_end=exact_t_end, facts=q[6])
-            got, _ = _prefix_frame(idx, rays, sc, col, exact_t_end, want)
+            got, _ = _prefix_frame(idx, rays, sc, col, exact_t_end, want, want if whole == "want" else whole)
             _assert_same(got, full)
 
 
@@ -154,8 +156,8 @@ def test_prefix_sampling_on_dense_rays(k, mode, gamma, exact_t_end):
     colors = torch.from_numpy(cloud.colors).cuda()
     full = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, colors, exact_t_end=exact_t_end, facts=q[6])
     seen = []
-    for want in (16, 64, 512):
-        got, nf = _prefix_frame(idx, rays, sc, colors, exact_t_end, want)
+    for want, whole in ((16, 16), (16, 1024), (64, 64), (512, 512), (512, 1024)):
+        got, nf = _prefix_frame(idx, rays, sc, colors, exact_t_end, want, whole)
         _assert_same(got, full)
         seen.append(nf)
     assert seen[0] > 0  # the small heads do send rays to the full path
