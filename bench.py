@@ -42,14 +42,18 @@ WORKLOADS = {
     # dense large scene, smallest delta of the sweep: Q ~ 4.3e9 does not fit
     # one GPU's memory in one pass -> ray-chunk streaming (pipeline)
     "cfg4": (dict(kind="sphere_surface", n=10_000_000, seed=0, noise=0.005), (1920, 1080, 40.0), 0.005),
+    # the rest of the cfg4 radius sweep (Q ~ 1.7e10 / 6.9e10: several ray chunks per frame)
+    "cfg4_d01": (dict(kind="sphere_surface", n=10_000_000, seed=0, noise=0.005), (1920, 1080, 40.0), 0.01),
+    "cfg4_d02": (dict(kind="sphere_surface", n=10_000_000, seed=0, noise=0.005), (1920, 1080, 40.0), 0.02),
 }
 # ScanNet-shaped indoor batch: 64 views orbiting a multi-plane cloud, one
 # index per view; views are sharded across ranks
 CFG3 = dict(scene=dict(kind="parallel_planes", n=3_000_000, seed=0, plane_count=6, plane_gap=0.5,
                        extent=4.0, noise=0.005), size=(640, 480, 60.0), delta=0.01, views=64)
 # rays checked against the oracle before timing / timed on the host CPU
-PARITY_STRIDE = {"cfg1": 53, "cfg2": 53, "cfg4": 4999}
-CPU_STRIDE = {"cfg1": 97, "cfg2": 97, "cfg4": 20011}
+# (the oracle runs the reference's O(q^2) sampler: sparser subsets for the larger radii)
+PARITY_STRIDE = {"cfg1": 53, "cfg2": 53, "cfg4": 4999, "cfg4_d01": 20011, "cfg4_d02": 200003}
+CPU_STRIDE = {"cfg1": 97, "cfg2": 97, "cfg4": 20011, "cfg4_d01": 200003, "cfg4_d02": 1000003}
 T_NEAR, T_FAR = 1.0, 10.0
 
 
@@ -89,28 +93,36 @@ def make_views(n_views=None):
 def run_views(args, rank, world, dist):
     """cfg3: every rank builds, queries and samples its share of the 64 views
     (views[rank::world]; no collective on the data path); the step time is
-    the max over ranks; value = all views' rays / step time."""
+    the max over ranks; value = all views' rays / step time.  Parity gate
+    (rank 0, after timing): every view's index (hence every point's bucket,
+    the rotated-camera hazard of geometry.py:122-134) against the oracle's
+    build, and every 8th view's timed samples on every 97th ray."""
     import torch
 
     import paper_2404_14044_b200 as hp
-    from paper_2404_14044_b200 import _lib, pipeline
+    from paper_2404_14044_b200 import _lib, device as dv, pipeline
     dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     cloud, views = make_views(args.views)
-    mine = views[rank::world]
+    mine = list(range(len(views)))[rank::world]
     up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     xyz, col = up(cloud.positions), up(cloud.colors)
-    rays = [[up(v["pixels"]), up(v["dirs"]), up(np.full(v["m"], T_NEAR)), up(np.full(v["m"], T_FAR)),
-             up(v["slopes"])] for v in mine]
+    rays = {i: [up(views[i]["pixels"]), up(views[i]["dirs"]), up(np.full(views[i]["m"], T_NEAR)),
+                up(np.full(views[i]["m"], T_FAR)), up(views[i]["slopes"])] for i in mine}
     scfg = hp.SamplerConfig()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    gated = [i for i in mine if i % 8 == 0]
+    kept = {}
 
-    def step():
+    def step(keep=False):
         Q = R = 0
-        for v, r in zip(mine, rays):
-            fr = pipeline.frame_device(xyz, col, v["cam"], v["cfg"], *r, scfg, True)
+        for i in mine:
+            v = views[i]
+            fr = pipeline.frame_device(xyz, col, v["cam"], v["cfg"], *rays[i], scfg, True)
             Q += fr.Q
             R += fr.R
+            if keep and i in gated:
+                kept[i] = fr.samples
         return Q, R
 
     for _ in range(args.warmup):
@@ -120,14 +132,14 @@ def run_views(args, rank, world, dist):
     _lib.timing_collect()
     smi = ClockSampler(dev.index)
     with smi:
-        for _ in range(args.steps):
+        for it in range(args.steps):
             flush.fill_(1.0)
             if dist is not None:
                 dist.barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            Q, R = step()
+            Q, R = step(keep=it == args.steps - 1)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -146,19 +158,43 @@ def run_views(args, rank, world, dist):
         qr = (int(x[0]), int(x[1]))
     if rank != 0:
         return
+    parity = "skipped"
+    if not args.no_parity:
+        from oracle import oracle as orc
+        bad_builds, checked = [], 0
+        for i, v in enumerate(views):  # every view's build, bit for bit
+            ob = orc.build(cloud.positions, v["cam"], v["cfg"].pad)
+            idx = dv.build(xyz, v["cam"], v["cfg"].pad)
+            same = all(np.array_equal(getattr(idx, k).cpu().numpy(), ob[k])
+                       for k in ("table_start", "table_count", "reordered_ids", "slot_x", "slot_y", "slot_z"))
+            if not same:
+                bad_builds.append(i)
+            if i in kept:  # this view's timed samples, every 97th ray
+                sel = np.arange(0, v["m"], 97)
+                ref, _ = oracle_samples(cloud, v["cam"], v["cfg"], v["pixels"][sel], v["dirs"][sel],
+                                        np.full(len(sel), T_NEAR), np.full(len(sel), T_FAR), v["slopes"][sel],
+                                        build=ob)
+                if not same_samples(rays_of(kept[i], sel), ref):
+                    raise SystemExit(f"parity gate failed: cfg3 view {i} differs from the oracle; number rejected")
+                checked += 1
+        if bad_builds:
+            raise SystemExit(f"parity gate failed: cfg3 builds of views {bad_builds} differ from the oracle")
+        parity = (f"pass ({len(views)} views' builds bit-exact vs the oracle: every point's bucket; timed "
+                  f"samples of {checked} views (every 8th) on every 97th ray, ids/t/dist/udf/primary bit-exact, "
+                  "alpha/w/colour/t_end rtol 1e-12)")
     m_total = sum(v["m"] for v in views)
     W, H, fov = CFG3["size"]
     line = {
         "metric": "rays/sec (search+primary-surface sampling)", "value": m_total / (ms / 1e3), "unit": "rays/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded reference scene generators)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded reference scene generators)",
         "config": {"workload": f"cfg3: {cloud.count:,}-point 6-plane indoor cloud, {len(views)} orbiting "
                                f"{W}x{H} views (one index each), delta={CFG3['delta']}, t in [{T_NEAR},{T_FAR}], "
                                "SamplerConfig() eps retention K=8 with colours, exact transmittance",
                    "rays": m_total, "views": len(views), "Q": qr[0], "R": qr[1],
                    "l2": "flushed between timed steps (256 MB write)",
-                   "parallelism": f"views x{world}" if world > 1 else "single GPU"},
+                   "parallelism": f"views x{world}" if world > 1 else "single GPU", "parity_gate": parity},
         "kernels_ms": {k: round(v / args.steps, 3) for k, (v, _) in sorted(kern_tot.items(), key=lambda x: -x[1][0])},
         "clocks": smi.summary(),
     }
@@ -385,9 +421,15 @@ def local_device():
 
 def row_bands(w, world, rank):
     """Contiguous ray range of this rank (whole image rows, cost-balanced by
-    the scan count each ray will do; every rank computes the same split)."""
+    the slots each ray's window scans, from the device index's table; every
+    rank computes the same split)."""
+    import torch
+
+    from paper_2404_14044_b200 import device as dv
     from paper_2404_14044_b200.shard import balanced_row_bands
-    lo, hi = balanced_row_bands(w["cloud"].positions, w["cam"], w["cfg"].pad, world)[rank]
+    dev = torch.device("cuda", local_device())
+    idx = dv.build(torch.from_numpy(np.ascontiguousarray(w["cloud"].positions)).to(dev), w["cam"], w["cfg"].pad)
+    lo, hi = balanced_row_bands(None, w["cam"], w["cfg"].pad, world, table_count=idx.table_count)[rank]
     W = w["cam"].width
     return lo * W, hi * W
 
@@ -416,11 +458,6 @@ def run_ours(args, w, rank, world, dist):
             gather_samples(fr.samples, dist)
         return fr
 
-    # parity gate (fairness gate of the reference bench, bench.py:114-134):
-    # refuse to time if the device result differs from the oracle on a subset
-    parity = "skipped"
-    if rank == 0 and not args.no_parity:
-        parity = parity_gate(w, dev)
     for _ in range(args.warmup):
         fr = step()
     torch.cuda.synchronize()
@@ -452,6 +489,10 @@ def run_ours(args, w, rank, world, dist):
                 kern_tot[k] = (a + v, b + c)
     _lib.timing_enable(False)
     launches = _lib.launch_count() - launches0
+    # parity gate on the last timed frame's own output
+    parity = "skipped"
+    if rank == 0 and not args.no_parity:
+        parity = parity_gate(w, fr.samples, r0, r1, PARITY_STRIDE.get(w["name"], 53))
     ms = statistics.mean(times)
     if dist is not None:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -487,19 +528,25 @@ def run_ours(args, w, rank, world, dist):
     m_loc, q_loc, r_loc = r1 - r0, fr.Q, fr.R
     qs = np.diff(fr.query[0].cpu().numpy()) if fr.query is not None else np.zeros(0, np.int64)
     cls = {"k_query_sort": (qs > 0) & (qs <= 2048), "k_query_sort_large": qs > 2048}
+    st = plen_fr.prefix_len.cpu().numpy() if plen_fr.prefix_len is not None else np.zeros(4, np.int64)
+    plen, q_cut, q_whole, hit = (int(x) for x in st)
     kbytes = {
-        "hp_build": 24 * n + 16 * P + 32 * n_in + 4 * (P + 1) + 44 * n_in,
+        "hp_build": 24 * n + 16 * P + 32 * n_in + 4 * (P + 1) + 44 * n_in + 32 * n_in,
         "k_query_bound": 64 * m_loc + 4 * (P + 1) + 8 * m_loc,
-        "k_query_scan": 64 * m_loc + 4 * (P + 1) + 44 * n_in + 20 * q_loc + 32 * m_loc,
-        "k_sample_plan": 8 * (m_loc + 1) + 16 * q_loc + 8 * m_loc + 24 * m_loc,
+        # rays in (64 B), row pointers, the fp32 copies (16 B / point), 8 B per
+        # match out, per-ray counts / head counts / key bounds / probes / scanned
+        "k_head_scan": 64 * m_loc + 4 * (P + 1) + 16 * n_in + 8 * q_loc + 56 * m_loc,
+        # the cut rays' keys (4 B / match) in, per-ray cut out
+        "k_head_select": 4 * q_cut + 8 * m_loc,
+        # slots of whole rays, keys of cut rays + slots of the staged, exact
+        # records (32 B / point, once), heads out (t, id32, dist: 20 B) and
+        # per-ray inputs / outputs
+        "k_head_sort": 4 * q_whole + 4 * q_cut + 4 * plen + 32 * n_in + 20 * plen + 112 * hit,
+        "k_sample_plan": 8 * (m_loc + 1) + 16 * plen + 8 * m_loc + 24 * m_loc,
         "k_emit": 8 * (m_loc + 1) + 52 * r_loc + 24 * r_loc + 72 * r_loc,
     }
     for k, sel in cls.items():  # read the unsorted matches (20 B), write the CSR (24 B)
         kbytes[k] = 44 * int(qs[sel].sum()) + 24 * int(sel.sum())
-    plen = int(plen_fr.prefix_len.item()) if plen_fr.prefix_len is not None else 0
-    # prefix mode: read the unsorted matches (20 B), write the sorted heads
-    # (t, id32, dist: 20 B), per ray offsets/soff/t-bounds in, length/facts/cuts out
-    kbytes["k_query_prefix"] = 20 * q_loc + 20 * plen + 56 * m_loc
     kern = {k: (v / args.steps, c // args.steps) for k, (v, c) in kern_tot.items()}
     top = max((k for k in kern if k in kbytes), key=lambda k: kern[k][0])
     t_top = kern[top][0] / max(kern[top][1], 1)
@@ -528,7 +575,7 @@ def run_ours(args, w, rank, world, dist):
                            # reported beside B_frame, not divided by it
                            "b_fused": 24 * n + 64 * fr.index.n_in + 32 * P + 96 * m_total + 48 * R
                            if fr.prefix else None,
-                           "prefix_len": plen if plen_fr.prefix_len is not None else None},
+                           "head_len": plen if plen_fr.prefix_len is not None else None},
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "kernels_ms": {k: round(v[0], 4) for k, v in sorted(kern.items(), key=lambda x: -x[1][0])},
         "kernels_gbs": {k: round(kbytes[k] / (kern[k][0] / 1e3) / 1e9, 1) for k in kern if k in kbytes
@@ -548,9 +595,15 @@ def run_ours(args, w, rank, world, dist):
 
 
 def run_e2e(args, w, r0, r1, dist=None):
+    """End to end through the public host-buffer API: numpy / pinned host
+    inputs in, numpy out, copies inside the timed region.  N = 1:
+    pipeline.search_and_sample (rays from the host) and
+    search_and_sample_view (rays on the device); N > 1:
+    shard.search_and_sample_distributed (every rank its band, the tiles
+    gathered to rank 0 inside the timed region), max over ranks."""
     import torch
 
-    from paper_2404_14044_b200 import pipeline
+    from paper_2404_14044_b200 import pipeline, shard
     m = r1 - r0
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
 
@@ -558,15 +611,37 @@ def run_e2e(args, w, r0, r1, dist=None):
         positions = pin(w["cloud"].positions)
         colors = pin(w["cloud"].colors)
     cloud = PinnedCloud()
+    cam = w["cam"]
+    tn, tf = w["t_near"], w["t_far"]
+    if dist is not None:
+        times, out = [], None
+        for i in range(args.warmup + args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = shard.search_and_sample_distributed(cloud, cam, w["cfg"], float(tn[0]), float(tf[0]), dist)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        sec = statistics.mean(times)
+        h2d = cloud.positions.numel() * 8 + cloud.colors.numel() * 8 + 8 * m
+        d2h = sum(int(x.nbytes) for x in out) if out is not None else 0
+        dev = torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([sec, h2d, d2h], device=dev, dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return {"value": w["m"] / float(mx[0]), "unit": "rays/s", "h2d_bytes_per_step": int(t[1]),
+                "d2h_bytes_per_step": int(t[2]),
+                "api": "paper_2404_14044_b200.shard.search_and_sample_distributed (numpy in on every rank, the "
+                       "view's 9-tuple out on rank 0; row bands, device rays, gather to rank 0)"}
     host = dict(pixels=pin(w["pixels"][r0:r1]), dirs=pin(w["dirs"][r0:r1]),
-                t_near=pin(w["t_near"][r0:r1]), t_far=pin(w["t_far"][r0:r1]))
+                t_near=pin(tn[r0:r1]), t_far=pin(tf[r0:r1]))
     times, out = [], None
     for i in range(args.warmup + args.steps):
-        if dist is not None:
-            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = pipeline.search_and_sample(cloud, w["cam"], w["cfg"], host["pixels"], host["dirs"],
+        out = pipeline.search_and_sample(cloud, cam, w["cfg"], host["pixels"], host["dirs"],
                                          host["t_near"], host["t_far"])
         torch.cuda.synchronize()
         if i >= args.warmup:
@@ -575,70 +650,91 @@ def run_e2e(args, w, r0, r1, dist=None):
     h2d = (cloud.positions.numel() * 8 + cloud.colors.numel() * 8 + 16 * m + 24 * m + 8 * m + 8 * m
            + 8 * m)
     d2h = sum(int(x.nbytes) for x in out)
-    if dist is not None:  # whole job: slowest rank's time, bytes of all ranks
-        dev = torch.device("cuda", torch.cuda.current_device())
-        t = torch.tensor([sec, h2d, d2h], device=dev, dtype=torch.float64)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        sec, h2d, d2h = float(mx[0]), float(t[1]), float(t[2])
     res = {"value": w["m"] / sec, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h), "api": "paper_2404_14044_b200.pipeline.search_and_sample "
-                                                 "(numpy in / numpy out; per rank: its row band)"}
-    cam = w["cam"]
-    tn, tf = w["t_near"], w["t_far"]
-    if (dist is None and w["m"] == cam.width * cam.height and np.all(tn == tn[0]) and np.all(tf == tf[0])
+                                                 "(pinned host tensors in / numpy out)"}
+    if (w["m"] == cam.width * cam.height and np.all(tn == tn[0]) and np.all(tf == tf[0])
             and np.array_equal(w["pixels"][[0, -1]], [[0, 0], [cam.width - 1, cam.height - 1]])):
-        # the same frame as a whole view: rays generated on the device, only the cloud goes up
+        # the same frame as a whole view from plain numpy inputs (pageable
+        # copies): rays generated on the device, only the cloud goes up
+        npcloud = w["cloud"]
         vt = []
         for i in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            vout = pipeline.search_and_sample_view(cloud, cam, w["cfg"], float(tn[0]), float(tf[0]))
+            vout = pipeline.search_and_sample_view(npcloud, cam, w["cfg"], float(tn[0]), float(tf[0]))
             torch.cuda.synchronize()
             if i >= args.warmup:
                 vt.append(time.perf_counter() - t0)
         vsec = statistics.mean(vt)
         res["view"] = {"value": w["m"] / vsec, "unit": "rays/s",
-                       "h2d_bytes_per_step": int(cloud.positions.numel() * 8 + cloud.colors.numel() * 8 + 8 * m),
+                       "h2d_bytes_per_step": int(npcloud.positions.nbytes + npcloud.colors.nbytes + 8 * m),
                        "d2h_bytes_per_step": int(sum(int(x.nbytes) for x in vout)),
-                       "api": "paper_2404_14044_b200.pipeline.search_and_sample_view (the camera's ray grid "
-                              "on the device; slopes on host threads)"}
+                       "api": "paper_2404_14044_b200.pipeline.search_and_sample_view (numpy arrays in: the "
+                              "camera's ray grid on the device, slopes on host threads; numpy out)"}
     return res
 
 
-def parity_gate(w, dev):
-    """Device vs oracle on every k-th ray of the frame (PARITY_STRIDE) (bit-exact ids/t/dist/
-    udf/primary; alpha/w within 1e-12)."""
-    import torch
+def rays_of(samples, rays):
+    """The listed rays' part of a sampler 9-tuple (device tensors) as numpy,
+    CSR offsets rebased (the same layout the oracle returns for those rays)."""
+    off = samples[0].cpu().numpy()
+    rays = np.asarray(rays, np.int64)
+    lo, hi = off[rays], off[rays + 1]
+    rows = np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)]) if len(rays) else np.zeros(0, np.int64)
+    idx = torch_index(rows, samples[1].device)
+    out = [np.concatenate([[0], np.cumsum(hi - lo)]).astype(np.int64)]
+    for k in range(1, 7):
+        out.append(samples[k][idx].cpu().numpy())
+    col = samples[7]
+    out.append(col[idx].cpu().numpy() if col.shape[0] else np.zeros((0, 3)))
+    out.append(samples[8][torch_index(rays, samples[8].device)].cpu().numpy())
+    return out
 
+
+def torch_index(a, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).to(dev)
+
+
+def same_samples(got, ref, colors=True):
+    """Bit-exact r_off / ids / t / dist / udf (and so the primary-surface point,
+    the first retained candidate of each ray); alpha / w / colour / t_end
+    within rtol 1e-12 (exp() of CUDA vs glibc may differ by an ulp)."""
+    ok = all(np.array_equal(got[k], ref[k]) for k in range(5))
+    ok &= all(np.allclose(got[k], ref[k], rtol=1e-12, atol=1e-300) for k in (5, 6, 8))
+    if colors:
+        ok &= np.allclose(got[7], ref[7], rtol=1e-12, atol=1e-300)
+    return bool(ok)
+
+
+def oracle_samples(cloud, cam, cfg, pixels, dirs, tn, tf, slopes, build=None):
+    """The reference algorithm (C oracle) on the given rays: build, query, sample."""
     from oracle import oracle as orc
-    from paper_2404_14044_b200 import device as dv
     from paper_2404_14044_b200.sampler import SamplerConfig
-    sel = slice(0, None, PARITY_STRIDE.get(w["name"], 53))
-    cam, cfg, cloud = w["cam"], w["cfg"], w["cloud"]
-    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-    idx = dv.build(up(cloud.positions), cam, cfg.pad)
-    px = np.ascontiguousarray(w["pixels"][sel])
-    q = dv.query(idx, up(px), up(w["dirs"][sel]), up(w["t_near"][sel]), up(w["t_far"][sel]),
-                 up(w["slopes"][sel]))
+    b = build if build is not None else orc.build(cloud.positions, cam, cfg.pad)
+    px = np.ascontiguousarray(pixels)
+    q = orc.query(b["table_start"], b["table_count"], b["slot_x"], b["slot_y"], b["slot_z"],
+                  b["reordered_ids"], cam.width + 2 * cfg.pad, cfg.pad, px[:, 0], px[:, 1],
+                  dirs, cam.origin, tn, tf, slopes, threads=host_threads())
     sc = SamplerConfig()
-    s = dv.sample(q[0], q[1], q[2], q[3], up(w["slopes"][sel]), sc, up(cloud.colors))
-    b = orc.build(cloud.positions, cam, cfg.pad)
-    oq = orc.query(b["table_start"], b["table_count"], b["slot_x"], b["slot_y"], b["slot_z"],
-                   b["reordered_ids"], cam.width + 2 * cfg.pad, cfg.pad, px[:, 0], px[:, 1],
-                   w["dirs"][sel], cam.origin, w["t_near"][sel], w["t_far"][sel], w["slopes"][sel],
-                   threads=host_threads())
-    os_ = orc.sample(*oq[:4], w["slopes"][sel], sc.k_neighbors, sc.beta * sc.beta, sc.gamma, True,
-                     sc.epsilon, sc.tau_min, cloud.colors, threads=host_threads())
-    ok = all(np.array_equal(a.cpu().numpy(), b_) for a, b_ in zip(q, oq))
-    s = [x.cpu().numpy() for x in s]
-    ok &= all(np.array_equal(s[k], os_[k]) for k in range(5))
-    ok &= all(np.allclose(s[k], os_[k], rtol=1e-12, atol=1e-300) for k in (5, 6, 7, 8))
-    if not ok:
-        raise SystemExit("parity gate failed: device results differ from the oracle; not timing")
-    return (f"pass (every {PARITY_STRIDE.get(w['name'], 53)}th ray, {len(px)} rays, Q={len(oq[1])}, "
-            f"R={len(os_[1])})")
+    s = orc.sample(*q[:4], slopes, sc.k_neighbors, sc.beta * sc.beta, sc.gamma, True,
+                   sc.epsilon, sc.tau_min, cloud.colors, threads=host_threads())
+    return s, int(q[0][-1])
+
+
+def parity_gate(w, samples, r0, r1, stride):
+    """Fairness gate of the reference bench (bench.py:114-134): the TIMED
+    frame's own output (the last timed step's samples of rays [r0, r1)) on
+    every stride-th ray against the oracle; refuses the number on a mismatch."""
+    sel = np.arange(r0, r1, stride)
+    got = rays_of(samples, sel - r0)
+    ref, Q = oracle_samples(w["cloud"], w["cam"], w["cfg"], w["pixels"][sel], w["dirs"][sel],
+                            w["t_near"][sel], w["t_far"][sel], w["slopes"][sel])
+    if not same_samples(got, ref):
+        raise SystemExit("parity gate failed: the timed frame differs from the oracle; number rejected")
+    return (f"pass (timed frame, every {stride}th ray: {len(sel)} rays, Q={Q}, R={len(ref[1])}; "
+            "ids/t/dist/udf/primary bit-exact, alpha/w/colour/t_end rtol 1e-12)")
 
 
 def main():

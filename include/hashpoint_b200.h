@@ -13,6 +13,7 @@
  *
  * Reference interfaces replaced (reference = /root/reference/pkg/src/hashpoint):
  *   hp_build            hash_index.build            hash_index.py:151-190
+ *   hp_scatter_by_bucket _kernels.scatter_by_bucket  _kernels.py:76-83
  *                       + _kernels.scatter_by_bucket  _kernels.py:76-83
  *                       + rasterize_points / morton_codes hash_index.py:81-112
  *   hp_layout_from_table (internal re-layout of a HashIndex built elsewhere;
@@ -106,6 +107,18 @@ int hp_build(const double* positions, int64_t n, const hp_camera* cam, int64_t p
              int64_t* table_start, int64_t* table_count, int64_t* reordered_ids,
              double* slot_x, double* slot_y, double* slot_z, hp_query_layout layout,
              int64_t* n_in, void* workspace, size_t workspace_bytes, hp_stream_t stream);
+
+/* The reference's counting-sort placement operator on its own
+ * (_kernels.scatter_by_bucket, _kernels.py:76-83): for j in input order,
+ * out_ids[cursor[buckets[j]]++] = orig_ids[j].  buckets / orig_ids int64 [n],
+ * cursor int64 [n_buckets] (updated in place, as the reference), out_ids
+ * int64 [n_out] (only the placed positions are written).  The buckets'
+ * destination ranges must not overlap (cursor = an exclusive scan of the
+ * counts, as hash_index.build passes it); the caller checks ranges. */
+int hp_scatter_by_bucket_workspace_bytes(int64_t n, int64_t n_buckets, int64_t n_out, size_t* bytes);
+int hp_scatter_by_bucket(const int64_t* buckets, const int64_t* orig_ids, int64_t n, int64_t* cursor,
+                         int64_t n_buckets, int64_t* out_ids, int64_t n_out, void* workspace,
+                         size_t workspace_bytes, hp_stream_t stream);
 
 int hp_layout_workspace_bytes(int64_t n_in, int64_t padded_w, int64_t padded_h, size_t* bytes);
 int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,

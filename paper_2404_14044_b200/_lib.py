@@ -52,6 +52,8 @@ _SIGNATURES = {
     "hp_build_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
     "hp_build": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(Camera), c_i64, c_p, c_p, c_p, c_p, c_p,
                                 c_p, Layout, c_p, c_p, c_size, c_p]),
+    "hp_scatter_by_bucket_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_scatter_by_bucket": (ctypes.c_int, [c_p, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_size, c_p]),
     "hp_layout_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
     "hp_layout_from_table": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, c_i64,
                                             ctypes.POINTER(c_f64), Layout, c_p, c_size, c_p]),

@@ -259,6 +259,34 @@ __global__ void k_layout_fill(int64_t P, const int64_t* __restrict__ table_start
     }
 }
 
+// ---------------------------------------------------------------- scatter_by_bucket
+// The reference operator on its own (_kernels.py:76-83): out_ids[cursor[b]++]
+// = orig_ids[j] for j in input order.  Placement by atomic cursor bumps, then
+// every bucket's segment is put back in input order (k_bucket_order on the
+// element indices), then the ids are gathered.
+__global__ void k_sbb_place(int64_t n, const int64_t* __restrict__ buckets, unsigned long long* __restrict__ cursor,
+                            int32_t* __restrict__ slot_j) {
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+        slot_j[atomicAdd(cursor + buckets[j], 1ull)] = int32_t(j);
+}
+
+__global__ void k_sbb_counts(int64_t P, const int64_t* __restrict__ start, const int64_t* __restrict__ cursor,
+                             int64_t* __restrict__ cnt) {
+    for (int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b < P; b += int64_t(gridDim.x) * blockDim.x)
+        cnt[b] = cursor[b] - start[b];
+}
+
+// one warp per bucket: out_ids over the bucket's (now ordered) segment
+__global__ void k_sbb_gather(int64_t P, const int64_t* __restrict__ start, const int64_t* __restrict__ cnt,
+                             const int32_t* __restrict__ slot_j, const int64_t* __restrict__ orig_ids,
+                             int64_t* __restrict__ out_ids) {
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t b = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); b < P; b += warps) {
+        const int64_t s0 = start[b], c = cnt[b];
+        for (int64_t k = lane_id(); k < c; k += 32) out_ids[s0 + k] = orig_ids[slot_j[s0 + k]];
+    }
+}
+
 int levels_for(int wp, int hp) {
     int m = wp > hp ? wp : hp, lv = 0;
     while ((1 << lv) < m) lv++;
@@ -315,6 +343,10 @@ extern "C" int hp_build(const double* positions, int64_t n, const hp_camera* cam
         return HP_EINVAL;
     }
     const int64_t P = wp * hp_;
+    if (P >= (int64_t(1) << 31)) {  // bucket ids, row pointers and scans are int32
+        set_error("hp_build: padded grid of %lld pixels must be below 2^31", (long long)P);
+        return HP_EINVAL;
+    }
     Carver c(workspace, workspace_bytes);
     BuildWs w = carve_build(c, n, P);
     if (!c.ok()) {
@@ -381,6 +413,10 @@ extern "C" int hp_layout_from_table(const int64_t* table_start, const int64_t* t
                                     int64_t padded_h, const double* origin_host, hp_query_layout layout,
                                     void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     const int64_t P = padded_w * padded_h;
+    if (padded_w < 0 || padded_h < 0 || n_in < 0 || P >= (int64_t(1) << 31) || n_in >= (int64_t(1) << 31)) {
+        set_error("hp_layout_from_table: padded grid and point count must be below 2^31");
+        return HP_EINVAL;
+    }
     Carver c(workspace, workspace_bytes);
     int32_t* cnt = c.take<int32_t>(P);
     void* scan = c.take<char>(scan_workspace_bytes(P + 1));
@@ -397,5 +433,53 @@ extern "C" int hp_layout_from_table(const int64_t* table_start, const int64_t* t
                                                         slot_ids, origin_host[0], origin_host[1],
                                                         origin_host[2], layout);
     HP_CHECK_LAUNCH("k_layout_fill");
+    return HP_OK;
+}
+
+extern "C" int hp_scatter_by_bucket_workspace_bytes(int64_t n, int64_t n_buckets, int64_t n_out, size_t* bytes) {
+    Carver c(nullptr, 0);
+    c.take<int64_t>(n_buckets > 0 ? n_buckets : 1);
+    c.take<int64_t>(n_buckets > 0 ? n_buckets : 1);
+    c.take<int32_t>(n_out > 0 ? n_out : 1);
+    c.take<int32_t>(n_buckets > 0 ? n_buckets : 1);
+    c.take<int32_t>(1);
+    *bytes = c.used + 256;
+    (void)n;
+    return HP_OK;
+}
+
+extern "C" int hp_scatter_by_bucket(const int64_t* buckets, const int64_t* orig_ids, int64_t n, int64_t* cursor,
+                                    int64_t n_buckets, int64_t* out_ids, int64_t n_out, void* workspace,
+                                    size_t workspace_bytes, hp_stream_t stream) {
+    if (n < 0 || n_buckets < 0 || n_out < 0 || n >= (int64_t(1) << 31) || n_out >= (int64_t(1) << 31)) {
+        set_error("hp_scatter_by_bucket: invalid sizes");
+        return HP_EINVAL;
+    }
+    Carver c(workspace, workspace_bytes);
+    int64_t* start = c.take<int64_t>(n_buckets > 0 ? n_buckets : 1);
+    int64_t* cnt = c.take<int64_t>(n_buckets > 0 ? n_buckets : 1);
+    int32_t* slot_j = c.take<int32_t>(n_out > 0 ? n_out : 1);
+    int32_t* big_list = c.take<int32_t>(n_buckets > 0 ? n_buckets : 1);
+    int32_t* big_n = c.take<int32_t>(1);
+    if (!c.ok()) {
+        set_error("hp_scatter_by_bucket: workspace too small");
+        return HP_ESPACE;
+    }
+    if (n == 0) return HP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(start, cursor, size_t(n_buckets) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess ||
+        cudaMemsetAsync(big_n, 0, sizeof(int32_t), s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_scatter_by_bucket copy");
+    k_sbb_place<<<grid_for(n, 256), 256, 0, s>>>(n, buckets, reinterpret_cast<unsigned long long*>(cursor), slot_j);
+    HP_CHECK_LAUNCH("k_sbb_place");
+    k_sbb_counts<<<grid_for(n_buckets, 256), 256, 0, s>>>(n_buckets, start, cursor, cnt);
+    HP_CHECK_LAUNCH("k_sbb_counts");
+    k_bucket_order<<<grid_for(n_buckets, 256), 256, 0, s>>>(n_buckets, start, cnt, slot_j, big_list, big_n);
+    HP_CHECK_LAUNCH("k_bucket_order");
+    k_big_bucket_order<<<device_sms() * 2, 512, 0, s>>>(start, cnt, slot_j, big_list, big_n);
+    HP_CHECK_LAUNCH("k_big_bucket_order");
+    k_sbb_gather<<<grid_for(n_buckets * 32, 256), 256, 0, s>>>(n_buckets, start, cnt, slot_j, orig_ids, out_ids);
+    HP_CHECK_LAUNCH("k_sbb_gather");
     return HP_OK;
 }

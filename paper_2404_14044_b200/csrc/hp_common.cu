@@ -4,7 +4,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -28,6 +30,57 @@ int cuda_status(cudaError_t e, const char* where) {
 }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Per-device launch facts: the SM count, and per (kernel, device) the
+// max-dynamic-shared-memory attribute (set once) and the resident CTAs per
+// SM at the given block size / shared memory.  Function attributes apply per
+// device, so a process that moves to another GPU configures it there too.
+namespace {
+std::mutex g_dev_mu;
+std::map<int, int> g_sms;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+}  // namespace
+
+int device_sms() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 148;
+    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = 148;
+    }
+    g_sms[dev] = n;
+    return n;
+}
+
+int kernel_occupancy(const void* fn, int threads, size_t smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    const auto key = std::make_tuple(fn, dev, threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+    }
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (n < 1) {
+        set_error("kernel does not fit one CTA per SM (%d threads, %zu B shared memory)", threads, smem);
+        return HP_ECUDA;
+    }
+    g_occ[key] = n;
+    return n;
+}
 
 // ------------------------------------------------------------------ timing
 namespace {

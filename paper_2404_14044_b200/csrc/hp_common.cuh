@@ -39,7 +39,12 @@ struct TimedSpan {
         if (_rc != HP_OK) return _rc;                                          \
     } while (0)
 
-constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+// SM count of the current device (148 on a B200: 2 dies x 74), cached per device
+int device_sms();
+// Resident CTAs per SM of `fn` at this block size / dynamic shared memory on
+// the current device; sets the kernel's max-dynamic-shared-memory attribute
+// there first (once per device).  Negative HP_E* on failure.
+int kernel_occupancy(const void* fn, int threads, size_t smem);
 
 // ---------------------------------------------------------------- workspace
 // Bump allocator over the caller's workspace; every carve is 256-B aligned.

@@ -616,14 +616,10 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
                              const double* t_near, const double* t_far, const double* slopes, int64_t m,
                              int64_t* offsets, int64_t* head_off, int64_t* probes, int64_t* scanned,
                              int64_t capacity, void* workspace, size_t workspace_bytes, hp_stream_t stream) {
-    HP_TRY(check_common(layout, pad, m));
-    (void)padded_h;
+    HP_TRY(check_common(layout, pad, m, padded_w, padded_h));
     if (!layout.rel4 || !layout.relf || !head_off) {
         set_error("hp_head_count: the layout's relf / rel4 and head_off are required");
         return HP_EINVAL;
-    }
-    if (capacity > INT32_MAX) {  // layout slots are int32; the scratch is indexed by int64
-        capacity = INT32_MAX;
     }
     Carver cv(workspace, workspace_bytes);
     HeadWs w = carve_head(cv, m, capacity);
@@ -641,10 +637,8 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
             HP_CHECK_LAUNCH("k_query_bound");
         }
         HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
-        static const int occ = [] {  // once (thread-safe)
-            set_smem(k_head_scan, sizeof(HeadScanSmem));
-            return resident(k_head_scan, kThreads, sizeof(HeadScanSmem));
-        }();
+        const int occ = kernel_occupancy((const void*)k_head_scan, kThreads, sizeof(HeadScanSmem));
+        if (occ < 0) return occ;
         TimedSpan ts("k_head_scan", s);
         k_head_scan<<<group_grid(m, occ), kThreads, sizeof(HeadScanSmem), s>>>(
             layout, padded_w, int(pad), R, QC, m, w.soff, w.key, w.slot, w.meta, offsets, head_off, probes, scanned,
@@ -671,7 +665,6 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d)", kHeadCap);
         return HP_EINVAL;
     }
-    if (capacity > INT32_MAX) capacity = INT32_MAX;
     Carver cv(workspace, workspace_bytes);
     HeadWs w = carve_head(cv, m, capacity);
     if (!cv.ok()) {
@@ -689,29 +682,26 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     HP_CHECK_LAUNCH("k_head_classes");
     {
         constexpr auto kselect = k_head_select<kHeadCap>;
-        static const int occ_sel = resident(kselect, 128, 0);  // once (thread-safe)
+        const int occ_sel = kernel_occupancy((const void*)kselect, 128, 0);
+        if (occ_sel < 0) return occ_sel;
         TimedSpan ts("k_head_select", s);
-        kselect<<<kNumSMs * occ_sel, 128, 0, s>>>(offsets, w.soff, w.meta, want, whole, w.key, w.sel, list_big,
+        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, w.soff, w.meta, want, whole, w.key, w.sel, list_big,
                                                   w.counts + 1);
         HP_CHECK_LAUNCH("k_head_select");
     }
     constexpr auto ksmall = k_head_sort<kHeadSmall, 128>;
     constexpr auto kbig = k_head_sort<kHeadCap, 256>;
-    static const int occ_small = [] {
-        set_smem(ksmall, sizeof(HeadSmem<kHeadSmall>));
-        return resident(ksmall, 128, sizeof(HeadSmem<kHeadSmall>));
-    }();
-    static const int occ_big = [] {
-        set_smem(kbig, sizeof(HeadSmem<kHeadCap>));
-        return resident(kbig, 256, sizeof(HeadSmem<kHeadCap>));
-    }();
+    const int occ_small = kernel_occupancy((const void*)ksmall, 128, sizeof(HeadSmem<kHeadSmall>));
+    if (occ_small < 0) return occ_small;
+    const int occ_big = kernel_occupancy((const void*)kbig, 256, sizeof(HeadSmem<kHeadCap>));
+    if (occ_big < 0) return occ_big;
     TimedSpan ts("k_head_sort", s);
-    ksmall<<<kNumSMs * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
+    ksmall<<<device_sms() * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
         layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts, whole,
         head_t,
         head_ids, head_dist, plen, facts, cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_sort small");
-    kbig<<<kNumSMs * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
+    kbig<<<device_sms() * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
         layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big, w.counts + 1,
         whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_sort");

@@ -592,11 +592,9 @@ struct SortArgs {
 template <int kCap, int kT>
 static int launch_sort(const SortArgs& A, int cls, cudaStream_t s) {
     // once per process (thread-safe initialisation); a failure shows at launch
-    static const int occ = [] {
-        set_smem(k_query_sort<kCap, kT>, sizeof(SortSmem<kCap>));
-        return resident(k_query_sort<kCap, kT>, kT, sizeof(SortSmem<kCap>));
-    }();
-    k_query_sort<kCap, kT><<<kNumSMs * occ, kT, sizeof(SortSmem<kCap>), s>>>(
+    const int occ = kernel_occupancy((const void*)k_query_sort<kCap, kT>, kT, sizeof(SortSmem<kCap>));
+    if (occ < 0) return occ;
+    k_query_sort<kCap, kT><<<device_sms() * occ, kT, sizeof(SortSmem<kCap>), s>>>(
         A.offsets, A.w.soff, A.w.tmm, A.slopes, A.facts, A.w.lists + int64_t(cls) * A.m, A.w.counts + cls, A.w.st, A.w.sid, A.w.sd,
         A.ids, A.t, A.d);
     HP_CHECK_LAUNCH("k_query_sort");
@@ -635,8 +633,7 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
                               const double* t_near, const double* t_far, const double* slopes, int64_t m,
                               int64_t* offsets, int64_t* probes, int64_t* scanned, int64_t capacity,
                               void* workspace, size_t workspace_bytes, hp_stream_t stream) {
-    HP_TRY(check_common(layout, pad, m));
-    (void)padded_h;
+    HP_TRY(check_common(layout, pad, m, padded_w, padded_h));
     Carver cv(workspace, workspace_bytes);
     QueryWs w = carve_query(cv, m, capacity);
     if (!cv.ok()) {
@@ -653,8 +650,8 @@ extern "C" int hp_query_count(hp_query_layout layout, const hp_camera* cam, int6
             HP_CHECK_LAUNCH("k_query_bound");
         }
         HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
-        static const int attr = set_smem(k_query_scan, sizeof(FillSmem));  // once (thread-safe)
-        (void)attr;
+        const int occ = kernel_occupancy((const void*)k_query_scan, kThreads, sizeof(FillSmem));
+        if (occ < 0) return occ;
         TimedSpan ts("k_query_scan", s);
         k_query_scan<<<group_grid(m, HP_SCAN_MINB ? HP_SCAN_MINB : 4), kThreads, sizeof(FillSmem), s>>>(layout, padded_w, int(pad), R, QC, m, w.soff,
                                                                          w.sid, w.st, w.sd, w.tmm, offsets, probes,
@@ -707,19 +704,19 @@ extern "C" int hp_query_fill(const int64_t* offsets, int64_t m, int64_t total, i
         HP_TRY((launch_sort<kSortHuge, 1024>(A, 3, s)));
     }
     // rays above kSortHuge: split into t-ordered parts, sort the parts in place
-    static const int occ_parts = [] {  // once (thread-safe)
-        set_smem(k_query_split, sizeof(SplitSmem));
-        set_smem(k_query_sort_parts<kSortHuge, 1024>, sizeof(SortSmem<kSortHuge>));
-        return resident(k_query_sort_parts<kSortHuge, 1024>, 1024, sizeof(SortSmem<kSortHuge>));
-    }();
+    const int occ_split = kernel_occupancy((const void*)k_query_split, kSplitThreads, sizeof(SplitSmem));
+    if (occ_split < 0) return occ_split;
+    const int occ_parts =
+        kernel_occupancy((const void*)k_query_sort_parts<kSortHuge, 1024>, 1024, sizeof(SortSmem<kSortHuge>));
+    if (occ_parts < 0) return occ_parts;
     if (cudaMemsetAsync(w.parts_n, 0, sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_query_fill memset");
     TimedSpan tsp("k_query_split", s);
-    k_query_split<<<kNumSMs, kSplitThreads, sizeof(SplitSmem), s>>>(
+    k_query_split<<<device_sms(), kSplitThreads, sizeof(SplitSmem), s>>>(
         offsets, w.soff, w.tmm, w.lists + kSortClasses * m, w.counts + kSortClasses, w.st, w.sid, w.sd, ids, t_proj,
         dist_perp, w.parts, w.parts_n, w.parts_cap);
     HP_CHECK_LAUNCH("k_query_split");
-    k_query_sort_parts<kSortHuge, 1024><<<kNumSMs * occ_parts, 1024, sizeof(SortSmem<kSortHuge>), s>>>(
+    k_query_sort_parts<kSortHuge, 1024><<<device_sms() * occ_parts, 1024, sizeof(SortSmem<kSortHuge>), s>>>(
         w.parts, w.parts_n, w.parts_cap, ids, t_proj, dist_perp);
     HP_CHECK_LAUNCH("k_query_sort_parts");
     return HP_OK;
@@ -729,8 +726,7 @@ extern "C" int hp_query_bounds(hp_query_layout layout, const hp_camera* cam, int
                                int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
                                const double* t_near, const double* t_far, const double* slopes, int64_t m,
                                int64_t* bound_off, void* workspace, size_t workspace_bytes, hp_stream_t stream) {
-    HP_TRY(check_common(layout, pad, m));
-    (void)padded_h;
+    HP_TRY(check_common(layout, pad, m, padded_w, padded_h));
     if (workspace_bytes < scan_workspace_bytes(m + 1)) {
         set_error("hp_query_bounds: workspace too small");
         return HP_ESPACE;

@@ -235,23 +235,6 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 }
 
 
-// Resident CTAs per SM of a kernel at its block size / dynamic smem (>= 1).
-template <class K>
-int resident(K kernel, int threads, size_t smem) {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) {
-        cudaGetLastError();
-        n = 1;
-    }
-    return n;
-}
-
-template <class K>
-int set_smem(K kernel, size_t bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    return e == cudaSuccess ? HP_OK : cuda_status(e, "cudaFuncSetAttribute");
-}
-
 QCam make_qcam(const hp_camera* cam) {
     QCam q{};
     q.has_cam = cam != nullptr;
@@ -272,9 +255,13 @@ QCam make_qcam(const hp_camera* cam) {
     return q;
 }
 
-int check_common(const hp_query_layout& L, int64_t pad, int64_t m) {
-    if (pad < 0 || m < 0 || !L.row_ptr) {
+int check_common(const hp_query_layout& L, int64_t pad, int64_t m, int64_t wp, int64_t hp) {
+    if (pad < 0 || m < 0 || !L.row_ptr || wp < 0 || hp < 0) {
         set_error("hp_query: invalid arguments");
+        return HP_EINVAL;
+    }
+    if (wp * hp >= (int64_t(1) << 31)) {  // row pointers are int32 (hp_build rejects such grids)
+        set_error("hp_query: padded grid must be below 2^31 pixels");
         return HP_EINVAL;
     }
     if (2 * pad + 1 > 0xFFFF) {
@@ -286,7 +273,7 @@ int check_common(const hp_query_layout& L, int64_t pad, int64_t m) {
 
 unsigned group_grid(int64_t m, int per_sm) {
     const int64_t groups = (m + kGroupMax - 1) / kGroupMax;
-    const int64_t cap = int64_t(kNumSMs) * per_sm;
+    const int64_t cap = int64_t(device_sms()) * per_sm;
     return unsigned(groups < cap ? (groups > 0 ? groups : 1) : cap);
 }
 

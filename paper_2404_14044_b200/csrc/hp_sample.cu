@@ -523,7 +523,7 @@ template <class BestT>
 int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     {
         TimedSpan ts("k_sample_plan", s);
-        k_sample_plan<<<kNumSMs * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff);
+        k_sample_plan<<<device_sms() * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff);
         HP_CHECK_LAUNCH("k_sample_plan");
     }
     HP_TRY(exclusive_scan_i64(w.eoff, w.eoff, C.m, w.scan, s));
@@ -531,12 +531,12 @@ int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     // device and do nothing if it exceeds the capacity (reported in r_off[m])
     {
         TimedSpan ts("k_sample_expand", s);
-        k_sample_expand<<<kNumSMs * 8, 256, 0, s>>>(C.m, w.eoff, w.x.ray, w.x.cap);
+        k_sample_expand<<<device_sms() * 8, 256, 0, s>>>(C.m, w.eoff, w.x.ray, w.x.cap);
         HP_CHECK_LAUNCH("k_sample_expand");
     }
     {
         TimedSpan ts("k_sample_exact", s);
-        k_sample_exact<BestT><<<kNumSMs * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
+        k_sample_exact<BestT><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
         HP_CHECK_LAUNCH("k_sample_exact");
     }
     return HP_OK;

@@ -222,6 +222,8 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
         total = int(offsets[m].item())
         if total >= 0:
             break
+        if _ == 1:
+            raise RuntimeError(f"hp_query_count: scratch of {cap} slots still short ({-total} needed)")
         needed = -total  # scratch too small: nothing was written, grow it once (and remember)
         if max_scratch is not None and needed > max_scratch:
             raise MatchBudgetExceeded(needed, int(max_scratch))
@@ -325,6 +327,8 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
         total, hcap = int(both[0]), int(both[1])
         if total >= 0:
             break
+        if _ == 1:
+            raise RuntimeError(f"hp_head_count: scratch of {cap} slots still short ({-total} needed)")
         needed = -total
         if max_scratch is not None and needed > max_scratch:
             raise MatchBudgetExceeded(needed, int(max_scratch))
@@ -366,6 +370,7 @@ def _head(index, counted, dirs, slopes, want=PREFIX_WANT, whole=None) -> QueryPr
     _mark("query.prefix")
     pre = QueryPrefix(offsets, probes, scanned, head_off[:m], plen, ht, hi, hd, cut[0], cut[1], fa, ws)
     pre.total = total
+    pre.want, pre.whole = int(want), whole
     return pre
 
 
@@ -382,6 +387,15 @@ def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix:
 
 
 def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerParams:
+    """C parameter block from a SamplerConfig; a ready _lib.SamplerParams
+    (the reference operator's raw arguments, e.g. beta2 given directly) is
+    taken as is, with want_color / exact_t_end applied."""
+    if isinstance(cfg, _lib.SamplerParams):
+        p = _lib.SamplerParams()
+        ctypes.pointer(p)[0] = cfg
+        p.want_color = 1 if want_color else 0
+        p.exact_t_end = 1 if exact_t_end else 0
+        return p
     p = _lib.SamplerParams()
     p.k_neighbors = int(cfg.k_neighbors)
     p.eps_mode = 1 if cfg.retention_mode == "epsilon" else 0

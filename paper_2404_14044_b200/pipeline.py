@@ -76,7 +76,7 @@ class FrameResult:
     chunks: int = 1
     flagged: int = 0         # prefix mode: rays re-run through the full query
     prefix: bool = False     # the frame ran in prefix mode
-    prefix_len: object = None  # prefix mode: device tensor, total prefix length (sum over rays)
+    prefix_len: object = None  # TRACK_PREFIX_LEN: device int64[4] (Σ head length, Σ q cut / whole, hit rays)
 
     @property
     def R(self) -> int:
@@ -152,8 +152,8 @@ _PREFIX_ENV = os.environ.get("HP_PREFIX", "1")
 PREFIX = _PREFIX_ENV != "0"
 
 
-_PREFIX_LEN: list = []  # prefix lengths of the passes of the current frame (device scalars)
-TRACK_PREFIX_LEN = False  # bench.py: report Σ prefix length (one extra reduction per pass)
+_PREFIX_LEN: list = []  # head statistics of the passes of the current frame (device tensors)
+TRACK_PREFIX_LEN = False  # bench.py: report the head statistics (a few extra reductions per pass)
 
 
 def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None):
@@ -163,8 +163,11 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     need more).  (samples 9-tuple, Q, flagged)"""
     *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
     Q = pre.total
-    if TRACK_PREFIX_LEN:
-        _PREFIX_LEN.append(pre.length.sum())
+    if TRACK_PREFIX_LEN:  # [Σ head length, Σ q of the cut rays, Σ q of the whole rays, rays with matches]
+        q = pre.offsets[1:] - pre.offsets[:-1]
+        cut = q > pre.whole
+        _PREFIX_LEN.append(torch.stack([pre.length.sum().to(torch.int64), torch.where(cut, q, 0).sum(),
+                                        torch.where(cut, 0, q).sum(), (q > 0).sum()]))
     # the heads and their workspace are no longer needed (sample_prefix copied its outputs)
     pre.t = pre.ids = pre.dist = pre._ws = None
     if n_flagged:

@@ -1,7 +1,9 @@
-"""Multi-rank sharding on CPU (gloo, world_size 2): cost-balanced row bands +
-the retained-sample gather reassemble exactly the single-rank frame.  The
-per-rank compute here is the oracle (the device kernels need a GPU); the
-sharding and collective logic is the same code bench.py runs over NCCL."""
+"""Multi-rank sharding on CPU (gloo, world_size 2): cost-balanced row bands
+(computed from the index's table, as every rank does on its GPU) + the
+retained-sample gather to rank 0 reassemble exactly the single-rank frame.
+The per-rank compute here is the oracle (the device kernels need a GPU); the
+sharding and collective logic is the same code
+shard.search_and_sample_distributed / bench.py run over NCCL."""
 
 import os
 import socket
@@ -13,7 +15,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_2404_14044_b200 as hp
-from paper_2404_14044_b200.shard import balanced_row_bands, gather_samples, row_costs, split_by_cost
+from paper_2404_14044_b200.shard import (balanced_row_bands, gather_samples, row_costs, row_costs_from_table,
+                                         split_by_cost)
 
 
 def _setup():
@@ -38,12 +41,18 @@ def _frame(cloud, cam, cfg, dirs, pixels, slopes, lo, hi):
                       sc.epsilon, sc.tau_min, cloud.colors)
 
 
-def _worker(rank, world, port, result_q):
+def _worker(rank, world, port, result_q, mode="bands"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cloud, cam, cfg, dirs, pixels, slopes = _setup()
-    bands = balanced_row_bands(cloud.positions, cam, cfg.pad, world)
-    lo, hi = bands[rank][0] * cam.width, bands[rank][1] * cam.width
+    if mode == "bands":  # bands from the index's table (as each GPU rank computes them)
+        from oracle import oracle as orc
+        tc = torch.from_numpy(orc.build(cloud.positions, cam, cfg.pad)["table_count"])
+        bands = balanced_row_bands(None, cam, cfg.pad, world, table_count=tc)
+        lo, hi = bands[rank][0] * cam.width, bands[rank][1] * cam.width
+    else:  # "empty": rank 1 holds only sky rays (no samples), rank 0 the rest
+        sky = 2 * cam.width  # the first two rows miss the sphere
+        lo, hi = (sky, dirs.shape[0]) if rank == 0 else (0, sky)
     out = _frame(cloud, cam, cfg, dirs, pixels, slopes, lo, hi)
     tens = tuple(torch.from_numpy(np.ascontiguousarray(x)) for x in out)
     g = gather_samples(tens, dist)
@@ -61,23 +70,54 @@ def _free_port():
     return port
 
 
-@pytest.mark.timeout(300)
-def test_two_rank_gather_equals_single_rank():
+def _run_two(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, mode)) for r in range(2)]
     for p in procs:
         p.start()
     got = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return got
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gather_equals_single_rank():
+    got = _run_two("bands")
     cloud, cam, cfg, dirs, pixels, slopes = _setup()
     ref = _frame(cloud, cam, cfg, dirs, pixels, slopes, 0, dirs.shape[0])
     assert len(ref[1]) > 0
+    assert got[1].dtype == np.int64
     for a, b in zip(got, ref):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.timeout(300)
+def test_gather_with_a_rank_without_samples_keeps_colours():
+    """a rank whose band retained nothing (sky rows) packs the same
+    tile width as the others, so colours survive the gather."""
+    got = _run_two("empty")
+    cloud, cam, cfg, dirs, pixels, slopes = _setup()
+    sky = 2 * cam.width
+    a = _frame(cloud, cam, cfg, dirs, pixels, slopes, sky, dirs.shape[0])
+    b = _frame(cloud, cam, cfg, dirs, pixels, slopes, 0, sky)
+    assert len(b[1]) == 0 and len(a[1]) > 0 and a[7].shape[0] == len(a[1])
+    ref_off = np.concatenate([a[0], a[0][-1] + b[0][1:]])
+    np.testing.assert_array_equal(got[0], ref_off)
+    for k in range(1, 8):
+        np.testing.assert_array_equal(got[k], a[k])
+    np.testing.assert_array_equal(got[8], np.concatenate([a[8], b[8]]))
+
+
+def test_row_costs_from_table_equal_host_projection():
+    from oracle import oracle as orc
+    cloud, cam, cfg, dirs, pixels, slopes = _setup()
+    tc = torch.from_numpy(orc.build(cloud.positions, cam, cfg.pad)["table_count"])
+    np.testing.assert_array_equal(row_costs_from_table(tc, cam, cfg.pad).numpy(),
+                                  row_costs(cloud.positions, cam, cfg.pad))
 
 
 def test_split_by_cost_is_contiguous_and_balanced():
