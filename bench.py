@@ -509,8 +509,10 @@ def run_ours(args, w, rank, world, dist):
     # N > 1 every rank runs its band concurrently, max time over ranks
     # one more (untimed) frame for the prefix kernel's bytes: Σ prefix length
     pipeline.TRACK_PREFIX_LEN = True
+    pipeline.FLAG_REASONS.clear()
     plen_fr = step()
     pipeline.TRACK_PREFIX_LEN = False
+    flag_reasons = [int(x) for x in sum(pipeline.FLAG_REASONS).cpu()] if pipeline.FLAG_REASONS else None
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, w, r0, r1, dist)
@@ -563,7 +565,9 @@ def run_ours(args, w, rank, world, dist):
                    "n_indexed": fr.index.n_in, "Q": Q, "R": R, "P": P,
                    "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"row bands x{world}" if world > 1 else "single GPU",
-                   "ray_chunks": fr.chunks, "prefix_mode": fr.prefix, "prefix_flagged_rays": fr.flagged,
+                   "ray_chunks": fr.chunks, "prefix_mode": fr.prefix, "head_resorted_rays": fr.resorted,
+                   "full_path_rays": fr.flagged,
+                   "flag_reasons": flag_reasons,
                    "parity_gate": parity},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

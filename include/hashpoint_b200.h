@@ -181,7 +181,10 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
  * head_ids int32 (same workspace and capacity), plen [m] = the head length,
  * facts [m] (as hp_query_fill's, over the head; -1 when unknown), and cut_t /
  * cut_d [m] = lower bounds of the t / dist of every match left out (+inf when
- * none).  hp_sample_run_prefix consumes them. */
+ * none).  hp_sample_run_prefix consumes them.  rays (int32 [n], or NULL for
+ * all m rays): re-sort only these rays of the same count pass (e.g. with a
+ * longer `want` for rays the sampler flagged); output i (head_off[i], plen[i],
+ * facts[i], cuts[i]) then stands for ray rays[i]. */
 int hp_head_workspace_bytes(int64_t m, int64_t capacity, size_t* bytes);
 int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
                   int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
@@ -189,10 +192,10 @@ int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w
                   int64_t* offsets, int64_t* head_off, int64_t* probes, int64_t* scanned,
                   int64_t capacity, void* workspace, size_t workspace_bytes, hp_stream_t stream);
 int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
-                 const int64_t* offsets, const int64_t* head_off, int32_t want, int32_t whole, double* head_t,
-                 int32_t* head_ids, double* head_dist, int32_t* plen, int32_t* facts, double* cut_t,
-                 double* cut_d, int64_t capacity, void* workspace, size_t workspace_bytes,
-                 hp_stream_t stream);
+                 const int64_t* offsets, const int32_t* rays, int64_t n, const int64_t* head_off, int32_t want,
+                 int32_t whole, double* head_t, int32_t* head_ids, double* head_dist, int32_t* plen,
+                 int32_t* facts, double* cut_t, double* cut_d, int64_t capacity, void* workspace,
+                 size_t workspace_bytes, hp_stream_t stream);
 
 /* Upper bounds of the match counts (the slots pass 1 will test per ray),
  * exclusive-scanned into bound_off [m+1] (bound_off[m] = the scratch pass 1

@@ -67,9 +67,8 @@ _SIGNATURES = {
     "hp_head_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                      c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_i64,
                                      c_p, c_size, c_p]),
-    "hp_head_sort": (ctypes.c_int, [Layout, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, ctypes.c_int32, c_p, c_p,
-                                    c_p, c_p,
-                                    c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
+    "hp_head_sort": (ctypes.c_int, [Layout, c_p, c_p, c_i64, c_p, c_p, c_i64, c_p, ctypes.c_int32, ctypes.c_int32,
+                                    c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
     "hp_ray_grid": (ctypes.c_int, [ctypes.POINTER(Camera), c_i64, c_i64, c_p, c_p, ctypes.c_double,
                                    ctypes.c_double, c_p, c_p, c_p]),
     "hp_render": (ctypes.c_int, [ctypes.c_int, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,

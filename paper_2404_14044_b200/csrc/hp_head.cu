@@ -307,14 +307,16 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
 // list 0: rays of 1..min(kHeadSmall, whole) matches (sorted whole by the
 // small configuration), list 1: the longer ones; the empty rays' outputs are
 // written here.
-__global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int whole, int* __restrict__ lists,
-                               int* __restrict__ counts, int* __restrict__ plen, int* __restrict__ facts,
-                               double* __restrict__ cut_t, double* __restrict__ cut_d) {
+// With `rays`, output i stands for ray rays[i] (a re-sort of a subset).
+__global__ void k_head_classes(const int64_t* __restrict__ off, const int* __restrict__ rays, int64_t m, int whole,
+                               int* __restrict__ lists, int* __restrict__ counts, int* __restrict__ plen,
+                               int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
          r += int64_t(gridDim.x) * blockDim.x) {
         int cls = -1;
         if (r < m) {
-            const int64_t q = off[r + 1] - off[r];
+            const int64_t ri = rays ? rays[r] : r;
+            const int64_t q = off[ri + 1] - off[ri];
             cls = q == 0 ? -1 : (q <= min(kHeadSmall, whole) ? 0 : 1);
             if (q == 0) {
                 plen[r] = 0;
@@ -343,7 +345,7 @@ __global__ void k_head_classes(const int64_t* __restrict__ off, int64_t m, int w
 // largest key of bin b: sel[r] = (K_c, #{key <= K_c}).  No cut (b < 0):
 // K_c = kmin - 1, count 0.
 template <int kBins>
-__global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__ off,
+__global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__ off, const int* __restrict__ rays,
                                                      const int64_t* __restrict__ soff,
                                                      const RayMeta* __restrict__ meta, int want, int whole,
                                                      const unsigned* __restrict__ sc_key, uint2* __restrict__ sel,
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
     const int64_t warps = int64_t(gridDim.x) * 4;
     const int64_t nr = *list_n;
     for (int64_t k = int64_t(blockIdx.x) * 4 + warp_id(); k < nr; k += warps) {
-        const int64_t r = list[k];
+        const int64_t i = list[k], r = rays ? rays[i] : i;  // output i, ray r
         const int q = int(off[r + 1] - off[r]);
         if (q <= whole) continue;
         const int64_t so = soff[r];
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
             }
             // largest key of bin b (keys above kmax do not occur)
             const unsigned long long kc = (unsigned long long)M.kmin + ((unsigned long long)(b + 1) << sh) - 1ull;
-            sel[r] = make_uint2(unsigned(kc < M.kmax ? kc : M.kmax), unsigned(c));
+            sel[i] = make_uint2(unsigned(kc < M.kmax ? kc : M.kmax), unsigned(c));
         }
         __syncwarp();
     }
@@ -433,7 +435,8 @@ struct HeadSmem {
 template <int kCap, int kT>
 __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head_sort(
     hp_query_layout L, const double* __restrict__ dirs, const double* __restrict__ slopes,
-    const int64_t* __restrict__ off, const int64_t* __restrict__ soff, const int64_t* __restrict__ hoff,
+    const int64_t* __restrict__ off, const int* __restrict__ rays, const int64_t* __restrict__ soff,
+    const int64_t* __restrict__ hoff,
     const RayMeta* __restrict__ meta, const unsigned* __restrict__ sc_key, const int* __restrict__ sc_slot,
     const uint2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n, int whole,
     double* __restrict__ head_t, int* __restrict__ head_id, double* __restrict__ head_d, int* __restrict__ plen,
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
     const int tid = threadIdx.x;
     const int nr = *list_n;
     for (int k = blockIdx.x; k < nr; k += gridDim.x) {
-        const int64_t r = list[k];
+        const int64_t i = list[k], r = rays ? rays[i] : i;  // output i, ray r
         const int64_t so = soff[r];
         const int q = int(off[r + 1] - off[r]);
         const RayMeta M = meta[r];
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
         unsigned kc = 0xffffffffu;
         int S = q;  // pairs to stage
         if (!all) {
-            const uint2 sv = sel[r];
+            const uint2 sv = sel[i];
             kc = sv.x;
             S = int(sv.y);
         }
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
             rank_segment<kCap, kT>(S, from_fkey(M.kmin), from_fkey(F.thi), F.t, F.id, F.bk, F.hist, F.lst, F.perm,
                                    F.chist, F.scan_sh);
         const int Lh = F.keep;
-        const int64_t ho = hoff[r];
+        const int64_t ho = hoff[i];
         const double r0 = Lh > 0 ? dmul(__ldg(slopes + r), F.t[F.perm[0]]) : 0.0;
         int cnt = 0;
         bool bad = false;
@@ -552,8 +555,8 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
         }
         __syncthreads();
         if (tid == 0) {
-            plen[r] = Lh;
-            facts[r] = (F.fbad || Lh == 0) ? -1 : F.fcount;
+            plen[i] = Lh;
+            facts[i] = (F.fbad || Lh == 0) ? -1 : F.fcount;
             // lower bounds of the left-out t / dist: a pair never staged has
             // t >= its key (> K_c) and an unknown dist (0); a trimmed pair's
             // are exact (the smallest trimmed t is the next in order)
@@ -567,8 +570,8 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
                 ct = fmin(ct, F.t[F.perm[Lh]]);
                 cd = fmin(cd, sqrt(dkey_inv(F.cut_d2)));
             }
-            cut_t[r] = ct;
-            cut_d[r] = cd;
+            cut_t[i] = ct;
+            cut_d[i] = cd;
         }
         __syncthreads();
     }
@@ -655,14 +658,13 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
 }
 
 extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
-                            const int64_t* offsets, const int64_t* head_off, int32_t want, int32_t whole,
-                            double* head_t,
-                            int32_t* head_ids, double* head_dist, int32_t* plen, int32_t* facts, double* cut_t,
-                            double* cut_d, int64_t capacity, void* workspace, size_t workspace_bytes,
-                            hp_stream_t stream) {
-    if (m < 0 || want < 1 || want > kHeadCap || whole < want || whole > kHeadCap ||
+                            const int64_t* offsets, const int32_t* rays, int64_t n, const int64_t* head_off,
+                            int32_t want, int32_t whole, double* head_t, int32_t* head_ids, double* head_dist,
+                            int32_t* plen, int32_t* facts, double* cut_t, double* cut_d, int64_t capacity,
+                            void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+    if (m < 0 || want < 1 || want > kHeadCap || whole < want || whole > kHeadCap || (rays && (n < 0 || n > m)) ||
         (m > 0 && (!dirs || !slopes || !facts || !plen || !cut_t || !cut_d || !layout.rel4))) {
-        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d)", kHeadCap);
+        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d, n <= m)", kHeadCap);
         return HP_EINVAL;
     }
     Carver cv(workspace, workspace_bytes);
@@ -671,22 +673,23 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         set_error("hp_head_sort: workspace too small");
         return HP_ESPACE;
     }
-    if (m == 0) return HP_OK;
+    const int64_t nout = rays ? n : m;  // outputs (rays[i] or i)
+    if (nout == 0) return HP_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_head_sort memset");
     const int* list_small = w.lists;
-    const int* list_big = w.lists + m;
-    k_head_classes<<<grid_for(m, 256), 256, 0, s>>>(offsets, m, whole, w.lists, w.counts, plen, facts, cut_t,
-                                                    cut_d);
+    const int* list_big = w.lists + nout;
+    k_head_classes<<<grid_for(nout, 256), 256, 0, s>>>(offsets, rays, nout, whole, w.lists, w.counts, plen, facts,
+                                                       cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_classes");
     {
         constexpr auto kselect = k_head_select<kHeadCap>;
         const int occ_sel = kernel_occupancy((const void*)kselect, 128, 0);
         if (occ_sel < 0) return occ_sel;
         TimedSpan ts("k_head_select", s);
-        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, w.soff, w.meta, want, whole, w.key, w.sel, list_big,
-                                                  w.counts + 1);
+        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, rays, w.soff, w.meta, want, whole, w.key, w.sel,
+                                                       list_big, w.counts + 1);
         HP_CHECK_LAUNCH("k_head_select");
     }
     constexpr auto ksmall = k_head_sort<kHeadSmall, 128>;
@@ -697,13 +700,12 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     if (occ_big < 0) return occ_big;
     TimedSpan ts("k_head_sort", s);
     ksmall<<<device_sms() * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
-        layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts, whole,
-        head_t,
-        head_ids, head_dist, plen, facts, cut_t, cut_d);
+        layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts,
+        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_sort small");
     kbig<<<device_sms() * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
-        layout, dirs, slopes, offsets, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big, w.counts + 1,
-        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
+        layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big,
+        w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_sort");
     return HP_OK;
 }

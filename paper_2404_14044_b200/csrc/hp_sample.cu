@@ -124,14 +124,17 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     const int fact = C.facts ? C.facts[ray] : -1;
     // prefix mode: a ray whose work may reach past its prefix is flagged for
     // the full path (no facts, or a prefix shorter than K)
-    auto flag_out = [&]() {
+    // flag values say why (diagnostics; any nonzero value means "flagged"):
+    // 1 no facts / head shorter than K, 2 preconditions, 3 eligibility past
+    // the head, 4 retention / the zero proof past the head, 5 K nearest past it
+    auto flag_out = [&](int why) {
         if (lane == 0) {
             plan[ray] = make_int4(0, 0, 0, 0);
             ecnt[ray] = 0;
-            C.flag[ray] = 1;
+            C.flag[ray] = why;
         }
     };
-    if (partial && (fact < 0 || q < P.K)) return flag_out();
+    if (partial && (fact < 0 || q < P.K)) return flag_out(1);
     if (C.start && lane == 0) C.flag[ray] = 0;
     if (q == 0) {
         if (lane == 0) {
@@ -163,7 +166,7 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
         }
     }
     const bool fast = __all_sync(0xffffffffu, ok);
-    if (partial && !fast) return flag_out();
+    if (partial && !fast) return flag_out(2);
     int jstar = 0;
     if (fast) {
         if (warp_sum(c0cnt) >= P.K) {
@@ -180,7 +183,7 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
             });
             // prefix counts are the full counts while r_j < cut_d (the
             // left-out matches are all farther out); beyond, unknown
-            if (partial && jstar > 0 && !(dmul(slope, V.t(jstar - 1)) < __ldg(C.cut_d + ray))) return flag_out();
+            if (partial && jstar > 0 && !(dmul(slope, V.t(jstar - 1)) < __ldg(C.cut_d + ray))) return flag_out(3);
         }
     }
     // ---- 1. bound chain (fast path): chain_chunk over 32 candidates at a time
@@ -247,7 +250,7 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     }
     // prefix mode: retention (and, exact t_end, the zero) must be decided
     // inside the prefix
-    if (partial && (je == q || (P.exact_t_end && !proved_zero))) return flag_out();
+    if (partial && (je == q || (P.exact_t_end && !proved_zero))) return flag_out(4);
     if (lane == 0) {
         plan[ray] = make_int4(jstar, je, (fast ? 1 : 0) | (proved_zero ? 2 : 0), q);
         // exact region [0, E): everything unless retention is decided before je
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
             eval_exact<BestT>(V, q, q, CUDART_INF, j, pl.z & 1, pl.x, C.slopes[ray], P, C.ids + lo, C.colors, u, a,
                               col, evals);
         }
-        if (!ok) C.flag[ray] = 1;
+        if (!ok) C.flag[ray] = 5;
         X.udf[c] = u;
         X.alpha[c] = a;
         if (P.want_color) {

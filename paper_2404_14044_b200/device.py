@@ -295,7 +295,7 @@ class QueryPrefix:
 PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "400"))  # head length the sampler usually needs
 HEAD_CAP = 1024  # longest head (hp_head.cu kHeadCap)
 # rays of at most this many matches are sorted whole; longer ones are cut near PREFIX_WANT
-HEAD_WHOLE = int(os.environ.get("HP_HEAD_WHOLE", "1024"))
+HEAD_WHOLE = int(os.environ.get("HP_HEAD_WHOLE", "512"))
 
 
 def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
@@ -341,7 +341,7 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
 
 
 def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
-                 t_far: torch.Tensor, slopes: torch.Tensor, want: int = PREFIX_WANT, footprint: bool = True,
+                 t_far: torch.Tensor, slopes: torch.Tensor, want: int | None = None, footprint: bool = True,
                  max_scratch: int | None = None, whole: int | None = None) -> QueryPrefix:
     """The query for callers that only want samples (hp_head_count +
     hp_head_sort): each ray's head of matches in (t, id) order, without the
@@ -351,8 +351,10 @@ def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
                  slopes, want, whole)
 
 
-def _head(index, counted, dirs, slopes, want=PREFIX_WANT, whole=None) -> QueryPrefix:
-    """hp_head_sort after :func:`_count_head`."""
+def _head(index, counted, dirs, slopes, want=None, whole=None) -> QueryPrefix:
+    """hp_head_sort after :func:`_count_head` (want / whole default to
+    PREFIX_WANT / HEAD_WHOLE, read at call time)."""
+    want = PREFIX_WANT if want is None else want
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
     offsets, head_off, probes, scanned, total, hcap, ws, nb, cap = counted
@@ -364,18 +366,54 @@ def _head(index, counted, dirs, slopes, want=PREFIX_WANT, whole=None) -> QueryPr
     hd = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hi = torch.empty(max(hcap, 1), dtype=torch.int32, device=dev)
     whole = max(int(want), min(HEAD_WHOLE if whole is None else int(whole), HEAD_CAP))
-    _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(offsets), _ptr(head_off),
-                                int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa), _ptr(cut[0]),
-                                _ptr(cut[1]), cap, _ptr(ws), nb, _stream()))
+    _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(offsets), None, 0,
+                                _ptr(head_off), int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen),
+                                _ptr(fa), _ptr(cut[0]), _ptr(cut[1]), cap, _ptr(ws), nb, _stream()))
     _mark("query.prefix")
     pre = QueryPrefix(offsets, probes, scanned, head_off[:m], plen, ht, hi, hd, cut[0], cut[1], fa, ws)
     pre.total = total
     pre.want, pre.whole = int(want), whole
+    pre._sort_args = (index, dirs, slopes, nb, cap)
     return pre
 
 
+def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whole: int = HEAD_CAP) -> QueryPrefix:
+    """Second chance for rays the sampler flagged: re-sort the heads of
+    ``rays`` (int64 indices into ``pre``'s rays) from the same count pass
+    (``pre`` still holds its workspace) with a longer ``want``; no re-scan.
+    Returns a :class:`QueryPrefix` over just those rays (their own offsets,
+    counts unchanged)."""
+    lib = _lib.load(require_device=True)
+    index, dirs, slopes, nb, cap = pre._sort_args
+    dev = pre.offsets.device
+    m = int(pre.offsets.shape[0]) - 1
+    n = int(rays.numel())
+    r32 = rays.to(torch.int32).contiguous()
+    counts = (pre.offsets[1:] - pre.offsets[:-1])[rays]
+    sub_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=sub_off[1:])
+    head_off = torch.arange(n + 1, dtype=torch.int64, device=dev) * HEAD_CAP
+    fa = torch.empty(n, dtype=torch.int32, device=dev)
+    plen = torch.empty(n, dtype=torch.int32, device=dev)
+    cut = torch.empty((2, n), dtype=torch.float64, device=dev)
+    cap_h = max(n * HEAD_CAP, 1)
+    ht = torch.empty(cap_h, dtype=torch.float64, device=dev)
+    hd = torch.empty(cap_h, dtype=torch.float64, device=dev)
+    hi = torch.empty(cap_h, dtype=torch.int32, device=dev)
+    whole = max(int(want), min(int(whole), HEAD_CAP))
+    _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(pre.offsets), _ptr(r32), n,
+                                _ptr(head_off), int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa),
+                                _ptr(cut[0]), _ptr(cut[1]), cap, _ptr(pre._ws), nb, _stream()))
+    sub = QueryPrefix(sub_off, pre.probes[rays], pre.scanned[rays], head_off[:n], plen, ht, hi, hd, cut[0], cut[1],
+                      fa, pre._ws)
+    sub.total = None
+    sub.want, sub.whole = int(want), whole
+    sub._sort_args = None
+    return sub
+
+
 def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix: bool | None = None,
-                max_scratch: int | None = None, want: int = PREFIX_WANT):
+                max_scratch: int | None = None, want: int | None = None):
     """The query of a sampling frame: the heads (``prefix`` True or None;
     returns a :class:`QueryPrefix`) or the full CSR with facts (``prefix``
     False; returns the 7-tuple of :func:`query`)."""

@@ -75,6 +75,7 @@ class FrameResult:
     Q: int = 0
     chunks: int = 1
     flagged: int = 0         # prefix mode: rays re-run through the full query
+    resorted: int = 0        # prefix mode: rays whose heads were re-sorted longer (second chance)
     prefix: bool = False     # the frame ran in prefix mode
     prefix_len: object = None  # TRACK_PREFIX_LEN: device int64[4] (Σ head length, Σ q cut / whole, hit rays)
 
@@ -154,28 +155,53 @@ PREFIX = _PREFIX_ENV != "0"
 
 _PREFIX_LEN: list = []  # head statistics of the passes of the current frame (device tensors)
 TRACK_PREFIX_LEN = False  # bench.py: report the head statistics (a few extra reductions per pass)
+FLAG_REASONS: list = []  # with TRACK_PREFIX_LEN: per pass, counts of flagged rays by reason 1..5
 
 
 def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None):
-    """Sample over the heads of ``pre``; rays whose sampling may reach past
-    their head re-run through the full query (within ``budget`` full-path
-    match slots -- default: from the free memory -- in ray chunks when they
-    need more).  (samples 9-tuple, Q, flagged)"""
+    """Sample over the heads of ``pre``.  Rays whose sampling may reach past
+    their head get a second chance: their heads are re-sorted from the same
+    count pass up to 1024 matches (device.head_resort, no re-scan) and
+    sampled again; the few still flagged re-run through the full query (within
+    ``budget`` full-path match slots -- default: from the free memory -- in
+    ray chunks when they need more).  (samples 9-tuple, Q, rays re-run on the
+    full path, rays re-sorted)"""
     *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
     Q = pre.total
+    if TRACK_PREFIX_LEN:  # flag reasons (hp_sample.cu plan_ray) of this pass
+        FLAG_REASONS.append(torch.bincount(flagged.to(torch.int64), minlength=6)[1:6])
     if TRACK_PREFIX_LEN:  # [Σ head length, Σ q of the cut rays, Σ q of the whole rays, rays with matches]
         q = pre.offsets[1:] - pre.offsets[:-1]
         cut = q > pre.whole
         _PREFIX_LEN.append(torch.stack([pre.length.sum().to(torch.int64), torch.where(cut, q, 0).sum(),
                                         torch.where(cut, 0, q).sum(), (q > 0).sum()]))
-    # the heads and their workspace are no longer needed (sample_prefix copied its outputs)
-    pre.t = pre.ids = pre.dist = pre._ws = None
+    n_full, n_resorted = 0, 0
     if n_flagged:
         sel = torch.nonzero(flagged, as_tuple=True)[0]
-        sub = _full_rays(idx, colors, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], sampler_cfg,
-                         exact_t_end, budget)
-        s = device.merge_flagged(tuple(s), flagged, sub, sel)
-    return tuple(s), Q, n_flagged
+        if pre.want < device.HEAD_CAP:  # second chance: longer heads from the same count pass
+            n_resorted = n_flagged
+            sub_pre = device.head_resort(pre, sel)
+            pre.t = pre.ids = pre.dist = pre._ws = None
+            sl = slopes[sel]
+            *s2, fl2, nf2 = device.sample_prefix(sub_pre, sl, sampler_cfg, colors, exact_t_end)
+            sub_pre.t = sub_pre.ids = sub_pre.dist = sub_pre._ws = None
+            if nf2:
+                sel2 = torch.nonzero(fl2, as_tuple=True)[0]
+                r2 = sel[sel2]
+                sub2 = _full_rays(idx, colors, pixels[r2], dirs[r2], t_near[r2], t_far[r2], slopes[r2], sampler_cfg,
+                                  exact_t_end, budget)
+                s2 = device.merge_flagged(tuple(s2), fl2, sub2, sel2)
+                n_full = nf2
+            s = device.merge_flagged(tuple(s), flagged, tuple(s2), sel)
+        else:
+            pre.t = pre.ids = pre.dist = pre._ws = None
+            sub = _full_rays(idx, colors, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], sampler_cfg,
+                             exact_t_end, budget)
+            s = device.merge_flagged(tuple(s), flagged, sub, sel)
+            n_full = n_flagged
+    # the heads and their workspace are no longer needed (sample_prefix copied its outputs)
+    pre.t = pre.ids = pre.dist = pre._ws = None
+    return tuple(s), Q, n_full, n_resorted
 
 
 def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget):
@@ -217,10 +243,10 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
     before_sample()
     if isinstance(q, device.QueryPrefix):
         _PREFIX_LEN.clear()
-        s, Q, n_flagged = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                                         exact_t_end, max_matches)
+        s, Q, n_flagged, n_res = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
+                                                exact_t_end, max_matches)
         mark("sample")
-        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, prefix=True,
+        return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, resorted=n_res, prefix=True,
                            prefix_len=_PREFIX_LEN.pop() if _PREFIX_LEN else None)
     s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
     mark("sample")
@@ -238,15 +264,16 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
         if b <= a:
             raise device.MatchBudgetExceeded(int(bo[a + 1] - bo[a]), budget)
         cuts.append(min(b, m))
-    parts, Q, nf = [], 0, 0
+    parts, Q, nf, nr = [], 0, 0, 0
     _PREFIX_LEN.clear()
     for a, b in zip(cuts[:-1], cuts[1:]):
         if prefix:
-            s, q_n, f_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
-                                       slopes[a:b], sampler_cfg, exact_t_end, rerun_budget)
+            s, q_n, f_n, r_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
+                                            slopes[a:b], sampler_cfg, exact_t_end, rerun_budget)
             parts.append(s)
             Q += q_n
             nf += f_n
+            nr += r_n
             continue
         q = device.query(idx, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b], slopes[a:b], facts=True)
         parts.append(device.sample(q[0], q[1], q[2], q[3], slopes[a:b], sampler_cfg, colors,
@@ -257,8 +284,8 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
     mark("sample")
     plen = sum(_PREFIX_LEN) if (prefix and _PREFIX_LEN) else None
     _PREFIX_LEN.clear()
-    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf, prefix=prefix,
-                       prefix_len=plen)
+    return FrameResult(idx, None, _concat_samples(parts), Q=Q, chunks=len(parts), flagged=nf, resorted=nr,
+                       prefix=prefix, prefix_len=plen)
 
 
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
