@@ -90,6 +90,13 @@ typedef struct {
     double gamma;
     double eps;
     double tau_min;
+    int32_t emit_knn;    /* 1: also emit each retained sample's K neighbour point
+                            ids and blend weights (hp_sample_emit*: r_knn_id /
+                            r_knn_w [R, k_neighbors]; the K nearest of
+                            _kernels.py:603-620 and the weights of its colour
+                            blend :622-656, w_b = (1/d_b) / sum(1/d); coincident
+                            points 1/nz; -1 / 0 past the pool size) */
+    int32_t reserved;
 } hp_sampler_params;
 
 #define HP_MAX_K 256
@@ -244,8 +251,8 @@ int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const 
                    const hp_sampler_params* p, const double* colors, int64_t n_colors,
                    const int64_t* r_off, int64_t R, int64_t* r_id,
                    double* r_t, double* r_dist, double* r_udf, double* r_alpha, double* r_w,
-                   double* r_color, void* workspace, size_t workspace_bytes,
-                   hp_stream_t stream);
+                   double* r_color, int64_t* r_knn_id, double* r_knn_w, void* workspace,
+                   size_t workspace_bytes, hp_stream_t stream);
 
 /* Prefix mode: the sampler over hp_head_sort's heads (offsets = the full
  * match counts from hp_head_count, query_facts = hp_head_sort's facts,
@@ -271,8 +278,8 @@ int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp_sample_pre
                           int64_t exact_capacity, const double* slopes, const hp_sampler_params* p,
                           const double* colors, int64_t n_colors, const int64_t* r_off, int64_t R,
                           int64_t* r_id, double* r_t, double* r_dist, double* r_udf, double* r_alpha,
-                          double* r_w, double* r_color, void* workspace, size_t workspace_bytes,
-                          hp_stream_t stream);
+                          double* r_w, double* r_color, int64_t* r_knn_id, double* r_knn_w, void* workspace,
+                          size_t workspace_bytes, hp_stream_t stream);
 
 /* ---------------- render (consumer of the samples) ---------------- */
 /* Colour / depth of each ray's pixel from its retained samples (replaces the

@@ -37,7 +37,7 @@ class Layout(ctypes.Structure):
 class SamplerParams(ctypes.Structure):
     _fields_ = [("k_neighbors", c_i32), ("eps_mode", c_i32), ("want_color", c_i32),
                 ("exact_t_end", c_i32), ("beta2", c_f64), ("gamma", c_f64), ("eps", c_f64),
-                ("tau_min", c_f64)]
+                ("tau_min", c_f64), ("emit_knn", c_i32), ("reserved", c_i32)]
 
 
 class SamplePrefix(ctypes.Structure):
@@ -84,13 +84,13 @@ _SIGNATURES = {
                                      c_p, c_size, c_p]),
     "hp_sample_emit": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_i64, c_i64, c_p,
                                       ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_i64,
-                                      c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
+                                      c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
     "hp_sample_run_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(SamplePrefix), c_i64, c_p, c_p,
                                             ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_p, c_p, c_p,
                                             c_size, c_p]),
     "hp_sample_emit_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(SamplePrefix), c_i64, c_p,
                                              ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_i64,
-                                             c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
+                                             c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
     "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "hp_sample_debug_counters": (ctypes.c_int, [c_p, ctypes.c_int]),

@@ -81,18 +81,20 @@ HP_HD RayF ray_f(const RayParams& r) { return RayF{r.f0, r.f1, r.f2, r.ftn, r.ft
 // pair |t - t64| <= eps (the band covers the t error bound with a wide
 // margin), so t - eps rounded down is a lower bound of the exact t.
 HP_HD int cone_filter_te(const float4 P, const RayF& r, float& t, float& eps) {
+    // every term computed, the decision by selects (no early exits: the warp
+    // runs all paths anyway, and branch-free code schedules better)
     eps = fmaf(P.w, r.smax, r.eps_ray);
     t = fmaf(P.z, r.f2, fmaf(P.y, r.f1, P.x * r.f0));
-    if (t < r.ftn - eps || t > r.ftf + eps) return 0;
+    const bool t_out = t < r.ftn - eps || t > r.ftf + eps;
     const float ex = fmaf(-t, r.f0, P.x), ey = fmaf(-t, r.f1, P.y), ez = fmaf(-t, r.f2, P.z);
     const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
     const float rr = t * r.fslope;
     const float hi = rr + eps;
-    if (d2 > hi * hi * (1.0f + 0x1p-20f)) return 0;
+    const bool d_out = d2 > hi * hi * (1.0f + 0x1p-20f);
     const float lo = rr - eps;
     const bool t_in = (t >= r.ftn + eps) && (t <= r.ftf - eps);
-    if (t_in && lo > 0.0f && d2 < lo * lo * (1.0f - 0x1p-20f)) return 1;
-    return 2;
+    const bool sure = t_in && lo > 0.0f && d2 < lo * lo * (1.0f - 0x1p-20f);
+    return (t_out || d_out) ? 0 : (sure ? 1 : 2);
 }
 HP_HD int cone_filter(const float4 P, const RayF& r) {
     float t, eps;

@@ -95,7 +95,7 @@ __device__ void group_setup(GroupHead& S, const Rays& R, const QCam& QC, int64_t
 // Order-preserving uint32 key of a float (and back).
 __device__ __forceinline__ unsigned fkey(float x) {
     const unsigned u = __float_as_uint(x);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return u ^ (unsigned(int(u) >> 31) | 0x80000000u);  // negative: all bits flipped; else the sign bit
 }
 __device__ __forceinline__ float from_fkey(unsigned k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);

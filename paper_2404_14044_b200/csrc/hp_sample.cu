@@ -102,6 +102,8 @@ struct Csr {
 struct Outputs {
     int64_t* r_id;
     double *r_t, *r_dist, *r_udf, *r_alpha, *r_w, *r_color;
+    int64_t* r_knn_id;  // [R, K] with P.emit_knn
+    double* r_knn_w;
 };
 
 struct RayOut {  // per-ray results of pass 1
@@ -291,7 +293,9 @@ struct Exact {
     double* udf;
     double* alpha;
     double* w;
-    double* col;  // [n, 3]
+    double* col;      // [n, 3]
+    int64_t* knn_id;  // [n, K] with P.emit_knn
+    double* knn_w;
     int* ray;
     int64_t cap;
 };
@@ -316,10 +320,12 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
         if (C.start) {
             const int qt = C.qtrue(ray);
             ok = eval_exact<BestT>(V, q, qt, q < qt ? __ldg(C.cut_t + ray) : CUDART_INF, j, pl.z & 1, pl.x,
-                                   C.slopes[ray], P, C.ids32 + lo, C.colors, u, a, col, evals);
+                                   C.slopes[ray], P, C.ids32 + lo, C.colors, u, a, col, evals,
+                                   P.emit_knn ? X.knn_id + c * P.K : nullptr, P.emit_knn ? X.knn_w + c * P.K : nullptr);
         } else {
             eval_exact<BestT>(V, q, q, CUDART_INF, j, pl.z & 1, pl.x, C.slopes[ray], P, C.ids + lo, C.colors, u, a,
-                              col, evals);
+                              col, evals, P.emit_knn ? X.knn_id + c * P.K : nullptr,
+                              P.emit_knn ? X.knn_w + c * P.K : nullptr);
         }
         if (!ok) C.flag[ray] = 5;
         X.udf[c] = u;
@@ -406,6 +412,26 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
                     for (int x = 0; x < 3; x++) X.col[3 * dst + x] = c[x];
             }
             __syncwarp();
+            if (P.emit_knn) {  // the neighbour rows, 8 columns at a time (every read before any write)
+                for (int b0 = 0; b0 < P.K; b0 += 8) {
+                    int64_t kid[8];
+                    double kw[8];
+#pragma unroll
+                    for (int b = 0; b < 8; b++)
+                        if (mine && b0 + b < P.K) {
+                            kid[b] = X.knn_id[(e0 + j) * P.K + b0 + b];
+                            kw[b] = X.knn_w[(e0 + j) * P.K + b0 + b];
+                        }
+                    __syncwarp();
+#pragma unroll
+                    for (int b = 0; b < 8; b++)
+                        if (mine && b0 + b < P.K) {
+                            X.knn_id[dst * P.K + b0 + b] = kid[b];
+                            X.knn_w[dst * P.K + b0 + b] = kw[b];
+                        }
+                    __syncwarp();
+                }
+            }
         }
         nret += __popc(keep);
         if (stop) break;
@@ -454,6 +480,11 @@ __global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const
                 O.r_color[3 * (o + k) + 1] = X.col[3 * (st + k) + 1];
                 O.r_color[3 * (o + k) + 2] = X.col[3 * (st + k) + 2];
             }
+            if (P.emit_knn)
+                for (int b = 0; b < P.K; b++) {
+                    O.r_knn_id[(o + k) * P.K + b] = X.knn_id[(st + k) * P.K + b];
+                    O.r_knn_w[(o + k) * P.K + b] = X.knn_w[(st + k) * P.K + b];
+                }
         }
     }
 }
@@ -489,7 +520,7 @@ struct SampleWs {
     void* scan;
 };
 
-SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color) {
+SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color, int knn_k = 0) {
     SampleWs w;
     w.plan = c.take<int4>(m > 0 ? m : 1);
     w.eoff = c.take<int64_t>(m + 1);
@@ -499,6 +530,8 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color) {
     w.x.alpha = c.take<double>(xc);
     w.x.w = c.take<double>(xc);
     w.x.col = color ? c.take<double>(3 * xc) : nullptr;
+    w.x.knn_id = knn_k > 0 ? c.take<int64_t>(xc * knn_k) : nullptr;
+    w.x.knn_w = knn_k > 0 ? c.take<double>(xc * knn_k) : nullptr;
     w.x.ray = c.take<int>(xc);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     return w;
@@ -510,6 +543,7 @@ Params to_params(const hp_sampler_params* p) {
     P.eps_mode = p->eps_mode;
     P.want_color = p->want_color;
     P.exact_t_end = p->exact_t_end;
+    P.emit_knn = p->emit_knn;
     P.beta2 = p->beta2;
     P.gamma = p->gamma;
     P.eps = p->eps;
@@ -580,7 +614,7 @@ using namespace hp;
 extern "C" int hp_sample_workspace_bytes(int64_t m, int64_t total, int64_t exact_capacity,
                                          const hp_sampler_params* p, size_t* bytes) {
     Carver c(nullptr, 0);
-    carve_sample(c, m, exact_capacity, p && p->want_color);
+    carve_sample(c, m, exact_capacity, p && p->want_color, p && p->emit_knn ? p->k_neighbors : 0);
     *bytes = c.used + 256;
     (void)total;
     return HP_OK;
@@ -594,7 +628,7 @@ extern "C" int hp_sample_run(const int64_t* offsets, int64_t m, const int64_t* i
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color, p->emit_knn ? p->k_neighbors : 0);
     if (!c.ok()) {
         set_error("hp_sample_run: workspace too small");
         return HP_ESPACE;
@@ -627,7 +661,7 @@ extern "C" int hp_sample_run_prefix(const int64_t* offsets, int64_t m, const hp_
         return HP_EINVAL;
     }
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color, p->emit_knn ? p->k_neighbors : 0);
     if (!c.ok()) {
         set_error("hp_sample_run_prefix: workspace too small");
         return HP_ESPACE;
@@ -654,8 +688,8 @@ extern "C" int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp
                                      int64_t exact_capacity, const double* slopes, const hp_sampler_params* p,
                                      const double* colors, int64_t n_colors, const int64_t* r_off, int64_t R,
                                      int64_t* r_id, double* r_t, double* r_dist, double* r_udf, double* r_alpha,
-                                     double* r_w, double* r_color, void* workspace, size_t workspace_bytes,
-                                     hp_stream_t stream) {
+                                     double* r_w, double* r_color, int64_t* r_knn_id, double* r_knn_w,
+                                     void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     if (!pre) {
         set_error("hp_sample_emit_prefix: prefix is NULL");
@@ -663,7 +697,7 @@ extern "C" int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp
     }
     if (R == 0 || m == 0) return HP_OK;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color, p->emit_knn ? p->k_neighbors : 0);
     if (!c.ok()) {
         set_error("hp_sample_emit_prefix: workspace too small");
         return HP_ESPACE;
@@ -672,7 +706,11 @@ extern "C" int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp
     Csr C{offsets, nullptr, pre->t, pre->dist, slopes, colors, m, nullptr,
           pre->start, pre->length, pre->ids, pre->cut_t, pre->cut_d, nullptr};
     Params P = to_params(p);
-    Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
+    Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color, r_knn_id, r_knn_w};
+    if (P.emit_knn && (!r_knn_id || !r_knn_w)) {
+        set_error("emit_knn set but r_knn_id / r_knn_w is NULL");
+        return HP_EINVAL;
+    }
     TimedSpan ts("k_emit", s);
     k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
     HP_CHECK_LAUNCH("k_emit");
@@ -684,12 +722,13 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
                               const double* slopes, const hp_sampler_params* p, const double* colors,
                               int64_t n_colors, const int64_t* r_off, int64_t R, int64_t* r_id, double* r_t,
                               double* r_dist, double* r_udf, double* r_alpha, double* r_w, double* r_color,
-                              void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+                              int64_t* r_knn_id, double* r_knn_w, void* workspace, size_t workspace_bytes,
+                              hp_stream_t stream) {
     HP_TRY(validate(p, colors, n_colors));
     (void)total;
     if (R == 0 || m == 0) return HP_OK;
     Carver c(workspace, workspace_bytes);
-    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color);
+    SampleWs w = carve_sample(c, m, exact_capacity, p->want_color, p->emit_knn ? p->k_neighbors : 0);
     if (!c.ok()) {
         set_error("hp_sample_emit: workspace too small");
         return HP_ESPACE;
@@ -697,7 +736,11 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Csr C{offsets, ids, t, dist, slopes, colors, m, nullptr};
     Params P = to_params(p);
-    Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color};
+    Outputs O{r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color, r_knn_id, r_knn_w};
+    if (P.emit_knn && (!r_knn_id || !r_knn_w)) {
+        set_error("emit_knn set but r_knn_id / r_knn_w is NULL");
+        return HP_EINVAL;
+    }
     TimedSpan ts("k_emit", s);
     k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
     HP_CHECK_LAUNCH("k_emit");

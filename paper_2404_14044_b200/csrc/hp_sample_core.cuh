@@ -16,7 +16,7 @@ namespace {
 
 struct Params {
     int K;
-    int eps_mode, want_color, exact_t_end;
+    int eps_mode, want_color, exact_t_end, emit_knn;
     double beta2, gamma, eps, tau_min;
     double inv_beta2_up;  // 1 / beta2 rounded up (bound factors only)
 };
@@ -152,7 +152,7 @@ template <class BestT, class View, class IdT>
 __device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, bool fast,
                            int jstar, double slope, const Params& P, const IdT* __restrict__ ids_ray,
                            const double* __restrict__ colors, double& udf, double& alpha, double* col3,
-                           unsigned long long& evals) {
+                           unsigned long long& evals, int64_t* knn_id = nullptr, double* knn_w = nullptr) {
     const double tj = V.t(j);
     const double rj = dmul(slope, tj);
     const bool partial = q < qt;
@@ -253,6 +253,23 @@ __device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, boo
     best.for_each(ksel, [&](double d2, int) { acc = dadd(acc, sqrt(d2)); });
     udf = __ddiv_rn(acc, double(ksel));
     alpha = dmul(P.gamma, exp(__ddiv_rn(-dmul(udf, udf), P.beta2)));
+    if (knn_id) {  // the K nearest's point ids and blend weights (the colour blend's)
+        int nz = 0;
+        double wsum = 0.0;
+        best.for_each(ksel, [&](double d2, int) { nz += (d2 == 0.0); });
+        if (nz == 0) best.for_each(ksel, [&](double d2, int) { wsum = dadd(wsum, __ddiv_rn(1.0, sqrt(d2))); });
+        int b = 0;
+        best.for_each(ksel, [&](double d2, int i) {
+            knn_id[b] = int64_t(ids_ray[i]);
+            knn_w[b] = nz > 0 ? (d2 == 0.0 ? __ddiv_rn(1.0, double(nz)) : 0.0)
+                              : __ddiv_rn(__ddiv_rn(1.0, sqrt(d2)), wsum);
+            b++;
+        });
+        for (; b < P.K; b++) {
+            knn_id[b] = -1;
+            knn_w[b] = 0.0;
+        }
+    }
     if (P.want_color) {
         int nz = 0;
         best.for_each(ksel, [&](double d2, int) { nz += (d2 == 0.0); });

@@ -424,7 +424,7 @@ def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix:
                  want)
 
 
-def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerParams:
+def sampler_params(cfg, want_color: bool, exact_t_end: bool, emit_knn: bool = False) -> _lib.SamplerParams:
     """C parameter block from a SamplerConfig; a ready _lib.SamplerParams
     (the reference operator's raw arguments, e.g. beta2 given directly) is
     taken as is, with want_color / exact_t_end applied."""
@@ -433,8 +433,10 @@ def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerPara
         ctypes.pointer(p)[0] = cfg
         p.want_color = 1 if want_color else 0
         p.exact_t_end = 1 if exact_t_end else 0
+        p.emit_knn = 1 if emit_knn else 0
         return p
     p = _lib.SamplerParams()
+    p.emit_knn = 1 if emit_knn else 0
     p.k_neighbors = int(cfg.k_neighbors)
     p.eps_mode = 1 if cfg.retention_mode == "epsilon" else 0
     p.want_color = 1 if want_color else 0
@@ -448,7 +450,7 @@ def sampler_params(cfg, want_color: bool, exact_t_end: bool) -> _lib.SamplerPara
 
 def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torch.Tensor,
            slopes: torch.Tensor, cfg, colors: torch.Tensor | None = None,
-           exact_t_end: bool = True, facts: torch.Tensor | None = None):
+           exact_t_end: bool = True, facts: torch.Tensor | None = None, emit_knn: bool = False):
     """_kernels.sample_batch on the device (reference _kernels.py:552-700).
 
     Returns (r_off, r_id, r_t, r_dist, r_udf, r_alpha, r_w, r_color, t_end).
@@ -456,14 +458,17 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     the transmittance at that point instead of over all candidates.
     ``facts``: the per-ray facts :func:`query` returned with this very CSR and
     these slopes (lets the sampler skip its full precondition pass); results
-    are identical with or without them.
+    are identical with or without them.  ``emit_knn``: two more outputs, the
+    retained samples' K neighbour point ids (int64 [R, K], -1 past the pool)
+    and blend weights (float64 [R, K]) -- north_star stage 4's per-sample
+    candidate indices and weights (the K nearest of _kernels.py:603-620).
     """
     lib = _lib.load(require_device=True)
     dev = offsets.device
     m = int(offsets.shape[0]) - 1
     total = int(ids.numel())
     want = colors is not None
-    p = sampler_params(cfg, want, exact_t_end)
+    p = sampler_params(cfg, want, exact_t_end, emit_knn)
     exact_cap = max(SAMPLE_EXACT_PER_RAY * m, 1 << 16)
     r_off = torch.empty(m + 1, dtype=torch.int64, device=dev)
     t_end = torch.empty(max(m, 0), dtype=torch.float64, device=dev)
@@ -489,16 +494,28 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
     r_id = torch.empty(R, **i64)
     outs = [torch.empty(R, **f64) for _ in range(5)]
     r_color = torch.empty((R, 3), **f64) if want else torch.zeros((0, 3), **f64)
+    knn = _knn_outputs(R, p, dev)
     _mark("sample.sync")
     _lib.check(lib.hp_sample_emit(*common, _ptr(r_off), R, _ptr(r_id), *[_ptr(o) for o in outs],
-                                  _ptr(r_color) if want else ctypes.c_void_p(0), _ptr(ws),
+                                  _ptr(r_color) if want else ctypes.c_void_p(0), *_knn_ptrs(knn), _ptr(ws),
                                   nb.value, _stream()))
     _mark("sample.emit")
-    return (r_off, r_id, *outs, r_color, t_end)
+    return (r_off, r_id, *outs, r_color, t_end, *knn)
+
+
+def _knn_ptrs(knn):
+    return [_ptr(x) for x in knn] if knn else [ctypes.c_void_p(0), ctypes.c_void_p(0)]
+
+
+def _knn_outputs(R, p, dev):
+    if not p.emit_knn:
+        return ()
+    return (torch.empty((R, p.k_neighbors), dtype=torch.int64, device=dev),
+            torch.empty((R, p.k_neighbors), dtype=torch.float64, device=dev))
 
 
 def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Tensor | None = None,
-                  exact_t_end: bool = False):
+                  exact_t_end: bool = False, emit_knn: bool = False):
     """:func:`sample` over :func:`query_prefix`'s prefixes
     (hp_sample_run_prefix / hp_sample_emit_prefix).
 
@@ -512,7 +529,7 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
     dev = pre.offsets.device
     m = int(pre.offsets.shape[0]) - 1
     want = colors is not None
-    p = sampler_params(cfg, want, exact_t_end)
+    p = sampler_params(cfg, want, exact_t_end, emit_knn)
     exact_cap = max(SAMPLE_EXACT_PER_RAY * m, 1 << 16)
     r_off = torch.empty(m + 1, dtype=torch.int64, device=dev)
     t_end = torch.empty(max(m, 0), dtype=torch.float64, device=dev)
@@ -539,21 +556,22 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
     r_id = torch.empty(R, **i64)
     outs = [torch.empty(R, **f64) for _ in range(5)]
     r_color = torch.empty((R, 3), **f64) if want else torch.zeros((0, 3), **f64)
+    knn = _knn_outputs(R, p, dev)
     _lib.check(lib.hp_sample_emit_prefix(_ptr(pre.offsets), m, ctypes.byref(sp), exact_cap, _ptr(slopes),
                                          ctypes.byref(p), colp, ncol, _ptr(r_off), R, _ptr(r_id),
                                          *[_ptr(o) for o in outs], _ptr(r_color) if want else ctypes.c_void_p(0),
-                                         _ptr(ws), nb.value, _stream()))
+                                         *_knn_ptrs(knn), _ptr(ws), nb.value, _stream()))
     _mark("sample.emit")
-    return (r_off, r_id, *outs, r_color, t_end, flagged[:m], n_flagged)
+    return (r_off, r_id, *outs, r_color, t_end, *knn, flagged[:m], n_flagged)
 
 
 def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = None):
     """Splice the full-path samples ``sub`` of the flagged rays into the
     prefix-mode samples ``main`` (both (r_off, r_id, r_t, r_dist, r_udf,
-    r_alpha, r_w, r_color, t_end)); flagged rays hold no candidates in main.
-    ``sel``: the flagged ray indices if the caller has them already."""
-    r_off, *rows, r_color, t_end = main
-    s_off, *s_rows, s_color, s_tend = sub
+    r_alpha, r_w, r_color, t_end[, r_knn_id, r_knn_w])); flagged rays hold no
+    candidates in main.  ``sel``: the flagged ray indices if the caller has
+    them already."""
+    r_off, s_off = main[0], sub[0]
     dev = r_off.device
     m = int(r_off.shape[0]) - 1
     if sel is None:
@@ -562,7 +580,7 @@ def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = N
     counts[sel] = s_off[1:] - s_off[:-1]
     off = torch.zeros(m + 1, dtype=torch.int64, device=dev)
     torch.cumsum(counts, 0, out=off[1:])
-    R_main, R_sub = int(rows[0].shape[0]), int(s_rows[0].shape[0])  # host values: no synchronisation
+    R_main, R_sub = int(main[1].shape[0]), int(sub[1].shape[0])  # host values: no synchronisation
     R = R_main + R_sub  # flagged rays hold nothing in main
 
     def dst(src_off, rays, k):  # destination row of every source row
@@ -573,10 +591,15 @@ def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = N
 
     d_main = dst(r_off, torch.arange(m, device=dev), R_main)
     d_sub = dst(s_off, sel, R_sub)
-    out = []
-    colored = r_color.shape[0] == rows[0].shape[0] and s_color.shape[0] == s_rows[0].shape[0]
-    for a, b in zip(rows + [r_color], s_rows + [s_color]):
-        if a.dim() == 2 and not colored:
+    out = [off]
+    for k in range(1, len(main)):
+        a, b = main[k], sub[k]
+        if k == 8:  # t_end: per ray
+            te = a.clone()
+            te[sel] = b
+            out.append(te)
+            continue
+        if k == 7 and not (a.shape[0] == R_main and b.shape[0] == R_sub):  # no colours
             out.append(torch.zeros((0, 3), dtype=a.dtype, device=dev))
             continue
         o = torch.empty((R,) + tuple(a.shape[1:]), dtype=a.dtype, device=dev)
@@ -585,9 +608,7 @@ def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = N
         if b.shape[0]:
             o[d_sub] = b
         out.append(o)
-    te = t_end.clone()
-    te[sel] = s_tend
-    return (off, *out[:-1], out[-1], te)
+    return tuple(out)
 
 
 def ray_grid(camera, dev=None, row0: int = 0, rows: int | None = None, t_near: float | None = None,

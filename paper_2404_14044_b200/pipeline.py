@@ -121,7 +121,7 @@ def _concat_samples(parts):
         offs.append(p[0][1:] + base)
         base += int(p[1].numel())
     out = [torch.cat(offs)]
-    for k in range(1, 9):
+    for k in range(1, len(parts[0])):
         out.append(torch.cat([p[k] for p in parts]))
     return tuple(out)
 
@@ -129,7 +129,7 @@ def _concat_samples(parts):
 def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_cfg, pixels,
                  dirs, t_near, t_far, slopes, sampler_cfg: SamplerConfig | None = None,
                  exact_t_end: bool = True, timer: StageTimer | None = None,
-                 max_matches: int | None = None) -> FrameResult:
+                 max_matches: int | None = None, emit_knn: bool = False) -> FrameResult:
     """build -> query -> sample, all on the device (CUDA tensors in and out).
 
     A frame whose query would need more than ``max_matches`` match slots
@@ -142,7 +142,7 @@ def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_
     idx = device.build(xyz, camera, search_cfg.pad)
     mark("build")
     return _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg or SamplerConfig(),
-                         exact_t_end, max_matches, mark)
+                         exact_t_end, max_matches, mark, emit_knn=emit_knn)
 
 
 # Frames that only want samples keep 8 bytes per match and sort each ray's
@@ -158,7 +158,8 @@ TRACK_PREFIX_LEN = False  # bench.py: report the head statistics (a few extra re
 FLAG_REASONS: list = []  # with TRACK_PREFIX_LEN: per pass, counts of flagged rays by reason 1..5
 
 
-def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None):
+def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None,
+                   emit_knn=False):
     """Sample over the heads of ``pre``.  Rays whose sampling may reach past
     their head get a second chance: their heads are re-sorted from the same
     count pass up to 1024 matches (device.head_resort, no re-scan) and
@@ -166,7 +167,7 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     ``budget`` full-path match slots -- default: from the free memory -- in
     ray chunks when they need more).  (samples 9-tuple, Q, rays re-run on the
     full path, rays re-sorted)"""
-    *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end)
+    *s, flagged, n_flagged = device.sample_prefix(pre, slopes, sampler_cfg, colors, exact_t_end, emit_knn)
     Q = pre.total
     if TRACK_PREFIX_LEN:  # flag reasons (hp_sample.cu plan_ray) of this pass
         FLAG_REASONS.append(torch.bincount(flagged.to(torch.int64), minlength=6)[1:6])
@@ -183,20 +184,20 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
             sub_pre = device.head_resort(pre, sel)
             pre.t = pre.ids = pre.dist = pre._ws = None
             sl = slopes[sel]
-            *s2, fl2, nf2 = device.sample_prefix(sub_pre, sl, sampler_cfg, colors, exact_t_end)
+            *s2, fl2, nf2 = device.sample_prefix(sub_pre, sl, sampler_cfg, colors, exact_t_end, emit_knn)
             sub_pre.t = sub_pre.ids = sub_pre.dist = sub_pre._ws = None
             if nf2:
                 sel2 = torch.nonzero(fl2, as_tuple=True)[0]
                 r2 = sel[sel2]
                 sub2 = _full_rays(idx, colors, pixels[r2], dirs[r2], t_near[r2], t_far[r2], slopes[r2], sampler_cfg,
-                                  exact_t_end, budget)
+                                  exact_t_end, budget, emit_knn)
                 s2 = device.merge_flagged(tuple(s2), fl2, sub2, sel2)
                 n_full = nf2
             s = device.merge_flagged(tuple(s), flagged, tuple(s2), sel)
         else:
             pre.t = pre.ids = pre.dist = pre._ws = None
             sub = _full_rays(idx, colors, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], sampler_cfg,
-                             exact_t_end, budget)
+                             exact_t_end, budget, emit_knn)
             s = device.merge_flagged(tuple(s), flagged, sub, sel)
             n_full = n_flagged
     # the heads and their workspace are no longer needed (sample_prefix copied its outputs)
@@ -204,7 +205,7 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     return tuple(s), Q, n_full, n_resorted
 
 
-def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget):
+def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget, emit_knn=False):
     """Full-CSR query + sample of a set of rays, in ray chunks of at most
     ``budget`` match slots."""
     if budget is None:
@@ -213,19 +214,23 @@ def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, ex
         q = device.query(idx, pixels, dirs, t_near, t_far, slopes, facts=True, max_scratch=budget)
     except device.MatchBudgetExceeded:
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget,
-                              lambda name: None, prefix=False).samples
-    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
+                              lambda name: None, prefix=False, emit_knn=emit_knn).samples
+    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6],
+                      emit_knn=emit_knn)
     del q
     return s
 
 
-def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None):
+def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None,
+                 emit_knn=False):
     pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes)
-    return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget)
+    return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget,
+                          emit_knn)
 
 
 def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
-                  mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None) -> FrameResult:
+                  mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None,
+                  emit_knn: bool = False) -> FrameResult:
     """query -> sample of one frame on the device.  ``prefix``: True (heads)
     / False (full CSR); None: the HP_PREFIX setting."""
     prefix = PREFIX if prefix is None else prefix
@@ -238,23 +243,24 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
         # such frames are dominated by long rays)
         before_sample()
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                              exact_t_end, budget, mark, prefix is not False, max_matches)
+                              exact_t_end, budget, mark, prefix is not False, max_matches, emit_knn)
     mark("query")
     before_sample()
     if isinstance(q, device.QueryPrefix):
         _PREFIX_LEN.clear()
         s, Q, n_flagged, n_res = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
-                                                exact_t_end, max_matches)
+                                                exact_t_end, max_matches, emit_knn)
         mark("sample")
         return FrameResult(idx, None, s, Q=Q, flagged=n_flagged, resorted=n_res, prefix=True,
                            prefix_len=_PREFIX_LEN.pop() if _PREFIX_LEN else None)
-    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6])
+    s = device.sample(q[0], q[1], q[2], q[3], slopes, sampler_cfg, colors, exact_t_end, facts=q[6],
+                      emit_knn=emit_knn)
     mark("sample")
     return FrameResult(idx, q[:6], s, Q=int(q[1].numel()))
 
 
 def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end,
-                   budget, mark, prefix=False, rerun_budget=None):
+                   budget, mark, prefix=False, rerun_budget=None, emit_knn=False):
     bo = device.query_bounds(idx, pixels, dirs, t_near, t_far, slopes).cpu().numpy()
     m = bo.shape[0] - 1
     cuts = [0]
@@ -269,7 +275,7 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
     for a, b in zip(cuts[:-1], cuts[1:]):
         if prefix:
             s, q_n, f_n, r_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
-                                            slopes[a:b], sampler_cfg, exact_t_end, rerun_budget)
+                                            slopes[a:b], sampler_cfg, exact_t_end, rerun_budget, emit_knn)
             parts.append(s)
             Q += q_n
             nf += f_n
@@ -277,7 +283,7 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
             continue
         q = device.query(idx, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b], slopes[a:b], facts=True)
         parts.append(device.sample(q[0], q[1], q[2], q[3], slopes[a:b], sampler_cfg, colors,
-                                   exact_t_end, facts=q[6]))
+                                   exact_t_end, facts=q[6], emit_knn=emit_knn))
         Q += int(q[1].numel())
         del q
     mark("query")
