@@ -29,6 +29,8 @@
  *   hp_primary_surface  derived: first retained candidate per ray
  *   hp_ray_grid         geometry.ray_grid            geometry.py:289-306
  *   hp_render           renderer.render_volume / render_knp renderer.py:138-185
+ *   hp_pointnerf_*      (no reference symbol) the Point-NeRF aggregation MLP the
+ *                       paper integrates with, cfg5
  */
 #ifndef HASHPOINT_B200_H
 #define HASHPOINT_B200_H
@@ -280,6 +282,26 @@ int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp_sample_pre
                           int64_t* r_id, double* r_t, double* r_dist, double* r_udf, double* r_alpha,
                           double* r_w, double* r_color, int64_t* r_knn_id, double* r_knn_w, void* workspace,
                           size_t workspace_bytes, hp_stream_t stream);
+
+/* ---------------- Point-NeRF aggregation MLP (cfg5; bf16 on tcgen05) ----------------
+ * The consumer of emit_knn.  No
+ * reference implementation: parity vs an fp32 PyTorch
+ * restatement (pointnerf.py).  hp_pointnerf_aggregate: per retained sample s
+ * (R of them, k neighbours each, k a power of two <= 32), input rows
+ * [feature (32 bf16) | sin/cos(2^l pi (p_i - x_s)), l < 4 | p_i - x_s | 1 | 0...]
+ * (64), h1 = relu(W1 in), h2 = relu(W2 h1 + b2), g_s = sum_k w_sk h2 ->
+ * g_out bf16 [R,128].  x_s = origin + r_t[s] * dirs[sample_ray[s]].
+ * features: bf16 [n,32]; w1 bf16 [128,64]; w2 bf16 [128,128]; b2 f32 [128].
+ * hp_pointnerf_head: out f32 [R,4] = (softplus, sigmoid x3) of
+ * W4 relu(W3 g + b3) + b4; w3 bf16 [64,128], b3 f32 [64], w4 f32 [4,64],
+ * b4 f32 [4].  Device pointers except origin_host (host double[3]). */
+int hp_pointnerf_aggregate(const int64_t* knn_id, const double* knn_w, int64_t R, int32_t k,
+                           const int32_t* sample_ray, const double* r_t, const double* dirs,
+                           const double* origin_host, const double* positions, const uint16_t* features,
+                           const uint16_t* w1, const uint16_t* w2, const float* b2, uint16_t* g_out,
+                           hp_stream_t stream);
+int hp_pointnerf_head(const uint16_t* g, int64_t R, const uint16_t* w3, const float* b3, const float* w4,
+                      const float* b4, float* out, hp_stream_t stream);
 
 /* ---------------- render (consumer of the samples) ---------------- */
 /* Colour / depth of each ray's pixel from its retained samples (replaces the

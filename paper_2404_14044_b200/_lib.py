@@ -91,6 +91,9 @@ _SIGNATURES = {
     "hp_sample_emit_prefix": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(SamplePrefix), c_i64, c_p,
                                              ctypes.POINTER(SamplerParams), c_p, c_i64, c_p, c_i64,
                                              c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_size, c_p]),
+    "hp_pointnerf_aggregate": (ctypes.c_int, [c_p, c_p, c_i64, ctypes.c_int32, c_p, c_p, c_p,
+                                              ctypes.POINTER(c_f64), c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "hp_pointnerf_head": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p]),
     "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "hp_sample_debug_counters": (ctypes.c_int, [c_p, ctypes.c_int]),

@@ -1,0 +1,426 @@
+// hp_mlp.cu — Point-NeRF-style feature aggregation MLP on the 5th-generation
+// tensor cores (tcgen05 + TMEM), the consumer of the sampler's K neighbours
+// (the paper's integration PAPER.md:256-259, the
+// Point-NeRF aggregation it plugs into).  No reference implementation exists
+// (SPEC.md:15): parity is against an fp32 PyTorch restatement
+// (paper_2404_14044_b200/pointnerf.py, tests/test_pointnerf_gpu.py).
+//
+// Per retained sample s with neighbours i = knn_id[s, k] and blend weights
+// w_{s,k} (hp_sample_emit, emit_knn):
+//   x_s  = origin + t_s * dir(ray of s)
+//   in   = [ f_i (32) | sin, cos(2^l pi (p_i - x_s)), l < 4 (24) | p_i - x_s (3) | 1 | 0 x 4 ]  (64, bf16)
+//   h1   = relu(W1 in)                 W1: 128 x 64    (bias folded: the constant-1 input)
+//   h2   = relu(W2 h1 + b2)            W2: 128 x 128
+//   g_s  = sum_k w_{s,k} h2            (128, fp32 -> bf16)
+//   o    = W4 relu(W3 g_s + b3) + b4   W3: 64 x 128, W4: 4 x 64
+//   sigma = softplus(o_0), rgb = sigmoid(o_1..3)
+//
+// k_agg (per 128-row tile = 128 / K samples x K neighbours): every thread
+// builds one row of `in` straight into shared memory in the UMMA canonical
+// K-major layout (8-row x 16-byte core matrices, no swizzle); one thread
+// issues the tcgen05.mma chains (M = 128, N = 128, K = 16 per instruction)
+// into a TMEM accumulator (256 of the SM's 512 columns: layer 1 in [0, 128),
+// layer 2 in [128, 256)); completion is committed to an mbarrier; the four
+// warps read their 32 TMEM lanes back with tcgen05.ld (32x32b), apply
+// ReLU / bias, and either feed the next MMA through shared memory (h1, bf16)
+// or reduce the K rows of each sample with warp shuffles (g).  k_head: the
+// same pattern over 128 samples (M = 128, N = 64, K = 128), then the 64 -> 4
+// layer and the activations on the CUDA cores.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "hp_common.cuh"
+
+namespace hp {
+namespace {
+
+constexpr int kFeat = 32;     // point feature width
+constexpr int kIn = 64;       // layer-1 input width
+constexpr int kHid = 128;     // per-neighbour hidden width
+constexpr int kHead = 64;     // head hidden width
+constexpr int kTile = 128;    // rows per MMA tile (UMMA M)
+constexpr int kThreadsMlp = 128;
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n HP_MLP_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra HP_MLP_WAIT_%=;\n}\n" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// make this thread's generic-proxy shared-memory writes visible to the async
+// proxy (the tensor core reads operands through it)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc(unsigned* dst_smem) {  // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(dst_smem)),
+                 "r"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_dealloc(unsigned taddr) {  // whole warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(kCols) : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8
+// rows x 16 bytes; lbo = byte distance between the two 16-byte K halves of
+// one K = 16 step, sbo = byte distance between consecutive 8-row groups.
+__device__ __forceinline__ uint64_t smem_desc(const void* p, unsigned lbo, unsigned sbo) {
+    const uint64_t a = su32(p);
+    return ((a >> 4) & 0x3FFFull) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
+           (1ull << 46);  // descriptor version 1 (sm_100); base offset 0; layout SWIZZLE_NONE
+}
+// instruction descriptor: kind::f16 with bf16 A / B, fp32 D, both K-major
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(unsigned d_tmem, uint64_t a, uint64_t b, uint32_t idesc, bool accum) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum ? 1 : 0)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
+                 : "memory");
+}
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, float* v) {
+    unsigned r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of element (row, k) (k a multiple of 8) in a K-major canonical
+// tile with `kb` 16-byte k-blocks per 8-row group: sbo = kb * 128, lbo = 128
+__device__ __forceinline__ unsigned core_off(int row, int k, int kb) {
+    return unsigned((row >> 3) * kb * 128 + (k >> 3) * 128 + (row & 7) * 16);
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 8 floats -> one 16-byte chunk of bf16 at byte offset `off` of `base`
+__device__ __forceinline__ void st_chunk(unsigned char* base, unsigned off, const float* x) {
+    *reinterpret_cast<uint4*>(base + off) =
+        make_uint4(pack2(x[0], x[1]), pack2(x[2], x[3]), pack2(x[4], x[5]), pack2(x[6], x[7]));
+}
+
+// weights [rows x cols] bf16 row-major (K-major) -> canonical tile in smem
+__device__ void load_weights(unsigned char* dst, const uint16_t* __restrict__ w, int rows, int cols) {
+    const int kb = cols / 8;
+    for (int c = threadIdx.x; c < rows * kb; c += blockDim.x) {
+        const int row = c / kb, k = (c % kb) * 8;
+        *reinterpret_cast<uint4*>(dst + core_off(row, k, kb)) =
+            *reinterpret_cast<const uint4*>(w + int64_t(row) * cols + k);
+    }
+}
+
+struct AggSmem {
+    alignas(1024) unsigned char w1[kHid * kIn * 2];    // 16 KB
+    alignas(1024) unsigned char w2[kHid * kHid * 2];   // 32 KB
+    alignas(1024) unsigned char a[kTile * kIn * 2];    // 16 KB
+    alignas(1024) unsigned char h1[kTile * kHid * 2];  // 32 KB
+    float b2[kHid];
+    uint64_t bar;
+    unsigned tmem;
+};
+
+// One persistent CTA per tile stream (4 warps; warp w <-> TMEM lanes 32w..).
+__global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__ knn_id,
+                                                      const double* __restrict__ knn_w, int64_t R, int K,
+                                                      const int* __restrict__ sample_ray,
+                                                      const double* __restrict__ r_t, const double* __restrict__ dirs,
+                                                      double o0, double o1, double o2,
+                                                      const double* __restrict__ xyz,
+                                                      const uint16_t* __restrict__ feat,
+                                                      const uint16_t* __restrict__ w1,
+                                                      const uint16_t* __restrict__ w2,
+                                                      const float* __restrict__ b2, __nv_bfloat16* __restrict__ g) {
+    extern __shared__ __align__(1024) unsigned char dyn_raw[];
+    AggSmem& S = *reinterpret_cast<AggSmem*>(dyn_raw);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    load_weights(S.w1, w1, kHid, kIn);
+    load_weights(S.w2, w2, kHid, kHid);
+    for (int c = tid; c < kHid; c += blockDim.x) S.b2[c] = b2[c];
+    if (tid == 0) mbar_init1(&S.bar);
+    if (warp == 0) tmem_alloc<256>(&S.tmem);
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tbase = S.tmem;
+    const unsigned lane_addr = unsigned(warp * 32) << 16;
+    unsigned phase = 0;
+    const int per = kTile / K;  // samples per tile
+    const int64_t tiles = (R + per - 1) / per;
+    constexpr uint32_t kId1 = idesc_bf16(kTile, kHid);
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        // ---- the tile's input rows, straight into the canonical layout
+        const int row = tid;
+        const int64_t s = tile * per + row / K;
+        const int k = row % K;
+        float x[kIn];
+        double wk = 0.0;
+#pragma unroll
+        for (int i = 0; i < kIn; i++) x[i] = 0.0f;
+        if (row < per * K && s < R) {
+            const int64_t id = knn_id[s * K + k];
+            wk = knn_w[s * K + k];
+            if (id >= 0) {
+                const uint4* fp = reinterpret_cast<const uint4*>(feat + id * kFeat);
+#pragma unroll
+                for (int q4 = 0; q4 < kFeat / 8; q4++) {
+                    const uint4 u = fp[q4];
+                    const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int h = 0; h < 4; h++) {
+                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uu[h]));
+                        x[q4 * 8 + 2 * h] = f2.x;
+                        x[q4 * 8 + 2 * h + 1] = f2.y;
+                    }
+                }
+                const int ray = sample_ray[s];
+                const double t = r_t[s];
+                const double xs[3] = {o0 + t * dirs[3 * ray], o1 + t * dirs[3 * ray + 1], o2 + t * dirs[3 * ray + 2]};
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    const float d = float(xyz[3 * id + c] - xs[c]);
+                    x[kFeat + 24 + c] = d;
+#pragma unroll
+                    for (int l = 0; l < 4; l++) {
+                        float sn, cs;
+                        sincospif(d * float(1 << l), &sn, &cs);
+                        x[kFeat + 8 * c + 2 * l] = sn;
+                        x[kFeat + 8 * c + 2 * l + 1] = cs;
+                    }
+                }
+                x[kFeat + 27] = 1.0f;
+            }
+        }
+#pragma unroll
+        for (int kk = 0; kk < kIn; kk += 8) st_chunk(S.a, core_off(row, kk, kIn / 8), x + kk);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        // ---- layer 1: D[0:128) = A (128 x 64) W1^T
+        if (tid == 0) {
+#pragma unroll
+            for (int st = 0; st < kIn / 16; st++)
+                mma_bf16(tbase, smem_desc(S.a + st * 256, 128, kIn / 8 * 128),
+                         smem_desc(S.w1 + st * 256, 128, kIn / 8 * 128), kId1, st > 0);
+            mma_commit(&S.bar);
+        }
+        mbar_wait_parity(&S.bar, phase);
+        phase ^= 1u;
+        tc_fence_after();
+        // ---- h1 = relu(.) -> bf16 -> shared memory (the next A operand)
+#pragma unroll 1
+        for (int c0 = 0; c0 < kHid; c0 += 32) {
+            float v[32];
+            tmem_ld32(tbase + lane_addr + unsigned(c0), v);
+#pragma unroll
+            for (int i = 0; i < 32; i++) v[i] = fmaxf(v[i], 0.0f);
+#pragma unroll
+            for (int kk = 0; kk < 32; kk += 8) st_chunk(S.h1, core_off(row, c0 + kk, kHid / 8), v + kk);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        // ---- layer 2: D[128:256) = H1 (128 x 128) W2^T
+        if (tid == 0) {
+#pragma unroll
+            for (int st = 0; st < kHid / 16; st++)
+                mma_bf16(tbase + kHid, smem_desc(S.h1 + st * 256, 128, kHid / 8 * 128),
+                         smem_desc(S.w2 + st * 256, 128, kHid / 8 * 128), kId1, st > 0);
+            mma_commit(&S.bar);
+        }
+        mbar_wait_parity(&S.bar, phase);
+        phase ^= 1u;
+        tc_fence_after();
+        // ---- g_s = sum_k w_{s,k} relu(. + b2): the K rows of a sample are K
+        // consecutive lanes of one warp
+        const float wf = float(wk);
+#pragma unroll 1
+        for (int c0 = 0; c0 < kHid; c0 += 32) {
+            float v[32];
+            tmem_ld32(tbase + lane_addr + unsigned(kHid + c0), v);
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                float y = fmaxf(v[i] + S.b2[c0 + i], 0.0f) * wf;
+                for (int o = 1; o < K; o <<= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+                v[i] = y;
+            }
+            if (k == 0 && row < per * K && s < R) {
+                uint4* gp = reinterpret_cast<uint4*>(g + s * kHid + c0);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; q4++)
+                    gp[q4] = make_uint4(pack2(v[8 * q4], v[8 * q4 + 1]), pack2(v[8 * q4 + 2], v[8 * q4 + 3]),
+                                        pack2(v[8 * q4 + 4], v[8 * q4 + 5]), pack2(v[8 * q4 + 6], v[8 * q4 + 7]));
+            }
+        }
+        tc_fence_before();
+        __syncthreads();  // TMEM and the A / h1 tiles are reused by the next tile
+        tc_fence_after();
+    }
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<256>(tbase);
+}
+
+struct HeadSmemM {
+    alignas(1024) unsigned char w3[kHead * kHid * 2];  // 16 KB
+    alignas(1024) unsigned char a[kTile * kHid * 2];   // 32 KB
+    float b3[kHead];
+    float w4[4 * kHead];
+    float b4[4];
+    uint64_t bar;
+    unsigned tmem;
+};
+
+__global__ void __launch_bounds__(kThreadsMlp) k_mlp_head(const __nv_bfloat16* __restrict__ g, int64_t R,
+                                                           const uint16_t* __restrict__ w3,
+                                                           const float* __restrict__ b3,
+                                                           const float* __restrict__ w4,
+                                                           const float* __restrict__ b4, float* __restrict__ out) {
+    extern __shared__ __align__(1024) unsigned char dyn_raw[];
+    HeadSmemM& S = *reinterpret_cast<HeadSmemM*>(dyn_raw);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    load_weights(S.w3, w3, kHead, kHid);
+    for (int c = tid; c < kHead; c += blockDim.x) S.b3[c] = b3[c];
+    for (int c = tid; c < 4 * kHead; c += blockDim.x) S.w4[c] = w4[c];
+    if (tid < 4) S.b4[tid] = b4[tid];
+    if (tid == 0) mbar_init1(&S.bar);
+    if (warp == 0) tmem_alloc<64>(&S.tmem);
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tbase = S.tmem;
+    const unsigned lane_addr = unsigned(warp * 32) << 16;
+    unsigned phase = 0;
+    const int64_t tiles = (R + kTile - 1) / kTile;
+    constexpr uint32_t kId = idesc_bf16(kTile, kHead);
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t s = tile * kTile + tid;
+        // the tile's g rows (16-byte chunks) into the canonical layout
+#pragma unroll
+        for (int kk = 0; kk < kHid; kk += 8) {
+            uint4 u = make_uint4(0, 0, 0, 0);
+            if (s < R) u = *reinterpret_cast<const uint4*>(g + s * kHid + kk);
+            *reinterpret_cast<uint4*>(S.a + core_off(tid, kk, kHid / 8)) = u;
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (tid == 0) {
+#pragma unroll
+            for (int st = 0; st < kHid / 16; st++)
+                mma_bf16(tbase, smem_desc(S.a + st * 256, 128, kHid / 8 * 128),
+                         smem_desc(S.w3 + st * 256, 128, kHid / 8 * 128), kId, st > 0);
+            mma_commit(&S.bar);
+        }
+        mbar_wait_parity(&S.bar, phase);
+        phase ^= 1u;
+        tc_fence_after();
+        float o[4] = {S.b4[0], S.b4[1], S.b4[2], S.b4[3]};
+#pragma unroll 1
+        for (int c0 = 0; c0 < kHead; c0 += 32) {
+            float v[32];
+            tmem_ld32(tbase + lane_addr + unsigned(c0), v);
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                const float h = fmaxf(v[i] + S.b3[c0 + i], 0.0f);
+#pragma unroll
+                for (int j = 0; j < 4; j++) o[j] = fmaf(S.w4[j * kHead + c0 + i], h, o[j]);
+            }
+        }
+        if (s < R) {
+            const float sigma = o[0] > 20.0f ? o[0] : log1pf(expf(o[0]));
+            float4 res;
+            res.x = sigma;
+            res.y = 1.0f / (1.0f + expf(-o[1]));
+            res.z = 1.0f / (1.0f + expf(-o[2]));
+            res.w = 1.0f / (1.0f + expf(-o[3]));
+            reinterpret_cast<float4*>(out)[s] = res;
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<64>(tbase);
+}
+
+}  // namespace
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" int hp_pointnerf_aggregate(const int64_t* knn_id, const double* knn_w, int64_t R, int32_t k,
+                                      const int32_t* sample_ray, const double* r_t, const double* dirs,
+                                      const double* origin_host, const double* positions, const uint16_t* features,
+                                      const uint16_t* w1, const uint16_t* w2, const float* b2, uint16_t* g_out,
+                                      hp_stream_t stream) {
+    if (R < 0 || k < 1 || k > 32 || (k & (k - 1)) || !origin_host) {
+        set_error("hp_pointnerf_aggregate: k must be a power of two in [1, 32]");
+        return HP_EINVAL;
+    }
+    if (R == 0) return HP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int occ = kernel_occupancy((const void*)k_agg, kThreadsMlp, sizeof(AggSmem));
+    if (occ < 0) return occ;
+    const int64_t tiles = (R + kTile / k - 1) / (kTile / k);
+    const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * std::min(occ, 2));
+    TimedSpan ts("k_mlp_agg", s);
+    k_agg<<<unsigned(grid), kThreadsMlp, sizeof(AggSmem), s>>>(
+        knn_id, knn_w, R, k, sample_ray, r_t, dirs, origin_host[0], origin_host[1], origin_host[2], positions,
+        features, w1, w2, b2, reinterpret_cast<__nv_bfloat16*>(g_out));
+    HP_CHECK_LAUNCH("k_mlp_agg");
+    return HP_OK;
+}
+
+extern "C" int hp_pointnerf_head(const uint16_t* g, int64_t R, const uint16_t* w3, const float* b3, const float* w4,
+                                 const float* b4, float* out, hp_stream_t stream) {
+    if (R < 0) {
+        set_error("hp_pointnerf_head: invalid arguments");
+        return HP_EINVAL;
+    }
+    if (R == 0) return HP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int occ = kernel_occupancy((const void*)k_mlp_head, kThreadsMlp, sizeof(HeadSmemM));
+    if (occ < 0) return occ;
+    const int64_t tiles = (R + kTile - 1) / kTile;
+    const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * std::min(occ, 4));
+    TimedSpan ts("k_mlp_head", s);
+    k_mlp_head<<<unsigned(grid), kThreadsMlp, sizeof(HeadSmemM), s>>>(reinterpret_cast<const __nv_bfloat16*>(g), R,
+                                                                       w3, b3, w4, b4, out);
+    HP_CHECK_LAUNCH("k_mlp_head");
+    return HP_OK;
+}
