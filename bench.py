@@ -45,6 +45,9 @@ WORKLOADS = {
     # the rest of the cfg4 radius sweep (Q ~ 1.7e10 / 6.9e10: several ray chunks per frame)
     "cfg4_d01": (dict(kind="sphere_surface", n=10_000_000, seed=0, noise=0.005), (1920, 1080, 40.0), 0.01),
     "cfg4_d02": (dict(kind="sphere_surface", n=10_000_000, seed=0, noise=0.005), (1920, 1080, 40.0), 0.02),
+    # full render step: cfg2's search + sampling (with the K neighbours emitted)
+    # + the Point-NeRF aggregation MLP (bf16, tcgen05) + volume compositing
+    "cfg5": (dict(kind="sphere_surface", n=1_000_000, seed=0, noise=0.005), (800, 800, 40.0), 0.01),
 }
 # ScanNet-shaped indoor batch: 64 views orbiting a multi-plane cloud, one
 # index per view; views are sharded across ranks
@@ -52,8 +55,8 @@ CFG3 = dict(scene=dict(kind="parallel_planes", n=3_000_000, seed=0, plane_count=
                        extent=4.0, noise=0.005), size=(640, 480, 60.0), delta=0.01, views=64)
 # rays checked against the oracle before timing / timed on the host CPU
 # (the oracle runs the reference's O(q^2) sampler: sparser subsets for the larger radii)
-PARITY_STRIDE = {"cfg1": 53, "cfg2": 53, "cfg4": 4999, "cfg4_d01": 20011, "cfg4_d02": 200003}
-CPU_STRIDE = {"cfg1": 97, "cfg2": 97, "cfg4": 20011, "cfg4_d01": 200003, "cfg4_d02": 1000003}
+PARITY_STRIDE = {"cfg1": 53, "cfg2": 53, "cfg5": 53, "cfg4": 4999, "cfg4_d01": 20011, "cfg4_d02": 200003}
+CPU_STRIDE = {"cfg1": 97, "cfg2": 97, "cfg5": 97, "cfg4": 20011, "cfg4_d01": 200003, "cfg4_d02": 1000003}
 T_NEAR, T_FAR = 1.0, 10.0
 
 
@@ -452,10 +455,18 @@ def run_ours(args, w, rank, world, dist):
     scfg = hp.SamplerConfig()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    render = w["name"] == "cfg5"
+    if render:
+        from paper_2404_14044_b200.pointnerf import PointNeRFMLP, render_step
+        mlp = PointNeRFMLP(w["cloud"].count, seed=0, device_=dev)
+
     def step(timer=None):
-        fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer)
+        fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer, emit_knn=render)
+        if render:  # the full render step: aggregation MLP + compositing of this rank's rays
+            fr.image = render_step(mlp, fr.samples, rays[1], w["cam"].origin, xyz, rays[0], rays[3],
+                                   w["cam"].width, w["cam"].height)
         if world > 1:
-            gather_samples(fr.samples, dist)
+            gather_samples(fr.samples[:9], dist)
         return fr
 
     for _ in range(args.warmup):
@@ -492,7 +503,7 @@ def run_ours(args, w, rank, world, dist):
     # parity gate on the last timed frame's own output
     parity = "skipped"
     if rank == 0 and not args.no_parity:
-        parity = parity_gate(w, fr.samples, r0, r1, PARITY_STRIDE.get(w["name"], 53))
+        parity = parity_gate(w, fr.samples[:9], r0, r1, PARITY_STRIDE.get(w["name"], 53))
     ms = statistics.mean(times)
     if dist is not None:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -514,7 +525,7 @@ def run_ours(args, w, rank, world, dist):
     pipeline.TRACK_PREFIX_LEN = False
     flag_reasons = [int(x) for x in sum(pipeline.FLAG_REASONS).cpu()] if pipeline.FLAG_REASONS else None
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not render:
         e2e = run_e2e(args, w, r0, r1, dist)
     if rank != 0:
         return
@@ -587,6 +598,19 @@ def run_ours(args, w, rank, world, dist):
         "gpu_launches": launches,
         "clocks": smi.summary(),
     }
+    if render:  # the MLP kernels against the tensor-core peak
+        R_all, Kn = fr.R, scfg.k_neighbors
+        flops = {"k_mlp_agg": R_all * Kn * 2 * (64 * 128 + 128 * 128), "k_mlp_head": R_all * 2 * (128 * 64 + 64 * 4)}
+        tf_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1590.0
+        line["mlp_roofline"] = {
+            "bound": "tensor", "unit": "TFLOP/s", "peak": tf_peak, "peak_source": "measured bf16 burst (cuBLAS)",
+            "kernels": {k: {"ms": kern[k][0], "flop": f, "achieved": f / (kern[k][0] / 1e3) / 1e12,
+                            "frac": f / (kern[k][0] / 1e3) / 1e12 / tf_peak} for k, f in flops.items() if k in kern},
+            "rows": R_all * Kn, "samples": R_all, "k": Kn}
+        line["config"]["workload"] = ("cfg5: cfg2 search + primary-surface sampling (K=8 neighbours emitted) + "
+                                      "Point-NeRF aggregation MLP (bf16 tcgen05: 64->128->128 per neighbour, "
+                                      "weighted sum, 128->64->4 head) + volume compositing; random-init weights")
     if e2e is not None:
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:

@@ -143,16 +143,20 @@ __device__ void load_weights(unsigned char* dst, const uint16_t* __restrict__ w,
 struct AggSmem {
     alignas(1024) unsigned char w1[kHid * kIn * 2];    // 16 KB
     alignas(1024) unsigned char w2[kHid * kHid * 2];   // 32 KB
-    alignas(1024) unsigned char a[kTile * kIn * 2];    // 16 KB
-    alignas(1024) unsigned char h1[kTile * kHid * 2];  // 32 KB
+    alignas(1024) unsigned char ah[kTile * kHid * 2];  // 32 KB: the input tile (16 KB), then h1 over it
     float b2[kHid];
     uint64_t bar;
     unsigned tmem;
 };
 
-// One persistent CTA per tile stream (4 warps; warp w <-> TMEM lanes 32w..).
-__global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__ knn_id,
-                                                      const double* __restrict__ knn_w, int64_t R, int K,
+constexpr int kThreadsAgg = 256;  // 8 warps: warps w and w + 4 share TMEM lanes 32 (w % 4).., split the columns
+
+// One persistent CTA per tile stream.  Thread t builds half of row t % 128
+// (t < 128: the point feature; t >= 128: the positional terms); in the
+// epilogues warp w reads TMEM lanes 32 (w % 4).. and columns 64 (w / 4)..
+template <int K>
+__global__ void __launch_bounds__(kThreadsAgg) k_agg(const int64_t* __restrict__ knn_id,
+                                                      const double* __restrict__ knn_w, int64_t R,
                                                       const int* __restrict__ sample_ray,
                                                       const double* __restrict__ r_t, const double* __restrict__ dirs,
                                                       double o0, double o1, double o2,
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__
                                                       const float* __restrict__ b2, __nv_bfloat16* __restrict__ g) {
     extern __shared__ __align__(1024) unsigned char dyn_raw[];
     AggSmem& S = *reinterpret_cast<AggSmem*>(dyn_raw);
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     load_weights(S.w1, w1, kHid, kIn);
     load_weights(S.w2, w2, kHid, kHid);
     for (int c = tid; c < kHid; c += blockDim.x) S.b2[c] = b2[c];
@@ -174,24 +178,25 @@ __global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__
     __syncthreads();
     tc_fence_after();
     const unsigned tbase = S.tmem;
-    const unsigned lane_addr = unsigned(warp * 32) << 16;
+    const int quad = warp & 3, chalf = warp >> 2;
+    const int erow = quad * 32 + lane;  // this thread's row in the epilogues
+    const unsigned lane_addr = unsigned(quad * 32) << 16;
     unsigned phase = 0;
     const int per = kTile / K;  // samples per tile
     const int64_t tiles = (R + per - 1) / per;
     constexpr uint32_t kId1 = idesc_bf16(kTile, kHid);
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         // ---- the tile's input rows, straight into the canonical layout
-        const int row = tid;
-        const int64_t s = tile * per + row / K;
-        const int k = row % K;
-        float x[kIn];
-        double wk = 0.0;
+        {
+            const int row = tid & (kTile - 1), part = tid >> 7;
+            const int64_t s = tile * per + row / K;
+            const int k = row % K;
+            float x[32];
 #pragma unroll
-        for (int i = 0; i < kIn; i++) x[i] = 0.0f;
-        if (row < per * K && s < R) {
-            const int64_t id = knn_id[s * K + k];
-            wk = knn_w[s * K + k];
-            if (id >= 0) {
+            for (int i = 0; i < 32; i++) x[i] = 0.0f;
+            const bool live = row < per * K && s < R;
+            const int64_t id = live ? knn_id[s * K + k] : -1;
+            if (id >= 0 && part == 0) {
                 const uint4* fp = reinterpret_cast<const uint4*>(feat + id * kFeat);
 #pragma unroll
                 for (int q4 = 0; q4 < kFeat / 8; q4++) {
@@ -204,26 +209,30 @@ __global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__
                         x[q4 * 8 + 2 * h + 1] = f2.y;
                     }
                 }
+            } else if (id >= 0) {
                 const int ray = sample_ray[s];
                 const double t = r_t[s];
                 const double xs[3] = {o0 + t * dirs[3 * ray], o1 + t * dirs[3 * ray + 1], o2 + t * dirs[3 * ray + 2]};
 #pragma unroll
                 for (int c = 0; c < 3; c++) {
                     const float d = float(xyz[3 * id + c] - xs[c]);
-                    x[kFeat + 24 + c] = d;
+                    x[24 + c] = d;
+                    float sn, cs;
+                    sincospif(d, &sn, &cs);
 #pragma unroll
-                    for (int l = 0; l < 4; l++) {
-                        float sn, cs;
-                        sincospif(d * float(1 << l), &sn, &cs);
-                        x[kFeat + 8 * c + 2 * l] = sn;
-                        x[kFeat + 8 * c + 2 * l + 1] = cs;
+                    for (int l = 0; l < 4; l++) {  // doubling: sin 2a = 2 sin a cos a, cos 2a = 1 - 2 sin^2 a
+                        x[8 * c + 2 * l] = sn;
+                        x[8 * c + 2 * l + 1] = cs;
+                        const float s2 = 2.0f * sn * cs, c2 = fmaf(-2.0f * sn, sn, 1.0f);
+                        sn = s2;
+                        cs = c2;
                     }
                 }
-                x[kFeat + 27] = 1.0f;
+                x[27] = 1.0f;
             }
-        }
 #pragma unroll
-        for (int kk = 0; kk < kIn; kk += 8) st_chunk(S.a, core_off(row, kk, kIn / 8), x + kk);
+            for (int kk = 0; kk < 32; kk += 8) st_chunk(S.ah, core_off(row, part * 32 + kk, kIn / 8), x + kk);
+        }
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
@@ -232,22 +241,23 @@ __global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__
         if (tid == 0) {
 #pragma unroll
             for (int st = 0; st < kIn / 16; st++)
-                mma_bf16(tbase, smem_desc(S.a + st * 256, 128, kIn / 8 * 128),
+                mma_bf16(tbase, smem_desc(S.ah + st * 256, 128, kIn / 8 * 128),
                          smem_desc(S.w1 + st * 256, 128, kIn / 8 * 128), kId1, st > 0);
             mma_commit(&S.bar);
         }
         mbar_wait_parity(&S.bar, phase);
         phase ^= 1u;
         tc_fence_after();
-        // ---- h1 = relu(.) -> bf16 -> shared memory (the next A operand)
+        // ---- h1 = relu(.) -> bf16 -> shared memory over the input tile (the
+        // MMA that read it has completed)
 #pragma unroll 1
-        for (int c0 = 0; c0 < kHid; c0 += 32) {
+        for (int c0 = chalf * 64; c0 < chalf * 64 + 64; c0 += 32) {
             float v[32];
             tmem_ld32(tbase + lane_addr + unsigned(c0), v);
 #pragma unroll
             for (int i = 0; i < 32; i++) v[i] = fmaxf(v[i], 0.0f);
 #pragma unroll
-            for (int kk = 0; kk < 32; kk += 8) st_chunk(S.h1, core_off(row, c0 + kk, kHid / 8), v + kk);
+            for (int kk = 0; kk < 32; kk += 8) st_chunk(S.ah, core_off(erow, c0 + kk, kHid / 8), v + kk);
         }
         fence_async_smem();
         tc_fence_before();
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__
         if (tid == 0) {
 #pragma unroll
             for (int st = 0; st < kHid / 16; st++)
-                mma_bf16(tbase + kHid, smem_desc(S.h1 + st * 256, 128, kHid / 8 * 128),
+                mma_bf16(tbase + kHid, smem_desc(S.ah + st * 256, 128, kHid / 8 * 128),
                          smem_desc(S.w2 + st * 256, 128, kHid / 8 * 128), kId1, st > 0);
             mma_commit(&S.bar);
         }
@@ -265,28 +275,54 @@ __global__ void __launch_bounds__(kThreadsMlp) k_agg(const int64_t* __restrict__
         phase ^= 1u;
         tc_fence_after();
         // ---- g_s = sum_k w_{s,k} relu(. + b2): the K rows of a sample are K
-        // consecutive lanes of one warp
-        const float wf = float(wk);
-#pragma unroll 1
-        for (int c0 = 0; c0 < kHid; c0 += 32) {
-            float v[32];
-            tmem_ld32(tbase + lane_addr + unsigned(kHid + c0), v);
+        // consecutive lanes; a shuffle reduce-scatter leaves each of them
+        // 64 / K of the sample's columns to write
+        {
+            const int64_t s = tile * per + erow / K;
+            const bool live = erow < per * K && s < R;
+            const float wf = live ? float(knn_w[s * K + erow % K]) : 0.0f;
+            float v[64];
+            tmem_ld32(tbase + lane_addr + unsigned(kHid + chalf * 64), v);
+            tmem_ld32(tbase + lane_addr + unsigned(kHid + chalf * 64 + 32), v + 32);
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-                float y = fmaxf(v[i] + S.b2[c0 + i], 0.0f) * wf;
-                for (int o = 1; o < K; o <<= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-                v[i] = y;
+            for (int i = 0; i < 64; i++) v[i] = fmaxf(v[i] + S.b2[chalf * 64 + i], 0.0f) * wf;
+            // step with partner distance d: keep the lower (lane bit d clear) or
+            // upper half of the current span, add the partner's copy of it;
+            // the kept half moves to the front
+#pragma unroll
+            for (int d = 1; d < K; d <<= 1) {
+                const bool upper = (lane & d) != 0;
+                const int h = 32 / d;  // 64 >> (log2 d + 1)
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                    if (i < h) {
+                        const float send = upper ? v[i] : v[h + i];
+                        const float recv = __shfl_xor_sync(0xffffffffu, send, d);
+                        v[i] = (upper ? v[h + i] : v[i]) + recv;
+                    }
+                }
             }
-            if (k == 0 && row < per * K && s < R) {
-                uint4* gp = reinterpret_cast<uint4*>(g + s * kHid + c0);
+            constexpr int kSpan = 64 / K;  // columns this lane holds, at block (bit-reversed lane % K)
+            if (live) {
+                int blk = 0;
 #pragma unroll
-                for (int q4 = 0; q4 < 4; q4++)
-                    gp[q4] = make_uint4(pack2(v[8 * q4], v[8 * q4 + 1]), pack2(v[8 * q4 + 2], v[8 * q4 + 3]),
-                                        pack2(v[8 * q4 + 4], v[8 * q4 + 5]), pack2(v[8 * q4 + 6], v[8 * q4 + 7]));
+                for (int d = 1, bit = K / 2; d < K; d <<= 1, bit >>= 1)
+                    if (lane & d) blk |= bit;
+                __nv_bfloat16* gp = g + s * kHid + chalf * 64 + blk * kSpan;
+                if constexpr (kSpan >= 8) {
+#pragma unroll
+                    for (int i = 0; i < kSpan; i += 8)
+                        *reinterpret_cast<uint4*>(gp + i) =
+                            make_uint4(pack2(v[i], v[i + 1]), pack2(v[i + 2], v[i + 3]), pack2(v[i + 4], v[i + 5]),
+                                       pack2(v[i + 6], v[i + 7]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kSpan; i++) gp[i] = __float2bfloat16_rn(v[i]);
+                }
             }
         }
         tc_fence_before();
-        __syncthreads();  // TMEM and the A / h1 tiles are reused by the next tile
+        __syncthreads();  // TMEM and the shared tile are reused by the next tile
         tc_fence_after();
     }
     __syncthreads();
@@ -394,16 +430,26 @@ extern "C" int hp_pointnerf_aggregate(const int64_t* knn_id, const double* knn_w
     }
     if (R == 0) return HP_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int occ = kernel_occupancy((const void*)k_agg, kThreadsMlp, sizeof(AggSmem));
-    if (occ < 0) return occ;
-    const int64_t tiles = (R + kTile / k - 1) / (kTile / k);
-    const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * std::min(occ, 2));
-    TimedSpan ts("k_mlp_agg", s);
-    k_agg<<<unsigned(grid), kThreadsMlp, sizeof(AggSmem), s>>>(
-        knn_id, knn_w, R, k, sample_ray, r_t, dirs, origin_host[0], origin_host[1], origin_host[2], positions,
-        features, w1, w2, b2, reinterpret_cast<__nv_bfloat16*>(g_out));
-    HP_CHECK_LAUNCH("k_mlp_agg");
-    return HP_OK;
+    auto launch = [&](auto kern) -> int {
+        const int occ = kernel_occupancy((const void*)kern, kThreadsAgg, sizeof(AggSmem));
+        if (occ < 0) return occ;
+        const int64_t tiles = (R + kTile / k - 1) / (kTile / k);
+        const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * std::min(occ, 2));  // TMEM: 2 x 256
+        TimedSpan ts("k_mlp_agg", s);
+        kern<<<unsigned(grid), kThreadsAgg, sizeof(AggSmem), s>>>(
+            knn_id, knn_w, R, sample_ray, r_t, dirs, origin_host[0], origin_host[1], origin_host[2], positions,
+            features, w1, w2, b2, reinterpret_cast<__nv_bfloat16*>(g_out));
+        HP_CHECK_LAUNCH("k_mlp_agg");
+        return HP_OK;
+    };
+    switch (k) {
+        case 1: return launch(k_agg<1>);
+        case 2: return launch(k_agg<2>);
+        case 4: return launch(k_agg<4>);
+        case 8: return launch(k_agg<8>);
+        case 16: return launch(k_agg<16>);
+        default: return launch(k_agg<32>);
+    }
 }
 
 extern "C" int hp_pointnerf_head(const uint16_t* g, int64_t R, const uint16_t* w3, const float* b3, const float* w4,
