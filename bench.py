@@ -368,6 +368,57 @@ def cpu_run(w, stride, threads):
     return w["m"] / secs, dict(t_build_s=t_build, t_subset_s=t_sub, m_sub=m_sub)
 
 
+def reference_numba_run(w, stride, threads):
+    """The reference's OWN CPU path (hashpoint from baseline/_ref, numba,
+    unmodified): hash_index.build, then query_batch_arrays +
+    sample_batch_arrays on every stride-th ray of the frame, split into
+    interleaved ray chunks over a thread pool (the kernels are nogil,
+    _kernels.py:19; chunks are independent, hash_index.py:263-293), as the
+    reference's bench convention times them (bench.py:175-199).  Returns
+    (rays/s extrapolated to the frame, info) or None when the reference or
+    numba is not importable."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "hashpoint")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/hp_numba_cache")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import hashpoint as R
+        from hashpoint import geometry as RG, hash_index as RH, sampler as RS
+    except Exception:
+        return None
+    from concurrent.futures import ThreadPoolExecutor
+    scene, (W, H, fov), delta = WORKLOADS[w["name"]]
+    cloud = R.generate_scene(R.SceneSpec(**scene))
+    cam = R.scene_camera(W, H, fov_deg=fov)
+    cfg = R.SearchConfig(R.kernel_radius_for_min_radius(cam, T_NEAR, delta), R.pixel_disc_radius(cam))
+    dirs, pixels = RG.ray_grid(cam)
+    sc = R.SamplerConfig()
+
+    def run(idx, sel):
+        px = np.ascontiguousarray(pixels[sel])
+        m = len(px)
+        tn, tf = np.full(m, T_NEAR), np.full(m, T_FAR)
+        q = RH.query_batch_arrays(idx, px, dirs[sel], tn, tf, cfg)
+        sl = RG.radius_slopes(cam, px, cfg.kernel_radius, cfg.use_approx_radius)
+        RS.sample_batch_arrays(q[0], q[1], q[2], q[3], sl, sc, cloud.colors)
+
+    small = R.generate_scene(R.SceneSpec("sphere_surface", n=2000, seed=1))  # numba JIT compile, untimed
+    run(RH.build(small, cam, cfg), np.arange(0, len(dirs), max(len(dirs) // 64, 1)))
+    t0 = time.perf_counter()
+    idx = RH.build(cloud, cam, cfg)
+    t_build = time.perf_counter() - t0
+    sel = np.arange(0, len(dirs), stride)
+    chunks = [sel[c::threads] for c in range(threads)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda c: run(idx, c), chunks))
+    t_sub = time.perf_counter() - t0
+    secs = t_build + (len(dirs) / len(sel)) * t_sub
+    return len(dirs) / secs, dict(t_build_s=t_build, t_subset_s=t_sub, m_sub=len(sel))
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -387,29 +438,46 @@ def cpu_model():
 
 
 def run_reference(args, w, rank, world):
+    """--impl reference: the reference's own CPU path (numba, from
+    baseline/_ref) on all host threads, each step a bounded strided ray
+    subset of the frame extrapolated to the frame; the C restatement of the
+    same algorithm (oracle/hp_oracle.c) is timed beside it.  Falls back to
+    the C port if the reference cannot be imported."""
     if rank != 0:
         return
     threads = host_threads()
     stride = args.cpu_stride
-    vals = []
-    info = None
+    vals, info, kind = [], None, "reference"
+    for _ in range(args.steps):
+        r = reference_numba_run(w, stride, threads)
+        if r is None:
+            kind = "port"
+            break
+        vals.append(r[0])
+        info = r[1]
+    port_vals = []
     for _ in range(args.warmup if args.warmup < 1 else 1):
         cpu_run(w, stride * 4, threads)
-    for _ in range(args.steps):
-        v, info = cpu_run(w, stride, threads)
-        vals.append(v)
+    for _ in range(1 if kind == "reference" else args.steps):
+        v, pinfo = cpu_run(w, stride, threads)
+        port_vals.append(v)
+    if kind == "port":
+        vals, info = port_vals, pinfo
     value = statistics.median(vals)
+    port = statistics.median(port_vals)
+    sample = (f"full build + every {stride}th ray ({info['m_sub']} rays) of the frame through query+sample on "
+              f"{threads} threads (interleaved chunks), extrapolated to {w['m']} rays; " +
+              ("the reference's own numba path (hashpoint from baseline/_ref: hash_index.build, "
+               "query_batch_arrays, sample_batch_arrays)" if kind == "reference" else
+               "C restatement of the reference kernels (oracle/hp_oracle.c)") + f"; {cpu_model()}")
     line = {
         "impl": "reference", "metric": "rays/sec (search+primary-surface sampling)",
         "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * w["m"] / value, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": describe(w), "rays": w["m"], "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "port",
-                         "sample": f"full build + every {stride}th ray ({info['m_sub']} rays) of the "
-                                   f"frame through query+sample, extrapolated to {w['m']} rays; "
-                                   f"C restatement of the reference kernels (oracle/hp_oracle.c), "
-                                   f"{cpu_model()}"},
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": kind, "sample": sample,
+                         "c_port_rays_per_s": port},
         "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -615,10 +683,16 @@ def run_ours(args, w, rank, world, dist):
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:
         v, info = cpu_run(w, args.cpu_stride, host_threads())
+        ref = reference_numba_run(w, args.cpu_stride, host_threads()) if w["name"] != "cfg5" else None
         line["cpu_baseline"] = {"value": v, "unit": "rays/s", "cores": host_threads(), "kind": "port",
                                 "sample": f"full build + every {args.cpu_stride}th ray "
                                           f"({info['m_sub']} rays) through query+sample, "
                                           f"extrapolated; oracle/hp_oracle.c; {cpu_model()}"}
+        if ref is not None:
+            line["cpu_baseline"]["reference_numba"] = {
+                "value": ref[0], "unit": "rays/s", "cores": host_threads(), "kind": "reference",
+                "sample": f"the reference's own numba path (baseline/_ref hashpoint), same subset "
+                          f"({ref[1]['m_sub']} rays), interleaved chunks over the host threads"}
     print(json.dumps(line), flush=True)
 
 
