@@ -117,13 +117,18 @@ def run_views(args, rank, world, dist):
     gated = [i for i in mine if i % 8 == 0]
     kept = {}
 
+    counts = {"head_resorted_rays": 0, "full_path_rays": 0}
+
     def step(keep=False):
         Q = R = 0
+        counts["head_resorted_rays"] = counts["full_path_rays"] = 0
         for i in mine:
             v = views[i]
             fr = pipeline.frame_device(xyz, col, v["cam"], v["cfg"], *rays[i], scfg, True)
             Q += fr.Q
             R += fr.R
+            counts["head_resorted_rays"] += fr.resorted
+            counts["full_path_rays"] += fr.flagged
             if keep and i in gated:
                 kept[i] = fr.samples
         return Q, R
@@ -197,7 +202,8 @@ def run_views(args, rank, world, dist):
                                "SamplerConfig() eps retention K=8 with colours, exact transmittance",
                    "rays": m_total, "views": len(views), "Q": qr[0], "R": qr[1],
                    "l2": "flushed between timed steps (256 MB write)",
-                   "parallelism": f"views x{world}" if world > 1 else "single GPU", "parity_gate": parity},
+                   "parallelism": f"views x{world}" if world > 1 else "single GPU", "parity_gate": parity,
+                   **counts},
         "kernels_ms": {k: round(v / args.steps, 3) for k, (v, _) in sorted(kern_tot.items(), key=lambda x: -x[1][0])},
         "clocks": smi.summary(),
     }

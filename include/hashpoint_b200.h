@@ -338,6 +338,13 @@ int hp_timing_enable(int on);
 int hp_timing_collect(char* names, int names_len, double* ms, int64_t* counts, int max_entries,
                       int* n_entries);
 
+/* Checked build (libhp_b200_checked.so, `make checked`): device-side
+ * bounds / invariant checks record the source line of the first failure of
+ * each translation unit; this returns how many report one (lines[] gets up
+ * to max_out of them) and optionally clears them.  Always 0 in the normal
+ * build. */
+int hp_check_failures(int64_t* lines, int max_out, int reset);
+
 /* Kernel launches issued by this library since load (for bench gpu_launches). */
 int64_t hp_launch_count(void);
 

@@ -97,6 +97,7 @@ _SIGNATURES = {
     "hp_csr_stats": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "hp_primary_surface": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "hp_sample_debug_counters": (ctypes.c_int, [c_p, ctypes.c_int]),
+    "hp_check_failures": (ctypes.c_int, [c_p, ctypes.c_int, ctypes.c_int]),
     "hp_timing_enable": (ctypes.c_int, [ctypes.c_int]),
     "hp_timing_collect": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, c_p, c_p, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_int)]),
@@ -158,3 +159,14 @@ def timing_collect() -> dict:
                               ctypes.byref(n)))
     keys = names.value.decode().split("\n")[: n.value]
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}
+
+
+def check_failures(reset: bool = True) -> list:
+    """Checked build: source lines of failed device-side checks (empty
+    otherwise)."""
+    import numpy as np
+    out = np.zeros(16, np.int64)
+    n = load().hp_check_failures(out.ctypes.data_as(c_p), 16, 1 if reset else 0)
+    if n < 0:
+        check(n)
+    return [int(x) for x in out[: min(n, 16)]]

@@ -146,6 +146,7 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ lin, int32_t* _
             if (lane_id() == leader) pos = atomicAdd(&cursor[l], __popc(peers));
             pos = __shfl_sync(peers, pos, leader);
             pos += __popc(peers & ((1u << lane_id()) - 1));
+            HP_ASSERT(pos >= 0 && pos < n);
             slot_pid[pos] = int32_t(i);
         }
     }

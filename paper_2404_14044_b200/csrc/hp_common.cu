@@ -261,6 +261,38 @@ extern "C" int hp_timing_collect(char* names, int names_len, double* ms, int64_t
     return HP_OK;
 }
 
+namespace hp {
+namespace {
+std::mutex g_chk_mu;
+std::vector<CheckReader>& check_readers() {
+    static std::vector<CheckReader> v;
+    return v;
+}
+}  // namespace
+int register_check_reader(CheckReader f) {
+    std::lock_guard<std::mutex> lk(g_chk_mu);
+    check_readers().push_back(f);
+    return int(check_readers().size());
+}
+}  // namespace hp
+
+// Checked build: the source lines of the first failing HP_ASSERT of each
+// translation unit (0 = none), up to max_out of them; returns how many
+// translation units report a failure (always 0 in the normal build).
+extern "C" int hp_check_failures(int64_t* lines, int max_out, int reset) {
+    std::lock_guard<std::mutex> lk(hp::g_chk_mu);
+    int n = 0;
+    for (auto f : hp::check_readers()) {
+        unsigned long long v = 0;
+        if (f(&v, reset) != 0) return hp::cuda_status(cudaGetLastError(), "hp_check_failures");
+        if (v) {
+            if (n < max_out && lines) lines[n] = int64_t(v);
+            n++;
+        }
+    }
+    return n;
+}
+
 extern "C" const char* hp_last_error(void) { return hp::g_err; }
 extern "C" int hp_version(void) { return 1; }
 extern "C" int64_t hp_launch_count(void) { return hp::g_launches.load(); }

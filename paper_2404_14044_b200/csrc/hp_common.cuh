@@ -33,6 +33,35 @@ struct TimedSpan {
         if (_e != cudaSuccess) return ::hp::cuda_status(_e, where);            \
     } while (0)
 
+// ---------------------------------------------------------------- checked build
+// `make checked` (-DHP_CHECKED) builds libhp_b200_checked.so: HP_ASSERT
+// records the first failing check of each translation unit (source line)
+// in a device word instead of touching memory out of bounds;
+// hp_check_failures() reads them (the test suite runs against it: the
+// substitute for compute-sanitizer, which is closed on this pool).  In the
+// normal build HP_ASSERT compiles to nothing.
+using CheckReader = int (*)(unsigned long long* out, int reset);
+int register_check_reader(CheckReader f);
+#ifdef HP_CHECKED
+static __device__ unsigned long long g_hp_check;
+#define HP_ASSERT(c)                                                                     \
+    do {                                                                                 \
+        if (!(c)) atomicCAS(&::hp::g_hp_check, 0ull, (unsigned long long)__LINE__);      \
+    } while (0)
+namespace {
+[[maybe_unused]] const int hp_check_registered = register_check_reader([](unsigned long long* out, int reset) -> int {
+    if (cudaMemcpyFromSymbol(out, g_hp_check, sizeof(*out)) != cudaSuccess) return -1;
+    if (reset) {
+        const unsigned long long z = 0;
+        if (cudaMemcpyToSymbol(g_hp_check, &z, sizeof(z)) != cudaSuccess) return -1;
+    }
+    return 0;
+});
+}  // namespace
+#else
+#define HP_ASSERT(c) ((void)0)
+#endif
+
 #define HP_TRY(expr)                                                           \
     do {                                                                       \
         int _rc = (expr);                                                      \

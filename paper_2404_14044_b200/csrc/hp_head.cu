@@ -165,7 +165,7 @@ struct HeadScanSmem {
     uint64_t bar[2];
     int fill[kGroupMax], scn[kGroupMax], bad[kGroupMax];
     unsigned kmin[kGroupMax], kmax[kGroupMax];
-    int64_t off[kGroupMax];
+    int64_t off[kGroupMax], end[kGroupMax];
     int dq[kWarps][64];  // deferred (uncertain) slots of the warp's current ray run
 };
 
@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
             S.kmin[threadIdx.x] = 0xffffffffu;
             S.kmax[threadIdx.x] = 0u;
             S.off[threadIdx.x] = soff[r0 + threadIdx.x];
+            S.end[threadIdx.x] = soff[r0 + threadIdx.x + 1];
         }
         group_setup(S.head, R, QC, r0, G, s);
         unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's key bounds for the current ray
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                     const unsigned b = __ballot_sync(0xffffffffu, ok);
                     if (ok) {
                         const int64_t pos = off + fill + __popc(b & lanemask_lt());
+                        HP_ASSERT(pos < S.end[g]);
                         const unsigned key = fkey(__double2float_rd(t));
                         sc_key[pos] = key;
                         sc_slot[pos] = k;
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                     const unsigned acc = __ballot_sync(0xffffffffu, cls == 1);
                     if (cls == 1) {
                         const int64_t pos = off + fill + __popc(acc & lanemask_lt());
+                        HP_ASSERT(pos < S.end[g]);
                         const unsigned key = fkey(__fsub_rd(tf, eps));
                         sc_key[pos] = key;
                         sc_slot[pos] = k;
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                     fill += __popc(acc);
                     const unsigned unc = __ballot_sync(0xffffffffu, cls == 2);
                     if (unc) {
+                        HP_ASSERT(nq + __popc(unc) <= 64);
                         if (cls == 2) dq[nq + __popc(unc & lanemask_lt())] = k;
                         nq += __popc(unc);
                         if (nq >= 32) flush(32);
@@ -375,8 +379,10 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
             }
 #pragma unroll
             for (int u = 0; u < 4; u++)
-                if (e0 + u * 32 + lane < q)
+                if (e0 + u * 32 + lane < q) {
+                    HP_ASSERT(kv[u] >= M.kmin && ((kv[u] - M.kmin) >> sh) < unsigned(kBins));
                     atomicAdd(&H[(kv[u] - M.kmin) >> sh], 1);
+                }
         }
         __syncwarp();
         constexpr int kPer = kBins / 32;  // lane owns bins [lane * kPer, lane * kPer + kPer)
@@ -459,6 +465,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
             kc = sv.x;
             S = int(sv.y);
         }
+        HP_ASSERT(S <= kCap && S <= q);
         if (tid == 0) {
             F.cnt = F.keep = F.fcount = 0;
             F.fbad = M.bad;
@@ -491,6 +498,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
                     int base = 0;
                     if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
                     base = __shfl_sync(0xffffffffu, base, 0);
+                    HP_ASSERT(!in || base + __popc(b & lanemask_lt()) < S);
                     if (in) F.slot[base + __popc(b & lanemask_lt())] = sc_slot[so + e];
                 }
             }
@@ -526,6 +534,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
                                    F.chist, F.scan_sh);
         const int Lh = F.keep;
         const int64_t ho = hoff[i];
+        HP_ASSERT(Lh <= S && ho + Lh <= hoff[i + 1] && (all || F.cnt == S));
         const double r0 = Lh > 0 ? dmul(__ldg(slopes + r), F.t[F.perm[0]]) : 0.0;
         int cnt = 0;
         bool bad = false;

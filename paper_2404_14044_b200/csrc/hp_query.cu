@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, HP_SCAN_MINB) k_query_scan(hp_query_
                     const unsigned b = __ballot_sync(0xffffffffu, cls == 1);
                     if (cls == 1) {
                         const int64_t pos = off + fill + __popc(b & ((1u << lane_id()) - 1));
+                        HP_ASSERT(pos < capacity);
                         sc_t[pos] = t;
                         sc_d[pos] = d2;  // dist^2: the sort takes the square root
                         sc_id[pos] = S.pid[buf][k - c0];

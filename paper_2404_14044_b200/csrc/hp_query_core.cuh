@@ -196,6 +196,7 @@ __device__ void rank_segment(int q, float tlo, float thi, const double* t, const
                 f += min(off, width - 1);
             }
             f = min(f, nb - 1);
+            HP_ASSERT(f >= 0 && f < nb);
             const int li = atomicAdd(&hist[f], 1);
             bk[e] = (unsigned(f) << 16) | unsigned(li);
         }
@@ -204,6 +205,7 @@ __device__ void rank_segment(int q, float tlo, float thi, const double* t, const
         __syncthreads();
         for (int e = tid; e < q; e += kT) {
             const unsigned be_k = bk[e];
+            HP_ASSERT(hist[be_k >> 16] + int(be_k & 0xffffu) < q);
             lst[hist[be_k >> 16] + (be_k & 0xffffu)] = (unsigned short)e;
         }
         __syncthreads();
@@ -220,6 +222,7 @@ __device__ void rank_segment(int q, float tlo, float thi, const double* t, const
                     rank += key_less(t[o], id[o], te, ie);
                 }
             }
+            HP_ASSERT(bs + rank < q);
             perm[bs + rank] = (unsigned short)e;
         }
         __syncthreads();

@@ -281,7 +281,10 @@ __global__ void k_sample_expand(int64_t m, const int64_t* __restrict__ eoff, int
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t ray = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); ray < m; ray += warps) {
         const int64_t a = eoff[ray], b = eoff[ray + 1];
-        for (int64_t k = a + lane_id(); k < b; k += 32) cand_ray[k] = int(ray);
+        for (int64_t k = a + lane_id(); k < b; k += 32) {
+            HP_ASSERT(k < cap);
+            cand_ray[k] = int(ray);
+        }
     }
 }
 
@@ -302,7 +305,7 @@ struct Exact {
 
 // One thread per exact candidate (all lanes busy regardless of how few
 // candidates a ray needs): exact udf / alpha / colour of candidate j of ray.
-template <class BestT>
+template <class BestT, bool kKnn>
 __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
                                                            const int64_t* __restrict__ eoff, Exact X) {
     const int64_t n = eoff[C.m];
@@ -321,11 +324,10 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
             const int qt = C.qtrue(ray);
             ok = eval_exact<BestT>(V, q, qt, q < qt ? __ldg(C.cut_t + ray) : CUDART_INF, j, pl.z & 1, pl.x,
                                    C.slopes[ray], P, C.ids32 + lo, C.colors, u, a, col, evals,
-                                   P.emit_knn ? X.knn_id + c * P.K : nullptr, P.emit_knn ? X.knn_w + c * P.K : nullptr);
+                                   kKnn ? X.knn_id + c * P.K : nullptr, kKnn ? X.knn_w + c * P.K : nullptr);
         } else {
             eval_exact<BestT>(V, q, q, CUDART_INF, j, pl.z & 1, pl.x, C.slopes[ray], P, C.ids + lo, C.colors, u, a,
-                              col, evals, P.emit_knn ? X.knn_id + c * P.K : nullptr,
-                              P.emit_knn ? X.knn_w + c * P.K : nullptr);
+                              col, evals, kKnn ? X.knn_id + c * P.K : nullptr, kKnn ? X.knn_w + c * P.K : nullptr);
         }
         if (!ok) C.flag[ray] = 5;
         X.udf[c] = u;
@@ -347,6 +349,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, cons
 // candidates are compacted to the front of the ray's exact slots (a retained
 // candidate's position never exceeds its index, and every lane reads its
 // chunk before any lane writes).
+template <bool kKnn>
 __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const RayOut& RO,
                            const int4* __restrict__ plan, const int64_t* __restrict__ eoff, const Exact& X) {
     const int lane = lane_id();
@@ -396,6 +399,7 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
         if (keep) {
             const bool mine = (keep >> lane) & 1u;
             const int64_t dst = e0 + nret + __popc(keep & ((1u << lane) - 1));
+            HP_ASSERT(dst < e0 + E && dst <= e0 + j);
             double u = 0.0, c[3] = {0.0, 0.0, 0.0};
             if (mine) {
                 u = X.udf[e0 + j];
@@ -412,7 +416,7 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
                     for (int x = 0; x < 3; x++) X.col[3 * dst + x] = c[x];
             }
             __syncwarp();
-            if (P.emit_knn) {  // the neighbour rows, 8 columns at a time (every read before any write)
+            if (kKnn) {  // the neighbour rows, 8 columns at a time (every read before any write)
                 for (int b0 = 0; b0 < P.K; b0 += 8) {
                     int64_t kid[8];
                     double kw[8];
@@ -451,15 +455,17 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
     }
 }
 
+template <bool kKnn>
 __global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, RayOut RO, const int4* __restrict__ plan,
                                                             const int64_t* __restrict__ eoff, Exact X) {
     if (eoff[C.m] > X.cap) return;
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
-        retain_ray(C, P, ray, RO, plan, eoff, X);
+        retain_ray<kKnn>(C, P, ray, RO, plan, eoff, X);
 }
 
 // Copy the compacted retained candidates to the outputs (ray order).
+template <bool kKnn>
 __global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const int64_t* __restrict__ eoff,
                        Exact X, Outputs O) {
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -480,7 +486,7 @@ __global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const
                 O.r_color[3 * (o + k) + 1] = X.col[3 * (st + k) + 1];
                 O.r_color[3 * (o + k) + 2] = X.col[3 * (st + k) + 2];
             }
-            if (P.emit_knn)
+            if (kKnn)
                 for (int b = 0; b < P.K; b++) {
                     O.r_knn_id[(o + k) * P.K + b] = X.knn_id[(st + k) * P.K + b];
                     O.r_knn_w[(o + k) * P.K + b] = X.knn_w[(st + k) * P.K + b];
@@ -573,7 +579,10 @@ int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     }
     {
         TimedSpan ts("k_sample_exact", s);
-        k_sample_exact<BestT><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
+        if (P.emit_knn)
+            k_sample_exact<BestT, true><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
+        else
+            k_sample_exact<BestT, false><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
         HP_CHECK_LAUNCH("k_sample_exact");
     }
     return HP_OK;
@@ -589,7 +598,11 @@ int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleW
     TimedSpan ts("k_sample_retain", s);
     // one ray per warp: as many warps in flight as the SMs hold (latency-bound)
     const int64_t blocks = (C.m + kWarps - 1) / kWarps;
-    k_sample_retain<<<int(blocks < (1 << 30) ? blocks : (1 << 30)), kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
+    const int grid = int(blocks < (1 << 30) ? blocks : (1 << 30));
+    if (P.emit_knn)
+        k_sample_retain<true><<<grid, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
+    else
+        k_sample_retain<false><<<grid, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
     HP_CHECK_LAUNCH("k_sample_retain");
     return HP_OK;
 }
@@ -712,7 +725,10 @@ extern "C" int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp
         return HP_EINVAL;
     }
     TimedSpan ts("k_emit", s);
-    k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    if (P.emit_knn)
+        k_emit<true><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    else
+        k_emit<false><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
     HP_CHECK_LAUNCH("k_emit");
     return HP_OK;
 }
@@ -742,7 +758,10 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
         return HP_EINVAL;
     }
     TimedSpan ts("k_emit", s);
-    k_emit<<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    if (P.emit_knn)
+        k_emit<true><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    else
+        k_emit<false><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
     HP_CHECK_LAUNCH("k_emit");
     return HP_OK;
 }

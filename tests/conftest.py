@@ -25,3 +25,19 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _device_checks(request):
+    """With HP_CHECKED=1 (and HP_LIB pointing at libhp_b200_checked.so, the
+    `make checked` build): every GPU test must leave no failed device-side
+    bounds / invariant check behind."""
+    yield
+    if os.environ.get("HP_CHECKED") != "1" or "gpu" not in request.keywords:
+        return
+    import torch
+
+    from paper_2404_14044_b200 import _lib
+    torch.cuda.synchronize()
+    lines = _lib.check_failures(reset=True)
+    assert not lines, f"device-side checks failed at source lines {lines}"
