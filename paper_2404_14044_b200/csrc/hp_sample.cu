@@ -399,7 +399,7 @@ __device__ void retain_ray(const Csr& C, const Params& P, int64_t ray, const Ray
         if (keep) {
             const bool mine = (keep >> lane) & 1u;
             const int64_t dst = e0 + nret + __popc(keep & ((1u << lane) - 1));
-            HP_ASSERT(dst < e0 + E && dst <= e0 + j);
+            HP_ASSERT(!mine || (dst < e0 + E && dst <= e0 + j));
             double u = 0.0, c[3] = {0.0, 0.0, 0.0};
             if (mine) {
                 u = X.udf[e0 + j];
