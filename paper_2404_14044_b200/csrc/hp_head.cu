@@ -308,9 +308,10 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
 }
 
 // ---------------------------------------------------------------- classes
-// list 0: rays of 1..min(kHeadSmall, whole) matches (sorted whole by the
-// small configuration), list 1: the longer ones; the empty rays' outputs are
-// written here.
+// Rays whose head is taken whole (q <= whole): list 0 when q <= kHeadSmall
+// (the small sort configuration), else list 1; rays to cut (q > whole):
+// list 2, which k_head_select distributes to lists 0 / 1 by the size of the
+// head it selects.  The empty rays' outputs are written here.
 // With `rays`, output i stands for ray rays[i] (a re-sort of a subset).
 __global__ void k_head_classes(const int64_t* __restrict__ off, const int* __restrict__ rays, int64_t m, int whole,
                                int* __restrict__ lists, int* __restrict__ counts, int* __restrict__ plen,
@@ -321,7 +322,7 @@ __global__ void k_head_classes(const int64_t* __restrict__ off, const int* __res
         if (r < m) {
             const int64_t ri = rays ? rays[r] : r;
             const int64_t q = off[ri + 1] - off[ri];
-            cls = q == 0 ? -1 : (q <= min(kHeadSmall, whole) ? 0 : 1);
+            cls = q == 0 ? -1 : (q > whole ? 2 : (q <= kHeadSmall ? 0 : 1));
             if (q == 0) {
                 plen[r] = 0;
                 facts[r] = -1;
@@ -329,7 +330,7 @@ __global__ void k_head_classes(const int64_t* __restrict__ off, const int* __res
             }
         }
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
+        for (int c = 0; c < 3; c++) {
             const unsigned b = __ballot_sync(0xffffffffu, cls == c);
             if (!b) continue;
             int base = 0;
@@ -353,7 +354,8 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
                                                      const int64_t* __restrict__ soff,
                                                      const RayMeta* __restrict__ meta, int want, int whole,
                                                      const unsigned* __restrict__ sc_key, uint2* __restrict__ sel,
-                                                     const int* __restrict__ list, const int* __restrict__ list_n) {
+                                                     const int* __restrict__ list, const int* __restrict__ list_n,
+                                                     int* __restrict__ lists, int* __restrict__ counts, int64_t m) {
     __shared__ int hist[4][kBins];
     int* H = hist[warp_id()];
     const int lane = lane_id();
@@ -408,6 +410,8 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
             // largest key of bin b (keys above kmax do not occur)
             const unsigned long long kc = (unsigned long long)M.kmin + ((unsigned long long)(b + 1) << sh) - 1ull;
             sel[i] = make_uint2(unsigned(kc < M.kmax ? kc : M.kmax), unsigned(c));
+            const int cls = c <= kHeadSmall ? 0 : 1;  // the sort configuration of this head
+            lists[int64_t(cls) * m + atomicAdd(&counts[cls], 1)] = int(i);
         }
         __syncwarp();
     }
@@ -603,7 +607,7 @@ HeadWs carve_head(Carver& c, int64_t m, int64_t cap) {
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
     w.soff = c.take<int64_t>(m + 1);
     w.meta = c.take<RayMeta>(mm);
-    w.lists = c.take<int>(2 * mm);
+    w.lists = c.take<int>(3 * mm);
     w.counts = c.take<int>(64);
     w.sel = c.take<uint2>(mm);
     w.key = c.take<unsigned>(cap > 0 ? cap : 1);
@@ -685,10 +689,11 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     const int64_t nout = rays ? n : m;  // outputs (rays[i] or i)
     if (nout == 0) return HP_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(w.counts, 0, 2 * sizeof(int), s) != cudaSuccess)
+    if (cudaMemsetAsync(w.counts, 0, 3 * sizeof(int), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_head_sort memset");
     const int* list_small = w.lists;
     const int* list_big = w.lists + nout;
+    const int* list_cut = w.lists + 2 * nout;
     k_head_classes<<<grid_for(nout, 256), 256, 0, s>>>(offsets, rays, nout, whole, w.lists, w.counts, plen, facts,
                                                        cut_t, cut_d);
     HP_CHECK_LAUNCH("k_head_classes");
@@ -698,7 +703,7 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         if (occ_sel < 0) return occ_sel;
         TimedSpan ts("k_head_select", s);
         kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, rays, w.soff, w.meta, want, whole, w.key, w.sel,
-                                                       list_big, w.counts + 1);
+                                                       list_cut, w.counts + 2, w.lists, w.counts, nout);
         HP_CHECK_LAUNCH("k_head_select");
     }
     constexpr auto ksmall = k_head_sort<kHeadSmall, 128>;
