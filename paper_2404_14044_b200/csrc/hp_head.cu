@@ -50,6 +50,9 @@ constexpr int kStage = HP_HEAD_STAGE;  // slots per staged chunk (16 B each)
 #ifndef HP_HEAD_SORT_MINB
 #define HP_HEAD_SORT_MINB 6
 #endif
+#ifndef HP_HEAD_SORT_U
+#define HP_HEAD_SORT_U 8  // keys + slots of a cut ray streamed per thread per round
+#endif
 
 // ---------------------------------------------------------------- bulk copies
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
@@ -484,17 +487,20 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
         for (int j = tid; j <= kCoarse; j += kT) F.chist[j] = 0;
         for (int j = tid; j <= S; j += kT) F.hist[j] = 0;
         __syncthreads();
-        if (!all) {  // stream the keys (4 per thread in flight); stage the selected slots
+        if (!all) {  // stream keys and slots (kU of each per thread in flight); stage the selected slots
+            constexpr int kU = HP_HEAD_SORT_U;
             unsigned kout = 0xffffffffu;
-            for (int e0 = 0; e0 < q; e0 += 4 * kT) {
-                unsigned kv[4];
+            for (int e0 = 0; e0 < q; e0 += kU * kT) {
+                unsigned kv[kU];
+                int sv[kU];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < kU; u++) {
                     const int e = e0 + u * kT + tid;
-                    kv[u] = e < q ? sc_key[so + e] : 0xffffffffu;
+                    kv[u] = e < q ? __ldcs(sc_key + so + e) : 0xffffffffu;
+                    sv[u] = e < q ? __ldcs(sc_slot + so + e) : 0;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < kU; u++) {
                     const int e = e0 + u * kT + tid;
                     const bool in = e < q && kv[u] <= kc;
                     if (e < q && !in) kout = min(kout, kv[u]);
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
                     if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
                     base = __shfl_sync(0xffffffffu, base, 0);
                     HP_ASSERT(!in || base + __popc(b & lanemask_lt()) < S);
-                    if (in) F.slot[base + __popc(b & lanemask_lt())] = sc_slot[so + e];
+                    if (in) F.slot[base + __popc(b & lanemask_lt())] = sv[u];
                 }
             }
             kout = __reduce_min_sync(0xffffffffu, kout);
