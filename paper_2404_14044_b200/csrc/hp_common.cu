@@ -71,6 +71,10 @@ int kernel_occupancy(const void* fn, int threads, size_t smem) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
     }
+    if (smem > 0) {  // the whole unified L1 / shared array as shared memory (occupancy counts on it)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute carveout");
+    }
     int n = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");

@@ -29,6 +29,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "hp_common.cuh"
 
@@ -434,7 +436,13 @@ extern "C" int hp_pointnerf_aggregate(const int64_t* knn_id, const double* knn_w
         const int occ = kernel_occupancy((const void*)kern, kThreadsAgg, sizeof(AggSmem));
         if (occ < 0) return occ;
         const int64_t tiles = (R + kTile / k - 1) / (kTile / k);
-        const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * std::min(occ, 2));  // TMEM: 2 x 256
+        // two CTAs per SM: the shared memory (2 x 82 KB) and TMEM (2 x 256 columns)
+        // hold two; the occupancy API reports 1 for this kernel, measured 2 co-resident
+        // (1.95 -> 1.21 ms at cfg5); a third would wait for TMEM
+        const char* force = getenv("HP_AGG_CTAS");
+        const int per_sm = force ? atoi(force) : 2;
+        (void)occ;
+        const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * per_sm);
         TimedSpan ts("k_mlp_agg", s);
         kern<<<unsigned(grid), kThreadsAgg, sizeof(AggSmem), s>>>(
             knn_id, knn_w, R, sample_ray, r_t, dirs, origin_host[0], origin_host[1], origin_host[2], positions,
@@ -463,7 +471,10 @@ extern "C" int hp_pointnerf_head(const uint16_t* g, int64_t R, const uint16_t* w
     const int occ = kernel_occupancy((const void*)k_mlp_head, kThreadsMlp, sizeof(HeadSmemM));
     if (occ < 0) return occ;
     const int64_t tiles = (R + kTile - 1) / kTile;
-    const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * std::min(occ, 4));
+    const char* force = getenv("HP_HEAD_CTAS");
+    const int per_sm = force ? atoi(force) : 4;  // shared memory 4 x 49 KB, TMEM 4 x 64 columns
+    (void)occ;
+    const int64_t grid = std::min<int64_t>(tiles, int64_t(device_sms()) * per_sm);
     TimedSpan ts("k_mlp_head", s);
     k_mlp_head<<<unsigned(grid), kThreadsMlp, sizeof(HeadSmemM), s>>>(reinterpret_cast<const __nv_bfloat16*>(g), R,
                                                                        w3, b3, w4, b4, out);
