@@ -187,17 +187,24 @@ __global__ void __launch_bounds__(kThreadsAgg) k_agg(const int64_t* __restrict__
     const int per = kTile / K;  // samples per tile
     const int64_t tiles = (R + per - 1) / per;
     constexpr uint32_t kId1 = idesc_bf16(kTile, kHid);
+    // this thread's row of the next tile: its neighbour id is loaded one tile
+    // ahead (the feature / position gathers depend on it)
+    auto row_id = [&](int64_t tl) -> int64_t {
+        const int row = tid & (kTile - 1);
+        const int64_t s = tl * per + row / K;
+        return (tl < tiles && row < per * K && s < R) ? knn_id[s * K + row % K] : -1;
+    };
+    int64_t id_next = row_id(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         // ---- the tile's input rows, straight into the canonical layout
         {
             const int row = tid & (kTile - 1), part = tid >> 7;
             const int64_t s = tile * per + row / K;
-            const int k = row % K;
             float x[32];
 #pragma unroll
             for (int i = 0; i < 32; i++) x[i] = 0.0f;
-            const bool live = row < per * K && s < R;
-            const int64_t id = live ? knn_id[s * K + k] : -1;
+            const int64_t id = id_next;
+            id_next = row_id(tile + gridDim.x);
             if (id >= 0 && part == 0) {
                 const uint4* fp = reinterpret_cast<const uint4*>(feat + id * kFeat);
 #pragma unroll
