@@ -193,7 +193,10 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
  * none).  hp_sample_run_prefix consumes them.  rays (int32 [n], or NULL for
  * all m rays): re-sort only these rays of the same count pass (e.g. with a
  * longer `want` for rays the sampler flagged); output i (head_off[i], plen[i],
- * facts[i], cuts[i]) then stands for ray rays[i]. */
+ * facts[i], cuts[i]) then stands for ray rays[i].  sampler + head_u (both
+ * or neither): the sampler's bound factors of every head entry (float, next
+ * to head_t; -1 where not precomputed), which hp_sample_run_prefix then
+ * multiplies instead of recomputing them (same results). */
 int hp_head_workspace_bytes(int64_t m, int64_t capacity, size_t* bytes);
 int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
                   int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,
@@ -203,8 +206,8 @@ int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w
 int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
                  const int64_t* offsets, const int32_t* rays, int64_t n, const int64_t* head_off, int32_t want,
                  int32_t whole, double* head_t, int32_t* head_ids, double* head_dist, int32_t* plen,
-                 int32_t* facts, double* cut_t, double* cut_d, int64_t capacity, void* workspace,
-                 size_t workspace_bytes, hp_stream_t stream);
+                 int32_t* facts, double* cut_t, double* cut_d, const hp_sampler_params* sampler, float* head_u,
+                 int64_t capacity, void* workspace, size_t workspace_bytes, hp_stream_t stream);
 
 /* Upper bounds of the match counts (the slots pass 1 will test per ray),
  * exclusive-scanned into bound_off [m+1] (bound_off[m] = the scratch pass 1
@@ -270,6 +273,7 @@ typedef struct hp_sample_prefix {
     const double* dist;
     const double* cut_t;   /* [m] */
     const double* cut_d;   /* [m] */
+    const float* u;        /* NULL, or hp_head_sort's head_u */
 } hp_sample_prefix;
 int hp_sample_run_prefix(const int64_t* offsets, int64_t m, const hp_sample_prefix* prefix,
                          int64_t exact_capacity, const double* slopes, const int32_t* query_facts,

@@ -42,7 +42,7 @@ class SamplerParams(ctypes.Structure):
 
 class SamplePrefix(ctypes.Structure):
     _fields_ = [("start", c_p), ("length", c_p), ("ids", c_p), ("t", c_p), ("dist", c_p),
-                ("cut_t", c_p), ("cut_d", c_p)]
+                ("cut_t", c_p), ("cut_d", c_p), ("u", c_p)]
 
 
 _SIGNATURES = {
@@ -68,7 +68,8 @@ _SIGNATURES = {
                                      c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_i64,
                                      c_p, c_size, c_p]),
     "hp_head_sort": (ctypes.c_int, [Layout, c_p, c_p, c_i64, c_p, c_p, c_i64, c_p, ctypes.c_int32, ctypes.c_int32,
-                                    c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_size, c_p]),
+                                    c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.POINTER(SamplerParams), c_p, c_i64, c_p,
+                                    c_size, c_p]),
     "hp_ray_grid": (ctypes.c_int, [ctypes.POINTER(Camera), c_i64, c_i64, c_p, c_p, ctypes.c_double,
                                    ctypes.c_double, c_p, c_p, c_p]),
     "hp_render": (ctypes.c_int, [ctypes.c_int, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,

@@ -34,6 +34,7 @@
 // cuts handed to the sampler are lower bounds of the left-out t and dist
 // (hp_sample.cu only relies on "every left-out t >= cut_t, dist >= cut_d").
 #include "hp_query_core.cuh"
+#include "hp_sample_core.cuh"
 
 namespace hp {
 namespace {
@@ -49,6 +50,9 @@ constexpr int kStage = HP_HEAD_STAGE;  // slots per staged chunk (16 B each)
 #endif
 #ifndef HP_HEAD_SORT_MINB
 #define HP_HEAD_SORT_MINB 6
+#endif
+#ifndef HP_HEAD_U_MAX
+#define HP_HEAD_U_MAX 384  // bound factors precomputed for the first this many head entries
 #endif
 #ifndef HP_HEAD_SORT_U
 #define HP_HEAD_SORT_U 8  // keys + slots of a cut ray streamed per thread per round
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
     const RayMeta* __restrict__ meta, const unsigned* __restrict__ sc_key, const int* __restrict__ sc_slot,
     const uint2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n, int whole,
     double* __restrict__ head_t, int* __restrict__ head_id, double* __restrict__ head_d, int* __restrict__ plen,
-    int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d) {
+    int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d, Params SP,
+    float* __restrict__ head_u) {
     extern __shared__ __align__(16) unsigned char dyn[];
     HeadSmem<kCap>& F = *reinterpret_cast<HeadSmem<kCap>*>(dyn);
     const double4* __restrict__ rel4 = reinterpret_cast<const double4*>(L.rel4);
@@ -549,11 +554,18 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
         int cnt = 0;
         bool bad = false;
         unsigned long long md = ~0ull;
-        for (int p = tid; p < S; p += kT) {
+        constexpr int kPer = kCap / kT;
+        double tv[kPer], dv[kPer];  // this thread's head entries, for the bound factors below
+#pragma unroll
+        for (int c = 0; c < kPer; c++) {
+            const int p = tid + c * kT;
+            if (p >= S) break;
             const int e = F.perm[p];
             const double t = F.t[e], dd = F.d2[e];
             if (p < Lh) {
                 const double d = sqrt(dd);
+                tv[c] = t;
+                dv[c] = d;
                 head_t[ho + p] = t;
                 head_id[ho + p] = F.id[e];
                 head_d[ho + p] = d;
@@ -591,6 +603,38 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
             }
             cut_t[i] = ct;
             cut_d[i] = cd;
+        }
+        // The sampler's bound factors u_j >= fl(1 - alpha_j) for the head (the
+        // plan's bound chain then only multiplies them): when every candidate
+        // is eligible from the start (facts >= K, so j* = 0), u_j is
+        // bound_factor_ring's (hp_sample_core.cuh) over the K candidates ending
+        // at j, here from the sorted head in shared memory; rounded up to
+        // float (still an upper bound); -1 where a member is not in j's pool.
+        if (head_u && SP.K <= 32 && Lh >= SP.K && !F.fbad && F.fcount >= SP.K) {  // uniform in the CTA
+            __syncthreads();  // F.t / F.d2 in element order are no longer read
+#pragma unroll
+            for (int c = 0; c < kPer; c++) {
+                const int p = tid + c * kT;
+                if (p < Lh) {
+                    F.t[p] = tv[c];
+                    F.d2[p] = dv[c];  // dist, in head order
+                }
+            }
+            __syncthreads();
+            const double slope = __ldg(slopes + r);
+            const int nu = min(Lh, HP_HEAD_U_MAX);  // the chain rarely needs more; the plan computes the rest
+            for (int p = tid; p < nu; p += kT) {
+                const double tj = F.t[p], rj = dmul(slope, tj);
+                const int i0 = p >= SP.K - 1 ? p - SP.K + 1 : 0;
+                double sum = 0.0;
+                bool ok = true;
+                for (int k = 0; k < SP.K; k++) {
+                    const double di = F.d2[i0 + k];
+                    ok &= !(di > rj);
+                    sum = dadd(sum, dadd(fabs(dsub(F.t[i0 + k], tj)), di));
+                }
+                head_u[ho + p] = ok ? __double2float_ru(factor_from_sum(sum, SP.K, SP)) : -1.0f;
+            }
         }
         __syncthreads();
     }
@@ -679,7 +723,8 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
 extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const double* slopes, int64_t m,
                             const int64_t* offsets, const int32_t* rays, int64_t n, const int64_t* head_off,
                             int32_t want, int32_t whole, double* head_t, int32_t* head_ids, double* head_dist,
-                            int32_t* plen, int32_t* facts, double* cut_t, double* cut_d, int64_t capacity,
+                            int32_t* plen, int32_t* facts, double* cut_t, double* cut_d,
+                            const hp_sampler_params* sampler, float* head_u, int64_t capacity,
                             void* workspace, size_t workspace_bytes, hp_stream_t stream) {
     if (m < 0 || want < 1 || want > kHeadCap || whole < want || whole > kHeadCap || (rays && (n < 0 || n > m)) ||
         (m > 0 && (!dirs || !slopes || !facts || !plen || !cut_t || !cut_d || !layout.rel4))) {
@@ -712,6 +757,16 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
                                                        list_cut, w.counts + 2, w.lists, w.counts, nout);
         HP_CHECK_LAUNCH("k_head_select");
     }
+    Params SP{};
+    if (sampler && head_u) {
+        SP.K = sampler->k_neighbors;
+        SP.gamma = sampler->gamma;
+        SP.beta2 = sampler->beta2;
+        SP.inv_beta2_up = nextafter(1.0 / sampler->beta2, INFINITY);  // as hp_sample.cu to_params
+        SP.inv_k_up = nextafter(1.0 / double(SP.K), INFINITY);
+    } else {
+        head_u = nullptr;
+    }
     constexpr auto ksmall = k_head_sort<kHeadSmall, 128>;
     constexpr auto kbig = k_head_sort<kHeadCap, 256>;
     const int occ_small = kernel_occupancy((const void*)ksmall, 128, sizeof(HeadSmem<kHeadSmall>));
@@ -721,11 +776,11 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     TimedSpan ts("k_head_sort", s);
     ksmall<<<device_sms() * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
         layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts,
-        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
+        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u);
     HP_CHECK_LAUNCH("k_head_sort small");
     kbig<<<device_sms() * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
         layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big,
-        w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d);
+        w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u);
     HP_CHECK_LAUNCH("k_head_sort");
     return HP_OK;
 }

@@ -93,6 +93,7 @@ struct Csr {
     const double* cut_t;
     const double* cut_d;
     int32_t* flag;  // [m + 1]: 1 = the ray needs its full CSR; flag[m] = count
+    const float* head_u;  // optional precomputed bound factors (hp_head_sort), at start[r]
     __device__ __forceinline__ int64_t lo(int64_t r) const { return start ? start[r] : off[r]; }
     __device__ __forceinline__ int n(int64_t r) const { return start ? len[r] : int(off[r + 1] - off[r]); }
     __device__ __forceinline__ int qtrue(int64_t r) const { return int(off[r + 1] - off[r]); }
@@ -206,16 +207,28 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
             }
             cp_commit();
         };
+        if (!(C.head_u && jstar == 0 && P.K <= 32)) {
 #pragma unroll
-        for (int a = 0; a < HP_PLAN_AHEAD; a++) fetch(32 * a);
+            for (int a = 0; a < HP_PLAN_AHEAD; a++) fetch(32 * a);
+        }
 #else
         // this lane's (t, ds) of the current chunk, loaded one chunk ahead
         double tn = lane < q ? ldg(T + lane) : 0.0, dn = lane < q ? ldg(DS + lane) : 0.0;
 #endif
+        // precomputed factors (hp_head_sort) when every candidate is eligible
+        const float* HU = (C.head_u && jstar == 0 && P.K <= 32) ? C.head_u + lo : nullptr;
+        float hu_next = (HU && lane < q) ? __ldg(HU + lane) : 1.0f;  // one chunk ahead
         for (int c0 = 0; c0 < q; c0 += 32) {
             const int j = c0 + lane;
             double u = 1.0;
-            if (P.K <= 32) {
+            if (HU) {
+                const float hu = hu_next;
+                hu_next = j + 32 < q ? __ldg(HU + j + 32) : 1.0f;
+                if (j < q) {
+                    u = double(hu);
+                    if (u < 0.0) u = bound_factor(V, q, j, jstar, slope, P);
+                }
+            } else if (P.K <= 32) {
 #if HP_PLAN_CPASYNC
                 cp_wait<HP_PLAN_AHEAD - 1>();  // chunk c0 has landed
                 __syncwarp();
@@ -557,6 +570,7 @@ Params to_params(const hp_sampler_params* p) {
     // 1/beta2 rounded toward +inf on the host (fesetround-free): next double up
     const double r = 1.0 / p->beta2;
     P.inv_beta2_up = nextafter(r, INFINITY);
+    P.inv_k_up = nextafter(1.0 / double(P.K), INFINITY);
     return P;
 }
 
@@ -683,7 +697,7 @@ extern "C" int hp_sample_run_prefix(const int64_t* offsets, int64_t m, const hp_
     if (cudaMemsetAsync(flagged + m, 0, sizeof(int32_t), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_sample_run_prefix memset");
     Csr C{offsets, nullptr, pre->t, pre->dist, slopes, colors, m, query_facts,
-          pre->start, pre->length, pre->ids, pre->cut_t, pre->cut_d, flagged};
+          pre->start, pre->length, pre->ids, pre->cut_t, pre->cut_d, flagged, pre->u};
     Params P = to_params(p);
     if (m > 0) {
         HP_TRY(dispatch_exact(C, P, w, s));

@@ -19,6 +19,7 @@ struct Params {
     int eps_mode, want_color, exact_t_end, emit_knn;
     double beta2, gamma, eps, tau_min;
     double inv_beta2_up;  // 1 / beta2 rounded up (bound factors only)
+    double inv_k_up;      // 1 / K rounded up (bound factors only)
 };
 
 __device__ __forceinline__ bool kless(double d2a, int ia, double d2b, int ib) {
@@ -316,7 +317,9 @@ __device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, boo
 // 1 - 2^-20 against expf's 2-ulp error).  Every later operation is monotone,
 // so U_{j+1} = U_j * u_j in the reference's order dominates T_j.
 __device__ __forceinline__ double factor_from_sum(double sum, int ksel, const Params& P) {
-    const double udf_up = __ddiv_rn(dmul(sum, 1.0 + 1e-12), double(ksel));
+    // x / ksel bounded above without a division: RU(x * RU(1 / ksel)) >= x / ksel
+    const double inv_up = ksel == P.K ? P.inv_k_up : __drcp_ru(double(ksel));
+    const double udf_up = __dmul_ru(dmul(sum, 1.0 + 1e-12), inv_up);
     const double y = dmul(dmul(udf_up, udf_up), P.inv_beta2_up);  // >= fl(udf^2) / beta^2
     const float e = expf(-__double2float_ru(y));
     const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));

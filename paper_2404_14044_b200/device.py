@@ -278,10 +278,11 @@ class QueryPrefix:
     of the matches left out (``cut_t``, ``cut_d``), and the sampler's facts
     over the head.  Keeps the query workspace alive."""
 
-    def __init__(self, offsets, probes, scanned, start, length, t, ids, dist, cut_t, cut_d, facts, ws):
+    def __init__(self, offsets, probes, scanned, start, length, t, ids, dist, cut_t, cut_d, facts, ws, u=None):
         self.offsets, self.probes, self.scanned = offsets, probes, scanned
         self.start, self.length, self.t, self.ids, self.dist = start, length, t, ids, dist
         self.cut_t, self.cut_d, self.facts = cut_t, cut_d, facts
+        self.u = u  # precomputed bound factors (float32, next to t) or None
         self._ws = ws
 
     def struct(self) -> _lib.SamplePrefix:
@@ -289,11 +290,14 @@ class QueryPrefix:
         sp.start, sp.length, sp.ids = self.start.data_ptr(), self.length.data_ptr(), self.ids.data_ptr()
         sp.t, sp.dist = self.t.data_ptr(), self.dist.data_ptr()
         sp.cut_t, sp.cut_d = self.cut_t.data_ptr(), self.cut_d.data_ptr()
+        sp.u = self.u.data_ptr() if self.u is not None else None
         return sp
 
 
 PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "400"))  # head length the sampler usually needs
 HEAD_CAP = 1024  # longest head (hp_head.cu kHeadCap)
+# HP_HEAD_FACTORS=1: heads carry the sampler's bound factors (measured: the sort pays more than the plan saves)
+HEAD_FACTORS = os.environ.get("HP_HEAD_FACTORS", "0") == "1"
 # rays of at most this many matches are sorted whole; longer ones are cut near PREFIX_WANT
 HEAD_WHOLE = int(os.environ.get("HP_HEAD_WHOLE", "512"))
 
@@ -342,18 +346,19 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
 
 def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
                  t_far: torch.Tensor, slopes: torch.Tensor, want: int | None = None, footprint: bool = True,
-                 max_scratch: int | None = None, whole: int | None = None) -> QueryPrefix:
+                 max_scratch: int | None = None, whole: int | None = None, sampler_cfg=None) -> QueryPrefix:
     """The query for callers that only want samples (hp_head_count +
     hp_head_sort): each ray's head of matches in (t, id) order, without the
     CSR of all matches."""
     pixels, dirs = pixels.contiguous(), dirs.contiguous()
     return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch), dirs,
-                 slopes, want, whole)
+                 slopes, want, whole, sampler_cfg)
 
 
-def _head(index, counted, dirs, slopes, want=None, whole=None) -> QueryPrefix:
+def _head(index, counted, dirs, slopes, want=None, whole=None, sampler_cfg=None) -> QueryPrefix:
     """hp_head_sort after :func:`_count_head` (want / whole default to
-    PREFIX_WANT / HEAD_WHOLE, read at call time)."""
+    PREFIX_WANT / HEAD_WHOLE, read at call time).  With ``sampler_cfg`` the
+    heads carry the sampler's precomputed bound factors."""
     want = PREFIX_WANT if want is None else want
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
@@ -365,15 +370,18 @@ def _head(index, counted, dirs, slopes, want=None, whole=None) -> QueryPrefix:
     ht = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hd = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hi = torch.empty(max(hcap, 1), dtype=torch.int32, device=dev)
+    sp = sampler_params(sampler_cfg, False, True) if (sampler_cfg is not None and HEAD_FACTORS) else None
+    hu = torch.empty(max(hcap, 1), dtype=torch.float32, device=dev) if sp is not None else None
     whole = max(int(want), min(HEAD_WHOLE if whole is None else int(whole), HEAD_CAP))
     _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(offsets), None, 0,
                                 _ptr(head_off), int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen),
-                                _ptr(fa), _ptr(cut[0]), _ptr(cut[1]), cap, _ptr(ws), nb, _stream()))
+                                _ptr(fa), _ptr(cut[0]), _ptr(cut[1]), ctypes.byref(sp) if sp is not None else None,
+                                _ptr(hu), cap, _ptr(ws), nb, _stream()))
     _mark("query.prefix")
-    pre = QueryPrefix(offsets, probes, scanned, head_off[:m], plen, ht, hi, hd, cut[0], cut[1], fa, ws)
+    pre = QueryPrefix(offsets, probes, scanned, head_off[:m], plen, ht, hi, hd, cut[0], cut[1], fa, ws, hu)
     pre.total = total
     pre.want, pre.whole = int(want), whole
-    pre._sort_args = (index, dirs, slopes, nb, cap)
+    pre._sort_args = (index, dirs, slopes, nb, cap, sp)
     return pre
 
 
@@ -384,7 +392,7 @@ def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whol
     Returns a :class:`QueryPrefix` over just those rays (their own offsets,
     counts unchanged)."""
     lib = _lib.load(require_device=True)
-    index, dirs, slopes, nb, cap = pre._sort_args
+    index, dirs, slopes, nb, cap, sp = pre._sort_args
     dev = pre.offsets.device
     m = int(pre.offsets.shape[0]) - 1
     n = int(rays.numel())
@@ -400,12 +408,14 @@ def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whol
     ht = torch.empty(cap_h, dtype=torch.float64, device=dev)
     hd = torch.empty(cap_h, dtype=torch.float64, device=dev)
     hi = torch.empty(cap_h, dtype=torch.int32, device=dev)
+    hu = torch.empty(cap_h, dtype=torch.float32, device=dev) if sp is not None else None
     whole = max(int(want), min(int(whole), HEAD_CAP))
     _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(pre.offsets), _ptr(r32), n,
                                 _ptr(head_off), int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa),
-                                _ptr(cut[0]), _ptr(cut[1]), cap, _ptr(pre._ws), nb, _stream()))
+                                _ptr(cut[0]), _ptr(cut[1]), ctypes.byref(sp) if sp is not None else None, _ptr(hu),
+                                cap, _ptr(pre._ws), nb, _stream()))
     sub = QueryPrefix(sub_off, pre.probes[rays], pre.scanned[rays], head_off[:n], plen, ht, hi, hd, cut[0], cut[1],
-                      fa, pre._ws)
+                      fa, pre._ws, hu)
     sub.total = None
     sub.want, sub.whole = int(want), whole
     sub._sort_args = None
@@ -413,7 +423,7 @@ def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whol
 
 
 def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix: bool | None = None,
-                max_scratch: int | None = None, want: int | None = None):
+                max_scratch: int | None = None, want: int | None = None, sampler_cfg=None):
     """The query of a sampling frame: the heads (``prefix`` True or None;
     returns a :class:`QueryPrefix`) or the full CSR with facts (``prefix``
     False; returns the 7-tuple of :func:`query`)."""
@@ -421,7 +431,7 @@ def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix:
     if prefix is False:
         return _fill(index, _count(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), slopes, True)
     return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), dirs, slopes,
-                 want)
+                 want, None, sampler_cfg)
 
 
 def sampler_params(cfg, want_color: bool, exact_t_end: bool, emit_knn: bool = False) -> _lib.SamplerParams:

@@ -94,9 +94,10 @@ def test_prefix_on_dense_rays():
         assert np.mean(plen[counts > want] >= 0.75 * want) > 0.9
 
 
-def _prefix_frame(idx, rays, sc, colors, exact_t_end, want, whole=None):
-    """prefix-mode sampling with the flagged rays re-run on the full path"""
-    pre = dv.query_prefix(idx, *rays, want=want, whole=whole)
+def _prefix_frame(idx, rays, sc, colors, exact_t_end, want, whole=None, factors=False):
+    """prefix-mode sampling with the flagged rays re-run on the full path
+    (``factors``: the heads carry precomputed bound factors)"""
+    pre = dv.query_prefix(idx, *rays, want=want, whole=whole, sampler_cfg=sc if factors else None)
     *s, flagged, n_flagged = dv.sample_prefix(pre, rays[4], sc, colors, exact_t_end)
     fl = flagged.cpu().numpy()
     assert int((fl != 0).sum()) == n_flagged
@@ -119,7 +120,8 @@ def _assert_same(a, b):
 @pytest.mark.parametrize("exact_t_end", [True, False])
 @pytest.mark.parametrize("want", [1, 9, 512])
 @pytest.mark.parametrize("whole", ["want", 1024])
-def test_prefix_sampling_equals_full(name, exact_t_end, want, whole):
+@pytest.mark.parametrize("factors", [False, True])
+def test_prefix_sampling_equals_full(name, exact_t_end, want, whole, factors):
     _, cloud, cam, cfg, tn, tf, stride, samplers = gu.get_case(name)
     dev = torch.device("cuda")
     idx = dv.build(torch.from_numpy(cloud.positions).to(dev), cam, cfg.pad)
@@ -132,7 +134,8 @@ def test_prefix_sampling_equals_full(name, exact_t_end, want, whole):
         sc = gu.sampler_config(sname)
         for col in ((colors, None) if sname == "default" else (colors,)):
             full = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, col, exact_t_end=exact_t_end, facts=q[6])
-            got, _ = _prefix_frame(idx, rays, sc, col, exact_t_end, want, want if whole == "want" else whole)
+            got, _ = _prefix_frame(idx, rays, sc, col, exact_t_end, want, want if whole == "want" else whole,
+                                   factors)
             _assert_same(got, full)
 
 
@@ -157,8 +160,9 @@ def test_prefix_sampling_on_dense_rays(k, mode, gamma, exact_t_end):
     full = dv.sample(q[0], q[1], q[2], q[3], rays[4], sc, colors, exact_t_end=exact_t_end, facts=q[6])
     seen = []
     for want, whole in ((16, 16), (16, 1024), (64, 64), (512, 512), (512, 1024)):
-        got, nf = _prefix_frame(idx, rays, sc, colors, exact_t_end, want, whole)
-        _assert_same(got, full)
+        for factors in (False, True):
+            got, nf = _prefix_frame(idx, rays, sc, colors, exact_t_end, want, whole, factors)
+            _assert_same(got, full)
         seen.append(nf)
     assert seen[0] > 0  # the small heads do send rays to the full path
 
