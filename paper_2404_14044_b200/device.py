@@ -370,7 +370,7 @@ def _head(index, counted, dirs, slopes, want=None, whole=None, sampler_cfg=None)
     ht = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hd = torch.empty(max(hcap, 1), dtype=torch.float64, device=dev)
     hi = torch.empty(max(hcap, 1), dtype=torch.int32, device=dev)
-    sp = sampler_params(sampler_cfg, False, True) if (sampler_cfg is not None and HEAD_FACTORS) else None
+    sp = sampler_params(sampler_cfg, False, True) if sampler_cfg is not None else None
     hu = torch.empty(max(hcap, 1), dtype=torch.float32, device=dev) if sp is not None else None
     whole = max(int(want), min(HEAD_WHOLE if whole is None else int(whole), HEAD_CAP))
     _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(offsets), None, 0,

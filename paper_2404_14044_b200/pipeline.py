@@ -223,7 +223,8 @@ def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, ex
 
 def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None,
                  emit_knn=False):
-    pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes, sampler_cfg=sampler_cfg)
+    pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes,
+                              sampler_cfg=sampler_cfg if device.HEAD_FACTORS else None)
     return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget,
                           emit_knn)
 
@@ -238,7 +239,7 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
         bytes_per_match=BYTES_PER_MATCH_PREFIX if prefix else BYTES_PER_MATCH)
     try:
         q = device.query_frame(idx, pixels, dirs, t_near, t_far, slopes, prefix=prefix, max_scratch=budget,
-                               sampler_cfg=sampler_cfg)
+                               sampler_cfg=sampler_cfg if device.HEAD_FACTORS else None)
     except device.MatchBudgetExceeded:
         # too big for one pass: ray chunks (prefix mode unless turned off --
         # such frames are dominated by long rays)
