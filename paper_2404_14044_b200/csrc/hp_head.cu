@@ -42,9 +42,10 @@ namespace {
 constexpr int kHeadCap = 1024;   // longest head; rays up to this are sorted whole
 constexpr int kHeadSmall = 512;  // rays up to this: a smaller, denser CTA configuration
 #ifndef HP_HEAD_STAGE
-#define HP_HEAD_STAGE 512
+#define HP_HEAD_STAGE 1024
 #endif
 constexpr int kStage = HP_HEAD_STAGE;  // slots per staged chunk (16 B each)
+constexpr int kMaxPieces = 8;          // row pieces per chunk
 #ifndef HP_HEAD_MINB
 #define HP_HEAD_MINB 4
 #endif
@@ -94,8 +95,9 @@ __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1
 // bit b = parity of buffer b's next completion).  Chunk i + 1 is in flight
 // while chunk i is tested.
 template <class Issue, class Test, class Tab, class Done>
-__device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, unsigned& phase, int G, const hp_query_layout L,
-                                  int64_t wp, int s, const QCam& QC, Issue issue, Test test, Tab tab, Done done) {
+__device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kMaxPieces], int* npieces,
+                                  unsigned& phase, int G, const hp_query_layout L, int64_t wp, int s,
+                                  const QCam& QC, Issue issue, Test test, Tab tab, Done done) {
     const int tid = threadIdx.x, warp = warp_id();
     const int pad = (s - 1) / 2;
     for (int yb = S.v0; yb < S.v1; yb += kRowsMax) {
@@ -130,39 +132,53 @@ __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, unsigned& phase, 
         for (int row = tid; row < nrows; row += kThreads)
             if (S.slo[row] > S.shi[row]) S.slo[row] = S.shi[row] = 0;  // nothing staged
         __syncthreads();
-        int row = 0, c0 = S.slo[0];
-        auto advance = [&](int& rw, int& cc) {
-            cc += kStage;
-            while (rw < nrows && cc >= S.shi[rw]) {
-                rw++;
-                if (rw < nrows) cc = S.slo[rw];
+        // Chunks of up to kStage slots packed from consecutive rows' staged
+        // ranges ("pieces"; a row longer than the space left is split), so a
+        // chunk barrier covers several rows of work.  Thread 0 plans chunk
+        // i + 1 (its pieces in shared memory, one bulk copy per piece on the
+        // buffer's mbarrier) while chunk i is tested.
+        int prow = 0, pc = S.slo[0];  // thread 0's cursor: next slot to stage
+        auto plan_issue = [&](int b) {
+            int n = 0, off = 0;
+            while (prow < nrows && n < kMaxPieces && off < kStage) {
+                if (pc >= S.shi[prow]) {
+                    if (++prow < nrows) pc = S.slo[prow];
+                    continue;
+                }
+                const int take = min(S.shi[prow] - pc, kStage - off);
+                pieces[b][n] = make_int4(prow, pc, pc + take, off);
+                n++;
+                off += take;
+                pc += take;
+            }
+            npieces[b] = n;
+            if (n) {
+                mbar_arrive_tx(&bar[b], unsigned(off) * 16u);
+                for (int i = 0; i < n; i++) issue(b, pieces[b][i].w, pieces[b][i].y, pieces[b][i].z);
             }
         };
-        if (c0 >= S.shi[0]) {  // empty first row(s)
-            c0 -= kStage;
-            advance(row, c0);
-        }
         int buf = 0;
-        if (row < nrows && tid == 0) issue(0, c0, min(c0 + kStage, S.shi[row]));
-        while (row < nrows) {
-            int nrow = row, nc0 = c0;
-            advance(nrow, nc0);
-            if (nrow < nrows && tid == 0) issue(buf ^ 1, nc0, min(nc0 + kStage, S.shi[nrow]));
+        if (tid == 0) plan_issue(0);
+        __syncthreads();
+        while (npieces[buf] > 0) {
+            if (tid == 0) plan_issue(buf ^ 1);
             mbar_wait(&bar[buf], (phase >> buf) & 1u);
             phase ^= 1u << buf;
-            const int c1 = min(c0 + kStage, S.shi[row]);
-            for (int g = warp; g < G; g += kWarps) {
-                const int lo = max(S.rlo[row][g], c0), hi = min(S.rhi[row][g], c1);
-                if (lo < hi) {  // warp-uniform
-                    test(buf, g, lo, hi, c0);
-                    done(g);
+            const int np = npieces[buf];
+            for (int i = 0; i < np; i++) {
+                const int4 pcs = pieces[buf][i];  // (row, a, b, smem offset)
+                for (int g = warp; g < G; g += kWarps) {
+                    const int lo = max(S.rlo[pcs.x][g], pcs.y), hi = min(S.rhi[pcs.x][g], pcs.z);
+                    if (lo < hi) {  // warp-uniform
+                        test(buf, g, lo, hi, pcs.y - pcs.w);
+                        done(g);
+                    }
                 }
             }
-            __syncthreads();  // buffer `buf` is refilled two chunks later
-            row = nrow;
-            c0 = nc0;
+            __syncthreads();  // buffer `buf` is refilled two chunks later; npieces[buf ^ 1] is visible
             buf ^= 1;
         }
+        __syncthreads();  // every thread has read npieces before the next batch plans over it
     }
 }
 
@@ -170,6 +186,8 @@ struct HeadScanSmem {
     GroupHead head;
     float4 pf[2][kStage];
     uint64_t bar[2];
+    int4 pieces[2][kMaxPieces];  // (row, a, b, smem offset) of each buffer's chunk
+    int npieces[2];
     int fill[kGroupMax], scn[kGroupMax], bad[kGroupMax];
     unsigned kmin[kGroupMax], kmax[kGroupMax];
     int64_t off[kGroupMax], end[kGroupMax];
@@ -216,11 +234,9 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
         unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's key bounds for the current ray
         int lbad = 0;
         stream_group_bulk(
-            S.head, S.bar, phase, G, L, wp, s, QC,
-            [&](int buf, int c0, int c1) {
-                const unsigned bytes = unsigned(c1 - c0) * 16u;
-                mbar_arrive_tx(&S.bar[buf], bytes);
-                bulk_g2s(&S.pf[buf][0], L.relf + 4 * int64_t(c0), bytes, &S.bar[buf]);
+            S.head, S.bar, S.pieces, S.npieces, phase, G, L, wp, s, QC,
+            [&](int buf, int off, int c0, int c1) {  // one piece: slots [c0, c1) to pf[buf][off..]
+                bulk_g2s(&S.pf[buf][off], L.relf + 4 * int64_t(c0), unsigned(c1 - c0) * 16u, &S.bar[buf]);
             },
             [&](int buf, int g, int lo, int hi, int c0) {
                 const RayParams& rp = S.head.ray[g];
