@@ -651,6 +651,9 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
                 }
                 head_u[ho + p] = ok ? __double2float_ru(factor_from_sum(sum, SP.K, SP)) : -1.0f;
             }
+            for (int p = nu + tid; p < Lh; p += kT) head_u[ho + p] = -1.0f;  // the plan computes these
+        } else if (head_u) {
+            for (int p = tid; p < Lh; p += kT) head_u[ho + p] = -1.0f;
         }
         __syncthreads();
     }
