@@ -625,10 +625,10 @@ def run_ours(args, w, rank, world, dist):
         "k_head_scan": 64 * m_loc + 4 * (P + 1) + 16 * n_in + 8 * q_loc + 56 * m_loc,
         # the cut rays' keys (4 B / match) in, per-ray cut out
         "k_head_select": 4 * q_cut + 8 * m_loc,
-        # slots of whole rays, keys of cut rays + slots of the staged, exact
+        # slots of whole rays, keys + slots of cut rays (streamed together), exact
         # records (32 B / point, once), heads out (t, id32, dist: 20 B) and
         # per-ray inputs / outputs
-        "k_head_sort": 4 * q_whole + 4 * q_cut + 4 * plen + 32 * n_in + 20 * plen + 112 * hit,
+        "k_head_sort": 4 * q_whole + 8 * q_cut + 32 * n_in + 20 * plen + 112 * hit,
         "k_sample_plan": 8 * (m_loc + 1) + 16 * plen + 8 * m_loc + 24 * m_loc,
         "k_emit": 8 * (m_loc + 1) + 52 * r_loc + 24 * r_loc + 72 * r_loc,
     }

@@ -23,6 +23,12 @@ SPANS = {
                            "k_query_sort_parts<8192, 1024>"],
     "k_query_prefix": ["k_query_prefix<512, 128>", "k_query_prefix<1024, 256>"],
     "k_prefix_select": ["k_prefix_select<1024, 1024>"],
+    "k_head_scan": ["k_head_scan"],
+    "k_head_select": ["k_head_select<1024>"],
+    "k_head_sort": ["k_head_sort<512, 128>", "k_head_sort<1024, 256>"],
+    "k_query_bound": ["k_query_bound"],
+    "k_mlp_agg": ["k_agg<8>"],
+    "k_mlp_head": ["k_mlp_head"],
     "k_sample_plan": ["k_sample_plan"],
     "k_sample_exact": ["k_sample_exact"],
     "k_sample_retain": ["k_sample_retain"],
