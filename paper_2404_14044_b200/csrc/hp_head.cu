@@ -376,7 +376,9 @@ template <int kBins>
 __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__ off, const int* __restrict__ rays,
                                                      const int64_t* __restrict__ soff,
                                                      const RayMeta* __restrict__ meta, int want, int whole,
-                                                     const unsigned* __restrict__ sc_key, uint2* __restrict__ sel,
+                                                     const unsigned* __restrict__ sc_key,
+                                                     const int* __restrict__ sc_slot, const int64_t* __restrict__ hoff,
+                                                     int* __restrict__ stage, uint4* __restrict__ sel,
                                                      const int* __restrict__ list, const int* __restrict__ list_n,
                                                      int* __restrict__ lists, int* __restrict__ counts, int64_t m) {
     __shared__ int hist[4][kBins];
@@ -417,6 +419,8 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
         const int incl = warp_incl_scan(sum);
         const unsigned hit = __ballot_sync(0xffffffffu, incl >= want);
         const int owner = __ffs(hit) - 1;  // exists: q > whole >= want
+        unsigned kcut = 0;
+        int cnt = 0;
         if (lane == owner) {
             int c = incl - sum, b = lane * kPer;
             for (int j = 0; j < kPer; j++) {
@@ -432,8 +436,41 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
             }
             // largest key of bin b (keys above kmax do not occur)
             const unsigned long long kc = (unsigned long long)M.kmin + ((unsigned long long)(b + 1) << sh) - 1ull;
-            sel[i] = make_uint2(unsigned(kc < M.kmax ? kc : M.kmax), unsigned(c));
-            const int cls = c <= kHeadSmall ? 0 : 1;  // the sort configuration of this head
+            kcut = unsigned(kc < M.kmax ? kc : M.kmax);
+            cnt = c;
+        }
+        kcut = __shfl_sync(0xffffffffu, kcut, owner);
+        cnt = __shfl_sync(0xffffffffu, cnt, owner);
+        // the selected pairs' slots, compacted into the ray's head storage (the
+        // head sort stages them from there: every cut ray then stages like a
+        // whole one); the smallest key left out
+        int* st = stage + hoff[i];
+        int n = 0;
+        unsigned kout = 0xffffffffu;
+        for (int e0 = 0; e0 < q; e0 += 128) {  // keys (L2-warm) and slots, four of each per lane in flight
+            unsigned kv[4];
+            int sv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * 32 + lane;
+                kv[u] = e < q ? sc_key[so + e] : 0xffffffffu;
+                sv[u] = e < q ? __ldcs(sc_slot + so + e) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * 32 + lane;
+                const bool in = e < q && kv[u] <= kcut;
+                if (e < q && !in) kout = min(kout, kv[u]);
+                const unsigned bb = __ballot_sync(0xffffffffu, in);
+                if (in) st[n + __popc(bb & lanemask_lt())] = sv[u];
+                n += __popc(bb);
+            }
+        }
+        kout = __reduce_min_sync(0xffffffffu, kout);
+        HP_ASSERT(n == cnt);
+        if (lane == 0) {
+            sel[i] = make_uint4(kcut, unsigned(cnt), kout, 0u);
+            const int cls = cnt <= kHeadSmall ? 0 : 1;  // the sort configuration of this head
             lists[int64_t(cls) * m + atomicAdd(&counts[cls], 1)] = int(i);
         }
         __syncwarp();
@@ -471,7 +508,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
     const int64_t* __restrict__ off, const int* __restrict__ rays, const int64_t* __restrict__ soff,
     const int64_t* __restrict__ hoff,
     const RayMeta* __restrict__ meta, const unsigned* __restrict__ sc_key, const int* __restrict__ sc_slot,
-    const uint2* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n, int whole,
+    const uint4* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n, int whole,
     double* __restrict__ head_t, int* __restrict__ head_id, double* __restrict__ head_d, int* __restrict__ plen,
     int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d, Params SP,
     float* __restrict__ head_u) {
@@ -486,56 +523,29 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
         const int q = int(off[r + 1] - off[r]);
         const RayMeta M = meta[r];
         const bool all = q <= whole;
-        unsigned kc = 0xffffffffu;
+        unsigned kc = 0xffffffffu, kout = 0xffffffffu;
         int S = q;  // pairs to stage
         if (!all) {
-            const uint2 sv = sel[i];
+            const uint4 sv = sel[i];
             kc = sv.x;
             S = int(sv.y);
+            kout = sv.z;
         }
         HP_ASSERT(S <= kCap && S <= q);
         if (tid == 0) {
             F.cnt = F.keep = F.fcount = 0;
             F.fbad = M.bad;
             F.cut_d2 = ~0ull;
-            F.kout = 0xffffffffu;
+            F.kout = kout;
             F.thi = 0u;
         }
-        if (all) {  // every slot in flight at once
-            for (int e = tid; e < q; e += kT) cp_async4(&F.slot[e], sc_slot + so + e);
-            cp_commit();
-        }
+        // every slot in flight at once: a whole ray's from its match scratch, a
+        // cut ray's selected ones from where k_head_select compacted them
+        const int* src = all ? sc_slot + so : head_id + hoff[i];
+        for (int e = tid; e < S; e += kT) cp_async4(&F.slot[e], src + e);
+        cp_commit();
         for (int j = tid; j <= kCoarse; j += kT) F.chist[j] = 0;
         for (int j = tid; j <= S; j += kT) F.hist[j] = 0;
-        __syncthreads();
-        if (!all) {  // stream keys and slots (kU of each per thread in flight); stage the selected slots
-            constexpr int kU = HP_HEAD_SORT_U;
-            unsigned kout = 0xffffffffu;
-            for (int e0 = 0; e0 < q; e0 += kU * kT) {
-                unsigned kv[kU];
-                int sv[kU];
-#pragma unroll
-                for (int u = 0; u < kU; u++) {
-                    const int e = e0 + u * kT + tid;
-                    kv[u] = e < q ? __ldcs(sc_key + so + e) : 0xffffffffu;
-                    sv[u] = e < q ? __ldcs(sc_slot + so + e) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < kU; u++) {
-                    const int e = e0 + u * kT + tid;
-                    const bool in = e < q && kv[u] <= kc;
-                    if (e < q && !in) kout = min(kout, kv[u]);
-                    const unsigned b = __ballot_sync(0xffffffffu, in);
-                    int base = 0;
-                    if (lane_id() == 0 && b) base = atomicAdd(&F.cnt, __popc(b));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    HP_ASSERT(!in || base + __popc(b & lanemask_lt()) < S);
-                    if (in) F.slot[base + __popc(b & lanemask_lt())] = sv[u];
-                }
-            }
-            kout = __reduce_min_sync(0xffffffffu, kout);
-            if (lane_id() == 0 && kout != 0xffffffffu) atomicMin(&F.kout, kout);
-        }
         cp_wait<0>();
         __syncthreads();
         // exact t / dist^2 / id of every staged pair; long rays keep t < T_c
@@ -565,7 +575,7 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
                                    F.chist, F.scan_sh);
         const int Lh = F.keep;
         const int64_t ho = hoff[i];
-        HP_ASSERT(Lh <= S && ho + Lh <= hoff[i + 1] && (all || F.cnt == S));
+        HP_ASSERT(Lh <= S && ho + Lh <= hoff[i + 1]);
         const double r0 = Lh > 0 ? dmul(__ldg(slopes + r), F.t[F.perm[0]]) : 0.0;
         int cnt = 0;
         bool bad = false;
@@ -665,7 +675,7 @@ struct HeadWs {
     RayMeta* meta;
     int* lists;
     int* counts;
-    uint2* sel;
+    uint4* sel;
     unsigned* key;
     int* slot;
 };
@@ -678,7 +688,7 @@ HeadWs carve_head(Carver& c, int64_t m, int64_t cap) {
     w.meta = c.take<RayMeta>(mm);
     w.lists = c.take<int>(3 * mm);
     w.counts = c.take<int>(64);
-    w.sel = c.take<uint2>(mm);
+    w.sel = c.take<uint4>(mm);
     w.key = c.take<unsigned>(cap > 0 ? cap : 1);
     w.slot = c.take<int>(cap > 0 ? cap : 1);
     return w;
@@ -772,8 +782,9 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         const int occ_sel = kernel_occupancy((const void*)kselect, 128, 0);
         if (occ_sel < 0) return occ_sel;
         TimedSpan ts("k_head_select", s);
-        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, rays, w.soff, w.meta, want, whole, w.key, w.sel,
-                                                       list_cut, w.counts + 2, w.lists, w.counts, nout);
+        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, rays, w.soff, w.meta, want, whole, w.key, w.slot,
+                                                       head_off, head_ids, w.sel, list_cut, w.counts + 2, w.lists,
+                                                       w.counts, nout);
         HP_CHECK_LAUNCH("k_head_select");
     }
     Params SP{};
