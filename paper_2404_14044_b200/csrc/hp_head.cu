@@ -55,6 +55,9 @@ constexpr int kMaxPieces = 8;          // row pieces per chunk
 #ifndef HP_HEAD_U_MAX
 #define HP_HEAD_U_MAX 384  // bound factors precomputed for the first this many head entries
 #endif
+#ifndef HP_SELECT_U
+#define HP_SELECT_U 8  // keys (and slots) per lane in flight in k_head_select
+#endif
 #ifndef HP_HEAD_SORT_U
 #define HP_HEAD_SORT_U 8  // keys + slots of a cut ray streamed per thread per round
 #endif
@@ -397,15 +400,16 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
         while ((span1 >> sh) >= unsigned(kBins)) sh++;
         for (int b = lane; b < kBins; b += 32) H[b] = 0;
         __syncwarp();
-        for (int e0 = 0; e0 < q; e0 += 128) {  // four loads per lane in flight
-            unsigned kv[4];
+        constexpr int kU = HP_SELECT_U;
+        for (int e0 = 0; e0 < q; e0 += 32 * kU) {  // kU loads per lane in flight
+            unsigned kv[kU];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < kU; u++) {
                 const int e = e0 + u * 32 + lane;
                 kv[u] = e < q ? sc_key[so + e] : 0u;
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+            for (int u = 0; u < kU; u++)
                 if (e0 + u * 32 + lane < q) {
                     HP_ASSERT(kv[u] >= M.kmin && ((kv[u] - M.kmin) >> sh) < unsigned(kBins));
                     atomicAdd(&H[(kv[u] - M.kmin) >> sh], 1);
@@ -447,17 +451,17 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
         int* st = stage + hoff[i];
         int n = 0;
         unsigned kout = 0xffffffffu;
-        for (int e0 = 0; e0 < q; e0 += 128) {  // keys (L2-warm) and slots, four of each per lane in flight
-            unsigned kv[4];
-            int sv[4];
+        for (int e0 = 0; e0 < q; e0 += 32 * kU) {  // keys (L2-warm) and slots, kU of each per lane in flight
+            unsigned kv[kU];
+            int sv[kU];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < kU; u++) {
                 const int e = e0 + u * 32 + lane;
                 kv[u] = e < q ? sc_key[so + e] : 0xffffffffu;
                 sv[u] = e < q ? __ldcs(sc_slot + so + e) : 0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < kU; u++) {
                 const int e = e0 + u * 32 + lane;
                 const bool in = e < q && kv[u] <= kcut;
                 if (e < q && !in) kout = min(kout, kv[u]);
