@@ -56,6 +56,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef HP_PLAN_CPASYNC
 #define HP_PLAN_CPASYNC 1
 #endif
+#ifndef HP_PLAN_F32
+#define HP_PLAN_F32 1  // fp32 ring bound factors in k_sample_plan
+#endif
 #ifndef HP_PLAN_AHEAD
 #define HP_PLAN_AHEAD 2  // chunks in flight
 #endif
@@ -118,7 +121,7 @@ struct RayOut {  // per-ray results of pass 1
 // transmittance provably underflows to exactly 0.  plan[ray] =
 // (jstar, je, flags: 1 fast | 2 proved_zero, q).
 __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __restrict__ plan,
-                         int64_t* __restrict__ ecnt, double* __restrict__ rt, double* __restrict__ rd) {
+                         int64_t* __restrict__ ecnt, double* __restrict__ rt, double* __restrict__ rd, float2* rf) {
     const int lane = lane_id();
     const int64_t lo = C.lo(ray);
     const int q = C.n(ray);  // candidates present (prefix mode: the prefix)
@@ -196,6 +199,7 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
     if (fast) {
         Chain S;
         S.je = q;
+        double tb = 0.0;  // the ray's base t for the fp32 bound terms
 #if HP_PLAN_CPASYNC
         // the ring is filled by cp.async two chunks ahead (no registers held
         // across the chunk; the chunk's own work does not cover a DRAM trip)
@@ -233,6 +237,15 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
                 cp_wait<HP_PLAN_AHEAD - 1>();  // chunk c0 has landed
                 __syncwarp();
                 const double tj = j < q ? rt[j & (kRing - 1)] : 0.0;
+                float thi = 0.0f, rj_lo = 0.0f;
+                if (P.f32_bounds) {
+                    if (c0 == 0) tb = __shfl_sync(0xffffffffu, tj, 0);
+                    const double dj = j < q ? rd[j & (kRing - 1)] : 0.0;
+                    rf[j & (kRing - 1)] = make_float2(__double2float_rd(__dsub_rd(tj, tb)), __double2float_ru(dj));
+                    thi = __double2float_ru(__dsub_ru(tj, tb));
+                    rj_lo = __double2float_rd(__dmul_rd(slope, tj));
+                    __syncwarp();
+                }
                 fetch(c0 + 32 * HP_PLAN_AHEAD);  // its slots are outside the windows still to be read
 #else
                 const double tj = tn, dj = dn;
@@ -245,6 +258,13 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
                 __syncwarp();
 #endif
                 if (j < q) {
+                    const bool use_el = j >= jstar;
+                    const int ksel = use_el ? P.K : (q < P.K ? q : P.K);
+#if HP_PLAN_CPASYNC
+                    if (P.f32_bounds && j >= ksel - 1)
+                        u = bound_factor_ringf<kRing>(rf, j, thi, rj_lo, ksel, use_el, P);
+                    else
+#endif
                     u = (j >= P.K - 1 || c0 + 32 >= min(q, P.K))
                             ? bound_factor_ring<kRing>(rt, rd, q, j, tj, jstar, slope, P)
                             : -1.0;
@@ -278,9 +298,10 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
 __global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan,
                                                           int64_t* __restrict__ ecnt) {
     __shared__ double ring[kWarps][2][kRing];  // recent candidates' t / ds per warp
+    __shared__ float2 ringf[kWarps][kRing];    // their fp32 bound terms
     const int64_t warps = int64_t(gridDim.x) * kWarps;
     for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
-        plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1]);
+        plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1], ringf[warp_id()]);
 }
 
 // r_off[m] = -(exact slots needed) when the caller's capacity is short
@@ -571,6 +592,13 @@ Params to_params(const hp_sampler_params* p) {
     const double r = 1.0 / p->beta2;
     P.inv_beta2_up = nextafter(r, INFINITY);
     P.inv_k_up = nextafter(1.0 / double(P.K), INFINITY);
+    auto f_up = [](double x) {
+        float f = float(x);
+        return double(f) < x ? nextafterf(f, INFINITY) : f;
+    };
+    P.inv_beta2_up_f = f_up(P.inv_beta2_up);
+    P.inv_k_up_f = f_up(P.inv_k_up);
+    P.f32_bounds = std::isfinite(P.inv_beta2_up_f) && HP_PLAN_F32;
     return P;
 }
 

@@ -20,6 +20,9 @@ struct Params {
     double beta2, gamma, eps, tau_min;
     double inv_beta2_up;  // 1 / beta2 rounded up (bound factors only)
     double inv_k_up;      // 1 / K rounded up (bound factors only)
+    float inv_beta2_up_f;  // the same two, as floats rounded up (fp32 bound factors)
+    float inv_k_up_f;
+    int f32_bounds;        // the fp32 ring bound is usable (inv_beta2_up_f finite)
 };
 
 __device__ __forceinline__ bool kless(double d2a, int ia, double d2b, int ib) {
@@ -326,6 +329,19 @@ __device__ __forceinline__ double factor_from_sum(double sum, int ksel, const Pa
     return dsub(1.0, a_lo);
 }
 
+// The same bound in fp32 with directed rounding (half the fp64 pipe work of
+// factor_from_sum): sum >= the exact real sum of (|dt| + ds) over the ksel
+// members; the 2^-20 inflation dominates every fp64 rounding of the
+// reference's udf (K <= 256), and y >= the reference's exp argument.
+__device__ __forceinline__ double factor_from_sum_f(float sum, int ksel, const Params& P) {
+    const float inv_up = ksel == P.K ? P.inv_k_up_f : __frcp_ru(float(ksel));
+    const float udf_up = __fmul_ru(__fmul_ru(sum, 1.0f + 0x1p-20f), inv_up);
+    const float y = __fmul_ru(__fmul_ru(udf_up, udf_up), P.inv_beta2_up_f);
+    const float e = expf(-y);
+    const double a_lo = dmul(P.gamma, dmul(double(e), 1.0 - 0x1p-20));
+    return dsub(1.0, a_lo);
+}
+
 template <class View>
 __device__ double bound_factor(const View& V, int q, int j, int jstar, double slope, const Params& P) {
     const double tj = V.t(j);
@@ -369,6 +385,24 @@ __device__ __forceinline__ double bound_factor_ring(const double* rt, const doub
         sum = dadd(sum, dadd(fabs(dsub(rt[i], tj)), di));
     }
     return ok ? factor_from_sum(sum, ksel, P) : -1.0;
+}
+
+// fp32 ring variant for j >= ksel - 1 (members [j - ksel + 1, j], all at or
+// before j).  rf[i] = (RD(t_i - tb), RU(ds_i)) for the ray's base tb,
+// thi = RU(t_j - tb), rj_lo = RD(slope * t_j): thi - rf[i].x >= t_j - t_i and
+// rf[i].y <= rj_lo proves ds_i <= r_j.  Negative: a member may be outside the
+// pool (the caller then uses bound_factor).
+template <int kRingSize>
+__device__ __forceinline__ double bound_factor_ringf(const float2* rf, int j, float thi, float rj_lo, int ksel,
+                                                     bool use_el, const Params& P) {
+    float sum = 0.0f;
+    bool ok = true;
+    for (int k = 0; k < ksel; k++) {
+        const float2 e = rf[(j - k) & (kRingSize - 1)];
+        ok &= !(use_el && e.y > rj_lo);
+        sum = __fadd_ru(sum, __fadd_ru(__fsub_ru(thi, e.x), e.y));
+    }
+    return ok ? factor_from_sum_f(sum, ksel, P) : -1.0;
 }
 
 // Warp: first j in [0, q) with pred(j) (monotone false..true); q if none.

@@ -233,7 +233,8 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                   mark=lambda name: None, before_sample=lambda: None, prefix: bool | None = None,
                   emit_knn: bool = False) -> FrameResult:
     """query -> sample of one frame on the device.  ``prefix``: True (heads)
-    / False (full CSR); None: the HP_PREFIX setting."""
+    / False (full CSR); None: the HP_PREFIX setting.  ``colors`` may be a
+    callable that returns them (called once the query is enqueued)."""
     prefix = PREFIX if prefix is None else prefix
     budget = int(max_matches) if max_matches is not None else match_budget(
         bytes_per_match=BYTES_PER_MATCH_PREFIX if prefix else BYTES_PER_MATCH)
@@ -244,10 +245,12 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
         # too big for one pass: ray chunks (prefix mode unless turned off --
         # such frames are dominated by long rays)
         before_sample()
+        colors = colors() if callable(colors) else colors
         return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                               exact_t_end, budget, mark, prefix is not False, max_matches, emit_knn)
     mark("query")
     before_sample()
+    colors = colors() if callable(colors) else colors
     if isinstance(q, device.QueryPrefix):
         _PREFIX_LEN.clear()
         s, Q, n_flagged, n_res = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
@@ -296,6 +299,170 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
                        prefix=prefix, prefix_len=plen)
 
 
+# Host-buffer calls run the frame in ray chunks so that the result copies
+# overlap the device work: every chunk's samples go down (pinned buffers, a
+# copy stream) while the next one computes, and only the last, smaller
+# chunk's copy is exposed.  Each extra chunk costs ~0.4 ms of device time
+# (cfg2), so one cut.  Rays are independent: the samples are one pass's.
+_CUTS_ENV = os.environ.get("HP_E2E_CUTS", "0.6")
+E2E_CUTS = tuple(float(x) for x in _CUTS_ENV.split(",") if x.strip()) if _CUTS_ENV != "none" else ()
+E2E_MIN_RAYS = 1 << 17   # smaller frames: one pass
+E2E_HEADROOM = 1.25      # host buffers: the first chunk's sample density times this
+_R_PER_RAY: dict = {}    # last frame's samples per ray, per device: the host buffers' first size
+_COPY: dict = {}
+
+
+def _copy_stream(dev) -> torch.cuda.Stream:
+    if dev not in _COPY:
+        _COPY[dev] = torch.cuda.Stream(device=dev)
+    return _COPY[dev]
+
+
+def _ray_chunks(m: int) -> list:
+    if m < E2E_MIN_RAYS or not E2E_CUTS:
+        return [0, m]
+    cuts = sorted({0, m, *(min(max(int(f * m), 0), m) for f in E2E_CUTS)})
+    return cuts
+
+
+def _host_buffers(s, m, cap, old=None, rows=0):
+    """Pinned host buffers for a frame's samples: offsets [m + 1], t_end [m]
+    and the per-sample fields with room for ``cap`` samples (the first
+    ``rows`` of ``old`` carried over when growing)."""
+    R = int(s[1].shape[0])
+    out = []
+    for k, x in enumerate(s):
+        if k in (0, 8):
+            out.append(old[k] if old is not None else
+                       torch.empty(m + 1 if k == 0 else m, dtype=x.dtype, pin_memory=True))
+        elif x.shape[0] != R:  # no colours: (0, 3)
+            out.append(torch.zeros(tuple(x.shape), dtype=x.dtype))
+        else:
+            h = torch.empty((cap,) + tuple(x.shape[1:]), dtype=x.dtype, pin_memory=True)
+            if old is not None and rows:
+                h[:rows].copy_(old[k][:rows])
+            out.append(h)
+    return out
+
+
+def _samples_to_host(run_chunk, cuts, dev):
+    """run_chunk(a, b) -> the device samples of rays [a, b), enqueued on the
+    current stream; every chunk's samples are copied to pinned host memory on
+    a copy stream while the next chunk runs.  Returns the numpy 9-tuple of
+    the whole frame (offsets rebased, samples in ray order)."""
+    m = cuts[-1]
+    main = torch.cuda.current_stream()
+    cp = _copy_stream(dev)
+    host, cap, R0, keep, bases = None, 0, 0, [], []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        s = run_chunk(a, b)
+        Rc = int(s[1].shape[0])
+        if host is None or R0 + Rc > cap:  # first chunk (or a short guess): size from the density so far
+            guess = int((R0 + Rc) * m / max(b, 1) * E2E_HEADROOM) + 1024
+            cap = max(guess, int(_R_PER_RAY.get(dev, 0.0) * m * 1.05) + 1024, R0 + Rc)
+            cp.synchronize()
+            host = _host_buffers(s, m, cap, host, R0)
+        cp.wait_event(main.record_event())
+        with torch.cuda.stream(cp):
+            host[0][a:b].copy_(s[0][:b - a], non_blocking=True)
+            host[8][a:b].copy_(s[8], non_blocking=True)
+            for k in range(1, len(s)):
+                if k != 8 and s[k].shape[0] == Rc and Rc:
+                    host[k][R0:R0 + Rc].copy_(s[k], non_blocking=True)
+        keep.append(s)  # the device results stay alive until their copies are done
+        bases.append((a, b, R0))
+        R0 += Rc
+    cp.synchronize()
+    off = host[0].numpy()
+    for a, b, base in bases:
+        if base:
+            off[a:b] += base
+    off[m] = R0
+    _R_PER_RAY[dev] = R0 / max(m, 1)
+    return tuple(h.numpy() if (k in (0, 8) or h.shape[0] == 0) else h.numpy()[:R0]
+                 for k, h in enumerate(host))
+
+
+H2D_PIECE = 4 << 20  # bytes per staged piece of a pageable upload
+_HOST_POOL: list = []
+
+
+def _host_pool():
+    if not _HOST_POOL:
+        from concurrent.futures import ThreadPoolExecutor
+        _HOST_POOL.append(ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1), thread_name_prefix="hp-h2d"))
+    return _HOST_POOL[0]
+
+
+def _h2d(a, dev, dtype) -> torch.Tensor:
+    """Upload host data (numpy array or CPU tensor, pinned or not) to ``dev``
+    on the current stream.  Pinned tensors go up directly; pageable data is
+    staged through pinned memory in pieces that host threads copy in
+    parallel (numpy releases the GIL), each piece's DMA enqueued as soon as
+    its copy is done -- the driver's own pageable path runs at ~11 GB/s on the
+    B200 box.  (torch's own multi-threaded copy is faster alone but its
+    spinning OpenMP threads slow the library's host slope threads.)"""
+    if isinstance(a, torch.Tensor):
+        if a.is_pinned() or a.numel() * a.element_size() < H2D_PIECE:
+            return a.to(device=dev, dtype=dtype, non_blocking=True)
+        a = a.numpy() if a.dtype == dtype else a.to(dtype).numpy()
+    arr = np.asarray(a)
+    np_dt = torch.empty((), dtype=dtype).numpy().dtype
+    if arr.dtype != np_dt or not arr.flags.c_contiguous:
+        arr = np.ascontiguousarray(arr, dtype=np_dt)
+    if arr.nbytes < H2D_PIECE:
+        return torch.from_numpy(arr).to(dev, non_blocking=True)
+    stage = torch.empty(arr.shape, dtype=dtype, pin_memory=True)  # caching host allocator: reused
+    src, dst = arr.reshape(-1), stage.numpy().reshape(-1)
+    step = max(1, H2D_PIECE // arr.itemsize)
+    pieces = [(i, min(i + step, src.size)) for i in range(0, src.size, step)]
+    pool = _host_pool()
+    futs = [pool.submit(np.copyto, dst[i:j], src[i:j]) for i, j in pieces]
+    out = torch.empty(arr.shape, dtype=dtype, device=dev)
+    flat_o, flat_s = out.view(-1), stage.view(-1)
+    for (i, j), f in zip(pieces, futs):
+        f.result()
+        flat_o[i:j].copy_(flat_s[i:j], non_blocking=True)  # the pinned block stays reserved until this copy ran
+    return out
+
+
+_COORD: list = []
+
+
+def _h2d_async(stream, dev, *items):
+    """:func:`_h2d` of every (host data, dtype) item on ``stream`` from a
+    coordinator thread, so the host staging overlaps the caller's own work.
+    Returns wait() -> the device tensors, after making the current stream
+    wait for the uploads."""
+    if not _COORD:
+        from concurrent.futures import ThreadPoolExecutor
+        _COORD.append(ThreadPoolExecutor(max_workers=1, thread_name_prefix="hp-upload"))
+
+    def run():
+        with torch.cuda.device(dev), torch.cuda.stream(stream):
+            outs = [None if a is None else _h2d(a, dev, dt) for a, dt in items]
+            return outs, stream.record_event()
+    fut = _COORD[0].submit(run)
+
+    def wait():
+        outs, ev = fut.result()
+        torch.cuda.current_stream().wait_event(ev)
+        return outs
+    return wait
+
+
+def _host_rays(a, m, dtype, cols=None):
+    """CPU torch tensor view of a per-ray host input (numpy / tensor / scalar)."""
+    if isinstance(a, torch.Tensor) and a.numel() == m * (cols or 1):
+        t = a.reshape(m, cols) if cols else a.reshape(m)
+        return t if t.dtype == dtype else t.to(dtype)
+    arr = a.numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    if arr.ndim == 0 and not cols:
+        arr = np.broadcast_to(arr.astype(np.float64), (m,))
+    t = torch.from_numpy(np.ascontiguousarray(arr)).reshape((m, cols) if cols else (m,))
+    return t if t.dtype == dtype else t.to(dtype)
+
+
 def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
                       sampler_cfg: SamplerConfig | None = None, with_colors: bool = True,
                       exact_t_end: bool = True, max_matches: int | None = None):
@@ -306,51 +473,45 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     Inputs may be numpy arrays or (preferably pinned) CPU torch tensors.  The
     device build and the ray uploads are enqueued first; the host-side slopes
     (host threads in the library, bit-identical to the reference's
-    ``radius_slopes``) are computed while they run; results come back through
-    pinned buffers with one synchronisation.
+    ``radius_slopes``) are computed while they run (pageable inputs are
+    staged through pinned memory by host threads, :func:`_h2d`).  The frame
+    then runs in ray chunks whose result copies (pinned buffers) overlap the
+    next chunk's device work (``E2E_CUTS``).
     """
     dev = torch.device("cuda", torch.cuda.current_device())
-
-    def up(a, dt):
-        if isinstance(a, torch.Tensor):
-            return a.to(device=dev, dtype=dt, non_blocking=True)
-        return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt, non_blocking=True)
-
     main = torch.cuda.current_stream()
     side = _side_stream(dev)  # persistent: the caching allocator pools blocks per stream
     side.wait_stream(main)
-    xyz = up(cloud.positions, torch.float64)
+    xyz = _h2d(cloud.positions, dev, torch.float64)
     idx = device.build(xyz, camera, search_cfg.pad)          # async on the stream
     px_host = pixels.numpy() if isinstance(pixels, torch.Tensor) else np.asarray(pixels)
     px_host = np.ascontiguousarray(px_host, dtype=np.int64).reshape(-1, 2)
     m = px_host.shape[0]
-
-    def per_ray(a):
-        if isinstance(a, torch.Tensor) and a.numel() == m:
-            return up(a.reshape(m), torch.float64)
-        return up(np.broadcast_to(np.asarray(a, np.float64), (m,)), torch.float64)
-
-    with torch.cuda.stream(side):  # ray uploads overlap the build and the host slopes
-        pix_d = up(pixels, torch.int64).view(m, 2)
-        dirs_d = up(dirs, torch.float64).view(m, 3)
-        tn, tf = per_ray(t_near), per_ray(t_far)
+    cuts = _ray_chunks(m)
+    # the rays go up (staged on a coordinator thread) while the build runs and
+    # the host slopes are computed; the colours after them, while the query runs
+    rays_up = _h2d_async(side, dev, (_host_rays(pixels, m, torch.int64, 2), torch.int64),
+                         (_host_rays(dirs, m, torch.float64, 3), torch.float64),
+                         (_host_rays(t_near, m, torch.float64), torch.float64),
+                         (_host_rays(t_far, m, torch.float64), torch.float64))
+    cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
     sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
-    host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius,
-                out=sl_host.numpy())
-    with torch.cuda.stream(side):
-        sl = sl_host.to(dev, non_blocking=True)
-        rays_ready = side.record_event()
-        # colours are needed by the sampler only: their upload overlaps the query
-        col = up(cloud.colors, torch.float64) if (with_colors and cloud.colors is not None) else None
-        cols_ready = side.record_event()
-    main.wait_event(rays_ready)
-    s = _query_sample(idx, col, pix_d, dirs_d, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
-                      max_matches, before_sample=lambda: main.wait_event(cols_ready)).samples
-    outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
-    for o, x in zip(outs, s):
-        o.copy_(x, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    return tuple(o.numpy() for o in outs)
+    host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
+    sl = sl_host.to(dev, non_blocking=True)
+    pix_d, dirs_d, tn, tf = rays_up()
+    cfg = sampler_cfg or SamplerConfig()
+    col = []
+
+    def colours():  # resolved by _query_sample right before its sampler
+        if not col:
+            col.append(cols_up()[0])
+        return col[0]
+
+    def run_chunk(a, b):
+        return _query_sample(idx, colours, pix_d[a:b], dirs_d[a:b], tn[a:b], tf[a:b], sl[a:b], cfg, exact_t_end,
+                             max_matches).samples
+
+    return _samples_to_host(run_chunk, cuts, dev)
 
 
 def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: float,
@@ -360,35 +521,33 @@ def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: floa
     row-major, scalar t_near / t_far -- the reference CLI's
     ``generate_rays`` + renderer ``_prepare``, cli.py:127-162,
     renderer.py:113-125) generated on the device (hp_ray_grid, bit-identical
-    to numpy), then build -> query -> sample as :func:`search_and_sample`.
-    Only the cloud (and its colours) go up; returns the numpy 9-tuple of
-    ``sample_batch_arrays``."""
+    to numpy), then build -> query -> sample as :func:`search_and_sample`
+    (ray chunks, copies overlapped).  Only the cloud (and its colours) go up;
+    returns the numpy 9-tuple of ``sample_batch_arrays``."""
     dev = torch.device("cuda", torch.cuda.current_device())
-
-    def up(a):
-        if isinstance(a, torch.Tensor):
-            return a.to(device=dev, dtype=torch.float64, non_blocking=True)
-        return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=torch.float64, non_blocking=True)
-
     main = torch.cuda.current_stream()
     side = _side_stream(dev)
     side.wait_stream(main)
-    xyz = up(cloud.positions)
+    xyz = _h2d(cloud.positions, dev, torch.float64)
     idx = device.build(xyz, camera, search_cfg.pad)
     dirs, pixels, tn, tf = device.ray_grid(camera, dev, t_near=t_near, t_far=t_far)
     m = int(dirs.shape[0])
+    cuts = _ray_chunks(m)
     sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
+    sl = torch.empty(m, dtype=torch.float64, device=dev)
+    cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
     host_slopes(camera, None, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
-    with torch.cuda.stream(side):
-        sl = sl_host.to(dev, non_blocking=True)
-        rays_ready = side.record_event()
-        col = up(cloud.colors) if (with_colors and cloud.colors is not None) else None
-        cols_ready = side.record_event()
-    main.wait_event(rays_ready)
-    s = _query_sample(idx, col, pixels, dirs, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
-                      max_matches, before_sample=lambda: main.wait_event(cols_ready)).samples
-    outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in s]
-    for o, x in zip(outs, s):
-        o.copy_(x, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    return tuple(o.numpy() for o in outs)
+    sl.copy_(sl_host, non_blocking=True)
+    cfg = sampler_cfg or SamplerConfig()
+    col = []
+
+    def colours():  # resolved by _query_sample right before its sampler
+        if not col:
+            col.append(cols_up()[0])
+        return col[0]
+
+    def run_chunk(a, b):
+        return _query_sample(idx, colours, pixels[a:b], dirs[a:b], tn[a:b], tf[a:b], sl[a:b], cfg, exact_t_end,
+                             max_matches).samples
+
+    return _samples_to_host(run_chunk, cuts, dev)

@@ -174,14 +174,18 @@ def test_degenerate_frames():
 
 @pytest.mark.parametrize("name", ["cfg1", "small_sphere_surface", "orbit_planes", "empty"])
 @pytest.mark.parametrize("mode", [None, True, False])
-def test_search_and_sample_host_api_matches_goldens(name, mode, monkeypatch):
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_search_and_sample_host_api_matches_goldens(name, mode, chunks, monkeypatch):
     """The public host-buffer pipeline (numpy in / numpy out, side-stream
-    uploads, host slopes in the library) reproduces the reference goldens in
-    every frame mode (auto, prefix, full CSR)."""
+    uploads, host slopes in the library, ray chunks whose copies overlap the
+    neighbouring chunks' work) reproduces the reference goldens in every
+    frame mode (auto, prefix, full CSR)."""
     from paper_2404_14044_b200 import pipeline
     if name not in gu.case_names():
         pytest.skip(f"no golden case {name}")
     monkeypatch.setattr(pipeline, "PREFIX", mode)
+    monkeypatch.setattr(pipeline, "E2E_CUTS", tuple(k / chunks for k in range(1, chunks)))
+    monkeypatch.setattr(pipeline, "E2E_MIN_RAYS", 1)
     g = gu.load(name)
     _, cloud, cam, cfg, tn, tf, stride, samplers = gu.get_case(name)
     pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)

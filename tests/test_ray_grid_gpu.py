@@ -52,3 +52,27 @@ def test_view_pipeline_equals_host_rays():
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
     assert a[1].size > 0
+
+
+@pytest.mark.parametrize("chunks", [2, 5])
+def test_chunked_host_copies_equal_one_pass(chunks, monkeypatch):
+    """Ray chunks with overlapped result copies (pipeline._samples_to_host)
+    give the one-pass arrays -- also when the host buffers sized from the
+    first chunk are short and grow mid-frame."""
+    cloud = hp.generate_scene(hp.SceneSpec("sphere_surface", n=50_000, seed=3, noise=0.005))
+    cam = hp.scene_camera(160, 120, fov_deg=25)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.01), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    m = dirs.shape[0]
+    monkeypatch.setattr(pipeline, "E2E_CUTS", ())
+    ref = pipeline.search_and_sample(cloud, cam, cfg, pixels, dirs, np.full(m, 1.0), np.full(m, 10.0))
+    monkeypatch.setattr(pipeline, "E2E_CUTS", tuple(k / chunks for k in range(1, chunks)))
+    monkeypatch.setattr(pipeline, "E2E_MIN_RAYS", 1)
+    monkeypatch.setattr(pipeline, "E2E_HEADROOM", 0.5)  # the first guess is short: the buffers grow
+    for view in (False, True):
+        pipeline._R_PER_RAY.clear()  # no size hint from an earlier frame
+        out = (pipeline.search_and_sample_view(cloud, cam, cfg, 1.0, 10.0) if view else
+               pipeline.search_and_sample(cloud, cam, cfg, pixels, dirs, 1.0, 10.0))
+        assert len(out) == len(ref)
+        for x, y in zip(out, ref):
+            np.testing.assert_array_equal(x, y)
