@@ -145,6 +145,16 @@ int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
 int hp_radius_slopes_host(const hp_camera* cam, const int64_t* pixels, int64_t pixel_stride, int64_t m,
                           double kernel_radius, int approx, double* slopes, int threads);
 
+/* Host -> device upload of PAGEABLE host memory (numpy arrays) through a
+ * caller-provided pinned staging buffer of >= bytes: `threads` host threads
+ * copy src into it in pieces of `piece` bytes (0: 2 MiB) and each piece's
+ * cudaMemcpyAsync to dst is enqueued on `stream` as soon as it is staged.
+ * Returns once every piece is enqueued; the staging buffer must stay
+ * untouched until the stream has run the copies.  (Host plumbing of the
+ * host-buffer entry points; no reference counterpart.) */
+int hp_host_upload(void* dst, const void* src, size_t bytes, void* staging, size_t piece, int threads,
+                   cudaStream_t stream);
+
 /* The camera's ray grid on the device (replaces geometry.ray_grid,
  * geometry.py:289-306, bit-identical): rows [row0, row0 + rows) of the image,
  * ray k = (row0 * width + k) in row-major order.  dirs float64 [m,3] unit

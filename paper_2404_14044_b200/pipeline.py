@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -22,6 +23,10 @@ from .sampler import SamplerConfig
 
 __all__ = ["FrameResult", "frame_device", "search_and_sample", "search_and_sample_view", "StageTimer",
            "host_slopes"]
+
+
+SLOPE_THREADS = int(os.environ.get("HP_SLOPE_THREADS", "0")) or min(16, os.cpu_count() or 1)
+H2D_THREADS = int(os.environ.get("HP_H2D_THREADS", "0")) or min(2, os.cpu_count() or 1)
 
 
 def host_slopes(camera, pixels: np.ndarray | None, kernel_radius: float, approx: bool = False,
@@ -38,7 +43,7 @@ def host_slopes(camera, pixels: np.ndarray | None, kernel_radius: float, approx:
         m = px.shape[0]
     if out is None:
         out = np.empty(m, dtype=np.float64)
-    threads = threads or min(16, os.cpu_count() or 1)
+    threads = threads or SLOPE_THREADS
     device._lib.check(lib.hp_radius_slopes_host(ctypes.byref(device.camera_struct(camera)),
                                                 px.ctypes.data_as(ctypes.c_void_p) if px is not None
                                                 else ctypes.c_void_p(0), 2, m,
@@ -383,25 +388,17 @@ def _samples_to_host(run_chunk, cuts, dev):
                  for k, h in enumerate(host))
 
 
-H2D_PIECE = 4 << 20  # bytes per staged piece of a pageable upload
-_HOST_POOL: list = []
-
-
-def _host_pool():
-    if not _HOST_POOL:
-        from concurrent.futures import ThreadPoolExecutor
-        _HOST_POOL.append(ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1), thread_name_prefix="hp-h2d"))
-    return _HOST_POOL[0]
+H2D_PIECE = int(os.environ.get("HP_H2D_PIECE", str(1 << 20)))  # bytes per staged piece of a pageable upload
+_INFLIGHT: list = []  # (pinned staging block, event): blocks an upload's DMA may still read
+_INFLIGHT_LOCK = threading.Lock()
 
 
 def _h2d(a, dev, dtype) -> torch.Tensor:
     """Upload host data (numpy array or CPU tensor, pinned or not) to ``dev``
-    on the current stream.  Pinned tensors go up directly; pageable data is
-    staged through pinned memory in pieces that host threads copy in
-    parallel (numpy releases the GIL), each piece's DMA enqueued as soon as
-    its copy is done -- the driver's own pageable path runs at ~11 GB/s on the
-    B200 box.  (torch's own multi-threaded copy is faster alone but its
-    spinning OpenMP threads slow the library's host slope threads.)"""
+    on the current stream.  Pinned tensors go up directly; pageable data goes
+    through hp_host_upload: host threads stage it into pinned memory piece by
+    piece and each piece's DMA is enqueued as soon as it is staged (the
+    driver's own pageable path runs at ~11-20 GB/s on the B200 box)."""
     if isinstance(a, torch.Tensor):
         if a.is_pinned() or a.numel() * a.element_size() < H2D_PIECE:
             return a.to(device=dev, dtype=dtype, non_blocking=True)
@@ -412,17 +409,18 @@ def _h2d(a, dev, dtype) -> torch.Tensor:
         arr = np.ascontiguousarray(arr, dtype=np_dt)
     if arr.nbytes < H2D_PIECE:
         return torch.from_numpy(arr).to(dev, non_blocking=True)
-    stage = torch.empty(arr.shape, dtype=dtype, pin_memory=True)  # caching host allocator: reused
-    src, dst = arr.reshape(-1), stage.numpy().reshape(-1)
-    step = max(1, H2D_PIECE // arr.itemsize)
-    pieces = [(i, min(i + step, src.size)) for i in range(0, src.size, step)]
-    pool = _host_pool()
-    futs = [pool.submit(np.copyto, dst[i:j], src[i:j]) for i, j in pieces]
+    with _INFLIGHT_LOCK:  # release the staging blocks whose copies have run
+        _INFLIGHT[:] = [x for x in _INFLIGHT if not x[1].query()]
+    stage = torch.empty(arr.nbytes, dtype=torch.uint8, pin_memory=True)  # caching host allocator: reused
     out = torch.empty(arr.shape, dtype=dtype, device=dev)
-    flat_o, flat_s = out.view(-1), stage.view(-1)
-    for (i, j), f in zip(pieces, futs):
-        f.result()
-        flat_o[i:j].copy_(flat_s[i:j], non_blocking=True)  # the pinned block stays reserved until this copy ran
+    stream = torch.cuda.current_stream(dev)
+    lib = device._lib.load(require_device=True)
+    device._lib.check(lib.hp_host_upload(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(arr.ctypes.data),
+                                         arr.nbytes, ctypes.c_void_p(stage.data_ptr()), H2D_PIECE, H2D_THREADS,
+                                         ctypes.c_void_p(stream.cuda_stream)))
+    ev = stream.record_event()
+    with _INFLIGHT_LOCK:  # torch does not see these DMAs: keep the block until they ran
+        _INFLIGHT.append((stage, ev))
     return out
 
 

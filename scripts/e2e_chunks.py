@@ -7,10 +7,18 @@ import bench
 from paper_2404_14044_b200 import pipeline
 w = bench.make_workload(os.environ.get("WL", "cfg2"))
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-C = type("C", (), dict(positions=pin(w["cloud"].positions), colors=pin(w["cloud"].colors)))()
-P = [pin(w[k]) for k in ("pixels", "dirs", "t_near", "t_far")]
+if os.environ.get("INPUT", "numpy") == "pinned":
+    C = type("C", (), dict(positions=pin(w["cloud"].positions), colors=pin(w["cloud"].colors)))()
+    P = [pin(w[k]) for k in ("pixels", "dirs", "t_near", "t_far")]
+else:
+    C, P = w["cloud"], [w[k] for k in ("pixels", "dirs", "t_near", "t_far")]
 T = []
-orig_qs, orig_hb = pipeline._query_sample, pipeline._host_buffers
+orig_qs, orig_hb, orig_sl, orig_b = pipeline._query_sample, pipeline._host_buffers, pipeline.host_slopes, pipeline.device.build
+def sl(*a, **k):
+    T.append(("sl+", time.perf_counter())); r = orig_sl(*a, **k); T.append(("sl-", time.perf_counter())); return r
+def bd(*a, **k):
+    T.append(("build", time.perf_counter())); return orig_b(*a, **k)
+pipeline.host_slopes, pipeline.device.build = sl, bd
 def qs(*a, **k):
     T.append(("qs+", time.perf_counter())); r = orig_qs(*a, **k); T.append(("qs-", time.perf_counter())); return r
 def hb(*a, **k):
