@@ -107,6 +107,28 @@ __device__ __forceinline__ unsigned long long okey(double x) {
 
 // ---------------------------------------------------------------- warp helpers
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Dynamic work distribution for warp-per-item kernels: lane 0 claims kBatch
+// items at a time from a zeroed global counter (item costs vary widely, so a
+// static split leaves a long tail).  Warp-uniform.
+template <int kBatch>
+struct WarpClaim {
+    unsigned long long* ctr;
+    int64_t cur = 0, end = 0;
+    __device__ __forceinline__ explicit WarpClaim(unsigned long long* c) : ctr(c) {}
+    __device__ __forceinline__ bool next(int64_t n, int64_t& item) {
+        if (cur >= end) {
+            unsigned long long b = 0;
+            if ((threadIdx.x & 31) == 0) b = atomicAdd(ctr, (unsigned long long)kBatch);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            cur = int64_t(b);
+            end = cur + kBatch;
+        }
+        if (cur >= n) return false;
+        item = cur++;
+        return true;
+    }
+};
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 
 template <class T>

@@ -195,6 +195,7 @@ struct HeadScanSmem {
     unsigned kmin[kGroupMax], kmax[kGroupMax];
     int64_t off[kGroupMax], end[kGroupMax];
     int dq[kWarps][64];  // deferred (uncertain) slots of the warp's current ray run
+    int64_t next;        // the CTA's current group (claimed from the work counter)
 };
 
 // Per-ray results of the scan: key bounds of the accepted pairs, and whether
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
     k_head_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC, int64_t m, const int64_t* __restrict__ soff,
                 unsigned* __restrict__ sc_key, int* __restrict__ sc_slot, RayMeta* __restrict__ meta,
                 int64_t* __restrict__ counts, int64_t* __restrict__ hcount, int64_t* __restrict__ probes,
-                int64_t* __restrict__ scanned, int64_t capacity) {
+                int64_t* __restrict__ scanned, int64_t capacity, unsigned long long* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char dyn[];
     HeadScanSmem& S = *reinterpret_cast<HeadScanSmem*>(dyn);
     if (soff[m] > capacity) return;  // scratch too small: reported in offsets[m]
@@ -222,7 +223,13 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
     }
     __syncthreads();
     unsigned phase = 0;
-    for (int64_t r0 = int64_t(blockIdx.x) * kGroupMax; r0 < m; r0 += int64_t(gridDim.x) * kGroupMax) {
+    // groups of kGroupMax rays claimed dynamically (their costs differ widely:
+    // a static split leaves a long tail on small frames / row bands)
+    for (;;) {
+        if (threadIdx.x == 0) S.next = int64_t(atomicAdd(work, 1ull)) * kGroupMax;
+        __syncthreads();
+        const int64_t r0 = S.next;
+        if (r0 >= m) break;
         const int G = int(m - r0 < kGroupMax ? m - r0 : kGroupMax);
         if (threadIdx.x < G) {
             S.fill[threadIdx.x] = 0;
@@ -387,8 +394,8 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
     __shared__ int hist[4][kBins];
     int* H = hist[warp_id()];
     const int lane = lane_id();
-    const int64_t warps = int64_t(gridDim.x) * 4;
     const int64_t nr = *list_n;
+    const int64_t warps = int64_t(gridDim.x) * 4;  // (static: a dynamic claim measured slower here)
     for (int64_t k = int64_t(blockIdx.x) * 4 + warp_id(); k < nr; k += warps) {
         const int64_t i = list[k], r = rays ? rays[i] : i;  // output i, ray r
         const int q = int(off[r + 1] - off[r]);
@@ -498,6 +505,7 @@ struct HeadSmem {
     unsigned long long cut_d2;         // order key of the trimmed pairs' smallest dist^2
     unsigned kout, thi;                // smallest left-out key; fkey of the largest float(t) staged
     int cnt, keep, fcount, fbad;
+    int next;                          // the CTA's current list entry (claimed from the work counter)
 };
 
 // One CTA per ray: a ray of <= kCap matches is staged whole (its slots by
@@ -515,13 +523,17 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
     const uint4* __restrict__ sel, const int* __restrict__ list, const int* __restrict__ list_n, int whole,
     double* __restrict__ head_t, int* __restrict__ head_id, double* __restrict__ head_d, int* __restrict__ plen,
     int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d, Params SP,
-    float* __restrict__ head_u) {
+    float* __restrict__ head_u, unsigned long long* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char dyn[];
     HeadSmem<kCap>& F = *reinterpret_cast<HeadSmem<kCap>*>(dyn);
     const double4* __restrict__ rel4 = reinterpret_cast<const double4*>(L.rel4);
     const int tid = threadIdx.x;
     const int nr = *list_n;
-    for (int k = blockIdx.x; k < nr; k += gridDim.x) {
+    for (;;) {  // rays claimed dynamically (head lengths vary: no static tail)
+        if (tid == 0) F.next = int(atomicAdd(work, 1ull));
+        __syncthreads();
+        const int k = F.next;
+        if (k >= nr) break;
         const int64_t i = list[k], r = rays ? rays[i] : i;  // output i, ray r
         const int64_t so = soff[r];
         const int q = int(off[r + 1] - off[r]);
@@ -682,6 +694,7 @@ struct HeadWs {
     uint4* sel;
     unsigned* key;
     int* slot;
+    unsigned long long* work;  // work counters of the dynamically scheduled kernels
 };
 
 HeadWs carve_head(Carver& c, int64_t m, int64_t cap) {
@@ -695,6 +708,7 @@ HeadWs carve_head(Carver& c, int64_t m, int64_t cap) {
     w.sel = c.take<uint4>(mm);
     w.key = c.take<unsigned>(cap > 0 ? cap : 1);
     w.slot = c.take<int>(cap > 0 ? cap : 1);
+    w.work = c.take<unsigned long long>(4);  // [0] scan groups, [1] / [2] small / big sort rays
     return w;
 }
 
@@ -738,10 +752,12 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
         HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
         const int occ = kernel_occupancy((const void*)k_head_scan, kThreads, sizeof(HeadScanSmem));
         if (occ < 0) return occ;
+        if (cudaMemsetAsync(w.work, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "hp_head_count memset");
         TimedSpan ts("k_head_scan", s);
         k_head_scan<<<group_grid(m, occ), kThreads, sizeof(HeadScanSmem), s>>>(
             layout, padded_w, int(pad), R, QC, m, w.soff, w.key, w.slot, w.meta, offsets, head_off, probes, scanned,
-            capacity);
+            capacity, w.work);
         HP_CHECK_LAUNCH("k_head_scan");
     }
     HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
@@ -773,7 +789,8 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     const int64_t nout = rays ? n : m;  // outputs (rays[i] or i)
     if (nout == 0) return HP_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(w.counts, 0, 3 * sizeof(int), s) != cudaSuccess)
+    if (cudaMemsetAsync(w.counts, 0, 3 * sizeof(int), s) != cudaSuccess ||
+        cudaMemsetAsync(w.work + 1, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_head_sort memset");
     const int* list_small = w.lists;
     const int* list_big = w.lists + nout;
@@ -810,11 +827,11 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     TimedSpan ts("k_head_sort", s);
     ksmall<<<device_sms() * occ_small, 128, sizeof(HeadSmem<kHeadSmall>), s>>>(
         layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts,
-        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u);
+        whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u, w.work + 1);
     HP_CHECK_LAUNCH("k_head_sort small");
     kbig<<<device_sms() * occ_big, 256, sizeof(HeadSmem<kHeadCap>), s>>>(
         layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big,
-        w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u);
+        w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u, w.work + 2);
     HP_CHECK_LAUNCH("k_head_sort");
     return HP_OK;
 }

@@ -296,11 +296,13 @@ __device__ void plan_ray(const Csr& C, const Params& P, int64_t ray, int4* __res
 }
 
 __global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4* __restrict__ plan,
-                                                          int64_t* __restrict__ ecnt) {
+                                                          int64_t* __restrict__ ecnt,
+                                                          unsigned long long* __restrict__ work) {
     __shared__ double ring[kWarps][2][kRing];  // recent candidates' t / ds per warp
     __shared__ float2 ringf[kWarps][kRing];    // their fp32 bound terms
-    const int64_t warps = int64_t(gridDim.x) * kWarps;
-    for (int64_t ray = int64_t(blockIdx.x) * kWarps + warp_id(); ray < C.m; ray += warps)
+    WarpClaim<4> claim(work);  // chain lengths vary widely: rays claimed dynamically
+    int64_t ray;
+    while (claim.next(C.m, ray))
         plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1], ringf[warp_id()]);
 }
 
@@ -558,6 +560,7 @@ struct SampleWs {
     int64_t* eoff;  // [m + 1] exact-candidate offsets
     Exact x;
     void* scan;
+    unsigned long long* work;  // k_sample_plan's ray counter
 };
 
 SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color, int knn_k = 0) {
@@ -574,6 +577,7 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color, int knn_k 
     w.x.knn_w = knn_k > 0 ? c.take<double>(xc * knn_k) : nullptr;
     w.x.ray = c.take<int>(xc);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
+    w.work = c.take<unsigned long long>(2);
     return w;
 }
 
@@ -607,8 +611,10 @@ Params to_params(const hp_sampler_params* p) {
 template <class BestT>
 int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     {
+        if (cudaMemsetAsync(w.work, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "k_sample_plan memset");
         TimedSpan ts("k_sample_plan", s);
-        k_sample_plan<<<device_sms() * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff);
+        k_sample_plan<<<device_sms() * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.work);
         HP_CHECK_LAUNCH("k_sample_plan");
     }
     HP_TRY(exclusive_scan_i64(w.eoff, w.eoff, C.m, w.scan, s));
