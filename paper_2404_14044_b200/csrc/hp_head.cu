@@ -196,6 +196,8 @@ struct HeadScanSmem {
     int64_t off[kGroupMax], end[kGroupMax];
     int dq[kWarps][64];  // deferred (uncertain) slots of the warp's current ray run
     int64_t next;        // the CTA's current group (claimed from the work counter)
+    int bnd[kGroupMax];  // the group's per-ray scratch bounds (footprint slots)
+    int skip;            // the group's scratch did not fit the capacity
 };
 
 // Per-ray results of the scan: key bounds of the accepted pairs, and whether
@@ -206,13 +208,12 @@ struct RayMeta {
 };
 
 __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
-    k_head_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC, int64_t m, const int64_t* __restrict__ soff,
+    k_head_scan(hp_query_layout L, int64_t wp, int pad, Rays R, QCam QC, int64_t m, int64_t* __restrict__ soff,
                 unsigned* __restrict__ sc_key, int* __restrict__ sc_slot, RayMeta* __restrict__ meta,
                 int64_t* __restrict__ counts, int64_t* __restrict__ hcount, int64_t* __restrict__ probes,
                 int64_t* __restrict__ scanned, int64_t capacity, unsigned long long* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char dyn[];
     HeadScanSmem& S = *reinterpret_cast<HeadScanSmem*>(dyn);
-    if (soff[m] > capacity) return;  // scratch too small: reported in offsets[m]
     const int s = 2 * pad + 1;
     const int lane = lane_id(), warp = warp_id();
     const double4* __restrict__ rel4 = reinterpret_cast<const double4*>(L.rel4);
@@ -237,10 +238,41 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
             S.bad[threadIdx.x] = 0;
             S.kmin[threadIdx.x] = 0xffffffffu;
             S.kmax[threadIdx.x] = 0u;
-            S.off[threadIdx.x] = soff[r0 + threadIdx.x];
-            S.end[threadIdx.x] = soff[r0 + threadIdx.x + 1];
+            S.bnd[threadIdx.x] = 0;
         }
         group_setup(S.head, R, QC, r0, G, s);
+        // each ray's scratch segment: its bound (the footprint slots the
+        // stream below tests, as k_query_bound counts them), placed by one
+        // atomic per group on the scratch cursor work[3] (which ends at the
+        // total the frame needs, also when it exceeds the capacity)
+        for (int idx = threadIdx.x; idx < s * G; idx += kThreads) {
+            const int row = idx / G, g = idx - row * G;
+            const RayParams& r = S.head.ray[g];
+            const int y = r.v + row;
+            int x0, x1;
+            if (footprint_row(S.head.fp[g], QC.C, pad, QC.width, QC.height, r.u, r.v, y, x0, x1)) {
+                const int64_t base = int64_t(y) * wp;
+                const int n = L.row_ptr[base + x1 + 1] - L.row_ptr[base + x0];
+                if (n > 0) atomicAdd(&S.bnd[g], n);
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int b = lane < G ? S.bnd[lane] : 0;
+            const int inc = warp_incl_scan(b);
+            const int tot = __shfl_sync(0xffffffffu, inc, 31);
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(work + 3, (unsigned long long)tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (lane < G) {
+                S.off[lane] = int64_t(base) + inc - b;
+                S.end[lane] = int64_t(base) + inc;
+                soff[r0 + lane] = int64_t(base) + inc - b;
+            }
+            if (lane == 0) S.skip = int64_t(base) + tot > capacity;
+        }
+        __syncthreads();
+        if (S.skip) continue;  // the frame is re-run with the reported size; S.next is rewritten after a barrier
         unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's key bounds for the current ray
         int lbad = 0;
         stream_group_bulk(
@@ -744,15 +776,9 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
     const Rays R{pixels, pixel_stride, dirs, t_near, t_far, slopes};
     const QCam QC = make_qcam(cam);
     if (m > 0) {
-        {
-            TimedSpan ts("k_query_bound", s);
-            k_query_bound<<<group_grid(m, 8), kThreads, 0, s>>>(layout, padded_w, int(pad), R, QC, m, w.soff);
-            HP_CHECK_LAUNCH("k_query_bound");
-        }
-        HP_TRY(exclusive_scan_i64(w.soff, w.soff, m, w.scan, s));
         const int occ = kernel_occupancy((const void*)k_head_scan, kThreads, sizeof(HeadScanSmem));
         if (occ < 0) return occ;
-        if (cudaMemsetAsync(w.work, 0, sizeof(unsigned long long), s) != cudaSuccess)
+        if (cudaMemsetAsync(w.work, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess)
             return cuda_status(cudaGetLastError(), "hp_head_count memset");
         TimedSpan ts("k_head_scan", s);
         k_head_scan<<<group_grid(m, occ), kThreads, sizeof(HeadScanSmem), s>>>(
@@ -763,7 +789,7 @@ extern "C" int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64
     HP_TRY(exclusive_scan_i64(offsets, offsets, m, w.scan, s));
     HP_TRY(exclusive_scan_i64(head_off, head_off, m, w.scan, s));
     if (m > 0) {
-        k_mark_overflow<<<1, 1, 0, s>>>(w.soff + m, capacity, offsets + m);
+        k_mark_overflow<<<1, 1, 0, s>>>(reinterpret_cast<const int64_t*>(w.work + 3), capacity, offsets + m);
         HP_CHECK_LAUNCH("k_mark_overflow");
     }
     return HP_OK;
