@@ -206,7 +206,11 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
  * facts[i], cuts[i]) then stands for ray rays[i].  sampler + head_u (both
  * or neither): the sampler's bound factors of every head entry (float, next
  * to head_t; -1 where not precomputed), which hp_sample_run_prefix then
- * multiplies instead of recomputing them (same results). */
+ * multiplies instead of recomputing them (same results).  hp_head_sort may
+ * be enqueued right after hp_head_count, before the caller has read
+ * offsets[m]: the head arrays may then be sized by `capacity` (>= head_off[m]
+ * whenever the count fit), and when the count ran short (offsets[m] < 0) it
+ * writes empty heads and the caller re-runs both with the reported size. */
 int hp_head_workspace_bytes(int64_t m, int64_t capacity, size_t* bytes);
 int hp_head_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_w, int64_t padded_h,
                   int64_t pad, const int64_t* pixels, int64_t pixel_stride, const double* dirs,

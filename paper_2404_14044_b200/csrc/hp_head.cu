@@ -380,13 +380,17 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
 // With `rays`, output i stands for ray rays[i] (a re-sort of a subset).
 __global__ void k_head_classes(const int64_t* __restrict__ off, const int* __restrict__ rays, int64_t m, int whole,
                                int* __restrict__ lists, int* __restrict__ counts, int* __restrict__ plen,
-                               int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d) {
+                               int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d,
+                               const int64_t* __restrict__ total) {
+    // the count pass ran short of scratch (offsets[m] < 0, the caller re-runs
+    // it): every head empty, nothing sorted (its counts are not all written)
+    const bool over = *total < 0;
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r - threadIdx.x < m;
          r += int64_t(gridDim.x) * blockDim.x) {
         int cls = -1;
         if (r < m) {
             const int64_t ri = rays ? rays[r] : r;
-            const int64_t q = off[ri + 1] - off[ri];
+            const int64_t q = over ? 0 : off[ri + 1] - off[ri];
             cls = q == 0 ? -1 : (q > whole ? 2 : (q <= kHeadSmall ? 0 : 1));
             if (q == 0) {
                 plen[r] = 0;
@@ -822,7 +826,7 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     const int* list_big = w.lists + nout;
     const int* list_cut = w.lists + 2 * nout;
     k_head_classes<<<grid_for(nout, 256), 256, 0, s>>>(offsets, rays, nout, whole, w.lists, w.counts, plen, facts,
-                                                       cut_t, cut_d);
+                                                       cut_t, cut_d, offsets + m);
     HP_CHECK_LAUNCH("k_head_classes");
     {
         constexpr auto kselect = k_head_select<kHeadCap>;

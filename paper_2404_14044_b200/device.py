@@ -302,10 +302,24 @@ HEAD_FACTORS = os.environ.get("HP_HEAD_FACTORS", "0") == "1"
 HEAD_WHOLE = int(os.environ.get("HP_HEAD_WHOLE", "512"))
 
 
-def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
+class CountShort(Exception):
+    """A deferred head count (no host read between hp_head_count and the
+    sampler) ran short of scratch: re-run the frame's query synchronously."""
+
+
+# Frames enqueue hp_head_count -> hp_head_sort -> the sampler with no host
+# read in between once a scratch size is known for the device (the head
+# arrays then sized by that capacity; Q and a short count are checked at the
+# sampler's read).  False: read Q after the count, as a first frame does.
+DEFER_COUNT = os.environ.get("HP_DEFER_COUNT", "1") != "0"
+
+
+def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, defer=False):
     """hp_head_count with the workspace sized (retrying once); returns
     (offsets, head_off, probes, scanned, Q, head capacity, workspace, bytes,
-    capacity) -- Q and the head capacity read in one synchronisation."""
+    capacity) -- Q and the head capacity read in one synchronisation.
+    ``defer``: no read when a scratch size is known (Q None, head capacity =
+    the scratch capacity; the caller checks offsets[m] later)."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
     m = int(pixels.shape[0])
@@ -321,6 +335,13 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
     if max_scratch is not None:
         cap = min(cap, int(max_scratch))
     _mark("query.setup")
+    if defer and cap > 0:
+        _lib.check(lib.hp_head_workspace_bytes(m, cap, ctypes.byref(nb)))
+        ws = _workspace(nb.value, dev)
+        _lib.check(lib.hp_head_count(*args, _ptr(offsets), _ptr(head_off), _ptr(probes), _ptr(scanned), cap,
+                                     _ptr(ws), nb.value, _stream()))
+        _mark("query.count")
+        return offsets, head_off, probes, scanned, None, cap, ws, nb.value, cap
     for _ in range(2):
         _lib.check(lib.hp_head_workspace_bytes(m, cap, ctypes.byref(nb)))
         ws = _workspace(nb.value, dev)
@@ -423,15 +444,18 @@ def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whol
 
 
 def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix: bool | None = None,
-                max_scratch: int | None = None, want: int | None = None, sampler_cfg=None):
+                max_scratch: int | None = None, want: int | None = None, sampler_cfg=None, defer=None):
     """The query of a sampling frame: the heads (``prefix`` True or None;
     returns a :class:`QueryPrefix`) or the full CSR with facts (``prefix``
-    False; returns the 7-tuple of :func:`query`)."""
+    False; returns the 7-tuple of :func:`query`).  ``defer`` (None:
+    DEFER_COUNT): no host read after the head count (sample_prefix then
+    checks it and raises :class:`CountShort` when it ran short)."""
     pixels, dirs = pixels.contiguous(), dirs.contiguous()
     if prefix is False:
         return _fill(index, _count(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), slopes, True)
-    return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), dirs, slopes,
-                 want, None, sampler_cfg)
+    defer = DEFER_COUNT if defer is None else defer
+    return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch, defer),
+                 dirs, slopes, want, None, sampler_cfg)
 
 
 def sampler_params(cfg, want_color: bool, exact_t_end: bool, emit_knn: bool = False) -> _lib.SamplerParams:
@@ -556,8 +580,15 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
                                             _ptr(pre.facts), ctypes.byref(p), colp, ncol, _ptr(r_off),
                                             _ptr(t_end), _ptr(flagged), _ptr(ws), nb.value, _stream()))
         _mark("sample.run")
-        both = torch.stack([r_off[m], flagged[m].to(torch.int64)]).cpu()  # one synchronisation
+        vals = [r_off[m], flagged[m].to(torch.int64)]
+        if pre.total is None:  # deferred count: Q (or a short count) read here too
+            vals.append(pre.offsets[m])
+        both = torch.stack(vals).cpu()  # one synchronisation
         R, n_flagged = int(both[0]), int(both[1])
+        if pre.total is None:
+            pre.total = int(both[2])
+            if pre.total < 0:
+                raise CountShort(-pre.total)
         if R >= 0:
             break
         exact_cap = int(-R * 1.0625) + 1024   # exact scratch too small: grow it once

@@ -243,19 +243,34 @@ def _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
     prefix = PREFIX if prefix is None else prefix
     budget = int(max_matches) if max_matches is not None else match_budget(
         bytes_per_match=BYTES_PER_MATCH_PREFIX if prefix else BYTES_PER_MATCH)
+    col = []
+
+    def colours():
+        if not col:
+            col.append(colors() if callable(colors) else colors)
+        return col[0]
+    try:
+        return _query_sample_once(idx, colours, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end,
+                                  max_matches, mark, before_sample, prefix, emit_knn, budget, None)
+    except device.CountShort:  # the deferred count ran short: again, reading the count first
+        return _query_sample_once(idx, colours, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end,
+                                  max_matches, mark, lambda: None, prefix, emit_knn, budget, False)
+
+
+def _query_sample_once(idx, colours, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, max_matches,
+                       mark, before_sample, prefix, emit_knn, budget, defer) -> FrameResult:
     try:
         q = device.query_frame(idx, pixels, dirs, t_near, t_far, slopes, prefix=prefix, max_scratch=budget,
-                               sampler_cfg=sampler_cfg if device.HEAD_FACTORS else None)
+                               sampler_cfg=sampler_cfg if device.HEAD_FACTORS else None, defer=defer)
     except device.MatchBudgetExceeded:
         # too big for one pass: ray chunks (prefix mode unless turned off --
         # such frames are dominated by long rays)
         before_sample()
-        colors = colors() if callable(colors) else colors
-        return _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
+        return _frame_chunked(idx, colours(), pixels, dirs, t_near, t_far, slopes, sampler_cfg,
                               exact_t_end, budget, mark, prefix is not False, max_matches, emit_knn)
     mark("query")
     before_sample()
-    colors = colors() if callable(colors) else colors
+    colors = colours()
     if isinstance(q, device.QueryPrefix):
         _PREFIX_LEN.clear()
         s, Q, n_flagged, n_res = _prefix_finish(q, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg,
