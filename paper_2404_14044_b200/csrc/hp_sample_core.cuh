@@ -397,10 +397,19 @@ __device__ __forceinline__ double bound_factor_ringf(const float2* rf, int j, fl
                                                      bool use_el, const Params& P) {
     float sum = 0.0f;
     bool ok = true;
-    for (int k = 0; k < ksel; k++) {
-        const float2 e = rf[(j - k) & (kRingSize - 1)];
-        ok &= !(use_el && e.y > rj_lo);
-        sum = __fadd_ru(sum, __fadd_ru(__fsub_ru(thi, e.x), e.y));
+    if (ksel == 8) {  // the default K: unrolled
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const float2 e = rf[(j - k) & (kRingSize - 1)];
+            ok &= !(use_el && e.y > rj_lo);
+            sum = __fadd_ru(sum, __fadd_ru(__fsub_ru(thi, e.x), e.y));
+        }
+    } else {
+        for (int k = 0; k < ksel; k++) {
+            const float2 e = rf[(j - k) & (kRingSize - 1)];
+            ok &= !(use_el && e.y > rj_lo);
+            sum = __fadd_ru(sum, __fadd_ru(__fsub_ru(thi, e.x), e.y));
+        }
     }
     return ok ? factor_from_sum_f(sum, ksel, P) : -1.0;
 }
