@@ -338,7 +338,8 @@ def ncu_traffic(span):
     committed `ncu --set full` summary of the same bench command
     (profiles/*_ncu_full.json, scripts/ncu_summary.py); None if absent."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), key=os.path.getmtime)
+    # newest capture first: the names sort by round / version (mtimes do not survive a checkout)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), key=os.path.basename)
     for f in reversed(files):
         try:
             sp = json.load(open(f))["spans"].get(span)
@@ -623,12 +624,13 @@ def run_ours(args, w, rank, world, dist):
         # rays in (64 B), row pointers, the fp32 copies (16 B / point), 8 B per
         # match out, per-ray counts / head counts / key bounds / probes / scanned
         "k_head_scan": 64 * m_loc + 4 * (P + 1) + 16 * n_in + 8 * q_loc + 56 * m_loc,
-        # the cut rays' keys (4 B / match) in, per-ray cut out
-        "k_head_select": 4 * q_cut + 8 * m_loc,
-        # slots of whole rays, keys + slots of cut rays (streamed together), exact
+        # the cut rays' keys and slots (4 + 4 B / match) in, their selected
+        # slots (4 B each, ~ the cut rays' head) and per-ray selection (16 B) out
+        "k_head_select": 8 * q_cut + 4 * max(plen - q_whole, 0) + 16 * m_loc,
+        # slots of whole rays (scratch) and of cut rays (the selection), exact
         # records (32 B / point, once), heads out (t, id32, dist: 20 B) and
         # per-ray inputs / outputs
-        "k_head_sort": 4 * q_whole + 8 * q_cut + 32 * n_in + 20 * plen + 112 * hit,
+        "k_head_sort": 4 * q_whole + 4 * max(plen - q_whole, 0) + 32 * n_in + 20 * plen + 112 * hit,
         "k_sample_plan": 8 * (m_loc + 1) + 16 * plen + 8 * m_loc + 24 * m_loc,
         "k_emit": 8 * (m_loc + 1) + 52 * r_loc + 24 * r_loc + 72 * r_loc,
     }

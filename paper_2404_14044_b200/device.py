@@ -312,14 +312,16 @@ class CountShort(Exception):
 # arrays then sized by that capacity; Q and a short count are checked at the
 # sampler's read).  False: read Q after the count, as a first frame does.
 DEFER_COUNT = os.environ.get("HP_DEFER_COUNT", "1") != "0"
+_DEFER_OK: dict = {}  # per device: False after a deferred count ran short / a frame needed chunks
 
 
-def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, defer=False):
+def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch, defer=False, frame=False):
     """hp_head_count with the workspace sized (retrying once); returns
     (offsets, head_off, probes, scanned, Q, head capacity, workspace, bytes,
     capacity) -- Q and the head capacity read in one synchronisation.
     ``defer``: no read when a scratch size is known (Q None, head capacity =
-    the scratch capacity; the caller checks offsets[m] later)."""
+    the scratch capacity; the caller checks offsets[m] later).  ``frame``: a
+    whole frame's count (its outcome decides whether later frames defer)."""
     lib = _lib.load(require_device=True)
     dev = index.table_start.device
     m = int(pixels.shape[0])
@@ -335,13 +337,26 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
     if max_scratch is not None:
         cap = min(cap, int(max_scratch))
     _mark("query.setup")
-    if defer and cap > 0:
+    if defer and cap > 0 and _DEFER_OK.get(dev, True):
         _lib.check(lib.hp_head_workspace_bytes(m, cap, ctypes.byref(nb)))
         ws = _workspace(nb.value, dev)
         _lib.check(lib.hp_head_count(*args, _ptr(offsets), _ptr(head_off), _ptr(probes), _ptr(scanned), cap,
                                      _ptr(ws), nb.value, _stream()))
         _mark("query.count")
-        return offsets, head_off, probes, scanned, None, cap, ws, nb.value, cap
+        # head arrays: sum_r min(q_r, 1024) <= min(Q, 1024 m)
+        return offsets, head_off, probes, scanned, None, min(cap, HEAD_CAP * max(m, 1)), ws, nb.value, cap
+    # read first: the exact scratch need from the (cheap) bound pass -- a
+    # count over a short capacity still streams every group placed below it
+    need = int(query_bounds(index, pixels, dirs, t_near, t_far, slopes, footprint)[m])
+    if max_scratch is not None and need > max_scratch:
+        if frame:
+            _DEFER_OK[dev] = False  # frames of this size run in chunks
+        raise MatchBudgetExceeded(need, int(max_scratch))
+    cap = int(need * 1.0625) + 1024  # headroom for the next (deferred) frame
+    if max_scratch is not None:
+        cap = max(min(cap, int(max_scratch)), need)
+    if cap > _QUERY_CAP.get(dev, 0):
+        _QUERY_CAP[dev] = cap
     for _ in range(2):
         _lib.check(lib.hp_head_workspace_bytes(m, cap, ctypes.byref(nb)))
         ws = _workspace(nb.value, dev)
@@ -351,11 +366,15 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
         both = torch.stack([offsets[m], head_off[m]]).cpu()  # one synchronisation
         total, hcap = int(both[0]), int(both[1])
         if total >= 0:
+            if _ == 0 and frame:
+                _DEFER_OK[dev] = True  # the remembered size fits: later frames may defer the read
             break
         if _ == 1:
             raise RuntimeError(f"hp_head_count: scratch of {cap} slots still short ({-total} needed)")
         needed = -total
         if max_scratch is not None and needed > max_scratch:
+            if frame:
+                _DEFER_OK[dev] = False  # frames of this size run in chunks: no deferred first attempt
             raise MatchBudgetExceeded(needed, int(max_scratch))
         cap = int(needed * 1.0625) + 1024
         if max_scratch is not None:
@@ -454,7 +473,7 @@ def query_frame(index: DeviceIndex, pixels, dirs, t_near, t_far, slopes, prefix:
     if prefix is False:
         return _fill(index, _count(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch), slopes, True)
     defer = DEFER_COUNT if defer is None else defer
-    return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch, defer),
+    return _head(index, _count_head(index, pixels, dirs, t_near, t_far, slopes, True, max_scratch, defer, True),
                  dirs, slopes, want, None, sampler_cfg)
 
 
@@ -588,6 +607,7 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
         if pre.total is None:
             pre.total = int(both[2])
             if pre.total < 0:
+                _DEFER_OK[dev] = False
                 raise CountShort(-pre.total)
         if R >= 0:
             break

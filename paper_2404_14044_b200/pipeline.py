@@ -295,6 +295,11 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
         if b <= a:
             raise device.MatchBudgetExceeded(int(bo[a + 1] - bo[a]), budget)
         cuts.append(min(b, m))
+    # every chunk's scratch need is below its bound: size the counts for the
+    # largest chunk up front (a count over a short capacity wastes a pass)
+    dev = idx.table_start.device
+    big = max(int(bo[b] - bo[a]) for a, b in zip(cuts[:-1], cuts[1:]))
+    device._QUERY_CAP[dev] = max(device._QUERY_CAP.get(dev, 0), big)
     parts, Q, nf, nr = [], 0, 0, 0
     _PREFIX_LEN.clear()
     for a, b in zip(cuts[:-1], cuts[1:]):

@@ -231,3 +231,44 @@ def test_pipeline_second_chance_resort_equals_full(monkeypatch, want, whole):
         if want == 16:
             assert a.resorted > 0
         assert a.flagged <= a.resorted
+
+
+def test_deferred_count_short_and_chunk_switch(monkeypatch):
+    """The deferred head count (no host read between hp_head_count and the
+    sampler): a remembered scratch size that is too small for this frame makes
+    the sort write empty heads and the sampler's read raise CountShort; the
+    frame re-runs reading the count and equals the full-CSR frame.  A frame
+    that then needs ray chunks turns deferral off for the next frame (no
+    wasted deferred pass), and a fitting frame turns it back on."""
+    from paper_2404_14044_b200 import pipeline
+    _, cloud, cam, cfg, tn, tf, stride, _ = gu.get_case("cfg1")
+    dev = torch.device("cuda")
+    xyz = torch.from_numpy(cloud.positions).to(dev)
+    col = torch.from_numpy(cloud.colors).to(dev)
+    pixels, dirs, t_near, t_far, slopes = gu.rays_and_slopes(cam, cfg, tn, tf, stride)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    rays = (up(pixels), up(dirs), up(t_near), up(t_far), up(slopes))
+    idx = dv.build(xyz, cam, cfg.pad)
+    sc = hp.SamplerConfig()
+    full = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=False)
+    dev = idx.table_start.device  # the library's per-device key (cuda:N)
+    monkeypatch.setitem(dv._QUERY_CAP, dev, 1000)      # far below this frame's Q
+    monkeypatch.setitem(dv._DEFER_OK, dev, True)
+    calls = []
+    orig = dv.CountShort.__init__
+    monkeypatch.setattr(dv.CountShort, "__init__", lambda self, *a: (calls.append(a), orig(self, *a))[1])
+    a = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)
+    assert calls, "the deferred count should have run short"
+    _assert_same(a.samples, full.samples)
+    assert a.Q == full.Q
+    # a smaller budget: the deferred attempt (the last frame fit) runs short,
+    # the bound pass then shows the frame needs chunks
+    b = pipeline._query_sample(idx, col, *rays, sc, True, max(full.Q // 5, 4096), prefix=True)
+    assert b.chunks > 1 and dv._DEFER_OK[dev] is False and len(calls) == 2
+    _assert_same(b.samples, full.samples)
+    c = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)  # fits: read first, then defer again
+    _assert_same(c.samples, full.samples)
+    assert dv._DEFER_OK[dev] is True
+    d = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)  # deferred, fits
+    _assert_same(d.samples, full.samples)
+    assert len(calls) == 2
