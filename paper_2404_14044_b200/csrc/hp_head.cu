@@ -97,10 +97,10 @@ __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1
 // slot range; every thread waits on the barrier's phase (tracked in `phase`,
 // bit b = parity of buffer b's next completion).  Chunk i + 1 is in flight
 // while chunk i is tested.
-template <class Issue, class Test, class Tab, class Done>
+template <class Issue, class Chunk, class Tab>
 __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kMaxPieces], int* npieces,
                                   unsigned& phase, int G, const hp_query_layout L, int64_t wp, int s,
-                                  const QCam& QC, Issue issue, Test test, Tab tab, Done done) {
+                                  const QCam& QC, Issue issue, Chunk chunk, Tab tab) {
     const int tid = threadIdx.x, warp = warp_id();
     const int pad = (s - 1) / 2;
     for (int yb = S.v0; yb < S.v1; yb += kRowsMax) {
@@ -167,17 +167,10 @@ __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kM
             if (tid == 0) plan_issue(buf ^ 1);
             mbar_wait(&bar[buf], (phase >> buf) & 1u);
             phase ^= 1u << buf;
+            // ray-major: a warp takes each of its rays through all of the
+            // chunk's pieces (rows), its per-ray state loaded once per chunk
             const int np = npieces[buf];
-            for (int i = 0; i < np; i++) {
-                const int4 pcs = pieces[buf][i];  // (row, a, b, smem offset)
-                for (int g = warp; g < G; g += kWarps) {
-                    const int lo = max(S.rlo[pcs.x][g], pcs.y), hi = min(S.rhi[pcs.x][g], pcs.z);
-                    if (lo < hi) {  // warp-uniform
-                        test(buf, g, lo, hi, pcs.y - pcs.w);
-                        done(g);
-                    }
-                }
-            }
+            for (int g = warp; g < G; g += kWarps) chunk(buf, g, np, pieces[buf]);
             __syncthreads();  // buffer `buf` is refilled two chunks later; npieces[buf ^ 1] is visible
             buf ^= 1;
         }
@@ -273,20 +266,26 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
         }
         __syncthreads();
         if (S.skip) continue;  // the frame is re-run with the reported size; S.next is rewritten after a barrier
-        unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's key bounds for the current ray
-        int lbad = 0;
         stream_group_bulk(
             S.head, S.bar, S.pieces, S.npieces, phase, G, L, wp, s, QC,
             [&](int buf, int off, int c0, int c1) {  // one piece: slots [c0, c1) to pf[buf][off..]
                 bulk_g2s(&S.pf[buf][off], L.relf + 4 * int64_t(c0), unsigned(c1 - c0) * 16u, &S.bar[buf]);
             },
-            [&](int buf, int g, int lo, int hi, int c0) {
+            [&](int buf, int g, int np, const int4* pcs) {  // ray g over the chunk's pieces
+                bool touched = false;
+                for (int i = 0; i < np; i++) {
+                    const int4 pc = pcs[i];  // (row, a, b, smem offset)
+                    touched |= max(S.head.rlo[pc.x][g], pc.y) < min(S.head.rhi[pc.x][g], pc.z);
+                }
+                if (!touched) return;  // warp-uniform
                 const RayParams& rp = S.head.ray[g];
                 const RayF rf = ray_f(rp);
                 const int64_t off = S.off[g];
                 int fill = S.fill[g];
                 int* dq = S.dq[warp];
                 int nq = 0;  // deferred pairs (warp-uniform)
+                unsigned lmin = 0xffffffffu, lmax = 0u;  // this lane's key bounds for ray g
+                int lbad = 0;
                 // the deferred pairs, 32 at a time on all lanes: gather the exact
                 // coordinates, the reference's fp64 test, append the accepted
                 auto flush = [&](int n) {
@@ -316,48 +315,48 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                     __syncwarp();
                     nq -= n;
                 };
-                for (int base = lo; base < hi; base += 32) {
-                    const int k = base + lane;
-                    int cls = 0;
-                    float tf = 0.0f, eps = 0.0f;
-                    if (k < hi) cls = cone_filter_te(S.pf[buf][k - c0], rf, tf, eps);
-                    const unsigned acc = __ballot_sync(0xffffffffu, cls == 1);
-                    if (cls == 1) {
-                        const int64_t pos = off + fill + __popc(acc & lanemask_lt());
-                        HP_ASSERT(pos < S.end[g]);
-                        const unsigned key = fkey(__fsub_rd(tf, eps));
-                        sc_key[pos] = key;
-                        sc_slot[pos] = k;
-                        lmin = min(lmin, key);
-                        lmax = max(lmax, key);
-                    }
-                    fill += __popc(acc);
-                    const unsigned unc = __ballot_sync(0xffffffffu, cls == 2);
-                    if (unc) {
-                        HP_ASSERT(nq + __popc(unc) <= 64);
-                        if (cls == 2) dq[nq + __popc(unc & lanemask_lt())] = k;
-                        nq += __popc(unc);
-                        if (nq >= 32) flush(32);
+                for (int i = 0; i < np; i++) {
+                    const int4 pc = pcs[i];
+                    const int lo = max(S.head.rlo[pc.x][g], pc.y), hi = min(S.head.rhi[pc.x][g], pc.z);
+                    const int c0 = pc.y - pc.w;
+                    for (int base = lo; base < hi; base += 32) {
+                        const int k = base + lane;
+                        int cls = 0;
+                        float tf = 0.0f, eps = 0.0f;
+                        if (k < hi) cls = cone_filter_te(S.pf[buf][k - c0], rf, tf, eps);
+                        const unsigned acc = __ballot_sync(0xffffffffu, cls == 1);
+                        if (cls == 1) {
+                            const int64_t pos = off + fill + __popc(acc & lanemask_lt());
+                            HP_ASSERT(pos < S.end[g]);
+                            const unsigned key = fkey(__fsub_rd(tf, eps));
+                            sc_key[pos] = key;
+                            sc_slot[pos] = k;
+                            lmin = min(lmin, key);
+                            lmax = max(lmax, key);
+                        }
+                        fill += __popc(acc);
+                        const unsigned unc = __ballot_sync(0xffffffffu, cls == 2);
+                        if (unc) {
+                            HP_ASSERT(nq + __popc(unc) <= 64);
+                            if (cls == 2) dq[nq + __popc(unc & lanemask_lt())] = k;
+                            nq += __popc(unc);
+                            if (nq >= 32) flush(32);
+                        }
                     }
                 }
                 if (nq > 0) flush(nq);
-                if (lane == 0) S.fill[g] = fill;  // ray g belongs to this warp alone
-                __syncwarp();
-            },
-            [&](int g, int n) { atomicAdd(&S.scn[g], n); },
-            [&](int g) {
-                const unsigned lo = __reduce_min_sync(0xffffffffu, lmin);
-                const unsigned hi = __reduce_max_sync(0xffffffffu, lmax);
+                const unsigned klo = __reduce_min_sync(0xffffffffu, lmin);
+                const unsigned khi = __reduce_max_sync(0xffffffffu, lmax);
                 const bool anybad = __any_sync(0xffffffffu, lbad);
-                if (lane == 0) {
-                    S.kmin[g] = min(S.kmin[g], lo);
-                    S.kmax[g] = max(S.kmax[g], hi);
+                if (lane == 0) {  // ray g belongs to this warp alone
+                    S.fill[g] = fill;
+                    S.kmin[g] = min(S.kmin[g], klo);
+                    S.kmax[g] = max(S.kmax[g], khi);
                     if (anybad) S.bad[g] = 1;
                 }
-                lmin = 0xffffffffu;
-                lmax = 0u;
-                lbad = 0;
-            });
+                __syncwarp();
+            },
+            [&](int g, int n) { atomicAdd(&S.scn[g], n); });
         __syncthreads();
         if (threadIdx.x < G) {
             const int64_t r = r0 + threadIdx.x;
