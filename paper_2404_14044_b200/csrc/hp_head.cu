@@ -272,11 +272,16 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                 bulk_g2s(&S.pf[buf][off], L.relf + 4 * int64_t(c0), unsigned(c1 - c0) * 16u, &S.bar[buf]);
             },
             [&](int buf, int g, int np, const int4* pcs) {  // ray g over the chunk's pieces
-                bool touched = false;
-                for (int i = 0; i < np; i++) {
-                    const int4 pc = pcs[i];  // (row, a, b, smem offset)
-                    touched |= max(S.head.rlo[pc.x][g], pc.y) < min(S.head.rhi[pc.x][g], pc.z);
+                // lane i < np: ray g's sub-range of piece i (row, a, b, smem offset); the
+                // touched pieces are then walked from the ballot
+                int plo = 0, phi = 0, pc0 = 0;
+                if (lane < np) {
+                    const int4 pc = pcs[lane];
+                    plo = max(S.head.rlo[pc.x][g], pc.y);
+                    phi = min(S.head.rhi[pc.x][g], pc.z);
+                    pc0 = pc.y - pc.w;
                 }
+                const unsigned touched = __ballot_sync(0xffffffffu, plo < phi);
                 if (!touched) return;  // warp-uniform
                 const RayParams& rp = S.head.ray[g];
                 const RayF rf = ray_f(rp);
@@ -315,10 +320,10 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                     __syncwarp();
                     nq -= n;
                 };
-                for (int i = 0; i < np; i++) {
-                    const int4 pc = pcs[i];
-                    const int lo = max(S.head.rlo[pc.x][g], pc.y), hi = min(S.head.rhi[pc.x][g], pc.z);
-                    const int c0 = pc.y - pc.w;
+                for (unsigned tm = touched; tm; tm &= tm - 1) {
+                    const int i = __ffs(tm) - 1;
+                    const int lo = __shfl_sync(0xffffffffu, plo, i), hi = __shfl_sync(0xffffffffu, phi, i);
+                    const int c0 = __shfl_sync(0xffffffffu, pc0, i);
                     for (int base = lo; base < hi; base += 32) {
                         const int k = base + lane;
                         int cls = 0;
