@@ -44,6 +44,20 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _host_read(*vals) -> list:
+    """Host values of scalar device tensors (one synchronisation): copied into
+    pinned memory and waited for with an event -- a pageable read holds the
+    driver while it waits, stalling other threads' uploads (the host-buffer
+    entry points stage the next chunk's rays on a thread meanwhile)."""
+    t = torch.stack([v.reshape(()).to(torch.int64) for v in vals])
+    h = torch.empty(t.shape, dtype=torch.int64, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    ev.synchronize()
+    return [int(x) for x in h.tolist()]
+
+
 def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
@@ -219,7 +233,7 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
         _lib.check(lib.hp_query_count(*args, _ptr(offsets), _ptr(probes), _ptr(scanned), cap, _ptr(ws),
                                       nb.value, _stream()))
         _mark("query.count")
-        total = int(offsets[m].item())
+        total = _host_read(offsets[m])[0]
         if total >= 0:
             break
         if _ == 1:
@@ -347,7 +361,7 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
         return offsets, head_off, probes, scanned, None, min(cap, HEAD_CAP * max(m, 1)), ws, nb.value, cap
     # read first: the exact scratch need from the (cheap) bound pass -- a
     # count over a short capacity still streams every group placed below it
-    need = int(query_bounds(index, pixels, dirs, t_near, t_far, slopes, footprint)[m])
+    need = _host_read(query_bounds(index, pixels, dirs, t_near, t_far, slopes, footprint)[m])[0]
     if max_scratch is not None and need > max_scratch:
         if frame:
             _DEFER_OK[dev] = False  # frames of this size run in chunks
@@ -363,8 +377,7 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
         _lib.check(lib.hp_head_count(*args, _ptr(offsets), _ptr(head_off), _ptr(probes), _ptr(scanned), cap,
                                      _ptr(ws), nb.value, _stream()))
         _mark("query.count")
-        both = torch.stack([offsets[m], head_off[m]]).cpu()  # one synchronisation
-        total, hcap = int(both[0]), int(both[1])
+        total, hcap = _host_read(offsets[m], head_off[m])  # one synchronisation
         if total >= 0:
             if _ == 0 and frame:
                 _DEFER_OK[dev] = True  # the remembered size fits: later frames may defer the read
@@ -538,7 +551,7 @@ def sample(offsets: torch.Tensor, ids: torch.Tensor, t: torch.Tensor, dist: torc
         run_args = common[:8] + (_ptr(facts) if facts is not None else ctypes.c_void_p(0),) + common[8:]
         _lib.check(lib.hp_sample_run(*run_args, _ptr(r_off), _ptr(t_end), _ptr(ws), nb.value, _stream()))
         _mark("sample.run")
-        R = int(r_off[m].item())
+        R = _host_read(r_off[m])[0]
         if R >= 0:
             break
         exact_cap = int(-R * 1.0625) + 1024   # exact scratch too small: grow it once
@@ -602,8 +615,8 @@ def sample_prefix(pre: QueryPrefix, slopes: torch.Tensor, cfg, colors: torch.Ten
         vals = [r_off[m], flagged[m].to(torch.int64)]
         if pre.total is None:  # deferred count: Q (or a short count) read here too
             vals.append(pre.offsets[m])
-        both = torch.stack(vals).cpu()  # one synchronisation
-        R, n_flagged = int(both[0]), int(both[1])
+        both = _host_read(*vals)  # one synchronisation
+        R, n_flagged = both[0], both[1]
         if pre.total is None:
             pre.total = int(both[2])
             if pre.total < 0:

@@ -26,7 +26,9 @@ __all__ = ["FrameResult", "frame_device", "search_and_sample", "search_and_sampl
 
 
 SLOPE_THREADS = int(os.environ.get("HP_SLOPE_THREADS", "0")) or min(16, os.cpu_count() or 1)
-H2D_THREADS = int(os.environ.get("HP_H2D_THREADS", "0")) or min(2, os.cpu_count() or 1)
+H2D_THREADS = int(os.environ.get("HP_H2D_THREADS", "0")) or min(4, os.cpu_count() or 1)
+# pageable uploads through hp_host_upload (host threads + pinned staging) instead of the driver's own path
+H2D_STAGED = os.environ.get("HP_H2D_STAGED", "1") == "1"
 
 
 def host_slopes(camera, pixels: np.ndarray | None, kernel_radius: float, approx: bool = False,
@@ -427,8 +429,8 @@ def _h2d(a, dev, dtype) -> torch.Tensor:
     np_dt = torch.empty((), dtype=dtype).numpy().dtype
     if arr.dtype != np_dt or not arr.flags.c_contiguous:
         arr = np.ascontiguousarray(arr, dtype=np_dt)
-    if arr.nbytes < H2D_PIECE:
-        return torch.from_numpy(arr).to(dev, non_blocking=True)
+    if arr.nbytes < H2D_PIECE or not H2D_STAGED:
+        return torch.from_numpy(arr).to(dev, non_blocking=True)  # the driver's pageable path (~20 GB/s here)
     with _INFLIGHT_LOCK:  # release the staging blocks whose copies have run
         _INFLIGHT[:] = [x for x in _INFLIGHT if not x[1].query()]
     stage = torch.empty(arr.nbytes, dtype=torch.uint8, pin_memory=True)  # caching host allocator: reused
@@ -500,25 +502,28 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     main = torch.cuda.current_stream()
     side = _side_stream(dev)  # persistent: the caching allocator pools blocks per stream
     side.wait_stream(main)
-    xyz = _h2d(cloud.positions, dev, torch.float64)
+    xyz = _h2d(cloud.positions, dev, torch.float64)          # the critical path: the build needs it
     idx = device.build(xyz, camera, search_cfg.pad)          # async on the stream
     px_host = pixels.numpy() if isinstance(pixels, torch.Tensor) else np.asarray(pixels)
     px_host = np.ascontiguousarray(px_host, dtype=np.int64).reshape(-1, 2)
     m = px_host.shape[0]
     cuts = _ray_chunks(m)
-    # the rays go up (staged on a coordinator thread) while the build runs and
-    # the host slopes are computed; the colours after them, while the query runs
-    rays_up = _h2d_async(side, dev, (_host_rays(pixels, m, torch.int64, 2), torch.int64),
-                         (_host_rays(dirs, m, torch.float64, 3), torch.float64),
-                         (_host_rays(t_near, m, torch.float64), torch.float64),
-                         (_host_rays(t_far, m, torch.float64), torch.float64))
+    # uploads on a coordinator thread, in the order the device needs them: the
+    # first chunk's rays (while the build runs and the host slopes are
+    # computed), the colours (the first chunk's sampler), the other chunks' rays
+    h_rays = (_host_rays(pixels, m, torch.int64, 2), _host_rays(dirs, m, torch.float64, 3),
+              _host_rays(t_near, m, torch.float64), _host_rays(t_far, m, torch.float64))
+    kinds = (torch.int64, torch.float64, torch.float64, torch.float64)
+    ray_up = [_h2d_async(side, dev, *[(h[cuts[0]:cuts[1]], k) for h, k in zip(h_rays, kinds)])]
     cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
+    ray_up += [_h2d_async(side, dev, *[(h[a:b], k) for h, k in zip(h_rays, kinds)])
+               for a, b in zip(cuts[1:-1], cuts[2:])]
     sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
     host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
     sl = sl_host.to(dev, non_blocking=True)
-    pix_d, dirs_d, tn, tf = rays_up()
     cfg = sampler_cfg or SamplerConfig()
     col = []
+    chunk_of = {a: i for i, a in enumerate(cuts[:-1])}
 
     def colours():  # resolved by _query_sample right before its sampler
         if not col:
@@ -526,8 +531,8 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
         return col[0]
 
     def run_chunk(a, b):
-        return _query_sample(idx, colours, pix_d[a:b], dirs_d[a:b], tn[a:b], tf[a:b], sl[a:b], cfg, exact_t_end,
-                             max_matches).samples
+        pix_d, dirs_d, tn, tf = ray_up[chunk_of[a]]()  # waits for this chunk's uploads only
+        return _query_sample(idx, colours, pix_d, dirs_d, tn, tf, sl[a:b], cfg, exact_t_end, max_matches).samples
 
     return _samples_to_host(run_chunk, cuts, dev)
 

@@ -19,6 +19,14 @@ def sl(*a, **k):
 def bd(*a, **k):
     T.append(("build", time.perf_counter())); return orig_b(*a, **k)
 pipeline.host_slopes, pipeline.device.build = sl, bd
+orig_h2d, orig_up = pipeline._h2d, pipeline._h2d_async
+def h2d(*a, **k):
+    T.append(("h2d+", time.perf_counter())); r = orig_h2d(*a, **k); T.append(("h2d-", time.perf_counter())); return r
+pipeline._h2d = h2d
+def s2h(*a, **k):
+    T.append(("s2h+", time.perf_counter())); r = orig_s2h(*a, **k); T.append(("s2h-", time.perf_counter())); return r
+orig_s2h = pipeline._samples_to_host
+pipeline._samples_to_host = s2h
 def qs(*a, **k):
     T.append(("qs+", time.perf_counter())); r = orig_qs(*a, **k); T.append(("qs-", time.perf_counter())); return r
 def hb(*a, **k):
