@@ -608,7 +608,13 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
         // (the trimmed pairs, t >= T_c, end up last in the order below)
         const double d0 = dirs[3 * r], d1 = dirs[3 * r + 1], d2v = dirs[3 * r + 2];
         const double Tc = (all || kc == 0xffffffffu) ? CUDART_INF : double(from_fkey(kc + 1u));
-        unsigned thi = 0u;
+        // the rank's coarse map, counted in the same pass: [lower bound of every
+        // t, T_c (cut rays) or the largest key (whole rays)]; a t above it lands
+        // in the last bin (the map stays monotone: the order is unchanged)
+        const float tlo = from_fkey(M.kmin);
+        const float thi = all ? from_fkey(M.kmax) : float(Tc);
+        const float cscale = coarse_scale(tlo, thi);
+        const bool coarse = S > 64;  // rank_segment ranks up to 64 directly
         int nkeep = 0;
         for (int e = tid; e < S; e += kT) {
             const double4 a = rel4[F.slot[e]];
@@ -617,18 +623,19 @@ __global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head
             F.d2[e] = cone_dist2(a.x, a.y, a.z, t, d0, d1, d2v);
             F.id[e] = int(__double_as_longlong(a.w));
             nkeep += t < Tc;
-            thi = max(thi, fkey(__double2float_rn(t)));
+            if (coarse) {  // CTA-uniform
+                const float x = coarse_of(t, tlo, cscale);
+                F.bk[e] = __float_as_uint(x);  // over slot[e], read above by this thread
+                const int b = min(int(x), kCoarse - 1);
+                const unsigned peers = __match_any_sync(__activemask(), b);
+                if (lane_id() == __ffs(peers) - 1) atomicAdd(&F.chist[b], __popc(peers));
+            }
         }
-        thi = __reduce_max_sync(0xffffffffu, thi);
         nkeep = warp_sum(nkeep);
-        if (lane_id() == 0) {
-            atomicMax(&F.thi, thi);
-            if (nkeep) atomicAdd(&F.keep, nkeep);
-        }
-        __syncthreads();  // every slot read (bk may now be overwritten)
+        if (lane_id() == 0 && nkeep) atomicAdd(&F.keep, nkeep);
+        __syncthreads();
         if (S > 0)
-            rank_segment<kCap, kT>(S, from_fkey(M.kmin), from_fkey(F.thi), F.t, F.id, F.bk, F.hist, F.lst, F.perm,
-                                   F.chist, F.scan_sh);
+            rank_segment<kCap, kT, true>(S, tlo, thi, F.t, F.id, F.bk, F.hist, F.lst, F.perm, F.chist, F.scan_sh);
         const int Lh = F.keep;
         const int64_t ho = hoff[i];
         HP_ASSERT(Lh <= S && ho + Lh <= hoff[i + 1]);

@@ -142,7 +142,18 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
 // proportion -> linear inside a bin; fp32, every step monotone) and an exact
 // rank inside each bucket.  hist needs kCap + 1 entries; chist kCoarse + 1
 // (both zeroed by the caller when q > 64).  Ends with a barrier.
-template <int kCap, int kT>
+// kPreCoarse: the caller has already placed every element's coarse
+// coordinate in bk[] and counted chist (with coarse_of below), and synced.
+__device__ __forceinline__ float coarse_of(double t, float tlo, float cscale) {
+    return fminf((__double2float_rn(t) - tlo) * cscale, float(kCoarse));
+}
+__device__ __forceinline__ float coarse_scale(float tlo, float thi) {
+    const float span = thi - tlo;
+    // capped so that 0 * scale stays 0 when the span is tiny
+    return span > 0.0f ? fminf(float(kCoarse) / span, FLT_MAX) : 0.0f;
+}
+
+template <int kCap, int kT, bool kPreCoarse = false>
 __device__ void rank_segment(int q, float tlo, float thi, const double* t, const int* id, unsigned* bk, int* hist,
                              unsigned short* lst, unsigned short* perm, int* chist, int* scan_sh) {
     const int tid = threadIdx.x;
@@ -162,17 +173,17 @@ __device__ void rank_segment(int q, float tlo, float thi, const double* t, const
         // The map is computed in fp32 (each step is monotone under round to
         // nearest: float(t), - tlo, * scale, fminf), once per element; the
         // coarse coordinate is kept in bk[] for the fine pass.
-        const float span = thi - tlo;
-        // capped so that 0 * scale stays 0 when the span is tiny
-        const float cscale = span > 0.0f ? fminf(float(kCoarse) / span, FLT_MAX) : 0.0f;
-        for (int e = tid; e < q; e += kT) {
-            const float x = fminf((__double2float_rn(t[e]) - tlo) * cscale, float(kCoarse));
-            bk[e] = __float_as_uint(x);
-            const int b = min(int(x), kCoarse - 1);
-            const unsigned peers = __match_any_sync(__activemask(), b);
-            if (lane_id() == __ffs(peers) - 1) atomicAdd(&chist[b], __popc(peers));
+        if (!kPreCoarse) {
+            const float cscale = coarse_scale(tlo, thi);
+            for (int e = tid; e < q; e += kT) {
+                const float x = coarse_of(t[e], tlo, cscale);
+                bk[e] = __float_as_uint(x);
+                const int b = min(int(x), kCoarse - 1);
+                const unsigned peers = __match_any_sync(__activemask(), b);
+                if (lane_id() == __ffs(peers) - 1) atomicAdd(&chist[b], __popc(peers));
+            }
+            __syncthreads();
         }
-        __syncthreads();
         // coarse prefix counts -> first fine bucket of each coarse bin
         if (tid < 32) {
             int run = 0;
