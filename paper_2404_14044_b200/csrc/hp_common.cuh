@@ -151,7 +151,8 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
 
 // Block-wide exclusive scan of one value per thread; returns the exclusive
 // prefix, writes the block total to *total.  `sh` needs blockDim/32 + 1 slots.
-template <class T>
+// kTail = false: no trailing barrier (the caller syncs before `sh` is reused).
+template <class T, bool kTail = true>
 __device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
     const int nw = blockDim.x >> 5;
     T inc = warp_incl_scan(v);
@@ -166,7 +167,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
     __syncthreads();
     T res = inc - v + sh[warp_id()];
     *total = sh[nw];
-    __syncthreads();
+    if (kTail) __syncthreads();
     return res;
 }
 

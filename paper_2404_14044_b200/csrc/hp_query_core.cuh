@@ -120,7 +120,7 @@ __device__ void block_scan_inplace(int* a, int n, int* sh) {
         acc += v[k];
     }
     int total;
-    int run = block_excl_scan<int>(acc, sh, &total);
+    int run = block_excl_scan<int, false>(acc, sh, &total);  // callers sync before sh is reused
 #pragma unroll
     for (int k = 0; k < kPer; k++) {
         const int i = tid * kPer + k;
