@@ -459,6 +459,15 @@ struct Chain {
 __device__ __forceinline__ bool chain_chunk(Chain& S, double u, int c0, int n, int q, double thr, const Params& P) {
     const int lane = lane_id();
     if (!S.seq) {
+        // Tail proof without the sequential chain: below 2^-1022 the
+        // reference's T is n units of 2^-1074, and a factor <= 1/2 maps n to
+        // at most ceil(n / 2) (round to nearest even; 1 -> 0).  From T <= Vs <=
+        // 2^-1049 (n <= 2^25), 26 factors <= 1/2 reach exactly 0.
+        if (S.Vs <= 0x1p-1049 && S.je < q && n >= 26 &&
+            __all_sync(0xffffffffu, lane >= n || u <= 0.5)) {
+            S.proved_zero = true;
+            return true;
+        }
         double Pl = u;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -476,7 +485,9 @@ __device__ __forceinline__ bool chain_chunk(Chain& S, double u, int c0, int n, i
             }
         }
         const double Vn = __shfl_sync(0xffffffffu, B, n - 1);
-        if (Vn >= 0x1p-1000) {
+        if (Vn >= 0x1p-1000 || (S.Vs >= 0x1p-1000 && S.je < q)) {
+            // far from underflow; or the first chunk below it: its end bound
+            // may open the tail proof above for the next chunk
             S.Vs = Vn;
             return !P.exact_t_end && S.je < q;
         }
