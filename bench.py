@@ -535,8 +535,15 @@ def run_ours(args, w, rank, world, dist):
         from paper_2404_14044_b200.pointnerf import PointNeRFMLP, render_step
         mlp = PointNeRFMLP(w["cloud"].count, seed=0, device_=dev)
 
+    # a row band (N > 1): the index holds only the points its rays can reach
+    band_rows = None
+    if world > 1 and r1 > r0:
+        v = w["pixels"][r0:r1, 1]
+        band_rows = (int(v.min()), int(v.max()) + 1)
+
     def step(timer=None):
-        fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer, emit_knn=render)
+        fr = pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, scfg, True, timer, emit_knn=render,
+                                   rows=band_rows)
         if render:  # the full render step: aggregation MLP + compositing of this rank's rays
             fr.image = render_step(mlp, fr.samples, rays[1], w["cam"].origin, xyz, rays[0], rays[3],
                                    w["cam"].width, w["cam"].height)
@@ -619,7 +626,8 @@ def run_ours(args, w, rank, world, dist):
     st = plen_fr.prefix_len.cpu().numpy() if plen_fr.prefix_len is not None else np.zeros(4, np.int64)
     plen, q_cut, q_whole, hit = (int(x) for x in st)
     kbytes = {
-        "hp_build": 24 * n + 16 * P + 32 * n_in + 4 * (P + 1) + 44 * n_in + 32 * n_in,
+        # the query layout alone: xyz in, counts / scan / row pointers, 100 B out per placed point
+        "hp_build": 24 * n + 16 * P + 4 * (P + 1) + 4 * n + 100 * n_in,
         "k_query_bound": 64 * m_loc + 4 * (P + 1) + 8 * m_loc,
         # rays in (64 B), row pointers, the fp32 copies (16 B / point), 8 B per
         # match out, per-ray counts / head counts / key bounds / probes / scanned

@@ -117,6 +117,16 @@ int hp_build(const double* positions, int64_t n, const hp_camera* cam, int64_t p
              double* slot_x, double* slot_y, double* slot_z, hp_query_layout layout,
              int64_t* n_in, void* workspace, size_t workspace_bytes, hp_stream_t stream);
 
+/* The query layout alone (no reference HashIndex arrays) for the padded rows
+ * [row0, row1) (row1 <= 0: all): what a frame that only queries needs (the
+ * points outside the rows are left out; inside a pixel the order is
+ * arbitrary -- the query ranks matches by (t, id)).  n_in [1] (device) = the
+ * placed points.  Rays of image rows [a, b) reach padded rows [a, b + 2 pad). */
+int hp_build_layout_workspace_bytes(int64_t n, int64_t padded_w, int64_t padded_h, size_t* bytes);
+int hp_build_layout(const double* positions, int64_t n, const hp_camera* cam, int64_t pad, int64_t row0,
+                    int64_t row1, hp_query_layout layout, int64_t* n_in, void* workspace, size_t workspace_bytes,
+                    hp_stream_t stream);
+
 /* The reference's counting-sort placement operator on its own
  * (_kernels.scatter_by_bucket, _kernels.py:76-83): for j in input order,
  * out_ids[cursor[buckets[j]]++] = orig_ids[j].  buckets / orig_ids int64 [n],

@@ -50,6 +50,9 @@ _SIGNATURES = {
     "hp_version": (ctypes.c_int, []),
     "hp_launch_count": (c_i64, []),
     "hp_build_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_build_layout_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "hp_build_layout": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, Layout, c_p, c_p,
+                                       c_size, c_p]),
     "hp_build": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(Camera), c_i64, c_p, c_p, c_p, c_p, c_p,
                                 c_p, Layout, c_p, c_p, c_size, c_p]),
     "hp_scatter_by_bucket_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),

@@ -9,6 +9,8 @@
 // see DESIGN.md "projection"), table starts follow the Morton order of the
 // padded pixel grid, empty pixels get start 0, and points inside a pixel are
 // ordered by ascending original index.
+#include <climits>
+
 #include "hp_common.cuh"
 #include "hp_cone.cuh"
 #include "hp_sortnet.cuh"
@@ -49,7 +51,8 @@ __device__ __forceinline__ int32_t bucket_of(const CamDev& c, double x, double y
 __global__ void __launch_bounds__(kProjThreads) k_project(const double* __restrict__ xyz, int64_t n,
                                                           CamDev cam, int pad, int wp, int hp,
                                                           int32_t* __restrict__ lin,
-                                                          int32_t* __restrict__ cnt) {
+                                                          int32_t* __restrict__ cnt, int row0 = 0,
+                                                          int row1 = INT_MAX) {
     __shared__ __align__(16) double tile[kProjThreads * 3];
     for (int64_t base = int64_t(blockIdx.x) * kProjThreads; base < n;
          base += int64_t(gridDim.x) * kProjThreads) {
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const double* __restri
         if (threadIdx.x < pts) {
             l = bucket_of(cam, tile[3 * threadIdx.x], tile[3 * threadIdx.x + 1],
                           tile[3 * threadIdx.x + 2], pad, wp, hp);
+            if (l >= 0 && (l / wp < row0 || l / wp >= row1)) l = -1;  // outside the row window
             lin[i] = l;
         }
         const unsigned act = __ballot_sync(0xffffffffu, l >= 0);
@@ -398,6 +402,115 @@ extern "C" int hp_build(const double* positions, int64_t n, const hp_camera* cam
                                                  reordered_ids, slot_x, slot_y, slot_z, layout);
         HP_CHECK_LAUNCH("k_gather");
     }
+    return HP_OK;
+}
+
+// Layout-only build (the query layout of the rows a frame's rays can reach,
+// no reference HashIndex arrays): every placed point goes straight to its
+// row-major slot (warp-aggregated cursor bumps, the order inside a pixel is
+// the atomics' -- the query ranks by (t, id), so results do not depend on it).
+__global__ void k_scatter_layout(int64_t n, const double* __restrict__ xyz, const int32_t* __restrict__ lin,
+                                 int32_t* __restrict__ cursor, double o0, double o1, double o2,
+                                 hp_query_layout L) {
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n; base += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int32_t l = i < n ? lin[i] : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, l >= 0);
+        if (l >= 0) {
+            const unsigned peers = __match_any_sync(act, l);
+            const int leader = __ffs(peers) - 1;
+            int32_t pos = 0;
+            if (lane_id() == leader) pos = atomicAdd(&cursor[l], __popc(peers));
+            pos = __shfl_sync(peers, pos, leader);
+            pos += __popc(peers & ((1u << lane_id()) - 1));
+            HP_ASSERT(pos >= 0 && pos < n);
+            const double rx = hp::dsub(xyz[3 * i], o0), ry = hp::dsub(xyz[3 * i + 1], o1),
+                         rz = hp::dsub(xyz[3 * i + 2], o2);
+            L.rel_x[pos] = rx;
+            L.rel_y[pos] = ry;
+            L.rel_z[pos] = rz;
+            L.point_id[pos] = int32_t(i);
+            reinterpret_cast<float4*>(L.relf)[pos] = filter_point(rx, ry, rz);
+            store_rel4(L.rel4, pos, rx, ry, rz, int32_t(i));
+        }
+    }
+}
+
+__global__ void k_layout_n_in(const int32_t* __restrict__ row_ptr, int64_t P, int64_t* __restrict__ n_in) {
+    *n_in = row_ptr[P];
+}
+
+extern "C" int hp_build_layout_workspace_bytes(int64_t n, int64_t padded_w, int64_t padded_h, size_t* bytes) {
+    const int64_t P = padded_w * padded_h;
+    const int64_t nn = n > 0 ? n : 1;
+    *bytes = 3 * 256 + ((sizeof(int32_t) * nn + 255) & ~size_t(255)) + 2 * ((sizeof(int32_t) * (P + 1) + 255) & ~size_t(255)) +
+             scan_workspace_bytes(P + 1) + 256;
+    return HP_OK;
+}
+
+extern "C" int hp_build_layout(const double* positions, int64_t n, const hp_camera* cam, int64_t pad, int64_t row0,
+                               int64_t row1, hp_query_layout layout, int64_t* n_in, void* workspace,
+                               size_t workspace_bytes, hp_stream_t stream) {
+    if (!cam || pad < 0 || n < 0) {
+        set_error("hp_build_layout: invalid arguments");
+        return HP_EINVAL;
+    }
+    const int64_t wp = cam->width + 2 * pad, hp_ = cam->height + 2 * pad;
+    if (wp > 0xFFFF || hp_ > 0xFFFF) {
+        set_error("padded image exceeds 16-bit pixel coordinates");
+        return HP_EINVAL;
+    }
+    if (n >= (int64_t(1) << 31)) {
+        set_error("hp_build_layout: point count must be below 2^31");
+        return HP_EINVAL;
+    }
+    const int64_t P = wp * hp_;
+    if (P >= (int64_t(1) << 31)) {
+        set_error("hp_build_layout: padded grid of %lld pixels must be below 2^31", (long long)P);
+        return HP_EINVAL;
+    }
+    Carver c(workspace, workspace_bytes);
+    int32_t* lin = c.take<int32_t>(n > 0 ? n : 1);
+    int32_t* cnt = c.take<int32_t>(P + 1);
+    int32_t* cursor = c.take<int32_t>(P + 1);
+    void* scan = c.take<char>(scan_workspace_bytes(P + 1));
+    if (!c.ok()) {
+        set_error("hp_build_layout: workspace too small");
+        return HP_ESPACE;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CamDev cd;
+    for (int k = 0; k < 3; k++) {
+        cd.o[k] = cam->origin[k];
+        cd.r[k] = cam->right[k];
+        cd.u[k] = cam->up[k];
+        cd.f[k] = cam->forward[k];
+    }
+    cd.focal = cam->focal_length;
+    cd.pw = cam->pixel_width;
+    cd.ph = cam->pixel_height;
+    cd.half_w = 0.5 * double(cam->width);
+    cd.half_h = 0.5 * double(cam->height);
+    const int r0 = int(row0 < 0 ? 0 : (row0 > hp_ ? hp_ : row0));
+    const int r1 = int(row1 <= 0 || row1 > hp_ ? hp_ : row1);
+    TimedSpan ts("hp_build", s);
+    if (cudaMemsetAsync(cnt, 0, sizeof(int32_t) * P, s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_build_layout memset");
+    if (n > 0) {
+        k_project<<<grid_for(n, kProjThreads, 148 * 16), kProjThreads, 0, s>>>(positions, n, cd, int(pad), int(wp),
+                                                                               int(hp_), lin, cnt, r0, r1);
+        HP_CHECK_LAUNCH("k_project");
+    }
+    HP_TRY(exclusive_scan_i32(cnt, layout.row_ptr, P, scan, s));
+    if (cudaMemcpyAsync(cursor, layout.row_ptr, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "hp_build_layout copy");
+    if (n > 0) {
+        k_scatter_layout<<<grid_for(n, 256), 256, 0, s>>>(n, positions, lin, cursor, cam->origin[0], cam->origin[1],
+                                                          cam->origin[2], layout);
+        HP_CHECK_LAUNCH("k_scatter_layout");
+    }
+    k_layout_n_in<<<1, 1, 0, s>>>(layout.row_ptr, P, n_in);
+    HP_CHECK_LAUNCH("k_layout_n_in");
     return HP_OK;
 }
 

@@ -110,6 +110,10 @@ class DeviceIndex:
     slot_y = property(lambda self: self._sy[: self.n_in])
     slot_z = property(lambda self: self._sz[: self.n_in])
 
+    @property
+    def device(self) -> torch.device:
+        return self.row_ptr.device
+
     def layout(self) -> _lib.Layout:
         return _lib.Layout(_ptr(self.row_ptr), _ptr(self.rel_x), _ptr(self.rel_y),
                            _ptr(self.rel_z), _ptr(self.point_id), _ptr(self.relf), _ptr(self.rel4))
@@ -149,6 +153,43 @@ def build(positions: torch.Tensor, camera, pad: int) -> DeviceIndex:
                             _stream()))
     _mark("build.kernels")
     return DeviceIndex(camera, pad, wp, hp, n_in_d, ts, tc, rid, sx, sy, sz, row_ptr, rx, ry, rz,
+                       pid, rf, r4, n_in=0 if n == 0 else None)
+
+
+def build_layout(positions: torch.Tensor, camera, pad: int, rows: tuple | None = None) -> DeviceIndex:
+    """The query layout alone (hp_build_layout): what a frame that only
+    queries needs, without the reference's HashIndex arrays (table_start ...
+    are None).  ``rows``: (a, b) image rows of the frame's rays -- only points
+    in the padded rows those rays reach, [a, b + 2 pad), are placed.  Inside a
+    pixel the order is arbitrary (the query ranks by (t, id))."""
+    lib = _lib.load(require_device=True)
+    pad = int(pad)
+    wp, hp = int(camera.width) + 2 * pad, int(camera.height) + 2 * pad
+    if max(wp, hp) > 0xFFFF:
+        raise ValueError("padded image exceeds 16-bit pixel coordinates")
+    dev = positions.device
+    xyz = positions.contiguous().view(-1, 3)
+    n = xyz.shape[0]
+    P = wp * hp
+    nb = c_size(0)
+    _lib.check(lib.hp_build_layout_workspace_bytes(n, wp, hp, ctypes.byref(nb)))
+    ws = _workspace(nb.value, dev)
+    cap = max(n, 1)
+    f64 = dict(dtype=torch.float64, device=dev)
+    row_ptr = torch.empty(P + 1, dtype=torch.int32, device=dev)
+    rx, ry, rz = (torch.empty(cap, **f64) for _ in range(3))
+    pid = torch.empty(cap, dtype=torch.int32, device=dev)
+    rf = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    r4 = torch.empty((cap, 4), **f64)
+    n_in_d = torch.zeros(1, dtype=torch.int64, device=dev)
+    r0, r1 = (0, 0) if rows is None else (int(rows[0]), int(rows[1]) + 2 * pad)
+    _mark("build.setup")
+    L = _lib.Layout(_ptr(row_ptr), _ptr(rx), _ptr(ry), _ptr(rz), _ptr(pid), _ptr(rf), _ptr(r4))
+    cam = camera_struct(camera)
+    _lib.check(lib.hp_build_layout(_ptr(xyz), n, ctypes.byref(cam), pad, r0, r1, L, _ptr(n_in_d), _ptr(ws),
+                                   nb.value, _stream()))
+    _mark("build.kernels")
+    return DeviceIndex(camera, pad, wp, hp, n_in_d, None, None, None, None, None, None, row_ptr, rx, ry, rz,
                        pid, rf, r4, n_in=0 if n == 0 else None)
 
 
@@ -193,7 +234,7 @@ def query_bounds(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
     """Exclusive scan of the per-ray match upper bounds (hp_query_bounds),
     int64 [m+1]; used to split a frame into ray chunks that fit memory."""
     lib = _lib.load(require_device=True)
-    dev = index.table_start.device
+    dev = index.row_ptr.device
     m = int(pixels.shape[0])
     pixels, dirs = pixels.contiguous(), dirs.contiguous()
     nb = c_size(0)
@@ -211,7 +252,7 @@ def _count(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scratch):
     """hp_query_count with the workspace sized (retrying once); returns
     (offsets, probes, scanned, total, workspace, workspace bytes, capacity)."""
     lib = _lib.load(require_device=True)
-    dev = index.table_start.device
+    dev = index.row_ptr.device
     m = int(pixels.shape[0])
     nb = c_size(0)
     offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
@@ -268,7 +309,7 @@ def query(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: 
 def _fill(index, counted, slopes, facts):
     """hp_query_fill after :func:`_count`: the (t, id)-sorted CSR."""
     lib = _lib.load(require_device=True)
-    dev = index.table_start.device
+    dev = index.row_ptr.device
     offsets, probes, scanned, total, ws, nb, cap = counted
     m = int(offsets.shape[0]) - 1
     ids = torch.empty(total, dtype=torch.int64, device=dev)
@@ -337,7 +378,7 @@ def _count_head(index, pixels, dirs, t_near, t_far, slopes, footprint, max_scrat
     the scratch capacity; the caller checks offsets[m] later).  ``frame``: a
     whole frame's count (its outcome decides whether later frames defer)."""
     lib = _lib.load(require_device=True)
-    dev = index.table_start.device
+    dev = index.row_ptr.device
     m = int(pixels.shape[0])
     nb = c_size(0)
     offsets = torch.empty(m + 1, dtype=torch.int64, device=dev)
@@ -414,7 +455,7 @@ def _head(index, counted, dirs, slopes, want=None, whole=None, sampler_cfg=None)
     heads carry the sampler's precomputed bound factors."""
     want = PREFIX_WANT if want is None else want
     lib = _lib.load(require_device=True)
-    dev = index.table_start.device
+    dev = index.row_ptr.device
     offsets, head_off, probes, scanned, total, hcap, ws, nb, cap = counted
     m = int(offsets.shape[0]) - 1
     fa = torch.empty(m, dtype=torch.int32, device=dev)

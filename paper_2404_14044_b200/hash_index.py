@@ -187,7 +187,7 @@ def query_batch_arrays(index: HashIndex, pixels, dirs, t_near, t_far, config=Non
 
 def query_device_arrays(index: HashIndex, pixels, dirs, t_near, t_far, slopes):
     """Host arrays in, CUDA tensors out (H2D of the rays, no D2H)."""
-    dev = index.device.table_start.device
+    dev = index.device.device
 
     def up(a, dt):
         return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)

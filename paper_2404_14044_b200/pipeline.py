@@ -136,17 +136,21 @@ def _concat_samples(parts):
 def frame_device(xyz: torch.Tensor, colors: torch.Tensor | None, camera, search_cfg, pixels,
                  dirs, t_near, t_far, slopes, sampler_cfg: SamplerConfig | None = None,
                  exact_t_end: bool = True, timer: StageTimer | None = None,
-                 max_matches: int | None = None, emit_knn: bool = False) -> FrameResult:
+                 max_matches: int | None = None, emit_knn: bool = False,
+                 rows: tuple | None = None) -> FrameResult:
     """build -> query -> sample, all on the device (CUDA tensors in and out).
 
     A frame whose query would need more than ``max_matches`` match slots
     (default: :func:`match_budget`) runs in ray chunks (ray-chunk
     streaming): the per-ray bounds split the rays, each chunk is queried and
     sampled in turn, and only the retained samples are kept.  Results are
-    identical (rays are independent)."""
+    identical (rays are independent).  The index is the query layout alone
+    (device.build_layout: no reference HashIndex arrays); ``rows`` = (a, b)
+    when every ray lies in image rows [a, b) (a row band): only the points
+    those rays can reach are placed."""
     mark = timer.mark if timer is not None else (lambda name: None)
     mark("start")
-    idx = device.build(xyz, camera, search_cfg.pad)
+    idx = device.build_layout(xyz, camera, search_cfg.pad, rows)
     mark("build")
     return _query_sample(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg or SamplerConfig(),
                          exact_t_end, max_matches, mark, emit_knn=emit_knn)
@@ -299,7 +303,7 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
         cuts.append(min(b, m))
     # every chunk's scratch need is below its bound: size the counts for the
     # largest chunk up front (a count over a short capacity wastes a pass)
-    dev = idx.table_start.device
+    dev = idx.device
     big = max(int(bo[b] - bo[a]) for a, b in zip(cuts[:-1], cuts[1:]))
     device._QUERY_CAP[dev] = max(device._QUERY_CAP.get(dev, 0), big)
     parts, Q, nf, nr = [], 0, 0, 0
@@ -503,7 +507,7 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     side = _side_stream(dev)  # persistent: the caching allocator pools blocks per stream
     side.wait_stream(main)
     xyz = _h2d(cloud.positions, dev, torch.float64)          # the critical path: the build needs it
-    idx = device.build(xyz, camera, search_cfg.pad)          # async on the stream
+    idx = device.build_layout(xyz, camera, search_cfg.pad)   # async on the stream
     px_host = pixels.numpy() if isinstance(pixels, torch.Tensor) else np.asarray(pixels)
     px_host = np.ascontiguousarray(px_host, dtype=np.int64).reshape(-1, 2)
     m = px_host.shape[0]
@@ -552,7 +556,7 @@ def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: floa
     side = _side_stream(dev)
     side.wait_stream(main)
     xyz = _h2d(cloud.positions, dev, torch.float64)
-    idx = device.build(xyz, camera, search_cfg.pad)
+    idx = device.build_layout(xyz, camera, search_cfg.pad)
     dirs, pixels, tn, tf = device.ray_grid(camera, dev, t_near=t_near, t_far=t_far)
     m = int(dirs.shape[0])
     cuts = _ray_chunks(m)

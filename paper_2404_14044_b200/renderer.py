@@ -120,7 +120,7 @@ def _render(index: HashIndex, rays: list, search_cfg, sampler_cfg, render_cfg: R
     if m == 0:
         return image
     lib = device._lib.load(require_device=True)
-    dev = index.device.table_start.device
+    dev = index.device.device
     up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
     slopes = radius_slopes(cam, pixels, search_cfg.kernel_radius, search_cfg.use_approx_radius)
     pix_d, tf_d = up(pixels, np.int64), up(t_far, np.float64)

@@ -163,8 +163,9 @@ def search_and_sample_distributed(cloud, camera, search_cfg, t_near: float, t_fa
     if with_colors and cloud.colors is not None:
         col = torch.from_numpy(np.ascontiguousarray(cloud.colors)).to(dev, dtype=torch.float64,
                                                                       non_blocking=True)
-    idx = device.build(xyz, camera, search_cfg.pad)
-    y0, y1 = balanced_row_bands(None, camera, search_cfg.pad, world, table_count=idx.table_count)[rank]
+    idx = device.build_layout(xyz, camera, search_cfg.pad)  # the query layout of the whole view
+    counts = (idx.row_ptr[1:] - idx.row_ptr[:-1]).to(torch.int64)  # points per padded pixel (row-major)
+    y0, y1 = balanced_row_bands(None, camera, search_cfg.pad, world, table_count=counts)[rank]
     W = int(camera.width)
     dirs, pixels, tn, tf = device.ray_grid(camera, dev, row0=y0, rows=y1 - y0, t_near=t_near, t_far=t_far)
     m = (y1 - y0) * W

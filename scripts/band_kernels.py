@@ -13,6 +13,8 @@ xyz, col = up(w["cloud"].positions), up(w["cloud"].colors)
 n, k = (int(x) for x in (sys.argv[1:3] if len(sys.argv) > 2 else (8, 3)))
 r0, r1 = bench.row_bands(w, n, k)
 rays = [up(w[x][r0:r1]) for x in ("pixels", "dirs", "t_near", "t_far", "slopes")]
+vv = w["pixels"][r0:r1, 1]
+rows = (int(vv.min()), int(vv.max()) + 1) if n > 1 else None
 tot, kern, cnt = [], {}, {}
 for it in range(8):
     torch.cuda.synchronize()
@@ -20,7 +22,7 @@ for it in range(8):
         _lib.timing_enable(True); _lib.timing_collect()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, SamplerConfig(), True)
+    pipeline.frame_device(xyz, col, w["cam"], w["cfg"], *rays, SamplerConfig(), True, rows=rows)
     e1.record(); torch.cuda.synchronize()
     if it >= 3:
         tot.append(e0.elapsed_time(e1))

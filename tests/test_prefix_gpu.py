@@ -251,7 +251,7 @@ def test_deferred_count_short_and_chunk_switch(monkeypatch):
     idx = dv.build(xyz, cam, cfg.pad)
     sc = hp.SamplerConfig()
     full = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=False)
-    dev = idx.table_start.device  # the library's per-device key (cuda:N)
+    dev = idx.device  # the library's per-device key (cuda:N)
     monkeypatch.setitem(dv._QUERY_CAP, dev, 1000)      # far below this frame's Q
     monkeypatch.setitem(dv._DEFER_OK, dev, True)
     calls = []
