@@ -409,30 +409,22 @@ extern "C" int hp_build(const double* positions, int64_t n, const hp_camera* cam
 // no reference HashIndex arrays): every placed point goes straight to its
 // row-major slot (warp-aggregated cursor bumps, the order inside a pixel is
 // the atomics' -- the query ranks by (t, id), so results do not depend on it).
-__global__ void k_scatter_layout(int64_t n, const double* __restrict__ xyz, const int32_t* __restrict__ lin,
-                                 int32_t* __restrict__ cursor, double o0, double o1, double o2,
-                                 hp_query_layout L) {
-    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n; base += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const int32_t l = i < n ? lin[i] : -1;
-        const unsigned act = __ballot_sync(0xffffffffu, l >= 0);
-        if (l >= 0) {
-            const unsigned peers = __match_any_sync(act, l);
-            const int leader = __ffs(peers) - 1;
-            int32_t pos = 0;
-            if (lane_id() == leader) pos = atomicAdd(&cursor[l], __popc(peers));
-            pos = __shfl_sync(peers, pos, leader);
-            pos += __popc(peers & ((1u << lane_id()) - 1));
-            HP_ASSERT(pos >= 0 && pos < n);
-            const double rx = hp::dsub(xyz[3 * i], o0), ry = hp::dsub(xyz[3 * i + 1], o1),
-                         rz = hp::dsub(xyz[3 * i + 2], o2);
-            L.rel_x[pos] = rx;
-            L.rel_y[pos] = ry;
-            L.rel_z[pos] = rz;
-            L.point_id[pos] = int32_t(i);
-            reinterpret_cast<float4*>(L.relf)[pos] = filter_point(rx, ry, rz);
-            store_rel4(L.rel4, pos, rx, ry, rz, int32_t(i));
-        }
+// (slot -> point by the scatter of k_scatter, then this gather: the layout's
+// writes stay coalesced, the reads of the points are the random ones)
+__global__ void k_gather_layout(const int64_t* __restrict__ n_in_dev, const double* __restrict__ xyz,
+                                const int32_t* __restrict__ slot_pid, double o0, double o1, double o2,
+                                hp_query_layout L) {
+    const int64_t n_in = *n_in_dev;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n_in; k += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t id = slot_pid[k];
+        const double rx = hp::dsub(xyz[3 * int64_t(id)], o0), ry = hp::dsub(xyz[3 * int64_t(id) + 1], o1),
+                     rz = hp::dsub(xyz[3 * int64_t(id) + 2], o2);
+        L.rel_x[k] = rx;
+        L.rel_y[k] = ry;
+        L.rel_z[k] = rz;
+        L.point_id[k] = id;
+        reinterpret_cast<float4*>(L.relf)[k] = filter_point(rx, ry, rz);
+        store_rel4(L.rel4, k, rx, ry, rz, id);
     }
 }
 
@@ -443,8 +435,8 @@ __global__ void k_layout_n_in(const int32_t* __restrict__ row_ptr, int64_t P, in
 extern "C" int hp_build_layout_workspace_bytes(int64_t n, int64_t padded_w, int64_t padded_h, size_t* bytes) {
     const int64_t P = padded_w * padded_h;
     const int64_t nn = n > 0 ? n : 1;
-    *bytes = 3 * 256 + ((sizeof(int32_t) * nn + 255) & ~size_t(255)) + 2 * ((sizeof(int32_t) * (P + 1) + 255) & ~size_t(255)) +
-             scan_workspace_bytes(P + 1) + 256;
+    *bytes = 4 * 256 + 2 * ((sizeof(int32_t) * nn + 255) & ~size_t(255)) +
+             2 * ((sizeof(int32_t) * (P + 1) + 255) & ~size_t(255)) + scan_workspace_bytes(P + 1) + 256;
     return HP_OK;
 }
 
@@ -471,6 +463,7 @@ extern "C" int hp_build_layout(const double* positions, int64_t n, const hp_came
     }
     Carver c(workspace, workspace_bytes);
     int32_t* lin = c.take<int32_t>(n > 0 ? n : 1);
+    int32_t* slot_pid = c.take<int32_t>(n > 0 ? n : 1);
     int32_t* cnt = c.take<int32_t>(P + 1);
     int32_t* cursor = c.take<int32_t>(P + 1);
     void* scan = c.take<char>(scan_workspace_bytes(P + 1));
@@ -504,13 +497,15 @@ extern "C" int hp_build_layout(const double* positions, int64_t n, const hp_came
     HP_TRY(exclusive_scan_i32(cnt, layout.row_ptr, P, scan, s));
     if (cudaMemcpyAsync(cursor, layout.row_ptr, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "hp_build_layout copy");
-    if (n > 0) {
-        k_scatter_layout<<<grid_for(n, 256), 256, 0, s>>>(n, positions, lin, cursor, cam->origin[0], cam->origin[1],
-                                                          cam->origin[2], layout);
-        HP_CHECK_LAUNCH("k_scatter_layout");
-    }
     k_layout_n_in<<<1, 1, 0, s>>>(layout.row_ptr, P, n_in);
     HP_CHECK_LAUNCH("k_layout_n_in");
+    if (n > 0) {
+        k_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, lin, cursor, slot_pid);
+        HP_CHECK_LAUNCH("k_scatter");
+        k_gather_layout<<<grid_for(n, 256), 256, 0, s>>>(n_in, positions, slot_pid, cam->origin[0], cam->origin[1],
+                                                         cam->origin[2], layout);
+        HP_CHECK_LAUNCH("k_gather_layout");
+    }
     return HP_OK;
 }
 
