@@ -12,9 +12,10 @@
 // the head, from the L2-resident layout, with the reference's own expression
 // (bit-identical: cone_t / cone_dist2 of hp_cone.cuh).
 //
-//   k_query_bound  (hp_query_core.cuh) per-ray footprint bound -> scratch offsets
-//   k_head_scan    the streaming pass: a CTA owns a group of <= 32 adjacent
-//                  rays and streams the union of their footprint rows through
+//   k_head_scan    the streaming pass: a CTA claims a group of <= 32 adjacent
+//                  rays, places their scratch segments (each ray's footprint
+//                  slot count, one cursor atomic per group) and streams the
+//                  union of their footprint rows through
 //                  shared memory, fp32 copies only (16 B per point), staged by
 //                  1-D bulk copies (cp.async.bulk + mbarrier); the fp32 filter
 //                  settles almost every pair; the few uncertain pairs are
@@ -58,9 +59,6 @@ constexpr int kMaxPieces = 8;          // row pieces per chunk
 #ifndef HP_SELECT_U
 #define HP_SELECT_U 8  // keys (and slots) per lane in flight in k_head_select
 #endif
-#ifndef HP_HEAD_SORT_U
-#define HP_HEAD_SORT_U 8  // keys + slots of a cut ray streamed per thread per round
-#endif
 
 // ---------------------------------------------------------------- bulk copies
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
@@ -93,10 +91,12 @@ __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1
 
 // ---------------------------------------------------------------- scan
 // stream_group (hp_query.cu) with the chunks staged by bulk copies: thread 0
-// arms the buffer's mbarrier and issues one copy of the chunk's contiguous
-// slot range; every thread waits on the barrier's phase (tracked in `phase`,
-// bit b = parity of buffer b's next completion).  Chunk i + 1 is in flight
-// while chunk i is tested.
+// packs a chunk from consecutive rows' staged ranges ("pieces"), arms the
+// buffer's mbarrier and issues one bulk copy per piece; every thread waits on
+// the barrier's phase (tracked in `phase`, bit b = parity of buffer b's next
+// completion).  Chunk i + 1 is in flight while chunk i is tested; a warp takes
+// each of its rays through all of a chunk's pieces (`chunk`).  `tab` counts
+// the slots of each ray's full window row (the scanned output).
 template <class Issue, class Chunk, class Tab>
 __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kMaxPieces], int* npieces,
                                   unsigned& phase, int G, const hp_query_layout L, int64_t wp, int s,
