@@ -286,6 +286,9 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                 const RayParams& rp = S.head.ray[g];
                 const RayF rf = ray_f(rp);
                 const int64_t off = S.off[g];
+                unsigned* __restrict__ kout = sc_key + off;  // ray g's scratch segment
+                int* __restrict__ sout = sc_slot + off;
+                const unsigned below = lanemask_lt();
                 int fill = S.fill[g];
                 int* dq = S.dq[warp];
                 int nq = 0;  // deferred pairs (warp-uniform)
@@ -305,11 +308,11 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                     }
                     const unsigned b = __ballot_sync(0xffffffffu, ok);
                     if (ok) {
-                        const int64_t pos = off + fill + __popc(b & lanemask_lt());
-                        HP_ASSERT(pos < S.end[g]);
+                        const int pos = fill + __popc(b & below);
+                        HP_ASSERT(off + pos < S.end[g]);
                         const unsigned key = fkey(__double2float_rd(t));
-                        sc_key[pos] = key;
-                        sc_slot[pos] = k;
+                        kout[pos] = key;
+                        sout[pos] = k;
                         lmin = min(lmin, key);
                         lmax = max(lmax, key);
                         lbad |= !(fabs(t) <= DBL_MAX) || !(d2 <= DBL_MAX);
@@ -331,11 +334,11 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                         if (k < hi) cls = cone_filter_te(S.pf[buf][k - c0], rf, tf, eps);
                         const unsigned acc = __ballot_sync(0xffffffffu, cls == 1);
                         if (cls == 1) {
-                            const int64_t pos = off + fill + __popc(acc & lanemask_lt());
-                            HP_ASSERT(pos < S.end[g]);
+                            const int pos = fill + __popc(acc & below);
+                            HP_ASSERT(off + pos < S.end[g]);
                             const unsigned key = fkey(__fsub_rd(tf, eps));
-                            sc_key[pos] = key;
-                            sc_slot[pos] = k;
+                            kout[pos] = key;
+                            sout[pos] = k;
                             lmin = min(lmin, key);
                             lmax = max(lmax, key);
                         }
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
                         const unsigned unc = __ballot_sync(0xffffffffu, cls == 2);
                         if (unc) {
                             HP_ASSERT(nq + __popc(unc) <= 64);
-                            if (cls == 2) dq[nq + __popc(unc & lanemask_lt())] = k;
+                            if (cls == 2) dq[nq + __popc(unc & below)] = k;
                             nq += __popc(unc);
                             if (nq >= 32) flush(32);
                         }
