@@ -66,3 +66,28 @@ def test_band_frame_with_row_window_equals_whole_index():
     for x, y in zip(whole.samples, band.samples):
         assert torch.equal(x, y)
     assert band.R > 0
+
+
+def test_distributed_view_single_rank_equals_view(tmp_path):
+    """shard.search_and_sample_distributed on a one-rank group: the layout
+    build's per-pixel counts give the (single) band, and the result equals
+    search_and_sample_view's arrays."""
+    import torch.distributed as dist
+
+    from paper_2404_14044_b200 import shard
+    cloud = hp.generate_scene(hp.SceneSpec("sphere_surface", n=40_000, seed=4, noise=0.005))
+    cam = hp.scene_camera(120, 90, fov_deg=30)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.01), hp.pixel_disc_radius(cam))
+    init = not dist.is_initialized()
+    if init:
+        dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        got = shard.search_and_sample_distributed(cloud, cam, cfg, 1.0, 10.0, dist)
+    finally:
+        if init:
+            dist.destroy_process_group()
+    ref = pipeline.search_and_sample_view(cloud, cam, cfg, 1.0, 10.0)
+    assert len(got) == len(ref)
+    for x, y in zip(got, ref):
+        np.testing.assert_array_equal(x, y)
+    assert ref[1].size > 0
