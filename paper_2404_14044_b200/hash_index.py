@@ -190,7 +190,10 @@ def query_device_arrays(index: HashIndex, pixels, dirs, t_near, t_far, slopes):
     dev = index.device.device
 
     def up(a, dt):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+        a = np.ascontiguousarray(a, dtype=dt)
+        if not a.flags.writeable:  # broadcast / frozen views: torch wants a writable buffer
+            a = a.copy()
+        return torch.from_numpy(a).to(dev)
 
     m = int(np.asarray(pixels).shape[0])
     return device.query(index.device, up(pixels, np.int64).view(m, 2), up(dirs, np.float64).view(m, 3),

@@ -29,7 +29,7 @@ def test_layout_build_matches_full_build(name):
         pytest.skip(f"no golden case {name}")
     _, cloud, cam, cfg, *_ = gu.get_case(name)
     dev = torch.device("cuda")
-    xyz = torch.from_numpy(np.ascontiguousarray(cloud.positions)).to(dev)
+    xyz = torch.from_numpy(np.array(cloud.positions)).to(dev)
     full = dv.build(xyz, cam, cfg.pad)
     lay = dv.build_layout(xyz, cam, cfg.pad)
     assert lay.n_in == full.n_in and lay.table_start is None
