@@ -164,6 +164,35 @@ def run_views(args, rank, world, dist):
         x = torch.tensor([Q, R], device=dev, dtype=torch.int64)
         dist.all_reduce(x)
         qr = (int(x[0]), int(x[1]))
+    e2e = None
+    if not args.no_e2e:
+        # end to end through the library's multi-view driver: numpy cloud in,
+        # every view's numpy 9-tuple out (rays on the device, slopes on host
+        # threads, view k's copies overlapping view k + 1); max over ranks
+        cams, cfgs = [v["cam"] for v in views], [v["cfg"] for v in views]
+        et, out = [], {}
+        warm = max(args.warmup, 3)  # pinned host buffers reach the caching allocator's steady state
+        for it in range(warm + args.steps):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = pipeline.search_and_sample_views(cloud, cams, cfgs, T_NEAR, T_FAR, dist=dist)
+            torch.cuda.synchronize()
+            if it >= warm:
+                et.append(time.perf_counter() - t0)
+        t = torch.tensor([statistics.mean(et), cloud.positions.nbytes + cloud.colors.nbytes
+                          + 8 * sum(views[i]["m"] for i in mine),
+                          sum(int(x.nbytes) for o in out.values() for x in o)], device=dev, dtype=torch.float64)
+        if dist is not None:
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t)
+            t[0] = mx[0]
+        e2e = {"value": sum(v["m"] for v in views) / float(t[0]), "unit": "rays/s",
+               "h2d_bytes_per_step": int(t[1]), "d2h_bytes_per_step": int(t[2]),
+               "api": "paper_2404_14044_b200.pipeline.search_and_sample_views (numpy cloud in, every view's "
+                      "numpy 9-tuple out; views[rank::world] per rank)"}
     if rank != 0:
         return
     parity = "skipped"
@@ -207,6 +236,8 @@ def run_views(args, rank, world, dist):
         "kernels_ms": {k: round(v / args.steps, 3) for k, (v, _) in sorted(kern_tot.items(), key=lambda x: -x[1][0])},
         "clocks": smi.summary(),
     }
+    if e2e is not None:
+        line["e2e"] = e2e
     print(json.dumps(line), flush=True)
 
 

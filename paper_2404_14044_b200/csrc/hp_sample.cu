@@ -342,7 +342,10 @@ struct Exact {
 // One thread per exact candidate (all lanes busy regardless of how few
 // candidates a ray needs): exact udf / alpha / colour of candidate j of ray.
 template <class BestT, bool kKnn>
-__global__ void __launch_bounds__(kThreads) k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
+#ifndef HP_EXACT_MINB
+#define HP_EXACT_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, HP_EXACT_MINB) k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
                                                            const int64_t* __restrict__ eoff, Exact X) {
     const int64_t n = eoff[C.m];
     if (n > X.cap) return;

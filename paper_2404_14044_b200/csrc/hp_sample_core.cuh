@@ -11,6 +11,18 @@
 
 #include "hp_common.cuh"
 
+// the exact sampler's K-nearest walk: seed window, then each side alone (1),
+// or one merged two-sided walk (0); DESIGN.md §5 "Sampler"
+#ifndef HP_EXACT_SIDES
+#define HP_EXACT_SIDES 1
+#endif
+#ifndef HP_EXACT_SEED
+#define HP_EXACT_SEED 4
+#endif
+#ifndef HP_EXACT_LA
+#define HP_EXACT_LA 1
+#endif
+
 namespace hp {
 namespace {
 
@@ -178,6 +190,103 @@ __device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, boo
     int ki = INT_MAX;
     constexpr int kMaxK = BestT::kMax;
     const bool full = ksel == kMaxK;
+    // one pool member i at (t_i, ds_i): returns false once (t_i - t_j)^2
+    // exceeds the K-th best (every point further out on that side is then out)
+    auto visit = [&](int i, double ti, double di) -> bool {
+        const double dt = dsub(ti, tj);
+        const double lb = dmul(dt, dt);
+        if (lb > kd) return false;
+        if (use_el && di > rj) return true;
+        const double d2 = dadd(lb, dmul(di, di));
+        evals++;
+        if (kless(d2, i, kd, ki)) {
+            if (full) {
+                best.insert_full(d2, i);
+                kd = best.d[kMaxK - 1];
+                ki = best.i[kMaxK - 1];
+            } else if (kMaxK <= 8) {
+                best.insert_full(d2, i);
+                best.kth(ksel, kd, ki);
+            } else {
+                best.insert(ksel, d2, i);
+                best.kth(ksel, kd, ki);
+            }
+        }
+        return true;
+    };
+#if HP_EXACT_SIDES
+    if (fast) {
+        // The K nearest do not depend on the visiting order: a side is left
+        // only at a point with (t_i - t_j)^2 > the current K-th best >= the
+        // final one, and every point further out on that side is at least as
+        // far in t.  So: a seed window j - kSeed .. j + kSeed (a tight bound
+        // of the K-th best), then each side outward with its own simple loop
+        // (the next point loaded one step ahead).  Prefix mode: when the right
+        // side runs out of the prefix, the cut is a lower bound of the t of
+        // every left-out match.
+        constexpr int kSeed = HP_EXACT_SEED;
+        const int s0 = j - kSeed > 0 ? j - kSeed : 0;
+        const int s1 = j + kSeed + 1 < q ? j + kSeed + 1 : q;
+        for (int i = s0; i < s1; i++) visit(i, V.t(i), V.d(i));
+#if HP_EXACT_LA == 2
+        if (s0 > 0) {
+            double tn = V.t(s0 - 1), dn = V.d(s0 - 1);
+            const int n2 = s0 > 1 ? s0 - 2 : 0;
+            double tm = V.t(n2), dm = V.d(n2);
+            for (int i = s0 - 1; i >= 0; --i) {
+                const double ti = tn, di = dn;
+                tn = tm;
+                dn = dm;
+                const int nx = i > 1 ? i - 2 : 0;
+                tm = V.t(nx);
+                dm = V.d(nx);
+                if (!visit(i, ti, di)) break;
+            }
+        }
+        int r = s1;
+        if (r < q) {
+            double tn = V.t(r), dn = V.d(r);
+            const int n2 = r + 1 < q ? r + 1 : r;
+            double tm = V.t(n2), dm = V.d(n2);
+            for (; r < q; ++r) {
+                const double ti = tn, di = dn;
+                tn = tm;
+                dn = dm;
+                const int nx = r + 2 < q ? r + 2 : q - 1;
+                tm = V.t(nx);
+                dm = V.d(nx);
+                if (!visit(r, ti, di)) break;
+            }
+        }
+#else
+        if (s0 > 0) {
+            double tn = V.t(s0 - 1), dn = V.d(s0 - 1);
+            for (int i = s0 - 1; i >= 0; --i) {
+                const double ti = tn, di = dn;
+                const int nx = i > 0 ? i - 1 : 0;
+                tn = V.t(nx);
+                dn = V.d(nx);
+                if (!visit(i, ti, di)) break;
+            }
+        }
+        int r = s1;
+        if (r < q) {
+            double tn = V.t(r), dn = V.d(r);
+            for (; r < q; ++r) {
+                const double ti = tn, di = dn;
+                const int nx = r + 1 < q ? r + 1 : r;
+                tn = V.t(nx);
+                dn = V.d(nx);
+                if (!visit(r, ti, di)) break;
+            }
+        }
+#endif
+        if (partial && r == q) {
+            const double dc = dsub(tcut, tj);
+            if (!(dmul(dc, dc) > kd)) return false;
+        }
+    } else
+#endif
     if (fast) {
         // outward from j in t order; stop once (t_i - t_j)^2 > K-th best
         // (t, ds) of the next candidate on each side are loaded one step ahead

@@ -21,8 +21,8 @@ import torch
 from . import device
 from .sampler import SamplerConfig
 
-__all__ = ["FrameResult", "frame_device", "search_and_sample", "search_and_sample_view", "StageTimer",
-           "host_slopes"]
+__all__ = ["FrameResult", "frame_device", "search_and_sample", "search_and_sample_view",
+           "search_and_sample_views", "StageTimer", "host_slopes"]
 
 
 SLOPE_THREADS = int(os.environ.get("HP_SLOPE_THREADS", "0")) or min(16, os.cpu_count() or 1)
@@ -578,3 +578,90 @@ def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: floa
                              max_matches).samples
 
     return _samples_to_host(run_chunk, cuts, dev)
+
+
+_SLOPE_POOL: list = []
+
+
+def _views_of(n_views: int, dist=None) -> list:
+    """The views this rank runs: views[rank::world] (views are independent:
+    no collective on the data path)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return list(range(n_views))
+    return list(range(n_views))[dist.get_rank()::dist.get_world_size()]
+
+
+def search_and_sample_views(cloud, cameras, search_cfg, t_near: float, t_far: float,
+                            sampler_cfg: SamplerConfig | None = None, with_colors: bool = True,
+                            exact_t_end: bool = True, max_matches: int | None = None, dist=None):
+    """A batch of views of one cloud (the reference renders one index per
+    view, renderer.py:113-125 / cli.py:127-162, one view after the other):
+    every view's whole ray grid, build -> query -> sample, host arrays out.
+
+    ``search_cfg`` is one SearchConfig or one per camera.  The cloud and its
+    colours go up once and stay resident; each view's index, rays (generated
+    on the device) and slopes are per view.  View k's samples are copied to
+    pinned host memory on a copy stream while view k + 1 runs, and view
+    k + 1's host slopes are computed on a host thread while view k runs.
+    With ``dist`` (torch.distributed, one process per GPU) each rank runs
+    views[rank::world].  Returns {view index: numpy 9-tuple of
+    ``sample_batch_arrays``} for this rank's views."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfgs = list(search_cfg) if isinstance(search_cfg, (list, tuple)) else [search_cfg] * len(cameras)
+    if len(cfgs) != len(cameras):
+        raise ValueError("one search config per camera (or a single one for all)")
+    mine = _views_of(len(cameras), dist)
+    if not mine:
+        return {}
+    main = torch.cuda.current_stream()
+    side = _side_stream(dev)
+    side.wait_stream(main)
+    xyz = _h2d(cloud.positions, dev, torch.float64)
+    cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
+    if not _SLOPE_POOL:
+        from concurrent.futures import ThreadPoolExecutor
+        _SLOPE_POOL.append(ThreadPoolExecutor(max_workers=1, thread_name_prefix="hp-slopes"))
+
+    def slopes_of(i):  # host threads in the library (ctypes drops the GIL)
+        cam, cfg = cameras[i], cfgs[i]
+        h = torch.empty(int(cam.width) * int(cam.height), dtype=torch.float64, pin_memory=True)
+        host_slopes(cam, None, cfg.kernel_radius, cfg.use_approx_radius, out=h.numpy())
+        return h
+
+    cfg_s = sampler_cfg or SamplerConfig()
+    cp = _copy_stream(dev)
+    col, out, pending = [], {}, []
+
+    def colours():
+        if not col:
+            col.append(cols_up()[0])
+        return col[0]
+
+    nxt = _SLOPE_POOL[0].submit(slopes_of, mine[0])
+    for n, i in enumerate(mine):
+        cam, cfg = cameras[i], cfgs[i]
+        idx = device.build_layout(xyz, cam, cfg.pad)
+        dirs, pixels, tn, tf = device.ray_grid(cam, dev, t_near=t_near, t_far=t_far)
+        sl_host = nxt.result()
+        if n + 1 < len(mine):
+            nxt = _SLOPE_POOL[0].submit(slopes_of, mine[n + 1])
+        sl = sl_host.to(dev, non_blocking=True)
+        s = _query_sample(idx, colours, pixels, dirs, tn, tf, sl, cfg_s, exact_t_end, max_matches).samples
+        R = int(s[1].shape[0])
+        host = [torch.empty(tuple(x.shape), dtype=x.dtype, pin_memory=True)
+                if (x.shape[0] == R and R) or k in (0, 8) else torch.zeros(tuple(x.shape), dtype=x.dtype)
+                for k, x in enumerate(s)]
+        cp.wait_event(main.record_event())
+        with torch.cuda.stream(cp):
+            for k, x in enumerate(s):
+                if host[k].is_pinned():
+                    host[k].copy_(x, non_blocking=True)
+            done = cp.record_event()
+        pending.append((i, host, s, sl_host, done))  # device results / pinned slopes live until copied
+        while pending and pending[0][4].query():
+            j, h, *_ = pending.pop(0)
+            out[j] = tuple(x.numpy() for x in h)
+    for j, h, _, _, done in pending:
+        done.synchronize()
+        out[j] = tuple(x.numpy() for x in h)
+    return out

@@ -139,3 +139,31 @@ def test_row_costs_equal_oracle_scanned():
                   dirs, cam.origin, np.ones(m), np.full(m, 10.0), slopes)
     per_row = q[5].reshape(cam.height, cam.width).sum(axis=1) + cam.width
     np.testing.assert_array_equal(row_costs(cloud.positions, cam, cfg.pad), per_row)
+
+
+def _views_worker(rank, world, port, result_q):
+    from paper_2404_14044_b200.pipeline import _views_of
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    result_q.put((rank, _views_of(7, dist)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_views_are_split_across_ranks():
+    """pipeline.search_and_sample_views: rank r runs views[r::world]; the
+    ranks' views are disjoint and cover the batch (no data-path collective)."""
+    from paper_2404_14044_b200.pipeline import _views_of
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_views_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: [0, 2, 4, 6], 1: [1, 3, 5]}
+    assert _views_of(3, None) == [0, 1, 2]
