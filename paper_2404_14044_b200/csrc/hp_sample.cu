@@ -342,10 +342,17 @@ struct Exact {
 // One thread per exact candidate (all lanes busy regardless of how few
 // candidates a ray needs): exact udf / alpha / colour of candidate j of ray.
 template <class BestT, bool kKnn>
+// HP_EXACT_MINB > 0: minimum resident CTAs per SM for the K <= 8 instances
+// (an explicit 1 is not the same as none: ptxas then allots more registers)
 #ifndef HP_EXACT_MINB
-#define HP_EXACT_MINB 1
+#define HP_EXACT_MINB 4
 #endif
-__global__ void __launch_bounds__(kThreads, HP_EXACT_MINB) k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
+#if HP_EXACT_MINB > 0
+#define HP_EXACT_BOUNDS __launch_bounds__(kThreads, BestT::kMax <= 8 ? HP_EXACT_MINB : 1)
+#else
+#define HP_EXACT_BOUNDS __launch_bounds__(kThreads)
+#endif
+__global__ void HP_EXACT_BOUNDS k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
                                                            const int64_t* __restrict__ eoff, Exact X) {
     const int64_t n = eoff[C.m];
     if (n > X.cap) return;

@@ -22,6 +22,9 @@
 #ifndef HP_EXACT_LA
 #define HP_EXACT_LA 1
 #endif
+#ifndef HP_EXACT_SORTSEED
+#define HP_EXACT_SORTSEED 1
+#endif
 
 namespace hp {
 namespace {
@@ -227,6 +230,51 @@ __device__ bool eval_exact(const View& V, int q, int qt, double tcut, int j, boo
         constexpr int kSeed = HP_EXACT_SEED;
         const int s0 = j - kSeed > 0 ? j - kSeed : 0;
         const int s1 = j + kSeed + 1 < q ? j + kSeed + 1 : q;
+#if HP_EXACT_SORTSEED
+        if constexpr (kMaxK == 8 && kSeed == 4) {
+            // the 9 seed points sorted by one network (25 compare-exchanges,
+            // checked by the 0-1 principle) instead of 9 insertions: the 8
+            // smallest of the 9 in (d2, i) order are exactly what the
+            // insertions leave; missing / out-of-pool points are (inf, INT_MAX)
+            double sd[9];
+            int si[9];
+#pragma unroll
+            for (int b = 0; b < 9; b++) {
+                const int i = j - kSeed + b;
+                sd[b] = CUDART_INF;
+                si[b] = INT_MAX;
+                if (i >= s0 && i < s1) {
+                    const double ti = V.t(i), di = V.d(i);
+                    if (!(use_el && di > rj)) {
+                        const double dt = dsub(ti, tj);
+                        sd[b] = dadd(dmul(dt, dt), dmul(di, di));
+                        si[b] = i;
+                        evals++;
+                    }
+                }
+            }
+            constexpr int kNet[25][2] = {{0, 1}, {3, 4}, {6, 7}, {1, 2}, {4, 5}, {7, 8}, {0, 1}, {3, 4}, {6, 7},
+                                         {0, 3}, {3, 6}, {0, 3}, {1, 4}, {4, 7}, {1, 4}, {2, 5}, {5, 8}, {2, 5},
+                                         {1, 3}, {5, 7}, {2, 6}, {4, 6}, {2, 4}, {2, 3}, {5, 6}};
+#pragma unroll
+            for (int c = 0; c < 25; c++) {
+                const int a = kNet[c][0], b = kNet[c][1];
+                const bool sw = kless(sd[b], si[b], sd[a], si[a]);
+                const double da = sw ? sd[b] : sd[a], db = sw ? sd[a] : sd[b];
+                const int ia = sw ? si[b] : si[a], ib = sw ? si[a] : si[b];
+                sd[a] = da;
+                sd[b] = db;
+                si[a] = ia;
+                si[b] = ib;
+            }
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                best.d[b] = sd[b];
+                best.i[b] = si[b];
+            }
+            best.kth(ksel, kd, ki);
+        } else
+#endif
         for (int i = s0; i < s1; i++) visit(i, V.t(i), V.d(i));
 #if HP_EXACT_LA == 2
         if (s0 > 0) {
