@@ -28,6 +28,7 @@
  *   hp_sample_emit        (two-phase for the same reason; R unknown)
  *   hp_primary_surface  derived: first retained candidate per ray
  *   hp_ray_grid         geometry.ray_grid            geometry.py:289-306
+ *   hp_radius_slopes    geometry.radius_slopes       geometry.py:249-260
  *   hp_render           renderer.render_volume / render_knp renderer.py:138-185
  *   hp_pointnerf_*      (no reference symbol) the Point-NeRF aggregation MLP the
  *                       paper integrates with, cfg5
@@ -154,6 +155,14 @@ int hp_layout_from_table(const int64_t* table_start, const int64_t* table_count,
  * grid (ray k = pixel (k % width, k / width)); slopes float64 [m] (host). */
 int hp_radius_slopes_host(const hp_camera* cam, const int64_t* pixels, int64_t pixel_stride, int64_t m,
                           double kernel_radius, int approx, double* slopes, int threads);
+
+/* The same slopes on the device (replaces geometry.radius_slopes,
+ * geometry.py:249-260, bit-identical to numpy: glibc's hypot restated in
+ * round-to-nearest): pixels int64 [m,2] on the device with element stride
+ * pixel_stride, or NULL for rays row0 * width + k of the camera's ray grid;
+ * slopes float64 [m] on the device. */
+int hp_radius_slopes(const hp_camera* cam, int64_t row0, const int64_t* pixels, int64_t pixel_stride, int64_t m,
+                     double kernel_radius, int approx, double* slopes, hp_stream_t stream);
 
 /* Host -> device upload of PAGEABLE host memory (numpy arrays) through a
  * caller-provided pinned staging buffer of >= bytes: `threads` host threads

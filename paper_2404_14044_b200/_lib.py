@@ -62,6 +62,8 @@ _SIGNATURES = {
                                             ctypes.POINTER(c_f64), Layout, c_p, c_size, c_p]),
     "hp_radius_slopes_host": (ctypes.c_int, [ctypes.POINTER(Camera), c_p, c_i64, c_i64, c_f64, ctypes.c_int,
                                              c_p, ctypes.c_int]),
+    "hp_radius_slopes": (ctypes.c_int, [ctypes.POINTER(Camera), c_i64, c_p, c_i64, c_i64, c_f64, ctypes.c_int,
+                                        c_p, c_p]),
     "hp_host_upload": (ctypes.c_int, [c_p, c_p, c_size, c_p, c_size, ctypes.c_int, c_p]),
     "hp_query_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
     "hp_query_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,

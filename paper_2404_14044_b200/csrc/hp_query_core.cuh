@@ -105,7 +105,10 @@ __device__ __forceinline__ bool key_less(double ta, int64_t ia, double tb, int64
     return ta < tb || (ta == tb && ia < ib);
 }
 
-constexpr int kCoarse = 256;
+#ifndef HP_COARSE
+#define HP_COARSE 256
+#endif
+constexpr int kCoarse = HP_COARSE;
 
 
 // Block-wide exclusive scan of a[0..n) in place (n <= per * blockDim.x).

@@ -747,6 +747,29 @@ def ray_grid(camera, dev=None, row0: int = 0, rows: int | None = None, t_near: f
     return dirs, pixels, tn, tf
 
 
+def radius_slopes(camera, kernel_radius: float, approx: bool = False, pixels: torch.Tensor | None = None,
+                  row0: int = 0, m: int | None = None, dev=None) -> torch.Tensor:
+    """geometry.radius_slopes on the device (hp_radius_slopes, bit-identical
+    to numpy; reference geometry.py:249-260): for ``pixels`` (int64 [m, 2] on
+    the device), or for rays row0 * W .. row0 * W + m of the camera's ray grid."""
+    lib = _lib.load(require_device=True)
+    if pixels is not None:
+        if pixels.stride(-1) != 1:
+            pixels = pixels.contiguous()
+        dev = pixels.device
+        m = int(pixels.shape[0])
+        stride = int(pixels.stride(0)) if m else 2
+    else:
+        dev = dev or torch.device("cuda", torch.cuda.current_device())
+        m = int(camera.width) * int(camera.height) - row0 * int(camera.width) if m is None else int(m)
+        stride = 2
+    out = torch.empty(m, dtype=torch.float64, device=dev)
+    _lib.check(lib.hp_radius_slopes(ctypes.byref(camera_struct(camera)), int(row0),
+                                    _ptr(pixels) if pixels is not None else ctypes.c_void_p(0), stride, m,
+                                    float(kernel_radius), 1 if approx else 0, _ptr(out), _stream()))
+    return out
+
+
 def primary_surface(r_off: torch.Tensor, r_id: torch.Tensor, r_t: torch.Tensor):
     """Primary-surface point per ray: (point id or -1, t or NaN)."""
     lib = _lib.load(require_device=True)

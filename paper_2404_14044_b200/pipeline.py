@@ -522,9 +522,6 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
     ray_up += [_h2d_async(side, dev, *[(h[a:b], k) for h, k in zip(h_rays, kinds)])
                for a, b in zip(cuts[1:-1], cuts[2:])]
-    sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
-    host_slopes(camera, px_host, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
-    sl = sl_host.to(dev, non_blocking=True)
     cfg = sampler_cfg or SamplerConfig()
     col = []
     chunk_of = {a: i for i, a in enumerate(cuts[:-1])}
@@ -536,7 +533,8 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
 
     def run_chunk(a, b):
         pix_d, dirs_d, tn, tf = ray_up[chunk_of[a]]()  # waits for this chunk's uploads only
-        return _query_sample(idx, colours, pix_d, dirs_d, tn, tf, sl[a:b], cfg, exact_t_end, max_matches).samples
+        sl = device.radius_slopes(camera, search_cfg.kernel_radius, search_cfg.use_approx_radius, pixels=pix_d)
+        return _query_sample(idx, colours, pix_d, dirs_d, tn, tf, sl, cfg, exact_t_end, max_matches).samples
 
     return _samples_to_host(run_chunk, cuts, dev)
 
@@ -560,11 +558,8 @@ def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: floa
     dirs, pixels, tn, tf = device.ray_grid(camera, dev, t_near=t_near, t_far=t_far)
     m = int(dirs.shape[0])
     cuts = _ray_chunks(m)
-    sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
-    sl = torch.empty(m, dtype=torch.float64, device=dev)
     cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
-    host_slopes(camera, None, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
-    sl.copy_(sl_host, non_blocking=True)
+    sl = device.radius_slopes(camera, search_cfg.kernel_radius, search_cfg.use_approx_radius, dev=dev)
     cfg = sampler_cfg or SamplerConfig()
     col = []
 
@@ -578,9 +573,6 @@ def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: floa
                              max_matches).samples
 
     return _samples_to_host(run_chunk, cuts, dev)
-
-
-_SLOPE_POOL: list = []
 
 
 def _views_of(n_views: int, dist=None) -> list:
@@ -618,16 +610,6 @@ def search_and_sample_views(cloud, cameras, search_cfg, t_near: float, t_far: fl
     side.wait_stream(main)
     xyz = _h2d(cloud.positions, dev, torch.float64)
     cols_up = _h2d_async(side, dev, (cloud.colors if with_colors else None, torch.float64))
-    if not _SLOPE_POOL:
-        from concurrent.futures import ThreadPoolExecutor
-        _SLOPE_POOL.append(ThreadPoolExecutor(max_workers=1, thread_name_prefix="hp-slopes"))
-
-    def slopes_of(i):  # host threads in the library (ctypes drops the GIL)
-        cam, cfg = cameras[i], cfgs[i]
-        h = torch.empty(int(cam.width) * int(cam.height), dtype=torch.float64, pin_memory=True)
-        host_slopes(cam, None, cfg.kernel_radius, cfg.use_approx_radius, out=h.numpy())
-        return h
-
     cfg_s = sampler_cfg or SamplerConfig()
     cp = _copy_stream(dev)
     col, out, pending = [], {}, []
@@ -637,15 +619,11 @@ def search_and_sample_views(cloud, cameras, search_cfg, t_near: float, t_far: fl
             col.append(cols_up()[0])
         return col[0]
 
-    nxt = _SLOPE_POOL[0].submit(slopes_of, mine[0])
-    for n, i in enumerate(mine):
+    for i in mine:
         cam, cfg = cameras[i], cfgs[i]
         idx = device.build_layout(xyz, cam, cfg.pad)
         dirs, pixels, tn, tf = device.ray_grid(cam, dev, t_near=t_near, t_far=t_far)
-        sl_host = nxt.result()
-        if n + 1 < len(mine):
-            nxt = _SLOPE_POOL[0].submit(slopes_of, mine[n + 1])
-        sl = sl_host.to(dev, non_blocking=True)
+        sl = device.radius_slopes(cam, cfg.kernel_radius, cfg.use_approx_radius, dev=dev)
         s = _query_sample(idx, colours, pixels, dirs, tn, tf, sl, cfg_s, exact_t_end, max_matches).samples
         R = int(s[1].shape[0])
         host = [torch.empty(tuple(x.shape), dtype=x.dtype, pin_memory=True)
@@ -657,11 +635,11 @@ def search_and_sample_views(cloud, cameras, search_cfg, t_near: float, t_far: fl
                 if host[k].is_pinned():
                     host[k].copy_(x, non_blocking=True)
             done = cp.record_event()
-        pending.append((i, host, s, sl_host, done))  # device results / pinned slopes live until copied
-        while pending and pending[0][4].query():
+        pending.append((i, host, s, done))  # the device results live until copied
+        while pending and pending[0][3].query():
             j, h, *_ = pending.pop(0)
             out[j] = tuple(x.numpy() for x in h)
-    for j, h, _, _, done in pending:
+    for j, h, _, done in pending:
         done.synchronize()
         out[j] = tuple(x.numpy() for x in h)
     return out

@@ -168,12 +168,8 @@ def search_and_sample_distributed(cloud, camera, search_cfg, t_near: float, t_fa
     y0, y1 = balanced_row_bands(None, camera, search_cfg.pad, world, table_count=counts)[rank]
     W = int(camera.width)
     dirs, pixels, tn, tf = device.ray_grid(camera, dev, row0=y0, rows=y1 - y0, t_near=t_near, t_far=t_far)
-    m = (y1 - y0) * W
-    k = np.arange(y0 * W, y1 * W, dtype=np.int64)
-    px = np.stack([k % W, k // W], axis=1)
-    sl_host = torch.empty(m, dtype=torch.float64, pin_memory=True)
-    pipeline.host_slopes(camera, px, search_cfg.kernel_radius, search_cfg.use_approx_radius, out=sl_host.numpy())
-    sl = sl_host.to(dev, non_blocking=True)
+    sl = device.radius_slopes(camera, search_cfg.kernel_radius, search_cfg.use_approx_radius, row0=y0,
+                              m=(y1 - y0) * W, dev=dev)
     fr = pipeline._query_sample(idx, col, pixels, dirs, tn, tf, sl, sampler_cfg or SamplerConfig(), exact_t_end,
                                 None)
     g = gather_samples(fr.samples, dist) if world > 1 else fr.samples
