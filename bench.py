@@ -167,8 +167,8 @@ def run_views(args, rank, world, dist):
     e2e = None
     if not args.no_e2e:
         # end to end through the library's multi-view driver: numpy cloud in,
-        # every view's numpy 9-tuple out (rays on the device, slopes on host
-        # threads, view k's copies overlapping view k + 1); max over ranks
+        # every view's numpy 9-tuple out (rays and slopes on the device,
+        # view k's copies overlapping view k + 1); max over ranks
         cams, cfgs = [v["cam"] for v in views], [v["cfg"] for v in views]
         et, out = [], {}
         warm = max(args.warmup, 3)  # pinned host buffers reach the caching allocator's steady state
@@ -829,7 +829,7 @@ def run_e2e(args, w, r0, r1, dist=None):
                        "h2d_bytes_per_step": int(npcloud.positions.nbytes + npcloud.colors.nbytes + 8 * m),
                        "d2h_bytes_per_step": int(sum(int(x.nbytes) for x in vout)),
                        "api": "paper_2404_14044_b200.pipeline.search_and_sample_view (numpy arrays in: the "
-                              "camera's ray grid on the device, slopes on host threads; numpy out)"}
+                              "camera's ray grid and slopes on the device; numpy out)"}
     return res
 
 

@@ -495,12 +495,12 @@ def search_and_sample(cloud, camera, search_cfg, pixels, dirs, t_near, t_far,
     ``sample_batch_arrays`` (reference sampler.py:196-217).
 
     Inputs may be numpy arrays or (preferably pinned) CPU torch tensors.  The
-    device build and the ray uploads are enqueued first; the host-side slopes
-    (host threads in the library, bit-identical to the reference's
-    ``radius_slopes``) are computed while they run (pageable inputs are
-    staged through pinned memory by host threads, :func:`_h2d`).  The frame
-    then runs in ray chunks whose result copies (pinned buffers) overlap the
-    next chunk's device work (``E2E_CUTS``).
+    device build and the ray uploads are enqueued first (pageable inputs are
+    staged through pinned memory by host threads, :func:`_h2d`); each chunk's
+    slopes are computed on the device from its uploaded pixels
+    (hp_radius_slopes, bit-identical to the reference's ``radius_slopes``).
+    The frame runs in ray chunks whose result copies (pinned buffers) overlap
+    the next chunk's device work (``E2E_CUTS``).
     """
     dev = torch.device("cuda", torch.cuda.current_device())
     main = torch.cuda.current_stream()
@@ -545,8 +545,9 @@ def search_and_sample_view(cloud, camera, search_cfg, t_near: float, t_far: floa
     """A whole view: the camera's ray grid (``ray_grid(camera)``, every pixel,
     row-major, scalar t_near / t_far -- the reference CLI's
     ``generate_rays`` + renderer ``_prepare``, cli.py:127-162,
-    renderer.py:113-125) generated on the device (hp_ray_grid, bit-identical
-    to numpy), then build -> query -> sample as :func:`search_and_sample`
+    renderer.py:113-125) and its slopes generated on the device (hp_ray_grid,
+    hp_radius_slopes, bit-identical to numpy), then build -> query -> sample
+    as :func:`search_and_sample`
     (ray chunks, copies overlapped).  Only the cloud (and its colours) go up;
     returns the numpy 9-tuple of ``sample_batch_arrays``."""
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -591,10 +592,9 @@ def search_and_sample_views(cloud, cameras, search_cfg, t_near: float, t_far: fl
     every view's whole ray grid, build -> query -> sample, host arrays out.
 
     ``search_cfg`` is one SearchConfig or one per camera.  The cloud and its
-    colours go up once and stay resident; each view's index, rays (generated
-    on the device) and slopes are per view.  View k's samples are copied to
-    pinned host memory on a copy stream while view k + 1 runs, and view
-    k + 1's host slopes are computed on a host thread while view k runs.
+    colours go up once and stay resident; each view's index, rays and slopes
+    are generated on the device.  View k's samples are copied to pinned host
+    memory on a copy stream while view k + 1 runs.
     With ``dist`` (torch.distributed, one process per GPU) each rank runs
     views[rank::world].  Returns {view index: numpy 9-tuple of
     ``sample_batch_arrays``} for this rank's views."""
