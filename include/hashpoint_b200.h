@@ -209,7 +209,9 @@ int hp_query_count(hp_query_layout layout, const hp_camera* cam, int64_t padded_
  * sample_batch as chained by renderer.py:119-124): per ray, the head of its
  * matches in (t, id) order -- all of them when it has few, else the
  * smallest-t matches up to a cut near the `want`-th (want <= whole <= 1024:
- * rays of at most `whole` matches are sorted whole) -- without the
+ * rays of at most `whole` matches are sorted whole; with `rays`, whole up to
+ * 4096 selects the long-head mode for rays 1024 do not cover, head_off
+ * spaced for it) -- without the
  * full match list.  hp_head_count is the streaming pass (same arguments and
  * probes / scanned / offsets outputs as hp_query_count, offsets[m] = Q or
  * -(slots needed) when `capacity` is short); it keeps 8 bytes per match in

@@ -41,6 +41,7 @@ namespace hp {
 namespace {
 
 constexpr int kHeadCap = 1024;   // longest head; rays up to this are sorted whole
+constexpr int kHeadLong = 4096;  // the long-head mode (a later chance for rays 1024 do not cover)
 constexpr int kHeadSmall = 512;  // rays up to this: a smaller, denser CTA configuration
 #ifndef HP_HEAD_STAGE
 #define HP_HEAD_STAGE 1024
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
 // head it selects.  The empty rays' outputs are written here.
 // With `rays`, output i stands for ray rays[i] (a re-sort of a subset).
 __global__ void k_head_classes(const int64_t* __restrict__ off, const int* __restrict__ rays, int64_t m, int whole,
-                               int* __restrict__ lists, int* __restrict__ counts, int* __restrict__ plen,
+                               int small, int* __restrict__ lists, int* __restrict__ counts, int* __restrict__ plen,
                                int* __restrict__ facts, double* __restrict__ cut_t, double* __restrict__ cut_d,
                                const int64_t* __restrict__ total) {
     // the count pass ran short of scratch (offsets[m] < 0, the caller re-runs
@@ -398,7 +399,7 @@ __global__ void k_head_classes(const int64_t* __restrict__ off, const int* __res
         if (r < m) {
             const int64_t ri = rays ? rays[r] : r;
             const int64_t q = over ? 0 : off[ri + 1] - off[ri];
-            cls = q == 0 ? -1 : (q > whole ? 2 : (q <= kHeadSmall ? 0 : 1));
+            cls = q == 0 ? -1 : (q > whole ? 2 : (q <= small ? 0 : 1));
             if (q == 0) {
                 plen[r] = 0;
                 facts[r] = -1;
@@ -429,7 +430,7 @@ template <int kBins>
 __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__ off, const int* __restrict__ rays,
                                                      const int64_t* __restrict__ soff,
                                                      const RayMeta* __restrict__ meta, int want, int whole,
-                                                     const unsigned* __restrict__ sc_key,
+                                                     int cap, int small, const unsigned* __restrict__ sc_key,
                                                      const int* __restrict__ sc_slot, const int64_t* __restrict__ hoff,
                                                      int* __restrict__ stage, uint4* __restrict__ sel,
                                                      const int* __restrict__ list, const int* __restrict__ list_n,
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
                     break;
                 }
             }
-            if (c > kHeadCap) {  // that bin alone overflows: stop before it
+            if (c > cap) {  // that bin alone overflows: stop before it
                 c -= H[b];
                 b -= 1;
             }
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(128) k_head_select(const int64_t* __restrict__
         HP_ASSERT(n == cnt);
         if (lane == 0) {
             sel[i] = make_uint4(kcut, unsigned(cnt), kout, 0u);
-            const int cls = cnt <= kHeadSmall ? 0 : 1;  // the sort configuration of this head
+            const int cls = cnt <= small ? 0 : 1;  // the sort configuration of this head
             lists[int64_t(cls) * m + atomicAdd(&counts[cls], 1)] = int(i);
         }
         __syncwarp();
@@ -558,7 +559,7 @@ struct HeadSmem {
 // moves to the left-out side), the exact (t, id) rank, and the write-out of
 // the head at hoff[r] with the sampler's facts and cuts.
 template <int kCap, int kT>
-__global__ void __launch_bounds__(kT, kT == 128 ? 12 : HP_HEAD_SORT_MINB) k_head_sort(
+__global__ void __launch_bounds__(kT, kT == 128 ? 12 : (kT == 256 ? HP_HEAD_SORT_MINB : 1)) k_head_sort(
     hp_query_layout L, const double* __restrict__ dirs, const double* __restrict__ slopes,
     const int64_t* __restrict__ off, const int* __restrict__ rays, const int64_t* __restrict__ soff,
     const int64_t* __restrict__ hoff,
@@ -819,11 +820,14 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
                             int32_t* plen, int32_t* facts, double* cut_t, double* cut_d,
                             const hp_sampler_params* sampler, float* head_u, int64_t capacity,
                             void* workspace, size_t workspace_bytes, hp_stream_t stream) {
-    if (m < 0 || want < 1 || want > kHeadCap || whole < want || whole > kHeadCap || (rays && (n < 0 || n > m)) ||
+    if (m < 0 || want < 1 || want > kHeadLong || whole < want || whole > kHeadLong || (rays && (n < 0 || n > m)) ||
         (m > 0 && (!dirs || !slopes || !facts || !plen || !cut_t || !cut_d || !layout.rel4))) {
-        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d, n <= m)", kHeadCap);
+        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d, n <= m)", kHeadLong);
         return HP_EINVAL;
     }
+    // whole > kHeadCap: the long-head mode (every head in one 4096-entry CTA configuration)
+    const bool lng = whole > kHeadCap;
+    const int small = lng ? 0 : kHeadSmall, cap = lng ? kHeadLong : kHeadCap;
     Carver cv(workspace, workspace_bytes);
     HeadWs w = carve_head(cv, m, capacity);
     if (!cv.ok()) {
@@ -839,17 +843,17 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
     const int* list_small = w.lists;
     const int* list_big = w.lists + nout;
     const int* list_cut = w.lists + 2 * nout;
-    k_head_classes<<<grid_for(nout, 256), 256, 0, s>>>(offsets, rays, nout, whole, w.lists, w.counts, plen, facts,
-                                                       cut_t, cut_d, offsets + m);
+    k_head_classes<<<grid_for(nout, 256), 256, 0, s>>>(offsets, rays, nout, whole, small, w.lists, w.counts, plen,
+                                                       facts, cut_t, cut_d, offsets + m);
     HP_CHECK_LAUNCH("k_head_classes");
     {
         constexpr auto kselect = k_head_select<kHeadCap>;
         const int occ_sel = kernel_occupancy((const void*)kselect, 128, 0);
         if (occ_sel < 0) return occ_sel;
         TimedSpan ts("k_head_select", s);
-        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, rays, w.soff, w.meta, want, whole, w.key, w.slot,
-                                                       head_off, head_ids, w.sel, list_cut, w.counts + 2, w.lists,
-                                                       w.counts, nout);
+        kselect<<<device_sms() * occ_sel, 128, 0, s>>>(offsets, rays, w.soff, w.meta, want, whole, cap, small, w.key,
+                                                       w.slot, head_off, head_ids, w.sel, list_cut, w.counts + 2,
+                                                       w.lists, w.counts, nout);
         HP_CHECK_LAUNCH("k_head_select");
     }
     Params SP{};
@@ -861,6 +865,17 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         SP.inv_k_up = nextafter(1.0 / double(SP.K), INFINITY);
     } else {
         head_u = nullptr;
+    }
+    if (lng) {
+        constexpr auto klong = k_head_sort<kHeadLong, 512>;
+        const int occ_long = kernel_occupancy((const void*)klong, 512, sizeof(HeadSmem<kHeadLong>));
+        if (occ_long < 0) return occ_long;
+        TimedSpan ts("k_head_sort", s);
+        klong<<<device_sms() * occ_long, 512, sizeof(HeadSmem<kHeadLong>), s>>>(
+            layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big,
+            w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u, w.work + 2);
+        HP_CHECK_LAUNCH("k_head_sort long");
+        return HP_OK;
     }
     constexpr auto ksmall = k_head_sort<kHeadSmall, 128>;
     constexpr auto kbig = k_head_sort<kHeadCap, 256>;

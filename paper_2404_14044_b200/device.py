@@ -351,6 +351,7 @@ class QueryPrefix:
 
 PREFIX_WANT = int(os.environ.get("HP_PREFIX_WANT", "400"))  # head length the sampler usually needs
 HEAD_CAP = 1024  # longest head (hp_head.cu kHeadCap)
+HEAD_LONG = 4096  # the long-head mode of a re-sort (hp_head.cu kHeadLong)
 # HP_HEAD_FACTORS=1: heads carry the sampler's bound factors (measured: the sort pays more than the plan saves)
 HEAD_FACTORS = os.environ.get("HP_HEAD_FACTORS", "0") == "1"
 # rays of at most this many matches are sorted whole; longer ones are cut near PREFIX_WANT
@@ -482,7 +483,8 @@ def _head(index, counted, dirs, slopes, want=None, whole=None, sampler_cfg=None)
 def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whole: int = HEAD_CAP) -> QueryPrefix:
     """Second chance for rays the sampler flagged: re-sort the heads of
     ``rays`` (int64 indices into ``pre``'s rays) from the same count pass
-    (``pre`` still holds its workspace) with a longer ``want``; no re-scan.
+    (``pre`` still holds its workspace) with a longer ``want`` (up to
+    HEAD_LONG: ``whole`` > HEAD_CAP is the long-head mode); no re-scan.
     Returns a :class:`QueryPrefix` over just those rays (their own offsets,
     counts unchanged)."""
     lib = _lib.load(require_device=True)
@@ -494,16 +496,17 @@ def head_resort(pre: QueryPrefix, rays: torch.Tensor, want: int = HEAD_CAP, whol
     counts = (pre.offsets[1:] - pre.offsets[:-1])[rays]
     sub_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(counts, 0, out=sub_off[1:])
-    head_off = torch.arange(n + 1, dtype=torch.int64, device=dev) * HEAD_CAP
+    whole = max(int(want), min(int(whole), HEAD_LONG))
+    per = HEAD_LONG if whole > HEAD_CAP else HEAD_CAP  # head storage per ray
+    head_off = torch.arange(n + 1, dtype=torch.int64, device=dev) * per
     fa = torch.empty(n, dtype=torch.int32, device=dev)
     plen = torch.empty(n, dtype=torch.int32, device=dev)
     cut = torch.empty((2, n), dtype=torch.float64, device=dev)
-    cap_h = max(n * HEAD_CAP, 1)
+    cap_h = max(n * per, 1)
     ht = torch.empty(cap_h, dtype=torch.float64, device=dev)
     hd = torch.empty(cap_h, dtype=torch.float64, device=dev)
     hi = torch.empty(cap_h, dtype=torch.int32, device=dev)
     hu = torch.empty(cap_h, dtype=torch.float32, device=dev) if sp is not None else None
-    whole = max(int(want), min(int(whole), HEAD_CAP))
     _lib.check(lib.hp_head_sort(index.layout(), _ptr(dirs), _ptr(slopes), m, _ptr(pre.offsets), _ptr(r32), n,
                                 _ptr(head_off), int(want), whole, _ptr(ht), _ptr(hi), _ptr(hd), _ptr(plen), _ptr(fa),
                                 _ptr(cut[0]), _ptr(cut[1]), ctypes.byref(sp) if sp is not None else None, _ptr(hu),

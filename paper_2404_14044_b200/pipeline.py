@@ -193,17 +193,21 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
         if pre.want < device.HEAD_CAP:  # second chance: longer heads from the same count pass
             n_resorted = n_flagged
             sub_pre = device.head_resort(pre, sel)
-            pre.t = pre.ids = pre.dist = pre._ws = None
+            pre.t = pre.ids = pre.dist = None  # (the count pass's workspace stays for a third chance)
             sl = slopes[sel]
             *s2, fl2, nf2 = device.sample_prefix(sub_pre, sl, sampler_cfg, colors, exact_t_end, emit_knn)
             sub_pre.t = sub_pre.ids = sub_pre.dist = sub_pre._ws = None
             if nf2:
                 sel2 = torch.nonzero(fl2, as_tuple=True)[0]
                 r2 = sel[sel2]
-                sub2 = _full_rays(idx, colors, pixels[r2], dirs[r2], t_near[r2], t_far[r2], slopes[r2], sampler_cfg,
-                                  exact_t_end, budget, emit_knn)
+                if LONG_HEADS:  # third chance: heads of up to HEAD_LONG, still from the count pass
+                    sub2, n_full = _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, r2,
+                                               sampler_cfg, exact_t_end, budget, emit_knn)
+                else:
+                    sub2 = _full_rays(idx, colors, pixels[r2], dirs[r2], t_near[r2], t_far[r2], slopes[r2],
+                                      sampler_cfg, exact_t_end, budget, emit_knn)
+                    n_full = nf2
                 s2 = device.merge_flagged(tuple(s2), fl2, sub2, sel2)
-                n_full = nf2
             s = device.merge_flagged(tuple(s), flagged, tuple(s2), sel)
         else:
             pre.t = pre.ids = pre.dist = pre._ws = None
@@ -214,6 +218,36 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     # the heads and their workspace are no longer needed (sample_prefix copied its outputs)
     pre.t = pre.ids = pre.dist = pre._ws = None
     return tuple(s), Q, n_full, n_resorted
+
+
+# rays the 1024-entry second chance leaves flagged get heads of up to
+# device.HEAD_LONG (HP_LONG_HEADS=0: straight to the full query), in batches
+# of at most LONG_BATCH rays (24 bytes of head storage per entry)
+LONG_HEADS = os.environ.get("HP_LONG_HEADS", "1") == "1"
+LONG_BATCH = int(os.environ.get("HP_LONG_BATCH", str(1 << 15)))
+
+
+def _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, rays, sampler_cfg, exact_t_end, budget,
+                emit_knn=False):
+    """Samples of ``rays`` (indices into ``pre``'s rays) over heads of up to
+    device.HEAD_LONG re-sorted from ``pre``'s count pass; the rays still
+    flagged take the full query.  (samples of ``rays`` in order, rays on the
+    full path)"""
+    parts, n_full = [], 0
+    for a in range(0, int(rays.numel()), LONG_BATCH):
+        r = rays[a:a + LONG_BATCH]
+        sub = device.head_resort(pre, r, want=device.HEAD_LONG, whole=device.HEAD_LONG)
+        *s3, fl3, nf3 = device.sample_prefix(sub, slopes[r], sampler_cfg, colors, exact_t_end, emit_knn)
+        sub.t = sub.ids = sub.dist = sub._ws = None
+        if nf3:
+            sel3 = torch.nonzero(fl3, as_tuple=True)[0]
+            r3 = r[sel3]
+            full = _full_rays(idx, colors, pixels[r3], dirs[r3], t_near[r3], t_far[r3], slopes[r3], sampler_cfg,
+                              exact_t_end, budget, emit_knn)
+            s3 = device.merge_flagged(tuple(s3), fl3, full, sel3)
+            n_full += nf3
+        parts.append(tuple(s3))
+    return _concat_samples(parts), n_full
 
 
 def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget, emit_knn=False):

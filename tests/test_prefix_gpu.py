@@ -272,3 +272,51 @@ def test_deferred_count_short_and_chunk_switch(monkeypatch):
     d = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)  # deferred, fits
     _assert_same(d.samples, full.samples)
     assert len(calls) == 2
+
+
+def _dense_planes(stride=1):
+    cloud = hp.generate_scene(hp.SceneSpec("parallel_planes", n=60_000, seed=3, plane_count=3,
+                                           plane_gap=0.05, extent=0.8, noise=0.01))
+    cam = hp.scene_camera(48, 40, fov_deg=14)
+    cfg = hp.SearchConfig(hp.kernel_radius_for_min_radius(cam, 1.0, 0.04), hp.pixel_disc_radius(cam))
+    dirs, pixels = hp.ray_grid(cam)
+    dirs, pixels = dirs[::stride], pixels[::stride]
+    tn, tf = np.full(len(dirs), 1.0), np.full(len(dirs), 10.0)
+    slopes = hp.radius_slopes(cam, pixels, cfg.kernel_radius)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    idx = dv.build(up(cloud.positions), cam, cfg.pad)
+    return cloud, idx, (up(pixels), up(dirs), up(tn), up(tf), up(slopes)), up(cloud.colors)
+
+
+def test_long_head_resort_is_the_sorted_csr_head():
+    """The long-head mode (hp_head_sort with whole up to 4096, re-sorting a
+    subset from the same count pass): every head is the first plen entries
+    of the full (t, id)-sorted CSR, up to ~4096 long."""
+    _, idx, rays, _ = _dense_planes(stride=3)
+    pre = dv.query_prefix(idx, *rays, want=16, whole=16)
+    sel = torch.arange(0, int(rays[0].shape[0]), 2, device=rays[0].device)
+    sub = dv.head_resort(pre, sel, want=dv.HEAD_LONG, whole=dv.HEAD_LONG)
+    q = dv.query(idx, *[r[sel] for r in rays], facts=True)
+    plen, counts = _check_prefix(q, sub, dv.HEAD_LONG)
+    assert counts.max() > 1024 and plen.max() > 1024  # heads longer than the second chance's
+    assert np.all(plen[counts <= dv.HEAD_LONG] == counts[counts <= dv.HEAD_LONG])
+
+
+@pytest.mark.parametrize("gamma", [0.5, 0.3])
+def test_pipeline_long_heads_equal_full(monkeypatch, gamma):
+    """Rays whose exact transmittance needs more than 1024 candidates: the
+    third chance (heads of up to 4096 from the same count pass) keeps them
+    off the full query; the frame equals the full-CSR frame either way."""
+    from paper_2404_14044_b200 import pipeline
+    _, idx, rays, col = _dense_planes()
+    sc = hp.SamplerConfig(gamma=gamma)
+    b = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=False)
+    flagged = {}
+    for on in (False, True):
+        monkeypatch.setattr(pipeline, "LONG_HEADS", on)
+        monkeypatch.setattr(pipeline, "LONG_BATCH", 97)  # several batches
+        a = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)
+        _assert_same(a.samples, b.samples)
+        flagged[on] = a.flagged
+    assert flagged[False] > 0 and flagged[True] < flagged[False]
