@@ -190,7 +190,16 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     n_full, n_resorted = 0, 0
     if n_flagged:
         sel = torch.nonzero(flagged, as_tuple=True)[0]
-        if pre.want < device.HEAD_CAP:  # second chance: longer heads from the same count pass
+        m = int(pre.offsets.shape[0]) - 1
+        if LONG_HEADS and n_flagged > LONG_DIRECT * m:
+            # most rays flagged (very dense rays): a 1024-entry second chance
+            # would mostly fail, so they go straight to the long heads
+            n_resorted = n_flagged
+            pre.t = pre.ids = pre.dist = None
+            sub, n_full = _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sel, sampler_cfg,
+                                      exact_t_end, budget, emit_knn)
+            s = device.merge_flagged(tuple(s), flagged, sub, sel)
+        elif pre.want < device.HEAD_CAP:  # second chance: longer heads from the same count pass
             n_resorted = n_flagged
             sub_pre = device.head_resort(pre, sel)
             pre.t = pre.ids = pre.dist = None  # (the count pass's workspace stays for a third chance)
@@ -225,6 +234,7 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
 # of at most LONG_BATCH rays (24 bytes of head storage per entry)
 LONG_HEADS = os.environ.get("HP_LONG_HEADS", "1") == "1"
 LONG_BATCH = int(os.environ.get("HP_LONG_BATCH", str(1 << 15)))
+LONG_DIRECT = float(os.environ.get("HP_LONG_DIRECT", "0.25"))  # flagged fraction that skips the 1024 heads
 
 
 def _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, rays, sampler_cfg, exact_t_end, budget,

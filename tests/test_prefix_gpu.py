@@ -313,10 +313,12 @@ def test_pipeline_long_heads_equal_full(monkeypatch, gamma):
     sc = hp.SamplerConfig(gamma=gamma)
     b = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=False)
     flagged = {}
-    for on in (False, True):
+    for on, direct in ((False, 1.0), (True, 1.0), (True, 0.0)):  # direct 0: no 1024-entry second chance
         monkeypatch.setattr(pipeline, "LONG_HEADS", on)
+        monkeypatch.setattr(pipeline, "LONG_DIRECT", direct)
         monkeypatch.setattr(pipeline, "LONG_BATCH", 97)  # several batches
         a = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)
         _assert_same(a.samples, b.samples)
-        flagged[on] = a.flagged
-    assert flagged[False] > 0 and flagged[True] < flagged[False]
+        flagged[on, direct] = a.flagged
+    assert flagged[False, 1.0] > 0 and flagged[True, 1.0] < flagged[False, 1.0]
+    assert flagged[True, 0.0] == flagged[True, 1.0]
