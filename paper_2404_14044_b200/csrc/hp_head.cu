@@ -820,9 +820,12 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
                             int32_t* plen, int32_t* facts, double* cut_t, double* cut_d,
                             const hp_sampler_params* sampler, float* head_u, int64_t capacity,
                             void* workspace, size_t workspace_bytes, hp_stream_t stream) {
+    // (the long-head mode needs a ray list: hp_head_count spaces head_off for 1024-entry heads)
     if (m < 0 || want < 1 || want > kHeadLong || whole < want || whole > kHeadLong || (rays && (n < 0 || n > m)) ||
+        (!rays && whole > kHeadCap) ||
         (m > 0 && (!dirs || !slopes || !facts || !plen || !cut_t || !cut_d || !layout.rel4))) {
-        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d, n <= m)", kHeadLong);
+        set_error("hp_head_sort: invalid arguments (1 <= want <= whole <= %d with a ray list, else <= %d; n <= m)",
+                  kHeadLong, kHeadCap);
         return HP_EINVAL;
     }
     // whole > kHeadCap: the long-head mode (every head in one 4096-entry CTA configuration)

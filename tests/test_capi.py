@@ -69,3 +69,17 @@ def test_no_cpu_fallback_without_device():
     cam = hp.scene_camera(8, 8)
     with pytest.raises(RuntimeError, match="CUDA device"):
         hp.build(hp.PointCloud(np.zeros((3, 3)) + [0, 0, 4]), cam, hp.SearchConfig.for_camera(cam))
+
+
+def test_head_sort_long_mode_needs_a_ray_list():
+    """hp_head_sort's long-head mode (whole > 1024) re-sorts a ray list whose
+    head_off the caller spaced for it; without a list it is rejected before
+    any launch (hp_head_count spaces head_off for 1024-entry heads)."""
+    import ctypes
+    L = _lib.load()
+    x = ctypes.c_void_p(8)  # never dereferenced: the arguments are rejected first
+    args = lambda rays, n, whole: (_lib.Layout(), x, x, 1, x, rays, n, x, 400, whole, x, x, x, x, x,  # noqa: E731
+                                   x, x, None, None, 0, None, 0, None)
+    assert L.hp_head_sort(*args(None, 0, 2048)) == _lib.HP_EINVAL
+    assert L.hp_head_sort(*args(None, 0, 5000)) == _lib.HP_EINVAL
+    assert L.hp_head_sort(*args(x, 1, 5000)) == _lib.HP_EINVAL  # past the long heads
