@@ -57,6 +57,9 @@ constexpr int kMaxPieces = 8;          // row pieces per chunk
 #ifndef HP_HEAD_U_MAX
 #define HP_HEAD_U_MAX 384  // bound factors precomputed for the first this many head entries
 #endif
+#ifndef HP_SCAN_DYN
+#define HP_SCAN_DYN 1  // k_head_scan: a chunk's rays claimed by the warps one at a time
+#endif
 #ifndef HP_SELECT_U
 #define HP_SELECT_U 8  // keys (and slots) per lane in flight in k_head_select
 #endif
@@ -100,7 +103,7 @@ __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1
 // the slots of each ray's full window row (the scanned output).
 template <class Issue, class Chunk, class Tab>
 __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kMaxPieces], int* npieces,
-                                  unsigned& phase, int G, const hp_query_layout L, int64_t wp, int s,
+                                  int* ctr, unsigned& phase, int G, const hp_query_layout L, int64_t wp, int s,
                                   const QCam& QC, Issue issue, Chunk chunk, Tab tab) {
     const int tid = threadIdx.x, warp = warp_id();
     const int pad = (s - 1) / 2;
@@ -156,6 +159,7 @@ __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kM
                 pc += take;
             }
             npieces[b] = n;
+            ctr[b] = 0;  // nobody reads it: the chunk that used it ended at a barrier
             if (n) {
                 mbar_arrive_tx(&bar[b], unsigned(off) * 16u);
                 for (int i = 0; i < n; i++) issue(b, pieces[b][i].w, pieces[b][i].y, pieces[b][i].z);
@@ -171,7 +175,19 @@ __device__ void stream_group_bulk(GroupHead& S, uint64_t* bar, int4 (*pieces)[kM
             // ray-major: a warp takes each of its rays through all of the
             // chunk's pieces (rows), its per-ray state loaded once per chunk
             const int np = npieces[buf];
+#if HP_SCAN_DYN
+            // rays handed out one at a time (their footprints differ: a static
+            // split leaves warps waiting at the chunk barrier)
+            for (;;) {
+                int g = 0;
+                if (lane_id() == 0) g = atomicAdd(&ctr[buf], 1);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g >= G) break;
+                chunk(buf, g, np, pieces[buf]);
+            }
+#else
             for (int g = warp; g < G; g += kWarps) chunk(buf, g, np, pieces[buf]);
+#endif
             __syncthreads();  // buffer `buf` is refilled two chunks later; npieces[buf ^ 1] is visible
             buf ^= 1;
         }
@@ -185,6 +201,7 @@ struct HeadScanSmem {
     uint64_t bar[2];
     int4 pieces[2][kMaxPieces];  // (row, a, b, smem offset) of each buffer's chunk
     int npieces[2];
+    int ctr[2];          // each buffer's next ray (HP_SCAN_DYN)
     int fill[kGroupMax], scn[kGroupMax], bad[kGroupMax];
     unsigned kmin[kGroupMax], kmax[kGroupMax];
     int64_t off[kGroupMax], end[kGroupMax];
@@ -268,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, HP_HEAD_MINB)
         __syncthreads();
         if (S.skip) continue;  // the frame is re-run with the reported size; S.next is rewritten after a barrier
         stream_group_bulk(
-            S.head, S.bar, S.pieces, S.npieces, phase, G, L, wp, s, QC,
+            S.head, S.bar, S.pieces, S.npieces, S.ctr, phase, G, L, wp, s, QC,
             [&](int buf, int off, int c0, int c1) {  // one piece: slots [c0, c1) to pf[buf][off..]
                 bulk_g2s(&S.pf[buf][off], L.relf + 4 * int64_t(c0), unsigned(c1 - c0) * 16u, &S.bar[buf]);
             },
