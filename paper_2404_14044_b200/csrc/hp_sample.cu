@@ -510,6 +510,96 @@ __global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, Ray
         retain_ray<kKnn>(C, P, ray, RO, plan, eoff, X);
 }
 
+#ifndef HP_RETAIN_SHORT
+#define HP_RETAIN_SHORT 16  // rays of at most this many exact candidates: one thread each
+#endif
+// One thread per ray for the (common) rays with few exact candidates: the
+// same sequential compositing as retain_ray, every read of a candidate
+// before its (lower or equal) compacted slot is written; longer rays are
+// listed for the warp-per-ray kernel below.
+template <bool kKnn>
+__global__ void __launch_bounds__(kThreads) k_sample_retain_short(Csr C, Params P, RayOut RO,
+                                                                  const int4* __restrict__ plan,
+                                                                  const int64_t* __restrict__ eoff, Exact X,
+                                                                  int* __restrict__ longs,
+                                                                  unsigned long long* __restrict__ nlong) {
+    if (eoff[C.m] > X.cap) return;
+    for (int64_t ray = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ray < C.m;
+         ray += int64_t(gridDim.x) * blockDim.x) {
+        const int4 pl = plan[ray];
+        const int q = pl.w;
+        if (C.start && C.flag[ray]) {  // left to the full path
+            RO.rcount[ray] = 0;
+            RO.t_end[ray] = CUDART_NAN;
+            atomicAdd(C.flag + C.m, 1);
+            continue;
+        }
+        if (q == 0) {
+            RO.rcount[ray] = 0;
+            RO.t_end[ray] = 1.0;
+            continue;
+        }
+        const int64_t e0 = eoff[ray];
+        const int E = int(eoff[ray + 1] - e0);
+        if (E > HP_RETAIN_SHORT) {
+            longs[atomicAdd(nlong, 1ull)] = int(ray);
+            continue;
+        }
+        const bool fast = pl.z & 1, proved_zero = (pl.z >> 1) & 1;
+        const double thr = P.eps_mode ? P.eps : P.tau_min;
+        double Tr = 1.0, exit_T = -1.0;
+        int nret = 0;
+        for (int j = 0; j < E; j++) {
+            if (!P.exact_t_end && Tr < thr) {  // exit mode: retention decided
+                exit_T = Tr;
+                break;
+            }
+            const double a = X.alpha[e0 + j];
+            const double w = dmul(a, Tr);
+            if (P.eps_mode ? (w >= P.eps) : !(Tr < P.tau_min)) {
+                const int64_t src = e0 + j, dst = e0 + nret;
+                X.udf[dst] = X.udf[src];
+                X.alpha[dst] = a;
+                X.w[dst] = w;
+                X.ray[dst] = j;
+                if (P.want_color)
+                    for (int x = 0; x < 3; x++) X.col[3 * dst + x] = X.col[3 * src + x];
+                if (kKnn)
+                    for (int b = 0; b < P.K; b++) {
+                        X.knn_id[dst * P.K + b] = X.knn_id[src * P.K + b];
+                        X.knn_w[dst * P.K + b] = X.knn_w[src * P.K + b];
+                    }
+                nret++;
+            }
+            Tr = dmul(Tr, dsub(1.0, a));
+        }
+        HP_DBG_ADD(0, 1);
+        HP_DBG_ADD(1, fast ? 1 : 0);
+        HP_DBG_ADD(2, proved_zero ? 1 : 0);
+        HP_DBG_ADD(4, q);
+        double te;
+        if (P.exact_t_end)
+            te = (fast && proved_zero) ? 0.0 : Tr;
+        else
+            te = exit_T >= 0.0 ? exit_T : Tr;
+        RO.rcount[ray] = nret;
+        RO.t_end[ray] = te;
+    }
+}
+
+template <bool kKnn>
+__global__ void __launch_bounds__(kThreads) k_sample_retain_long(Csr C, Params P, RayOut RO,
+                                                                 const int4* __restrict__ plan,
+                                                                 const int64_t* __restrict__ eoff, Exact X,
+                                                                 const int* __restrict__ longs,
+                                                                 const unsigned long long* __restrict__ nlong) {
+    if (eoff[C.m] > X.cap) return;
+    const int64_t n = int64_t(*nlong);
+    const int64_t warps = int64_t(gridDim.x) * kWarps;
+    for (int64_t k = int64_t(blockIdx.x) * kWarps + warp_id(); k < n; k += warps)
+        retain_ray<kKnn>(C, P, longs[k], RO, plan, eoff, X);
+}
+
 // Copy the compacted retained candidates to the outputs (ray order).
 template <bool kKnn>
 __global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const int64_t* __restrict__ eoff,
@@ -571,6 +661,7 @@ struct SampleWs {
     Exact x;
     void* scan;
     unsigned long long* work;  // k_sample_plan's ray counter
+    int* longs;                // rays left to the warp-per-ray retain
 };
 
 SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color, int knn_k = 0) {
@@ -587,7 +678,8 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color, int knn_k 
     w.x.knn_w = knn_k > 0 ? c.take<double>(xc * knn_k) : nullptr;
     w.x.ray = c.take<int>(xc);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
-    w.work = c.take<unsigned long long>(2);
+    w.work = c.take<unsigned long long>(2);  // [0] k_sample_plan's rays, [1] the long rays of the retain
+    w.longs = c.take<int>(m > 0 ? m : 1);
     return w;
 }
 
@@ -621,7 +713,7 @@ Params to_params(const hp_sampler_params* p) {
 template <class BestT>
 int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     {
-        if (cudaMemsetAsync(w.work, 0, sizeof(unsigned long long), s) != cudaSuccess)
+        if (cudaMemsetAsync(w.work, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess)
             return cuda_status(cudaGetLastError(), "k_sample_plan memset");
         TimedSpan ts("k_sample_plan", s);
         k_sample_plan<<<device_sms() * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.work);
@@ -654,6 +746,19 @@ int dispatch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
 
 int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleWs& w, cudaStream_t s) {
     TimedSpan ts("k_sample_retain", s);
+#if HP_RETAIN_SHORT > 0
+    // short rays one thread each; the rest one warp each (the list's length
+    // stays on the device: a fixed grid strides over it)
+    const int gshort = grid_for(C.m, kThreads);
+    const int glong = device_sms() * 8;
+    if (P.emit_knn) {
+        k_sample_retain_short<true><<<gshort, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x, w.longs, w.work + 1);
+        k_sample_retain_long<true><<<glong, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x, w.longs, w.work + 1);
+    } else {
+        k_sample_retain_short<false><<<gshort, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x, w.longs, w.work + 1);
+        k_sample_retain_long<false><<<glong, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x, w.longs, w.work + 1);
+    }
+#else
     // one ray per warp: as many warps in flight as the SMs hold (latency-bound)
     const int64_t blocks = (C.m + kWarps - 1) / kWarps;
     const int grid = int(blocks < (1 << 30) ? blocks : (1 << 30));
@@ -661,7 +766,21 @@ int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleW
         k_sample_retain<true><<<grid, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
     else
         k_sample_retain<false><<<grid, kThreads, 0, s>>>(C, P, RO, w.plan, w.eoff, w.x);
+#endif
     HP_CHECK_LAUNCH("k_sample_retain");
+    return HP_OK;
+}
+
+int launch_emit(const Csr& C, const Params& P, const int64_t* r_off, const SampleWs& w, const Outputs& O,
+                cudaStream_t s) {
+    // one warp per ray (a thread per short ray measured slower: its writes do not coalesce)
+    TimedSpan ts("k_emit", s);
+    const int64_t m = C.m;
+    if (P.emit_knn)
+        k_emit<true><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    else
+        k_emit<false><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    HP_CHECK_LAUNCH("k_emit");
     return HP_OK;
 }
 
@@ -782,13 +901,7 @@ extern "C" int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp
         set_error("emit_knn set but r_knn_id / r_knn_w is NULL");
         return HP_EINVAL;
     }
-    TimedSpan ts("k_emit", s);
-    if (P.emit_knn)
-        k_emit<true><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
-    else
-        k_emit<false><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
-    HP_CHECK_LAUNCH("k_emit");
-    return HP_OK;
+    return launch_emit(C, P, r_off, w, O, s);
 }
 
 extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* ids, const double* t,
@@ -815,13 +928,7 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
         set_error("emit_knn set but r_knn_id / r_knn_w is NULL");
         return HP_EINVAL;
     }
-    TimedSpan ts("k_emit", s);
-    if (P.emit_knn)
-        k_emit<true><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
-    else
-        k_emit<false><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
-    HP_CHECK_LAUNCH("k_emit");
-    return HP_OK;
+    return launch_emit(C, P, r_off, w, O, s);
 }
 
 extern "C" int hp_primary_surface(const int64_t* r_off, int64_t m, const int64_t* r_id, const double* r_t,
