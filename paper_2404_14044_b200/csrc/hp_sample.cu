@@ -510,6 +510,9 @@ __global__ void __launch_bounds__(kThreads) k_sample_retain(Csr C, Params P, Ray
         retain_ray<kKnn>(C, P, ray, RO, plan, eoff, X);
 }
 
+#ifndef HP_EMIT_FLAT
+#define HP_EMIT_FLAT 1  // k_emit: a warp per 32 consecutive rays, coalesced writes
+#endif
 #ifndef HP_RETAIN_SHORT
 #define HP_RETAIN_SHORT 16  // rays of at most this many exact candidates: one thread each
 #endif
@@ -626,6 +629,62 @@ __global__ void k_emit(Csr C, Params P, const int64_t* __restrict__ r_off, const
                 for (int b = 0; b < P.K; b++) {
                     O.r_knn_id[(o + k) * P.K + b] = X.knn_id[(st + k) * P.K + b];
                     O.r_knn_w[(o + k) * P.K + b] = X.knn_w[(st + k) * P.K + b];
+                }
+        }
+    }
+}
+
+// The same copy with a warp per 32 consecutive rays: their retained samples
+// are one contiguous output range, so lane l writes samples l, l + 32, ...
+// of it (coalesced); each sample's ray is found among the warp's 32 by a
+// binary search over the inclusive counts held in the lanes.
+template <bool kKnn>
+__global__ void k_emit_flat(Csr C, Params P, const int64_t* __restrict__ r_off, const int64_t* __restrict__ eoff,
+                            Exact X, Outputs O) {
+    const int lane = lane_id();
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r0 = (blockIdx.x * int64_t(blockDim.x >> 5) + warp_id()) * 32; r0 < C.m; r0 += warps * 32) {
+        const int64_t r = r0 + lane;
+        int n = 0;
+        int64_t st = 0, lo = 0;
+        if (r < C.m) {
+            n = int(r_off[r + 1] - r_off[r]);
+            if (n) {
+                st = eoff[r];
+                lo = C.lo(r);
+            }
+        }
+        const int64_t o0 = __shfl_sync(0xffffffffu, r < C.m ? r_off[r] : 0, 0);
+        const int incl = warp_incl_scan(n);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int base = 0; base < total; base += 32) {  // whole warp in every round (shuffles)
+            const int sidx = base + lane;
+            int owner = 0;  // first lane whose inclusive count exceeds sidx
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= sidx) owner += step;
+            }
+            const int excl = __shfl_sync(0xffffffffu, incl - n, owner);
+            const int64_t sto = __shfl_sync(0xffffffffu, st, owner), loo = __shfl_sync(0xffffffffu, lo, owner);
+            if (sidx >= total) continue;
+            const int64_t k = sidx - excl, o = o0 + sidx;
+            const int64_t j = loo + X.ray[sto + k];
+            O.r_id[o] = C.id(j);
+            O.r_t[o] = C.t[j];
+            O.r_dist[o] = C.ds[j];
+            O.r_udf[o] = X.udf[sto + k];
+            O.r_alpha[o] = X.alpha[sto + k];
+            O.r_w[o] = X.w[sto + k];
+            if (P.want_color) {
+                O.r_color[3 * o] = X.col[3 * (sto + k)];
+                O.r_color[3 * o + 1] = X.col[3 * (sto + k) + 1];
+                O.r_color[3 * o + 2] = X.col[3 * (sto + k) + 2];
+            }
+            if (kKnn)
+                for (int b = 0; b < P.K; b++) {
+                    O.r_knn_id[o * P.K + b] = X.knn_id[(sto + k) * P.K + b];
+                    O.r_knn_w[o * P.K + b] = X.knn_w[(sto + k) * P.K + b];
                 }
         }
     }
@@ -773,9 +832,17 @@ int launch_retain(const Csr& C, const Params& P, const RayOut& RO, const SampleW
 
 int launch_emit(const Csr& C, const Params& P, const int64_t* r_off, const SampleWs& w, const Outputs& O,
                 cudaStream_t s) {
-    // one warp per ray (a thread per short ray measured slower: its writes do not coalesce)
     TimedSpan ts("k_emit", s);
     const int64_t m = C.m;
+#if HP_EMIT_FLAT
+    if (P.emit_knn)
+        k_emit_flat<true><<<grid_for(m, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    else
+        k_emit_flat<false><<<grid_for(m, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
+    HP_CHECK_LAUNCH("k_emit");
+    return HP_OK;
+#endif
+    // one warp per ray (a thread per short ray measured slower: its writes do not coalesce)
     if (P.emit_knn)
         k_emit<true><<<grid_for(m * 32, 256), 256, 0, s>>>(C, P, r_off, w.eoff, w.x, O);
     else
