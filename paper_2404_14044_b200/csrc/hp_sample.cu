@@ -311,15 +311,32 @@ __global__ void k_mark_exact_overflow(const int64_t* __restrict__ need_at, int64
     if (*need_at > cap) *total = -*need_at;
 }
 
-// candidate slot -> ray (warp per ray)
+// candidate slot -> ray: a warp per 32 consecutive rays, whose slots are one
+// contiguous range [eoff[r0], eoff[r0 + 32]); lane l fills slots l, l + 32,
+// ... of it (coalesced), the ray found by a binary search over the lanes'
+// inclusive counts
 __global__ void k_sample_expand(int64_t m, const int64_t* __restrict__ eoff, int* __restrict__ cand_ray, int64_t cap) {
     if (eoff[m] > cap) return;  // exact scratch too small (hp_sample_run reports it in r_off[m])
+    const int lane = lane_id();
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    for (int64_t ray = blockIdx.x * int64_t(blockDim.x >> 5) + warp_id(); ray < m; ray += warps) {
-        const int64_t a = eoff[ray], b = eoff[ray + 1];
-        for (int64_t k = a + lane_id(); k < b; k += 32) {
-            HP_ASSERT(k < cap);
-            cand_ray[k] = int(ray);
+    for (int64_t r0 = (blockIdx.x * int64_t(blockDim.x >> 5) + warp_id()) * 32; r0 < m; r0 += warps * 32) {
+        const int64_t r = r0 + lane;
+        const int n = r < m ? int(eoff[r + 1] - eoff[r]) : 0;
+        const int64_t base = __shfl_sync(0xffffffffu, eoff[r0], 0);
+        const int incl = warp_incl_scan(n);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int b0 = 0; b0 < total; b0 += 32) {  // whole warp in every round (shuffles)
+            const int sidx = b0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= sidx) owner += step;
+            }
+            if (sidx < total) {
+                HP_ASSERT(base + sidx < cap);
+                cand_ray[base + sidx] = int(r0 + owner);
+            }
         }
     }
 }
@@ -783,7 +800,7 @@ int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     // device and do nothing if it exceeds the capacity (reported in r_off[m])
     {
         TimedSpan ts("k_sample_expand", s);
-        k_sample_expand<<<device_sms() * 8, 256, 0, s>>>(C.m, w.eoff, w.x.ray, w.x.cap);
+        k_sample_expand<<<grid_for(C.m, 256), 256, 0, s>>>(C.m, w.eoff, w.x.ray, w.x.cap);
         HP_CHECK_LAUNCH("k_sample_expand");
     }
     {
