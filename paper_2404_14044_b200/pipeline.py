@@ -218,6 +218,12 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
                     n_full = nf2
                 s2 = device.merge_flagged(tuple(s2), fl2, sub2, sel2)
             s = device.merge_flagged(tuple(s), flagged, tuple(s2), sel)
+        elif LONG_HEADS and pre.want < device.HEAD_LONG:  # heads already 1024 long: the long heads next
+            n_resorted = n_flagged
+            pre.t = pre.ids = pre.dist = None
+            sub, n_full = _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sel, sampler_cfg,
+                                      exact_t_end, budget, emit_knn)
+            s = device.merge_flagged(tuple(s), flagged, sub, sel)
         else:
             pre.t = pre.ids = pre.dist = pre._ws = None
             sub = _full_rays(idx, colors, pixels[sel], dirs[sel], t_near[sel], t_far[sel], slopes[sel], sampler_cfg,

@@ -322,3 +322,18 @@ def test_pipeline_long_heads_equal_full(monkeypatch, gamma):
         flagged[on, direct] = a.flagged
     assert flagged[False, 1.0] > 0 and flagged[True, 1.0] < flagged[False, 1.0]
     assert flagged[True, 0.0] == flagged[True, 1.0]
+
+
+def test_pipeline_long_heads_after_1024_heads(monkeypatch):
+    """Frames whose first heads are already 1024 long send flagged rays to
+    the 4096-entry heads (not the full query); same frame as the full CSR."""
+    from paper_2404_14044_b200 import pipeline
+    monkeypatch.setattr(dv, "PREFIX_WANT", 1024)
+    monkeypatch.setattr(dv, "HEAD_WHOLE", 1024)
+    monkeypatch.setattr(pipeline, "LONG_DIRECT", 1.0)
+    _, idx, rays, col = _dense_planes()
+    sc = hp.SamplerConfig(gamma=0.5)
+    b = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=False)
+    a = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)
+    _assert_same(a.samples, b.samples)
+    assert a.resorted > 0 and a.flagged < a.resorted
