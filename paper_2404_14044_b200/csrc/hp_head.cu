@@ -42,6 +42,7 @@ namespace {
 
 constexpr int kHeadCap = 1024;   // longest head; rays up to this are sorted whole
 constexpr int kHeadLong = 4096;  // the long-head mode (a later chance for rays 1024 do not cover)
+constexpr int kHeadMid = 2048;   // long-head mode: heads up to this in a denser CTA configuration
 constexpr int kHeadSmall = 512;  // rays up to this: a smaller, denser CTA configuration
 #ifndef HP_HEAD_STAGE
 #define HP_HEAD_STAGE 1024
@@ -576,7 +577,7 @@ struct HeadSmem {
 // moves to the left-out side), the exact (t, id) rank, and the write-out of
 // the head at hoff[r] with the sampler's facts and cuts.
 template <int kCap, int kT>
-__global__ void __launch_bounds__(kT, kT == 128 ? 12 : (kT == 256 ? HP_HEAD_SORT_MINB : 1)) k_head_sort(
+__global__ void __launch_bounds__(kT, kT == 128 ? 12 : (kCap <= 1024 ? HP_HEAD_SORT_MINB : 1)) k_head_sort(
     hp_query_layout L, const double* __restrict__ dirs, const double* __restrict__ slopes,
     const int64_t* __restrict__ off, const int* __restrict__ rays, const int64_t* __restrict__ soff,
     const int64_t* __restrict__ hoff,
@@ -845,9 +846,10 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
                   kHeadLong, kHeadCap);
         return HP_EINVAL;
     }
-    // whole > kHeadCap: the long-head mode (every head in one 4096-entry CTA configuration)
+    // whole > kHeadCap: the long-head mode (heads up to 2048 in a <2048, 256> configuration, longer
+    // ones in <4096, 512>)
     const bool lng = whole > kHeadCap;
-    const int small = lng ? 0 : kHeadSmall, cap = lng ? kHeadLong : kHeadCap;
+    const int small = lng ? kHeadMid : kHeadSmall, cap = lng ? kHeadLong : kHeadCap;
     Carver cv(workspace, workspace_bytes);
     HeadWs w = carve_head(cv, m, capacity);
     if (!cv.ok()) {
@@ -887,10 +889,17 @@ extern "C" int hp_head_sort(hp_query_layout layout, const double* dirs, const do
         head_u = nullptr;
     }
     if (lng) {
+        constexpr auto kmid = k_head_sort<kHeadMid, 256>;
         constexpr auto klong = k_head_sort<kHeadLong, 512>;
+        const int occ_mid = kernel_occupancy((const void*)kmid, 256, sizeof(HeadSmem<kHeadMid>));
+        if (occ_mid < 0) return occ_mid;
         const int occ_long = kernel_occupancy((const void*)klong, 512, sizeof(HeadSmem<kHeadLong>));
         if (occ_long < 0) return occ_long;
         TimedSpan ts("k_head_sort", s);
+        kmid<<<device_sms() * occ_mid, 256, sizeof(HeadSmem<kHeadMid>), s>>>(
+            layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_small, w.counts,
+            whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u, w.work + 1);
+        HP_CHECK_LAUNCH("k_head_sort mid");
         klong<<<device_sms() * occ_long, 512, sizeof(HeadSmem<kHeadLong>), s>>>(
             layout, dirs, slopes, offsets, rays, w.soff, head_off, w.meta, w.key, w.slot, w.sel, list_big,
             w.counts + 1, whole, head_t, head_ids, head_dist, plen, facts, cut_t, cut_d, SP, head_u, w.work + 2);

@@ -191,9 +191,13 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
     if n_flagged:
         sel = torch.nonzero(flagged, as_tuple=True)[0]
         m = int(pre.offsets.shape[0]) - 1
+        direct = False
         if LONG_HEADS and n_flagged > LONG_DIRECT * m:
-            # most rays flagged (very dense rays): a 1024-entry second chance
-            # would mostly fail, so they go straight to the long heads
+            # many rays flagged, most of them far longer than 1024 matches (very
+            # dense rays): a 1024-entry second chance would mostly fail
+            q_sel = (pre.offsets[1:] - pre.offsets[:-1])[sel]
+            direct = int((q_sel > 2 * device.HEAD_CAP).sum()) > n_flagged // 2
+        if direct:
             n_resorted = n_flagged
             pre.t = pre.ids = pre.dist = None
             sub, n_full = _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sel, sampler_cfg,
