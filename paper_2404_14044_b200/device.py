@@ -450,6 +450,22 @@ def query_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t
                  slopes, want, whole, sampler_cfg)
 
 
+def count_prefix(index: DeviceIndex, pixels: torch.Tensor, dirs: torch.Tensor, t_near: torch.Tensor,
+                 t_far: torch.Tensor, slopes: torch.Tensor, max_scratch: int | None = None) -> QueryPrefix:
+    """hp_head_count alone (the count read on the host): a QueryPrefix with
+    no heads yet, for :func:`head_resort` over rays that are known to need
+    long heads (very dense frames)."""
+    pixels, dirs = pixels.contiguous(), dirs.contiguous()
+    offsets, head_off, probes, scanned, total, hcap, ws, nb, cap = _count_head(
+        index, pixels, dirs, t_near, t_far, slopes, True, max_scratch)
+    m = int(offsets.shape[0]) - 1
+    pre = QueryPrefix(offsets, probes, scanned, head_off[:m], None, None, None, None, None, None, None, ws, None)
+    pre.total = total
+    pre.want = pre.whole = HEAD_CAP
+    pre._sort_args = (index, dirs, slopes, nb, cap, None)
+    return pre
+
+
 def _head(index, counted, dirs, slopes, want=None, whole=None, sampler_cfg=None) -> QueryPrefix:
     """hp_head_sort after :func:`_count_head` (want / whole default to
     PREFIX_WANT / HEAD_WHOLE, read at call time).  With ``sampler_cfg`` the

@@ -245,6 +245,8 @@ def _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sample
 LONG_HEADS = os.environ.get("HP_LONG_HEADS", "1") == "1"
 LONG_BATCH = int(os.environ.get("HP_LONG_BATCH", str(1 << 15)))
 LONG_DIRECT = float(os.environ.get("HP_LONG_DIRECT", "0.25"))  # flagged fraction that skips the 1024 heads
+# ray chunks whose footprint bound exceeds this many slots per ray start with the long heads
+LONG_FIRST = int(os.environ.get("HP_LONG_FIRST", "16384"))
 
 
 def _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, rays, sampler_cfg, exact_t_end, budget,
@@ -287,7 +289,15 @@ def _full_rays(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, ex
 
 
 def _prefix_pass(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget=None,
-                 emit_knn=False):
+                 emit_knn=False, long_first=False):
+    if long_first and LONG_HEADS:  # very dense rays: the long heads from the start
+        pre = device.count_prefix(idx, pixels, dirs, t_near, t_far, slopes)
+        m = int(pre.offsets.shape[0]) - 1
+        s, n_full = _long_heads(pre, idx, colors, pixels, dirs, t_near, t_far, slopes,
+                                torch.arange(m, device=pre.offsets.device), sampler_cfg, exact_t_end, budget,
+                                emit_knn)
+        pre._ws = None
+        return s, int(pre.total), n_full, m
     pre = device.query_prefix(idx, pixels, dirs, t_near, t_far, slopes,
                               sampler_cfg=sampler_cfg if device.HEAD_FACTORS else None)
     return _prefix_finish(pre, idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg, exact_t_end, budget,
@@ -364,8 +374,10 @@ def _frame_chunked(idx, colors, pixels, dirs, t_near, t_far, slopes, sampler_cfg
     _PREFIX_LEN.clear()
     for a, b in zip(cuts[:-1], cuts[1:]):
         if prefix:
+            dense = (bo[b] - bo[a]) > LONG_FIRST * (b - a)  # the rays' footprint slots bound their matches
             s, q_n, f_n, r_n = _prefix_pass(idx, colors, pixels[a:b], dirs[a:b], t_near[a:b], t_far[a:b],
-                                            slopes[a:b], sampler_cfg, exact_t_end, rerun_budget, emit_knn)
+                                            slopes[a:b], sampler_cfg, exact_t_end, rerun_budget, emit_knn,
+                                            long_first=dense)
             parts.append(s)
             Q += q_n
             nf += f_n

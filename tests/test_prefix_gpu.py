@@ -337,3 +337,19 @@ def test_pipeline_long_heads_after_1024_heads(monkeypatch):
     a = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=True)
     _assert_same(a.samples, b.samples)
     assert a.resorted > 0 and a.flagged < a.resorted
+
+
+@pytest.mark.parametrize("gamma", [0.9, 0.5])
+def test_chunked_frame_long_first_equals_full(monkeypatch, gamma):
+    """Ray chunks dense enough (footprint bound per ray over LONG_FIRST)
+    start with the 4096-entry heads; the frame equals the full-CSR frame."""
+    from paper_2404_14044_b200 import pipeline
+    _, idx, rays, col = _dense_planes()
+    sc = hp.SamplerConfig(gamma=gamma)
+    b = pipeline._query_sample(idx, col, *rays, sc, True, None, prefix=False)
+    for first in (1, 1 << 30):  # every chunk long-first / none
+        monkeypatch.setattr(pipeline, "LONG_FIRST", first)
+        a = pipeline._query_sample(idx, col, *rays, sc, True, max(b.Q // 4, 4096), prefix=True)
+        assert a.chunks > 1
+        _assert_same(a.samples, b.samples)
+        assert a.Q == b.Q
