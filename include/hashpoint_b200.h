@@ -322,6 +322,29 @@ int hp_sample_emit_prefix(const int64_t* offsets, int64_t m, const hp_sample_pre
                           double* r_w, double* r_color, int64_t* r_knn_id, double* r_knn_w, void* workspace,
                           size_t workspace_bytes, hp_stream_t stream);
 
+/* Per-sample output arrays of a sampling pass (R rows each; r_color [R,3],
+ * r_knn_id / r_knn_w [R,K], or NULL). */
+typedef struct hp_sample_fields {
+    int64_t* r_id;
+    double* r_t;
+    double* r_dist;
+    double* r_udf;
+    double* r_alpha;
+    double* r_w;
+    double* r_color;
+    int64_t* r_knn_id;
+    double* r_knn_w;
+} hp_sample_fields;
+/* Splice the samples of re-run rays into a pass's samples (the flagged rays
+ * of hp_sample_run_prefix, which hold none there): output ray r (of m) takes
+ * its rows from `sub` at s_off[pos[r]] when pos[r] >= 0, else from `main` at
+ * r_off[r]; off_out [m+1] is the merged CSR (caller-computed).  k_neighbors:
+ * the row width of the knn fields (0: none).  (Host plumbing of the head
+ * path's second chance; no reference counterpart.) */
+int hp_splice_samples(int64_t m, const int64_t* off_out, const int64_t* r_off, const int64_t* s_off,
+                      const int64_t* pos, int32_t k_neighbors, const hp_sample_fields* main_rows,
+                      const hp_sample_fields* sub_rows, const hp_sample_fields* out, hp_stream_t stream);
+
 /* ---------------- Point-NeRF aggregation MLP (cfg5; bf16 on tcgen05) ----------------
  * The consumer of emit_knn.  No
  * reference implementation: parity vs an fp32 PyTorch

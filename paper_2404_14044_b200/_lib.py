@@ -40,6 +40,11 @@ class SamplerParams(ctypes.Structure):
                 ("tau_min", c_f64), ("emit_knn", c_i32), ("reserved", c_i32)]
 
 
+class SampleFields(ctypes.Structure):
+    _fields_ = [("r_id", c_p), ("r_t", c_p), ("r_dist", c_p), ("r_udf", c_p), ("r_alpha", c_p), ("r_w", c_p),
+                ("r_color", c_p), ("r_knn_id", c_p), ("r_knn_w", c_p)]
+
+
 class SamplePrefix(ctypes.Structure):
     _fields_ = [("start", c_p), ("length", c_p), ("ids", c_p), ("t", c_p), ("dist", c_p),
                 ("cut_t", c_p), ("cut_d", c_p), ("u", c_p)]
@@ -65,6 +70,8 @@ _SIGNATURES = {
     "hp_radius_slopes": (ctypes.c_int, [ctypes.POINTER(Camera), c_i64, c_p, c_i64, c_i64, c_f64, ctypes.c_int,
                                         c_p, c_p]),
     "hp_host_upload": (ctypes.c_int, [c_p, c_p, c_size, c_p, c_size, ctypes.c_int, c_p]),
+    "hp_splice_samples": (ctypes.c_int, [c_i64, c_p, c_p, c_p, c_p, ctypes.c_int32, ctypes.POINTER(SampleFields),
+                                         ctypes.POINTER(SampleFields), ctypes.POINTER(SampleFields), c_p]),
     "hp_query_workspace_bytes": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_size)]),
     "hp_query_count": (ctypes.c_int, [Layout, ctypes.POINTER(Camera), c_i64, c_i64, c_i64, c_p, c_i64,
                                       c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,

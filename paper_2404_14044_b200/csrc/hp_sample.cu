@@ -1015,6 +1015,78 @@ extern "C" int hp_sample_emit(const int64_t* offsets, int64_t m, const int64_t* 
     return launch_emit(C, P, r_off, w, O, s);
 }
 
+namespace hp {
+namespace {
+// a warp per 32 consecutive output rays, rows copied with the flat lane map
+// of k_emit_flat (coalesced writes)
+__global__ void k_splice(int64_t m, const int64_t* __restrict__ off_out, const int64_t* __restrict__ r_off,
+                         const int64_t* __restrict__ s_off, const int64_t* __restrict__ pos, int K,
+                         hp_sample_fields A, hp_sample_fields B, hp_sample_fields O) {
+    const int lane = lane_id();
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r0 = (blockIdx.x * int64_t(blockDim.x >> 5) + warp_id()) * 32; r0 < m; r0 += warps * 32) {
+        const int64_t r = r0 + lane;
+        int n = 0, sub = 0;
+        int64_t src = 0;
+        if (r < m) {
+            n = int(off_out[r + 1] - off_out[r]);
+            const int64_t p = pos[r];
+            sub = p >= 0;
+            src = sub ? s_off[p] : r_off[r];
+        }
+        const int64_t o0 = __shfl_sync(0xffffffffu, r < m ? off_out[r] : 0, 0);
+        const int incl = warp_incl_scan(n);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int b0 = 0; b0 < total; b0 += 32) {
+            const int sidx = b0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= sidx) owner += step;
+            }
+            const int excl = __shfl_sync(0xffffffffu, incl - n, owner);
+            const int64_t so = __shfl_sync(0xffffffffu, src, owner);
+            const int fs = __shfl_sync(0xffffffffu, sub, owner);
+            if (sidx >= total) continue;
+            const hp_sample_fields& S = fs ? B : A;
+            const int64_t i = so + (sidx - excl), o = o0 + sidx;
+            O.r_id[o] = S.r_id[i];
+            O.r_t[o] = S.r_t[i];
+            O.r_dist[o] = S.r_dist[i];
+            O.r_udf[o] = S.r_udf[i];
+            O.r_alpha[o] = S.r_alpha[i];
+            O.r_w[o] = S.r_w[i];
+            if (O.r_color)
+                for (int x = 0; x < 3; x++) O.r_color[3 * o + x] = S.r_color[3 * i + x];
+            if (O.r_knn_id)
+                for (int b = 0; b < K; b++) {
+                    O.r_knn_id[o * K + b] = S.r_knn_id[i * K + b];
+                    O.r_knn_w[o * K + b] = S.r_knn_w[i * K + b];
+                }
+        }
+    }
+}
+}  // namespace
+}  // namespace hp
+
+extern "C" int hp_splice_samples(int64_t m, const int64_t* off_out, const int64_t* r_off, const int64_t* s_off,
+                                 const int64_t* pos, int32_t k_neighbors, const hp_sample_fields* main_rows,
+                                 const hp_sample_fields* sub_rows, const hp_sample_fields* out, hp_stream_t stream) {
+    if (m < 0 || !main_rows || !sub_rows || !out || (m > 0 && (!off_out || !r_off || !s_off || !pos)) ||
+        k_neighbors < 0 || (out->r_knn_id && k_neighbors < 1)) {
+        set_error("hp_splice_samples: invalid arguments");
+        return HP_EINVAL;
+    }
+    if (m == 0) return HP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    TimedSpan ts("k_splice", s);
+    k_splice<<<grid_for(m, 256), 256, 0, s>>>(m, off_out, r_off, s_off, pos, k_neighbors, *main_rows, *sub_rows,
+                                               *out);
+    HP_CHECK_LAUNCH("k_splice");
+    return HP_OK;
+}
+
 extern "C" int hp_primary_surface(const int64_t* r_off, int64_t m, const int64_t* r_id, const double* r_t,
                                   int64_t* primary_id, double* primary_t, hp_stream_t stream) {
     if (m <= 0) return HP_OK;

@@ -704,7 +704,8 @@ def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = N
     prefix-mode samples ``main`` (both (r_off, r_id, r_t, r_dist, r_udf,
     r_alpha, r_w, r_color, t_end[, r_knn_id, r_knn_w])); flagged rays hold no
     candidates in main.  ``sel``: the flagged ray indices if the caller has
-    them already."""
+    them already.  One copy kernel (hp_splice_samples)."""
+    lib = _lib.load(require_device=True)
     r_off, s_off = main[0], sub[0]
     dev = r_off.device
     m = int(r_off.shape[0]) - 1
@@ -716,32 +717,33 @@ def merge_flagged(main, flagged: torch.Tensor, sub, sel: torch.Tensor | None = N
     torch.cumsum(counts, 0, out=off[1:])
     R_main, R_sub = int(main[1].shape[0]), int(sub[1].shape[0])  # host values: no synchronisation
     R = R_main + R_sub  # flagged rays hold nothing in main
+    pos = torch.full((m,), -1, dtype=torch.int64, device=dev)
+    pos[sel] = torch.arange(int(sel.numel()), dtype=torch.int64, device=dev)
+    colours = main[7].shape[0] == R_main and sub[7].shape[0] == R_sub and (R_main + R_sub == 0 or
+                                                                            main[7].numel() + sub[7].numel() > 0)
+    knn = len(main) > 9
+    K = int(main[9].shape[1]) if knn else 0
+    out = [off, torch.empty(R, dtype=torch.int64, device=dev)] + \
+        [torch.empty(R, dtype=torch.float64, device=dev) for _ in range(5)]
+    out.append(torch.empty((R, 3), dtype=torch.float64, device=dev) if colours
+               else torch.zeros((0, 3), dtype=torch.float64, device=dev))
+    te = main[8].clone()
+    te[sel] = sub[8]
+    out.append(te)
+    if knn:
+        out += [torch.empty((R, K), dtype=torch.int64, device=dev), torch.empty((R, K), dtype=torch.float64,
+                                                                                device=dev)]
 
-    def dst(src_off, rays, k):  # destination row of every source row
-        n = src_off[1:] - src_off[:-1]
-        ray = torch.repeat_interleave(rays, n, output_size=k)
-        pos = torch.arange(k, device=dev) - torch.repeat_interleave(src_off[:-1], n, output_size=k)
-        return off[ray] + pos
-
-    d_main = dst(r_off, torch.arange(m, device=dev), R_main)
-    d_sub = dst(s_off, sel, R_sub)
-    out = [off]
-    for k in range(1, len(main)):
-        a, b = main[k], sub[k]
-        if k == 8:  # t_end: per ray
-            te = a.clone()
-            te[sel] = b
-            out.append(te)
-            continue
-        if k == 7 and not (a.shape[0] == R_main and b.shape[0] == R_sub):  # no colours
-            out.append(torch.zeros((0, 3), dtype=a.dtype, device=dev))
-            continue
-        o = torch.empty((R,) + tuple(a.shape[1:]), dtype=a.dtype, device=dev)
-        if a.shape[0]:
-            o[d_main] = a
-        if b.shape[0]:
-            o[d_sub] = b
-        out.append(o)
+    def fields(t):
+        f = _lib.SampleFields(*[t[k].data_ptr() if t[k].numel() else 0 for k in range(1, 7)])
+        f.r_color = t[7].data_ptr() if (colours and t[7].numel()) else None
+        if knn:
+            f.r_knn_id, f.r_knn_w = (t[9].data_ptr() or None), (t[10].data_ptr() or None)
+        return f
+    if R:
+        A, B, O = fields(main), fields(sub), fields(out)
+        _lib.check(lib.hp_splice_samples(m, _ptr(off), _ptr(r_off), _ptr(s_off), _ptr(pos), K, ctypes.byref(A),
+                                         ctypes.byref(B), ctypes.byref(O), _stream()))
     return tuple(out)
 
 
