@@ -361,6 +361,9 @@ struct Exact {
 template <class BestT, bool kKnn>
 // HP_EXACT_MINB > 0: minimum resident CTAs per SM for the K <= 8 instances
 // (an explicit 1 is not the same as none: ptxas then allots more registers)
+#ifndef HP_EXACT_DYN
+#define HP_EXACT_DYN 1  // k_sample_exact: candidates claimed 32 at a time per warp
+#endif
 #ifndef HP_EXACT_MINB
 #define HP_EXACT_MINB 4
 #endif
@@ -370,11 +373,25 @@ template <class BestT, bool kKnn>
 #define HP_EXACT_BOUNDS __launch_bounds__(kThreads)
 #endif
 __global__ void HP_EXACT_BOUNDS k_sample_exact(Csr C, Params P, const int4* __restrict__ plan,
-                                                           const int64_t* __restrict__ eoff, Exact X) {
+                                                           const int64_t* __restrict__ eoff, Exact X,
+                                                           unsigned long long* __restrict__ claim) {
     const int64_t n = eoff[C.m];
     if (n > X.cap) return;
     unsigned long long evals = 0;
+#if HP_EXACT_DYN
+    // 32 candidates per warp claimed dynamically (their costs vary widely:
+    // a static stride leaves a tail)
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane_id() == 0) b = atomicAdd(claim, 32ull);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (int64_t(b) >= n) break;
+        const int64_t c = int64_t(b) + lane_id();
+        if (c >= n) continue;
+#else
+    (void)claim;
     for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
+#endif
         const int ray = X.ray[c];
         const int j = int(c - eoff[ray]);
         const int4 pl = plan[ray];
@@ -754,7 +771,7 @@ SampleWs carve_sample(Carver& c, int64_t m, int64_t xcap, bool color, int knn_k 
     w.x.knn_w = knn_k > 0 ? c.take<double>(xc * knn_k) : nullptr;
     w.x.ray = c.take<int>(xc);
     w.scan = c.take<char>(scan_workspace_bytes(m + 1));
-    w.work = c.take<unsigned long long>(2);  // [0] k_sample_plan's rays, [1] the long rays of the retain
+    w.work = c.take<unsigned long long>(3);  // [0] k_sample_plan's rays, [1] the retain's long rays, [2] exact claims
     w.longs = c.take<int>(m > 0 ? m : 1);
     return w;
 }
@@ -789,7 +806,7 @@ Params to_params(const hp_sampler_params* p) {
 template <class BestT>
 int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     {
-        if (cudaMemsetAsync(w.work, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess)
+        if (cudaMemsetAsync(w.work, 0, 3 * sizeof(unsigned long long), s) != cudaSuccess)
             return cuda_status(cudaGetLastError(), "k_sample_plan memset");
         TimedSpan ts("k_sample_plan", s);
         k_sample_plan<<<device_sms() * 8, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.work);
@@ -806,9 +823,9 @@ int launch_exact(const Csr& C, const Params& P, SampleWs& w, cudaStream_t s) {
     {
         TimedSpan ts("k_sample_exact", s);
         if (P.emit_knn)
-            k_sample_exact<BestT, true><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
+            k_sample_exact<BestT, true><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x, w.work + 2);
         else
-            k_sample_exact<BestT, false><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x);
+            k_sample_exact<BestT, false><<<device_sms() * 16, kThreads, 0, s>>>(C, P, w.plan, w.eoff, w.x, w.work + 2);
         HP_CHECK_LAUNCH("k_sample_exact");
     }
     return HP_OK;
