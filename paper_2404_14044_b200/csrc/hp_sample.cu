@@ -59,6 +59,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef HP_PLAN_F32
 #define HP_PLAN_F32 1  // fp32 ring bound factors in k_sample_plan
 #endif
+#ifndef HP_PLAN_CLAIM
+#define HP_PLAN_CLAIM 4  // rays per warp claim in k_sample_plan
+#endif
 #ifndef HP_PLAN_AHEAD
 #define HP_PLAN_AHEAD 2  // chunks in flight
 #endif
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_plan(Csr C, Params P, int4*
                                                           unsigned long long* __restrict__ work) {
     __shared__ double ring[kWarps][2][kRing];  // recent candidates' t / ds per warp
     __shared__ float2 ringf[kWarps][kRing];    // their fp32 bound terms
-    WarpClaim<4> claim(work);  // chain lengths vary widely: rays claimed dynamically
+    WarpClaim<HP_PLAN_CLAIM> claim(work);  // chain lengths vary widely: rays claimed dynamically
     int64_t ray;
     while (claim.next(C.m, ray))
         plan_ray(C, P, ray, plan, ecnt, ring[warp_id()][0], ring[warp_id()][1], ringf[warp_id()]);
